@@ -1,0 +1,374 @@
+#!/usr/bin/env python3
+"""Throughput benchmark: whole-body env-steps/s on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): the whole-body planar model
+``wb700_fixed`` (80 links, 700 Hill muscles, pinned pelvis, no contacts),
+4096 envs per GPU, Philox random excitations, eval mode, horizon 1000 on the
+synthetic ``dance`` clip.  One "step" = one control step (10 x 2 ms
+substeps) of every env, i.e. E env-steps.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+N > 1 runs under torchrun: every rank steps its own contiguous shard of
+envs (independent units, no data-path collective -> scaling "weak");
+timing is the max over ranks of the device time.
+
+JSON line fields beyond the base contract:
+  value       device-resident throughput (inputs generated on device)
+  e2e         same metric through the C-ABI host-buffer call
+              (msk_gpu_step_host: H2D actions, step, D2H obs/Δ/reward/flags)
+  roofline    step kernel: algorithmic HBM bytes/launch ÷ its event time,
+              vs MEASURED_PEAKS.json hbm_gbs; "fp32" adds the binding FP32
+              roofline (algorithmic flops vs the measured FFMA peak)
+  cpu_baseline the reference's own CPU path (oracle/_ref, compiled from
+              /root/reference sources) on the box's host cores, bounded sample
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+DEFAULT_MODEL = "wb700_fixed"
+CLIPS = {"wb700_fixed": "wb700_fixed_dance", "wb700": "wb700_dance", "arm2_m6": "arm2_m6_sine",
+         "walker5_m16": "walker5_m16_sine"}
+
+
+def ensure_assets():
+    d = os.path.join(ROOT, "assets", "generated")
+    need = ["wb700_fixed.json", "wb700_fixed_dance.csv", "wb700.json", "wb700_dance.csv", "arm2_m6.json"]
+    if not all(os.path.exists(os.path.join(d, n)) for n in need):
+        from tools.gen_assets import generate
+        generate(d)
+    return d
+
+
+def model_files(name):
+    d = ensure_assets()
+    return os.path.join(d, name + ".json"), os.path.join(d, CLIPS[name] + ".csv")
+
+
+# ----------------------------------------------------------------------------
+# algorithmic cost model
+# ----------------------------------------------------------------------------
+def cost_model(model_json):
+    """Algorithmic HBM bytes and FLOPs per env-step, from the model file."""
+    with open(model_json) as f:
+        js = json.load(f)
+    floating = js["root"] == "floating"
+    joints = js.get("joints", [])
+    mus = js.get("muscles", [])
+    vias = [vp for m in mus for vp in m["via_points"]]
+    starts = [0]
+    for m in mus:
+        starts.append(starts[-1] + len(m["via_points"]))
+    spheres = js.get("contacts", {}).get("spheres", [])
+    d = {"floating": floating, "joint_parent": [int(j["parent"]) for j in joints], "via_link": [int(v[0]) for v in vias],
+         "m_via_start": starts, "n_spheres": len(spheres), "sphere_link": [int(s["link"]) for s in spheres]}
+    nj, nl, nm, nk = len(joints), len(js["links"]), len(mus), len(js.get("key_bodies", []))
+    nq = (3 if floating else 0) + nj
+    obs_dim = 3 * nq + 6 * nk + 4 * nm
+    ddim = 3 + nj + 2 * nk
+    bytes_per = 4 * (nm + 2 * (2 * nq + 2 * nm) + obs_dim + ddim + 3)
+    # tree depths
+    fc = 1 if d["floating"] else 0
+    parent = [-1] * nl
+    for j in range(nj):
+        parent[fc + j] = int(d["joint_parent"][j])
+    depth = [0] * nl
+    for l in range(nl):
+        depth[l] = depth[parent[l]] + 1 if parent[l] >= 0 else (0 if d["floating"] and l == 0 else 1)
+    V = len(d["via_link"])
+    S = V - nm
+    # segment/joint pairs of J_m^T F (joints strictly between a segment's links)
+    def path(l):
+        out = set()
+        while l >= fc:
+            out.add(l - fc)
+            l = parent[l]
+        return out
+    P = 0
+    for m in range(nm):
+        a, b = d["m_via_start"][m], d["m_via_start"][m + 1]
+        for v in range(a + 1, b):
+            la, lb = int(d["via_link"][v - 1]), int(d["via_link"][v])
+            if la != lb:
+                P += len(path(la) ^ path(lb))
+    ns = d["n_spheres"]
+    f_sub = (12 * nl + 8 * V + 7 * S + 41 * nm + 2 * S + 6 * P + 8 * nl + sum(21 + 12 * dl for dl in depth)
+             + 4 * nj + sum(35 + 5 * depth[int(s)] for s in d["sphere_link"])
+             + sum(2 * dl + 2.5 * dl * dl for dl in depth) + sum(dl * dl + 4 * dl for dl in depth) + 4 * nq)
+    f_ctrl = 12 * nl + 30 * nk + nj
+    flops_per = 10 * f_sub + f_ctrl
+    return dict(bytes_per_env_step=int(bytes_per), flops_per_env_step=float(flops_per), n_pairs=P, n_via=V,
+                obs_dim=obs_dim, delta_dim=ddim, nq=nq, nm=nm, ns=ns)
+
+
+# ----------------------------------------------------------------------------
+def clocks_sampler(stop, out, gpu_index):
+    q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    try:
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200",
+                              "-i", str(gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+    except FileNotFoundError:
+        return
+    while not stop.is_set():
+        line = p.stdout.readline()
+        if not line:
+            break
+        out.append(line.strip())
+    p.terminate()
+
+
+def summarize_clocks(lines):
+    sm, mx, reasons = [], 0.0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for ln in lines:
+        f = [x.strip() for x in ln.split(",")]
+        if len(f) < 9:
+            continue
+        try:
+            sm.append(float(f[1]))
+            mx = max(mx, float(f[2]))
+        except ValueError:
+            continue
+        for n, v in zip(names, f[5:9]):
+            if v.lower().startswith("active"):
+                reasons.add(n)
+    sm.sort()
+    return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx or None, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+def run_reference(args, rank, world):
+    """--impl reference: the reference's CPU path (oracle/_ref) on the host cores."""
+    if rank != 0:
+        return
+    from oracle.ref import RefBatch, env_config
+
+    mp, cp = model_files(args.model)
+    threads = args.cpu_threads or os.cpu_count() or 1
+    n_envs = args.ref_envs or max(threads, 8)
+    cfg = env_config(episode_horizon=1000, rsi=False)
+    b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads)
+    b.set_eval_mode(True)
+    b.reset()
+    for _ in range(args.warmup):
+        b.bench(1)
+    secs, steps = b.bench(args.steps)
+    v = steps / secs
+    line = {"metric": "env-steps/sec (700-muscle whole-body)", "value": v, "unit": "env-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Philox excitations, generated dance clip)", "impl": "reference",
+            "config": {"workload": f"{args.model} eval-mode random excitations (CPU sample)",
+                       "envs": n_envs, "parallelism": f"{threads} host threads (ThreadPool::parallel_chunks)"},
+            "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "reference",
+                             "sample": f"{n_envs} envs x {args.steps} control steps"},
+            "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_sample(args):
+    """Bounded sample (~10-20 s) of the reference CPU path for the cpu_baseline key."""
+    from oracle.ref import RefBatch, env_config
+
+    mp, cp = model_files(args.model)
+    threads = args.cpu_threads or os.cpu_count() or 1
+    n_envs = max(threads, 8)
+    b = RefBatch(mp, cp, n_envs, cfg=env_config(episode_horizon=1000, rsi=False), threads=threads)
+    b.set_eval_mode(True)
+    b.reset()
+    b.bench(1)
+    secs, steps = b.bench(1)
+    per_step = secs
+    k = max(1, min(50, int(args.cpu_seconds / max(per_step, 1e-3))))
+    secs, steps = b.bench(k)
+    return {"value": steps / secs, "unit": "env-steps/s", "cores": threads, "kind": "reference",
+            "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--envs", type=int, default=4096, help="envs per GPU")
+    ap.add_argument("--model", default=DEFAULT_MODEL)
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-envs", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_29332_b200 as pk
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mp, cp = model_files(args.model)
+    E = args.envs
+    cfg = pk.EnvConfig(episode_horizon=1000, rsi=False)
+    env = pk.EnvBatch(mp, cp, E, cfg=cfg, global_env_offset=rank * E)
+    env.set_eval_mode(True)
+    dev = env.device
+    stream = torch.cuda.current_stream(dev)
+    actions = torch.empty(E, env.nm, device=dev)
+    obs = torch.empty(E, env.obs_dim, device=dev)
+    delta = torch.empty(E, env.delta_dim, device=dev)
+    raux = torch.empty(E, device=dev)
+    flags = torch.zeros(E, dtype=torch.uint8, device=dev)
+    env.reset(obs=obs)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
+    seed = 0x5EED
+
+    def one_step(s):
+        env.fill_excitations(seed, s, actions)
+        env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags)
+        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
+
+    for s in range(args.warmup):
+        one_step(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk_lines, stop = [], threading.Event()
+    th = threading.Thread(target=clocks_sampler, args=(stop, clk_lines, local), daemon=True)
+    th.start()
+    time.sleep(0.3)
+    # timed region: per-step CUDA events (L2 flushed between steps, outside the events)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kst = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ken = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    n0 = env.launch_count
+    torch.cuda.synchronize()
+    for s in range(args.steps):
+        flush.zero_()
+        starts[s].record(stream)
+        env.fill_excitations(seed, args.warmup + s, actions)
+        kst[s].record(stream)
+        env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags)
+        ken[s].record(stream)
+        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
+        ends[s].record(stream)
+    torch.cuda.synchronize()
+    launches = env.launch_count - n0
+    stop.set()
+    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
+    kms = sum(a.elapsed_time(b) for a, b in zip(kst, ken)) / args.steps
+    t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, kms = float(t[0]), float(t[1])
+    value = E * world * args.steps / (ms * 1e-3)
+
+    # e2e through the C-ABI host-buffer call (pinned host in/out)
+    e2e = None
+    if not args.no_e2e:
+        ha = torch.empty(E, env.nm, dtype=torch.float32, pin_memory=True)
+        env.fill_excitations(seed, 12345, actions)
+        ha.copy_(actions.cpu())
+        ho = torch.empty(E, env.obs_dim, dtype=torch.float32, pin_memory=True)
+        hd = torch.empty(E, env.delta_dim, dtype=torch.float32, pin_memory=True)
+        hr = torch.empty(E, dtype=torch.float32, pin_memory=True)
+        hf = torch.empty(E, dtype=torch.uint8, pin_memory=True)
+        for _ in range(2):
+            env.step_host(ha, ho, hd, hr, hf)
+            env.reset(mask=hf.to(dev), mask_bits=pk.FLAG_DONE)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        tt = 0.0
+        k2 = max(3, args.steps // 2)
+        for _ in range(k2):
+            t0 = time.perf_counter()
+            env.step_host(ha, ho, hd, hr, hf)
+            tt += time.perf_counter() - t0
+            if hf.any():
+                env.reset(mask=hf.to(dev), mask_bits=pk.FLAG_DONE)
+                torch.cuda.synchronize()
+        tv = torch.tensor([tt], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+        e2e = {"value": E * world * k2 / float(tv[0]), "unit": "env-steps/s",
+               "h2d_bytes_per_step": E * env.nm * 4,
+               "d2h_bytes_per_step": E * (env.obs_dim + env.delta_dim + 1) * 4 + E}
+
+    if rank == 0:
+        cm = cost_model(mp)
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except OSError:
+            pass
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        achieved_gbs = cm["bytes_per_env_step"] * E / (kms * 1e-3) / 1e9
+        fp32 = None
+        try:
+            import paper_2603_29332_b200.diag as diag
+            pk_tf = diag.fp32_peak_tflops()
+            ach_tf = cm["flops_per_env_step"] * E / (kms * 1e-3) / 1e12
+            fp32 = {"achieved": ach_tf, "peak": pk_tf, "unit": "TFLOP/s", "frac": ach_tf / pk_tf,
+                    "flops_per_env_step": cm["flops_per_env_step"], "peak_source": "measured FFMA probe"}
+        except Exception as ex:  # pragma: no cover
+            fp32 = {"error": str(ex)}
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "step_kernel_traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get("bytes_per_launch")
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                cpu = cpu_baseline_sample(args)
+            except Exception as ex:
+                cpu = {"error": str(ex)}
+        line = {
+            "metric": "env-steps/sec (700-muscle whole-body)", "value": value, "unit": "env-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 q/qdot, sampler)",
+            "data": "synthetic (Philox excitations, generated dance clip, random-init model)",
+            "config": {"workload": f"{args.model}: 80 links, 700 muscles, no contacts, eval mode, random excitations",
+                       "envs_per_gpu": E, "global_envs": E * world, "clip": CLIPS[args.model],
+                       "parallelism": f"env shards x{world}", "l2": "flushed between timed steps"},
+            "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm_peak, "traffic": traffic,
+                         "bytes_per_env_step": cm["bytes_per_env_step"], "step_kernel_ms": kms,
+                         "note": "path is FP32-issue bound (SURVEY §8(d)); see fp32", "fp32": fp32},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": summarize_clocks(clk_lines),
+        }
+        print(json.dumps(line), flush=True)
+    env.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,174 @@
+/* msk_gpu.h — C ABI of the B200-native batched musculoskeletal env-stepper.
+ *
+ * Drop-in for the data-parallel hot path of the reference's environment API
+ * (/root/reference/proj/include/msk/env.hpp:86-145, class msk::Env): one
+ * context holds E independent environments on one GPU and exposes the Env
+ * verbs in batched form.  All buffers are caller-owned, row-major
+ * [E x dim], and — unless the name ends in _host — DEVICE pointers; calls are
+ * asynchronous on the given CUDA stream (passed as void*, a cudaStream_t;
+ * NULL = legacy default stream).  No C++ exceptions cross this boundary:
+ * every entry point returns an msk_status and msk_gpu_last_error() describes
+ * the last failure.  There is no CPU fallback: a context can only be created
+ * on a CUDA device with the sm_100a kernels of this library.
+ *
+ * Mapping to the reference (file:line of the interface each one replaces):
+ *   msk_gpu_create          Env::Env (env.cpp:74-87) + load_model (model.cpp:198-204)
+ *                           + load_reference (reference.cpp:88-93)
+ *   msk_gpu_reset           Env::reset (env.cpp:108-121)
+ *   msk_gpu_reset_to_frame  Env::reset_to_frame (env.cpp:95-106)
+ *   msk_gpu_step            Env::step(action) (env.cpp:206-263) incl. msk::step
+ *                           (skeleton.cpp:286-331); StepResult fields as buffers
+ *   msk_gpu_observe         Env::observe (env.cpp:129-163)
+ *   msk_gpu_tracking_error  Env::tracking_error (env.cpp:170-193) + TrackingError::flatten
+ *   msk_gpu_force_state_to_reference  Env::force_state_to_reference (env.cpp:123-127)
+ *   msk_gpu_set_eval_mode   Env::set_eval_mode (env.hpp:115)
+ *   msk_gpu_get/set_state   Env::state / mutable_state (env.hpp:110-111) + EnvSerde (env.hpp:144)
+ *   msk_gpu_get/set_sampler, msk_gpu_record_own_outcomes
+ *                           Env::sampler (env.hpp:118-119), AdaptiveSampler::record (env.cpp:34-37)
+ *   msk_gpu_drain_outcomes  Env::drain_episode_outcomes (env.cpp:200-204)
+ *   msk_gpu_merge_outcomes  the order-fixed merge of SPEC.md:296 (global sampler convention)
+ *   msk_gpu_rng_raw         Rng::raw (rng.hpp:24) of one env's mt19937_64 stream
+ */
+#ifndef MSK_GPU_H
+#define MSK_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct msk_gpu_ctx msk_gpu_ctx;
+
+typedef enum msk_status {
+    MSK_OK = 0,
+    MSK_ERR_CONTRACT = 1, /* bad argument / config / model (ContractError, ConfigError) */
+    MSK_ERR_CUDA = 3      /* CUDA runtime error, or no sm_100 device */
+} msk_status;
+
+/* Per-env flag bits written by msk_gpu_step (StepResult::done/failed/diverged
+ * plus the two ContractError cases of Env::step, which leave the env untouched). */
+enum {
+    MSK_FLAG_DONE = 1,
+    MSK_FLAG_FAILED = 2,
+    MSK_FLAG_DIVERGED = 4,
+    MSK_FLAG_NOT_STEPPED = 8, /* env was already done (env.cpp:207) */
+    MSK_FLAG_BAD_ACTION = 16  /* non-finite action (env.cpp:209) */
+};
+
+/* msk::EnvConfig (env.hpp:39-47); field order is ABI. */
+typedef struct msk_env_config {
+    int32_t episode_horizon; /* 250 */
+    int32_t rsi;             /* 1 */
+    int32_t adaptive_bins;   /* 10 */
+    int32_t pad0;
+    double adaptive_mix;         /* 0.2 */
+    double adaptive_decay;       /* 0.99 */
+    double termination_body_err; /* 0.5 m */
+    double init_activation;      /* 0.01 */
+} msk_env_config;
+
+/* msk::RewardConfig (env.hpp:30-37). mode: 0 ImitationOnly, 1 ImitationEmg, 2 ImitationPower. */
+typedef struct msk_reward_config {
+    int32_t mode;
+    int32_t n_emg_channels;
+    double w_emg;   /* 100 */
+    double w_power; /* 0.05 */
+    const int32_t* emg_channel_map; /* host pointer, n_emg_channels muscle indices */
+} msk_reward_config;
+
+typedef struct msk_dims {
+    int32_t n_envs, nq, n_muscles, obs_dim, delta_dim;
+    int32_t n_links, n_joints, n_key, n_spheres, frames;
+    int32_t floating, adaptive_bins;
+} msk_dims;
+
+/* Creates E envs (seed of env e = base_seed + global_env_offset + e, as
+ * Env(seed) with one mt19937_64 each, env.cpp:76).  Envs start done
+ * (env.hpp:140): call msk_gpu_reset before stepping.  cfg/rc may be NULL for
+ * the reference defaults. */
+int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const msk_env_config* cfg,
+                   const msk_reward_config* rc, int32_t n_envs, uint64_t base_seed,
+                   int64_t global_env_offset, int device, msk_gpu_ctx** out);
+void msk_gpu_destroy(msk_gpu_ctx* ctx);
+/* Last error of ctx (or of the calling thread when ctx is NULL). */
+const char* msk_gpu_last_error(const msk_gpu_ctx* ctx);
+int msk_gpu_dims(const msk_gpu_ctx* ctx, msk_dims* out);
+int msk_gpu_set_eval_mode(msk_gpu_ctx* ctx, int32_t eval_mode);
+
+/* Env::reset for every env whose mask byte has any of mask_bits set (mask NULL
+ * = all envs).  Passing the step's flags with mask_bits = MSK_FLAG_DONE is the
+ * batched auto-reset.  obs [E x obs_dim] (nullable) receives observe() of the
+ * reset envs; start_frames [E] (nullable) their start frame. */
+int msk_gpu_reset(msk_gpu_ctx* ctx, const uint8_t* mask, uint8_t mask_bits, float* obs, int32_t* start_frames,
+                  void* stream);
+/* Env::reset_to_frame.  bad [E] (nullable) is set to 1 for envs whose frame is
+ * out of range (reference: ContractError); those envs are left untouched. */
+int msk_gpu_reset_to_frame(msk_gpu_ctx* ctx, const int32_t* frames, const uint8_t* mask, float* obs, uint8_t* bad,
+                           void* stream);
+
+/* One control step (10 x 2 ms substeps) of every env.  actions [E x n_muscles]
+ * (clipped to [0,1]); obs [E x obs_dim]; delta [E x delta_dim]; reward_aux [E];
+ * flags [E] (MSK_FLAG_*); muscle_power [E x n_muscles] and contact_force
+ * [E x n_links x 2] optional.  Every output except flags is nullable. */
+int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward_aux,
+                 uint8_t* flags, float* muscle_power, float* contact_force, void* stream);
+
+/* Same verb with HOST buffers (pinned or pageable): copies actions in, steps,
+ * and copies obs/delta/reward_aux/flags out, pipelined over env chunks so the
+ * PCIe transfers overlap the step kernel.  Synchronous on return. */
+int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                      float* reward_aux_host, uint8_t* flags_host);
+
+int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream);
+int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream);
+int msk_gpu_force_state_to_reference(msk_gpu_ctx* ctx, void* stream);
+
+/* State of every env: q, dq [E x nq] (f64), act, l_m, v_m, f_m [E x n_muscles]
+ * (f32), t [E] (f64), ints [E x 4] = {t_index, start_index, steps, done}.
+ * Any pointer may be NULL. */
+int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float* l_m, float* v_m, float* f_m,
+                      double* t, int32_t* ints, void* stream);
+int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const float* l_m,
+                      const float* v_m, const float* f_m, const double* t, const int32_t* ints, void* stream);
+
+/* Adaptive sampler failure EMA [E x bins] (f64).  set: broadcast != 0 copies
+ * one [bins] row to every env. */
+int msk_gpu_get_sampler(msk_gpu_ctx* ctx, double* ema, void* stream);
+int msk_gpu_set_sampler(msk_gpu_ctx* ctx, const double* ema, int32_t broadcast, void* stream);
+/* Pending episode outcomes: bins/failed [E x cap], counts [E]; then cleared. */
+int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int32_t* counts, int32_t cap,
+                           void* stream);
+/* Each env records its own pending outcomes into its own sampler, in order. */
+int msk_gpu_record_own_outcomes(msk_gpu_ctx* ctx, void* stream);
+/* Order-fixed merge: outcome blocks of n_envs_total envs in
+ * global env order (e.g. the allgather of every rank's drain) are recorded in
+ * env order then time order into ONE sampler, which is then copied to every
+ * local env.  Identical on every rank, so replicas stay bit-identical. */
+int msk_gpu_merge_outcomes(msk_gpu_ctx* ctx, const int32_t* bins, const uint8_t* failed, const int32_t* counts,
+                           int64_t n_envs_total, int32_t cap, void* stream);
+
+/* n raw mt19937_64 draws of env `env` (advances its stream). */
+int msk_gpu_rng_raw(msk_gpu_ctx* ctx, int32_t env, int32_t n, uint64_t* out, void* stream);
+/* Philox4x32-10 excitations u in [0,1) [E x n_muscles] for control step `step`
+ * (key = seed, counter = {step, global env, muscle/4, 0}). */
+int msk_gpu_fill_excitations(msk_gpu_ctx* ctx, uint64_t seed, uint32_t step, float* actions, void* stream);
+
+/* Number of kernels launched by this context since creation (diagnostics). */
+int64_t msk_gpu_launch_count(const msk_gpu_ctx* ctx);
+
+/* Host-only: parse + validate a model and clip exactly as msk_gpu_create does
+ * (ModelSpec::validate, model.cpp:18-86; ReferenceTrajectory::validate,
+ * reference.cpp:11-33) without touching a GPU — the `msk model validate`
+ * check.  dims (nullable) receives the sizes (n_envs = 0).
+ * Returns MSK_OK or MSK_ERR_CONTRACT with msk_gpu_last_error(NULL) set. */
+int msk_gpu_validate(const char* model_json_path, const char* clip_csv_path, msk_dims* dims);
+
+/* Measured FFMA throughput of `device` in TFLOP/s (FP32 roofline denominator). */
+int msk_gpu_fp32_peak_probe(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MSK_GPU_H */

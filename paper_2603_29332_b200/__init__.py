@@ -1,0 +1,311 @@
+"""B200-native batched musculoskeletal env-stepper (host mirror of msk::Env).
+
+The product is the sm_100a shared library ``libmsk_b200.so`` with the C ABI in
+``include/msk_gpu.h``.  This module binds that ABI with ctypes and exposes the
+reference's environment verbs (``/root/reference/proj/include/msk/env.hpp:86-145``)
+in batched form over torch CUDA tensors — torch is used for device memory
+and streams only.  There is no CPU fallback: importing works anywhere, but
+creating an :class:`EnvBatch` needs the library and a B200, and fails loudly
+otherwise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError",
+           "FLAG_DONE", "FLAG_FAILED", "FLAG_DIVERGED", "FLAG_NOT_STEPPED", "FLAG_BAD_ACTION"]
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmsk_b200.so")
+
+FLAG_DONE, FLAG_FAILED, FLAG_DIVERGED, FLAG_NOT_STEPPED, FLAG_BAD_ACTION = 1, 2, 4, 8, 16
+
+
+class MskError(RuntimeError):
+    """A non-zero msk_status from the C ABI (1 = contract/config, 3 = CUDA)."""
+
+    def __init__(self, code, msg):
+        super().__init__(f"[msk status {code}] {msg}")
+        self.code = code
+
+
+class RewardMode:
+    """msk::RewardMode (env.hpp:30)."""
+    ImitationOnly, ImitationEmg, ImitationPower = 0, 1, 2
+
+
+@dataclass
+class EnvConfig:
+    """msk::EnvConfig defaults (env.hpp:39-47)."""
+    episode_horizon: int = 250
+    rsi: bool = True
+    adaptive_bins: int = 10
+    adaptive_mix: float = 0.2
+    adaptive_decay: float = 0.99
+    termination_body_err: float = 0.5
+    init_activation: float = 0.01
+
+
+@dataclass
+class RewardConfig:
+    """msk::RewardConfig defaults (env.hpp:32-37)."""
+    mode: int = RewardMode.ImitationOnly
+    w_emg: float = 100.0
+    w_power: float = 0.05
+    emg_channel_map: list = field(default_factory=list)
+
+
+class _EnvConfigC(C.Structure):
+    _fields_ = [("episode_horizon", C.c_int32), ("rsi", C.c_int32), ("adaptive_bins", C.c_int32),
+                ("pad0", C.c_int32), ("adaptive_mix", C.c_double), ("adaptive_decay", C.c_double),
+                ("termination_body_err", C.c_double), ("init_activation", C.c_double)]
+
+
+class _RewardConfigC(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("n_emg_channels", C.c_int32), ("w_emg", C.c_double),
+                ("w_power", C.c_double), ("emg_channel_map", C.POINTER(C.c_int32))]
+
+
+class _Dims(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("n_envs", "nq", "n_muscles", "obs_dim", "delta_dim", "n_links",
+                                          "n_joints", "n_key", "n_spheres", "frames", "floating",
+                                          "adaptive_bins")]
+
+
+_LIB = None
+_vp = C.c_void_p
+
+
+def lib():
+    """Loads libmsk_b200.so (raises if it was not built — there is no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                              f"g.build()'` (make -C paper_2603_29332_b200/csrc)")
+        L = C.CDLL(LIB_PATH)
+        L.msk_gpu_create.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(_EnvConfigC), C.POINTER(_RewardConfigC),
+                                     C.c_int32, C.c_uint64, C.c_int64, C.c_int, C.POINTER(_vp)]
+        L.msk_gpu_destroy.argtypes = [_vp]
+        L.msk_gpu_last_error.restype = C.c_char_p
+        L.msk_gpu_last_error.argtypes = [_vp]
+        L.msk_gpu_dims.argtypes = [_vp, C.POINTER(_Dims)]
+        L.msk_gpu_set_eval_mode.argtypes = [_vp, C.c_int32]
+        L.msk_gpu_reset.argtypes = [_vp, _vp, C.c_uint8, _vp, _vp, _vp]
+        L.msk_gpu_reset_to_frame.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+        L.msk_gpu_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
+        L.msk_gpu_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+        L.msk_gpu_observe.argtypes = [_vp, _vp, _vp]
+        L.msk_gpu_tracking_error.argtypes = [_vp, _vp, _vp]
+        L.msk_gpu_force_state_to_reference.argtypes = [_vp, _vp]
+        L.msk_gpu_get_state.argtypes = [_vp] + [_vp] * 8 + [_vp]
+        L.msk_gpu_set_state.argtypes = [_vp] + [_vp] * 8 + [_vp]
+        L.msk_gpu_get_sampler.argtypes = [_vp, _vp, _vp]
+        L.msk_gpu_set_sampler.argtypes = [_vp, _vp, C.c_int32, _vp]
+        L.msk_gpu_drain_outcomes.argtypes = [_vp, _vp, _vp, _vp, C.c_int32, _vp]
+        L.msk_gpu_record_own_outcomes.argtypes = [_vp, _vp]
+        L.msk_gpu_merge_outcomes.argtypes = [_vp, _vp, _vp, _vp, C.c_int64, C.c_int32, _vp]
+        L.msk_gpu_rng_raw.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp]
+        L.msk_gpu_fill_excitations.argtypes = [_vp, C.c_uint64, C.c_uint32, _vp, _vp]
+        L.msk_gpu_launch_count.restype = C.c_int64
+        L.msk_gpu_launch_count.argtypes = [_vp]
+        for name in ("msk_gpu_create", "msk_gpu_dims", "msk_gpu_set_eval_mode", "msk_gpu_reset",
+                     "msk_gpu_reset_to_frame", "msk_gpu_step", "msk_gpu_step_host", "msk_gpu_observe",
+                     "msk_gpu_tracking_error", "msk_gpu_force_state_to_reference", "msk_gpu_get_state",
+                     "msk_gpu_set_state", "msk_gpu_get_sampler", "msk_gpu_set_sampler", "msk_gpu_drain_outcomes",
+                     "msk_gpu_record_own_outcomes", "msk_gpu_merge_outcomes", "msk_gpu_rng_raw",
+                     "msk_gpu_fill_excitations"):
+            getattr(L, name).restype = C.c_int
+        _LIB = L
+    return _LIB
+
+
+def _p(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class EnvBatch:
+    """E environments on one GPU with the verbs of ``msk::Env``.
+
+    Buffers are torch CUDA tensors; every call is asynchronous on the current
+    torch stream (or ``stream``).  Env e's seed is ``base_seed +
+    global_env_offset + e`` (``Env(seed)``, env.cpp:74-76).
+    """
+
+    def __init__(self, model_path, clip_path, n_envs, cfg: EnvConfig | None = None,
+                 reward: RewardConfig | None = None, base_seed=0x5EED, global_env_offset=0, device=None):
+        import torch
+
+        self.torch = torch
+        cfg = cfg or EnvConfig()
+        reward = reward or RewardConfig()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.device = torch.device("cuda", device)
+        ec = _EnvConfigC(int(cfg.episode_horizon), int(bool(cfg.rsi)), int(cfg.adaptive_bins), 0,
+                         float(cfg.adaptive_mix), float(cfg.adaptive_decay), float(cfg.termination_body_err),
+                         float(cfg.init_activation))
+        self._emg = (C.c_int32 * max(1, len(reward.emg_channel_map)))(*reward.emg_channel_map)
+        rc = _RewardConfigC(int(reward.mode), len(reward.emg_channel_map), float(reward.w_emg),
+                            float(reward.w_power), self._emg)
+        L = lib()
+        h = _vp()
+        rcode = L.msk_gpu_create(os.fsencode(model_path), os.fsencode(clip_path), C.byref(ec), C.byref(rc),
+                                 int(n_envs), C.c_uint64(base_seed), int(global_env_offset), int(device), C.byref(h))
+        if rcode != 0:
+            raise MskError(rcode, L.msk_gpu_last_error(None).decode())
+        self.h = h
+        d = _Dims()
+        L.msk_gpu_dims(h, C.byref(d))
+        self.n = d.n_envs
+        self.nq, self.nm, self.obs_dim, self.delta_dim = d.nq, d.n_muscles, d.obs_dim, d.delta_dim
+        self.n_links, self.nj, self.nk, self.n_spheres = d.n_links, d.n_joints, d.n_key, d.n_spheres
+        self.frames, self.floating, self.bins = d.frames, bool(d.floating), d.adaptive_bins
+        self.cfg, self.reward = cfg, reward
+
+    # -- plumbing ---------------------------------------------------------------
+    def _s(self, stream):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return C.c_void_p(s.cuda_stream)
+
+    def _ck(self, rcode):
+        if rcode != 0:
+            raise MskError(rcode, lib().msk_gpu_last_error(self.h).decode())
+
+    def _empty(self, *shape, dtype=None):
+        return self.torch.empty(*shape, dtype=dtype or self.torch.float32, device=self.device)
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().msk_gpu_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def launch_count(self):
+        return int(lib().msk_gpu_launch_count(self.h))
+
+    # -- Env verbs (env.hpp:86-123) ---------------------------------------------
+    def set_eval_mode(self, eval_mode=True):
+        self._ck(lib().msk_gpu_set_eval_mode(self.h, int(bool(eval_mode))))
+
+    def reset(self, mask=None, mask_bits=0xFF, obs=None, start_frames=None, stream=None):
+        """Env::reset for envs with ``mask & mask_bits`` (all when mask is None)."""
+        obs = obs if obs is not None else self._empty(self.n, self.obs_dim)
+        self._ck(lib().msk_gpu_reset(self.h, _p(mask), int(mask_bits), _p(obs), _p(start_frames), self._s(stream)))
+        return obs
+
+    def reset_to_frame(self, frames, mask=None, obs=None, stream=None):
+        torch = self.torch
+        fr = torch.as_tensor(frames, dtype=torch.int32, device=self.device).expand(self.n).contiguous()
+        obs = obs if obs is not None else self._empty(self.n, self.obs_dim)
+        bad = self._empty(self.n, dtype=torch.uint8)
+        self._ck(lib().msk_gpu_reset_to_frame(self.h, _p(fr), _p(mask), _p(obs), _p(bad), self._s(stream)))
+        return obs, bad
+
+    def step(self, actions, obs=None, delta=None, reward_aux=None, flags=None, muscle_power=None,
+             contact_force=None, want_power=False, want_contact=False, stream=None):
+        """Env::step for every env; returns a dict of [E x ...] tensors (StepResult fields)."""
+        torch = self.torch
+        a = actions if actions.dtype == torch.float32 and actions.is_contiguous() else actions.float().contiguous()
+        out = dict(
+            obs=obs if obs is not None else self._empty(self.n, self.obs_dim),
+            delta=delta if delta is not None else self._empty(self.n, self.delta_dim),
+            reward_aux=reward_aux if reward_aux is not None else self._empty(self.n),
+            flags=flags if flags is not None else self._empty(self.n, dtype=torch.uint8),
+        )
+        if want_power or muscle_power is not None:
+            out["muscle_power"] = muscle_power if muscle_power is not None else self._empty(self.n, self.nm)
+        if want_contact or contact_force is not None:
+            out["contact_force"] = contact_force if contact_force is not None else self._empty(self.n, self.n_links, 2)
+        self._ck(lib().msk_gpu_step(self.h, _p(a), _p(out["obs"]), _p(out["delta"]), _p(out["reward_aux"]),
+                                    _p(out["flags"]), _p(out.get("muscle_power")), _p(out.get("contact_force")),
+                                    self._s(stream)))
+        return out
+
+    def step_host(self, actions_host, obs_host=None, delta_host=None, reward_aux_host=None, flags_host=None):
+        """Env::step with HOST (ideally pinned) tensors; synchronous, pipelined H2D/kernel/D2H."""
+        self._ck(lib().msk_gpu_step_host(self.h, _p(actions_host), _p(obs_host), _p(delta_host),
+                                         _p(reward_aux_host), _p(flags_host)))
+
+    def observe(self, obs=None, stream=None):
+        obs = obs if obs is not None else self._empty(self.n, self.obs_dim)
+        self._ck(lib().msk_gpu_observe(self.h, _p(obs), self._s(stream)))
+        return obs
+
+    def tracking_error(self, delta=None, stream=None):
+        delta = delta if delta is not None else self._empty(self.n, self.delta_dim)
+        self._ck(lib().msk_gpu_tracking_error(self.h, _p(delta), self._s(stream)))
+        return delta
+
+    def force_state_to_reference(self, stream=None):
+        self._ck(lib().msk_gpu_force_state_to_reference(self.h, self._s(stream)))
+
+    def get_state(self, stream=None):
+        torch = self.torch
+        n, nq, nm = self.n, self.nq, self.nm
+        s = dict(q=self._empty(n, nq, dtype=torch.float64), dq=self._empty(n, nq, dtype=torch.float64),
+                 act=self._empty(n, nm), l_m=self._empty(n, nm), v_m=self._empty(n, nm), f_m=self._empty(n, nm),
+                 t=self._empty(n, dtype=torch.float64), ints=self._empty(n, 4, dtype=torch.int32))
+        self._ck(lib().msk_gpu_get_state(self.h, *[_p(s[k]) for k in ("q", "dq", "act", "l_m", "v_m", "f_m", "t",
+                                                                      "ints")], self._s(stream)))
+        return s
+
+    def set_state(self, s, stream=None):
+        torch = self.torch
+
+        def cv(k, dt):
+            if k not in s or s[k] is None:
+                return None
+            return torch.as_tensor(s[k], dtype=dt, device=self.device).contiguous()
+
+        t = [cv("q", torch.float64), cv("dq", torch.float64), cv("act", torch.float32), cv("l_m", torch.float32),
+             cv("v_m", torch.float32), cv("f_m", torch.float32), cv("t", torch.float64), cv("ints", torch.int32)]
+        self._ck(lib().msk_gpu_set_state(self.h, *[_p(x) for x in t], self._s(stream)))
+        self._keep = t
+
+    def get_sampler(self, stream=None):
+        ema = self._empty(self.n, self.bins, dtype=self.torch.float64)
+        self._ck(lib().msk_gpu_get_sampler(self.h, _p(ema), self._s(stream)))
+        return ema
+
+    def set_sampler(self, ema, stream=None):
+        torch = self.torch
+        e = torch.as_tensor(ema, dtype=torch.float64, device=self.device).contiguous()
+        bcast = int(e.dim() == 1)
+        self._ck(lib().msk_gpu_set_sampler(self.h, _p(e), bcast, self._s(stream)))
+        self._keep = e
+
+    def drain_outcomes(self, cap=64, stream=None):
+        torch = self.torch
+        bins = self._empty(self.n, cap, dtype=torch.int32)
+        failed = self._empty(self.n, cap, dtype=torch.uint8)
+        counts = self._empty(self.n, dtype=torch.int32)
+        self._ck(lib().msk_gpu_drain_outcomes(self.h, _p(bins), _p(failed), _p(counts), int(cap), self._s(stream)))
+        return bins, failed, counts
+
+    def record_own_outcomes(self, stream=None):
+        self._ck(lib().msk_gpu_record_own_outcomes(self.h, self._s(stream)))
+
+    def merge_outcomes(self, bins, failed, counts, stream=None):
+        """Order-fixed merge of gathered outcome blocks (global env order) into one replicated sampler."""
+        n_total, cap = bins.shape
+        self._ck(lib().msk_gpu_merge_outcomes(self.h, _p(bins.contiguous()), _p(failed.contiguous()),
+                                              _p(counts.contiguous()), int(n_total), int(cap), self._s(stream)))
+
+    def rng_raw(self, env, n, stream=None):
+        out = self._empty(n, dtype=self.torch.int64)  # raw u64 bits; view as uint64 on the host
+        self._ck(lib().msk_gpu_rng_raw(self.h, int(env), int(n), _p(out), self._s(stream)))
+        return out
+
+    def fill_excitations(self, seed, step, actions=None, stream=None):
+        actions = actions if actions is not None else self._empty(self.n, self.nm)
+        self._ck(lib().msk_gpu_fill_excitations(self.h, C.c_uint64(seed), C.c_uint32(step), _p(actions),
+                                                self._s(stream)))
+        return actions

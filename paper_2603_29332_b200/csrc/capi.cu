@@ -1,0 +1,619 @@
+// C ABI (include/msk_gpu.h): context ownership, device tables, launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "../../include/msk_gpu.h"
+#include "device.cuh"
+#include "model.hpp"
+
+namespace msk_b200 {
+cudaError_t prepare_kernels(int smem_bytes_per_block);
+int envs_per_block();
+void launch_step(const DevModel&, const DevState&, int env0, int n, const float* actions, float* obs, float* delta,
+                 float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t);
+void launch_reset(const DevModel&, const DevState&, int n, int mode, const uint8_t* mask, uint8_t bits,
+                  const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t);
+void launch_observe(const DevModel&, const DevState&, int n, float* obs, float* delta, cudaStream_t);
+void launch_seed(const DevState&, int n, uint64_t base_seed, cudaStream_t);
+void launch_rng_raw(const DevState&, int e, int n, uint64_t* out, cudaStream_t);
+void launch_record_own(const DevModel&, const DevState&, int n, cudaStream_t);
+void launch_merge(const DevModel&, const DevState&, int n_local, const int* bins, const uint8_t* failed,
+                  const int* counts, long long n_total, int cap, double* global_ema, cudaStream_t);
+void launch_broadcast_ema(const DevState&, int n, int bins, const double* row, cudaStream_t);
+void launch_drain(const DevState&, int n, int cap, int* bins, uint8_t* failed, int* counts, cudaStream_t);
+void launch_get_ints(const DevState&, int n, int* ints, cudaStream_t);
+void launch_set_ints(const DevState&, int n, const int* ints, cudaStream_t);
+void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint32_t step, float* out,
+                        cudaStream_t);
+double measure_fp32_peak_tflops();
+}  // namespace msk_b200
+
+using namespace msk_b200;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct CudaFail : std::exception {
+    std::string msg;
+    explicit CudaFail(std::string m) : msg(std::move(m)) {}
+    const char* what() const noexcept override { return msg.c_str(); }
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kHostChunks = 4;
+
+}  // namespace
+
+struct msk_gpu_ctx {
+    int device = 0;
+    int n_envs = 0;
+    long long env_offset = 0;
+    CompiledModel cm;
+    DevModel M{};
+    DevState St{};
+    std::vector<void*> allocs;
+    std::string err;
+    long long launches = 0;
+    int obs_dim = 0, delta_dim = 0;
+    // host-buffer path
+    cudaStream_t hs[2] = {nullptr, nullptr};
+    float* h_actions = nullptr;  // device staging
+    float* h_obs = nullptr;
+    float* h_delta = nullptr;
+    float* h_raux = nullptr;
+    uint8_t* h_flags = nullptr;
+    double* global_ema = nullptr;
+
+    template <class T>
+    T* dalloc(size_t n) {
+        void* p = nullptr;
+        ck(cudaMalloc(&p, std::max<size_t>(1, n) * sizeof(T)), "cudaMalloc");
+        ck(cudaMemset(p, 0, std::max<size_t>(1, n) * sizeof(T)), "cudaMemset");
+        allocs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    const T* upload(const std::vector<T>& v) {
+        T* p = dalloc<T>(v.size());
+        if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+        return p;
+    }
+    void count(int n = 1) { launches += n; }
+    void check_launch() { ck(cudaGetLastError(), "kernel launch"); }
+};
+
+namespace {
+
+int fail(msk_gpu_ctx* ctx, int code, const std::string& msg) {
+    g_last_error = msg;
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+template <class F>
+int guarded(msk_gpu_ctx* ctx, F&& f) {
+    if (!ctx) return fail(nullptr, MSK_ERR_CONTRACT, "null context");
+    try {
+        ck(cudaSetDevice(ctx->device), "cudaSetDevice");
+        f();
+        return MSK_OK;
+    } catch (const CudaFail& ex) {
+        return fail(ctx, MSK_ERR_CUDA, ex.what());
+    } catch (const std::exception& ex) {
+        return fail(ctx, MSK_ERR_CONTRACT, ex.what());
+    }
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int align16(int x) { return (x + 15) & ~15; }
+
+}  // namespace
+
+extern "C" {
+
+int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const msk_env_config* cfg,
+                   const msk_reward_config* rc, int32_t n_envs, uint64_t base_seed, int64_t global_env_offset,
+                   int device, msk_gpu_ctx** out) {
+    if (!out) return fail(nullptr, MSK_ERR_CONTRACT, "msk_gpu_create: out is null");
+    *out = nullptr;
+    auto ctx = new msk_gpu_ctx();
+    try {
+        if (n_envs < 1) throw ConfigError("msk_gpu_create: n_envs must be >= 1");
+        if (!model_json_path || !clip_csv_path) throw ConfigError("msk_gpu_create: model and clip paths required");
+        const ModelSpec spec = load_model(model_json_path);
+        const auto errs = spec.validate();
+        if (!errs.empty()) throw ConfigError("model '" + std::string(model_json_path) + "': " + errs.front());
+        const Clip clip = load_clip(clip_csv_path, spec);
+        msk_env_config ec{250, 1, 10, 0, 0.2, 0.99, 0.5, 0.01};
+        if (cfg) ec = *cfg;
+        msk_reward_config rw{0, 0, 100.0, 0.05, nullptr};
+        if (rc) rw = *rc;
+        std::vector<int32_t> emg_map(rw.emg_channel_map, rw.emg_channel_map + std::max(0, rw.n_emg_channels));
+        for (int ch : emg_map)
+            if (ch < 0 || ch >= static_cast<int>(spec.muscles.size()))
+                throw ConfigError("env: emg channel map references missing muscle");
+        if (rw.mode == 1 && static_cast<int>(emg_map.size()) != clip.n_emg)
+            throw ConfigError("env: emg channel map size must match reference emg columns");
+        ctx->cm = compile_model(spec);
+        const CompiledModel& c = ctx->cm;
+        if (c.nq > 32 * kMaxQSlots) throw ConfigError("model too large: n_q > 128");
+        if (c.nl > 32 * kMaxLinkSlots) throw ConfigError("model too large: n_links > 128");
+
+        int ndev = 0;
+        ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) throw CudaFail("no CUDA device " + std::to_string(device));
+        cudaDeviceProp prop{};
+        ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10) throw CudaFail("msk_gpu requires an sm_100 (Blackwell B200) device, found sm_" +
+                                             std::to_string(prop.major) + std::to_string(prop.minor));
+        ctx->device = device;
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        ctx->n_envs = n_envs;
+        ctx->env_offset = global_env_offset;
+
+        DevModel& M = ctx->M;
+        M.nl = c.nl;
+        M.nj = c.nj;
+        M.nq = c.nq;
+        M.nrd = c.nrd;
+        M.nm = c.nm;
+        M.nk = c.nk;
+        M.ns = c.ns;
+        M.floating = c.floating;
+        M.n_levels = c.n_levels;
+        M.n_pairs = c.n_pairs;
+        M.frames = clip.frames;
+        M.n_emg = clip.n_emg;
+        M.bins = std::max(1, ec.adaptive_bins);
+        M.gravity = c.gravity;
+        M.k_lim = c.k_lim;
+        M.k_lim_d = c.k_lim_d;
+        M.c_k = c.c_k;
+        M.c_c = c.c_c;
+        M.c_mu = c.c_mu;
+        M.inv_c_vs = c.inv_c_vs;
+        M.link_parent = ctx->upload(c.link_parent);
+        M.link_dof = ctx->upload(c.link_dof);
+        M.link_ax = ctx->upload(c.link_ax);
+        M.link_az = ctx->upload(c.link_az);
+        M.link_com = ctx->upload(c.link_com);
+        M.link_mass = ctx->upload(c.link_mass);
+        M.link_inertia = ctx->upload(c.link_inertia);
+        M.link_mount = ctx->upload(c.link_mount);
+        M.level_start = ctx->upload(c.level_start);
+        M.level_links = ctx->upload(c.level_links);
+        M.child_start = ctx->upload(c.child_start);
+        M.child_list = ctx->upload(c.child_list);
+        M.sphere_start = ctx->upload(c.sphere_start);
+        M.sphere_x = ctx->upload(c.sphere_x);
+        M.sphere_z = ctx->upload(c.sphere_z);
+        M.sphere_r = ctx->upload(c.sphere_r);
+        M.joint_damping = ctx->upload(c.joint_damping);
+        M.joint_lo = ctx->upload(c.joint_lo);
+        M.joint_hi = ctx->upload(c.joint_hi);
+        M.joint_slot_start = ctx->upload(c.joint_slot_start);
+        M.m_fmax = ctx->upload(c.m_fmax);
+        M.m_lopt = ctx->upload(c.m_lopt);
+        M.m_inv_lopt = ctx->upload(c.m_inv_lopt);
+        M.m_slack = ctx->upload(c.m_slack);
+        M.m_kv = ctx->upload(c.m_kv);
+        M.m_ndt_act = ctx->upload(c.m_ndt_act);
+        M.m_ndt_deact = ctx->upload(c.m_ndt_deact);
+        M.m_pw = ctx->upload(c.m_pw);
+        M.m_via_start = ctx->upload(c.m_via_start);
+        M.m_pair_start = ctx->upload(c.m_pair_start);
+        M.m_seg_start = ctx->upload(c.m_seg_start);
+        M.seg_info = ctx->upload(c.seg_info);
+        M.seg_slot = ctx->upload(c.seg_slot);
+        M.seg_ax = ctx->upload(c.seg_ax);
+        M.seg_az = ctx->upload(c.seg_az);
+        M.seg_cx = ctx->upload(c.seg_cx);
+        M.seg_cz = ctx->upload(c.seg_cz);
+        M.via_link = ctx->upload(c.via_link);
+        M.via_x = ctx->upload(c.via_x);
+        M.via_z = ctx->upload(c.via_z);
+        M.pair_joint = ctx->upload(c.pair_joint);
+        M.pair_via = ctx->upload(c.pair_via);
+        M.pair_slot = ctx->upload(c.pair_slot);
+        M.pair_sign = ctx->upload(c.pair_sign);
+        M.key_bodies = ctx->upload(c.key_bodies);
+        M.clip_q = ctx->upload(clip.q);
+        M.clip_dq = ctx->upload(clip.dq);
+        M.clip_kp = ctx->upload(clip.key_pos);
+        M.clip_ka = ctx->upload(clip.key_angle);
+        M.clip_emg = ctx->upload(clip.emg);
+        M.horizon = ec.episode_horizon;
+        M.rsi = ec.rsi;
+        M.eval_mode = 0;
+        M.reward_mode = rw.mode;
+        M.n_emg_ch = static_cast<int>(emg_map.size());
+        M.mix = ec.adaptive_mix;
+        M.decay = ec.adaptive_decay;
+        M.term_err = ec.termination_body_err;
+        M.init_act = ec.init_activation;
+        M.w_emg = static_cast<float>(rw.w_emg);
+        M.w_power = static_cast<float>(rw.w_power);
+        M.emg_map = ctx->upload(emg_map);
+        // per-env shared-memory layout
+        int off = 16 * c.nl;
+        M.off_theta = off;
+        off = align16(off + 4 * c.nl);
+        M.off_qang = off;
+        off = align16(off + 4 * c.nq);
+        M.off_dqf = off;
+        off = align16(off + 4 * c.nq);
+        M.off_tau = off;
+        off = align16(off + 4 * c.nq);
+        M.off_root = off;
+        off = align16(off + 16);
+        M.off_relcs = off;
+        off = align16(off + 8 * c.nq);
+        M.off_union = off;
+        off = align16(off + 4 * std::max({c.n_pairs, 16 * c.nl, 2 * c.nq}));
+        M.smem_env_bytes = off;
+        const int per_block = envs_per_block() * M.smem_env_bytes;
+        if (per_block > static_cast<int>(prop.sharedMemPerBlockOptin))
+            throw ConfigError("model needs " + std::to_string(per_block) + " B of shared memory per block");
+        ck(prepare_kernels(per_block), "cudaFuncSetAttribute");
+
+        DevState& S = ctx->St;
+        const size_t E = static_cast<size_t>(n_envs);
+        S.q = ctx->dalloc<double>(E * c.nq);
+        S.dq = ctx->dalloc<double>(E * c.nq);
+        S.act = ctx->dalloc<float>(E * c.nm);
+        S.lm = ctx->dalloc<float>(E * c.nm);
+        S.vm = ctx->dalloc<float>(E * c.nm);
+        S.fm = ctx->dalloc<float>(E * c.nm);
+        S.t = ctx->dalloc<double>(E);
+        S.t_index = ctx->dalloc<int>(E);
+        S.start = ctx->dalloc<int>(E);
+        S.steps = ctx->dalloc<int>(E);
+        S.done = ctx->dalloc<uint8_t>(E);
+        S.mt = ctx->dalloc<uint64_t>(E * 312);
+        S.mti = ctx->dalloc<int>(E);
+        S.ema = ctx->dalloc<double>(E * M.bins);
+        S.out_cap = 64;
+        S.out_bin = ctx->dalloc<int>(E * S.out_cap);
+        S.out_failed = ctx->dalloc<uint8_t>(E * S.out_cap);
+        S.out_count = ctx->dalloc<int>(E);
+        S.power_scratch = rw.mode == 2 ? ctx->dalloc<float>(E * c.nm) : nullptr;
+        ctx->global_ema = ctx->dalloc<double>(M.bins);
+        ctx->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
+        ctx->delta_dim = 3 + c.nj + 2 * c.nk;
+
+        launch_seed(S, n_envs, base_seed + static_cast<uint64_t>(global_env_offset), nullptr);
+        launch_reset(M, S, n_envs, 3 /* kResetInit */, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr);
+        ctx->count(2);
+        ctx->check_launch();
+        ck(cudaDeviceSynchronize(), "create");
+        *out = ctx;
+        return MSK_OK;
+    } catch (const CudaFail& ex) {
+        const int code = fail(nullptr, MSK_ERR_CUDA, ex.what());
+        msk_gpu_destroy(ctx);
+        return code;
+    } catch (const std::exception& ex) {
+        const int code = fail(nullptr, MSK_ERR_CONTRACT, ex.what());
+        msk_gpu_destroy(ctx);
+        return code;
+    }
+}
+
+void msk_gpu_destroy(msk_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    for (void* p : ctx->allocs) cudaFree(p);
+    for (auto& s : ctx->hs)
+        if (s) cudaStreamDestroy(s);
+    delete ctx;
+}
+
+const char* msk_gpu_last_error(const msk_gpu_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+int msk_gpu_dims(const msk_gpu_ctx* ctx, msk_dims* out) {
+    if (!ctx || !out) return fail(nullptr, MSK_ERR_CONTRACT, "msk_gpu_dims: null argument");
+    const auto& c = ctx->cm;
+    out->n_envs = ctx->n_envs;
+    out->nq = c.nq;
+    out->n_muscles = c.nm;
+    out->obs_dim = ctx->obs_dim;
+    out->delta_dim = ctx->delta_dim;
+    out->n_links = c.nl;
+    out->n_joints = c.nj;
+    out->n_key = c.nk;
+    out->n_spheres = c.ns;
+    out->frames = ctx->M.frames;
+    out->floating = c.floating;
+    out->adaptive_bins = ctx->M.bins;
+    return MSK_OK;
+}
+
+int msk_gpu_set_eval_mode(msk_gpu_ctx* ctx, int32_t eval_mode) {
+    return guarded(ctx, [&] { ctx->M.eval_mode = eval_mode != 0; });
+}
+
+int msk_gpu_reset(msk_gpu_ctx* ctx, const uint8_t* mask, uint8_t mask_bits, float* obs, int32_t* start_frames,
+                  void* stream) {
+    return guarded(ctx, [&] {
+        launch_reset(ctx->M, ctx->St, ctx->n_envs, 0, mask, mask ? mask_bits : 0, nullptr, obs, start_frames, nullptr,
+                     as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_reset_to_frame(msk_gpu_ctx* ctx, const int32_t* frames, const uint8_t* mask, float* obs, uint8_t* bad,
+                           void* stream) {
+    return guarded(ctx, [&] {
+        if (!frames) throw ConfigError("reset_to_frame: frames is null");
+        launch_reset(ctx->M, ctx->St, ctx->n_envs, 1, mask, 0xff, frames, obs, nullptr, bad, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward_aux, uint8_t* flags,
+                 float* muscle_power, float* contact_force, void* stream) {
+    return guarded(ctx, [&] {
+        if (!actions) throw ConfigError("step: actions is null");
+        launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, obs, delta, reward_aux, flags, muscle_power,
+                    contact_force, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                      float* reward_aux_host, uint8_t* flags_host) {
+    return guarded(ctx, [&] {
+        if (!actions_host) throw ConfigError("step_host: actions is null");
+        const size_t E = static_cast<size_t>(ctx->n_envs);
+        const int nm = ctx->cm.nm;
+        if (!ctx->hs[0]) {
+            for (auto& s : ctx->hs) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+            ctx->h_actions = ctx->dalloc<float>(E * nm);
+            ctx->h_obs = ctx->dalloc<float>(E * ctx->obs_dim);
+            ctx->h_delta = ctx->dalloc<float>(E * ctx->delta_dim);
+            ctx->h_raux = ctx->dalloc<float>(E);
+            ctx->h_flags = ctx->dalloc<uint8_t>(E);
+        }
+        // Chunked pipeline: H2D(actions c) -> step(c) -> D2H(outputs c), two
+        // streams so chunk c's transfers overlap chunk c-1's kernel.
+        const int chunks = static_cast<int>(std::min<size_t>(kHostChunks, E));
+        const size_t per = (E + chunks - 1) / chunks;
+        for (int c = 0; c < chunks; ++c) {
+            const size_t e0 = c * per, n = std::min(per, E - e0);
+            if (n == 0) break;
+            cudaStream_t s = ctx->hs[c & 1];
+            ck(cudaMemcpyAsync(ctx->h_actions + e0 * nm, actions_host + e0 * nm, n * nm * sizeof(float),
+                               cudaMemcpyHostToDevice, s),
+               "H2D actions");
+            launch_step(ctx->M, ctx->St, static_cast<int>(e0), static_cast<int>(n), ctx->h_actions + e0 * nm,
+                        ctx->h_obs + e0 * ctx->obs_dim, ctx->h_delta + e0 * ctx->delta_dim, ctx->h_raux + e0,
+                        ctx->h_flags + e0, nullptr, nullptr, s);
+            ctx->count();
+            ctx->check_launch();
+            if (obs_host)
+                ck(cudaMemcpyAsync(obs_host + e0 * ctx->obs_dim, ctx->h_obs + e0 * ctx->obs_dim,
+                                   n * ctx->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s),
+                   "D2H obs");
+            if (delta_host)
+                ck(cudaMemcpyAsync(delta_host + e0 * ctx->delta_dim, ctx->h_delta + e0 * ctx->delta_dim,
+                                   n * ctx->delta_dim * sizeof(float), cudaMemcpyDeviceToHost, s),
+                   "D2H delta");
+            if (reward_aux_host)
+                ck(cudaMemcpyAsync(reward_aux_host + e0, ctx->h_raux + e0, n * sizeof(float), cudaMemcpyDeviceToHost,
+                                   s),
+                   "D2H reward_aux");
+            if (flags_host)
+                ck(cudaMemcpyAsync(flags_host + e0, ctx->h_flags + e0, n, cudaMemcpyDeviceToHost, s), "D2H flags");
+        }
+        for (auto& s : ctx->hs) ck(cudaStreamSynchronize(s), "step_host sync");
+    });
+}
+
+int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream) {
+    return guarded(ctx, [&] {
+        launch_observe(ctx->M, ctx->St, ctx->n_envs, obs, nullptr, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream) {
+    return guarded(ctx, [&] {
+        launch_observe(ctx->M, ctx->St, ctx->n_envs, nullptr, delta, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_force_state_to_reference(msk_gpu_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        launch_reset(ctx->M, ctx->St, ctx->n_envs, 2, nullptr, 0, nullptr, nullptr, nullptr, nullptr,
+                     as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float* l_m, float* v_m, float* f_m,
+                      double* t, int32_t* ints, void* stream) {
+    return guarded(ctx, [&] {
+        const size_t E = ctx->n_envs, nq = ctx->cm.nq, nm = ctx->cm.nm;
+        cudaStream_t s = as_stream(stream);
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (dst) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s), "get_state");
+        };
+        cp(q, ctx->St.q, E * nq * 8);
+        cp(dq, ctx->St.dq, E * nq * 8);
+        cp(act, ctx->St.act, E * nm * 4);
+        cp(l_m, ctx->St.lm, E * nm * 4);
+        cp(v_m, ctx->St.vm, E * nm * 4);
+        cp(f_m, ctx->St.fm, E * nm * 4);
+        cp(t, ctx->St.t, E * 8);
+        if (ints) {
+            launch_get_ints(ctx->St, ctx->n_envs, ints, s);
+            ctx->count();
+            ctx->check_launch();
+        }
+    });
+}
+
+int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const float* l_m,
+                      const float* v_m, const float* f_m, const double* t, const int32_t* ints, void* stream) {
+    return guarded(ctx, [&] {
+        const size_t E = ctx->n_envs, nq = ctx->cm.nq, nm = ctx->cm.nm;
+        cudaStream_t s = as_stream(stream);
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (src) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s), "set_state");
+        };
+        cp(ctx->St.q, q, E * nq * 8);
+        cp(ctx->St.dq, dq, E * nq * 8);
+        cp(ctx->St.act, act, E * nm * 4);
+        cp(ctx->St.lm, l_m, E * nm * 4);
+        cp(ctx->St.vm, v_m, E * nm * 4);
+        cp(ctx->St.fm, f_m, E * nm * 4);
+        cp(ctx->St.t, t, E * 8);
+        if (ints) {
+            launch_set_ints(ctx->St, ctx->n_envs, ints, s);
+            ctx->count();
+            ctx->check_launch();
+        }
+    });
+}
+
+int msk_gpu_get_sampler(msk_gpu_ctx* ctx, double* ema, void* stream) {
+    return guarded(ctx, [&] {
+        ck(cudaMemcpyAsync(ema, ctx->St.ema, sizeof(double) * ctx->n_envs * ctx->M.bins, cudaMemcpyDeviceToDevice,
+                           as_stream(stream)),
+           "get_sampler");
+    });
+}
+
+int msk_gpu_set_sampler(msk_gpu_ctx* ctx, const double* ema, int32_t broadcast, void* stream) {
+    return guarded(ctx, [&] {
+        if (broadcast) {
+            launch_broadcast_ema(ctx->St, ctx->n_envs, ctx->M.bins, ema, as_stream(stream));
+            ctx->count();
+            ctx->check_launch();
+        } else {
+            ck(cudaMemcpyAsync(ctx->St.ema, ema, sizeof(double) * ctx->n_envs * ctx->M.bins,
+                               cudaMemcpyDeviceToDevice, as_stream(stream)),
+               "set_sampler");
+        }
+    });
+}
+
+int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int32_t* counts, int32_t cap,
+                           void* stream) {
+    return guarded(ctx, [&] {
+        if (!bins || !failed || !counts || cap < 0) throw ConfigError("drain_outcomes: bad arguments");
+        launch_drain(ctx->St, ctx->n_envs, cap, bins, failed, counts, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_record_own_outcomes(msk_gpu_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        launch_record_own(ctx->M, ctx->St, ctx->n_envs, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_merge_outcomes(msk_gpu_ctx* ctx, const int32_t* bins, const uint8_t* failed, const int32_t* counts,
+                           int64_t n_envs_total, int32_t cap, void* stream) {
+    return guarded(ctx, [&] {
+        if (!bins || !failed || !counts || cap < 0 || n_envs_total < 0)
+            throw ConfigError("merge_outcomes: bad arguments");
+        // the global sampler starts from env 0's current EMA (all envs hold the
+        // same replicated EMA under this convention)
+        ck(cudaMemcpyAsync(ctx->global_ema, ctx->St.ema, sizeof(double) * ctx->M.bins, cudaMemcpyDeviceToDevice,
+                           as_stream(stream)),
+           "merge_outcomes");
+        launch_merge(ctx->M, ctx->St, ctx->n_envs, bins, failed, counts, n_envs_total, cap, ctx->global_ema,
+                     as_stream(stream));
+        ctx->count(2);
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_rng_raw(msk_gpu_ctx* ctx, int32_t env, int32_t n, uint64_t* out, void* stream) {
+    return guarded(ctx, [&] {
+        if (env < 0 || env >= ctx->n_envs || n < 0 || !out) throw ConfigError("rng_raw: bad arguments");
+        launch_rng_raw(ctx->St, env, n, out, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_fill_excitations(msk_gpu_ctx* ctx, uint64_t seed, uint32_t step, float* actions, void* stream) {
+    return guarded(ctx, [&] {
+        if (!actions) throw ConfigError("fill_excitations: actions is null");
+        launch_excitations(ctx->n_envs, ctx->cm.nm, ctx->env_offset, seed, step, actions, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int64_t msk_gpu_launch_count(const msk_gpu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int msk_gpu_validate(const char* model_json_path, const char* clip_csv_path, msk_dims* dims) {
+    try {
+        if (!model_json_path) throw ConfigError("validate: model path is null");
+        const ModelSpec spec = load_model(model_json_path);
+        const auto errs = spec.validate();
+        if (!errs.empty()) throw ConfigError("model '" + std::string(model_json_path) + "': " + errs.front());
+        Clip clip;
+        if (clip_csv_path && clip_csv_path[0]) clip = load_clip(clip_csv_path, spec);
+        const CompiledModel c = compile_model(spec);
+        if (dims) {
+            dims->n_envs = 0;
+            dims->nq = c.nq;
+            dims->n_muscles = c.nm;
+            dims->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
+            dims->delta_dim = 3 + c.nj + 2 * c.nk;
+            dims->n_links = c.nl;
+            dims->n_joints = c.nj;
+            dims->n_key = c.nk;
+            dims->n_spheres = c.ns;
+            dims->frames = clip.frames;
+            dims->floating = c.floating;
+            dims->adaptive_bins = 0;
+        }
+        return MSK_OK;
+    } catch (const std::exception& ex) {
+        return fail(nullptr, MSK_ERR_CONTRACT, ex.what());
+    }
+}
+
+int msk_gpu_fp32_peak_probe(int device, double* tflops) {
+    try {
+        if (!tflops) throw ConfigError("fp32_peak_probe: null output");
+        ck(cudaSetDevice(device), "cudaSetDevice");
+        *tflops = measure_fp32_peak_tflops();
+        return MSK_OK;
+    } catch (const CudaFail& ex) {
+        return fail(nullptr, MSK_ERR_CUDA, ex.what());
+    } catch (const std::exception& ex) {
+        return fail(nullptr, MSK_ERR_CONTRACT, ex.what());
+    }
+}
+
+}  // extern "C"

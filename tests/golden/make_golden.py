@@ -1,0 +1,81 @@
+#!/usr/bin/env python3
+"""Generates the golden fixtures from the REFERENCE itself.
+
+Runs the reference's own msk::Env (oracle/_ref/libmsk_ref.so, compiled
+unchanged from /root/reference/proj/src by oracle/Makefile) on seeded inputs
+and stores what it produced, so the parity tests on machines without
+/root/reference (the GPU box) still check against reference output.
+
+    python tests/golden/make_golden.py      # writes tests/golden/*.npz
+
+Each fixture holds, for E envs of one model/clip: the start frames of two
+rounds of RSI resets, the excitations, and after every control step the
+flags, Δ, observation, reward_aux and the full state (q, dq, act, l_m, v_m,
+f_m, t, t_index/start/steps/done), plus raw mt19937_64 draws and the sampler.
+"""
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+from conftest import ensure_assets, model_paths  # noqa: E402
+from oracle.ref import RefBatch, env_config, excitations  # noqa: E402
+
+from golden_cases import CASES  # noqa: E402
+
+
+def make(name):
+    n, steps, cfg_kw, mode = CASES[name]
+    mp, cp = model_paths(name)
+    b = RefBatch(mp, cp, n, base_seed=0x5EED, cfg=env_config(**cfg_kw), reward_mode=mode)
+    # a non-trivial sampler so RSI exercises the failure-proportional branch
+    ema = np.linspace(0.0, 0.3, b.bins)[None, :] * (1 + np.arange(n)[:, None] * 0.1)
+    b.set_sampler(ema)
+    obs0, frames0 = b.reset()
+    rec = dict(frames0=frames0, obs0=obs0, ema0=ema)
+    keys = ("flags", "delta", "obs", "reward_aux", "power")
+    hist = {k: [] for k in keys}
+    shist = {k: [] for k in ("q", "dq", "act", "l_m", "v_m", "f_m", "t", "ints")}
+    acts, reset_frames = [], []
+    for s in range(steps):
+        a = excitations(0xA11CE, s, n, b.nm)
+        acts.append(a)
+        r = b.step(a)
+        for k in keys:
+            hist[k].append(r[k])
+        st = b.get_state()
+        for k in shist:
+            shist[k].append(st[k])
+        done = (r["flags"] & 1).astype(np.uint8)
+        fr = np.full(n, -1, dtype=np.int32)
+        if done.any():
+            b.record_own_outcomes()
+            _, f = b.reset(mask=done)
+            fr = np.where(done > 0, f, -1)
+        reset_frames.append(fr)
+    rec.update({k: np.stack(v) for k, v in hist.items()})
+    rec.update({"state_" + k: np.stack(v) for k, v in shist.items()})
+    rec["actions"] = np.stack(acts)
+    rec["reset_frames"] = np.stack(reset_frames)
+    rec["ema_end"] = b.get_sampler()
+    rec["rng_draws"] = b.rng_raw(0, 400)  # crosses a 312-word twist
+    rec["meta"] = np.array([n, steps, mode], dtype=np.int64)
+    return rec
+
+
+def main():
+    ensure_assets()
+    for name in CASES:
+        rec = make(name)
+        path = os.path.join(HERE, f"{name}.npz")
+        np.savez_compressed(path, **rec)
+        print(path, os.path.getsize(path))
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,71 @@
+"""Shared helpers for GPU-vs-oracle parity (tests and the diagnostics script).
+
+Parity protocol: both sides start a control step from the
+SAME state — the oracle's f64 state with the muscle state rounded to the
+device's f32 storage — and the same f32 excitations; the CUDA step is then
+compared with the oracle (oracle/msk_oracle.c, itself bit-identical to the
+reference build in oracle/_ref).
+"""
+import numpy as np
+
+from oracle.oracle import OracleBatch, excitations as oracle_excitations  # noqa: F401
+from oracle.ref import env_config
+
+
+def to_np(t):
+    return t.detach().cpu().numpy()
+
+
+def make_pair(model, clip, n, cfg_kw=None, reward_mode=0, base_seed=0x5EED, **kw):
+    import paper_2603_29332_b200 as pk
+
+    cfg_kw = dict(cfg_kw or {})
+    gcfg = pk.EnvConfig(**cfg_kw)
+    g = pk.EnvBatch(model, clip, n, cfg=gcfg, reward=pk.RewardConfig(mode=reward_mode, **kw), base_seed=base_seed)
+    o = OracleBatch(model, clip, n, base_seed=base_seed, cfg=env_config(**cfg_kw), reward_mode=reward_mode, **kw)
+    return g, o
+
+
+def f32_state(s):
+    s = {k: np.array(v) for k, v in s.items()}
+    for k in ("act", "l_m", "v_m", "f_m"):
+        s[k] = s[k].astype(np.float32).astype(np.float64)
+    return s
+
+
+def sync_from_oracle(g, o):
+    s = f32_state(o.get_state())
+    o.set_state(s)
+    g.set_state(s)
+    return s
+
+
+def gpu_state(g):
+    import torch
+
+    s = g.get_state()
+    torch.cuda.synchronize()
+    return {k: to_np(v).astype(np.float64) if k != "ints" else to_np(v) for k, v in s.items()}
+
+
+def rel_err(a, b, floor):
+    """max |a-b| / max(|b|, floor) elementwise."""
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor))) if a.size else 0.0
+
+
+def step_both(g, o, actions32):
+    import torch
+
+    a = torch.as_tensor(actions32, device=g.device)
+    out_g = g.step(a, want_power=True, want_contact=True)
+    torch.cuda.synchronize()
+    out_o = o.step(actions32.astype(np.float64))
+    out_g = {k: to_np(v) for k, v in out_g.items()}
+    return out_g, out_o
+
+
+def force_err(fm_g, fm_o, fmax):
+    """|ΔF| / f_max (force agreement relative to the muscle's max isometric force)."""
+    return float(np.max(np.abs(fm_g - fm_o) / fmax[None, :]))

@@ -1,0 +1,307 @@
+"""GPU parity tests: the sm_100a path (through the C ABI) vs the oracle.
+
+Tolerances (north_star: "rel <= 1e-4 on forces, <= 1e-5 on q/qdot"), for ONE
+control step (10 substeps) from identical state and excitations:
+  q, q̇        max|Δ| <= 1e-5 * max(1, max|ref|)      (per env, norm-wise)
+  activation  max|Δ| <= 1e-6
+  muscle force |ΔF| <= 1e-4 * f_max                  (per muscle)
+  Δ (tracking error) max|Δ| <= 1e-5 m / rad
+  observation max|Δ| <= 1e-4 * max(1, |ref|)         (element-wise)
+  flags, t_index, steps, start frames, RNG draws, sampler: bit-exact.
+Bounded drift over a short horizon is checked separately with a looser bound.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import model_paths
+from golden_cases import CASES
+from parity_util import f32_state, force_err, gpu_state, make_pair, step_both, sync_from_oracle, to_np
+from oracle.oracle import excitations
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+MODELS = ["pendulum1_m2", "arm2_m6", "walker5_m16", "wb700_fixed", "wb700", "wb700_backflip"]
+
+
+def _envs(name):
+    return 3 if name.startswith("wb700") else 8
+
+
+def _single_step_errors(g, o, step_seed):
+    sync_from_oracle(g, o)
+    a = excitations(step_seed, 0, g.n, g.nm).astype(np.float32)
+    og, oo = step_both(g, o, a)
+    sg, so = gpu_state(g), o.get_state()
+    return og, oo, sg, so
+
+
+@pytest.mark.parametrize("name", MODELS)
+def test_single_step_parity(assets, name):
+    import torch
+
+    n = _envs(name)
+    mp, cp = model_paths(name)
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    fmax = o.model.d["m_fmax"]
+    frames = (np.arange(n) * 97 + 13) % (o.frames - 2)
+    for trial in range(3):
+        g.reset_to_frame(frames + trial)
+        o.reset_to_frame(frames + trial)
+        torch.cuda.synchronize()
+        # perturb the start state so velocities/activations are non-trivial
+        s = o.get_state()
+        rng = np.random.default_rng(trial)
+        s["dq"] = s["dq"] + rng.normal(0, 0.3, s["dq"].shape)
+        s["act"] = rng.uniform(0, 1, s["act"].shape)
+        s = f32_state(s)
+        o.set_state(s)
+        g.set_state(s)
+        a = excitations(1000 + trial, 0, n, g.nm).astype(np.float32)
+        og, oo = step_both(g, o, a)
+        sg, so = gpu_state(g), o.get_state()
+        for e in range(n):
+            for k in ("q", "dq"):
+                err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
+                assert err <= 1e-5, (name, trial, e, k, err)
+        assert np.abs(sg["act"] - so["act"]).max() <= 1e-6
+        assert force_err(sg["f_m"], so["f_m"], fmax) <= 1e-4, force_err(sg["f_m"], so["f_m"], fmax)
+        assert np.abs(og["delta"] - oo["delta"]).max() <= 1e-5
+        obs_err = np.abs(og["obs"] - oo["obs"]) / np.maximum(1.0, np.abs(oo["obs"]))
+        assert obs_err.max() <= 1e-4, obs_err.max()
+        assert np.array_equal(og["flags"], oo["flags"])
+        assert np.array_equal(sg["ints"], so["ints"])
+        assert np.allclose(sg["t"], so["t"], rtol=0, atol=1e-12)
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["arm2_m6", "walker5_m16", "wb700_fixed", "wb700"])
+def test_short_horizon_drift(assets, name):
+    """Free-running GPU and oracle from one state: bounded divergence over 20 steps."""
+    n = _envs(name)
+    mp, cp = model_paths(name)
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    frames = (np.arange(n) * 53 + 7) % (o.frames - 30)
+    g.reset_to_frame(frames)
+    o.reset_to_frame(frames)
+    sync_from_oracle(g, o)
+    worst = 0.0
+    for s in range(20):
+        a = excitations(77, s, n, g.nm).astype(np.float32)
+        og, oo = step_both(g, o, a)
+        sg, so = gpu_state(g), o.get_state()
+        worst = max(worst, np.abs(sg["q"] - so["q"]).max() / max(1.0, np.abs(so["q"]).max()))
+        assert np.array_equal(og["flags"], oo["flags"])
+    assert worst < 1e-3, worst
+    g.close()
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_reset_logic_bit_exact_vs_reference_golden(assets, name):
+    """Start frames, t_index/steps/done, outcomes, sampler EMA and raw mt19937_64
+    draws equal the REFERENCE's (tests/golden, produced by oracle/_ref)."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    gd = np.load(os.path.join(HERE, "golden", name + ".npz"))
+    n, steps, mode = [int(x) for x in gd["meta"]]
+    cfg_kw = CASES[name][2]
+    mp, cp = model_paths(name)
+    g = pk.EnvBatch(mp, cp, n, cfg=pk.EnvConfig(**cfg_kw), reward=pk.RewardConfig(mode=mode))
+    g.set_sampler(torch.as_tensor(gd["ema0"], device=g.device))
+    sf = torch.empty(n, dtype=torch.int32, device=g.device)
+    obs0 = g.reset(start_frames=sf)
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(sf), gd["frames0"])
+    assert np.abs(to_np(obs0) - gd["obs0"]).max() / max(1.0, np.abs(gd["obs0"]).max()) < 1e-4
+    # Replay the reference's trajectory state-by-state: before every step load
+    # the reference's pre-step state (so termination/reset decisions depend on
+    # the reference's numbers), then require identical flags and reset frames.
+    for s in range(steps):
+        if s > 0:
+            prev = {k: gd["state_" + k][s - 1] for k in ("q", "dq", "act", "l_m", "v_m", "f_m", "t", "ints")}
+            done = (gd["flags"][s - 1] & 1) > 0
+            if not done.any():
+                g.set_state(f32_state(prev) | {"ints": prev["ints"]})
+        out = g.step(torch.as_tensor(gd["actions"][s].astype(np.float32), device=g.device))
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(out["flags"]), gd["flags"][s]), s
+        d = (to_np(out["flags"]) & 1).astype(np.uint8)
+        if d.any():
+            g.record_own_outcomes()
+            fr = torch.full((n,), -1, dtype=torch.int32, device=g.device)
+            g.reset(mask=torch.as_tensor(d, device=g.device), start_frames=fr)
+            torch.cuda.synchronize()
+            got = np.where(d > 0, to_np(fr), -1)
+            assert np.array_equal(got, gd["reset_frames"][s]), s
+    assert np.array_equal(to_np(g.get_sampler()), gd["ema_end"])
+    draws = to_np(g.rng_raw(0, 400)).view(np.uint64)
+    assert np.array_equal(draws, gd["rng_draws"])
+    g.close()
+
+
+def test_rsi_reset_sequences_match_oracle(assets):
+    """Hundreds of RSI resets with a non-uniform sampler: identical start frames."""
+    import torch
+
+    mp, cp = model_paths("walker5_m16")
+    n = 64
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=5, rsi=True, adaptive_bins=7))
+    ema = np.random.default_rng(3).uniform(0, 1, (n, 7))
+    ema[::5] = 0.0  # the total <= 1e-12 branch
+    g.set_sampler(torch.as_tensor(ema, device=g.device))
+    o.set_sampler(ema)
+    for r in range(20):
+        sf = torch.empty(n, dtype=torch.int32, device=g.device)
+        g.reset(start_frames=sf)
+        _, fo = o.reset()
+        torch.cuda.synchronize()
+        assert np.array_equal(to_np(sf), fo), r
+    for e in (0, 17, 63):
+        assert np.array_equal(to_np(g.rng_raw(e, 50)).view(np.uint64), o.rng_raw(e, 50))
+    g.close()
+
+
+def test_determinism_and_sharding_invariance(assets):
+    """Same inputs -> bit-identical outputs; per-env results independent of the shard split."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("wb700")
+    cfg = pk.EnvConfig(episode_horizon=1000, rsi=True)
+    full = pk.EnvBatch(mp, cp, 8, cfg=cfg)
+    halves = [pk.EnvBatch(mp, cp, 4, cfg=cfg, global_env_offset=4 * r) for r in range(2)]
+    outs_full, outs_half = [], []
+    full.reset()
+    for h in halves:
+        h.reset()
+    a = torch.empty(8, full.nm, device=full.device)
+    for s in range(3):
+        full.fill_excitations(5, s, a)
+        outs_full.append({k: to_np(v) for k, v in full.step(a).items()})
+        parts = [h.step(a[4 * r:4 * r + 4].contiguous()) for r, h in enumerate(halves)]
+        outs_half.append({k: np.concatenate([to_np(p[k]) for p in parts]) for k in parts[0]})
+    for x, y in zip(outs_full, outs_half):
+        for k in x:
+            assert np.array_equal(x[k], y[k]), k
+    # determinism: replay from the same state
+    st = full.get_state()
+    full.fill_excitations(9, 0, a)
+    o1 = {k: to_np(v) for k, v in full.step(a).items()}
+    full.set_state(st)
+    o2 = {k: to_np(v) for k, v in full.step(a).items()}
+    for k in o1:
+        assert np.array_equal(o1[k], o2[k]), k
+    for b in [full] + halves:
+        b.close()
+
+
+def test_excitations_match_oracle(assets):
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("arm2_m6")
+    g = pk.EnvBatch(mp, cp, 5, global_env_offset=11)
+    a = g.fill_excitations(0x5EED, 42)
+    torch.cuda.synchronize()
+    ref = excitations(0x5EED, 42, 5, g.nm, global_env_offset=11)
+    assert np.array_equal(to_np(a).astype(np.float64), ref)
+    g.close()
+
+
+def test_contract_errors(assets):
+    """Env::step ContractErrors map to per-env flags and leave the env untouched."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("arm2_m6")
+    g = pk.EnvBatch(mp, cp, 3, cfg=pk.EnvConfig(rsi=False))
+    a = torch.full((3, g.nm), 0.5, device=g.device)
+    out = g.step(a)  # envs start done (env.hpp:140)
+    assert (to_np(out["flags"]) == pk.FLAG_NOT_STEPPED).all()
+    g.reset()
+    s0 = g.get_state()
+    a[1, 2] = float("nan")
+    out = g.step(a)
+    f = to_np(out["flags"])
+    assert f[1] == pk.FLAG_BAD_ACTION and f[0] == 0 and f[2] == 0
+    s1 = g.get_state()
+    assert torch.equal(s0["q"][1], s1["q"][1])
+    _, bad = g.reset_to_frame(torch.tensor([0, 10**6, -1], dtype=torch.int32, device=g.device))
+    assert to_np(bad).tolist() == [0, 1, 1]
+    with pytest.raises(pk.MskError):
+        pk.EnvBatch(mp, cp, 0)
+    g.close()
+
+
+def test_divergence_flags_and_zeroed_outputs(assets):
+    """A non-finite state -> done|failed|diverged, zeroed obs/Δ, failed outcome (env.cpp:214-229)."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("arm2_m6")
+    g = pk.EnvBatch(mp, cp, 2, cfg=pk.EnvConfig(rsi=False))
+    g.reset()
+    s = g.get_state()
+    s["dq"][0, 0] = float("inf")
+    g.set_state(s)
+    out = g.step(torch.full((2, g.nm), 0.3, device=g.device))
+    f = to_np(out["flags"])
+    assert f[0] == pk.FLAG_DONE | pk.FLAG_FAILED | pk.FLAG_DIVERGED
+    assert f[1] == 0
+    assert (to_np(out["obs"][0]) == 0).all() and (to_np(out["delta"][0]) == 0).all()
+    bins, failed, counts = g.drain_outcomes(4)
+    assert to_np(counts).tolist() == [1, 0] and int(to_np(failed)[0, 0]) == 1
+    g.close()
+
+
+def test_host_buffer_step_matches_device_step(assets):
+    """msk_gpu_step_host (pipelined H2D/step/D2H) == msk_gpu_step on the same state."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("wb700_fixed")
+    n = 37
+    g = pk.EnvBatch(mp, cp, n, cfg=pk.EnvConfig(rsi=True))
+    g.reset()
+    st = g.get_state()
+    a = g.fill_excitations(3, 0)
+    dev = {k: to_np(v) for k, v in g.step(a).items()}
+    g.set_state(st)
+    ha = a.cpu().pin_memory()
+    ho = torch.empty(n, g.obs_dim).pin_memory()
+    hd = torch.empty(n, g.delta_dim).pin_memory()
+    hr = torch.empty(n).pin_memory()
+    hf = torch.empty(n, dtype=torch.uint8).pin_memory()
+    g.step_host(ha, ho, hd, hr, hf)
+    assert np.array_equal(ho.numpy(), dev["obs"])
+    assert np.array_equal(hd.numpy(), dev["delta"])
+    assert np.array_equal(hf.numpy(), dev["flags"])
+    g.close()
+
+
+def test_reward_aux_modes(assets):
+    """ImitationPower reward_aux = w_power * (-sum power / n_m) (env.cpp:244-246)."""
+    mp, cp = model_paths("arm2_m6")
+    g, o = make_pair(mp, cp, 4, cfg_kw=dict(rsi=False), reward_mode=2, w_power=0.1)
+    g.reset()
+    o.reset()
+    sync_from_oracle(g, o)
+    a = excitations(5, 0, 4, g.nm).astype(np.float32)
+    og, oo = step_both(g, o, a)
+    assert np.abs(og["reward_aux"] - oo["reward_aux"]).max() <= 1e-4 * max(1.0, np.abs(oo["reward_aux"]).max())
+    assert np.abs(og["muscle_power"] - oo["power"]).max() <= 1e-4 * max(1.0, np.abs(oo["power"]).max())
+    g.close()
