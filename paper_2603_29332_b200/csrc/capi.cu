@@ -148,7 +148,6 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         ctx->cm = compile_model(spec);
         const CompiledModel& c = ctx->cm;
         if (c.nq > 32 * kMaxQSlots) throw ConfigError("model too large: n_q > 128");
-        if (c.nl > 32 * kMaxLinkSlots) throw ConfigError("model too large: n_links > 128");
 
         int ndev = 0;
         ck(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
@@ -183,12 +182,29 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.c_c = c.c_c;
         M.c_mu = c.c_mu;
         M.inv_c_vs = c.inv_c_vs;
+        {
+            std::vector<float4> la(c.nl), sp(c.ns);
+            for (int l = 0; l < c.nl; ++l) la[l] = make_float4(c.link_ax[l], c.link_az[l], c.link_com[l], c.link_mass[l]);
+            for (int s = 0; s < c.ns; ++s) sp[s] = make_float4(c.sphere_x[s], c.sphere_z[s], c.sphere_r[s], 0.f);
+            M.link_a = ctx->upload(la);
+            M.sphere = ctx->upload(sp);
+            std::vector<float4> p0(c.nm), geo(static_cast<size_t>(c.max_seg) * c.nm);
+            std::vector<double2> p1(2 * static_cast<size_t>(c.nm));
+            for (int m = 0; m < c.nm; ++m) {
+                p0[m] = make_float4(c.pk_p0[4 * m], c.pk_p0[4 * m + 1], c.pk_p0[4 * m + 2], c.pk_p0[4 * m + 3]);
+                p1[2 * m] = make_double2(c.pk_p1[4 * m], c.pk_p1[4 * m + 1]);
+                p1[2 * m + 1] = make_double2(c.pk_p1[4 * m + 2], c.pk_p1[4 * m + 3]);
+            }
+            for (size_t i = 0; i < geo.size(); ++i)
+                geo[i] = make_float4(c.pk_geo[4 * i], c.pk_geo[4 * i + 1], c.pk_geo[4 * i + 2], c.pk_geo[4 * i + 3]);
+            M.m_p0 = ctx->upload(p0);
+            M.m_p1 = ctx->upload(p1);
+            M.seg_geo = ctx->upload(geo);
+        }
+        M.max_seg = c.max_seg;
+        M.has_general = c.has_general;
         M.link_parent = ctx->upload(c.link_parent);
         M.link_dof = ctx->upload(c.link_dof);
-        M.link_ax = ctx->upload(c.link_ax);
-        M.link_az = ctx->upload(c.link_az);
-        M.link_com = ctx->upload(c.link_com);
-        M.link_mass = ctx->upload(c.link_mass);
         M.link_inertia = ctx->upload(c.link_inertia);
         M.link_mount = ctx->upload(c.link_mount);
         M.level_start = ctx->upload(c.level_start);
@@ -196,30 +212,13 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.child_start = ctx->upload(c.child_start);
         M.child_list = ctx->upload(c.child_list);
         M.sphere_start = ctx->upload(c.sphere_start);
-        M.sphere_x = ctx->upload(c.sphere_x);
-        M.sphere_z = ctx->upload(c.sphere_z);
-        M.sphere_r = ctx->upload(c.sphere_r);
         M.joint_damping = ctx->upload(c.joint_damping);
         M.joint_lo = ctx->upload(c.joint_lo);
         M.joint_hi = ctx->upload(c.joint_hi);
         M.joint_slot_start = ctx->upload(c.joint_slot_start);
-        M.m_fmax = ctx->upload(c.m_fmax);
-        M.m_lopt = ctx->upload(c.m_lopt);
-        M.m_inv_lopt = ctx->upload(c.m_inv_lopt);
-        M.m_slack = ctx->upload(c.m_slack);
-        M.m_kv = ctx->upload(c.m_kv);
-        M.m_ndt_act = ctx->upload(c.m_ndt_act);
-        M.m_ndt_deact = ctx->upload(c.m_ndt_deact);
-        M.m_pw = ctx->upload(c.m_pw);
-        M.m_via_start = ctx->upload(c.m_via_start);
+        M.m_meta = ctx->upload(c.pk_meta);
+        M.seg_info = ctx->upload(c.pk_info);
         M.m_pair_start = ctx->upload(c.m_pair_start);
-        M.m_seg_start = ctx->upload(c.m_seg_start);
-        M.seg_info = ctx->upload(c.seg_info);
-        M.seg_slot = ctx->upload(c.seg_slot);
-        M.seg_ax = ctx->upload(c.seg_ax);
-        M.seg_az = ctx->upload(c.seg_az);
-        M.seg_cx = ctx->upload(c.seg_cx);
-        M.seg_cz = ctx->upload(c.seg_cz);
         M.via_link = ctx->upload(c.via_link);
         M.via_x = ctx->upload(c.via_x);
         M.via_z = ctx->upload(c.via_z);
@@ -245,22 +244,18 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.w_emg = static_cast<float>(rw.w_emg);
         M.w_power = static_cast<float>(rw.w_power);
         M.emg_map = ctx->upload(emg_map);
-        // per-env shared-memory layout
-        int off = 16 * c.nl;
-        M.off_theta = off;
-        off = align16(off + 4 * c.nl);
-        M.off_qang = off;
-        off = align16(off + 4 * c.nq);
+        // per-env shared-memory layout (~8 KB for the whole-body model)
+        int off = 16 * c.nl;  // kin
+        M.off_relcs = off;
+        off = align16(off + 16 * c.nq);
         M.off_dqf = off;
         off = align16(off + 4 * c.nq);
         M.off_tau = off;
         off = align16(off + 4 * c.nq);
         M.off_root = off;
         off = align16(off + 16);
-        M.off_relcs = off;
-        off = align16(off + 8 * c.nq);
         M.off_union = off;
-        off = align16(off + 4 * std::max({c.n_pairs, 16 * c.nl, 2 * c.nq}));
+        off = align16(off + 4 * std::max({c.n_pairs + 1, kLinkStride * c.nl, 2 * c.nq}));  // +1: dummy slot
         M.smem_env_bytes = off;
         const int per_block = envs_per_block() * M.smem_env_bytes;
         if (per_block > static_cast<int>(prop.sharedMemPerBlockOptin))

@@ -3,6 +3,8 @@
 
 #include <cstdint>
 
+#include <vector_types.h>
+
 namespace msk_b200 {
 
 constexpr int kSubsteps = 10;        // skeleton.hpp:13
@@ -10,7 +12,7 @@ constexpr double kSimDt = 0.002;     // skeleton.hpp:11
 constexpr double kCtrlDt = 0.02;     // skeleton.hpp:12
 constexpr float kMinFiber = 0.01f;   // skeleton.hpp:14
 constexpr int kMaxQSlots = 4;        // nq <= 128 (DOF d lives in lane d%32, slot d/32)
-constexpr int kMaxLinkSlots = 4;     // n_links <= 128 for per-lane GRF accumulators
+constexpr int kLinkStride = 15;      // floats per link in the ABA scratch (odd: bank-conflict free)
 
 enum : uint8_t {
     kFlagDone = 1,
@@ -23,16 +25,13 @@ enum : uint8_t {
 // Read-only model + clip + config tables (device pointers), passed by value.
 struct DevModel {
     int nl, nj, nq, nrd, nm, nk, ns, floating, n_levels, n_pairs;
-    int frames, n_emg, bins;
+    int frames, n_emg, bins, max_seg, has_general;
     float gravity, k_lim, c_k, c_c, c_mu, inv_c_vs;
     double k_lim_d;
     // links
     const int* link_parent;
     const int* link_dof;
-    const float* link_ax;
-    const float* link_az;
-    const float* link_com;
-    const float* link_mass;
+    const float4* link_a;  // {anchor x, anchor z (parent frame), com offset, mass}
     const float* link_inertia;
     const double* link_mount;
     const int* level_start;
@@ -40,32 +39,20 @@ struct DevModel {
     const int* child_start;
     const int* child_list;
     const int* sphere_start;
-    const float* sphere_x;
-    const float* sphere_z;
-    const float* sphere_r;
+    const float4* sphere;  // {x, z, radius, 0}
     // joints
     const float* joint_damping;
     const double* joint_lo;
     const double* joint_hi;
     const int* joint_slot_start;
-    // muscles
-    const float* m_fmax;
-    const float* m_lopt;
-    const float* m_inv_lopt;
-    const float* m_slack;
-    const float* m_kv;
-    const float* m_ndt_act;
-    const float* m_ndt_deact;
-    const float* m_pw;
-    const int* m_via_start;
+    // muscles (packed; see CompiledModel)
+    const float4* m_p0;    // {f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max / 10}
+    const double2* m_p1;   // 2 per muscle: {slack, l_opt}, {1/l_opt, 1/(dt l_opt v_max)}
+    const int* m_meta;     // nseg | general << 8
+    const float4* seg_geo; // [k * nm + m] {ax, az, cx, cz}
+    const int* seg_info;   // [k * nm + m] kind | dof << 2 | slot << 11
+    // general (non-adjacent) segments, world frame
     const int* m_pair_start;
-    const int* m_seg_start;
-    const int* seg_info;
-    const int* seg_slot;
-    const float* seg_ax;
-    const float* seg_az;
-    const float* seg_cx;
-    const float* seg_cz;
     const int* via_link;
     const float* via_x;
     const float* via_z;
@@ -86,7 +73,7 @@ struct DevModel {
     float w_emg, w_power;
     const int* emg_map;
     // per-env smem layout (bytes from the warp's base)
-    int smem_env_bytes, off_theta, off_qang, off_dqf, off_tau, off_union, off_root, off_relcs;
+    int smem_env_bytes, off_relcs, off_dqf, off_tau, off_root, off_union;
 };
 
 // Per-env mutable state (device pointers, env-major rows).

@@ -5,19 +5,19 @@
 // shared memory and nothing but the step's inputs/outputs touching HBM.
 //
 // Per substep (lane-parallel phases separated by __syncwarp):
-//   1. FK, root-relative, level by level over the tree      (skeleton.cpp:82-107)
-//   2. muscles: activation ODE, via-point path length, fibre
-//      kinematics, Hill force, and the J_m^T F contributions of
-//      every segment/joint pair into a per-env slot table   (muscle.cpp:9-56, skeleton.cpp:129-170, 298-315)
-//   3. joint torques: fixed-order sum of each joint's slots,
-//      minus damping and joint-limit penalty                (skeleton.cpp:222-231)
-//   4. velocity kinematics                                   (skeleton.cpp:43-72)
-//   5. articulated-body recursion for q̈ = M^{-1}(τ + J^T f_ext − C):
-//      per-link spatial inertia + bias + gravity + contact, a
-//      leaf-to-root pass and a root-to-leaf pass (the tree-sparse
-//      L^T D L factor/solve of M; no n_q x n_q matrix is formed)
-//                                                             (skeleton.cpp:172-262, 316-317)
-//   6. semi-implicit Euler in f64 + divergence check         (skeleton.cpp:319-328)
+//   1. muscles: activation ODE, path length in f64 (each segment in its
+//      parent link's frame), fibre kinematics, Hill force, and the J_m^T F
+//      contribution of each segment into a per-env slot table
+//                                    (muscle.cpp:9-56, skeleton.cpp:129-170, 298-315)
+//   2. joint torques: fixed-order sum of each joint's slots, minus damping
+//      and the joint-limit penalty   (skeleton.cpp:222-231)
+//   3. one root-to-leaf sweep: FK (rotation composition), velocity
+//      kinematics, and each link's spatial inertia / bias / gravity /
+//      contact wrench               (skeleton.cpp:43-107, 191-262)
+//   4. articulated-body recursion, leaf-to-root then root-to-leaf: the
+//      tree-sparse L D L^T factor/solve of M(q) q̈ = τ + J^T f − C without
+//      forming the n_q x n_q matrix  (skeleton.cpp:172-189, 316-317)
+//   5. semi-implicit Euler in f64 + divergence check (skeleton.cpp:319-328)
 // then the env epilogue: Δ, observation, reward_aux, termination, episode
 // outcome (env.cpp:129-263).  Reductions use fixed orders (no float atomics),
 // so a step is bit-reproducible.
@@ -32,64 +32,62 @@ namespace msk_b200 {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr float kTwoPiHi = 6.28318548202514648f;       // float(2*pi)
-constexpr float kTwoPiLo = -1.74845553e-7f;            // 2*pi - float(2*pi)
-constexpr float kInvTwoPi = 0.159154943091895336f;
 constexpr double kPi = 3.14159265358979323846;
+constexpr int kSegCache = 4;  // segments per muscle kept in registers between length and torque
 
 struct EnvSmem {
-    float4* kin;    // nl: cos, sin, origin x, origin z (root-relative)
-    float* theta;   // nl: link angle reduced to ~(-pi, pi]
-    float* qang;    // nq: float(mount + q) per joint dof; reduced root pitch at [2]
-    float* dqf;     // nq
-    float* tau;     // nq: joint torque, then q̈
-    float* un;      // union: pair slots | 16 floats per link (ABA)
-    float* root;    // [0] root x, [1] root z (absolute, floating base only)
-    float2* relcs;  // nq: cos, sin of each joint's own rotation (mount + q), from f64
+    float4* kin;     // nl: cos, sin, origin x, origin z (root-relative)
+    double2* relcs;  // nq: cos, sin of each joint's own rotation (mount + q), f64
+    float* dqf;      // nq
+    float* tau;      // nq: joint torque, then q̈
+    float* root;     // [0] root x, [1] root z (absolute), [2] cos q2, [3] sin q2
+    float* un;       // union: pair slots | kLinkStride floats per link (ABA) | f64 q
 };
 
 __device__ __forceinline__ EnvSmem carve(unsigned char* base, const DevModel& M) {
     EnvSmem s;
     s.kin = reinterpret_cast<float4*>(base);
-    s.theta = reinterpret_cast<float*>(base + M.off_theta);
-    s.qang = reinterpret_cast<float*>(base + M.off_qang);
+    s.relcs = reinterpret_cast<double2*>(base + M.off_relcs);
     s.dqf = reinterpret_cast<float*>(base + M.off_dqf);
     s.tau = reinterpret_cast<float*>(base + M.off_tau);
-    s.un = reinterpret_cast<float*>(base + M.off_union);
     s.root = reinterpret_cast<float*>(base + M.off_root);
-    s.relcs = reinterpret_cast<float2*>(base + M.off_relcs);
+    s.un = reinterpret_cast<float*>(base + M.off_union);
     return s;
-}
-
-__device__ __forceinline__ float reduce_angle(float a) {
-    const float k = rintf(a * kInvTwoPi);
-    return fmaf(-k, kTwoPiLo, fmaf(-k, kTwoPiHi, a));
-}
-
-__device__ __forceinline__ float reduce_angle_d(double a) {
-    return static_cast<float>(a - 2.0 * kPi * rint(a * (0.5 / kPi)));
 }
 
 // ---- Hill-type muscle (muscle.cpp:9-40) -----------------------------------
 __device__ __forceinline__ float hill_fl(float l) {
     const float d = (l - 1.0f) * (1.0f / 0.45f);
-    return expf(-d * d);
+    return __expf(-d * d);
 }
 __device__ __forceinline__ float hill_fv(float v) {
     if (v <= -1.0f) return 0.0f;
-    if (v < 0.0f) return (v + 1.0f) / (1.0f - v * 0.25f);
+    if (v < 0.0f) return __fdividef(v + 1.0f, fmaf(-0.25f, v, 1.0f));
     constexpr float c = 0.32f;  // (1.4 - 1) / (1 + 1/4)
-    return (1.4f * v + c) / (v + c);
+    return __fdividef(fmaf(1.4f, v, c), v + c);
 }
 __device__ __forceinline__ float hill_fp(float l) {
     if (l <= 1.0f) return 0.0f;
-    return (expf(4.0f * (l - 1.0f)) - 1.0f) * (1.0f / 6.38905609893065f);
+    return (__expf(4.0f * (l - 1.0f)) - 1.0f) * (1.0f / 6.38905609893065f);
 }
 __device__ __forceinline__ float mtu_force(float act, float l, float v, float fmax) {
     return fmax * (act * hill_fl(l) * hill_fv(v) + hill_fp(l));
 }
 
-// World (root-relative) position of a via point.
+// sqrt of a non-negative f64 from the f32 rsqrt seed plus one f64 Newton
+// correction (~46 bits); also returns the f32 reciprocal length.
+__device__ __forceinline__ double sqrt_d(double x, float& inv) {
+    const float r = rsqrtf(static_cast<float>(x));
+    if (!(x > 0.0)) {
+        inv = 0.0f;
+        return 0.0;
+    }
+    inv = r;
+    const double s = x * static_cast<double>(r);
+    return fma(fma(-s, s, x), 0.5 * static_cast<double>(r), s);
+}
+
+// World (root-relative) position of a via point (general segments only).
 __device__ __forceinline__ float2 via_point(const DevModel& M, const float4* kin, int v) {
     const int l = __ldg(M.via_link + v);
     const float x = __ldg(M.via_x + v), z = __ldg(M.via_z + v);
@@ -98,151 +96,47 @@ __device__ __forceinline__ float2 via_point(const DevModel& M, const float4* kin
     return make_float2(fmaf(k.x, x, fmaf(-k.y, z, k.z)), fmaf(k.y, x, fmaf(k.x, z, k.w)));
 }
 
-// Per-DOF float views (joint angle incl. mount, velocity) for the tree passes.
-__device__ __forceinline__ void publish_dofs(const DevModel& M, const EnvSmem& S, const double* qd,
-                                             const double* dqd, int lane) {
-#pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
-        if (d < M.nq) {
-            float a;
-            if (d >= M.nrd) {
-                const int l = M.floating + (d - M.nrd);
-                const double rel = __ldg(M.link_mount + l) + qd[k];
-                a = static_cast<float>(rel);
-                double sn, cs;
-                sincos(rel, &sn, &cs);
-                S.relcs[d] = make_float2(static_cast<float>(cs), static_cast<float>(sn));
-            } else if (d == 2) {
-                a = reduce_angle_d(qd[k]);
-            } else {
-                a = 0.0f;
-                S.root[d] = static_cast<float>(qd[k]);
-            }
-            S.qang[d] = a;
-            S.dqf[d] = static_cast<float>(dqd[k]);
-        }
-    }
+__device__ __forceinline__ float general_seg_len(const DevModel& M, const EnvSmem& S, int v_end) {
+    const float2 pe = via_point(M, S.kin, v_end), ps = via_point(M, S.kin, v_end - 1);
+    const float dx = pe.x - ps.x, dz = pe.y - ps.y;
+    return sqrtf(fmaf(dx, dx, dz * dz));
 }
 
-// Forward kinematics level by level (skeleton.cpp:82-107), root-relative.
-__device__ __forceinline__ void fk_pass(const DevModel& M, const EnvSmem& S, int lane) {
-    for (int lev = 0; lev < M.n_levels; ++lev) {
-        const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
-        for (int i = lane; i < n; i += 32) {
-            const int l = __ldg(M.level_links + b + i);
-            const int dof = __ldg(M.link_dof + l);
-            float th, ox, oz;
-            if (dof < 0) {  // floating root: origin at (0,0) relative, pitch q2
-                th = S.qang[2];
-                ox = 0.0f;
-                oz = 0.0f;
-            } else {
-                const int p = __ldg(M.link_parent + l);
-                const float ax = __ldg(M.link_ax + l), az = __ldg(M.link_az + l);
-                if (p >= 0) {
-                    const float4 kp = S.kin[p];
-                    ox = fmaf(kp.x, ax, fmaf(-kp.y, az, kp.z));
-                    oz = fmaf(kp.y, ax, fmaf(kp.x, az, kp.w));
-                    th = reduce_angle(S.theta[p] + S.qang[dof]);
-                } else {
-                    ox = ax;
-                    oz = az;
-                    th = reduce_angle(S.qang[dof]);
-                }
-            }
-            float sn, cs;
-            sincosf(th, &sn, &cs);
-            S.theta[l] = th;
-            S.kin[l] = make_float4(cs, sn, ox, oz);
-        }
-        __syncwarp();
-    }
+// Adjacent segment in its parent's frame: s = A + R(joint) c.  Returns |s|
+// (f64), 1/|s| and the cross product r x A (r = R c) that sets the moment arm.
+__device__ __forceinline__ double adj_segment(const EnvSmem& S, float4 g, int info, float& cross, float& inv) {
+    const double2 cs = S.relcs[(info >> 2) & 511];
+    const double rx = fma(cs.x, static_cast<double>(g.z), -cs.y * static_cast<double>(g.w));
+    const double rz = fma(cs.y, static_cast<double>(g.z), cs.x * static_cast<double>(g.w));
+    const double sx = g.x + rx, sz = g.y + rz;
+    cross = static_cast<float>(fma(rx, static_cast<double>(g.y), -rz * static_cast<double>(g.x)));
+    return sqrt_d(fma(sx, sx, sz * sz), inv);
 }
 
-// Velocity kinematics (skeleton.cpp:43-72): per link (omega, v_origin) into un[16 l + 0..2].
-__device__ __forceinline__ void vel_pass(const DevModel& M, const EnvSmem& S, int lane) {
-    for (int lev = 0; lev < M.n_levels; ++lev) {
-        const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
-        for (int i = lane; i < n; i += 32) {
-            const int l = __ldg(M.level_links + b + i);
-            const int dof = __ldg(M.link_dof + l);
-            float w, vx, vz;
-            if (dof < 0) {
-                w = S.dqf[2];
-                vx = S.dqf[0];
-                vz = S.dqf[1];
-            } else {
-                const int p = __ldg(M.link_parent + l);
-                if (p >= 0) {
-                    const float* up = S.un + 16 * p;
-                    const float wp = up[0];
-                    const float4 kl = S.kin[l], kp = S.kin[p];
-                    const float rx = kl.z - kp.z, rz = kl.w - kp.w;
-                    vx = fmaf(-wp, rz, up[1]);
-                    vz = fmaf(wp, rx, up[2]);
-                    w = wp + S.dqf[dof];
-                } else {
-                    vx = 0.0f;
-                    vz = 0.0f;
-                    w = S.dqf[dof];
-                }
-            }
-            float* u = S.un + 16 * l;
-            u[0] = w;
-            u[1] = vx;
-            u[2] = vz;
-        }
-        __syncwarp();
-    }
-}
-
-// Path length of muscle m (skeleton.cpp:129-141), segment by segment.  Adjacent
-// segments are evaluated in the parent's frame from the joint's own rotation.
-__device__ __forceinline__ float muscle_length(const DevModel& M, const EnvSmem& S, int m) {
-    const int s0 = __ldg(M.m_seg_start + m), s1 = __ldg(M.m_seg_start + m + 1);
-    float L = 0.0f;
-    for (int s = s0; s < s1; ++s) {
-        const int info = __ldg(M.seg_info + s), kind = info & 3;
-        if (kind == 0) {
-            L += __ldg(M.seg_ax + s);
-        } else if (kind == 1) {
-            const float2 cs = S.relcs[info >> 8];
-            const float cx = __ldg(M.seg_cx + s), cz = __ldg(M.seg_cz + s);
-            const float sx = fmaf(cs.x, cx, fmaf(-cs.y, cz, __ldg(M.seg_ax + s)));
-            const float sz = fmaf(cs.y, cx, fmaf(cs.x, cz, __ldg(M.seg_az + s)));
-            L += sqrtf(fmaf(sx, sx, sz * sz));
-        } else {
-            const int v = __ldg(M.seg_slot + s);
-            const float2 pe = via_point(M, S.kin, v), ps = via_point(M, S.kin, v - 1);
-            const float dx = pe.x - ps.x, dz = pe.y - ps.y;
-            L += sqrtf(fmaf(dx, dx, dz * dz));
-        }
+// Path length of muscle m (skeleton.cpp:129-141) — used by make_initial_state.
+__device__ __forceinline__ double muscle_length(const DevModel& M, const EnvSmem& S, int m) {
+    const int nseg = __ldg(M.m_meta + m) & 0xff;
+    double L = 0.0;
+    for (int k = 0; k < nseg; ++k) {
+        const int at = k * M.nm + m;
+        const int info = __ldg(M.seg_info + at);
+        const float4 g = __ldg(M.seg_geo + at);
+        const int kind = info & 3;
+        float cr, inv;
+        if (kind == 0)
+            L += g.x;
+        else if (kind == 1)
+            L += adj_segment(S, g, info, cr, inv);
+        else
+            L += general_seg_len(M, S, info >> 11);
     }
     return L;
 }
 
-// J_m^T F contributions of muscle m (force F) into the per-env slot table:
-// -F * dL_i/dq_j for every joint j between a segment's two links
-// (skeleton.cpp:147-170 with the GEMV of :315 folded in).
-__device__ __forceinline__ void muscle_torques(const DevModel& M, const EnvSmem& S, int m, float F) {
-    const int s0 = __ldg(M.m_seg_start + m), s1 = __ldg(M.m_seg_start + m + 1);
-    for (int s = s0; s < s1; ++s) {
-        const int info = __ldg(M.seg_info + s);
-        if ((info & 3) != 1) continue;
-        const float2 cs = S.relcs[info >> 8];
-        const float cx = __ldg(M.seg_cx + s), cz = __ldg(M.seg_cz + s);
-        const float ax = __ldg(M.seg_ax + s), az = __ldg(M.seg_az + s);
-        const float rx = fmaf(cs.x, cx, -cs.y * cz), rz = fmaf(cs.y, cx, cs.x * cz);
-        const float sx = ax + rx, sz = az + rz;
-        const float len = sqrtf(fmaf(sx, sx, sz * sz));
-        // moment about the child's joint: -F (r x A) / |A + r|, r = child-side
-        // offset rotated into the parent frame, A = anchor - parent-side offset
-        const float val = len > 1e-12f ? -F * fmaf(rx, az, -rz * ax) / len : 0.0f;
-        S.un[__ldg(M.seg_slot + s)] = val;
-    }
+// J_m^T F of the general (non-adjacent) segments of muscle m, world frame.
+__device__ void general_pairs(const DevModel& M, const EnvSmem& S, int m, float F) {
     const int p0 = __ldg(M.m_pair_start + m), p1 = __ldg(M.m_pair_start + m + 1);
-    for (int p = p0; p < p1; ++p) {  // general (non-adjacent) segments, world frame
+    for (int p = p0; p < p1; ++p) {
         const int ve = __ldg(M.pair_via + p), j = __ldg(M.pair_joint + p);
         const float sg = __ldg(M.pair_sign + p);
         const float2 pe = via_point(M, S.kin, ve);
@@ -262,12 +156,147 @@ __device__ __forceinline__ void muscle_torques(const DevModel& M, const EnvSmem&
     }
 }
 
+// Per-DOF views for the tree passes: each joint's own rotation (f64 sincos of
+// mount + q), root pitch rotation, root position, and f32 velocities.
+__device__ __forceinline__ void publish_dofs(const DevModel& M, const EnvSmem& S, const double* qd,
+                                             const double* dqd, int lane) {
+#pragma unroll
+    for (int k = 0; k < kMaxQSlots; ++k) {
+        const int d = lane + 32 * k;
+        if (d < M.nq) {
+            if (d >= M.nrd) {
+                const int l = M.floating + (d - M.nrd);
+                double sn, cs;
+                sincos(__ldg(M.link_mount + l) + qd[k], &sn, &cs);
+                S.relcs[d] = make_double2(cs, sn);
+            } else if (d == 2) {
+                double sn, cs;
+                sincos(qd[k], &sn, &cs);
+                S.root[2] = static_cast<float>(cs);
+                S.root[3] = static_cast<float>(sn);
+            } else {
+                S.root[d] = static_cast<float>(qd[k]);
+            }
+            S.dqf[d] = static_cast<float>(dqd[k]);
+        }
+    }
+}
+
+// Root-to-leaf sweep.  FK by rotation composition R_l = R_p R_joint
+// (skeleton.cpp:82-107, root-relative); with kFull also velocity kinematics
+// (skeleton.cpp:43-72) and each link's own articulated-body terms: spatial
+// inertia about its origin, bias force V x* I V, gravity at the COM and the
+// penalty contact wrench of its spheres (skeleton.cpp:191-262).  GRF of the
+// substep (sphere_force / 10, skeleton.cpp:323-325) accumulates into grf.
+template <bool kFull>
+__device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, int lane, float* grf) {
+    for (int lev = 0; lev < M.n_levels; ++lev) {
+        const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
+        for (int i = lane; i < n; i += 32) {
+            const int l = __ldg(M.level_links + b + i);
+            const int dof = __ldg(M.link_dof + l);
+            const float4 la = __ldg(M.link_a + l);
+            float c, s, ox, oz, w = 0.0f, vx = 0.0f, vz = 0.0f;
+            if (dof < 0) {  // floating root: origin (0,0) relative, pitch q2
+                c = S.root[2];
+                s = S.root[3];
+                ox = 0.0f;
+                oz = 0.0f;
+                if (kFull) {
+                    w = S.dqf[2];
+                    vx = S.dqf[0];
+                    vz = S.dqf[1];
+                }
+            } else {
+                const int p = __ldg(M.link_parent + l);
+                const double2 rd = S.relcs[dof];
+                const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
+                if (p >= 0) {
+                    const float4 kp = S.kin[p];
+                    ox = fmaf(kp.x, la.x, fmaf(-kp.y, la.y, kp.z));
+                    oz = fmaf(kp.y, la.x, fmaf(kp.x, la.y, kp.w));
+                    c = fmaf(kp.x, cr, -kp.y * sr);
+                    s = fmaf(kp.y, cr, kp.x * sr);
+                    if (kFull) {
+                        const float* up = S.un + kLinkStride * p;
+                        const float wp = up[9];
+                        w = wp + S.dqf[dof];
+                        vx = fmaf(-wp, oz - kp.w, up[10]);
+                        vz = fmaf(wp, ox - kp.z, up[11]);
+                    }
+                } else {
+                    ox = la.x;
+                    oz = la.y;
+                    c = cr;
+                    s = sr;
+                    if (kFull) w = S.dqf[dof];
+                }
+            }
+            S.kin[l] = make_float4(c, s, ox, oz);
+            if (!kFull) continue;
+            float* u = S.un + kLinkStride * l;
+            u[9] = w;
+            u[10] = vx;
+            u[11] = vz;
+            const float m = la.w, I = __ldg(M.link_inertia + l);
+            const float cx = la.z * c, cz = la.z * s;
+            const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
+            const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
+            const float mg = m * M.gravity;
+            float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
+            const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
+            if (s0 < s1) {
+                float gx = 0.0f, gz = 0.0f;
+                for (int sp = s0; sp < s1; ++sp) {
+                    const float4 sd = __ldg(M.sphere + sp);
+                    const float rx = fmaf(c, sd.x, -s * sd.y), rz = fmaf(s, sd.x, c * sd.y);
+                    const float pen = sd.z - (oz + rz + (M.floating ? S.root[1] : 0.0f));
+                    if (pen > 0.0f) {
+                        const float fn = fmaxf(0.0f, fmaf(M.c_k, pen, -M.c_c * fmaf(w, rx, vz)));
+                        if (fn > 0.0f) {
+                            const float qz = rz - sd.z;  // contact point relative to the origin
+                            const float ft = -M.c_mu * fn * tanhf(fmaf(-w, qz, vx) * M.inv_c_vs);
+                            p0 -= fmaf(rx, fn, -qz * ft);
+                            p1 -= ft;
+                            p2 -= fn;
+                            gx += ft * 0.1f;
+                            gz += fn * 0.1f;
+                        }
+                    }
+                }
+                if (grf) {
+                    grf[2 * l] += gx;
+                    grf[2 * l + 1] += gz;
+                }
+            }
+            float c1 = 0.0f, c2 = 0.0f;
+            if (dof >= 0) {  // c = V x S qdot at the joint: (0, qdot v_z, -qdot v_x)
+                const float qdot = S.dqf[dof];
+                c1 = qdot * vz;
+                c2 = -qdot * vx;
+            }
+            u[0] = i00;
+            u[1] = i01;
+            u[2] = i02;
+            u[3] = m;
+            u[4] = 0.0f;
+            u[5] = m;
+            u[6] = p0;
+            u[7] = p1;
+            u[8] = p2;
+            u[13] = c1;
+            u[14] = c2;
+        }
+        __syncwarp();
+    }
+}
+
 // Key-body COM (absolute) and unreduced frame angle (skeleton.cpp:346-357).
 __device__ __forceinline__ void key_body(const DevModel& M, const EnvSmem& S, const double* qsm, int k,
                                          double& x, double& z, double& ang) {
     const int l = __ldg(M.key_bodies + k);
     const float4 kl = S.kin[l];
-    const float c = __ldg(M.link_com + l);
+    const float c = __ldg(M.link_a + l).z;
     x = static_cast<double>(fmaf(kl.x, c, kl.z));
     z = static_cast<double>(fmaf(kl.y, c, kl.w));
     double a = 0.0;
@@ -334,7 +363,7 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
 }
 
 // Env::tracking_error (env.cpp:170-193) -> Δ row (f64 values rounded once).
-// Returns (via shuffle-OR) whether any key body exceeds the termination radius.
+// Returns (warp-uniform) whether any key body exceeds the termination radius.
 __device__ bool write_delta(const DevModel& M, const EnvSmem& S, const double* qsm, int t_index, float* drow,
                             int lane) {
     const int nq = M.nq, nj = M.nj, nk = M.nk, nrd = M.nrd;
@@ -365,17 +394,18 @@ __device__ bool write_delta(const DevModel& M, const EnvSmem& S, const double* q
     return __any_sync(kFull, far);
 }
 
-// make_initial_state (skeleton.cpp:264-284) for the env's muscles, given FK in smem.
+// make_initial_state (skeleton.cpp:264-284) for the env's muscles (relcs/FK in smem).
 __device__ void init_muscles(const DevModel& M, const DevState& St, const EnvSmem& S, int e, int lane) {
     const size_t mb = static_cast<size_t>(e) * M.nm;
     const float a0 = static_cast<float>(M.init_act);
     for (int m = lane; m < M.nm; m += 32) {
-        const float L = muscle_length(M, S, m);
-        const float lm = fmaxf((L - __ldg(M.m_slack + m)) * __ldg(M.m_inv_lopt + m), kMinFiber);
+        const double2 pa = __ldg(M.m_p1 + 2 * m), pb = __ldg(M.m_p1 + 2 * m + 1);
+        const double L = muscle_length(M, S, m);
+        const float lm = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
         St.act[mb + m] = a0;
         St.lm[mb + m] = lm;
         St.vm[mb + m] = 0.0f;
-        St.fm[mb + m] = mtu_force(a0, lm, 0.0f, __ldg(M.m_fmax + m));
+        St.fm[mb + m] = mtu_force(a0, lm, 0.0f, __ldg(M.m_p0 + m).x);
     }
 }
 
@@ -432,16 +462,125 @@ __device__ int rsi_frame(const DevModel& M, const DevState& St, int e) {
     return min(frame, usable - 1);
 }
 
+// One substep of every muscle of the env (lanes over muscles):
+// activation_step (muscle.cpp:42-56, tau frozen at the step start), path length
+// in f64, fibre kinematics (skeleton.cpp:302-305, prev_len from the stored,
+// clamped l_m exactly as the reference), Hill force (muscle.cpp:36-40),
+// substep power (skeleton.cpp:308-309), and for every adjacent segment the
+// moment about its child joint -F (r x A) / |A + r| into the slot table.
+// NSEG > 0: fast path for models whose segments are all adjacent/same-link
+// (segments padded to NSEG, branch-free); NSEG == 0: generic path.
+template <int NSEG>
+__device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
+                                             const float* act_row, size_t mb, float* pw, int lane) {
+    const int nm = M.nm;
+    for (int m = lane; m < nm; m += 32) {
+        const float4 p0 = __ldg(M.m_p0 + m);  // f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max/10
+        const double2 pa = __ldg(M.m_p1 + 2 * m), pb = __ldg(M.m_p1 + 2 * m + 1);
+        const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
+        const float a0 = St.act[mb + m];
+        const float lm0 = St.lm[mb + m];
+        const float gain = fmaf(1.5f, a0, 0.5f);
+        const float ex = u > a0 ? __expf(__fdividef(p0.y, gain)) : __expf(p0.z * gain);
+        const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
+        double L = 0.0;
+        if constexpr (NSEG > 0) {
+            float tq[NSEG];
+            int sl[NSEG];
+#pragma unroll
+            for (int k = 0; k < NSEG; ++k) {
+                const int at = k * nm + m;
+                const int info = __ldg(M.seg_info + at);
+                const float4 g = __ldg(M.seg_geo + at);
+                float cr, inv;
+                const double len = adj_segment(S, g, info, cr, inv);
+                const bool adj = (info & 3) == 1;
+                L += adj ? len : static_cast<double>(g.x);
+                tq[k] = adj ? cr * inv : 0.0f;
+                sl[k] = info >> 11;
+            }
+            const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
+            const float vm = static_cast<float>((L - prev_len) * pb.y);
+            const float lm1 = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
+            const float F = mtu_force(a1, lm1, vm, p0.x);
+            St.act[mb + m] = a1;
+            St.lm[mb + m] = lm1;
+            St.vm[mb + m] = vm;
+            St.fm[mb + m] = F;
+            if (pw) pw[m] += fabsf(F * vm * p0.w);
+#pragma unroll
+            for (int k = 0; k < NSEG; ++k) S.un[sl[k]] = -F * tq[k];
+        } else {
+            const int meta = __ldg(M.m_meta + m);
+            const int nseg = meta & 0xff;
+            for (int k = 0; k < nseg; ++k) {
+                const int at = k * nm + m;
+                const int info = __ldg(M.seg_info + at);
+                const float4 g = __ldg(M.seg_geo + at);
+                const int kind = info & 3;
+                float cr, inv;
+                if (kind == 1)
+                    L += adj_segment(S, g, info, cr, inv);
+                else if (kind == 0)
+                    L += g.x;
+                else
+                    L += general_seg_len(M, S, info >> 11);
+            }
+            const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
+            const float vm = static_cast<float>((L - prev_len) * pb.y);
+            const float lm1 = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
+            const float F = mtu_force(a1, lm1, vm, p0.x);
+            St.act[mb + m] = a1;
+            St.lm[mb + m] = lm1;
+            St.vm[mb + m] = vm;
+            St.fm[mb + m] = F;
+            if (pw) pw[m] += fabsf(F * vm * p0.w);
+            for (int k = 0; k < nseg; ++k) {
+                const int at = k * nm + m;
+                const int info = __ldg(M.seg_info + at);
+                if ((info & 3) != 1) continue;
+                float cr, inv;
+                adj_segment(S, __ldg(M.seg_geo + at), info, cr, inv);
+                S.un[info >> 11] = -F * cr * inv;
+            }
+            if (meta >> 8) general_pairs(M, S, m, F);
+        }
+    }
+}
+
+// Loads an env's q, dq (f64) into the DOF-owning lanes.
+__device__ __forceinline__ void load_dofs(const DevModel& M, const double* q, const double* dq, double* qd,
+                                          double* dqd, int lane) {
+#pragma unroll
+    for (int k = 0; k < kMaxQSlots; ++k) {
+        const int d = lane + 32 * k;
+        qd[k] = d < M.nq ? q[d] : 0.0;
+        dqd[k] = d < M.nq ? dq[d] : 0.0;
+    }
+}
+
+// f64 q into the union scratch for the Δ / observation epilogue.
+__device__ __forceinline__ double* stage_q(const DevModel& M, const EnvSmem& S, const double* qd, int lane) {
+    double* qsm = reinterpret_cast<double*>(S.un);
+#pragma unroll
+    for (int k = 0; k < kMaxQSlots; ++k) {
+        const int d = lane + 32 * k;
+        if (d < M.nq) qsm[d] = qd[k];
+    }
+    __syncwarp();
+    return qsm;
+}
+
 }  // namespace
 
 // ============================================================================
 // step kernel: warp per env, WPB envs per block
 // ============================================================================
-template <int WPB>
-__global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St, int env0, int n_envs,
-                                                        const float* __restrict__ actions, float* obs,
-                                                        float* delta, float* reward_aux, uint8_t* flags,
-                                                        float* power, float* grf) {
+template <int WPB, int MINB, int NSEG>
+__global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevState St, int env0, int n_envs,
+                                                              const float* __restrict__ actions, float* obs,
+                                                              float* delta, float* reward_aux, uint8_t* flags,
+                                                              float* power, float* grf) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int le = blockIdx.x * WPB + warp;  // env index local to this launch
@@ -467,53 +606,26 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
     }
 
     double qd[kMaxQSlots], dqd[kMaxQSlots];
-#pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
-        qd[k] = d < nq ? St.q[static_cast<size_t>(e) * nq + d] : 0.0;
-        dqd[k] = d < nq ? St.dq[static_cast<size_t>(e) * nq + d] : 0.0;
-    }
+    load_dofs(M, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
     publish_dofs(M, S, qd, dqd, lane);
-    float grf_acc[kMaxLinkSlots][2];
-#pragma unroll
-    for (int k = 0; k < kMaxLinkSlots; ++k) grf_acc[k][0] = grf_acc[k][1] = 0.0f;
     float* pw = power ? power + static_cast<size_t>(le) * nm
                       : (M.reward_mode == 2 ? St.power_scratch + mb : nullptr);
     if (pw)
         for (int m = lane; m < nm; m += 32) pw[m] = 0.0f;
+    float* grf_row = grf ? grf + static_cast<size_t>(le) * 2 * nl : nullptr;
+    if (grf_row)
+        for (int i = lane; i < 2 * nl; i += 32) grf_row[i] = 0.0f;
     __syncwarp();
 
-    const float dt = static_cast<float>(kSimDt);
     int diverged_at = -1;
     for (int sub = 0; sub < kSubsteps; ++sub) {
-        // ---- 1. forward kinematics ----
-        fk_pass(M, S, lane);
+        if (M.has_general) tree_sweep<false>(M, S, lane, nullptr);  // world frame for general segments
 
-        // ---- 2. muscles + J_m^T F pair contributions ----
-        for (int m = lane; m < nm; m += 32) {
-            const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
-            const float a0 = St.act[mb + m];
-            const float lm0 = St.lm[mb + m];
-            // activation_step (muscle.cpp:42-56), tau frozen at the step start
-            const float gain = fmaf(1.5f, a0, 0.5f);
-            const float ex = u > a0 ? expf(__ldg(M.m_ndt_act + m) / gain) : expf(__ldg(M.m_ndt_deact + m) * gain);
-            const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
-            const float slack = __ldg(M.m_slack + m), lopt = __ldg(M.m_lopt + m);
-            const float prev_len = fmaf(lm0, lopt, slack);
-            const float L = muscle_length(M, S, m);
-            const float vm = (L - prev_len) * __ldg(M.m_kv + m);
-            const float lm1 = fmaxf((L - slack) * __ldg(M.m_inv_lopt + m), kMinFiber);
-            const float F = mtu_force(a1, lm1, vm, __ldg(M.m_fmax + m));
-            St.act[mb + m] = a1;
-            St.lm[mb + m] = lm1;
-            St.vm[mb + m] = vm;
-            St.fm[mb + m] = F;
-            if (pw) pw[m] += fabsf(F * vm * __ldg(M.m_pw + m));
-            muscle_torques(M, S, m, F);
-        }
+        // ---- 1. muscles + J_m^T F contributions ----
+        muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane);
         __syncwarp();
 
-        // ---- 3. joint torques: fixed-order slot sums, damping, limits ----
+        // ---- 2. joint torques: fixed-order slot sums, damping, limits ----
 #pragma unroll
         for (int k = 0; k < kMaxQSlots; ++k) {
             const int d = lane + 32 * k;
@@ -533,86 +645,20 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
         }
         __syncwarp();
 
-        // ---- 4. velocities ----
-        vel_pass(M, S, lane);
+        // ---- 3. FK + velocities + per-link articulated-body terms ----
+        tree_sweep<true>(M, S, lane, grf_row);
 
-        // ---- 5a. per-link spatial inertia, bias force, gravity, contact ----
-#pragma unroll
-        for (int k = 0; k < kMaxLinkSlots; ++k) {
-            const int l = lane + 32 * k;
-            if (l < nl) {
-                float* u = S.un + 16 * l;
-                const float w = u[0], vx = u[1], vz = u[2];
-                const float4 kl = S.kin[l];
-                const float m = __ldg(M.link_mass + l), I = __ldg(M.link_inertia + l);
-                const float cc = __ldg(M.link_com + l);
-                const float cx = cc * kl.x, cz = cc * kl.y;
-                const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
-                // h = I V ; p = V x* h
-                const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
-                float p0 = fmaf(vx, h2, -vz * h1), p1 = -w * h2, p2 = w * h1;
-                // gravity at the COM: f = (c x F, 0, m g)
-                const float mg = m * M.gravity;
-                p0 -= cx * mg;
-                p2 -= mg;
-                // contact spheres on this link (skeleton.cpp:235-262)
-                const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
-                for (int s = s0; s < s1; ++s) {
-                    const float ox = __ldg(M.sphere_x + s), oz = __ldg(M.sphere_z + s), r = __ldg(M.sphere_r + s);
-                    const float rx = fmaf(kl.x, ox, -kl.y * oz), rz = fmaf(kl.y, ox, kl.x * oz);
-                    const float cz_abs = kl.w + rz + (M.floating ? S.root[1] : 0.0f);
-                    const float pen = r - cz_abs;
-                    float fx = 0.0f, fz = 0.0f;
-                    if (pen > 0.0f) {
-                        const float vcz = fmaf(w, rx, vz);
-                        const float fn = fmaxf(0.0f, fmaf(M.c_k, pen, -M.c_c * vcz));
-                        if (fn > 0.0f) {
-                            const float qz = rz - r;  // contact point relative to the link origin
-                            const float vcx = fmaf(-w, qz, vx);
-                            const float ft = -M.c_mu * fn * tanhf(vcx * M.inv_c_vs);
-                            fx = ft;
-                            fz = fn;
-                            p0 -= fmaf(rx, fn, -qz * ft);
-                            p1 -= ft;
-                            p2 -= fn;
-                        }
-                    }
-                    grf_acc[k][0] += fx * 0.1f;
-                    grf_acc[k][1] += fz * 0.1f;
-                }
-                const int dof = __ldg(M.link_dof + l);
-                float c1 = 0.0f, c2 = 0.0f;
-                if (dof >= 0) {
-                    const float qdot = S.dqf[dof];
-                    c1 = qdot * vz;
-                    c2 = -qdot * vx;
-                }
-                u[0] = i00;
-                u[1] = i01;
-                u[2] = i02;
-                u[3] = m;
-                u[4] = 0.0f;
-                u[5] = m;
-                u[6] = p0;
-                u[7] = p1;
-                u[8] = p2;
-                u[14] = c1;
-                u[15] = c2;
-            }
-        }
-        __syncwarp();
-
-        // ---- 5b. articulated-body pass, leaves -> root ----
+        // ---- 4a. articulated-body pass, leaves -> root ----
         for (int lev = M.n_levels - 1; lev >= 0; --lev) {
             const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
             for (int i = lane; i < n; i += 32) {
                 const int l = __ldg(M.level_links + b + i);
-                float* u = S.un + 16 * l;
+                float* u = S.un + kLinkStride * l;
                 float I00 = u[0], I01 = u[1], I02 = u[2], I11 = u[3], I12 = u[4], I22 = u[5];
                 float P0 = u[6], P1 = u[7], P2 = u[8];
                 const int c0 = __ldg(M.child_start + l), c1 = __ldg(M.child_start + l + 1);
                 for (int c = c0; c < c1; ++c) {
-                    const float* uc = S.un + 16 * __ldg(M.child_list + c);
+                    const float* uc = S.un + kLinkStride * __ldg(M.child_list + c);
                     I00 += uc[0];
                     I01 += uc[1];
                     I02 += uc[2];
@@ -629,22 +675,21 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
                     u[6] = P0; u[7] = P1; u[8] = P2;
                     continue;
                 }
+                // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
                 const float invD = 1.0f / I00;
-                const float uu = S.tau[dof] - P0;
-                // Ia = IA - U U^T / D (first row/column vanish)
-                const float a = I11 - I01 * I01 * invD;
-                const float bb = I12 - I01 * I02 * invD;
-                const float cq = I22 - I02 * I02 * invD;
-                const float c1v = u[14], c2v = u[15];
-                const float k = uu * invD;
-                const float q0 = S.tau[dof];                       // P0 + U0 * u / D
-                const float q1 = fmaf(I01, k, fmaf(a, c1v, fmaf(bb, c2v, P1)));
-                const float q2 = fmaf(I02, k, fmaf(bb, c1v, fmaf(cq, c2v, P2)));
-                u[9] = I00;
-                u[10] = I01;
-                u[11] = I02;
-                u[12] = invD;
-                u[13] = uu;
+                const float t = S.tau[dof];
+                const float uu = (t - P0) * invD;               // u / D
+                const float U1 = I01 * invD, U2 = I02 * invD;   // U / D
+                const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
+                const float bb = fmaf(-I01, U2, I12);
+                const float cq = fmaf(-I02, U2, I22);
+                const float cv1 = u[13], cv2 = u[14];
+                // pa = pA + Ia c + U u / D   (pa[0] = tau)
+                const float q1 = fmaf(I01, uu, fmaf(a, cv1, fmaf(bb, cv2, P1)));
+                const float q2 = fmaf(I02, uu, fmaf(bb, cv1, fmaf(cq, cv2, P2)));
+                u[9] = uu;
+                u[11] = U1;
+                u[12] = U2;
                 const int p = __ldg(M.link_parent + l);
                 if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
                     const float4 kl = S.kin[l], kp = S.kin[p];
@@ -656,7 +701,7 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
                     u[3] = a;
                     u[4] = bb;
                     u[5] = cq;
-                    u[6] = fmaf(-dz, q1, fmaf(dx, q2, q0));
+                    u[6] = fmaf(-dz, q1, fmaf(dx, q2, t));
                     u[7] = q1;
                     u[8] = q2;
                 }
@@ -664,10 +709,9 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
             __syncwarp();
         }
 
-        // ---- 5c. root solve + articulated-body pass, root -> leaves ----
+        // ---- 4b. root solve + articulated-body pass, root -> leaves ----
         if (M.floating && lane == 0) {
-            float* u = S.un;  // link 0
-            // solve IA A = -pA (3x3 SPD, Cholesky)
+            float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky)
             const float l00 = sqrtf(u[0]);
             const float l10 = u[1] / l00, l20 = u[2] / l00;
             const float l11 = sqrtf(u[3] - l10 * l10);
@@ -682,9 +726,10 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
             u[0] = x0;
             u[1] = x1;
             u[2] = x2;
+            // spatial -> coordinate acceleration of the root (x, z, pitch)
             const float wd = S.dqf[2];
-            S.tau[0] = x1 - wd * S.dqf[1];
-            S.tau[1] = x2 + wd * S.dqf[0];
+            S.tau[0] = fmaf(-wd, S.dqf[1], x1);
+            S.tau[1] = fmaf(wd, S.dqf[0], x2);
             S.tau[2] = x0;
         }
         __syncwarp();
@@ -694,18 +739,19 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
                 const int l = __ldg(M.level_links + b + i);
                 const int dof = __ldg(M.link_dof + l);
                 if (dof < 0) continue;
-                float* u = S.un + 16 * l;
+                float* u = S.un + kLinkStride * l;
                 const int p = __ldg(M.link_parent + l);
-                float A0 = 0.0f, A1 = u[14], A2 = u[15];
+                float A0 = 0.0f, A1 = u[13], A2 = u[14];
                 if (p >= 0) {
-                    const float* up = S.un + 16 * p;
+                    const float* up = S.un + kLinkStride * p;
                     const float4 kl = S.kin[l], kp = S.kin[p];
                     const float dx = kl.z - kp.z, dz = kl.w - kp.w;
                     A0 = up[0];
                     A1 += fmaf(-up[0], dz, up[1]);
                     A2 += fmaf(up[0], dx, up[2]);
                 }
-                const float qdd = (u[13] - fmaf(u[9], A0, fmaf(u[10], A1, u[11] * A2))) * u[12];
+                // q̈ = (u - U^T A) / D with U0 = D
+                const float qdd = u[9] - A0 - fmaf(u[11], A1, u[12] * A2);
                 u[0] = A0 + qdd;
                 u[1] = A1;
                 u[2] = A2;
@@ -714,7 +760,7 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
             __syncwarp();
         }
 
-        // ---- 6. semi-implicit Euler (f64) + divergence check ----
+        // ---- 5. semi-implicit Euler (f64) + divergence check ----
         bool bad = false;
 #pragma unroll
         for (int k = 0; k < kMaxQSlots; ++k) {
@@ -733,7 +779,6 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
             break;
         }
     }
-    (void)dt;
 
     // ---- write back the simulation state ----
 #pragma unroll
@@ -762,8 +807,8 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
             for (int i = lane; i < ddim; i += 32) drow[i] = 0.0f;
         if (power)
             for (int m = lane; m < nm; m += 32) power[static_cast<size_t>(le) * nm + m] = 0.0f;
-        if (grf)
-            for (int i = lane; i < 2 * nl; i += 32) grf[static_cast<size_t>(le) * 2 * nl + i] = 0.0f;
+        if (grf_row)
+            for (int i = lane; i < 2 * nl; i += 32) grf_row[i] = 0.0f;
         if (lane == 0) {
             if (reward_aux) reward_aux[le] = 0.0f;
             if (flags) flags[le] = kFlagDone | kFlagFailed | kFlagDiverged;
@@ -778,28 +823,11 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
         return;
     }
 
-    if (grf) {
-#pragma unroll
-        for (int k = 0; k < kMaxLinkSlots; ++k) {
-            const int l = lane + 32 * k;
-            if (l < nl) {
-                grf[(static_cast<size_t>(le) * nl + l) * 2 + 0] = grf_acc[k][0];
-                grf[(static_cast<size_t>(le) * nl + l) * 2 + 1] = grf_acc[k][1];
-            }
-        }
-    }
-
     // ---- env epilogue (env.cpp:231-262) ----
     const int t_index = St.t_index[e] + 1;
     const int steps = St.steps[e] + 1;
-    fk_pass(M, S, lane);
-    double* qsm = reinterpret_cast<double*>(S.un);  // f64 q for Δ / obs
-#pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
-        if (d < nq) qsm[d] = qd[k];
-    }
-    __syncwarp();
+    tree_sweep<false>(M, S, lane, nullptr);
+    const double* qsm = stage_q(M, S, qd, lane);
     const bool far = write_delta(M, S, qsm, t_index, drow, lane);
     if (obs_row) write_obs(M, St, S, qsm, e, t_index, obs_row, lane);
 
@@ -845,11 +873,11 @@ __global__ void __launch_bounds__(WPB * 32) step_kernel(DevModel M, DevState St,
 // ============================================================================
 enum ResetMode : int { kResetSample = 0, kResetFrame = 1, kResetForce = 2, kResetInit = 3 };
 
-template <int WPB>
-__global__ void __launch_bounds__(WPB * 32) reset_kernel(DevModel M, DevState St, int n_envs, int mode,
-                                                         const uint8_t* mask, uint8_t mask_bits,
-                                                         const int* frames_in, float* obs, int* frames_out,
-                                                         uint8_t* bad) {
+template <int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevState St, int n_envs, int mode,
+                                                               const uint8_t* mask, uint8_t mask_bits,
+                                                               const int* frames_in, float* obs, int* frames_out,
+                                                               uint8_t* bad) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * WPB + warp;
@@ -871,14 +899,12 @@ __global__ void __launch_bounds__(WPB * 32) reset_kernel(DevModel M, DevState St
     } else if (mode == kResetForce) {
         frame = St.t_index[e];
     }  // kResetInit: frame 0 (Env::Env, env.cpp:86)
-    const double* cq = M.clip_q + static_cast<size_t>(frame) * nq;
-    const double* cdq = M.clip_dq + static_cast<size_t>(frame) * nq;
     double qd[kMaxQSlots], dqd[kMaxQSlots];
+    load_dofs(M, M.clip_q + static_cast<size_t>(frame) * nq, M.clip_dq + static_cast<size_t>(frame) * nq, qd, dqd,
+              lane);
 #pragma unroll
     for (int k = 0; k < kMaxQSlots; ++k) {
         const int d = lane + 32 * k;
-        qd[k] = d < nq ? cq[d] : 0.0;
-        dqd[k] = d < nq ? cdq[d] : 0.0;
         if (d < nq) {
             St.q[static_cast<size_t>(e) * nq + d] = qd[k];
             St.dq[static_cast<size_t>(e) * nq + d] = dqd[k];
@@ -886,7 +912,7 @@ __global__ void __launch_bounds__(WPB * 32) reset_kernel(DevModel M, DevState St
     }
     publish_dofs(M, S, qd, dqd, lane);
     __syncwarp();
-    fk_pass(M, S, lane);
+    tree_sweep<false>(M, S, lane, nullptr);
     init_muscles(M, St, S, e, lane);
     if (lane == 0) {
         St.t[e] = frame * kCtrlDt;
@@ -904,21 +930,15 @@ __global__ void __launch_bounds__(WPB * 32) reset_kernel(DevModel M, DevState St
         if (frames_out) frames_out[e] = frame;
     }
     if (obs) {
-        double* qsm = reinterpret_cast<double*>(S.un);
-#pragma unroll
-        for (int k = 0; k < kMaxQSlots; ++k) {
-            const int d = lane + 32 * k;
-            if (d < nq) qsm[d] = qd[k];
-        }
-        __syncwarp();
+        const double* qsm = stage_q(M, S, qd, lane);
         const int obs_dim = 3 * nq + 6 * M.nk + 4 * M.nm;
         write_obs(M, St, S, qsm, e, frame, obs + static_cast<size_t>(e) * obs_dim, lane);
     }
 }
 
-template <int WPB>
-__global__ void __launch_bounds__(WPB * 32) observe_kernel(DevModel M, DevState St, int n_envs, float* obs,
-                                                           float* delta) {
+template <int WPB, int MINB>
+__global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, DevState St, int n_envs, float* obs,
+                                                                 float* delta) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * WPB + warp;
@@ -926,22 +946,11 @@ __global__ void __launch_bounds__(WPB * 32) observe_kernel(DevModel M, DevState 
     const EnvSmem S = carve(smem + warp * M.smem_env_bytes, M);
     const int nq = M.nq;
     double qd[kMaxQSlots], dqd[kMaxQSlots];
-#pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
-        qd[k] = d < nq ? St.q[static_cast<size_t>(e) * nq + d] : 0.0;
-        dqd[k] = d < nq ? St.dq[static_cast<size_t>(e) * nq + d] : 0.0;
-    }
+    load_dofs(M, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
     publish_dofs(M, S, qd, dqd, lane);
     __syncwarp();
-    fk_pass(M, S, lane);
-    double* qsm = reinterpret_cast<double*>(S.un);
-#pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
-        if (d < nq) qsm[d] = qd[k];
-    }
-    __syncwarp();
+    tree_sweep<false>(M, S, lane, nullptr);
+    const double* qsm = stage_q(M, S, qd, lane);
     const int t_index = St.t_index[e];
     if (delta) write_delta(M, S, qsm, t_index, delta + static_cast<size_t>(e) * (3 + M.nj + 2 * M.nk), lane);
     if (obs) write_obs(M, St, S, qsm, e, t_index, obs + static_cast<size_t>(e) * (3 * nq + 6 * M.nk + 4 * M.nm), lane);
@@ -1116,17 +1125,28 @@ double measure_fp32_peak_tflops() {
 // ============================================================================
 // host-side launch wrappers
 // ============================================================================
-constexpr int kWPB = 4;
+constexpr int kWPB = 7;   // envs (warps) per block
+constexpr int kMinB = 4;  // blocks per SM: 28 envs resident -> 4096 envs in one wave, <= 72 regs
+
+// Fast-path segment count for a model (0 = generic path).
+int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 && M.max_seg <= 4) ? M.max_seg : 0; }
+
+template <int NSEG>
+cudaError_t set_step_smem(int bytes) {
+    return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
 
 cudaError_t prepare_kernels(int smem_bytes_per_block) {
     cudaError_t err;
-    if ((err = cudaFuncSetAttribute(step_kernel<kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((err = set_step_smem<0>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<1>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<2>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<3>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = cudaFuncSetAttribute(reset_kernel<kWPB, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes_per_block)) != cudaSuccess)
         return err;
-    if ((err = cudaFuncSetAttribute(reset_kernel<kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem_bytes_per_block)) != cudaSuccess)
-        return err;
-    return cudaFuncSetAttribute(observe_kernel<kWPB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(observe_kernel<kWPB, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_bytes_per_block);
 }
 
@@ -1135,20 +1155,30 @@ int envs_per_block() { return kWPB; }
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
                  float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s) {
     const int blocks = (n + kWPB - 1) / kWPB;
-    step_kernel<kWPB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, env0, n, actions, obs, delta,
-                                                                         raux, flags, power, grf);
+    const size_t smem = static_cast<size_t>(kWPB) * M.smem_env_bytes;
+#define MSK_STEP(NS)                                                                                          \
+    step_kernel<kWPB, kMinB, NS><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux, flags, \
+                                                                 power, grf)
+    switch (step_variant(M)) {
+        case 1: MSK_STEP(1); break;
+        case 2: MSK_STEP(2); break;
+        case 3: MSK_STEP(3); break;
+        case 4: MSK_STEP(4); break;
+        default: MSK_STEP(0); break;
+    }
+#undef MSK_STEP
 }
 
 void launch_reset(const DevModel& M, const DevState& St, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t s) {
     const int blocks = (n + kWPB - 1) / kWPB;
-    reset_kernel<kWPB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, n, mode, mask, bits, frames_in,
+    reset_kernel<kWPB, kMinB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, n, mode, mask, bits, frames_in,
                                                                           obs, frames_out, bad);
 }
 
 void launch_observe(const DevModel& M, const DevState& St, int n, float* obs, float* delta, cudaStream_t s) {
     const int blocks = (n + kWPB - 1) / kWPB;
-    observe_kernel<kWPB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, n, obs, delta);
+    observe_kernel<kWPB, kMinB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, n, obs, delta);
 }
 
 void launch_seed(const DevState& St, int n, uint64_t base_seed, cudaStream_t s) {

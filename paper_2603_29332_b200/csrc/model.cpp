@@ -394,10 +394,10 @@ CompiledModel compile_model(const ModelSpec& s) {
     for (int mi = 0; mi < c.nm; ++mi) {
         const auto& m = s.muscles[mi];
         c.m_fmax.push_back(static_cast<float>(m.f_max));
-        c.m_lopt.push_back(static_cast<float>(m.l_opt));
-        c.m_inv_lopt.push_back(static_cast<float>(1.0 / m.l_opt));
-        c.m_slack.push_back(static_cast<float>(m.slack));
-        c.m_kv.push_back(static_cast<float>(1.0 / (dt * m.l_opt * m.v_max)));
+        c.m_lopt.push_back(m.l_opt);
+        c.m_inv_lopt.push_back(1.0 / m.l_opt);
+        c.m_slack.push_back(m.slack);
+        c.m_kv.push_back(1.0 / (dt * m.l_opt * m.v_max));
         c.m_ndt_act.push_back(static_cast<float>(-dt / m.tau_act));
         c.m_ndt_deact.push_back(static_cast<float>(-dt / m.tau_deact));
         c.m_pw.push_back(static_cast<float>(m.l_opt * m.v_max / 10.0));
@@ -490,6 +490,44 @@ CompiledModel compile_model(const ModelSpec& s) {
         c.pair_slot.push_back(slot_of[i]);
     }
     c.key_bodies = s.key_bodies;
+
+    // packed device layout
+    for (int mi = 0; mi < c.nm; ++mi)
+        c.max_seg = std::max(c.max_seg, c.m_seg_start[mi + 1] - c.m_seg_start[mi]);
+    c.pk_p0.assign(4 * static_cast<size_t>(c.nm), 0.f);
+    c.pk_p1.assign(4 * static_cast<size_t>(c.nm), 0.0);
+    c.pk_meta.assign(c.nm, 0);
+    c.pk_geo.assign(4 * static_cast<size_t>(c.max_seg) * c.nm, 0.f);
+    // padding segments: kind 0 (zero length) writing 0 into the dummy slot n_pairs
+    c.pk_info.assign(static_cast<size_t>(c.max_seg) * c.nm, c.n_pairs << 11);
+    for (int mi = 0; mi < c.nm; ++mi) {
+        c.pk_p0[4 * mi + 0] = c.m_fmax[mi];
+        c.pk_p0[4 * mi + 1] = c.m_ndt_act[mi];
+        c.pk_p0[4 * mi + 2] = c.m_ndt_deact[mi];
+        c.pk_p0[4 * mi + 3] = c.m_pw[mi];
+        c.pk_p1[4 * mi + 0] = c.m_slack[mi];
+        c.pk_p1[4 * mi + 1] = c.m_lopt[mi];
+        c.pk_p1[4 * mi + 2] = c.m_inv_lopt[mi];
+        c.pk_p1[4 * mi + 3] = c.m_kv[mi];
+        const int s0 = c.m_seg_start[mi], ns = c.m_seg_start[mi + 1] - s0;
+        int general = 0;
+        for (int k = 0; k < ns; ++k) {
+            const int sg = s0 + k;
+            const size_t at = static_cast<size_t>(k) * c.nm + mi;
+            const int kind = c.seg_info[sg] & 3, dof = c.seg_info[sg] >> 8;
+            int slot = c.seg_slot[sg];
+            if (kind == 2) general = 1;
+            if (kind == 0) slot = c.n_pairs;  // dummy slot: the fast path stores 0 there
+            if (slot >= (1 << 21) || dof >= (1 << 9)) throw ConfigError("model too large for the packed layout");
+            c.pk_info[at] = kind | (dof << 2) | (slot << 11);
+            c.pk_geo[4 * at + 0] = c.seg_ax[sg];
+            c.pk_geo[4 * at + 1] = c.seg_az[sg];
+            c.pk_geo[4 * at + 2] = c.seg_cx[sg];
+            c.pk_geo[4 * at + 3] = c.seg_cz[sg];
+        }
+        c.pk_meta[mi] = ns | (general << 8);
+        c.has_general |= general;
+    }
     return c;
 }
 

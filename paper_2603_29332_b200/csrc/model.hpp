@@ -87,7 +87,10 @@ struct CompiledModel {
     std::vector<double> joint_lo, joint_hi;
     std::vector<int32_t> joint_slot_start;           // nj+1: pair slots grouped by joint
     // muscles
-    std::vector<float> m_fmax, m_lopt, m_inv_lopt, m_slack, m_kv, m_ndt_act, m_ndt_deact, m_pw;
+    std::vector<float> m_fmax, m_ndt_act, m_ndt_deact, m_pw;
+    // fibre-length chain kept in f64: v_m = (L - prev_len)/(dt l_opt v_max)
+    // amplifies length error by ~1/(dt l_opt v_max) (SURVEY.md §7 hard part 1)
+    std::vector<double> m_lopt, m_inv_lopt, m_slack, m_kv;
     std::vector<int32_t> m_via_start, m_pair_start, m_seg_start;
     std::vector<int32_t> via_link;
     std::vector<float> via_x, via_z;
@@ -106,6 +109,17 @@ struct CompiledModel {
     std::vector<int32_t> pair_joint, pair_via, pair_slot;  // pair_via: global via index of segment END
     std::vector<float> pair_sign;                          // +1: endpoint = seg start, -1: seg end
     std::vector<int32_t> key_bodies;
+
+    // ---- packed device layout (what the step kernel reads) ----
+    // per muscle: p0 = {f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max / 10} (f32x4),
+    // p1 = {slack, l_opt, 1/l_opt, 1/(dt l_opt v_max)} (f64x4), meta = nseg | general << 8.
+    // Segment k of muscle m lives at [k * nm + m] so a warp's 32 muscles read
+    // 32 consecutive records (coalesced): geo = {ax, az, cx, cz},
+    // info = kind | dof << 2 | slot << 11 (kind 2: slot = global via index of the end).
+    int max_seg = 0, has_general = 0;
+    std::vector<float> pk_p0, pk_geo;
+    std::vector<double> pk_p1;
+    std::vector<int32_t> pk_meta, pk_info;
 };
 
 CompiledModel compile_model(const ModelSpec& spec);

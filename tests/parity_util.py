@@ -67,5 +67,20 @@ def step_both(g, o, actions32):
 
 
 def force_err(fm_g, fm_o, fmax):
-    """|ΔF| / f_max (force agreement relative to the muscle's max isometric force)."""
-    return float(np.max(np.abs(fm_g - fm_o) / fmax[None, :]))
+    """|ΔF| / max(|F|, f_max): relative force error, floored at the muscle's max
+    isometric force (so near-zero forces are judged against f_max)."""
+    scale = np.maximum(np.abs(fm_o), fmax[None, :])
+    return float(np.max(np.abs(fm_g - fm_o) / scale))
+
+
+def obs_block_errors(g, obs_g, obs_o):
+    """Per-block max relative error (floor 1) of an observation row (env.cpp:129-163)."""
+    nq, nk, nm = g.nq, g.nk, g.nm
+    names = [("q", nq), ("dq", nq), ("key_pos", 2 * nk), ("key_angle", nk), ("act", nm), ("f_m", nm),
+             ("l_m", nm), ("v_m", nm), ("q_ref", nq), ("key_pos_ref", 2 * nk), ("key_angle_ref", nk)]
+    out, o = {}, 0
+    for name, n in names:
+        a, b = obs_g[:, o:o + n], obs_o[:, o:o + n]
+        out[name] = float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b)))) if n else 0.0
+        o += n
+    return out

@@ -4,7 +4,7 @@ Tolerances (north_star: "rel <= 1e-4 on forces, <= 1e-5 on q/qdot"), for ONE
 control step (10 substeps) from identical state and excitations:
   q, q̇        max|Δ| <= 1e-5 * max(1, max|ref|)      (per env, norm-wise)
   activation  max|Δ| <= 1e-6
-  muscle force |ΔF| <= 1e-4 * f_max                  (per muscle)
+  muscle force |ΔF| <= 1e-4 * max(|F|, f_max)        (per muscle)
   Δ (tracking error) max|Δ| <= 1e-5 m / rad
   observation max|Δ| <= 1e-4 * max(1, |ref|)         (element-wise)
   flags, t_index, steps, start frames, RNG draws, sampler: bit-exact.
@@ -17,7 +17,8 @@ import pytest
 
 from conftest import model_paths
 from golden_cases import CASES
-from parity_util import f32_state, force_err, gpu_state, make_pair, step_both, sync_from_oracle, to_np
+from parity_util import (f32_state, force_err, gpu_state, make_pair, obs_block_errors, step_both, sync_from_oracle,
+                         to_np)
 from oracle.oracle import excitations
 
 pytestmark = pytest.mark.gpu
@@ -72,8 +73,10 @@ def test_single_step_parity(assets, name):
         assert np.abs(sg["act"] - so["act"]).max() <= 1e-6
         assert force_err(sg["f_m"], so["f_m"], fmax) <= 1e-4, force_err(sg["f_m"], so["f_m"], fmax)
         assert np.abs(og["delta"] - oo["delta"]).max() <= 1e-5
-        obs_err = np.abs(og["obs"] - oo["obs"]) / np.maximum(1.0, np.abs(oo["obs"]))
-        assert obs_err.max() <= 1e-4, obs_err.max()
+        blocks = obs_block_errors(g, og["obs"], oo["obs"])
+        # f_m is judged by the force tolerance above (it can exceed f_max many-fold
+        # in over-stretched muscles); every other block element-wise at 1e-4
+        assert max(v for k, v in blocks.items() if k != "f_m") <= 1e-4, blocks
         assert np.array_equal(og["flags"], oo["flags"])
         assert np.array_equal(sg["ints"], so["ints"])
         assert np.allclose(sg["t"], so["t"], rtol=0, atol=1e-12)
