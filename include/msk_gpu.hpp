@@ -1,0 +1,134 @@
+// msk_gpu.hpp — C++ host API over the C ABI (include/msk_gpu.h).
+//
+// msk::gpu::EnvBatch mirrors the verbs of the reference's msk::Env
+// (/root/reference/proj/include/msk/env.hpp:86-145) for E environments on one
+// GPU: reset / reset_to_frame / step / observe / tracking_error /
+// force_state_to_reference / set_eval_mode / sampler / drain_episode_outcomes.
+// Buffers are device pointers, calls are asynchronous on the given stream, and
+// C-ABI status codes are turned back into exceptions with the reference's
+// categories (ContractError-like for status 1, runtime_error for CUDA).
+// Header-only; link against libmsk_b200.so.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "msk_gpu.h"
+
+namespace msk::gpu {
+
+struct ContractError : std::logic_error {
+    using std::logic_error::logic_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+// msk::EnvConfig defaults (env.hpp:39-47).
+struct EnvConfig {
+    int episode_horizon = 250;
+    bool rsi = true;
+    int adaptive_bins = 10;
+    double adaptive_mix = 0.2;
+    double adaptive_decay = 0.99;
+    double termination_body_err = 0.5;
+    double init_activation = 0.01;
+};
+
+enum class RewardMode { ImitationOnly = 0, ImitationEmg = 1, ImitationPower = 2 };
+
+// msk::RewardConfig defaults (env.hpp:32-37).
+struct RewardConfig {
+    RewardMode mode = RewardMode::ImitationOnly;
+    double w_emg = 100.0;
+    double w_power = 0.05;
+    std::vector<int> emg_channel_map;
+};
+
+// Device output buffers of one step (StepResult fields, env.hpp:70-80); any may be null.
+struct StepBuffers {
+    float* observation = nullptr;    // [E x observation_dim]
+    float* delta = nullptr;          // [E x delta_dim]
+    float* reward_aux = nullptr;     // [E]
+    uint8_t* flags = nullptr;        // [E] MSK_FLAG_*
+    float* muscle_power = nullptr;   // [E x action_dim]
+    float* contact_force = nullptr;  // [E x n_links x 2]
+};
+
+inline void check(int status, const msk_gpu_ctx* ctx) {
+    if (status == MSK_OK) return;
+    const std::string msg = msk_gpu_last_error(ctx);
+    if (status == MSK_ERR_CONTRACT) throw ContractError(msg);
+    throw CudaError(msg);
+}
+
+class EnvBatch {
+public:
+    EnvBatch(const std::string& model_json, const std::string& clip_csv, int n_envs, const EnvConfig& cfg = {},
+             const RewardConfig& rw = {}, uint64_t base_seed = 0x5EED, int64_t global_env_offset = 0,
+             int device = 0) {
+        msk_env_config ec{cfg.episode_horizon, cfg.rsi ? 1 : 0, cfg.adaptive_bins, 0,
+                          cfg.adaptive_mix, cfg.adaptive_decay, cfg.termination_body_err, cfg.init_activation};
+        std::vector<int32_t> map(rw.emg_channel_map.begin(), rw.emg_channel_map.end());
+        msk_reward_config rc{static_cast<int32_t>(rw.mode), static_cast<int32_t>(map.size()), rw.w_emg, rw.w_power,
+                             map.empty() ? nullptr : map.data()};
+        check(msk_gpu_create(model_json.c_str(), clip_csv.c_str(), &ec, &rc, n_envs, base_seed, global_env_offset,
+                             device, &ctx_),
+              nullptr);
+        check(msk_gpu_dims(ctx_, &dims_), ctx_);
+    }
+    ~EnvBatch() { msk_gpu_destroy(ctx_); }
+    EnvBatch(const EnvBatch&) = delete;
+    EnvBatch& operator=(const EnvBatch&) = delete;
+
+    // Env::reset for envs whose mask byte has any of mask_bits (mask null = all).
+    void reset(const uint8_t* mask = nullptr, uint8_t mask_bits = 0xff, float* observation = nullptr,
+               int32_t* start_frames = nullptr, void* stream = nullptr) {
+        check(msk_gpu_reset(ctx_, mask, mask_bits, observation, start_frames, stream), ctx_);
+    }
+    void reset_to_frame(const int32_t* frames, const uint8_t* mask = nullptr, float* observation = nullptr,
+                        uint8_t* bad = nullptr, void* stream = nullptr) {
+        check(msk_gpu_reset_to_frame(ctx_, frames, mask, observation, bad, stream), ctx_);
+    }
+    void step(const float* actions, const StepBuffers& out, void* stream = nullptr) {
+        check(msk_gpu_step(ctx_, actions, out.observation, out.delta, out.reward_aux, out.flags, out.muscle_power,
+                           out.contact_force, stream),
+              ctx_);
+    }
+    void step_host(const float* actions, float* observation, float* delta, float* reward_aux, uint8_t* flags) {
+        check(msk_gpu_step_host(ctx_, actions, observation, delta, reward_aux, flags), ctx_);
+    }
+    void observe(float* observation, void* stream = nullptr) {
+        check(msk_gpu_observe(ctx_, observation, stream), ctx_);
+    }
+    void tracking_error(float* delta, void* stream = nullptr) {
+        check(msk_gpu_tracking_error(ctx_, delta, stream), ctx_);
+    }
+    void force_state_to_reference(void* stream = nullptr) {
+        check(msk_gpu_force_state_to_reference(ctx_, stream), ctx_);
+    }
+    void set_eval_mode(bool eval) { check(msk_gpu_set_eval_mode(ctx_, eval ? 1 : 0), ctx_); }
+    void drain_episode_outcomes(int32_t* bins, uint8_t* failed, int32_t* counts, int cap, void* stream = nullptr) {
+        check(msk_gpu_drain_outcomes(ctx_, bins, failed, counts, cap, stream), ctx_);
+    }
+    void record_own_outcomes(void* stream = nullptr) { check(msk_gpu_record_own_outcomes(ctx_, stream), ctx_); }
+    void fill_excitations(uint64_t seed, uint32_t step, float* actions, void* stream = nullptr) {
+        check(msk_gpu_fill_excitations(ctx_, seed, step, actions, stream), ctx_);
+    }
+
+    int n_envs() const { return dims_.n_envs; }
+    int observation_dim() const { return dims_.obs_dim; }  // Env::observation_dim (env.cpp:165-168)
+    int action_dim() const { return dims_.n_muscles; }     // Env::action_dim (env.hpp:105)
+    int delta_dim() const { return dims_.delta_dim; }      // TrackingError::dim (env.hpp:25-27)
+    int nq() const { return dims_.nq; }
+    int frames() const { return dims_.frames; }
+    msk_gpu_ctx* handle() { return ctx_; }
+
+private:
+    msk_gpu_ctx* ctx_ = nullptr;
+    msk_dims dims_{};
+};
+
+}  // namespace msk::gpu

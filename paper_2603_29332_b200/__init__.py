@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 __all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError",
            "FLAG_DONE", "FLAG_FAILED", "FLAG_DIVERGED", "FLAG_NOT_STEPPED", "FLAG_BAD_ACTION"]
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmsk_b200.so")
+LIB_PATH = os.environ.get("MSK_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmsk_b200.so")
 
 FLAG_DONE, FLAG_FAILED, FLAG_DIVERGED, FLAG_NOT_STEPPED, FLAG_BAD_ACTION = 1, 2, 4, 8, 16
 

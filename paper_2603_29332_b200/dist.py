@@ -1,0 +1,160 @@
+"""Multi-GPU exchange of the env-stepper.
+
+Envs are independent, so the data path has NO collective: rank r steps global
+envs [r*E, (r+1)*E) (seeds base + global index, so any sharding gives
+identical per-env results).  Once per rollout iteration every rank packs a
+fixed-size block
+
+    outcome bins  int32 [E, cap]   (Env::drain_episode_outcomes, env.cpp:200-204)
+    outcome failed int32 [E, cap]
+    outcome counts int32 [E]
+    rollout stats  float64 [7]     (n_steps, Σr, Σr², Σ episode length, episodes, failures, divergences)
+    obs moments    float64 [1 + 2 D]  (count, mean[D], population var[D] of this rank's batch)
+
+into one byte buffer and ``all_gather``s it (NCCL over NVLink on GPUs, gloo in
+the CPU tests).  Every rank then applies the SAME rank-ordered merge:
+
+* outcomes are recorded into ONE replicated adaptive sampler in global env
+  order, then time order (``AdaptiveSampler::record``, env.cpp:34-37 — the
+  "order-fixed reduction" of SPEC.md:296; on GPU: ``EnvBatch.merge_outcomes``);
+* rollout stats are summed in rank order (f64);
+* observation moments are folded in rank order with ``RunningNorm::update``'s
+  parallel-variance formula (nn.cpp:246-270).
+
+So all ranks end the iteration with bit-identical sampler and normaliser
+state without an all-reduce.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+N_STATS = 7
+
+
+def block_layout(n_envs: int, cap: int, obs_dim: int):
+    """Byte offsets of the per-rank block."""
+    sizes = [("bins", 4 * n_envs * cap), ("failed", 4 * n_envs * cap), ("counts", 4 * n_envs),
+             ("stats", 8 * N_STATS), ("norm", 8 * (1 + 2 * obs_dim))]
+    off, lay = 0, {}
+    for name, nbytes in sizes:
+        pad = (-off) % 8
+        off += pad
+        lay[name] = (off, nbytes)
+        off += nbytes
+    return lay, off
+
+
+def pack_block(bins, failed, counts, stats, norm, obs_dim):
+    """Packs one rank's iteration results into a uint8 tensor (same device as bins)."""
+    n, cap = bins.shape
+    lay, total = block_layout(n, cap, obs_dim)
+    buf = torch.zeros(total, dtype=torch.uint8, device=bins.device)
+
+    def put(name, t):
+        o, nb = lay[name]
+        buf[o:o + nb] = t.contiguous().view(torch.uint8).reshape(-1)
+
+    put("bins", bins.to(torch.int32))
+    put("failed", failed.to(torch.int32))
+    put("counts", counts.to(torch.int32))
+    put("stats", stats.to(torch.float64))
+    put("norm", norm.to(torch.float64))
+    return buf
+
+
+def unpack_block(buf, n_envs, cap, obs_dim):
+    lay, _ = block_layout(n_envs, cap, obs_dim)
+
+    def get(name, dtype, shape):
+        o, nb = lay[name]
+        return buf[o:o + nb].view(dtype).reshape(shape)
+
+    return dict(bins=get("bins", torch.int32, (n_envs, cap)), failed=get("failed", torch.int32, (n_envs, cap)),
+                counts=get("counts", torch.int32, (n_envs,)), stats=get("stats", torch.float64, (N_STATS,)),
+                norm=get("norm", torch.float64, (1 + 2 * obs_dim,)))
+
+
+def batch_moments(obs: torch.Tensor):
+    """(count, mean, population var) of an [n, D] batch, f64 (RunningNorm::update's batch terms)."""
+    x = obs.to(torch.float64)
+    n = x.shape[0]
+    mean = x.mean(0)
+    var = ((x - mean) ** 2).sum(0) / max(n, 1)
+    return torch.cat([torch.tensor([float(n)], dtype=torch.float64, device=x.device), mean, var])
+
+
+def running_norm_fold(count, mean, var, n, bmean, bvar):
+    """RunningNorm::update (nn.cpp:246-270) given a batch's (n, mean, var); numpy f64."""
+    if n == 0:
+        return count, mean, var
+    if count == 0.0:
+        return float(n), bmean.copy(), bvar.copy()
+    tot = count + n
+    delta = bmean - mean
+    var = (var * count + bvar * n + delta * delta * (count * n / tot)) / tot
+    mean = mean + delta * (n / tot)
+    return tot, mean, var
+
+
+def merge_outcomes_host(ema, bins, failed, counts, decay):
+    """Reference-order merge on the host (strict IEEE f64, no FMA contraction).
+
+    Mirrors msk_gpu_merge_outcomes: env order, then time order, into one
+    sampler EMA (AdaptiveSampler::record, env.cpp:34-37)."""
+    ema = [float(x) for x in ema]
+    bins_n = np.asarray(bins)
+    fail_n = np.asarray(failed)
+    cnt_n = np.asarray(counts)
+    cap = bins_n.shape[1]
+    for g in range(bins_n.shape[0]):
+        for i in range(min(int(cnt_n[g]), cap)):
+            b = int(bins_n[g, i])
+            if 0 <= b < len(ema):
+                ema[b] = decay * ema[b] + (1.0 - decay) * (1.0 if fail_n[g, i] else 0.0)
+    return np.array(ema)
+
+
+def exchange(block: torch.Tensor, group=None):
+    """all_gather of the fixed-size per-rank block; returns the list in rank order."""
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return [block]
+    out = [torch.empty_like(block) for _ in range(world)]
+    dist.all_gather(out, block, group=group)
+    return out
+
+
+def merged_iteration(blocks, n_envs, cap, obs_dim, norm_state, ema, decay, merge_on_device=None):
+    """Applies the rank-ordered merge to the gathered blocks.
+
+    Returns (stats_sum [7], norm_state, ema or None).  When ``merge_on_device``
+    (an EnvBatch) is given, the outcome merge runs on the GPU
+    (msk_gpu_merge_outcomes) and ``ema`` is ignored."""
+    parts = [unpack_block(b, n_envs, cap, obs_dim) for b in blocks]
+    stats = torch.zeros(N_STATS, dtype=torch.float64)
+    count, mean, var = norm_state
+    for p in parts:  # rank order
+        stats += p["stats"].cpu()
+        nm = p["norm"].cpu().numpy()
+        count, mean, var = running_norm_fold(count, mean, var, nm[0], nm[1:1 + obs_dim], nm[1 + obs_dim:])
+    bins = torch.cat([p["bins"] for p in parts])
+    failed = torch.cat([p["failed"] for p in parts])
+    counts = torch.cat([p["counts"] for p in parts])
+    if merge_on_device is not None:
+        merge_on_device.merge_outcomes(bins, failed.to(torch.uint8), counts)
+        new_ema = None
+    else:
+        new_ema = merge_outcomes_host(ema, bins.cpu(), failed.cpu(), counts.cpu(), decay)
+    return stats, (count, mean, var), new_ema
+
+
+def iteration_exchange(env, rollout_stats: torch.Tensor, obs_batch: torch.Tensor, norm_state, cap=64, group=None):
+    """One iteration boundary on a GPU rank: drain, pack, all_gather, ordered merge (device sampler)."""
+    bins, failed, counts = env.drain_outcomes(cap)
+    norm = batch_moments(obs_batch)
+    block = pack_block(bins, failed, counts, rollout_stats.to(bins.device), norm, env.obs_dim)
+    blocks = exchange(block, group)
+    return merged_iteration(blocks, env.n, cap, env.obs_dim, norm_state, None, env.cfg.adaptive_decay,
+                            merge_on_device=env)

@@ -1,0 +1,124 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the iteration exchange.
+
+The GPU path uses the same pack/all_gather/merge code with NCCL and the
+device merge kernel; here the outcome merge runs on the host
+(merge_outcomes_host), which the GPU test compares bit-exactly with
+msk_gpu_merge_outcomes.
+"""
+import ctypes as C
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2603_29332_b200 import dist as mdist
+
+N_ENVS, CAP, OBS_DIM, BINS, DECAY = 6, 5, 7, 10, 0.99
+
+
+def rank_data(rank):
+    g = np.random.default_rng(100 + rank)
+    counts = g.integers(0, CAP + 2, N_ENVS)  # some envs overflow the cap
+    bins = g.integers(0, BINS, (N_ENVS, CAP))
+    failed = g.integers(0, 2, (N_ENVS, CAP))
+    stats = g.normal(size=mdist.N_STATS)
+    obs = g.normal(size=(N_ENVS, OBS_DIM)) * (1 + rank)
+    return (torch.tensor(bins, dtype=torch.int32), torch.tensor(failed, dtype=torch.int32),
+            torch.tensor(counts, dtype=torch.int32), torch.tensor(stats), torch.tensor(obs))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    bins, failed, counts, stats, obs = rank_data(rank)
+    block = mdist.pack_block(bins, failed, counts, stats, mdist.batch_moments(obs), OBS_DIM)
+    blocks = mdist.exchange(block)
+    ema0 = np.linspace(0, 0.2, BINS)
+    st, norm, ema = mdist.merged_iteration(blocks, N_ENVS, CAP, OBS_DIM, (0.0, np.zeros(OBS_DIM), np.ones(OBS_DIM)),
+                                           ema0, DECAY)
+    np.savez(os.path.join(out_dir, f"r{rank}.npz"), stats=st.numpy(), count=norm[0], mean=norm[1], var=norm[2],
+             ema=ema)
+    dist.destroy_process_group()
+
+
+def test_pack_roundtrip():
+    bins, failed, counts, stats, obs = rank_data(0)
+    norm = mdist.batch_moments(obs)
+    p = mdist.unpack_block(mdist.pack_block(bins, failed, counts, stats, norm, OBS_DIM), N_ENVS, CAP, OBS_DIM)
+    assert torch.equal(p["bins"], bins) and torch.equal(p["failed"], failed) and torch.equal(p["counts"], counts)
+    assert torch.equal(p["stats"], stats) and torch.equal(p["norm"], norm)
+
+
+def test_two_rank_exchange_matches_single_rank_ordered_merge(tmp_path):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0, r1 = (np.load(tmp_path / f"r{r}.npz") for r in range(2))
+    for k in r0.files:  # every rank ends bit-identical
+        assert np.array_equal(r0[k], r1[k]), k
+    # single-rank reference: concatenation in global env order, merged in order
+    d0, d1 = rank_data(0), rank_data(1)
+    bins = torch.cat([d0[0], d1[0]])
+    failed = torch.cat([d0[1], d1[1]])
+    counts = torch.cat([d0[2], d1[2]])
+    ema = mdist.merge_outcomes_host(np.linspace(0, 0.2, BINS), bins, failed, counts, DECAY)
+    assert np.array_equal(ema, r0["ema"])
+    assert np.array_equal(r0["stats"], (d0[3] + d1[3]).numpy()) or np.allclose(r0["stats"], (d0[3] + d1[3]).numpy(),
+                                                                              rtol=0, atol=0)
+    # RunningNorm parallel fold == one update with all rows (up to rounding)
+    allobs = np.concatenate([d0[4].numpy(), d1[4].numpy()])
+    assert abs(r0["count"] - 2 * N_ENVS) == 0
+    assert np.allclose(r0["mean"], allobs.mean(0), rtol=1e-12, atol=1e-12)
+    assert np.allclose(r0["var"], allobs.var(0), rtol=1e-12, atol=1e-12)
+
+
+def test_host_merge_equals_oracle_sampler_record(assets):
+    """merge_outcomes_host follows AdaptiveSampler::record exactly (oracle, env.cpp:34-37)."""
+    from conftest import model_paths
+    from oracle.oracle import OracleBatch, lib
+    from oracle.ref import env_config
+
+    mp_, cp = model_paths("arm2_m6")
+    cfg = env_config(adaptive_bins=BINS, adaptive_decay=DECAY)
+    o = OracleBatch(mp_, cp, 1, cfg=cfg)
+    o.set_sampler(np.linspace(0, 0.2, BINS))
+    d = rank_data(0)
+    for g in range(N_ENVS):
+        for i in range(min(int(d[2][g]), CAP)):
+            lib().om_sampler_record(C.byref(cfg), C.byref(o.envs[0]), int(d[0][g, i]), int(d[1][g, i]))
+    host = mdist.merge_outcomes_host(np.linspace(0, 0.2, BINS), d[0], d[1], d[2], DECAY)
+    assert np.array_equal(o.get_sampler()[0], host)
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+@pytest.mark.gpu
+def test_device_merge_bit_exact_with_host(assets):
+    import paper_2603_29332_b200 as pk
+    from conftest import model_paths
+
+    mp_, cp = model_paths("arm2_m6")
+    g = pk.EnvBatch(mp_, cp, 3, cfg=pk.EnvConfig(adaptive_bins=BINS, adaptive_decay=DECAY))
+    ema0 = np.linspace(0, 0.2, BINS)
+    g.set_sampler(torch.as_tensor(ema0, device=g.device))
+    d0, d1 = rank_data(0), rank_data(1)
+    bins = torch.cat([d0[0], d1[0]]).cuda()
+    failed = torch.cat([d0[1], d1[1]]).to(torch.uint8).cuda()
+    counts = torch.cat([d0[2], d1[2]]).cuda()
+    g.merge_outcomes(bins, failed, counts)
+    host = mdist.merge_outcomes_host(ema0, bins.cpu(), failed.cpu(), counts.cpu(), DECAY)
+    got = g.get_sampler().cpu().numpy()
+    for e in range(3):
+        assert np.array_equal(got[e], host)
+    g.close()
