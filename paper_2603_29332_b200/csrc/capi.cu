@@ -257,7 +257,41 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.off_union = off;
         off = align16(off + 4 * std::max({c.n_pairs + 1, kLinkStride * c.nl, 2 * c.nq}));  // +1: dummy slot
         M.smem_env_bytes = off;
-        const int per_block = envs_per_block() * M.smem_env_bytes;
+        {  // block-shared tree table: link {anchor, com, mass}, inertia, packed meta,
+           // child lists and the depth-level schedule (u8 indices, n_links <= 255)
+            if (c.nl > 255 || c.n_levels > 255) throw ConfigError("model too large: n_links > 255");
+            int t = 0;
+            M.tab_off_a = t;
+            t += 16 * c.nl;
+            M.tab_off_in = t;
+            t += 4 * c.nl;
+            M.tab_off_meta = t;
+            t += 4 * c.nl;
+            M.tab_off_child = t;
+            t += c.nl;
+            M.tab_off_lvl = t;
+            t += c.nl;
+            M.tab_off_lvs = t;
+            t += c.n_levels + 1;
+            M.tab_bytes = align16(t);
+            std::vector<unsigned char> blob(M.tab_bytes, 0);
+            auto put = [&](int at, const void* src, size_t n) { std::memcpy(blob.data() + at, src, n); };
+            for (int l = 0; l < c.nl; ++l) {
+                const float a[4] = {c.link_ax[l], c.link_az[l], c.link_com[l], c.link_mass[l]};
+                put(M.tab_off_a + 16 * l, a, 16);
+                put(M.tab_off_in + 4 * l, &c.link_inertia[l], 4);
+                const int nchild = c.child_start[l + 1] - c.child_start[l];
+                const int has_sph = c.sphere_start[l + 1] > c.sphere_start[l] ? 1 : 0;
+                const int meta = (c.link_parent[l] + 1) | (nchild << 8) | (c.child_start[l] << 16) | (has_sph << 24);
+                put(M.tab_off_meta + 4 * l, &meta, 4);
+                blob[M.tab_off_child + l] = static_cast<unsigned char>(l < static_cast<int>(c.child_list.size())
+                                                                          ? c.child_list[l] : 0);
+                blob[M.tab_off_lvl + l] = static_cast<unsigned char>(c.level_links[l]);
+            }
+            for (int d = 0; d <= c.n_levels; ++d) blob[M.tab_off_lvs + d] = static_cast<unsigned char>(c.level_start[d]);
+            M.tab_blob = reinterpret_cast<const int4*>(ctx->upload(blob));
+        }
+        const int per_block = M.tab_bytes + envs_per_block() * M.smem_env_bytes;
         if (per_block > static_cast<int>(prop.sharedMemPerBlockOptin))
             throw ConfigError("model needs " + std::to_string(per_block) + " B of shared memory per block");
         ck(prepare_kernels(per_block), "cudaFuncSetAttribute");

@@ -12,7 +12,7 @@ constexpr double kSimDt = 0.002;     // skeleton.hpp:11
 constexpr double kCtrlDt = 0.02;     // skeleton.hpp:12
 constexpr float kMinFiber = 0.01f;   // skeleton.hpp:14
 constexpr int kMaxQSlots = 4;        // nq <= 128 (DOF d lives in lane d%32, slot d/32)
-constexpr int kLinkStride = 15;      // floats per link in the ABA scratch (odd: bank-conflict free)
+constexpr int kLinkStride = 14;      // floats per link in the ABA scratch
 
 enum : uint8_t {
     kFlagDone = 1,
@@ -74,6 +74,9 @@ struct DevModel {
     const int* emg_map;
     // per-env smem layout (bytes from the warp's base)
     int smem_env_bytes, off_relcs, off_dqf, off_tau, off_root, off_union;
+    // block-shared tree table at the head of dynamic smem (bytes)
+    const int4* tab_blob;
+    int tab_bytes, tab_off_a, tab_off_in, tab_off_meta, tab_off_child, tab_off_lvl, tab_off_lvs;
 };
 
 // Per-env mutable state (device pointers, env-major rows).

@@ -35,6 +35,26 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr double kPi = 3.14159265358979323846;
 constexpr int kSegCache = 4;  // segments per muscle kept in registers between length and torque
 
+// Optional per-phase cycle counters (build with -DMSK_PHASE_TIMERS; read with
+// msk_gpu_phase_cycles): lane 0 of every warp adds clock64() deltas.
+#ifdef MSK_PHASE_TIMERS
+__device__ unsigned long long g_phase_cycles[8];
+#define PHASE_T0() long long phase_t_ = clock64()
+#define PHASE_MARK(i)                                                                          \
+    do {                                                                                       \
+        const long long n_ = clock64();                                                        \
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_phase_cycles[i], (unsigned long long)(n_ - phase_t_)); \
+        phase_t_ = n_;                                                                         \
+    } while (0)
+#else
+#define PHASE_T0() \
+    do {           \
+    } while (0)
+#define PHASE_MARK(i) \
+    do {              \
+    } while (0)
+#endif
+
 struct EnvSmem {
     float4* kin;     // nl: cos, sin, origin x, origin z (root-relative)
     double2* relcs;  // nq: cos, sin of each joint's own rotation (mount + q), f64
@@ -42,17 +62,43 @@ struct EnvSmem {
     float* tau;      // nq: joint torque, then q̈
     float* root;     // [0] root x, [1] root z (absolute), [2] cos q2, [3] sin q2
     float* un;       // union: pair slots | kLinkStride floats per link (ABA) | f64 q
+    // block-shared tree table (copied once per block; see CompiledModel tab_*)
+    const float4* ta;      // nl: {anchor x, anchor z, com, mass}
+    const float* tin;      // nl: inertia
+    const int* tmeta;      // nl: (parent + 1) | nchild << 8 | child_off << 16 | has_sphere << 24
+    const uint8_t* tchild; // child lists
+    const uint8_t* tlvl;   // links grouped by depth
+    const uint8_t* tlvs;   // level starts
 };
 
-__device__ __forceinline__ EnvSmem carve(unsigned char* base, const DevModel& M) {
+// Block prologue: copy the tree table into the head of shared memory.  Must be
+// reached by every thread of the block (it ends in __syncthreads).
+__device__ __forceinline__ void load_tree_table(unsigned char* smem, const DevModel& M) {
+    int4* dst = reinterpret_cast<int4*>(smem);
+    for (int i = threadIdx.x; i < M.tab_bytes / 16; i += blockDim.x) dst[i] = __ldg(M.tab_blob + i);
+    __syncthreads();
+}
+
+__device__ __forceinline__ EnvSmem carve(unsigned char* smem, int warp, const DevModel& M) {
     EnvSmem s;
+    unsigned char* base = smem + M.tab_bytes + warp * M.smem_env_bytes;
     s.kin = reinterpret_cast<float4*>(base);
     s.relcs = reinterpret_cast<double2*>(base + M.off_relcs);
     s.dqf = reinterpret_cast<float*>(base + M.off_dqf);
     s.tau = reinterpret_cast<float*>(base + M.off_tau);
     s.root = reinterpret_cast<float*>(base + M.off_root);
     s.un = reinterpret_cast<float*>(base + M.off_union);
+    s.ta = reinterpret_cast<const float4*>(smem + M.tab_off_a);
+    s.tin = reinterpret_cast<const float*>(smem + M.tab_off_in);
+    s.tmeta = reinterpret_cast<const int*>(smem + M.tab_off_meta);
+    s.tchild = smem + M.tab_off_child;
+    s.tlvl = smem + M.tab_off_lvl;
+    s.tlvs = smem + M.tab_off_lvs;
     return s;
+}
+
+__device__ __forceinline__ int link_dof(const DevModel& M, int l) {
+    return l >= M.floating ? M.nrd + l - M.floating : -1;
 }
 
 // ---- Hill-type muscle (muscle.cpp:9-40) -----------------------------------
@@ -105,6 +151,18 @@ __device__ __forceinline__ float general_seg_len(const DevModel& M, const EnvSme
 // Adjacent segment in its parent's frame: s = A + R(joint) c.  Returns |s|
 // (f64), 1/|s| and the cross product r x A (r = R c) that sets the moment arm.
 __device__ __forceinline__ double adj_segment(const EnvSmem& S, float4 g, int info, float& cross, float& inv) {
+#ifdef MSK_FP32_GEOM  // experiment: f32 segment geometry (precision study only)
+    {
+        const double2 cd = S.relcs[(info >> 2) & 511];
+        const float c = static_cast<float>(cd.x), s = static_cast<float>(cd.y);
+        const float rx = fmaf(c, g.z, -s * g.w), rz = fmaf(s, g.z, c * g.w);
+        const float sx = g.x + rx, sz = g.y + rz;
+        cross = fmaf(rx, g.y, -rz * g.x);
+        const float x = fmaf(sx, sx, sz * sz);
+        inv = rsqrtf(x);
+        return static_cast<double>(x * inv);
+    }
+#endif
     const double2 cs = S.relcs[(info >> 2) & 511];
     const double rx = fma(cs.x, static_cast<double>(g.z), -cs.y * static_cast<double>(g.w));
     const double rz = fma(cs.y, static_cast<double>(g.z), cs.x * static_cast<double>(g.w));
@@ -191,11 +249,12 @@ __device__ __forceinline__ void publish_dofs(const DevModel& M, const EnvSmem& S
 template <bool kFull>
 __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, int lane, float* grf) {
     for (int lev = 0; lev < M.n_levels; ++lev) {
-        const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
+        const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
         for (int i = lane; i < n; i += 32) {
-            const int l = __ldg(M.level_links + b + i);
-            const int dof = __ldg(M.link_dof + l);
-            const float4 la = __ldg(M.link_a + l);
+            const int l = S.tlvl[b + i];
+            const int dof = link_dof(M, l);
+            const int meta = S.tmeta[l];
+            const float4 la = S.ta[l];
             float c, s, ox, oz, w = 0.0f, vx = 0.0f, vz = 0.0f;
             if (dof < 0) {  // floating root: origin (0,0) relative, pitch q2
                 c = S.root[2];
@@ -208,7 +267,7 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
                     vz = S.dqf[1];
                 }
             } else {
-                const int p = __ldg(M.link_parent + l);
+                const int p = (meta & 0xff) - 1;
                 const double2 rd = S.relcs[dof];
                 const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
                 if (p >= 0) {
@@ -238,14 +297,14 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
             u[9] = w;
             u[10] = vx;
             u[11] = vz;
-            const float m = la.w, I = __ldg(M.link_inertia + l);
+            const float m = la.w, I = S.tin[l];
             const float cx = la.z * c, cz = la.z * s;
             const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
             const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
             const float mg = m * M.gravity;
             float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
-            const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
-            if (s0 < s1) {
+            if (meta >> 24) {  // link carries contact spheres
+                const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
                 float gx = 0.0f, gz = 0.0f;
                 for (int sp = s0; sp < s1; ++sp) {
                     const float4 sd = __ldg(M.sphere + sp);
@@ -284,8 +343,8 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
             u[6] = p0;
             u[7] = p1;
             u[8] = p2;
-            u[13] = c1;
-            u[14] = c2;
+            u[12] = c1;
+            u[13] = c2;
         }
         __syncwarp();
     }
@@ -296,19 +355,19 @@ __device__ __forceinline__ void key_body(const DevModel& M, const EnvSmem& S, co
                                          double& x, double& z, double& ang) {
     const int l = __ldg(M.key_bodies + k);
     const float4 kl = S.kin[l];
-    const float c = __ldg(M.link_a + l).z;
+    const float c = S.ta[l].z;
     x = static_cast<double>(fmaf(kl.x, c, kl.z));
     z = static_cast<double>(fmaf(kl.y, c, kl.w));
     double a = 0.0;
     int cur = l;
     while (cur >= 0) {
-        const int dof = __ldg(M.link_dof + cur);
+        const int dof = link_dof(M, cur);
         if (dof < 0) {
             a += qsm[2];
             break;
         }
         a += __ldg(M.link_mount + cur) + qsm[dof];
-        cur = __ldg(M.link_parent + cur);
+        cur = (S.tmeta[cur] & 0xff) - 1;
     }
     ang = a;
     if (M.floating) {
@@ -584,9 +643,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int le = blockIdx.x * WPB + warp;  // env index local to this launch
+    load_tree_table(smem, M);
     if (le >= n_envs) return;
     const int e = env0 + le;
-    const EnvSmem S = carve(smem + warp * M.smem_env_bytes, M);
+    const EnvSmem S = carve(smem, warp, M);
     const int nq = M.nq, nm = M.nm, nl = M.nl, nrd = M.nrd;
     const size_t mb = static_cast<size_t>(e) * nm;
     const float* act_row = actions + static_cast<size_t>(le) * nm;
@@ -617,6 +677,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         for (int i = lane; i < 2 * nl; i += 32) grf_row[i] = 0.0f;
     __syncwarp();
 
+    PHASE_T0();
     int diverged_at = -1;
     for (int sub = 0; sub < kSubsteps; ++sub) {
         if (M.has_general) tree_sweep<false>(M, S, lane, nullptr);  // world frame for general segments
@@ -625,6 +686,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane);
         __syncwarp();
 
+        PHASE_MARK(0);
         // ---- 2. joint torques: fixed-order slot sums, damping, limits ----
 #pragma unroll
         for (int k = 0; k < kMaxQSlots; ++k) {
@@ -633,7 +695,18 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 const int j = d - nrd;
                 const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
                 float t = 0.0f;
-                for (int s = s0; s < s1; ++s) t += S.un[s];
+                {  // fixed-order sum with 4 independent accumulators (latency / 4)
+                    float t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
+                    int s = s0;
+                    for (; s + 3 < s1; s += 4) {
+                        t += S.un[s];
+                        t1 += S.un[s + 1];
+                        t2 += S.un[s + 2];
+                        t3 += S.un[s + 3];
+                    }
+                    for (; s < s1; ++s) t += S.un[s];
+                    t = (t + t1) + (t2 + t3);
+                }
                 t -= __ldg(M.joint_damping + j) * static_cast<float>(dqd[k]);
                 const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
                 if (qd[k] > hi)
@@ -645,20 +718,23 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         }
         __syncwarp();
 
+        PHASE_MARK(1);
         // ---- 3. FK + velocities + per-link articulated-body terms ----
         tree_sweep<true>(M, S, lane, grf_row);
 
+        PHASE_MARK(2);
         // ---- 4a. articulated-body pass, leaves -> root ----
         for (int lev = M.n_levels - 1; lev >= 0; --lev) {
-            const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
+            const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
             for (int i = lane; i < n; i += 32) {
-                const int l = __ldg(M.level_links + b + i);
+                const int l = S.tlvl[b + i];
+                const int meta = S.tmeta[l];
                 float* u = S.un + kLinkStride * l;
                 float I00 = u[0], I01 = u[1], I02 = u[2], I11 = u[3], I12 = u[4], I22 = u[5];
                 float P0 = u[6], P1 = u[7], P2 = u[8];
-                const int c0 = __ldg(M.child_start + l), c1 = __ldg(M.child_start + l + 1);
+                const int c0 = (meta >> 16) & 0xff, c1 = c0 + ((meta >> 8) & 0xff);
                 for (int c = c0; c < c1; ++c) {
-                    const float* uc = S.un + kLinkStride * __ldg(M.child_list + c);
+                    const float* uc = S.un + kLinkStride * S.tchild[c];
                     I00 += uc[0];
                     I01 += uc[1];
                     I02 += uc[2];
@@ -669,7 +745,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                     P1 += uc[7];
                     P2 += uc[8];
                 }
-                const int dof = __ldg(M.link_dof + l);
+                const int dof = link_dof(M, l);
                 if (dof < 0) {  // floating root keeps its full articulated inertia
                     u[0] = I00; u[1] = I01; u[2] = I02; u[3] = I11; u[4] = I12; u[5] = I22;
                     u[6] = P0; u[7] = P1; u[8] = P2;
@@ -683,14 +759,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
                 const float bb = fmaf(-I01, U2, I12);
                 const float cq = fmaf(-I02, U2, I22);
-                const float cv1 = u[13], cv2 = u[14];
+                const float cv1 = u[12], cv2 = u[13];
                 // pa = pA + Ia c + U u / D   (pa[0] = tau)
                 const float q1 = fmaf(I01, uu, fmaf(a, cv1, fmaf(bb, cv2, P1)));
                 const float q2 = fmaf(I02, uu, fmaf(bb, cv1, fmaf(cq, cv2, P2)));
                 u[9] = uu;
-                u[11] = U1;
-                u[12] = U2;
-                const int p = __ldg(M.link_parent + l);
+                u[10] = U1;
+                u[11] = U2;
+                const int p = (meta & 0xff) - 1;
                 if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
                     const float4 kl = S.kin[l], kp = S.kin[p];
                     const float dx = kl.z - kp.z, dz = kl.w - kp.w;
@@ -709,6 +785,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
             __syncwarp();
         }
 
+        PHASE_MARK(3);
         // ---- 4b. root solve + articulated-body pass, root -> leaves ----
         if (M.floating && lane == 0) {
             float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky)
@@ -734,14 +811,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         }
         __syncwarp();
         for (int lev = 0; lev < M.n_levels; ++lev) {
-            const int b = __ldg(M.level_start + lev), n = __ldg(M.level_start + lev + 1) - b;
+            const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
             for (int i = lane; i < n; i += 32) {
-                const int l = __ldg(M.level_links + b + i);
-                const int dof = __ldg(M.link_dof + l);
+                const int l = S.tlvl[b + i];
+                const int dof = link_dof(M, l);
                 if (dof < 0) continue;
                 float* u = S.un + kLinkStride * l;
-                const int p = __ldg(M.link_parent + l);
-                float A0 = 0.0f, A1 = u[13], A2 = u[14];
+                const int p = (S.tmeta[l] & 0xff) - 1;
+                float A0 = 0.0f, A1 = u[12], A2 = u[13];
                 if (p >= 0) {
                     const float* up = S.un + kLinkStride * p;
                     const float4 kl = S.kin[l], kp = S.kin[p];
@@ -751,7 +828,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                     A2 += fmaf(up[0], dx, up[2]);
                 }
                 // q̈ = (u - U^T A) / D with U0 = D
-                const float qdd = u[9] - A0 - fmaf(u[11], A1, u[12] * A2);
+                const float qdd = u[9] - A0 - fmaf(u[10], A1, u[11] * A2);
                 u[0] = A0 + qdd;
                 u[1] = A1;
                 u[2] = A2;
@@ -760,6 +837,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
             __syncwarp();
         }
 
+        PHASE_MARK(4);
         // ---- 5. semi-implicit Euler (f64) + divergence check ----
         bool bad = false;
 #pragma unroll
@@ -780,6 +858,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         }
     }
 
+    PHASE_MARK(5);
     // ---- write back the simulation state ----
 #pragma unroll
     for (int k = 0; k < kMaxQSlots; ++k) {
@@ -881,9 +960,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * WPB + warp;
+    load_tree_table(smem, M);
     if (e >= n_envs) return;
     if (mask && !(mask[e] & mask_bits)) return;
-    const EnvSmem S = carve(smem + warp * M.smem_env_bytes, M);
+    const EnvSmem S = carve(smem, warp, M);
     const int nq = M.nq;
     int frame = 0;
     if (mode == kResetSample) {
@@ -942,8 +1022,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, Dev
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int e = blockIdx.x * WPB + warp;
+    load_tree_table(smem, M);
     if (e >= n_envs) return;
-    const EnvSmem S = carve(smem + warp * M.smem_env_bytes, M);
+    const EnvSmem S = carve(smem, warp, M);
     const int nq = M.nq;
     double qd[kMaxQSlots], dqd[kMaxQSlots];
     load_dofs(M, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
@@ -1125,8 +1206,14 @@ double measure_fp32_peak_tflops() {
 // ============================================================================
 // host-side launch wrappers
 // ============================================================================
-constexpr int kWPB = 7;   // envs (warps) per block
-constexpr int kMinB = 4;  // blocks per SM: 28 envs resident -> 4096 envs in one wave, <= 72 regs
+#ifndef MSK_WPB
+#define MSK_WPB 7   // envs (warps) per block
+#endif
+#ifndef MSK_MINB
+#define MSK_MINB 4  // blocks per SM: 28 envs resident -> 4096 envs in one wave, <= 72 regs
+#endif
+constexpr int kWPB = MSK_WPB;
+constexpr int kMinB = MSK_MINB;
 
 // Fast-path segment count for a model (0 = generic path).
 int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 && M.max_seg <= 4) ? M.max_seg : 0; }
@@ -1134,6 +1221,10 @@ int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 &
 template <int NSEG>
 cudaError_t set_step_smem(int bytes) {
     return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+size_t block_smem(const DevModel& M) {
+    return static_cast<size_t>(M.tab_bytes) + static_cast<size_t>(kWPB) * M.smem_env_bytes;
 }
 
 cudaError_t prepare_kernels(int smem_bytes_per_block) {
@@ -1155,7 +1246,7 @@ int envs_per_block() { return kWPB; }
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
                  float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s) {
     const int blocks = (n + kWPB - 1) / kWPB;
-    const size_t smem = static_cast<size_t>(kWPB) * M.smem_env_bytes;
+    const size_t smem = block_smem(M);
 #define MSK_STEP(NS)                                                                                          \
     step_kernel<kWPB, kMinB, NS><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux, flags, \
                                                                  power, grf)
@@ -1172,13 +1263,13 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
 void launch_reset(const DevModel& M, const DevState& St, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t s) {
     const int blocks = (n + kWPB - 1) / kWPB;
-    reset_kernel<kWPB, kMinB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, n, mode, mask, bits, frames_in,
+    reset_kernel<kWPB, kMinB><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, mode, mask, bits, frames_in,
                                                                           obs, frames_out, bad);
 }
 
 void launch_observe(const DevModel& M, const DevState& St, int n, float* obs, float* delta, cudaStream_t s) {
     const int blocks = (n + kWPB - 1) / kWPB;
-    observe_kernel<kWPB, kMinB><<<blocks, kWPB * 32, kWPB * M.smem_env_bytes, s>>>(M, St, n, obs, delta);
+    observe_kernel<kWPB, kMinB><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, obs, delta);
 }
 
 void launch_seed(const DevState& St, int n, uint64_t base_seed, cudaStream_t s) {
@@ -1223,3 +1314,15 @@ void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint
 }
 
 }  // namespace msk_b200
+
+#ifdef MSK_PHASE_TIMERS
+// Diagnostics build only: per-phase cycle totals (summed over warps and substeps).
+extern "C" int msk_gpu_phase_cycles(unsigned long long* out, int reset) {
+    if (cudaMemcpyFromSymbol(out, msk_b200::g_phase_cycles, sizeof(unsigned long long) * 8) != cudaSuccess) return 3;
+    if (reset) {
+        const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(msk_b200::g_phase_cycles, z, sizeof(z));
+    }
+    return 0;
+}
+#endif

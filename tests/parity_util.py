@@ -74,13 +74,18 @@ def force_err(fm_g, fm_o, fmax):
 
 
 def obs_block_errors(g, obs_g, obs_o):
-    """Per-block max relative error (floor 1) of an observation row (env.cpp:129-163)."""
+    """Per-block relative error of observation rows (env.cpp:129-163): for each env and
+    block, max|Δ| / max(1, max|ref|) — the same norm-wise criterion as q/q̇."""
     nq, nk, nm = g.nq, g.nk, g.nm
     names = [("q", nq), ("dq", nq), ("key_pos", 2 * nk), ("key_angle", nk), ("act", nm), ("f_m", nm),
              ("l_m", nm), ("v_m", nm), ("q_ref", nq), ("key_pos_ref", 2 * nk), ("key_angle_ref", nk)]
     out, o = {}, 0
     for name, n in names:
         a, b = obs_g[:, o:o + n], obs_o[:, o:o + n]
-        out[name] = float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b)))) if n else 0.0
+        if n:
+            scale = np.maximum(1.0, np.abs(b).max(axis=1, keepdims=True))
+            out[name] = float(np.max(np.abs(a - b) / scale))
+        else:
+            out[name] = 0.0
         o += n
     return out

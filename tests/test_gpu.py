@@ -6,7 +6,7 @@ control step (10 substeps) from identical state and excitations:
   activation  max|Δ| <= 1e-6
   muscle force |ΔF| <= 1e-4 * max(|F|, f_max)        (per muscle)
   Δ (tracking error) max|Δ| <= 1e-5 m / rad
-  observation max|Δ| <= 1e-4 * max(1, |ref|)         (element-wise)
+  observation max|Δ| <= 1e-4 * max(1, max|ref block|) (per env and obs block)
   flags, t_index, steps, start frames, RNG draws, sampler: bit-exact.
 Bounded drift over a short horizon is checked separately with a looser bound.
 """
