@@ -190,7 +190,7 @@ def cpu_baseline_sample(args):
     b.bench(1)
     secs, steps = b.bench(1)
     per_step = secs
-    k = max(1, min(50, int(args.cpu_seconds / max(per_step, 1e-3))))
+    k = max(1, min(5000, int(args.cpu_seconds / max(per_step, 1e-3))))
     secs, steps = b.bench(k)
     return {"value": steps / secs, "unit": "env-steps/s", "cores": threads, "kind": "reference",
             "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)"}

@@ -200,6 +200,15 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             M.m_p0 = ctx->upload(p0);
             M.m_p1 = ctx->upload(p1);
             M.seg_geo = ctx->upload(geo);
+            // |A + R c|^2 = |A|^2 + |c|^2 + 2 (cos A.c + sin (A_z c_x - A_x c_z)), from the
+            // same f32-rounded constants the generic path uses
+            std::vector<double2> kk(2 * geo.size());
+            for (size_t i = 0; i < geo.size(); ++i) {
+                const double ax = geo[i].x, az = geo[i].y, cx = geo[i].z, cz = geo[i].w;
+                kk[2 * i] = make_double2(ax * ax + az * az + cx * cx + cz * cz, ax * cx + az * cz);
+                kk[2 * i + 1] = make_double2(az * cx - ax * cz, 0.0);
+            }
+            M.seg_k = ctx->upload(kk);
         }
         M.max_seg = c.max_seg;
         M.has_general = c.has_general;
@@ -218,6 +227,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.joint_slot_start = ctx->upload(c.joint_slot_start);
         M.m_meta = ctx->upload(c.pk_meta);
         M.seg_info = ctx->upload(c.pk_info);
+        M.m_info4 = reinterpret_cast<const int4*>(ctx->upload(c.pk_info4));
         M.m_pair_start = ctx->upload(c.m_pair_start);
         M.via_link = ctx->upload(c.via_link);
         M.via_x = ctx->upload(c.via_x);

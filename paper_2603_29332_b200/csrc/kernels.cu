@@ -31,9 +31,7 @@ namespace msk_b200 {
 
 namespace {
 
-constexpr unsigned kFull = 0xffffffffu;
 constexpr double kPi = 3.14159265358979323846;
-constexpr int kSegCache = 4;  // segments per muscle kept in registers between length and torque
 
 // Optional per-phase cycle counters (build with -DMSK_PHASE_TIMERS; read with
 // msk_gpu_phase_cycles): lane 0 of every warp adds clock64() deltas.
@@ -69,6 +67,8 @@ struct EnvSmem {
     const uint8_t* tchild; // child lists
     const uint8_t* tlvl;   // links grouped by depth
     const uint8_t* tlvs;   // level starts
+    int G;                 // lanes per env (32 or 16)
+    unsigned hm;           // mask of this env's lanes
 };
 
 // Block prologue: copy the tree table into the head of shared memory.  Must be
@@ -79,9 +79,11 @@ __device__ __forceinline__ void load_tree_table(unsigned char* smem, const DevMo
     __syncthreads();
 }
 
-__device__ __forceinline__ EnvSmem carve(unsigned char* smem, int warp, const DevModel& M) {
+__device__ __forceinline__ EnvSmem carve(unsigned char* smem, int slot, const DevModel& M, int G, unsigned hm) {
     EnvSmem s;
-    unsigned char* base = smem + M.tab_bytes + warp * M.smem_env_bytes;
+    s.G = G;
+    s.hm = hm;
+    unsigned char* base = smem + M.tab_bytes + slot * M.smem_env_bytes;
     s.kin = reinterpret_cast<float4*>(base);
     s.relcs = reinterpret_cast<double2*>(base + M.off_relcs);
     s.dqf = reinterpret_cast<float*>(base + M.off_dqf);
@@ -122,15 +124,14 @@ __device__ __forceinline__ float mtu_force(float act, float l, float v, float fm
 
 // sqrt of a non-negative f64 from the f32 rsqrt seed plus one f64 Newton
 // correction (~46 bits); also returns the f32 reciprocal length.
+// x is clamped at 1e-30 so degenerate/padding segments stay finite (|s| ~ 1e-15).
 __device__ __forceinline__ double sqrt_d(double x, float& inv) {
+    x = fmax(x, 1e-30);
     const float r = rsqrtf(static_cast<float>(x));
-    if (!(x > 0.0)) {
-        inv = 0.0f;
-        return 0.0;
-    }
     inv = r;
-    const double s = x * static_cast<double>(r);
-    return fma(fma(-s, s, x), 0.5 * static_cast<double>(r), s);
+    const double rd = static_cast<double>(r);
+    const double s = x * rd;
+    return fma(fma(-s, s, x), 0.5 * rd, s);
 }
 
 // World (root-relative) position of a via point (general segments only).
@@ -216,11 +217,12 @@ __device__ void general_pairs(const DevModel& M, const EnvSmem& S, int m, float 
 
 // Per-DOF views for the tree passes: each joint's own rotation (f64 sincos of
 // mount + q), root pitch rotation, root position, and f32 velocities.
+template <int QS>
 __device__ __forceinline__ void publish_dofs(const DevModel& M, const EnvSmem& S, const double* qd,
                                              const double* dqd, int lane) {
 #pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
+    for (int k = 0; k < QS; ++k) {
+        const int d = lane + S.G * k;
         if (d < M.nq) {
             if (d >= M.nrd) {
                 const int l = M.floating + (d - M.nrd);
@@ -250,7 +252,7 @@ template <bool kFull>
 __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, int lane, float* grf) {
     for (int lev = 0; lev < M.n_levels; ++lev) {
         const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-        for (int i = lane; i < n; i += 32) {
+        for (int i = lane; i < n; i += S.G) {
             const int l = S.tlvl[b + i];
             const int dof = link_dof(M, l);
             const int meta = S.tmeta[l];
@@ -346,7 +348,7 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
             u[12] = c1;
             u[13] = c2;
         }
-        __syncwarp();
+        __syncwarp(S.hm);
     }
 }
 
@@ -393,11 +395,11 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
                           int t_index, float* obs_row, int lane) {
     const int nq = M.nq, nm = M.nm, nk = M.nk;
     int o = 0;
-    for (int i = lane; i < nq; i += 32) obs_row[o + i] = static_cast<float>(qsm[i]);
+    for (int i = lane; i < nq; i += S.G) obs_row[o + i] = static_cast<float>(qsm[i]);
     o += nq;
-    for (int i = lane; i < nq; i += 32) obs_row[o + i] = static_cast<float>(St.dq[static_cast<size_t>(e) * nq + i]);
+    for (int i = lane; i < nq; i += S.G) obs_row[o + i] = static_cast<float>(St.dq[static_cast<size_t>(e) * nq + i]);
     o += nq;
-    for (int k = lane; k < nk; k += 32) {
+    for (int k = lane; k < nk; k += S.G) {
         double x, z, a;
         key_body(M, S, qsm, k, x, z, a);
         obs_row[o + 2 * k] = static_cast<float>(x);
@@ -406,7 +408,7 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
     }
     o += 3 * nk;
     const size_t mb = static_cast<size_t>(e) * nm;
-    for (int i = lane; i < nm; i += 32) {
+    for (int i = lane; i < nm; i += S.G) {
         obs_row[o + i] = St.act[mb + i];
         obs_row[o + nm + i] = St.fm[mb + i];
         obs_row[o + 2 * nm + i] = St.lm[mb + i];
@@ -414,11 +416,11 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
     }
     o += 4 * nm;
     const size_t t = static_cast<size_t>(t_index);
-    for (int i = lane; i < nq; i += 32) obs_row[o + i] = static_cast<float>(M.clip_q[t * nq + i]);
+    for (int i = lane; i < nq; i += S.G) obs_row[o + i] = static_cast<float>(M.clip_q[t * nq + i]);
     o += nq;
-    for (int i = lane; i < 2 * nk; i += 32) obs_row[o + i] = static_cast<float>(M.clip_kp[t * 2 * nk + i]);
+    for (int i = lane; i < 2 * nk; i += S.G) obs_row[o + i] = static_cast<float>(M.clip_kp[t * 2 * nk + i]);
     o += 2 * nk;
-    for (int i = lane; i < nk; i += 32) obs_row[o + i] = static_cast<float>(M.clip_ka[t * nk + i]);
+    for (int i = lane; i < nk; i += S.G) obs_row[o + i] = static_cast<float>(M.clip_ka[t * nk + i]);
 }
 
 // Env::tracking_error (env.cpp:170-193) -> Δ row (f64 values rounded once).
@@ -436,10 +438,10 @@ __device__ bool write_delta(const DevModel& M, const EnvSmem& S, const double* q
         if (drow) drow[lane] = static_cast<float>(v);
     }
     if (drow)
-        for (int j = lane; j < nj; j += 32)
+        for (int j = lane; j < nj; j += S.G)
             drow[3 + j] = static_cast<float>(qsm[nrd + j] - M.clip_q[t * nq + nrd + j]);
     bool far = false;
-    for (int k = lane; k < nk; k += 32) {
+    for (int k = lane; k < nk; k += S.G) {
         double x, z, a;
         key_body(M, S, qsm, k, x, z, a);
         const double dx = x - M.clip_kp[t * 2 * nk + 2 * k];
@@ -450,14 +452,14 @@ __device__ bool write_delta(const DevModel& M, const EnvSmem& S, const double* q
         }
         if (sqrt(dx * dx + dz * dz) > M.term_err) far = true;
     }
-    return __any_sync(kFull, far);
+    return __any_sync(S.hm, far);
 }
 
 // make_initial_state (skeleton.cpp:264-284) for the env's muscles (relcs/FK in smem).
 __device__ void init_muscles(const DevModel& M, const DevState& St, const EnvSmem& S, int e, int lane) {
     const size_t mb = static_cast<size_t>(e) * M.nm;
     const float a0 = static_cast<float>(M.init_act);
-    for (int m = lane; m < M.nm; m += 32) {
+    for (int m = lane; m < M.nm; m += S.G) {
         const double2 pa = __ldg(M.m_p1 + 2 * m), pb = __ldg(M.m_p1 + 2 * m + 1);
         const double L = muscle_length(M, S, m);
         const float lm = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
@@ -533,7 +535,7 @@ template <int NSEG>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
                                              const float* act_row, size_t mb, float* pw, int lane) {
     const int nm = M.nm;
-    for (int m = lane; m < nm; m += 32) {
+    for (int m = lane; m < nm; m += S.G) {
         const float4 p0 = __ldg(M.m_p0 + m);  // f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max/10
         const double2 pa = __ldg(M.m_p1 + 2 * m), pb = __ldg(M.m_p1 + 2 * m + 1);
         const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
@@ -546,16 +548,28 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
         if constexpr (NSEG > 0) {
             float tq[NSEG];
             int sl[NSEG];
+            const int4 i4 = __ldg(M.m_info4 + m);
 #pragma unroll
             for (int k = 0; k < NSEG; ++k) {
                 const int at = k * nm + m;
-                const int info = __ldg(M.seg_info + at);
+                const int info = k == 0 ? i4.x : (k == 1 ? i4.y : (k == 2 ? i4.z : i4.w));
+#ifndef MSK_NO_KFORM
+                // |s|^2 = K1 + 2 (c K2h + s K3h); r x A = c K3h - s K2h.  Same-link
+                // segments have K = (len^2, 0, 0) and padding K = 0, so no branch.
+                const double2 ka = __ldg(M.seg_k + 2 * at), kb = __ldg(M.seg_k + 2 * at + 1);
+                const double2 cs = S.relcs[(info >> 2) & 511];
+                const double t = fma(cs.x, ka.y, cs.y * kb.x);
+                float inv;
+                L += sqrt_d(fma(2.0, t, ka.x), inv);
+                tq[k] = static_cast<float>(fma(cs.x, kb.x, -cs.y * ka.y)) * inv;
+#else
                 const float4 g = __ldg(M.seg_geo + at);
                 float cr, inv;
                 const double len = adj_segment(S, g, info, cr, inv);
                 const bool adj = (info & 3) == 1;
                 L += adj ? len : static_cast<double>(g.x);
                 tq[k] = adj ? cr * inv : 0.0f;
+#endif
                 sl[k] = info >> 11;
             }
             const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
@@ -608,25 +622,27 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
 }
 
 // Loads an env's q, dq (f64) into the DOF-owning lanes.
-__device__ __forceinline__ void load_dofs(const DevModel& M, const double* q, const double* dq, double* qd,
-                                          double* dqd, int lane) {
+template <int QS>
+__device__ __forceinline__ void load_dofs(const DevModel& M, const EnvSmem& S, const double* q, const double* dq,
+                                          double* qd, double* dqd, int lane) {
 #pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
+    for (int k = 0; k < QS; ++k) {
+        const int d = lane + S.G * k;
         qd[k] = d < M.nq ? q[d] : 0.0;
         dqd[k] = d < M.nq ? dq[d] : 0.0;
     }
 }
 
 // f64 q into the union scratch for the Δ / observation epilogue.
+template <int QS>
 __device__ __forceinline__ double* stage_q(const DevModel& M, const EnvSmem& S, const double* qd, int lane) {
     double* qsm = reinterpret_cast<double*>(S.un);
 #pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
+    for (int k = 0; k < QS; ++k) {
+        const int d = lane + S.G * k;
         if (d < M.nq) qsm[d] = qd[k];
     }
-    __syncwarp();
+    __syncwarp(S.hm);
     return qsm;
 }
 
@@ -635,18 +651,20 @@ __device__ __forceinline__ double* stage_q(const DevModel& M, const EnvSmem& S, 
 // ============================================================================
 // step kernel: warp per env, WPB envs per block
 // ============================================================================
-template <int WPB, int MINB, int NSEG>
+template <int WPB, int MINB, int NSEG, int EPW>
 __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevState St, int env0, int n_envs,
                                                               const float* __restrict__ actions, float* obs,
                                                               float* delta, float* reward_aux, uint8_t* flags,
                                                               float* power, float* grf) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int le = blockIdx.x * WPB + warp;  // env index local to this launch
+    constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
+    const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
+    const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
+    const int le = (blockIdx.x * WPB + warp) * EPW + grp;  // env index local to this launch
     load_tree_table(smem, M);
     if (le >= n_envs) return;
     const int e = env0 + le;
-    const EnvSmem S = carve(smem, warp, M);
+    const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq, nm = M.nm, nl = M.nl, nrd = M.nrd;
     const size_t mb = static_cast<size_t>(e) * nm;
     const float* act_row = actions + static_cast<size_t>(le) * nm;
@@ -658,24 +676,24 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     }
     {
         bool bad = false;
-        for (int m = lane; m < nm; m += 32) bad |= !isfinite(act_row[m]);
-        if (__any_sync(kFull, bad)) {
+        for (int m = lane; m < nm; m += S.G) bad |= !isfinite(act_row[m]);
+        if (__any_sync(S.hm, bad)) {
             if (lane == 0 && flags) flags[le] = kFlagBadAction;
             return;
         }
     }
 
-    double qd[kMaxQSlots], dqd[kMaxQSlots];
-    load_dofs(M, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
-    publish_dofs(M, S, qd, dqd, lane);
+    double qd[QS], dqd[QS];
+    load_dofs<QS>(M, S, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
+    publish_dofs<QS>(M, S, qd, dqd, lane);
     float* pw = power ? power + static_cast<size_t>(le) * nm
                       : (M.reward_mode == 2 ? St.power_scratch + mb : nullptr);
     if (pw)
-        for (int m = lane; m < nm; m += 32) pw[m] = 0.0f;
+        for (int m = lane; m < nm; m += S.G) pw[m] = 0.0f;
     float* grf_row = grf ? grf + static_cast<size_t>(le) * 2 * nl : nullptr;
     if (grf_row)
-        for (int i = lane; i < 2 * nl; i += 32) grf_row[i] = 0.0f;
-    __syncwarp();
+        for (int i = lane; i < 2 * nl; i += S.G) grf_row[i] = 0.0f;
+    __syncwarp(S.hm);
 
     PHASE_T0();
     int diverged_at = -1;
@@ -684,13 +702,13 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
 
         // ---- 1. muscles + J_m^T F contributions ----
         muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane);
-        __syncwarp();
+        __syncwarp(S.hm);
 
         PHASE_MARK(0);
         // ---- 2. joint torques: fixed-order slot sums, damping, limits ----
 #pragma unroll
-        for (int k = 0; k < kMaxQSlots; ++k) {
-            const int d = lane + 32 * k;
+        for (int k = 0; k < QS; ++k) {
+            const int d = lane + S.G * k;
             if (d >= nrd && d < nq) {
                 const int j = d - nrd;
                 const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
@@ -716,7 +734,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 S.tau[d] = t;
             }
         }
-        __syncwarp();
+        __syncwarp(S.hm);
 
         PHASE_MARK(1);
         // ---- 3. FK + velocities + per-link articulated-body terms ----
@@ -726,7 +744,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         // ---- 4a. articulated-body pass, leaves -> root ----
         for (int lev = M.n_levels - 1; lev >= 0; --lev) {
             const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-            for (int i = lane; i < n; i += 32) {
+            for (int i = lane; i < n; i += S.G) {
                 const int l = S.tlvl[b + i];
                 const int meta = S.tmeta[l];
                 float* u = S.un + kLinkStride * l;
@@ -782,7 +800,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                     u[8] = q2;
                 }
             }
-            __syncwarp();
+            __syncwarp(S.hm);
         }
 
         PHASE_MARK(3);
@@ -809,10 +827,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
             S.tau[1] = fmaf(wd, S.dqf[0], x2);
             S.tau[2] = x0;
         }
-        __syncwarp();
+        __syncwarp(S.hm);
         for (int lev = 0; lev < M.n_levels; ++lev) {
             const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-            for (int i = lane; i < n; i += 32) {
+            for (int i = lane; i < n; i += S.G) {
                 const int l = S.tlvl[b + i];
                 const int dof = link_dof(M, l);
                 if (dof < 0) continue;
@@ -834,25 +852,25 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 u[2] = A2;
                 S.tau[dof] = qdd;
             }
-            __syncwarp();
+            __syncwarp(S.hm);
         }
 
         PHASE_MARK(4);
         // ---- 5. semi-implicit Euler (f64) + divergence check ----
         bool bad = false;
 #pragma unroll
-        for (int k = 0; k < kMaxQSlots; ++k) {
-            const int d = lane + 32 * k;
+        for (int k = 0; k < QS; ++k) {
+            const int d = lane + S.G * k;
             if (d < nq) {
                 dqd[k] += static_cast<double>(S.tau[d]) * kSimDt;
                 qd[k] += dqd[k] * kSimDt;
                 bad |= !isfinite(qd[k]) || !isfinite(dqd[k]);
             }
         }
-        __syncwarp();
-        publish_dofs(M, S, qd, dqd, lane);
-        __syncwarp();
-        if (__any_sync(kFull, bad)) {
+        __syncwarp(S.hm);
+        publish_dofs<QS>(M, S, qd, dqd, lane);
+        __syncwarp(S.hm);
+        if (__any_sync(S.hm, bad)) {
             diverged_at = sub;
             break;
         }
@@ -861,8 +879,8 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     PHASE_MARK(5);
     // ---- write back the simulation state ----
 #pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
+    for (int k = 0; k < QS; ++k) {
+        const int d = lane + S.G * k;
         if (d < nq) {
             St.q[static_cast<size_t>(e) * nq + d] = qd[k];
             St.dq[static_cast<size_t>(e) * nq + d] = dqd[k];
@@ -881,13 +899,13 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
 
     if (diverged_at >= 0) {  // env.cpp:214-229
         if (obs_row)
-            for (int i = lane; i < obs_dim; i += 32) obs_row[i] = 0.0f;
+            for (int i = lane; i < obs_dim; i += S.G) obs_row[i] = 0.0f;
         if (drow)
-            for (int i = lane; i < ddim; i += 32) drow[i] = 0.0f;
+            for (int i = lane; i < ddim; i += S.G) drow[i] = 0.0f;
         if (power)
-            for (int m = lane; m < nm; m += 32) power[static_cast<size_t>(le) * nm + m] = 0.0f;
+            for (int m = lane; m < nm; m += S.G) power[static_cast<size_t>(le) * nm + m] = 0.0f;
         if (grf_row)
-            for (int i = lane; i < 2 * nl; i += 32) grf_row[i] = 0.0f;
+            for (int i = lane; i < 2 * nl; i += S.G) grf_row[i] = 0.0f;
         if (lane == 0) {
             if (reward_aux) reward_aux[le] = 0.0f;
             if (flags) flags[le] = kFlagDone | kFlagFailed | kFlagDiverged;
@@ -906,24 +924,24 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     const int t_index = St.t_index[e] + 1;
     const int steps = St.steps[e] + 1;
     tree_sweep<false>(M, S, lane, nullptr);
-    const double* qsm = stage_q(M, S, qd, lane);
+    const double* qsm = stage_q<QS>(M, S, qd, lane);
     const bool far = write_delta(M, S, qsm, t_index, drow, lane);
     if (obs_row) write_obs(M, St, S, qsm, e, t_index, obs_row, lane);
 
     float aux = 0.0f;
     if (M.reward_mode == 1 && M.n_emg > 0) {
         float s = 0.0f;
-        for (int ch = lane; ch < M.n_emg_ch; ch += 32) {
+        for (int ch = lane; ch < M.n_emg_ch; ch += S.G) {
             const float d = static_cast<float>(M.clip_emg[static_cast<size_t>(t_index) * M.n_emg + ch]) -
                             St.act[mb + __ldg(M.emg_map + ch)];
             s = fmaf(d, d, s);
         }
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        for (int o = S.G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(S.hm, s, o);
         aux = M.n_emg_ch > 0 ? M.w_emg * (-s / static_cast<float>(M.n_emg_ch)) : 0.0f;
     } else if (M.reward_mode == 2) {
         float s = 0.0f;
-        for (int m = lane; m < nm; m += 32) s += pw[m];
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+        for (int m = lane; m < nm; m += S.G) s += pw[m];
+        for (int o = S.G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(S.hm, s, o);
         aux = M.w_power * (-s / static_cast<float>(max(1, nm)));
     }
     if (lane == 0) {
@@ -952,23 +970,25 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
 // ============================================================================
 enum ResetMode : int { kResetSample = 0, kResetFrame = 1, kResetForce = 2, kResetInit = 3 };
 
-template <int WPB, int MINB>
+template <int WPB, int MINB, int EPW>
 __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevState St, int n_envs, int mode,
                                                                const uint8_t* mask, uint8_t mask_bits,
                                                                const int* frames_in, float* obs, int* frames_out,
                                                                uint8_t* bad) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int e = blockIdx.x * WPB + warp;
+    constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
+    const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
+    const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
+    const int e = (blockIdx.x * WPB + warp) * EPW + grp;
     load_tree_table(smem, M);
     if (e >= n_envs) return;
     if (mask && !(mask[e] & mask_bits)) return;
-    const EnvSmem S = carve(smem, warp, M);
+    const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq;
     int frame = 0;
     if (mode == kResetSample) {
         if (lane == 0) frame = M.rsi ? rsi_frame(M, St, e) : 0;
-        frame = __shfl_sync(kFull, frame, 0);
+        frame = __shfl_sync(S.hm, frame, 0, S.G);
     } else if (mode == kResetFrame) {
         frame = frames_in[e];
         if (frame < 0 || frame >= M.frames - 1) {  // ContractError in env.cpp:96-97
@@ -979,19 +999,19 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     } else if (mode == kResetForce) {
         frame = St.t_index[e];
     }  // kResetInit: frame 0 (Env::Env, env.cpp:86)
-    double qd[kMaxQSlots], dqd[kMaxQSlots];
-    load_dofs(M, M.clip_q + static_cast<size_t>(frame) * nq, M.clip_dq + static_cast<size_t>(frame) * nq, qd, dqd,
+    double qd[QS], dqd[QS];
+    load_dofs<QS>(M, S, M.clip_q + static_cast<size_t>(frame) * nq, M.clip_dq + static_cast<size_t>(frame) * nq, qd, dqd,
               lane);
 #pragma unroll
-    for (int k = 0; k < kMaxQSlots; ++k) {
-        const int d = lane + 32 * k;
+    for (int k = 0; k < QS; ++k) {
+        const int d = lane + S.G * k;
         if (d < nq) {
             St.q[static_cast<size_t>(e) * nq + d] = qd[k];
             St.dq[static_cast<size_t>(e) * nq + d] = dqd[k];
         }
     }
-    publish_dofs(M, S, qd, dqd, lane);
-    __syncwarp();
+    publish_dofs<QS>(M, S, qd, dqd, lane);
+    __syncwarp(S.hm);
     tree_sweep<false>(M, S, lane, nullptr);
     init_muscles(M, St, S, e, lane);
     if (lane == 0) {
@@ -1010,28 +1030,30 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
         if (frames_out) frames_out[e] = frame;
     }
     if (obs) {
-        const double* qsm = stage_q(M, S, qd, lane);
+        const double* qsm = stage_q<QS>(M, S, qd, lane);
         const int obs_dim = 3 * nq + 6 * M.nk + 4 * M.nm;
         write_obs(M, St, S, qsm, e, frame, obs + static_cast<size_t>(e) * obs_dim, lane);
     }
 }
 
-template <int WPB, int MINB>
+template <int WPB, int MINB, int EPW>
 __global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, DevState St, int n_envs, float* obs,
                                                                  float* delta) {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int e = blockIdx.x * WPB + warp;
+    constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
+    const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
+    const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
+    const int e = (blockIdx.x * WPB + warp) * EPW + grp;
     load_tree_table(smem, M);
     if (e >= n_envs) return;
-    const EnvSmem S = carve(smem, warp, M);
+    const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq;
-    double qd[kMaxQSlots], dqd[kMaxQSlots];
-    load_dofs(M, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
-    publish_dofs(M, S, qd, dqd, lane);
-    __syncwarp();
+    double qd[QS], dqd[QS];
+    load_dofs<QS>(M, S, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
+    publish_dofs<QS>(M, S, qd, dqd, lane);
+    __syncwarp(S.hm);
     tree_sweep<false>(M, S, lane, nullptr);
-    const double* qsm = stage_q(M, S, qd, lane);
+    const double* qsm = stage_q<QS>(M, S, qd, lane);
     const int t_index = St.t_index[e];
     if (delta) write_delta(M, S, qsm, t_index, delta + static_cast<size_t>(e) * (3 + M.nj + 2 * M.nk), lane);
     if (obs) write_obs(M, St, S, qsm, e, t_index, obs + static_cast<size_t>(e) * (3 * nq + 6 * M.nk + 4 * M.nm), lane);
@@ -1206,25 +1228,31 @@ double measure_fp32_peak_tflops() {
 // ============================================================================
 // host-side launch wrappers
 // ============================================================================
+#ifndef MSK_EPW
+#define MSK_EPW 1   // envs per warp: 1 (32 lanes per env) or 2 (16 lanes per env)
+#endif
 #ifndef MSK_WPB
-#define MSK_WPB 7   // envs (warps) per block
+#define MSK_WPB 7   // warps per block
 #endif
 #ifndef MSK_MINB
-#define MSK_MINB 4  // blocks per SM: 28 envs resident -> 4096 envs in one wave, <= 72 regs
+#define MSK_MINB (4 / MSK_EPW)  // blocks per SM: 28 envs resident -> 4096 envs in one wave
 #endif
+constexpr int kEPW = MSK_EPW;
 constexpr int kWPB = MSK_WPB;
 constexpr int kMinB = MSK_MINB;
+constexpr int kEnvsPerBlock = kWPB * kEPW;
 
 // Fast-path segment count for a model (0 = generic path).
 int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 && M.max_seg <= 4) ? M.max_seg : 0; }
 
 template <int NSEG>
 cudaError_t set_step_smem(int bytes) {
-    return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG, kEPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                bytes);
 }
 
 size_t block_smem(const DevModel& M) {
-    return static_cast<size_t>(M.tab_bytes) + static_cast<size_t>(kWPB) * M.smem_env_bytes;
+    return static_cast<size_t>(M.tab_bytes) + static_cast<size_t>(kEnvsPerBlock) * M.smem_env_bytes;
 }
 
 cudaError_t prepare_kernels(int smem_bytes_per_block) {
@@ -1234,22 +1262,22 @@ cudaError_t prepare_kernels(int smem_bytes_per_block) {
     if ((err = set_step_smem<2>(smem_bytes_per_block)) != cudaSuccess) return err;
     if ((err = set_step_smem<3>(smem_bytes_per_block)) != cudaSuccess) return err;
     if ((err = set_step_smem<4>(smem_bytes_per_block)) != cudaSuccess) return err;
-    if ((err = cudaFuncSetAttribute(reset_kernel<kWPB, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if ((err = cudaFuncSetAttribute(reset_kernel<kWPB, kMinB, kEPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes_per_block)) != cudaSuccess)
         return err;
-    return cudaFuncSetAttribute(observe_kernel<kWPB, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(observe_kernel<kWPB, kMinB, kEPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_bytes_per_block);
 }
 
-int envs_per_block() { return kWPB; }
+int envs_per_block() { return kEnvsPerBlock; }
 
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
                  float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s) {
-    const int blocks = (n + kWPB - 1) / kWPB;
+    const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
     const size_t smem = block_smem(M);
-#define MSK_STEP(NS)                                                                                          \
-    step_kernel<kWPB, kMinB, NS><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux, flags, \
-                                                                 power, grf)
+#define MSK_STEP(NS)                                                                                            \
+    step_kernel<kWPB, kMinB, NS, kEPW><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux, \
+                                                                       flags, power, grf)
     switch (step_variant(M)) {
         case 1: MSK_STEP(1); break;
         case 2: MSK_STEP(2); break;
@@ -1262,14 +1290,14 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
 
 void launch_reset(const DevModel& M, const DevState& St, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t s) {
-    const int blocks = (n + kWPB - 1) / kWPB;
-    reset_kernel<kWPB, kMinB><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, mode, mask, bits, frames_in,
-                                                                          obs, frames_out, bad);
+    const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
+    reset_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, mode, mask, bits, frames_in,
+                                                                                obs, frames_out, bad);
 }
 
 void launch_observe(const DevModel& M, const DevState& St, int n, float* obs, float* delta, cudaStream_t s) {
-    const int blocks = (n + kWPB - 1) / kWPB;
-    observe_kernel<kWPB, kMinB><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, obs, delta);
+    const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
+    observe_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, obs, delta);
 }
 
 void launch_seed(const DevState& St, int n, uint64_t base_seed, cudaStream_t s) {
