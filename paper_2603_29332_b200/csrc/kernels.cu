@@ -280,10 +280,10 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
                     s = fmaf(kp.y, cr, kp.x * sr);
                     if (kFull) {
                         const float* up = S.un + kLinkStride * p;
-                        const float wp = up[9];
-                        w = wp + S.dqf[dof];
-                        vx = fmaf(-wp, oz - kp.w, up[10]);
-                        vz = fmaf(wp, ox - kp.z, up[11]);
+                        const float2 wv = reinterpret_cast<const float2*>(up)[5];  // parent (omega, v_x)
+                        w = wv.x + S.dqf[dof];
+                        vx = fmaf(-wv.x, oz - kp.w, wv.y);
+                        vz = fmaf(wv.x, ox - kp.z, up[9]);
                     }
                 } else {
                     ox = la.x;
@@ -296,9 +296,11 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
             S.kin[l] = make_float4(c, s, ox, oz);
             if (!kFull) continue;
             float* u = S.un + kLinkStride * l;
-            u[9] = w;
-            u[10] = vx;
-            u[11] = vz;
+            // link record (14 floats): [0..5] articulated inertia, [6..8] bias force,
+            // [9] u/D, [10..11] U1/D, U2/D, [12..13] c; velocity (omega, v_x | v_z)
+            // lives in [10..11 | 9] during this sweep only
+            reinterpret_cast<float2*>(u)[5] = make_float2(w, vx);
+            u[9] = vz;
             const float m = la.w, I = S.tin[l];
             const float cx = la.z * c, cz = la.z * s;
             const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
@@ -336,17 +338,13 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
                 c1 = qdot * vz;
                 c2 = -qdot * vx;
             }
-            u[0] = i00;
-            u[1] = i01;
-            u[2] = i02;
-            u[3] = m;
-            u[4] = 0.0f;
-            u[5] = m;
-            u[6] = p0;
-            u[7] = p1;
+            float2* u2 = reinterpret_cast<float2*>(u);  // 8-B aligned (stride 14 floats)
+            u2[0] = make_float2(i00, i01);
+            u2[1] = make_float2(i02, m);
+            u2[2] = make_float2(0.0f, m);
+            u2[3] = make_float2(p0, p1);
             u[8] = p2;
-            u[12] = c1;
-            u[13] = c2;
+            u2[6] = make_float2(c1, c2);
         }
         __syncwarp(S.hm);
     }
@@ -748,25 +746,33 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 const int l = S.tlvl[b + i];
                 const int meta = S.tmeta[l];
                 float* u = S.un + kLinkStride * l;
-                float I00 = u[0], I01 = u[1], I02 = u[2], I11 = u[3], I12 = u[4], I22 = u[5];
-                float P0 = u[6], P1 = u[7], P2 = u[8];
+                float2* u2 = reinterpret_cast<float2*>(u);
+                float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
+                float P2 = u[8];
                 const int c0 = (meta >> 16) & 0xff, c1 = c0 + ((meta >> 8) & 0xff);
                 for (int c = c0; c < c1; ++c) {
                     const float* uc = S.un + kLinkStride * S.tchild[c];
-                    I00 += uc[0];
-                    I01 += uc[1];
-                    I02 += uc[2];
-                    I11 += uc[3];
-                    I12 += uc[4];
-                    I22 += uc[5];
-                    P0 += uc[6];
-                    P1 += uc[7];
+                    const float2* uc2 = reinterpret_cast<const float2*>(uc);
+                    const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
+                    r0.x += a0.x;
+                    r0.y += a0.y;
+                    r1.x += a1.x;
+                    r1.y += a1.y;
+                    r2.x += a2.x;
+                    r2.y += a2.y;
+                    r3.x += a3.x;
+                    r3.y += a3.y;
                     P2 += uc[8];
                 }
+                const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
+                const float P0 = r3.x, P1 = r3.y;
                 const int dof = link_dof(M, l);
                 if (dof < 0) {  // floating root keeps its full articulated inertia
-                    u[0] = I00; u[1] = I01; u[2] = I02; u[3] = I11; u[4] = I12; u[5] = I22;
-                    u[6] = P0; u[7] = P1; u[8] = P2;
+                    u2[0] = r0;
+                    u2[1] = r1;
+                    u2[2] = r2;
+                    u2[3] = r3;
+                    u[8] = P2;
                     continue;
                 }
                 // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
@@ -777,26 +783,21 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
                 const float bb = fmaf(-I01, U2, I12);
                 const float cq = fmaf(-I02, U2, I22);
-                const float cv1 = u[12], cv2 = u[13];
+                const float2 cv = u2[6];
                 // pa = pA + Ia c + U u / D   (pa[0] = tau)
-                const float q1 = fmaf(I01, uu, fmaf(a, cv1, fmaf(bb, cv2, P1)));
-                const float q2 = fmaf(I02, uu, fmaf(bb, cv1, fmaf(cq, cv2, P2)));
+                const float q1 = fmaf(I01, uu, fmaf(a, cv.x, fmaf(bb, cv.y, P1)));
+                const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
                 u[9] = uu;
-                u[10] = U1;
-                u[11] = U2;
+                u2[5] = make_float2(U1, U2);
                 const int p = (meta & 0xff) - 1;
                 if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
                     const float4 kl = S.kin[l], kp = S.kin[p];
                     const float dx = kl.z - kp.z, dz = kl.w - kp.w;
                     const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
-                    u[0] = fmaf(-dz, al, be * dx);
-                    u[1] = al;
-                    u[2] = be;
-                    u[3] = a;
-                    u[4] = bb;
-                    u[5] = cq;
-                    u[6] = fmaf(-dz, q1, fmaf(dx, q2, t));
-                    u[7] = q1;
+                    u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
+                    u2[1] = make_float2(be, a);
+                    u2[2] = make_float2(bb, cq);
+                    u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
                     u[8] = q2;
                 }
             }
@@ -836,19 +837,23 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
                 if (dof < 0) continue;
                 float* u = S.un + kLinkStride * l;
                 const int p = (S.tmeta[l] & 0xff) - 1;
-                float A0 = 0.0f, A1 = u[12], A2 = u[13];
+                float2* u2 = reinterpret_cast<float2*>(u);
+                const float2 cv = u2[6];
+                float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
                 if (p >= 0) {
                     const float* up = S.un + kLinkStride * p;
+                    const float2 a01 = reinterpret_cast<const float2*>(up)[0];
+                    const float a2 = up[2];
                     const float4 kl = S.kin[l], kp = S.kin[p];
                     const float dx = kl.z - kp.z, dz = kl.w - kp.w;
-                    A0 = up[0];
-                    A1 += fmaf(-up[0], dz, up[1]);
-                    A2 += fmaf(up[0], dx, up[2]);
+                    A0 = a01.x;
+                    A1 += fmaf(-a01.x, dz, a01.y);
+                    A2 += fmaf(a01.x, dx, a2);
                 }
                 // q̈ = (u - U^T A) / D with U0 = D
-                const float qdd = u[9] - A0 - fmaf(u[10], A1, u[11] * A2);
-                u[0] = A0 + qdd;
-                u[1] = A1;
+                const float2 U = u2[5];
+                const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
+                u2[0] = make_float2(A0 + qdd, A1);
                 u[2] = A2;
                 S.tau[dof] = qdd;
             }
