@@ -188,27 +188,38 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             for (int s = 0; s < c.ns; ++s) sp[s] = make_float4(c.sphere_x[s], c.sphere_z[s], c.sphere_r[s], 0.f);
             M.link_a = ctx->upload(la);
             M.sphere = ctx->upload(sp);
-            std::vector<float4> p0(c.nm), geo(static_cast<size_t>(c.max_seg) * c.nm);
-            std::vector<double2> p1(2 * static_cast<size_t>(c.nm));
+            const size_t nsg = static_cast<size_t>(c.max_seg) * c.nm;
+            std::vector<float4> p0(c.nm), kf(nsg);
+            std::vector<double2> p1a(c.nm), p1b(c.nm);
             for (int m = 0; m < c.nm; ++m) {
                 p0[m] = make_float4(c.pk_p0[4 * m], c.pk_p0[4 * m + 1], c.pk_p0[4 * m + 2], c.pk_p0[4 * m + 3]);
-                p1[2 * m] = make_double2(c.pk_p1[4 * m], c.pk_p1[4 * m + 1]);
-                p1[2 * m + 1] = make_double2(c.pk_p1[4 * m + 2], c.pk_p1[4 * m + 3]);
+                p1a[m] = make_double2(c.pk_p1[4 * m], c.pk_p1[4 * m + 1]);
+                p1b[m] = make_double2(c.pk_p1[4 * m + 2], c.pk_p1[4 * m + 3]);
             }
-            for (size_t i = 0; i < geo.size(); ++i)
-                geo[i] = make_float4(c.pk_geo[4 * i], c.pk_geo[4 * i + 1], c.pk_geo[4 * i + 2], c.pk_geo[4 * i + 3]);
+            // |A + R c|^2 = |A|^2 + |c|^2 + 2 (cos A.c + sin (A_z c_x - A_x c_z)).  The
+            // K constants are rounded to f32 once (a fixed ~1e-8 relative perturbation of
+            // the geometry); reset and step both evaluate lengths from these same values,
+            // so the fibre-velocity difference L - prev_len sees no mismatch.
+            for (size_t i = 0; i < nsg; ++i) {
+                const double ax = c.pk_geo[4 * i], az = c.pk_geo[4 * i + 1];
+                const double cx = c.pk_geo[4 * i + 2], cz = c.pk_geo[4 * i + 3];
+                const int info = c.pk_info[i], kind = info & 3;
+                float k1 = 0.f, k2 = 0.f, k3 = 0.f;
+                if (kind == 0) {
+                    k1 = static_cast<float>(ax * ax);  // same-link: constant length in ax
+                } else if (kind == 1) {
+                    k1 = static_cast<float>(ax * ax + az * az + cx * cx + cz * cz);
+                    k2 = static_cast<float>(ax * cx + az * cz);
+                    k3 = static_cast<float>(az * cx - ax * cz);
+                }
+                float w;
+                std::memcpy(&w, &info, sizeof w);
+                kf[i] = make_float4(k1, k2, k3, w);
+            }
             M.m_p0 = ctx->upload(p0);
-            M.m_p1 = ctx->upload(p1);
-            M.seg_geo = ctx->upload(geo);
-            // |A + R c|^2 = |A|^2 + |c|^2 + 2 (cos A.c + sin (A_z c_x - A_x c_z)), from the
-            // same f32-rounded constants the generic path uses
-            std::vector<double2> kk(2 * geo.size());
-            for (size_t i = 0; i < geo.size(); ++i) {
-                const double ax = geo[i].x, az = geo[i].y, cx = geo[i].z, cz = geo[i].w;
-                kk[2 * i] = make_double2(ax * ax + az * az + cx * cx + cz * cz, ax * cx + az * cz);
-                kk[2 * i + 1] = make_double2(az * cx - ax * cz, 0.0);
-            }
-            M.seg_k = ctx->upload(kk);
+            M.m_p1a = ctx->upload(p1a);
+            M.m_p1b = ctx->upload(p1b);
+            M.seg_kf = ctx->upload(kf);
         }
         M.max_seg = c.max_seg;
         M.has_general = c.has_general;
@@ -227,7 +238,6 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.joint_slot_start = ctx->upload(c.joint_slot_start);
         M.m_meta = ctx->upload(c.pk_meta);
         M.seg_info = ctx->upload(c.pk_info);
-        M.m_info4 = reinterpret_cast<const int4*>(ctx->upload(c.pk_info4));
         M.m_pair_start = ctx->upload(c.m_pair_start);
         M.via_link = ctx->upload(c.via_link);
         M.via_x = ctx->upload(c.via_x);

@@ -47,13 +47,14 @@ struct DevModel {
     const int* joint_slot_start;
     // muscles (packed; see CompiledModel)
     const float4* m_p0;    // {f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max / 10}
-    const double2* m_p1;   // 2 per muscle: {slack, l_opt}, {1/l_opt, 1/(dt l_opt v_max)}
+    const double2* m_p1a;  // {slack, l_opt}
+    const double2* m_p1b;  // {1/l_opt, 1/(dt l_opt v_max)}
     const int* m_meta;     // nseg | general << 8
-    const float4* seg_geo; // [k * nm + m] {ax, az, cx, cz}
-    // fast path: |s|^2 = K1 + 2 (cos K2h + sin K3h), r x A = cos K3h - sin K2h
-    const double2* seg_k;  // 2 per segment at [2 (k * nm + m)]: {K1, K2h}, {K3h, 0}
+    // Same-link / adjacent segment k of muscle m at [k * nm + m] (coalesced over m):
+    // {K1, K2h, K3h, info bits} with |s|^2 = K1 + 2 (cos K2h + sin K3h) and
+    // r x A = cos K3h - sin K2h (cos/sin of the child joint's own angle, f64).
+    const float4* seg_kf;
     const int* seg_info;   // [k * nm + m] kind | dof << 2 | slot << 11
-    const int4* m_info4;   // [m] infos of segments 0..3 (fast path, one 16-B load)
     // general (non-adjacent) segments, world frame
     const int* m_pair_start;
     const int* via_link;

@@ -149,27 +149,18 @@ __device__ __forceinline__ float general_seg_len(const DevModel& M, const EnvSme
     return sqrtf(fmaf(dx, dx, dz * dz));
 }
 
-// Adjacent segment in its parent's frame: s = A + R(joint) c.  Returns |s|
-// (f64), 1/|s| and the cross product r x A (r = R c) that sets the moment arm.
-__device__ __forceinline__ double adj_segment(const EnvSmem& S, float4 g, int info, float& cross, float& inv) {
-#ifdef MSK_FP32_GEOM  // experiment: f32 segment geometry (precision study only)
-    {
-        const double2 cd = S.relcs[(info >> 2) & 511];
-        const float c = static_cast<float>(cd.x), s = static_cast<float>(cd.y);
-        const float rx = fmaf(c, g.z, -s * g.w), rz = fmaf(s, g.z, c * g.w);
-        const float sx = g.x + rx, sz = g.y + rz;
-        cross = fmaf(rx, g.y, -rz * g.x);
-        const float x = fmaf(sx, sx, sz * sz);
-        inv = rsqrtf(x);
-        return static_cast<double>(x * inv);
-    }
-#endif
+// Same-link (kind 0) or adjacent (kind 1) segment from its K constants
+// (device.cuh seg_kf), evaluated in the parent's frame with the child joint's
+// own f64 rotation: |s|^2 = K1 + 2 (c K2h + s K3h).  Returns |s| (f64) and the
+// moment-arm factor (r x A) / |s| about the child joint.  Same-link segments
+// have K = (len^2, 0, 0) and padding K = 0, so neither needs a branch.
+__device__ __forceinline__ double kseg(const EnvSmem& S, float4 k, int info, float& arm) {
     const double2 cs = S.relcs[(info >> 2) & 511];
-    const double rx = fma(cs.x, static_cast<double>(g.z), -cs.y * static_cast<double>(g.w));
-    const double rz = fma(cs.y, static_cast<double>(g.z), cs.x * static_cast<double>(g.w));
-    const double sx = g.x + rx, sz = g.y + rz;
-    cross = static_cast<float>(fma(rx, static_cast<double>(g.y), -rz * static_cast<double>(g.x)));
-    return sqrt_d(fma(sx, sx, sz * sz), inv);
+    const double k2 = k.y, k3 = k.z;
+    float inv;
+    const double len = sqrt_d(fma(2.0, fma(cs.x, k2, cs.y * k3), static_cast<double>(k.x)), inv);
+    arm = static_cast<float>(fma(cs.x, k3, -cs.y * k2)) * inv;
+    return len;
 }
 
 // Path length of muscle m (skeleton.cpp:129-141) — used by make_initial_state.
@@ -177,17 +168,10 @@ __device__ __forceinline__ double muscle_length(const DevModel& M, const EnvSmem
     const int nseg = __ldg(M.m_meta + m) & 0xff;
     double L = 0.0;
     for (int k = 0; k < nseg; ++k) {
-        const int at = k * M.nm + m;
-        const int info = __ldg(M.seg_info + at);
-        const float4 g = __ldg(M.seg_geo + at);
-        const int kind = info & 3;
-        float cr, inv;
-        if (kind == 0)
-            L += g.x;
-        else if (kind == 1)
-            L += adj_segment(S, g, info, cr, inv);
-        else
-            L += general_seg_len(M, S, info >> 11);
+        const float4 kf = __ldg(M.seg_kf + k * M.nm + m);
+        const int info = __float_as_int(kf.w);
+        float arm;
+        L += (info & 3) == 2 ? static_cast<double>(general_seg_len(M, S, info >> 11)) : kseg(S, kf, info, arm);
     }
     return L;
 }
@@ -458,7 +442,7 @@ __device__ void init_muscles(const DevModel& M, const DevState& St, const EnvSme
     const size_t mb = static_cast<size_t>(e) * M.nm;
     const float a0 = static_cast<float>(M.init_act);
     for (int m = lane; m < M.nm; m += S.G) {
-        const double2 pa = __ldg(M.m_p1 + 2 * m), pb = __ldg(M.m_p1 + 2 * m + 1);
+        const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
         const double L = muscle_length(M, S, m);
         const float lm = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
         St.act[mb + m] = a0;
@@ -535,7 +519,7 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
     const int nm = M.nm;
     for (int m = lane; m < nm; m += S.G) {
         const float4 p0 = __ldg(M.m_p0 + m);  // f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max/10
-        const double2 pa = __ldg(M.m_p1 + 2 * m), pb = __ldg(M.m_p1 + 2 * m + 1);
+        const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
         const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
         const float a0 = St.act[mb + m];
         const float lm0 = St.lm[mb + m];
@@ -546,28 +530,11 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
         if constexpr (NSEG > 0) {
             float tq[NSEG];
             int sl[NSEG];
-            const int4 i4 = __ldg(M.m_info4 + m);
 #pragma unroll
             for (int k = 0; k < NSEG; ++k) {
-                const int at = k * nm + m;
-                const int info = k == 0 ? i4.x : (k == 1 ? i4.y : (k == 2 ? i4.z : i4.w));
-#ifndef MSK_NO_KFORM
-                // |s|^2 = K1 + 2 (c K2h + s K3h); r x A = c K3h - s K2h.  Same-link
-                // segments have K = (len^2, 0, 0) and padding K = 0, so no branch.
-                const double2 ka = __ldg(M.seg_k + 2 * at), kb = __ldg(M.seg_k + 2 * at + 1);
-                const double2 cs = S.relcs[(info >> 2) & 511];
-                const double t = fma(cs.x, ka.y, cs.y * kb.x);
-                float inv;
-                L += sqrt_d(fma(2.0, t, ka.x), inv);
-                tq[k] = static_cast<float>(fma(cs.x, kb.x, -cs.y * ka.y)) * inv;
-#else
-                const float4 g = __ldg(M.seg_geo + at);
-                float cr, inv;
-                const double len = adj_segment(S, g, info, cr, inv);
-                const bool adj = (info & 3) == 1;
-                L += adj ? len : static_cast<double>(g.x);
-                tq[k] = adj ? cr * inv : 0.0f;
-#endif
+                const float4 kf = __ldg(M.seg_kf + k * nm + m);
+                const int info = __float_as_int(kf.w);
+                L += kseg(S, kf, info, tq[k]);
                 sl[k] = info >> 11;
             }
             const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
@@ -585,17 +552,10 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
             const int meta = __ldg(M.m_meta + m);
             const int nseg = meta & 0xff;
             for (int k = 0; k < nseg; ++k) {
-                const int at = k * nm + m;
-                const int info = __ldg(M.seg_info + at);
-                const float4 g = __ldg(M.seg_geo + at);
-                const int kind = info & 3;
-                float cr, inv;
-                if (kind == 1)
-                    L += adj_segment(S, g, info, cr, inv);
-                else if (kind == 0)
-                    L += g.x;
-                else
-                    L += general_seg_len(M, S, info >> 11);
+                const float4 kf = __ldg(M.seg_kf + k * nm + m);
+                const int info = __float_as_int(kf.w);
+                float arm;
+                L += (info & 3) == 2 ? static_cast<double>(general_seg_len(M, S, info >> 11)) : kseg(S, kf, info, arm);
             }
             const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
             const float vm = static_cast<float>((L - prev_len) * pb.y);
@@ -607,12 +567,12 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
             St.fm[mb + m] = F;
             if (pw) pw[m] += fabsf(F * vm * p0.w);
             for (int k = 0; k < nseg; ++k) {
-                const int at = k * nm + m;
-                const int info = __ldg(M.seg_info + at);
+                const float4 kf = __ldg(M.seg_kf + k * nm + m);
+                const int info = __float_as_int(kf.w);
                 if ((info & 3) != 1) continue;
-                float cr, inv;
-                adj_segment(S, __ldg(M.seg_geo + at), info, cr, inv);
-                S.un[info >> 11] = -F * cr * inv;
+                float arm;
+                kseg(S, kf, info, arm);
+                S.un[info >> 11] = -F * arm;
             }
             if (meta >> 8) general_pairs(M, S, m, F);
         }

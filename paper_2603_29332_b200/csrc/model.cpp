@@ -528,10 +528,6 @@ CompiledModel compile_model(const ModelSpec& s) {
         c.pk_meta[mi] = ns | (general << 8);
         c.has_general |= general;
     }
-    c.pk_info4.assign(4 * static_cast<size_t>(c.nm), c.n_pairs << 11);
-    for (int mi = 0; mi < c.nm; ++mi)
-        for (int k = 0; k < std::min(4, c.max_seg); ++k)
-            c.pk_info4[4 * static_cast<size_t>(mi) + k] = c.pk_info[static_cast<size_t>(k) * c.nm + mi];
     return c;
 }
 

@@ -120,7 +120,6 @@ struct CompiledModel {
     std::vector<float> pk_p0, pk_geo;
     std::vector<double> pk_p1;
     std::vector<int32_t> pk_meta, pk_info;
-    std::vector<int32_t> pk_info4;  // fast path: infos of segments 0..3 of muscle m at [4m..4m+3]
 };
 
 CompiledModel compile_model(const ModelSpec& spec);
