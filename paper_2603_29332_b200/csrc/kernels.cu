@@ -103,31 +103,50 @@ __device__ __forceinline__ int link_dof(const DevModel& M, int l) {
     return l >= M.floating ? M.nrd + l - M.floating : -1;
 }
 
+// ---- SFU helpers (flush-to-zero approximations; operands here are O(1)) ----
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
 // ---- Hill-type muscle (muscle.cpp:9-40) -----------------------------------
-__device__ __forceinline__ float hill_fl(float l) {
-    const float d = (l - 1.0f) * (1.0f / 0.45f);
-    return __expf(-d * d);
+__device__ __forceinline__ float hill_fl(float l) {  // exp(-((l-1)/0.45)^2)
+    const float d = l - 1.0f;
+    return ex2_ftz(d * d * (-kLog2e / (0.45f * 0.45f)));
 }
 __device__ __forceinline__ float hill_fv(float v) {
     if (v <= -1.0f) return 0.0f;
-    if (v < 0.0f) return __fdividef(v + 1.0f, fmaf(-0.25f, v, 1.0f));
+    if (v < 0.0f) return (v + 1.0f) * rcp_ftz(fmaf(-0.25f, v, 1.0f));
     constexpr float c = 0.32f;  // (1.4 - 1) / (1 + 1/4)
-    return __fdividef(fmaf(1.4f, v, c), v + c);
+    return fmaf(1.4f, v, c) * rcp_ftz(v + c);
 }
-__device__ __forceinline__ float hill_fp(float l) {
+__device__ __forceinline__ float hill_fp(float l) {  // (exp(4(l-1)) - 1) / (e^2 - 1)
     if (l <= 1.0f) return 0.0f;
-    return (__expf(4.0f * (l - 1.0f)) - 1.0f) * (1.0f / 6.38905609893065f);
+    return (ex2_ftz((l - 1.0f) * (4.0f * kLog2e)) - 1.0f) * (1.0f / 6.38905609893065f);
 }
 __device__ __forceinline__ float mtu_force(float act, float l, float v, float fmax) {
     return fmax * (act * hill_fl(l) * hill_fv(v) + hill_fp(l));
 }
 
 // sqrt of a non-negative f64 from the f32 rsqrt seed plus one f64 Newton
-// correction (~46 bits); also returns the f32 reciprocal length.
-// x is clamped at 1e-30 so degenerate/padding segments stay finite (|s| ~ 1e-15).
+// correction (~46 bits); also returns the f32 reciprocal length.  x is clamped
+// at ~1e-30 through its high word (one integer max; negative rounding noise has
+// the sign bit set and clamps too) so degenerate/padding segments stay finite.
 __device__ __forceinline__ double sqrt_d(double x, float& inv) {
-    x = fmax(x, 1e-30);
-    const float r = rsqrtf(static_cast<float>(x));
+    x = __hiloint2double(max(__double2hiint(x), 0x39B4484B), __double2loint(x));
+    const float r = rsqrt_ftz(static_cast<float>(x));
     inv = r;
     const double rd = static_cast<double>(r);
     const double s = x * rd;
@@ -513,59 +532,64 @@ __device__ int rsi_frame(const DevModel& M, const DevState& St, int e) {
 // moment about its child joint -F (r x A) / |A + r| into the slot table.
 // NSEG > 0: fast path for models whose segments are all adjacent/same-link
 // (segments padded to NSEG, branch-free); NSEG == 0: generic path.
+// Activation, fibre kinematics and Hill force of muscle m given its path
+// length L; stores the muscle state, accumulates power, returns F.
+__device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, int m, float4 p0, double2 pa, double2 pb,
+                                               float u, float a0, float lm0, double L, float* pw) {
+    const float gain = fmaf(1.5f, a0, 0.5f);
+    const float ex = ex2_ftz(u > a0 ? p0.y * rcp_ftz(gain) : p0.z * gain);  // p0.y/z carry log2(e)
+    const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
+    const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
+    const float vm = static_cast<float>((L - prev_len) * pb.y);
+    const float lm1 = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
+    const float F = mtu_force(a1, lm1, vm, p0.x);
+    St.act[mb + m] = a1;
+    St.lm[mb + m] = lm1;
+    St.vm[mb + m] = vm;
+    St.fm[mb + m] = F;
+    if (pw) pw[m] += fabsf(F * vm * p0.w);
+    return F;
+}
+
 template <int NSEG>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
                                              const float* act_row, size_t mb, float* pw, int lane) {
     const int nm = M.nm;
-    for (int m = lane; m < nm; m += S.G) {
-        const float4 p0 = __ldg(M.m_p0 + m);  // f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max/10
-        const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
-        const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
-        const float a0 = St.act[mb + m];
-        const float lm0 = St.lm[mb + m];
-        const float gain = fmaf(1.5f, a0, 0.5f);
-        const float ex = u > a0 ? __expf(__fdividef(p0.y, gain)) : __expf(p0.z * gain);
-        const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
-        double L = 0.0;
-        if constexpr (NSEG > 0) {
+    if constexpr (NSEG > 0) {
+        for (int m = lane; m < nm; m += S.G) {
+            float4 kc[NSEG];
+#pragma unroll
+            for (int k = 0; k < NSEG; ++k) kc[k] = __ldg(M.seg_kf + k * nm + m);
+            const float4 p0 = __ldg(M.m_p0 + m);  // f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max/10
+            const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
+            const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
+            const float a0 = St.act[mb + m];
+            const float lm0 = St.lm[mb + m];
+            double L = 0.0;
             float tq[NSEG];
-            int sl[NSEG];
 #pragma unroll
-            for (int k = 0; k < NSEG; ++k) {
-                const float4 kf = __ldg(M.seg_kf + k * nm + m);
-                const int info = __float_as_int(kf.w);
-                L += kseg(S, kf, info, tq[k]);
-                sl[k] = info >> 11;
-            }
-            const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
-            const float vm = static_cast<float>((L - prev_len) * pb.y);
-            const float lm1 = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
-            const float F = mtu_force(a1, lm1, vm, p0.x);
-            St.act[mb + m] = a1;
-            St.lm[mb + m] = lm1;
-            St.vm[mb + m] = vm;
-            St.fm[mb + m] = F;
-            if (pw) pw[m] += fabsf(F * vm * p0.w);
+            for (int k = 0; k < NSEG; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
+            const float F = muscle_update(St, mb, m, p0, pa, pb, u, a0, lm0, L, pw);
 #pragma unroll
-            for (int k = 0; k < NSEG; ++k) S.un[sl[k]] = -F * tq[k];
-        } else {
+            for (int k = 0; k < NSEG; ++k) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
+        }
+    } else {
+        for (int m = lane; m < nm; m += S.G) {
+            const float4 p0 = __ldg(M.m_p0 + m);
+            const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
+            const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
+            const float a0 = St.act[mb + m];
+            const float lm0 = St.lm[mb + m];
             const int meta = __ldg(M.m_meta + m);
             const int nseg = meta & 0xff;
+            double L = 0.0;
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
                 const int info = __float_as_int(kf.w);
                 float arm;
                 L += (info & 3) == 2 ? static_cast<double>(general_seg_len(M, S, info >> 11)) : kseg(S, kf, info, arm);
             }
-            const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
-            const float vm = static_cast<float>((L - prev_len) * pb.y);
-            const float lm1 = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
-            const float F = mtu_force(a1, lm1, vm, p0.x);
-            St.act[mb + m] = a1;
-            St.lm[mb + m] = lm1;
-            St.vm[mb + m] = vm;
-            St.fm[mb + m] = F;
-            if (pw) pw[m] += fabsf(F * vm * p0.w);
+            const float F = muscle_update(St, mb, m, p0, pa, pb, u, a0, lm0, L, pw);
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
                 const int info = __float_as_int(kf.w);

@@ -398,8 +398,9 @@ CompiledModel compile_model(const ModelSpec& s) {
         c.m_inv_lopt.push_back(1.0 / m.l_opt);
         c.m_slack.push_back(m.slack);
         c.m_kv.push_back(1.0 / (dt * m.l_opt * m.v_max));
-        c.m_ndt_act.push_back(static_cast<float>(-dt / m.tau_act));
-        c.m_ndt_deact.push_back(static_cast<float>(-dt / m.tau_deact));
+        // exp(-dt/tau) is evaluated as exp2: the constants carry log2(e)
+        c.m_ndt_act.push_back(static_cast<float>(-dt / m.tau_act * 1.4426950408889634));
+        c.m_ndt_deact.push_back(static_cast<float>(-dt / m.tau_deact * 1.4426950408889634));
         c.m_pw.push_back(static_cast<float>(m.l_opt * m.v_max / 10.0));
         const int v0 = static_cast<int>(c.via_link.size());
         for (const auto& v : m.vias) {
