@@ -29,6 +29,7 @@ void launch_broadcast_ema(const DevState&, int n, int bins, const double* row, c
 void launch_drain(const DevState&, int n, int cap, int* bins, uint8_t* failed, int* counts, cudaStream_t);
 void launch_get_ints(const DevState&, int n, int* ints, cudaStream_t);
 void launch_set_ints(const DevState&, int n, const int* ints, cudaStream_t);
+void launch_permute_muscles(const DevModel&, int n, const float* src, float* dst, int to_internal, cudaStream_t);
 void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint32_t step, float* out,
                         cudaStream_t);
 double measure_fp32_peak_tflops();
@@ -263,7 +264,9 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.init_act = ec.init_activation;
         M.w_emg = static_cast<float>(rw.w_emg);
         M.w_power = static_cast<float>(rw.w_power);
-        M.emg_map = ctx->upload(emg_map);
+        std::vector<int32_t> emg_int(emg_map.size());  // channel -> internal muscle index
+        for (size_t ch = 0; ch < emg_map.size(); ++ch) emg_int[ch] = c.m_int[emg_map[ch]];
+        M.emg_map = ctx->upload(emg_int);
         // per-env shared-memory layout (~8 KB for the whole-body model)
         int off = 16 * c.nl;  // kin
         M.off_relcs = off;
@@ -503,17 +506,21 @@ int msk_gpu_force_state_to_reference(msk_gpu_ctx* ctx, void* stream) {
 int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float* l_m, float* v_m, float* f_m,
                       double* t, int32_t* ints, void* stream) {
     return guarded(ctx, [&] {
-        const size_t E = ctx->n_envs, nq = ctx->cm.nq, nm = ctx->cm.nm;
+        const size_t E = ctx->n_envs, nq = ctx->cm.nq;
         cudaStream_t s = as_stream(stream);
         auto cp = [&](void* dst, const void* src, size_t bytes) {
             if (dst) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s), "get_state");
         };
         cp(q, ctx->St.q, E * nq * 8);
         cp(dq, ctx->St.dq, E * nq * 8);
-        cp(act, ctx->St.act, E * nm * 4);
-        cp(l_m, ctx->St.lm, E * nm * 4);
-        cp(v_m, ctx->St.vm, E * nm * 4);
-        cp(f_m, ctx->St.fm, E * nm * 4);
+        // muscle rows: internal (segment-count) order -> reference order
+        for (auto [dst, src] : {std::pair<float*, const float*>{act, ctx->St.act}, {l_m, ctx->St.lm},
+                                {v_m, ctx->St.vm}, {f_m, ctx->St.fm}})
+            if (dst) {
+                launch_permute_muscles(ctx->M, ctx->n_envs, src, dst, 0, s);
+                ctx->count();
+                ctx->check_launch();
+            }
         cp(t, ctx->St.t, E * 8);
         if (ints) {
             launch_get_ints(ctx->St, ctx->n_envs, ints, s);
@@ -526,17 +533,20 @@ int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float
 int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const float* l_m,
                       const float* v_m, const float* f_m, const double* t, const int32_t* ints, void* stream) {
     return guarded(ctx, [&] {
-        const size_t E = ctx->n_envs, nq = ctx->cm.nq, nm = ctx->cm.nm;
+        const size_t E = ctx->n_envs, nq = ctx->cm.nq;
         cudaStream_t s = as_stream(stream);
         auto cp = [&](void* dst, const void* src, size_t bytes) {
             if (src) ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s), "set_state");
         };
         cp(ctx->St.q, q, E * nq * 8);
         cp(ctx->St.dq, dq, E * nq * 8);
-        cp(ctx->St.act, act, E * nm * 4);
-        cp(ctx->St.lm, l_m, E * nm * 4);
-        cp(ctx->St.vm, v_m, E * nm * 4);
-        cp(ctx->St.fm, f_m, E * nm * 4);
+        for (auto [dst, src] : {std::pair<float*, const float*>{ctx->St.act, act}, {ctx->St.lm, l_m},
+                                {ctx->St.vm, v_m}, {ctx->St.fm, f_m}})
+            if (src) {
+                launch_permute_muscles(ctx->M, ctx->n_envs, src, dst, 1, s);
+                ctx->count();
+                ctx->check_launch();
+            }
         cp(ctx->St.t, t, E * 8);
         if (ints) {
             launch_set_ints(ctx->St, ctx->n_envs, ints, s);

@@ -121,6 +121,27 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 }
 constexpr float kLog2e = 1.4426950408889634f;
 
+// Read-only model-constant loads.  MSK_L1_KEEP marks them evict_last in L1 so
+// the per-env state stream does not push them out (A/B experiment).
+__device__ __forceinline__ float4 ldc4(const float4* p) {
+#ifdef MSK_L1_KEEP
+    float4 v;
+    asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ double2 ldc2d(const double2* p) {
+#ifdef MSK_L1_KEEP
+    double2 v;
+    asm("ld.global.nc.L1::evict_last.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // ---- Hill-type muscle (muscle.cpp:9-40) -----------------------------------
 __device__ __forceinline__ float hill_fl(float l) {  // exp(-((l-1)/0.45)^2)
     const float d = l - 1.0f;
@@ -195,7 +216,7 @@ __device__ __forceinline__ double muscle_length(const DevModel& M, const EnvSmem
     return L;
 }
 
-// J_m^T F of the general (non-adjacent) segments of muscle m, world frame.
+// J_m^T F of the general (non-adjacent) segments of muscle m (reference index), world frame.
 __device__ void general_pairs(const DevModel& M, const EnvSmem& S, int m, float F) {
     const int p0 = __ldg(M.m_pair_start + m), p1 = __ldg(M.m_pair_start + m + 1);
     for (int p = p0; p < p1; ++p) {
@@ -409,11 +430,12 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
     }
     o += 3 * nk;
     const size_t mb = static_cast<size_t>(e) * nm;
-    for (int i = lane; i < nm; i += S.G) {
-        obs_row[o + i] = St.act[mb + i];
-        obs_row[o + nm + i] = St.fm[mb + i];
-        obs_row[o + 2 * nm + i] = St.lm[mb + i];
-        obs_row[o + 3 * nm + i] = St.vm[mb + i];
+    for (int i = lane; i < nm; i += S.G) {  // internal muscle i -> reference slot
+        const int x = __ldg(M.m_meta + i) >> 9;
+        obs_row[o + x] = St.act[mb + i];
+        obs_row[o + nm + x] = St.fm[mb + i];
+        obs_row[o + 2 * nm + x] = St.lm[mb + i];
+        obs_row[o + 3 * nm + x] = St.vm[mb + i];
     }
     o += 4 * nm;
     const size_t t = static_cast<size_t>(t_index);
@@ -534,8 +556,8 @@ __device__ int rsi_frame(const DevModel& M, const DevState& St, int e) {
 // (segments padded to NSEG, branch-free); NSEG == 0: generic path.
 // Activation, fibre kinematics and Hill force of muscle m given its path
 // length L; stores the muscle state, accumulates power, returns F.
-__device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, int m, float4 p0, double2 pa, double2 pb,
-                                               float u, float a0, float lm0, double L, float* pw) {
+__device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, int m, int ext, float4 p0, double2 pa,
+                                               double2 pb, float u, float a0, float lm0, double L, float* pw) {
     const float gain = fmaf(1.5f, a0, 0.5f);
     const float ex = ex2_ftz(u > a0 ? p0.y * rcp_ftz(gain) : p0.z * gain);  // p0.y/z carry log2(e)
     const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
@@ -547,7 +569,7 @@ __device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, in
     St.lm[mb + m] = lm1;
     St.vm[mb + m] = vm;
     St.fm[mb + m] = F;
-    if (pw) pw[m] += fabsf(F * vm * p0.w);
+    if (pw) pw[ext] += fabsf(F * vm * p0.w);
     return F;
 }
 
@@ -557,31 +579,38 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
     const int nm = M.nm;
     if constexpr (NSEG > 0) {
         for (int m = lane; m < nm; m += S.G) {
+            // muscles are sorted by segment count: the warp's chunk pads to the
+            // count of its last muscle (a warp-uniform bound <= NSEG)
+            const int nsc = __ldg(M.m_meta + min(m - lane + S.G - 1, nm - 1)) & 0xff;
+            const int ext = __ldg(M.m_meta + m) >> 9;
             float4 kc[NSEG];
 #pragma unroll
-            for (int k = 0; k < NSEG; ++k) kc[k] = __ldg(M.seg_kf + k * nm + m);
-            const float4 p0 = __ldg(M.m_p0 + m);  // f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max/10
-            const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
-            const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
+            for (int k = 0; k < NSEG; ++k)
+                if (k < nsc) kc[k] = ldc4(M.seg_kf + k * nm + m);
+            const float4 p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
+            const double2 pa = ldc2d(M.m_p1a + m), pb = ldc2d(M.m_p1b + m);
+            const float u = fminf(fmaxf(act_row[ext], 0.0f), 1.0f);
             const float a0 = St.act[mb + m];
             const float lm0 = St.lm[mb + m];
             double L = 0.0;
             float tq[NSEG];
 #pragma unroll
-            for (int k = 0; k < NSEG; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
-            const float F = muscle_update(St, mb, m, p0, pa, pb, u, a0, lm0, L, pw);
+            for (int k = 0; k < NSEG; ++k)
+                if (k < nsc) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
+            const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw);
 #pragma unroll
-            for (int k = 0; k < NSEG; ++k) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
+            for (int k = 0; k < NSEG; ++k)
+                if (k < nsc) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
         }
     } else {
         for (int m = lane; m < nm; m += S.G) {
+            const int meta = __ldg(M.m_meta + m);
+            const int nseg = meta & 0xff, ext = meta >> 9;
             const float4 p0 = __ldg(M.m_p0 + m);
             const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
-            const float u = fminf(fmaxf(act_row[m], 0.0f), 1.0f);
+            const float u = fminf(fmaxf(act_row[ext], 0.0f), 1.0f);
             const float a0 = St.act[mb + m];
             const float lm0 = St.lm[mb + m];
-            const int meta = __ldg(M.m_meta + m);
-            const int nseg = meta & 0xff;
             double L = 0.0;
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
@@ -589,7 +618,7 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
                 float arm;
                 L += (info & 3) == 2 ? static_cast<double>(general_seg_len(M, S, info >> 11)) : kseg(S, kf, info, arm);
             }
-            const float F = muscle_update(St, mb, m, p0, pa, pb, u, a0, lm0, L, pw);
+            const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw);
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
                 const int info = __float_as_int(kf.w);
@@ -598,7 +627,7 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
                 kseg(S, kf, info, arm);
                 S.un[info >> 11] = -F * arm;
             }
-            if (meta >> 8) general_pairs(M, S, m, F);
+            if ((meta >> 8) & 1) general_pairs(M, S, ext, F);
         }
     }
 }
@@ -1116,6 +1145,22 @@ __global__ void drain_kernel(DevState St, int n_envs, int cap, int* bins, uint8_
     St.out_count[e] = 0;
 }
 
+// Muscle rows between the internal (segment-count sorted) order and the
+// reference order: to_internal ? dst[i] = src[ext(i)] : dst[ext(i)] = src[i].
+__global__ void permute_muscles_kernel(DevModel M, int n_envs, const float* src, float* dst, int to_internal) {
+    const long long tot = static_cast<long long>(n_envs) * M.nm;
+    for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < tot;
+         g += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long row = g / M.nm;
+        const int i = static_cast<int>(g - row * M.nm);
+        const long long x = row * M.nm + (__ldg(M.m_meta + i) >> 9);
+        if (to_internal)
+            dst[g] = src[x];
+        else
+            dst[x] = src[g];
+    }
+}
+
 __global__ void get_ints_kernel(DevState St, int n_envs, int* ints) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n_envs) return;
@@ -1314,6 +1359,12 @@ void launch_broadcast_ema(const DevState& St, int n, int bins, const double* row
 
 void launch_drain(const DevState& St, int n, int cap, int* bins, uint8_t* failed, int* counts, cudaStream_t s) {
     drain_kernel<<<(n + 127) / 128, 128, 0, s>>>(St, n, cap, bins, failed, counts);
+}
+
+void launch_permute_muscles(const DevModel& M, int n, const float* src, float* dst, int to_internal, cudaStream_t s) {
+    const long long tot = static_cast<long long>(n) * M.nm;
+    const int blocks = static_cast<int>(std::min<long long>((tot + 255) / 256, 148 * 16));
+    permute_muscles_kernel<<<blocks, 256, 0, s>>>(M, n, src, dst, to_internal);
 }
 
 void launch_get_ints(const DevState& St, int n, int* ints, cudaStream_t s) {

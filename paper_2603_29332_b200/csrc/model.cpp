@@ -495,26 +495,39 @@ CompiledModel compile_model(const ModelSpec& s) {
     // packed device layout
     for (int mi = 0; mi < c.nm; ++mi)
         c.max_seg = std::max(c.max_seg, c.m_seg_start[mi + 1] - c.m_seg_start[mi]);
+    // Internal (device) muscle order: by segment count, then reference index.
+    // A warp's 32 muscles then share one padded segment count, so padding
+    // costs only at class boundaries.  Per-muscle I/O (actions, obs, power,
+    // EMG channels, get/set_state) stays in reference order via m_ext / m_int.
+    c.m_ext.resize(c.nm);
+    for (int i = 0; i < c.nm; ++i) c.m_ext[i] = i;
+    std::stable_sort(c.m_ext.begin(), c.m_ext.end(), [&](int a, int b) {
+        return c.m_seg_start[a + 1] - c.m_seg_start[a] < c.m_seg_start[b + 1] - c.m_seg_start[b];
+    });
+    c.m_int.assign(c.nm, 0);
+    for (int i = 0; i < c.nm; ++i) c.m_int[c.m_ext[i]] = i;
+    if (c.nm >= (1 << 22)) throw ConfigError("model too large for the packed layout");
     c.pk_p0.assign(4 * static_cast<size_t>(c.nm), 0.f);
     c.pk_p1.assign(4 * static_cast<size_t>(c.nm), 0.0);
     c.pk_meta.assign(c.nm, 0);
     c.pk_geo.assign(4 * static_cast<size_t>(c.max_seg) * c.nm, 0.f);
     // padding segments: kind 0 (zero length) writing 0 into the dummy slot n_pairs
     c.pk_info.assign(static_cast<size_t>(c.max_seg) * c.nm, c.n_pairs << 11);
-    for (int mi = 0; mi < c.nm; ++mi) {
-        c.pk_p0[4 * mi + 0] = c.m_fmax[mi];
-        c.pk_p0[4 * mi + 1] = c.m_ndt_act[mi];
-        c.pk_p0[4 * mi + 2] = c.m_ndt_deact[mi];
-        c.pk_p0[4 * mi + 3] = c.m_pw[mi];
-        c.pk_p1[4 * mi + 0] = c.m_slack[mi];
-        c.pk_p1[4 * mi + 1] = c.m_lopt[mi];
-        c.pk_p1[4 * mi + 2] = c.m_inv_lopt[mi];
-        c.pk_p1[4 * mi + 3] = c.m_kv[mi];
+    for (int i = 0; i < c.nm; ++i) {
+        const int mi = c.m_ext[i];
+        c.pk_p0[4 * i + 0] = c.m_fmax[mi];
+        c.pk_p0[4 * i + 1] = c.m_ndt_act[mi];
+        c.pk_p0[4 * i + 2] = c.m_ndt_deact[mi];
+        c.pk_p0[4 * i + 3] = c.m_pw[mi];
+        c.pk_p1[4 * i + 0] = c.m_slack[mi];
+        c.pk_p1[4 * i + 1] = c.m_lopt[mi];
+        c.pk_p1[4 * i + 2] = c.m_inv_lopt[mi];
+        c.pk_p1[4 * i + 3] = c.m_kv[mi];
         const int s0 = c.m_seg_start[mi], ns = c.m_seg_start[mi + 1] - s0;
         int general = 0;
         for (int k = 0; k < ns; ++k) {
             const int sg = s0 + k;
-            const size_t at = static_cast<size_t>(k) * c.nm + mi;
+            const size_t at = static_cast<size_t>(k) * c.nm + i;
             const int kind = c.seg_info[sg] & 3, dof = c.seg_info[sg] >> 8;
             int slot = c.seg_slot[sg];
             if (kind == 2) general = 1;
@@ -526,7 +539,7 @@ CompiledModel compile_model(const ModelSpec& s) {
             c.pk_geo[4 * at + 2] = c.seg_cx[sg];
             c.pk_geo[4 * at + 3] = c.seg_cz[sg];
         }
-        c.pk_meta[mi] = ns | (general << 8);
+        c.pk_meta[i] = ns | (general << 8) | (mi << 9);
         c.has_general |= general;
     }
     return c;

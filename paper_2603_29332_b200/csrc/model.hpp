@@ -112,11 +112,14 @@ struct CompiledModel {
 
     // ---- packed device layout (what the step kernel reads) ----
     // per muscle: p0 = {f_max, -dt/tau_act, -dt/tau_deact, l_opt v_max / 10} (f32x4),
-    // p1 = {slack, l_opt, 1/l_opt, 1/(dt l_opt v_max)} (f64x4), meta = nseg | general << 8.
+    // p1 = {slack, l_opt, 1/l_opt, 1/(dt l_opt v_max)} (f64x4), meta = nseg | general << 8 | m_ext << 9.
     // Segment k of muscle m lives at [k * nm + m] so a warp's 32 muscles read
     // 32 consecutive records (coalesced): geo = {ax, az, cx, cz},
     // info = kind | dof << 2 | slot << 11 (kind 2: slot = global via index of the end).
     int max_seg = 0, has_general = 0;
+    // internal muscle order (sorted by segment count): m_ext[i] = reference
+    // index of internal muscle i, m_int = its inverse; pk_meta carries m_ext << 9
+    std::vector<int32_t> m_ext, m_int;
     std::vector<float> pk_p0, pk_geo;
     std::vector<double> pk_p1;
     std::vector<int32_t> pk_meta, pk_info;
