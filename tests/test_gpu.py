@@ -308,3 +308,39 @@ def test_reward_aux_modes(assets):
     assert np.abs(og["reward_aux"] - oo["reward_aux"]).max() <= 1e-4 * max(1.0, np.abs(oo["reward_aux"]).max())
     assert np.abs(og["muscle_power"] - oo["power"]).max() <= 1e-4 * max(1.0, np.abs(oo["power"]).max())
     g.close()
+
+
+def test_reward_aux_with_reordered_muscles(assets, tmp_path):
+    """ImitationEmg / ImitationPower on walker5_m16, whose muscles the device
+    keeps in segment-count order (not the reference order): channel map,
+    per-muscle power rows and muscle obs blocks must still be in reference order
+    (env.cpp:59-64, 236-246)."""
+    mp, cp = model_paths("walker5_m16")
+    lines = open(cp).read().splitlines()
+    rng = np.random.default_rng(3)
+    emg_map = [15, 0, 7, 4, 9]
+    hdr = lines[0] + "".join(f",emg_{i}" for i in range(len(emg_map)))
+    rows = [ln + "".join(f",{v:.6f}" for v in rng.uniform(0, 1, len(emg_map))) for ln in lines[1:]]
+    cp_emg = tmp_path / "walker5_emg.csv"
+    cp_emg.write_text("\n".join([hdr] + rows) + "\n")
+    n = 4
+    for mode in (1, 2):
+        import paper_2603_29332_b200 as pk
+        from oracle.oracle import OracleBatch
+        from oracle.ref import env_config
+
+        g = pk.EnvBatch(mp, str(cp_emg), n, cfg=pk.EnvConfig(rsi=False),
+                        reward=pk.RewardConfig(mode=mode, w_power=0.1, emg_channel_map=emg_map))
+        o = OracleBatch(mp, str(cp_emg), n, cfg=env_config(rsi=False), reward_mode=mode, w_power=0.1,
+                        emg_map=emg_map)
+        g.reset()
+        o.reset()
+        sync_from_oracle(g, o)
+        for step in range(3):
+            a = excitations(11 + step, 0, n, g.nm).astype(np.float32)
+            og, oo = step_both(g, o, a)
+            sync_from_oracle(g, o)
+            assert np.abs(og["reward_aux"] - oo["reward_aux"]).max() <= 1e-4 * max(1.0, np.abs(oo["reward_aux"]).max())
+            if mode == 2:
+                assert np.abs(og["muscle_power"] - oo["power"]).max() <= 1e-4 * max(1.0, np.abs(oo["power"]).max())
+        g.close()
