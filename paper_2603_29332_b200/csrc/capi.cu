@@ -238,6 +238,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.joint_hi = ctx->upload(c.joint_hi);
         M.joint_slot_start = ctx->upload(c.joint_slot_start);
         M.m_meta = ctx->upload(c.pk_meta);
+        M.m_int = ctx->upload(c.m_int);
         M.seg_info = ctx->upload(c.pk_info);
         M.m_pair_start = ctx->upload(c.m_pair_start);
         M.via_link = ctx->upload(c.via_link);

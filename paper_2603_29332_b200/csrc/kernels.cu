@@ -430,12 +430,12 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
     }
     o += 3 * nk;
     const size_t mb = static_cast<size_t>(e) * nm;
-    for (int i = lane; i < nm; i += S.G) {  // internal muscle i -> reference slot
-        const int x = __ldg(M.m_meta + i) >> 9;
-        obs_row[o + x] = St.act[mb + i];
-        obs_row[o + nm + x] = St.fm[mb + i];
-        obs_row[o + 2 * nm + x] = St.lm[mb + i];
-        obs_row[o + 3 * nm + x] = St.vm[mb + i];
+    for (int x = lane; x < nm; x += S.G) {  // reference slot x <- internal muscle m_int[x]
+        const size_t i = mb + __ldg(M.m_int + x);
+        obs_row[o + x] = St.act[i];
+        obs_row[o + nm + x] = St.fm[i];
+        obs_row[o + 2 * nm + x] = St.lm[i];
+        obs_row[o + 3 * nm + x] = St.vm[i];
     }
     o += 4 * nm;
     const size_t t = static_cast<size_t>(t_index);
@@ -662,13 +662,15 @@ __device__ __forceinline__ double* stage_q(const DevModel& M, const EnvSmem& S, 
 // ============================================================================
 // step kernel: warp per env, WPB envs per block
 // ============================================================================
-template <int WPB, int MINB, int NSEG, int EPW>
+// QSL: DOF register slots per lane (n_q <= 32 QSL); fewer slots, fewer live registers.
+template <int WPB, int MINB, int NSEG, int EPW, int QSL>
 __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevState St, int env0, int n_envs,
                                                               const float* __restrict__ actions, float* obs,
                                                               float* delta, float* reward_aux, uint8_t* flags,
                                                               float* power, float* grf) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
+    static_assert(QSL >= 1 && QSL <= kMaxQSlots, "DOF slots");
+    constexpr int G = 32 / EPW, QS = QSL * EPW;
     const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
     const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
     const int le = (blockIdx.x * WPB + warp) * EPW + grp;  // env index local to this launch
@@ -1278,10 +1280,12 @@ constexpr int kEnvsPerBlock = kWPB * kEPW;
 
 // Fast-path segment count for a model (0 = generic path).
 int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 && M.max_seg <= 4) ? M.max_seg : 0; }
+// DOF register slots per lane: 3 covers n_q <= 96 (the whole-body models), else 4.
+int step_qslots(const DevModel& M) { return M.nq <= 96 ? 3 : kMaxQSlots; }
 
-template <int NSEG>
+template <int NSEG, int QSL>
 cudaError_t set_step_smem(int bytes) {
-    return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG, kEPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG, kEPW, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 bytes);
 }
 
@@ -1291,11 +1295,14 @@ size_t block_smem(const DevModel& M) {
 
 cudaError_t prepare_kernels(int smem_bytes_per_block) {
     cudaError_t err;
-    if ((err = set_step_smem<0>(smem_bytes_per_block)) != cudaSuccess) return err;
-    if ((err = set_step_smem<1>(smem_bytes_per_block)) != cudaSuccess) return err;
-    if ((err = set_step_smem<2>(smem_bytes_per_block)) != cudaSuccess) return err;
-    if ((err = set_step_smem<3>(smem_bytes_per_block)) != cudaSuccess) return err;
-    if ((err = set_step_smem<4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<0, 4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<1, 4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<2, 4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<3, 4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<4, 4>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<0, 3>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<2, 3>(smem_bytes_per_block)) != cudaSuccess) return err;
+    if ((err = set_step_smem<3, 3>(smem_bytes_per_block)) != cudaSuccess) return err;
     if ((err = cudaFuncSetAttribute(reset_kernel<kWPB, kMinB, kEPW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     smem_bytes_per_block)) != cudaSuccess)
         return err;
@@ -1309,15 +1316,24 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
                  float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s) {
     const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
     const size_t smem = block_smem(M);
-#define MSK_STEP(NS)                                                                                            \
-    step_kernel<kWPB, kMinB, NS, kEPW><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux, \
-                                                                       flags, power, grf)
-    switch (step_variant(M)) {
-        case 1: MSK_STEP(1); break;
-        case 2: MSK_STEP(2); break;
-        case 3: MSK_STEP(3); break;
-        case 4: MSK_STEP(4); break;
-        default: MSK_STEP(0); break;
+#define MSK_STEP(NS, QSL)                                                                                  \
+    step_kernel<kWPB, kMinB, NS, kEPW, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, \
+                                                                            raux, flags, power, grf)
+    const int v = step_variant(M);
+    if (step_qslots(M) == 3 && (v == 0 || v == 2 || v == 3)) {  // whole-body sized models
+        switch (v) {
+            case 2: MSK_STEP(2, 3); break;
+            case 3: MSK_STEP(3, 3); break;
+            default: MSK_STEP(0, 3); break;
+        }
+    } else {
+        switch (v) {
+            case 1: MSK_STEP(1, 4); break;
+            case 2: MSK_STEP(2, 4); break;
+            case 3: MSK_STEP(3, 4); break;
+            case 4: MSK_STEP(4, 4); break;
+            default: MSK_STEP(0, 4); break;
+        }
     }
 #undef MSK_STEP
 }
