@@ -115,7 +115,7 @@ def clocks_sampler(stop, out, gpu_index):
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
     try:
-        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200",
+        p = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "20",
                               "-i", str(gpu_index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
     except FileNotFoundError:
         return
@@ -123,11 +123,13 @@ def clocks_sampler(stop, out, gpu_index):
         line = p.stdout.readline()
         if not line:
             break
-        out.append(line.strip())
+        out.append((time.monotonic(), line.strip()))
     p.terminate()
 
 
-def summarize_clocks(lines):
+def summarize_clocks(lines, t0=None, t1=None):
+    """Median SM clock and throttle reasons over the samples taken in [t0, t1]."""
+    lines = [ln for t, ln in lines if (t0 is None or t >= t0) and (t1 is None or t <= t1)]
     sm, mx, reasons = [], 0.0, set()
     names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
     for ln in lines:
@@ -199,7 +201,7 @@ def cpu_baseline_sample(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--envs", type=int, default=4096, help="envs per GPU")
@@ -265,6 +267,7 @@ def main():
     ken = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     n0 = env.launch_count
     torch.cuda.synchronize()
+    t_loop0 = time.monotonic()
     for s in range(args.steps):
         flush.zero_()
         starts[s].record(stream)
@@ -275,6 +278,7 @@ def main():
         env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
         ends[s].record(stream)
     torch.cuda.synchronize()
+    t_loop1 = time.monotonic()
     launches = env.launch_count - n0
     stop.set()
     ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
@@ -362,7 +366,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": summarize_clocks(clk_lines),
+            "clocks": summarize_clocks(clk_lines, t_loop0, t_loop1),
         }
         print(json.dumps(line), flush=True)
     env.close()

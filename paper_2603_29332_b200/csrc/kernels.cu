@@ -1000,9 +1000,12 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
     const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
     const int e = (blockIdx.x * WPB + warp) * EPW + grp;
+    // masked resets (the per-step auto-reset of done envs) usually select no env
+    // of a block: skip the block before staging the tree table
+    const bool mine = e < n_envs && (!mask || (mask[e] & mask_bits));
+    if (!__syncthreads_or(mine)) return;
     load_tree_table(smem, M);
-    if (e >= n_envs) return;
-    if (mask && !(mask[e] & mask_bits)) return;
+    if (!mine) return;
     const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq;
     int frame = 0;

@@ -1,0 +1,11 @@
+# Round evidence: GPU tests (+parity margins), default bench line, reference arm,
+# ncu launch list and one --set full capture of the step kernel.
+set -x
+mkdir -p gpurun_out
+MSK_PARITY_REPORT=gpurun_out/parity_report.json timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
+timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench rc=$?
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref rc=$?
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
+timeout 300 $CMD > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
+timeout 300 $CMD > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -f -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
+tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/bench.log; tail -1 gpurun_out/bench_ref.log
