@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -51,7 +52,13 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw CudaFail(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-constexpr int kHostChunks = 4;
+constexpr int kMaxHostStreams = 8;
+// host-buffer pipeline shape (chunks, streams); MSK_HOST_CHUNKS / MSK_HOST_STREAMS override
+int host_knob(const char* name, int dflt, int lo, int hi) {
+    const char* v = std::getenv(name);
+    if (!v) return dflt;
+    return std::max(lo, std::min(hi, std::atoi(v)));
+}
 
 }  // namespace
 
@@ -67,7 +74,8 @@ struct msk_gpu_ctx {
     long long launches = 0;
     int obs_dim = 0, delta_dim = 0;
     // host-buffer path
-    cudaStream_t hs[2] = {nullptr, nullptr};
+    cudaStream_t hs[kMaxHostStreams] = {};
+    int host_chunks = 4, host_streams = 4;
     float* h_actions = nullptr;  // device staging
     float* h_obs = nullptr;
     float* h_delta = nullptr;
@@ -437,7 +445,10 @@ int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_ho
         const size_t E = static_cast<size_t>(ctx->n_envs);
         const int nm = ctx->cm.nm;
         if (!ctx->hs[0]) {
-            for (auto& s : ctx->hs) ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+            ctx->host_chunks = host_knob("MSK_HOST_CHUNKS", 4, 1, 64);
+            ctx->host_streams = host_knob("MSK_HOST_STREAMS", 4, 1, kMaxHostStreams);
+            for (int i = 0; i < ctx->host_streams; ++i)
+                ck(cudaStreamCreateWithFlags(&ctx->hs[i], cudaStreamNonBlocking), "stream");
             ctx->h_actions = ctx->dalloc<float>(E * nm);
             ctx->h_obs = ctx->dalloc<float>(E * ctx->obs_dim);
             ctx->h_delta = ctx->dalloc<float>(E * ctx->delta_dim);
@@ -446,12 +457,12 @@ int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_ho
         }
         // Chunked pipeline: H2D(actions c) -> step(c) -> D2H(outputs c), two
         // streams so chunk c's transfers overlap chunk c-1's kernel.
-        const int chunks = static_cast<int>(std::min<size_t>(kHostChunks, E));
+        const int chunks = static_cast<int>(std::min<size_t>(ctx->host_chunks, E));
         const size_t per = (E + chunks - 1) / chunks;
         for (int c = 0; c < chunks; ++c) {
             const size_t e0 = c * per, n = std::min(per, E - e0);
             if (n == 0) break;
-            cudaStream_t s = ctx->hs[c & 1];
+            cudaStream_t s = ctx->hs[c % ctx->host_streams];
             ck(cudaMemcpyAsync(ctx->h_actions + e0 * nm, actions_host + e0 * nm, n * nm * sizeof(float),
                                cudaMemcpyHostToDevice, s),
                "H2D actions");
@@ -475,7 +486,7 @@ int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_ho
             if (flags_host)
                 ck(cudaMemcpyAsync(flags_host + e0, ctx->h_flags + e0, n, cudaMemcpyDeviceToHost, s), "D2H flags");
         }
-        for (auto& s : ctx->hs) ck(cudaStreamSynchronize(s), "step_host sync");
+        for (int i = 0; i < ctx->host_streams; ++i) ck(cudaStreamSynchronize(ctx->hs[i]), "step_host sync");
     });
 }
 
