@@ -818,3 +818,74 @@ double om_excitation(uint64_t seed, uint32_t step, uint32_t global_env, int32_t 
     const uint32_t out[4] = {c0, c1, c2, c3};
     return (double)(out[muscle % 4] >> 8) * (1.0 / 16777216.0);
 }
+
+/* ---- nn.cpp: Mlp as the tracking discriminator -------------------------- */
+static void mlp_dims(int32_t layer, int32_t in, int32_t h, int32_t out, int32_t *r, int32_t *c) {
+    /* Mlp::layer_dims (nn.cpp:9-14) */
+    if (layer == 0) { *r = h; *c = in; }
+    else if (layer < 3) { *r = h; *c = h; }
+    else { *r = out; *c = h; }
+}
+
+int64_t om_mlp_param_count(int32_t in, int32_t hidden, int32_t out) {
+    int64_t total = 0;
+    for (int l = 0; l <= 3; ++l) {
+        int32_t r, c;
+        mlp_dims(l, in, hidden, out, &r, &c);
+        total += (int64_t)r * c + r;
+    }
+    return total;
+}
+
+void om_mlp_init(double *theta, int32_t in, int32_t hidden, int32_t out, uint64_t seed, double final_init_scale) {
+    /* nn.cpp:16-38 */
+    const int64_t n = om_mlp_param_count(in, hidden, out);
+    for (int64_t i = 0; i < n; ++i) theta[i] = 0.0;
+    om_env rng;
+    om_rng_seed(&rng, seed);
+    int64_t off = 0;
+    for (int l = 0; l <= 3; ++l) {
+        int32_t r, c;
+        mlp_dims(l, in, hidden, out, &r, &c);
+        const double scale = (1.0 / sqrt((double)c)) * (l == 3 ? final_init_scale : 1.0);
+        for (int32_t j = 0; j < c; ++j)
+            for (int32_t i = 0; i < r; ++i) /* Rng::uniform(lo, hi), rng.hpp:30 */
+                theta[off + (int64_t)j * r + i] = -scale + (scale - -scale) * rng_uniform(&rng);
+        off += (int64_t)r * c + r; /* biases stay zero */
+    }
+}
+
+void om_mlp_forward_sigmoid(const double *theta, int32_t in, int32_t hidden, const double *x, int32_t n, double *y) {
+    /* nn.cpp:54-73: h1..h3 = tanh(W h + b), z = W4 h3 + b4, y = 1 / (1 + exp(-z)) */
+    const int32_t h = hidden;
+    double *a = (double *)malloc(sizeof(double) * (size_t)(h > in ? h : in));
+    double *b = (double *)malloc(sizeof(double) * (size_t)h);
+    for (int32_t row = 0; row < n; ++row) {
+        for (int32_t k = 0; k < in; ++k) a[k] = x[(int64_t)row * in + k];
+        int32_t cols = in;
+        int64_t off = 0;
+        for (int l = 0; l < 3; ++l) {
+            const double *W = theta + off, *bias = theta + off + (int64_t)h * cols;
+            for (int32_t i = 0; i < h; ++i) {
+                double s = 0.0;
+                for (int32_t k = 0; k < cols; ++k) s += a[k] * W[(int64_t)k * h + i];
+                b[i] = tanh(s + bias[i]);
+            }
+            off += (int64_t)h * cols + h;
+            cols = h;
+            for (int32_t i = 0; i < h; ++i) a[i] = b[i];
+        }
+        const double *W4 = theta + off, *b4 = theta + off + h; /* out = 1: W4 is 1 x h */
+        double z = 0.0;
+        for (int32_t k = 0; k < h; ++k) z += a[k] * W4[k];
+        z += b4[0];
+        y[row] = 1.0 / (1.0 + exp(-z));
+    }
+    free(a);
+    free(b);
+}
+
+double om_disc_reward(double d) {
+    const double c = d < 1e-4 ? 1e-4 : (d > 1.0 - 1e-4 ? 1.0 - 1e-4 : d);
+    return -log(1.0 - c);
+}

@@ -130,6 +130,18 @@ int32_t om_env_step(const om_model *m, const om_clip *c, const om_env_config *cf
                     double *delta, double *reward_aux, double *muscle_power, double *grf);
 void om_sampler_record(const om_env_config *cfg, om_env *e, int32_t bin, int32_t failed);
 
+/* ---- nn.cpp: Mlp (3 tanh hidden layers) as the tracking discriminator ---- */
+/* Parameter count of Mlp(in, hidden, out) (nn.cpp:16-27). */
+int64_t om_mlp_param_count(int32_t in, int32_t hidden, int32_t out);
+/* Mlp::Mlp(shape, seed) (nn.cpp:16-38): flat theta = W1 b1 W2 b2 W3 b3 W4 b4,
+ * W column-major (Eigen default), W(i,j) ~ Rng(seed).uniform(-s, s) in column
+ * order, s = 1/sqrt(cols) (x final_init_scale on the head), biases zero. */
+void om_mlp_init(double *theta, int32_t in, int32_t hidden, int32_t out, uint64_t seed, double final_init_scale);
+/* Mlp::forward with Head::Sigmoid (nn.cpp:54-73), out = 1: y[r] = D(x_r). */
+void om_mlp_forward_sigmoid(const double *theta, int32_t in, int32_t hidden, const double *x, int32_t n, double *y);
+/* reward_from_discriminator: -log(1 - clamp(d, 1e-4, 1 - 1e-4)). */
+double om_disc_reward(double d);
+
 /* Philox4x32-10 excitation in [0,1). */
 double om_excitation(uint64_t seed, uint32_t step, uint32_t global_env, int32_t muscle);
 

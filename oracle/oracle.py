@@ -229,6 +229,12 @@ def lib():
         L.om_excitation.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_int32]
         L.om_obs_dim.restype = C.c_int32
         L.om_obs_dim.argtypes = [P(OmModel)]
+        L.om_mlp_param_count.restype = C.c_int64
+        L.om_mlp_param_count.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        L.om_mlp_init.argtypes = [_dp, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_double]
+        L.om_mlp_forward_sigmoid.argtypes = [_dp, C.c_int32, C.c_int32, _dp, C.c_int32, _dp]
+        L.om_disc_reward.restype = C.c_double
+        L.om_disc_reward.argtypes = [C.c_double]
         L.om_delta_dim.restype = C.c_int32
         L.om_delta_dim.argtypes = [P(OmModel)]
         _LIB = L
@@ -475,3 +481,30 @@ def excitations(seed, step, n_envs, nm, global_env_offset=0):
         for m in range(nm):
             out[e, m] = L.om_excitation(C.c_uint64(seed), step, global_env_offset + e, m)
     return out
+
+
+# ---- discriminator (nn.cpp Mlp with Head::Sigmoid) --------
+def mlp_param_count(n_in, hidden, n_out=1):
+    return int(lib().om_mlp_param_count(n_in, hidden, n_out))
+
+
+def mlp_init(n_in, hidden, seed, n_out=1, final_init_scale=1.0):
+    """Mlp(MlpShape{in, hidden, out}, seed) parameters (nn.cpp:16-38), f64 flat."""
+    theta = np.zeros(mlp_param_count(n_in, hidden, n_out))
+    lib().om_mlp_init(_ptr(theta, _dp), n_in, hidden, n_out, C.c_uint64(seed), float(final_init_scale))
+    return theta
+
+
+def mlp_forward_sigmoid(theta, n_in, hidden, x):
+    """D(x) per row (nn.cpp:54-73, Sigmoid head, out = 1)."""
+    x = np.ascontiguousarray(x, dtype=np.float64).reshape(-1, n_in)
+    y = np.zeros(x.shape[0])
+    theta = np.ascontiguousarray(theta, dtype=np.float64)
+    lib().om_mlp_forward_sigmoid(_ptr(theta, _dp), n_in, hidden, _ptr(x, _dp), x.shape[0], _ptr(y, _dp))
+    return y
+
+
+def disc_reward(theta, n_in, hidden, delta):
+    """reward_from_discriminator: -log(1 - clamp(D(delta), 1e-4, 1 - 1e-4))."""
+    L = lib()
+    return np.array([L.om_disc_reward(d) for d in mlp_forward_sigmoid(theta, n_in, hidden, delta)])

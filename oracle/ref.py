@@ -96,6 +96,7 @@ def ref_lib():
         lib.ref_drain_outcomes.argtypes = [C.c_void_p, _ip, _up, _ip, C.c_int32]
         lib.ref_rng_raw.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
         lib.ref_excitations.argtypes = [C.c_uint64, C.c_uint32, C.c_int64, C.c_int32, C.c_int32, _dp]
+        lib.ref_rng_uniform.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int64, _dp]
         lib.ref_bench.restype = C.c_double
         lib.ref_bench.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int64)]
         for fn in ("ref_force_length_active", "ref_force_velocity", "ref_force_passive", "ref_wrap_angle"):
@@ -285,3 +286,10 @@ class RefBatch:
         ang = np.zeros(self.nk)
         self.lib.ref_key_bodies(self.h, _ptr(q, _dp), _ptr(pos, _dp), _ptr(ang, _dp))
         return pos, ang
+
+
+def rng_uniform(seed, lo, hi, n):
+    """n draws of the reference's msk::Rng(seed).uniform(lo, hi) (rng.hpp:26-30)."""
+    out = np.zeros(n)
+    ref_lib().ref_rng_uniform(C.c_uint64(seed), float(lo), float(hi), int(n), out.ctypes.data_as(_dp))
+    return out

@@ -382,6 +382,13 @@ void ref_rng_raw(void* h, int32_t e, int32_t n, uint64_t* out) {
     for (int i = 0; i < n; ++i) out[i] = b.envs[static_cast<size_t>(e)]->rng().raw();
 }
 
+// Rng(seed).uniform(lo, hi) draws (rng.hpp:26-30) of a fresh reference Rng:
+// the stream Mlp::Mlp (nn.cpp:29-37) consumes for its weight init.
+void ref_rng_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
+    msk::Rng r(seed);
+    for (int64_t i = 0; i < n; ++i) out[i] = r.uniform(lo, hi);
+}
+
 // Philox excitations for a whole batch (E x nm), identical to the device's.
 void ref_excitations(uint64_t seed, uint32_t step, int64_t global_env_offset, int32_t n_envs, int32_t nm,
                      double* out) {

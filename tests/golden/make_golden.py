@@ -68,8 +68,36 @@ def make(name):
     return rec
 
 
+def mlp_theta_from_reference_rng(n_in, hidden, seed, n_out=1, final_init_scale=1.0):
+    """Mlp::Mlp(shape, seed) weights (nn.cpp:16-38) from the reference's OWN
+    msk::Rng(seed) uniform stream: uniform(lo, hi) = lo + (hi - lo) * uniform()
+    (rng.hpp:26-30), column-major per layer, biases zero."""
+    from oracle.ref import rng_uniform
+
+    dims = [(hidden, n_in), (hidden, hidden), (hidden, hidden), (n_out, hidden)]
+    n_w = sum(r * c for r, c in dims)
+    u = rng_uniform(seed, 0.0, 1.0, n_w)  # lo + (1 - 0) * u == u exactly
+    theta, k = [], 0
+    for layer, (r, c) in enumerate(dims):
+        s = (1.0 / np.sqrt(float(c))) * (final_init_scale if layer == 3 else 1.0)
+        w = -s + (s - -s) * u[k:k + r * c]
+        k += r * c
+        theta += [w, np.zeros(r)]
+    return np.concatenate(theta)
+
+
+def make_mlp():
+    small = mlp_theta_from_reference_rng(9, 16, 7)
+    big = mlp_theta_from_reference_rng(102, 256, 7)
+    return dict(small=small, big_head=big[:512], big_tail=big[-512:], big_sum=np.array([np.sum(big)]),
+                big_len=np.array([big.size]))
+
+
 def main():
     ensure_assets()
+    path = os.path.join(HERE, "mlp_seed7.npz")
+    np.savez_compressed(path, **make_mlp())
+    print(path, os.path.getsize(path))
     for name in CASES:
         rec = make(name)
         path = os.path.join(HERE, f"{name}.npz")

@@ -237,7 +237,7 @@ def test_oracle_bit_exact_vs_reference(assets, name, n, steps, cfg_kw, mode):
 
 
 # ---- oracle vs golden fixtures (made by the reference) -----------------------
-GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz")) if os.path.isdir(GOLDEN) else []
+GOLDEN_CASES = sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f[:-4] in CASES) if os.path.isdir(GOLDEN) else []
 
 
 @pytest.mark.parametrize("name", GOLDEN_CASES)
@@ -266,3 +266,56 @@ def test_oracle_reproduces_reference_golden(assets, name):
             assert np.array_equal(np.where(d > 0, f, -1), g["reset_frames"][s])
     assert np.array_equal(o.get_sampler(), g["ema_end"])
     assert np.array_equal(o.rng_raw(0, 400), g["rng_draws"])
+
+
+# ---- discriminator (nn.cpp Mlp + SPEC reward_from_discriminator) -------------
+def test_mlp_init_matches_reference_rng_golden():
+    """Mlp(shape, seed 7) weights from the reference's own Rng stream (golden)."""
+    g = np.load(os.path.join(GOLDEN, "mlp_seed7.npz"))
+    assert np.array_equal(om.mlp_init(9, 16, 7), g["small"])
+    big = om.mlp_init(102, 256, 7)
+    assert big.size == int(g["big_len"][0]) == om.mlp_param_count(102, 256)
+    assert np.array_equal(big[:512], g["big_head"]) and np.array_equal(big[-512:], g["big_tail"])
+    assert np.sum(big) == g["big_sum"][0]
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference build (oracle/_ref) absent")
+def test_mlp_init_matches_reference_rng_live():
+    from oracle.ref import rng_uniform
+
+    theta = om.mlp_init(9, 16, 3)
+    u = rng_uniform(3, 0.0, 1.0, 16 * 9)
+    s = 1.0 / math.sqrt(9.0)
+    assert np.array_equal(theta[:16 * 9], -s + (s - -s) * u)
+
+
+def test_discriminator_spec_examples():
+    """zero-initialised head -> D = 0.5 -> r = log 2; clamp
+    bounds -> r in (1e-4, 9.2103]; r monotone in D."""
+    th = om.mlp_init(9, 16, 7, final_init_scale=0.0)
+    x = np.random.default_rng(0).normal(0, 1, (5, 9))
+    assert np.allclose(om.mlp_forward_sigmoid(th, 9, 16, x), 0.5, atol=0, rtol=0)
+    assert np.allclose(om.disc_reward(th, 9, 16, x), math.log(2.0), rtol=0, atol=1e-15)
+    L = om.lib()
+    assert abs(L.om_disc_reward(1.0) - 9.2103) < 1e-4 and abs(L.om_disc_reward(0.0) - 1.00005e-4) < 1e-8
+    d = np.linspace(0, 1, 101)
+    r = np.array([L.om_disc_reward(v) for v in d])
+    assert np.all(np.diff(r) >= 0)
+
+
+def test_mlp_forward_matches_numpy():
+    """Independent matrix-arithmetic evaluation (SPEC.md nn forward example)."""
+    n_in, h = 7, 16
+    th = om.mlp_init(n_in, h, 11)
+    x = np.random.default_rng(1).normal(0, 0.5, (6, n_in))
+    o, ws = 0, []
+    for r, c in [(h, n_in), (h, h), (h, h), (1, h)]:
+        W = th[o:o + r * c].reshape(c, r).T  # column-major
+        b = th[o + r * c:o + r * c + r]
+        ws.append((W, b))
+        o += r * c + r
+    a = x
+    for W, b in ws[:3]:
+        a = np.tanh(a @ W.T + b)
+    z = a @ ws[3][0].T + ws[3][1]
+    assert np.allclose(om.mlp_forward_sigmoid(th, n_in, h, x), 1 / (1 + np.exp(-z[:, 0])), rtol=1e-13, atol=0)
