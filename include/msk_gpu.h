@@ -115,6 +115,26 @@ int msk_gpu_reset_to_frame(msk_gpu_ctx* ctx, const int32_t* frames, const uint8_
 int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward_aux,
                  uint8_t* flags, float* muscle_power, float* contact_force, void* stream);
 
+/* Built-in tracking discriminator: the TrackingRewardFn of Env::step(action, fn)
+ * (env.hpp:82, env.cpp:265-270) for the adversarial tracking reward
+ * r = -log(1 - clamp(D(delta), 1e-4, 1 - 1e-4)), with
+ * D = Mlp(in = delta_dim, hidden, out = 1, Head::Sigmoid) given by its flat f64
+ * parameters in the reference layout (nn.cpp:16-38: W1 b1 W2 b2 W3 b3 W4 b4,
+ * W column-major).  hidden: multiple of 16 in [16, 256].  Evaluated on the
+ * tcgen05 tensor cores with bf16 operands and fp32 accumulation. */
+int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_params, int32_t hidden);
+int msk_gpu_clear_discriminator(msk_gpu_ctx* ctx);
+/* reward[i] = r(D(delta_i)) for n rows of delta [n x delta_dim]. */
+int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n, float* reward, void* stream);
+/* Env::step(action, fn) with fn = the discriminator reward: msk_gpu_step plus
+ * reward [E] = r(D(delta)) + reward_aux for stepped envs, 0 for diverged ones
+ * (StepResult::reward stays 0, env.cpp:267-268), untouched for envs flagged
+ * NOT_STEPPED / BAD_ACTION.  delta / reward_aux / flags may be null (internal
+ * scratch). */
+int msk_gpu_step_rewarded(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward,
+                          float* reward_aux, uint8_t* flags, float* muscle_power, float* contact_force,
+                          void* stream);
+
 /* Same verb with HOST buffers (pinned or pageable): copies actions in, steps,
  * and copies obs/delta/reward_aux/flags out, pipelined over env chunks so the
  * PCIe transfers overlap the step kernel.  Synchronous on return. */

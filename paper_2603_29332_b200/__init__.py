@@ -96,6 +96,10 @@ def lib():
         L.msk_gpu_reset_to_frame.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+        L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
+        L.msk_gpu_clear_discriminator.argtypes = [_vp]
+        L.msk_gpu_discriminator_reward.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
+        L.msk_gpu_step_rewarded.argtypes = [_vp] * 10
         L.msk_gpu_observe.argtypes = [_vp, _vp, _vp]
         L.msk_gpu_tracking_error.argtypes = [_vp, _vp, _vp]
         L.msk_gpu_force_state_to_reference.argtypes = [_vp, _vp]
@@ -209,9 +213,32 @@ class EnvBatch:
         self._ck(lib().msk_gpu_reset_to_frame(self.h, _p(fr), _p(mask), _p(obs), _p(bad), self._s(stream)))
         return obs, bad
 
+    def set_discriminator(self, theta, hidden):
+        """Load D = Mlp(delta_dim, hidden, 1, Sigmoid) from its flat f64 parameters (nn.cpp layout)."""
+        import numpy as np
+
+        th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64))
+        self._ck(lib().msk_gpu_set_discriminator(self.h, th.ctypes.data, th.size, int(hidden)))
+        self._disc = True
+
+    def clear_discriminator(self):
+        self._ck(lib().msk_gpu_clear_discriminator(self.h))
+        self._disc = False
+
+    def discriminator_reward(self, delta, reward=None, stream=None):
+        """r = -log(1 - clamp(D(delta), 1e-4, 1 - 1e-4)) per row of delta [n x delta_dim] (device)."""
+        d = delta if delta.dtype == self.torch.float32 and delta.is_contiguous() else delta.float().contiguous()
+        n = d.shape[0]
+        reward = reward if reward is not None else self._empty(n)
+        self._ck(lib().msk_gpu_discriminator_reward(self.h, _p(d), n, _p(reward), self._s(stream)))
+        return reward
+
     def step(self, actions, obs=None, delta=None, reward_aux=None, flags=None, muscle_power=None,
-             contact_force=None, want_power=False, want_contact=False, stream=None):
-        """Env::step for every env; returns a dict of [E x ...] tensors (StepResult fields)."""
+             contact_force=None, want_power=False, want_contact=False, stream=None, reward=None,
+             want_reward=False):
+        """Env::step for every env; returns a dict of [E x ...] tensors (StepResult fields).
+        With want_reward / reward (and a discriminator set): Env::step(action, fn),
+        reward = r(D(delta)) + reward_aux."""
         torch = self.torch
         a = actions if actions.dtype == torch.float32 and actions.is_contiguous() else actions.float().contiguous()
         out = dict(
@@ -224,6 +251,13 @@ class EnvBatch:
             out["muscle_power"] = muscle_power if muscle_power is not None else self._empty(self.n, self.nm)
         if want_contact or contact_force is not None:
             out["contact_force"] = contact_force if contact_force is not None else self._empty(self.n, self.n_links, 2)
+        if want_reward or reward is not None:
+            out["reward"] = reward if reward is not None else self._empty(self.n)
+            self._ck(lib().msk_gpu_step_rewarded(self.h, _p(a), _p(out["obs"]), _p(out["delta"]), _p(out["reward"]),
+                                                 _p(out["reward_aux"]), _p(out["flags"]),
+                                                 _p(out.get("muscle_power")), _p(out.get("contact_force")),
+                                                 self._s(stream)))
+            return out
         self._ck(lib().msk_gpu_step(self.h, _p(a), _p(out["obs"]), _p(out["delta"]), _p(out["reward_aux"]),
                                     _p(out["flags"]), _p(out.get("muscle_power")), _p(out.get("contact_force")),
                                     self._s(stream)))

@@ -11,6 +11,7 @@
 
 #include "../../include/msk_gpu.h"
 #include "device.cuh"
+#include "disc.hpp"
 #include "model.hpp"
 
 namespace msk_b200 {
@@ -82,6 +83,12 @@ struct msk_gpu_ctx {
     float* h_raux = nullptr;
     uint8_t* h_flags = nullptr;
     double* global_ema = nullptr;
+    // device discriminator (msk_gpu_set_discriminator)
+    DiscDev disc{};
+    std::vector<void*> disc_allocs;
+    float* r_delta = nullptr;  // scratch when the caller passes no Δ / reward_aux / flags
+    float* r_raux = nullptr;
+    uint8_t* r_flags = nullptr;
 
     template <class T>
     T* dalloc(size_t n) {
@@ -376,6 +383,7 @@ void msk_gpu_destroy(msk_gpu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     for (void* p : ctx->allocs) cudaFree(p);
+    for (void* p : ctx->disc_allocs) cudaFree(p);
     for (auto& s : ctx->hs)
         if (s) cudaStreamDestroy(s);
     delete ctx;
@@ -435,6 +443,78 @@ int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delt
                     contact_force, as_stream(stream));
         ctx->count();
         ctx->check_launch();
+    });
+}
+
+int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_params, int32_t hidden) {
+    return guarded(ctx, [&] {
+        if (!theta) throw ConfigError("set_discriminator: theta is null");
+        const DiscHost h = build_disc_images(theta, n_params, ctx->delta_dim, hidden);
+        for (void* p : ctx->disc_allocs) cudaFree(p);
+        ctx->disc_allocs.clear();
+        auto up = [&](const void* src, size_t bytes) {
+            void* p = nullptr;
+            ck(cudaMalloc(&p, bytes), "cudaMalloc");
+            ctx->disc_allocs.push_back(p);
+            ck(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice), "upload discriminator");
+            return p;
+        };
+        DiscDev d;
+        d.din = h.din;
+        d.hidden = h.hidden;
+        d.k1 = h.k1;
+        d.tmem_cols = 32;
+        while (d.tmem_cols < static_cast<uint32_t>(h.hidden)) d.tmem_cols <<= 1;
+        d.w1 = up(h.w1.data(), h.w1.size() * 2);
+        d.w2 = up(h.w2.data(), h.w2.size() * 2);
+        d.w3 = up(h.w3.data(), h.w3.size() * 2);
+        d.bias = static_cast<const float*>(up(h.bias.data(), h.bias.size() * 4));
+        d.b4 = h.b4;
+        ck(prepare_disc(d), "cudaFuncSetAttribute(disc)");
+        ctx->disc = d;
+        if (!ctx->r_delta) {
+            ctx->r_delta = ctx->dalloc<float>(static_cast<size_t>(ctx->n_envs) * ctx->delta_dim);
+            ctx->r_raux = ctx->dalloc<float>(ctx->n_envs);
+            ctx->r_flags = ctx->dalloc<uint8_t>(ctx->n_envs);
+        }
+    });
+}
+
+int msk_gpu_clear_discriminator(msk_gpu_ctx* ctx) {
+    return guarded(ctx, [&] {
+        ck(cudaDeviceSynchronize(), "clear_discriminator");
+        for (void* p : ctx->disc_allocs) cudaFree(p);
+        ctx->disc_allocs.clear();
+        ctx->disc = DiscDev{};
+    });
+}
+
+int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n, float* reward, void* stream) {
+    return guarded(ctx, [&] {
+        if (!ctx->disc.w1) throw ConfigError("discriminator_reward: no discriminator set");
+        if (!delta || !reward || n < 0) throw ConfigError("discriminator_reward: bad arguments");
+        ck(launch_disc(ctx->disc, delta, ctx->delta_dim, n, nullptr, nullptr, reward, as_stream(stream), false),
+           "launch discriminator");
+        ctx->count();
+    });
+}
+
+int msk_gpu_step_rewarded(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward,
+                          float* reward_aux, uint8_t* flags, float* muscle_power, float* contact_force,
+                          void* stream) {
+    return guarded(ctx, [&] {
+        if (!actions || !reward) throw ConfigError("step_rewarded: actions and reward are required");
+        if (!ctx->disc.w1) throw ConfigError("step_rewarded: no discriminator set");
+        float* d = delta ? delta : ctx->r_delta;
+        float* ra = reward_aux ? reward_aux : ctx->r_raux;
+        uint8_t* f = flags ? flags : ctx->r_flags;
+        cudaStream_t s = as_stream(stream);
+        launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, obs, d, ra, f, muscle_power, contact_force, s);
+        ctx->count();
+        ctx->check_launch();
+        // D(Δ) on the tensor cores, launched as a programmatic dependent of the step
+        ck(launch_disc(ctx->disc, d, ctx->delta_dim, ctx->n_envs, ra, f, reward, s, true), "launch discriminator");
+        ctx->count();
     });
 }
 

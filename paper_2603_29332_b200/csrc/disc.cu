@@ -1,0 +1,330 @@
+// Discriminator tracking reward on the 5th-generation tensor cores (sm_100a).
+//
+// r = -log(1 - clamp(D(Δ), 1e-4, 1 - 1e-4)),  D = sigmoid(MLP: Δ -> 3 x tanh(H) -> 1)
+// (reward_from_discriminator; Mlp::forward with Head::Sigmoid,
+// nn.cpp:54-73; parameters in the Mlp flat layout of nn.cpp:16-38).  In
+// Env::step(action, fn) the reward is fn(Δ) + reward_aux for a non-diverged
+// step (env.cpp:265-270); that is what the fused mode writes.
+//
+// One CTA per 128-row tile of Δ, 128 threads (4 warps), one tile resident per SM:
+//   * weights are pre-laid-out on the host as bf16 K-major "core matrix" images
+//     (8 rows x 16 B atoms, SWIZZLE_NONE) and staged global -> smem with 1-D TMA
+//     bulk copies (cp.async.bulk + mbarrier complete_tx);
+//   * each hidden layer is ONE chain of tcgen05.mma.kind::f16 (M = 128, N = H,
+//     K = 16 per instruction) issued by a single thread, accumulating in TMEM
+//     (H fp32 columns x 128 lanes);
+//   * the epilogue (warp w owns TMEM lanes 32w..32w+31 = rows) loads the
+//     accumulator with tcgen05.ld, adds the bias, applies tanh in fp32 and
+//     writes bf16 back to smem as the next layer's A operand; the head (N = 1)
+//     is an fp32 dot product in registers, then sigmoid / clamp / log.
+// Launched right after the step kernel with programmatic dependent launch, so
+// the TMEM allocation and the first weight copy overlap the step's tail.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <vector>
+
+#include "disc.hpp"
+
+namespace msk_b200 {
+
+namespace {
+
+constexpr int kTileM = 128;
+constexpr int kThreads = 128;
+constexpr uint8_t kFlagDiverged = 4, kFlagSkip = 8 | 16;  // NOT_STEPPED | BAD_ACTION: untouched
+
+// byte offset of element (r, k) in a K-major SWIZZLE_NONE core-matrix image
+// with K columns: 8-row groups at SBO = (K/8)*128 B, 8-element K chunks at 128 B
+__host__ __device__ constexpr uint32_t img_off(int r, int k, int K) {
+    return static_cast<uint32_t>(((r >> 3) * (K >> 3) + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// tcgen05 shared-memory matrix descriptor (K-major, no swizzle): start address,
+// leading byte offset (K-chunk stride), stride byte offset (8-row-group stride),
+// version 1 (bits 46-47), layout type 0 (bits 61-63).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+
+// kind::f16 instruction descriptor: D f32, A/B bf16, both K-major, M = 128, N = n.
+__device__ __forceinline__ uint32_t instr_desc(int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
+           (static_cast<uint32_t>(kTileM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completion counted on the mbarrier.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Stage `bytes` (multiple of 16) of a weight image; one thread.
+__device__ __forceinline__ void stage_weights(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    mbar_expect_tx(bar, bytes);
+    constexpr uint32_t kPiece = 32768;
+    for (uint32_t o = 0; o < bytes; o += kPiece)
+        bulk_g2s(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, (bytes - o < kPiece ? bytes - o : kPiece), bar);
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void proxy_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// One layer: D[tmem] = A[128 x K] * W[N x K]^T, K/16 MMAs from one thread, then
+// a commit that arrives on `bar` when they (and their smem reads) are done.
+__device__ __forceinline__ void mma_layer(uint32_t tmem, const void* sa, const void* sw, int K, int N, uint64_t* bar) {
+    const uint32_t a0 = smem_u32(sa), w0 = smem_u32(sw), sbo = static_cast<uint32_t>(K >> 3) * 128;
+    const uint32_t idesc = instr_desc(N);
+    for (int s = 0; s < K / 16; ++s) {
+        const uint64_t da = smem_desc(a0 + 256 * s, 128, sbo), dw = smem_desc(w0 + 256 * s, 128, sbo);
+        const uint32_t acc = s > 0;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+            "l"(da), "l"(dw), "r"(idesc), "r"(acc)
+            : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// Hidden-layer epilogue: row r's H accumulators -> tanh(acc + b) -> bf16 into the
+// next layer's A image (K = H).
+__device__ __forceinline__ void epilogue_hidden(uint32_t tmem_row, const float* bias, char* sa, int r, int H) {
+    for (int c = 0; c < H; c += 16) {
+        float v[16];
+        tmem_ld16(tmem_row + c, v);
+        uint32_t p[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            p[i] = pack_bf16(tanh_fast(v[2 * i] + bias[c + 2 * i]), tanh_fast(v[2 * i + 1] + bias[c + 2 * i + 1]));
+        *reinterpret_cast<uint4*>(sa + img_off(r, c, H)) = make_uint4(p[0], p[1], p[2], p[3]);
+        *reinterpret_cast<uint4*>(sa + img_off(r, c + 8, H)) = make_uint4(p[4], p[5], p[6], p[7]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    disc_reward_kernel(DiscDev P, const float* __restrict__ delta, int ld, int n, const float* __restrict__ raux,
+                       const uint8_t* __restrict__ flags, float* __restrict__ reward) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int H = P.hidden, K1 = P.k1, Kmax = K1 > H ? K1 : H;
+    char* sa = reinterpret_cast<char*>(smem);                                      // 128 x Kmax bf16
+    char* sw = sa + kTileM * Kmax * 2;                                             // H x Kmax bf16
+    float* sb = reinterpret_cast<float*>(sw + static_cast<size_t>(H) * Kmax * 2);  // b1 b2 b3 w4
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sb + 4 * H);                      // [0] weights, [1] mma
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int row0 = blockIdx.x * kTileM;
+
+    if (tid == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {  // TMEM: H fp32 columns (power of two >= 32)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(P.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    for (int i = tid; i < 4 * H; i += kThreads) sb[i] = P.bias[i];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (tid == 0) stage_weights(sw, P.w1, static_cast<uint32_t>(H) * K1 * 2, &bars[0]);
+
+    // Δ is the previous kernel's output: wait for it (programmatic dependent launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int i = tid; i < kTileM * K1; i += kThreads) {
+        const int r = i / K1, k = i - r * K1, row = row0 + r;
+        const float x = (row < n && k < P.din) ? delta[static_cast<size_t>(row) * ld + k] : 0.0f;
+        *reinterpret_cast<__nv_bfloat16*>(sa + img_off(r, k, K1)) = __float2bfloat16_rn(x);
+    }
+    proxy_fence();
+    __syncthreads();
+
+    const int r = warp * 32 + lane;                          // this thread's row of the tile
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);  // TMEM lane base of this warp
+    uint32_t wphase = 0, mphase = 0;
+    for (int layer = 0; layer < 3; ++layer) {
+        const int K = layer == 0 ? K1 : H;
+        if (tid == 0) {
+            mbar_wait(&bars[0], wphase);
+            tc_fence_after();
+            mma_layer(tmem, sa, sw, K, H, &bars[1]);
+        }
+        wphase ^= 1;
+        mbar_wait(&bars[1], mphase);
+        mphase ^= 1;
+        tc_fence_after();
+        if (layer < 2) {
+            if (tid == 0) stage_weights(sw, layer == 0 ? P.w2 : P.w3, static_cast<uint32_t>(H) * H * 2, &bars[0]);
+            epilogue_hidden(trow, sb + layer * H, sa, r, H);
+            proxy_fence();
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+        }
+    }
+    // head: z = w4 . tanh(acc3 + b3) + b4 (fp32), D = sigmoid(z)
+    float z = 0.0f;
+    for (int c = 0; c < H; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z = fmaf(tanh_fast(v[i] + sb[2 * H + c + i]), sb[3 * H + c + i], z);
+    }
+    z += P.b4;
+    const int row = row0 + r;
+    if (row < n) {
+        float d = 1.0f / (1.0f + __expf(-z));
+        d = fminf(fmaxf(d, 1e-4f), 1.0f - 1e-4f);
+        const float rw = -log1pf(-d);
+        if (!flags) {
+            reward[row] = rw;
+        } else {
+            const uint8_t f = flags[row];
+            if (!(f & kFlagSkip)) reward[row] = (f & kFlagDiverged) ? 0.0f : rw + (raux ? raux[row] : 0.0f);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols)
+                     : "memory");
+}
+
+}  // namespace
+
+size_t disc_smem_bytes(const DiscDev& P) {
+    const int Kmax = std::max(P.k1, P.hidden);
+    return static_cast<size_t>(kTileM) * Kmax * 2 + static_cast<size_t>(P.hidden) * Kmax * 2 + 16 * P.hidden + 64;
+}
+
+// Host: Mlp flat parameters (f64, nn.cpp layout) -> device images.
+DiscHost build_disc_images(const double* theta, long long n_params, int din, int hidden) {
+    if (hidden < 16 || hidden > 256 || hidden % 16 != 0)
+        throw std::invalid_argument("discriminator hidden width must be a multiple of 16 in [16, 256]");
+    if (din < 1 || din > 256) throw std::invalid_argument("discriminator input width out of range");
+    const int H = hidden, K1 = (din + 15) / 16 * 16;
+    const long long expect = static_cast<long long>(H) * din + H + 2LL * (H * H + H) + H + 1;
+    if (n_params != expect)
+        throw std::invalid_argument("discriminator parameter count " + std::to_string(n_params) + " != " +
+                                    std::to_string(expect) + " for Mlp(in=" + std::to_string(din) +
+                                    ", hidden=" + std::to_string(H) + ", out=1)");
+    DiscHost h;
+    h.din = din;
+    h.hidden = H;
+    h.k1 = K1;
+    auto image = [&](const double* W, int rows, int cols, int K) {  // W column-major rows x cols
+        std::vector<uint16_t> img(static_cast<size_t>(rows) * K, 0);
+        for (int r = 0; r < rows; ++r)
+            for (int k = 0; k < cols; ++k) {
+                const __nv_bfloat16 b = __float2bfloat16_rn(static_cast<float>(W[static_cast<size_t>(k) * rows + r]));
+                uint16_t u;
+                std::memcpy(&u, &b, 2);
+                img[img_off(r, k, K) / 2] = u;
+            }
+        return img;
+    };
+    long long o = 0;
+    h.w1 = image(theta + o, H, din, K1);
+    o += static_cast<long long>(H) * din;
+    const double* b1 = theta + o;
+    o += H;
+    h.w2 = image(theta + o, H, H, H);
+    o += static_cast<long long>(H) * H;
+    const double* b2 = theta + o;
+    o += H;
+    h.w3 = image(theta + o, H, H, H);
+    o += static_cast<long long>(H) * H;
+    const double* b3 = theta + o;
+    o += H;
+    const double* w4 = theta + o;  // 1 x H
+    o += H;
+    h.b4 = static_cast<float>(theta[o]);
+    h.bias.resize(4 * static_cast<size_t>(H));
+    for (int i = 0; i < H; ++i) {
+        h.bias[i] = static_cast<float>(b1[i]);
+        h.bias[H + i] = static_cast<float>(b2[i]);
+        h.bias[2 * H + i] = static_cast<float>(b3[i]);
+        h.bias[3 * H + i] = static_cast<float>(w4[i]);
+    }
+    return h;
+}
+
+cudaError_t prepare_disc(const DiscDev& P) {
+    return cudaFuncSetAttribute(disc_reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(disc_smem_bytes(P)));
+}
+
+cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, const float* raux,
+                        const uint8_t* flags, float* reward, cudaStream_t s, bool pdl) {
+    if (n <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((n + kTileM - 1) / kTileM);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = disc_smem_bytes(P);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, disc_reward_kernel, P, delta, ld, n, raux, flags, reward);
+}
+
+}  // namespace msk_b200

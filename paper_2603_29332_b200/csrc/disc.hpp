@@ -1,0 +1,39 @@
+// Device discriminator (tracking reward D(Δ)) — see disc.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace msk_b200 {
+
+// Host-side images built from the Mlp flat parameters (nn.cpp:16-38).
+struct DiscHost {
+    int din = 0, hidden = 0, k1 = 0;  // k1 = din rounded up to the MMA K step (16)
+    std::vector<uint16_t> w1, w2, w3;  // bf16 K-major core-matrix images (H x k1, H x H, H x H)
+    std::vector<float> bias;           // b1 | b2 | b3 | w4 (4 H floats)
+    float b4 = 0.0f;
+};
+
+// Device view passed to the kernel by value.
+struct DiscDev {
+    int din = 0, hidden = 0, k1 = 0;
+    uint32_t tmem_cols = 0;  // power of two >= max(32, hidden)
+    const void* w1 = nullptr;
+    const void* w2 = nullptr;
+    const void* w3 = nullptr;
+    const float* bias = nullptr;
+    float b4 = 0.0f;
+};
+
+DiscHost build_disc_images(const double* theta, long long n_params, int din, int hidden);
+size_t disc_smem_bytes(const DiscDev& P);
+cudaError_t prepare_disc(const DiscDev& P);
+// reward[i] = r(D(delta_i)); with flags: reward = r + raux for stepped envs,
+// 0 for diverged ones, untouched for NOT_STEPPED / BAD_ACTION rows.
+cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, const float* raux,
+                        const uint8_t* flags, float* reward, cudaStream_t s, bool pdl);
+
+}  // namespace msk_b200

@@ -371,3 +371,85 @@ def test_reward_aux_with_reordered_muscles(assets, tmp_path):
             if mode == 2:
                 assert np.abs(og["muscle_power"] - oo["power"]).max() <= 1e-4 * max(1.0, np.abs(oo["power"]).max())
         g.close()
+
+
+# ---- discriminator reward on the tensor cores ---------------------------------
+# bf16 operands (2^-9 relative rounding) through three tanh layers, fp32
+# accumulation and an fp32 head: |r_gpu - r_f64| <= 3e-3 * max(1, |r|)
+# (measured worst case ~1.2e-3 over input scales 0.05-3, tools/disc_check.py).
+DISC_TOL = 3e-3
+
+
+@pytest.mark.parametrize("hidden", [16, 256])
+def test_discriminator_reward_matches_oracle(assets, hidden):
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from oracle.oracle import disc_reward, mlp_init
+
+    mp, cp = model_paths("wb700")
+    g = pk.EnvBatch(mp, cp, 4)
+    dd = g.delta_dim
+    th = mlp_init(dd, hidden, 7)
+    g.set_discriminator(th, hidden)
+    rng = np.random.default_rng(hidden)
+    for scale in (0.05, 0.5, 3.0):
+        x = rng.normal(0, scale, (300, dd)).astype(np.float32)  # 300 rows: a ragged last tile
+        r = to_np(g.discriminator_reward(torch.as_tensor(x, device=g.device)))
+        ref = disc_reward(th, dd, hidden, x.astype(np.float64))
+        err = np.abs(r - ref) / np.maximum(1.0, np.abs(ref))
+        _note(f"disc H={hidden}", "reward rel (tol 3e-3)", err.max())
+        assert err.max() <= DISC_TOL, (scale, err.max())
+    # zero-initialised head: D = 0.5 exactly -> r = log 2
+    g.set_discriminator(mlp_init(dd, hidden, 7, final_init_scale=0.0), hidden)
+    r = to_np(g.discriminator_reward(torch.as_tensor(rng.normal(0, 1, (5, dd)), device=g.device)))
+    assert np.abs(r - np.log(2.0)).max() <= 1e-6
+    with pytest.raises(pk.MskError):
+        g.set_discriminator(th[:-1], hidden)  # wrong parameter count -> contract error
+    g.close()
+
+
+def test_step_rewarded_matches_oracle(assets):
+    """Env::step(action, fn) with fn = discriminator reward: reward = r(D(Δ)) + reward_aux
+    (env.cpp:265-270); diverged envs keep reward 0."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from oracle.oracle import disc_reward, mlp_init
+
+    mp, cp = model_paths("wb700")
+    n, H = 6, 256
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(rsi=False), reward_mode=2, w_power=0.05)
+    th = mlp_init(g.delta_dim, H, 7)
+    g.set_discriminator(th, H)
+    g.reset()
+    o.reset()
+    for step in range(3):
+        sync_from_oracle(g, o)
+        a = excitations(500 + step, 0, n, g.nm).astype(np.float32)
+        out = g.step(torch.as_tensor(a, device=g.device), want_reward=True)
+        torch.cuda.synchronize()
+        oo = o.step(a.astype(np.float64))
+        rg = to_np(out["reward"])
+        # fused == standalone D on the same Δ plus reward_aux
+        r_sep = to_np(g.discriminator_reward(out["delta"])) + to_np(out["reward_aux"])
+        assert np.abs(rg - r_sep).max() <= 1e-6
+        ref = disc_reward(th, g.delta_dim, H, oo["delta"]) + oo["reward_aux"]
+        err = np.abs(rg - ref) / np.maximum(1.0, np.abs(ref))
+        _note("step_rewarded wb700", "reward rel (tol 3e-3)", err.max())
+        assert err.max() <= DISC_TOL
+    # a diverged env: reward stays 0 (StepResult::reward default)
+    s = g.get_state()
+    s["dq"][0, 0] = float("inf")
+    g.set_state(s)
+    rew = torch.full((n,), 7.0, device=g.device)
+    out = g.step(torch.full((n, g.nm), 0.3, device=g.device), reward=rew)
+    torch.cuda.synchronize()
+    f = to_np(out["flags"])
+    assert f[0] & pk.FLAG_DIVERGED and to_np(rew)[0] == 0.0
+    # done env -> NOT_STEPPED: reward untouched
+    rew.fill_(7.0)
+    out = g.step(torch.full((n, g.nm), 0.3, device=g.device), reward=rew)
+    torch.cuda.synchronize()
+    assert to_np(out["flags"])[0] & pk.FLAG_NOT_STEPPED and to_np(rew)[0] == 7.0
+    g.close()
