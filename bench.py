@@ -35,8 +35,26 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 DEFAULT_MODEL = "wb700_fixed"
+
+# BASELINE.json configs -> workloads.  c2 is the headline (default); the others
+# are the rollout-shaped configurations (§8(d) C3-C5), measured on request.
+CONFIGS = {
+    "c2": dict(model="wb700_fixed", envs=4096, eval=True, rsi=False, horizon=1000, reward_mode=0, disc=None,
+               exchange=0, desc="wb700_fixed: 80 links, 700 muscles, no contacts, eval mode, random excitations"),
+    "c3": dict(model="wb700_fixed", envs=8192, eval=True, rsi=False, horizon=1000, reward_mode=0, disc=None,
+               exchange=8, desc="wb700_fixed, 8192 envs/GPU (65536 on 8 GPUs), rollout-stats allgather + "
+                            "ordered sampler/obs-norm merge every 8 control steps"),
+    "c4": dict(model="wb700", envs=16384, eval=False, rsi=True, horizon=250, reward_mode=2, disc=(256, 7),
+               exchange=8, desc="wb700 (floating root, 10 contact spheres), dance clip, training mode (RSI, "
+                            "adaptive sampler, 0.5 m termination, auto-reset), fused tracking reward "
+                            "-log(1-D(delta)) (D: Mlp W=256 seed 7 on tcgen05) + ImitationPower 0.05, "
+                            "allgather every 8 steps"),
+    "c5": dict(model="wb700_slow", envs=8192, eval=False, rsi=True, horizon=250, reward_mode=2, disc=None,
+               exchange=8, desc="stress: wb700 with contacts, tau_act=0.05 / tau_deact=0.20 for all muscles, "
+                            "training mode with mid-batch resets, allgather every 8 steps"),
+}
 CLIPS = {"wb700_fixed": "wb700_fixed_dance", "wb700": "wb700_dance", "arm2_m6": "arm2_m6_sine",
-         "walker5_m16": "walker5_m16_sine"}
+         "walker5_m16": "walker5_m16_sine", "wb700_slow": "wb700_dance"}
 
 
 def ensure_assets():
@@ -50,6 +68,13 @@ def ensure_assets():
 
 def model_files(name):
     d = ensure_assets()
+    if name == "wb700_slow" and not os.path.exists(os.path.join(d, "wb700_slow.json")):
+        with open(os.path.join(d, "wb700.json")) as f:  # C5: long activation/deactivation lag
+            m = json.load(f)
+        for mu in m["muscles"]:
+            mu["tau_act"], mu["tau_deact"] = 0.05, 0.20
+        with open(os.path.join(d, "wb700_slow.json"), "w") as f:
+            json.dump(m, f)
     return os.path.join(d, name + ".json"), os.path.join(d, CLIPS[name] + ".csv")
 
 
@@ -157,11 +182,12 @@ def run_reference(args, rank, world):
     from oracle.ref import RefBatch, env_config
 
     mp, cp = model_files(args.model)
+    C = args.C
     threads = args.cpu_threads or os.cpu_count() or 1
     n_envs = args.ref_envs or max(threads, 8)
-    cfg = env_config(episode_horizon=1000, rsi=False)
-    b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads)
-    b.set_eval_mode(True)
+    cfg = env_config(episode_horizon=C["horizon"], rsi=C["rsi"])
+    b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads, reward_mode=C["reward_mode"])
+    b.set_eval_mode(C["eval"])
     b.reset()
     for _ in range(args.warmup):
         b.bench(1)
@@ -171,8 +197,10 @@ def run_reference(args, rank, world):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Philox excitations, generated dance clip)", "impl": "reference",
-            "config": {"workload": f"{args.model} eval-mode random excitations (CPU sample)",
-                       "envs": n_envs, "parallelism": f"{threads} host threads (ThreadPool::parallel_chunks)"},
+            "config": {"workload": f"{args.config}: {C['desc']} (CPU sample"
+                                   + ("; D(Δ) reward not included: the reference's Mlp needs Eigen)" if C["disc"] else ")"),
+                       "config": args.config, "envs": n_envs,
+                       "parallelism": f"{threads} host threads (ThreadPool::parallel_chunks)"},
             "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "reference",
                              "sample": f"{n_envs} envs x {args.steps} control steps"},
             "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -184,10 +212,12 @@ def cpu_baseline_sample(args):
     from oracle.ref import RefBatch, env_config
 
     mp, cp = model_files(args.model)
+    C = args.C
     threads = args.cpu_threads or os.cpu_count() or 1
     n_envs = max(threads, 8)
-    b = RefBatch(mp, cp, n_envs, cfg=env_config(episode_horizon=1000, rsi=False), threads=threads)
-    b.set_eval_mode(True)
+    b = RefBatch(mp, cp, n_envs, cfg=env_config(episode_horizon=C["horizon"], rsi=C["rsi"]), threads=threads,
+                 reward_mode=C["reward_mode"])
+    b.set_eval_mode(C["eval"])
     b.reset()
     b.bench(1)
     secs, steps = b.bench(1)
@@ -204,8 +234,9 @@ def main():
     ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--envs", type=int, default=4096, help="envs per GPU")
-    ap.add_argument("--model", default=DEFAULT_MODEL)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS), help="BASELINE.json workload")
+    ap.add_argument("--envs", type=int, default=0, help="envs per GPU (default: the config's)")
+    ap.add_argument("--model", default="", help="override the config's model")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-envs", type=int, default=0)
@@ -213,6 +244,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    C = dict(CONFIGS[args.config])
+    args.model = args.model or C["model"]
+    args.envs = args.envs or C["envs"]
+    args.C = C
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -226,29 +261,52 @@ def main():
     import torch.distributed as dist
 
     import paper_2603_29332_b200 as pk
+    import paper_2603_29332_b200.dist as pkd
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     mp, cp = model_files(args.model)
     E = args.envs
-    cfg = pk.EnvConfig(episode_horizon=1000, rsi=False)
-    env = pk.EnvBatch(mp, cp, E, cfg=cfg, global_env_offset=rank * E)
-    env.set_eval_mode(True)
+    cfg = pk.EnvConfig(episode_horizon=C["horizon"], rsi=C["rsi"])
+    rcfg = pk.RewardConfig(mode=C["reward_mode"])
+    env = pk.EnvBatch(mp, cp, E, cfg=cfg, reward=rcfg, global_env_offset=rank * E)
+    env.set_eval_mode(C["eval"])
     dev = env.device
     stream = torch.cuda.current_stream(dev)
     actions = torch.empty(E, env.nm, device=dev)
     obs = torch.empty(E, env.obs_dim, device=dev)
     delta = torch.empty(E, env.delta_dim, device=dev)
     raux = torch.empty(E, device=dev)
+    reward = torch.zeros(E, device=dev) if C["disc"] else None
     flags = torch.zeros(E, dtype=torch.uint8, device=dev)
+    if C["disc"]:  # frozen D = Mlp(delta_dim, W, 1, Sigmoid) initialised as Mlp(shape, seed) (nn.cpp:16-38)
+        width, dseed = C["disc"]
+        env.set_discriminator(pk.mlp_init(env.delta_dim, width, dseed), width)
     env.reset(obs=obs)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
     seed = 0x5EED
+    norm_state = None
+    stats = torch.zeros(6, dtype=torch.float64, device=dev)  # count, sum r, sum r^2, done, failed, diverged
 
-    def one_step(s):
+    def one_step(s, ev=None):
+        nonlocal norm_state
         env.fill_excitations(seed, s, actions)
-        env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags)
+        if ev:
+            ev[0].record(stream)
+        env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags, reward=reward)
+        if ev:
+            ev[1].record(stream)
+        if C["exchange"]:
+            r = reward if reward is not None else raux
+            f = flags.to(torch.int32)
+            stats.add_(torch.stack([torch.tensor(float(E), device=dev, dtype=torch.float64),
+                                    r.double().sum(), r.double().square().sum(),
+                                    (f & pk.FLAG_DONE).ne(0).sum().double(), (f & pk.FLAG_FAILED).ne(0).sum().double(),
+                                    (f & pk.FLAG_DIVERGED).ne(0).sum().double()]))
+            if (s + 1) % C["exchange"] == 0:  # iteration boundary (h control steps)
+                _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state)
+                stats.zero_()
         env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
 
     for s in range(args.warmup):
@@ -271,11 +329,7 @@ def main():
     for s in range(args.steps):
         flush.zero_()
         starts[s].record(stream)
-        env.fill_excitations(seed, args.warmup + s, actions)
-        kst[s].record(stream)
-        env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags)
-        ken[s].record(stream)
-        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
+        one_step(args.warmup + s, (kst[s], ken[s]))
         ends[s].record(stream)
     torch.cuda.synchronize()
     t_loop1 = time.monotonic()
@@ -299,27 +353,46 @@ def main():
         hd = torch.empty(E, env.delta_dim, dtype=torch.float32, pin_memory=True)
         hr = torch.empty(E, dtype=torch.float32, pin_memory=True)
         hf = torch.empty(E, dtype=torch.uint8, pin_memory=True)
+        hw = torch.empty(E, dtype=torch.float32, pin_memory=True) if C["disc"] else None
         for _ in range(2):
-            env.step_host(ha, ho, hd, hr, hf)
+            env.step_host(ha, ho, hd, hr, hf, reward_host=hw)
             env.reset(mask=hf.to(dev), mask_bits=pk.FLAG_DONE)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         tt = 0.0
         k2 = max(3, args.steps // 2)
-        for _ in range(k2):
+        for _ in range(k2):  # user loop: step through the host-buffer C ABI, auto-reset done envs
             t0 = time.perf_counter()
-            env.step_host(ha, ho, hd, hr, hf)
-            tt += time.perf_counter() - t0
+            env.step_host(ha, ho, hd, hr, hf, reward_host=hw)
             if hf.any():
-                env.reset(mask=hf.to(dev), mask_bits=pk.FLAG_DONE)
+                env.reset(mask=hf.to(dev, non_blocking=True), mask_bits=pk.FLAG_DONE)
                 torch.cuda.synchronize()
+            tt += time.perf_counter() - t0
         tv = torch.tensor([tt], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tv, op=dist.ReduceOp.MAX)
         e2e = {"value": E * world * k2 / float(tv[0]), "unit": "env-steps/s",
                "h2d_bytes_per_step": E * env.nm * 4,
-               "d2h_bytes_per_step": E * (env.obs_dim + env.delta_dim + 1) * 4 + E}
+               "d2h_bytes_per_step": E * (env.obs_dim + env.delta_dim + 1 + (1 if C["disc"] else 0)) * 4 + E}
+
+    disc = None
+    if C["disc"]:  # the tensor-core kernel alone on this step's Δ (for its own roofline)
+        width = C["disc"][0]
+        rr = torch.empty(E, device=dev)
+        for _ in range(3):
+            env.discriminator_reward(delta, reward=rr)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 50
+        e0.record(stream)
+        for _ in range(reps):
+            env.discriminator_reward(delta, reward=rr)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        dms = e0.elapsed_time(e1) / reps
+        flops = 2.0 * (env.delta_dim * width + 2 * width * width + width) * E
+        disc = {"kernel": "disc_reward_kernel (tcgen05 kind::f16, bf16 operands, fp32 TMEM accumulate)",
+                "width": width, "ms": dms, "flops_per_launch": flops}
 
     if rank == 0:
         cm = cost_model(mp)
@@ -356,15 +429,21 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (f64 q/qdot, sampler)",
             "data": "synthetic (Philox excitations, generated dance clip, random-init model)",
-            "config": {"workload": f"{args.model}: 80 links, 700 muscles, no contacts, eval mode, random excitations",
-                       "envs_per_gpu": E, "global_envs": E * world, "clip": CLIPS[args.model],
-                       "parallelism": f"env shards x{world}", "l2": "flushed between timed steps"},
+            "config": {"workload": C["desc"] if args.model == C["model"] else f"{args.config} with model {args.model}",
+                       "config": args.config, "envs_per_gpu": E, "global_envs": E * world,
+                       "clip": CLIPS[args.model], "parallelism": f"env shards x{world}",
+                       "l2": "flushed between timed steps"},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                          "bytes_per_env_step": cm["bytes_per_env_step"], "step_kernel_ms": kms,
                          "note": "path is FP32-issue bound (SURVEY §8(d)); see fp32", "fp32": fp32},
             "cpu_baseline": cpu,
             "e2e": e2e,
+            **({"disc_kernel": dict(disc, achieved_tflops=disc["flops_per_launch"] / (disc["ms"] * 1e-3) / 1e12,
+                                    peak_tflops=float(peaks.get("bf16_tflops", 2250.0)),
+                                    frac=disc["flops_per_launch"] / (disc["ms"] * 1e-3) / 1e12
+                                    / float(peaks.get("bf16_tflops", 2250.0)), bound="tensor")}
+               if disc else {}),
             "gpu_launches": launches,
             "clocks": summarize_clocks(clk_lines, t_loop0, t_loop1),
         }

@@ -123,6 +123,10 @@ int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delt
  * W column-major).  hidden: multiple of 16 in [16, 256].  Evaluated on the
  * tcgen05 tensor cores with bf16 operands and fp32 accumulation. */
 int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_params, int32_t hidden);
+/* Host helpers for the parameter blob: Mlp(in, hidden, out) parameter count and
+ * the Mlp(shape, seed) initialisation (nn.cpp:16-38, msk::Rng = mt19937_64). */
+int64_t msk_mlp_param_count(int32_t in, int32_t hidden, int32_t out);
+int msk_mlp_init(double* theta, int32_t in, int32_t hidden, int32_t out, uint64_t seed, double final_init_scale);
 int msk_gpu_clear_discriminator(msk_gpu_ctx* ctx);
 /* reward[i] = r(D(delta_i)) for n rows of delta [n x delta_dim]. */
 int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n, float* reward, void* stream);
@@ -140,6 +144,10 @@ int msk_gpu_step_rewarded(msk_gpu_ctx* ctx, const float* actions, float* obs, fl
  * PCIe transfers overlap the step kernel.  Synchronous on return. */
 int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                       float* reward_aux_host, uint8_t* flags_host);
+/* Host-buffer Env::step(action, fn) with the discriminator reward (see
+ * msk_gpu_step_rewarded); reward_host [E] required. */
+int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                               float* reward_host, float* reward_aux_host, uint8_t* flags_host);
 
 int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream);
 int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream);

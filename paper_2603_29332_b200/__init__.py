@@ -14,12 +14,25 @@ import ctypes as C
 import os
 from dataclasses import dataclass, field
 
-__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError",
+__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError", "mlp_init",
            "FLAG_DONE", "FLAG_FAILED", "FLAG_DIVERGED", "FLAG_NOT_STEPPED", "FLAG_BAD_ACTION"]
 
 LIB_PATH = os.environ.get("MSK_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmsk_b200.so")
 
 FLAG_DONE, FLAG_FAILED, FLAG_DIVERGED, FLAG_NOT_STEPPED, FLAG_BAD_ACTION = 1, 2, 4, 8, 16
+
+
+def mlp_init(n_in, hidden, seed, n_out=1, final_init_scale=1.0):
+    """Mlp(MlpShape{n_in, hidden, n_out}, seed) flat f64 parameters (nn.cpp:16-38)."""
+    import numpy as np
+
+    n = lib().msk_mlp_param_count(n_in, hidden, n_out)
+    if n < 0:
+        raise ValueError("bad Mlp shape")
+    theta = np.zeros(n)
+    if lib().msk_mlp_init(theta.ctypes.data, n_in, hidden, n_out, C.c_uint64(seed), float(final_init_scale)) != 0:
+        raise MskError(lib().msk_gpu_last_error(None).decode())
+    return theta
 
 
 class MskError(RuntimeError):
@@ -96,7 +109,11 @@ def lib():
         L.msk_gpu_reset_to_frame.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+        L.msk_gpu_step_host_rewarded.argtypes = [_vp] * 7
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
+        L.msk_mlp_param_count.restype = C.c_int64
+        L.msk_mlp_param_count.argtypes = [C.c_int32, C.c_int32, C.c_int32]
+        L.msk_mlp_init.argtypes = [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_double]
         L.msk_gpu_clear_discriminator.argtypes = [_vp]
         L.msk_gpu_discriminator_reward.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_step_rewarded.argtypes = [_vp] * 10
@@ -263,8 +280,14 @@ class EnvBatch:
                                     self._s(stream)))
         return out
 
-    def step_host(self, actions_host, obs_host=None, delta_host=None, reward_aux_host=None, flags_host=None):
-        """Env::step with HOST (ideally pinned) tensors; synchronous, pipelined H2D/kernel/D2H."""
+    def step_host(self, actions_host, obs_host=None, delta_host=None, reward_aux_host=None, flags_host=None,
+                  reward_host=None):
+        """Env::step with HOST (ideally pinned) tensors; synchronous, pipelined H2D/kernel/D2H.
+        With reward_host (and a discriminator set): Env::step(action, fn)."""
+        if reward_host is not None:
+            self._ck(lib().msk_gpu_step_host_rewarded(self.h, _p(actions_host), _p(obs_host), _p(delta_host),
+                                                      _p(reward_host), _p(reward_aux_host), _p(flags_host)))
+            return
         self._ck(lib().msk_gpu_step_host(self.h, _p(actions_host), _p(obs_host), _p(delta_host),
                                          _p(reward_aux_host), _p(flags_host)))
 

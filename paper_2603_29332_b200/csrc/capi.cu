@@ -5,7 +5,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <cmath>
 #include <exception>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -82,6 +84,7 @@ struct msk_gpu_ctx {
     float* h_delta = nullptr;
     float* h_raux = nullptr;
     uint8_t* h_flags = nullptr;
+    float* h_reward = nullptr;
     double* global_ema = nullptr;
     // device discriminator (msk_gpu_set_discriminator)
     DiscDev disc{};
@@ -480,6 +483,34 @@ int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_p
     });
 }
 
+int64_t msk_mlp_param_count(int32_t in, int32_t hidden, int32_t out) {
+    if (in < 1 || hidden < 1 || out < 1) return -1;
+    return static_cast<int64_t>(hidden) * in + hidden + 2 * (static_cast<int64_t>(hidden) * hidden + hidden) +
+           static_cast<int64_t>(out) * hidden + out;
+}
+
+int msk_mlp_init(double* theta, int32_t in, int32_t hidden, int32_t out, uint64_t seed, double final_init_scale) {
+    // Mlp::Mlp(shape, seed) (nn.cpp:16-38) with msk::Rng (rng.hpp:13-30): W(i, j)
+    // ~ uniform(-s, s) in column-major order, s = 1/sqrt(cols) (x final_init_scale
+    // on the head), biases zero.
+    const int64_t n = msk_mlp_param_count(in, hidden, out);
+    if (!theta || n < 0) return fail(nullptr, MSK_ERR_CONTRACT, "msk_mlp_init: bad shape");
+    std::mt19937_64 eng(seed);
+    const int dims[4][2] = {{hidden, in}, {hidden, hidden}, {hidden, hidden}, {out, hidden}};
+    int64_t off = 0;
+    for (int l = 0; l < 4; ++l) {
+        const int r = dims[l][0], c = dims[l][1];
+        const double s = (1.0 / std::sqrt(static_cast<double>(c))) * (l == 3 ? final_init_scale : 1.0);
+        for (int j = 0; j < c; ++j)
+            for (int i = 0; i < r; ++i)
+                theta[off + static_cast<int64_t>(j) * r + i] = -s + (s - -s) * (static_cast<double>(eng() >> 11) * 0x1.0p-53);
+        off += static_cast<int64_t>(r) * c;
+        for (int i = 0; i < r; ++i) theta[off + i] = 0.0;
+        off += r;
+    }
+    return MSK_OK;
+}
+
 int msk_gpu_clear_discriminator(msk_gpu_ctx* ctx) {
     return guarded(ctx, [&] {
         ck(cudaDeviceSynchronize(), "clear_discriminator");
@@ -518,55 +549,82 @@ int msk_gpu_step_rewarded(msk_gpu_ctx* ctx, const float* actions, float* obs, fl
     });
 }
 
+namespace {
+
+// Host-buffer step, optionally with the discriminator reward.  Chunked
+// pipeline: H2D(actions c) -> step(c) [-> D(c)] -> D2H(outputs c), chunks on
+// separate streams so chunk c's transfers overlap the other chunks' kernels.
+void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                    float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
+    if (!actions_host) throw ConfigError("step_host: actions is null");
+    if (reward_host && !ctx->disc.w1) throw ConfigError("step_host: reward requested but no discriminator set");
+    const size_t E = static_cast<size_t>(ctx->n_envs);
+    const int nm = ctx->cm.nm;
+    if (!ctx->hs[0]) {
+        ctx->host_chunks = host_knob("MSK_HOST_CHUNKS", 4, 1, 64);
+        ctx->host_streams = host_knob("MSK_HOST_STREAMS", 4, 1, kMaxHostStreams);
+        for (int i = 0; i < ctx->host_streams; ++i)
+            ck(cudaStreamCreateWithFlags(&ctx->hs[i], cudaStreamNonBlocking), "stream");
+        ctx->h_actions = ctx->dalloc<float>(E * nm);
+        ctx->h_obs = ctx->dalloc<float>(E * ctx->obs_dim);
+        ctx->h_delta = ctx->dalloc<float>(E * ctx->delta_dim);
+        ctx->h_raux = ctx->dalloc<float>(E);
+        ctx->h_flags = ctx->dalloc<uint8_t>(E);
+        ctx->h_reward = ctx->dalloc<float>(E);
+    }
+    const int chunks = static_cast<int>(std::min<size_t>(ctx->host_chunks, E));
+    const size_t per = (E + chunks - 1) / chunks;
+    for (int c = 0; c < chunks; ++c) {
+        const size_t e0 = c * per, n = std::min(per, E - e0);
+        if (n == 0) break;
+        cudaStream_t s = ctx->hs[c % ctx->host_streams];
+        ck(cudaMemcpyAsync(ctx->h_actions + e0 * nm, actions_host + e0 * nm, n * nm * sizeof(float),
+                           cudaMemcpyHostToDevice, s),
+           "H2D actions");
+        launch_step(ctx->M, ctx->St, static_cast<int>(e0), static_cast<int>(n), ctx->h_actions + e0 * nm,
+                    ctx->h_obs + e0 * ctx->obs_dim, ctx->h_delta + e0 * ctx->delta_dim, ctx->h_raux + e0,
+                    ctx->h_flags + e0, nullptr, nullptr, s);
+        ctx->count();
+        ctx->check_launch();
+        if (reward_host) {
+            ck(launch_disc(ctx->disc, ctx->h_delta + e0 * ctx->delta_dim, ctx->delta_dim, static_cast<int>(n),
+                           ctx->h_raux + e0, ctx->h_flags + e0, ctx->h_reward + e0, s, true),
+               "launch discriminator");
+            ctx->count();
+            ck(cudaMemcpyAsync(reward_host + e0, ctx->h_reward + e0, n * sizeof(float), cudaMemcpyDeviceToHost, s),
+               "D2H reward");
+        }
+        if (obs_host)
+            ck(cudaMemcpyAsync(obs_host + e0 * ctx->obs_dim, ctx->h_obs + e0 * ctx->obs_dim,
+                               n * ctx->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s),
+               "D2H obs");
+        if (delta_host)
+            ck(cudaMemcpyAsync(delta_host + e0 * ctx->delta_dim, ctx->h_delta + e0 * ctx->delta_dim,
+                               n * ctx->delta_dim * sizeof(float), cudaMemcpyDeviceToHost, s),
+               "D2H delta");
+        if (reward_aux_host)
+            ck(cudaMemcpyAsync(reward_aux_host + e0, ctx->h_raux + e0, n * sizeof(float), cudaMemcpyDeviceToHost, s),
+               "D2H reward_aux");
+        if (flags_host)
+            ck(cudaMemcpyAsync(flags_host + e0, ctx->h_flags + e0, n, cudaMemcpyDeviceToHost, s), "D2H flags");
+    }
+    for (int i = 0; i < ctx->host_streams; ++i) ck(cudaStreamSynchronize(ctx->hs[i]), "step_host sync");
+}
+
+}  // namespace
+
 int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                       float* reward_aux_host, uint8_t* flags_host) {
     return guarded(ctx, [&] {
-        if (!actions_host) throw ConfigError("step_host: actions is null");
-        const size_t E = static_cast<size_t>(ctx->n_envs);
-        const int nm = ctx->cm.nm;
-        if (!ctx->hs[0]) {
-            ctx->host_chunks = host_knob("MSK_HOST_CHUNKS", 4, 1, 64);
-            ctx->host_streams = host_knob("MSK_HOST_STREAMS", 4, 1, kMaxHostStreams);
-            for (int i = 0; i < ctx->host_streams; ++i)
-                ck(cudaStreamCreateWithFlags(&ctx->hs[i], cudaStreamNonBlocking), "stream");
-            ctx->h_actions = ctx->dalloc<float>(E * nm);
-            ctx->h_obs = ctx->dalloc<float>(E * ctx->obs_dim);
-            ctx->h_delta = ctx->dalloc<float>(E * ctx->delta_dim);
-            ctx->h_raux = ctx->dalloc<float>(E);
-            ctx->h_flags = ctx->dalloc<uint8_t>(E);
-        }
-        // Chunked pipeline: H2D(actions c) -> step(c) -> D2H(outputs c), two
-        // streams so chunk c's transfers overlap chunk c-1's kernel.
-        const int chunks = static_cast<int>(std::min<size_t>(ctx->host_chunks, E));
-        const size_t per = (E + chunks - 1) / chunks;
-        for (int c = 0; c < chunks; ++c) {
-            const size_t e0 = c * per, n = std::min(per, E - e0);
-            if (n == 0) break;
-            cudaStream_t s = ctx->hs[c % ctx->host_streams];
-            ck(cudaMemcpyAsync(ctx->h_actions + e0 * nm, actions_host + e0 * nm, n * nm * sizeof(float),
-                               cudaMemcpyHostToDevice, s),
-               "H2D actions");
-            launch_step(ctx->M, ctx->St, static_cast<int>(e0), static_cast<int>(n), ctx->h_actions + e0 * nm,
-                        ctx->h_obs + e0 * ctx->obs_dim, ctx->h_delta + e0 * ctx->delta_dim, ctx->h_raux + e0,
-                        ctx->h_flags + e0, nullptr, nullptr, s);
-            ctx->count();
-            ctx->check_launch();
-            if (obs_host)
-                ck(cudaMemcpyAsync(obs_host + e0 * ctx->obs_dim, ctx->h_obs + e0 * ctx->obs_dim,
-                                   n * ctx->obs_dim * sizeof(float), cudaMemcpyDeviceToHost, s),
-                   "D2H obs");
-            if (delta_host)
-                ck(cudaMemcpyAsync(delta_host + e0 * ctx->delta_dim, ctx->h_delta + e0 * ctx->delta_dim,
-                                   n * ctx->delta_dim * sizeof(float), cudaMemcpyDeviceToHost, s),
-                   "D2H delta");
-            if (reward_aux_host)
-                ck(cudaMemcpyAsync(reward_aux_host + e0, ctx->h_raux + e0, n * sizeof(float), cudaMemcpyDeviceToHost,
-                                   s),
-                   "D2H reward_aux");
-            if (flags_host)
-                ck(cudaMemcpyAsync(flags_host + e0, ctx->h_flags + e0, n, cudaMemcpyDeviceToHost, s), "D2H flags");
-        }
-        for (int i = 0; i < ctx->host_streams; ++i) ck(cudaStreamSynchronize(ctx->hs[i]), "step_host sync");
+        step_host_impl(ctx, actions_host, obs_host, delta_host, nullptr, reward_aux_host, flags_host);
+    });
+}
+
+int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                               float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
+    return guarded(ctx, [&] {
+        if (!reward_host) throw ConfigError("step_host_rewarded: reward is null");
+        step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host);
     });
 }
 

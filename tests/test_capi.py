@@ -126,3 +126,19 @@ def test_no_cpu_fallback_without_gpu(assets):
     with pytest.raises(pk.MskError) as ei:
         pk.EnvBatch(mp, cp, 4, device=0)
     assert ei.value.code == 3
+
+
+def test_host_mlp_init_matches_oracle_and_reference_rng():
+    """msk_mlp_init (host C++, product side) == the oracle's Mlp init, which the
+    golden fixture pins to the reference's Rng stream (nn.cpp:16-38)."""
+    import numpy as np
+
+    import paper_2603_29332_b200 as pk
+    from oracle.oracle import mlp_init
+
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mlp_seed7.npz"))
+    assert np.array_equal(pk.mlp_init(9, 16, 7), g["small"])
+    big = pk.mlp_init(102, 256, 7)
+    assert np.array_equal(big, mlp_init(102, 256, 7))
+    assert np.array_equal(big[:512], g["big_head"]) and np.sum(big) == g["big_sum"][0]
+    assert np.array_equal(pk.mlp_init(5, 32, 1, final_init_scale=0.0)[-33:], np.zeros(33))
