@@ -286,28 +286,32 @@ def main():
     env.reset(obs=obs)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MB > 126 MB L2
     seed = 0x5EED
-    norm_state = None
-    stats = torch.zeros(6, dtype=torch.float64, device=dev)  # count, sum r, sum r^2, done, failed, diverged
+    norm_state = pkd.init_norm_state(env.obs_dim, dev)
+    # rollout stats (dist.py N_STATS): steps, sum r, sum r^2, sum episode length, episodes, failures, divergences
+    stats = torch.zeros(pkd.N_STATS, dtype=torch.float64, device=dev)
 
     def one_step(s, ev=None):
+        """One control step of the workload; ev (optional) = [start, excitations, step, stats,
+        exchange, reset] events recorded at the phase boundaries."""
         nonlocal norm_state
         env.fill_excitations(seed, s, actions)
         if ev:
-            ev[0].record(stream)
+            ev[1].record(stream)
         env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags, reward=reward)
         if ev:
-            ev[1].record(stream)
+            ev[2].record(stream)
         if C["exchange"]:
-            r = reward if reward is not None else raux
-            f = flags.to(torch.int32)
-            stats.add_(torch.stack([torch.tensor(float(E), device=dev, dtype=torch.float64),
-                                    r.double().sum(), r.double().square().sum(),
-                                    (f & pk.FLAG_DONE).ne(0).sum().double(), (f & pk.FLAG_FAILED).ne(0).sum().double(),
-                                    (f & pk.FLAG_DIVERGED).ne(0).sum().double()]))
-            if (s + 1) % C["exchange"] == 0:  # iteration boundary (h control steps)
-                _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state)
-                stats.zero_()
+            env.rollout_stats(flags, stats, reward=reward if reward is not None else raux)
+        if ev:
+            ev[3].record(stream)
+        if C["exchange"] and (s + 1) % C["exchange"] == 0:  # iteration boundary (h control steps)
+            _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state)
+            stats.zero_()
+        if ev:
+            ev[4].record(stream)
         env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
+        if ev:
+            ev[5].record(stream)
 
     for s in range(args.warmup):
         one_step(s)
@@ -319,24 +323,22 @@ def main():
     th.start()
     time.sleep(0.3)
     # timed region: per-step CUDA events (L2 flushed between steps, outside the events)
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    kst = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ken = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(args.steps)]
     n0 = env.launch_count
     torch.cuda.synchronize()
     t_loop0 = time.monotonic()
     for s in range(args.steps):
         flush.zero_()
-        starts[s].record(stream)
-        one_step(args.warmup + s, (kst[s], ken[s]))
-        ends[s].record(stream)
+        evs[s][0].record(stream)
+        one_step(args.warmup + s, evs[s])
     torch.cuda.synchronize()
     t_loop1 = time.monotonic()
     launches = env.launch_count - n0
     stop.set()
-    ms = sum(a.elapsed_time(b) for a, b in zip(starts, ends))
-    kms = sum(a.elapsed_time(b) for a, b in zip(kst, ken)) / args.steps
+    ms = sum(e[0].elapsed_time(e[5]) for e in evs)
+    kms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    phases = {name: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps
+              for i, name in enumerate(["excitations", "step", "rollout_stats", "iteration_exchange", "reset"])}
     t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -445,6 +447,7 @@ def main():
                                     / float(peaks.get("bf16_tflops", 2250.0)), bound="tensor")}
                if disc else {}),
             "gpu_launches": launches,
+            "phases_ms_per_step": phases,
             "clocks": summarize_clocks(clk_lines, t_loop0, t_loop1),
         }
         print(json.dumps(line), flush=True)

@@ -174,6 +174,14 @@ int msk_gpu_record_own_outcomes(msk_gpu_ctx* ctx, void* stream);
  * global env order (e.g. the allgather of every rank's drain) are recorded in
  * env order then time order into ONE sampler, which is then copied to every
  * local env.  Identical on every rank, so replicas stay bit-identical. */
+/* Iteration-boundary reductions for the per-rank stats block:
+ * stats[7] += {env-steps, Σreward, Σreward², Σ episode length of envs done this
+ * step, episodes, failures, divergences} over the envs stepped (flags from
+ * msk_gpu_step; reward nullable); deterministic single-block reduction. */
+int msk_gpu_rollout_stats(msk_gpu_ctx* ctx, const float* reward, const uint8_t* flags, double* stats, void* stream);
+/* Batch moments of obs [n x obs_dim] (RunningNorm::update's batch mean and
+ * population variance, nn.cpp:246-256) in f64: out = [n, mean[D], var[D]]. */
+int msk_gpu_obs_moments(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream);
 int msk_gpu_merge_outcomes(msk_gpu_ctx* ctx, const int32_t* bins, const uint8_t* failed, const int32_t* counts,
                            int64_t n_envs_total, int32_t cap, void* stream);
 

@@ -110,6 +110,8 @@ def lib():
         L.msk_gpu_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step_host_rewarded.argtypes = [_vp] * 7
+        L.msk_gpu_rollout_stats.argtypes = [_vp] * 5
+        L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
         L.msk_mlp_param_count.restype = C.c_int64
         L.msk_mlp_param_count.argtypes = [C.c_int32, C.c_int32, C.c_int32]
@@ -355,6 +357,19 @@ class EnvBatch:
         n_total, cap = bins.shape
         self._ck(lib().msk_gpu_merge_outcomes(self.h, _p(bins.contiguous()), _p(failed.contiguous()),
                                               _p(counts.contiguous()), int(n_total), int(cap), self._s(stream)))
+
+    def rollout_stats(self, flags, stats, reward=None, stream=None):
+        """stats[7] (f64, device) += this step's rollout statistics (see msk_gpu_rollout_stats)."""
+        self._ck(lib().msk_gpu_rollout_stats(self.h, _p(reward), _p(flags), _p(stats), self._s(stream)))
+        return stats
+
+    def obs_moments(self, obs, out=None, stream=None):
+        """[n, mean[D], var[D]] (f64, device) of an [n x obs_dim] observation batch."""
+        n = obs.shape[0]
+        out = out if out is not None else self.torch.empty(1 + 2 * self.obs_dim, dtype=self.torch.float64,
+                                                           device=self.device)
+        self._ck(lib().msk_gpu_obs_moments(self.h, _p(obs.contiguous()), int(n), _p(out), self._s(stream)))
+        return out
 
     def rng_raw(self, env, n, stream=None):
         out = self._empty(n, dtype=self.torch.int64)  # raw u64 bits; view as uint64 on the host

@@ -34,6 +34,10 @@ void launch_drain(const DevState&, int n, int cap, int* bins, uint8_t* failed, i
 void launch_get_ints(const DevState&, int n, int* ints, cudaStream_t);
 void launch_set_ints(const DevState&, int n, const int* ints, cudaStream_t);
 void launch_permute_muscles(const DevModel&, int n, const float* src, float* dst, int to_internal, cudaStream_t);
+void launch_rollout_stats(const DevState&, int n, const float* reward, const uint8_t* flags, double* stats,
+                          cudaStream_t);
+int obs_moments_chunks(int n);
+void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t);
 void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint32_t step, float* out,
                         cudaStream_t);
 double measure_fp32_peak_tflops();
@@ -85,6 +89,8 @@ struct msk_gpu_ctx {
     float* h_raux = nullptr;
     uint8_t* h_flags = nullptr;
     float* h_reward = nullptr;
+    double* mom_part = nullptr;  // obs-moment partials (msk_gpu_obs_moments)
+    size_t mom_cap = 0;
     double* global_ema = nullptr;
     // device discriminator (msk_gpu_set_discriminator)
     DiscDev disc{};
@@ -734,6 +740,30 @@ int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int
         if (!bins || !failed || !counts || cap < 0) throw ConfigError("drain_outcomes: bad arguments");
         launch_drain(ctx->St, ctx->n_envs, cap, bins, failed, counts, as_stream(stream));
         ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_rollout_stats(msk_gpu_ctx* ctx, const float* reward, const uint8_t* flags, double* stats,
+                          void* stream) {
+    return guarded(ctx, [&] {
+        if (!flags || !stats) throw ConfigError("rollout_stats: flags and stats are required");
+        launch_rollout_stats(ctx->St, ctx->n_envs, reward, flags, stats, as_stream(stream));
+        ctx->count();
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_obs_moments(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream) {
+    return guarded(ctx, [&] {
+        if (!obs || !out || n < 0) throw ConfigError("obs_moments: bad arguments");
+        const size_t need = static_cast<size_t>(obs_moments_chunks(n)) * ctx->obs_dim * 2;
+        if (need > ctx->mom_cap) {
+            ctx->mom_part = ctx->dalloc<double>(need);
+            ctx->mom_cap = need;
+        }
+        launch_obs_moments(obs, n, ctx->obs_dim, ctx->mom_part, out, as_stream(stream));
+        ctx->count(2);
         ctx->check_launch();
     });
 }

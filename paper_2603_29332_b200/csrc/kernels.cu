@@ -1121,15 +1121,54 @@ __global__ void record_own_kernel(DevModel M, DevState St, int n_envs) {
 }
 
 // Ordered merge into one sampler (env order, then time order), then broadcast.
-__global__ void merge_kernel(DevModel M, DevState St, int n_local, const int* bins, const uint8_t* failed,
-                             const int* counts, long long n_total, int cap, double* global_ema) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        for (long long g = 0; g < n_total; ++g) {
-            const int n = min(counts[g], cap);
-            for (int i = 0; i < n; ++i)
-                sampler_record(global_ema, M.bins, M.decay, bins[g * cap + i], failed[g * cap + i]);
+// Ordered merge of all ranks' outcomes into the global sampler EMA (global env
+// order, then time order — the sequential AdaptiveSampler::record of
+// env.cpp:34-37).  Bins are independent, so thread b < bins applies, in order,
+// exactly the outcomes of bin b (bit-identical to the sequential loop); the
+// block compacts each 1024-env chunk's outcomes into shared memory with a
+// block-wide scan so the per-bin passes read contiguous smem.
+constexpr int kMergeThreads = 1024, kMergeList = 4096;
+
+__global__ void __launch_bounds__(kMergeThreads) merge_kernel(DevModel M, const int* bins, const uint8_t* failed,
+                                                              const int* counts, long long n_total, int cap,
+                                                              double* global_ema) {
+    __shared__ int s_bin[kMergeList];
+    __shared__ uint8_t s_fail[kMergeList];
+    __shared__ int s_scan[kMergeThreads];
+    const int tid = threadIdx.x;
+    double ema = tid < M.bins ? global_ema[tid] : 0.0;
+    const double keep = M.decay, gain = __dsub_rn(1.0, M.decay);
+    for (long long base = 0; base < n_total; base += kMergeThreads) {
+        const long long g = base + tid;
+        const int c = g < n_total ? max(0, min(counts[g], cap)) : 0;
+        s_scan[tid] = c;  // inclusive Hillis-Steele scan of the chunk's counts
+        __syncthreads();
+        for (int o = 1; o < kMergeThreads; o <<= 1) {
+            const int v = tid >= o ? s_scan[tid - o] : 0;
+            __syncthreads();
+            s_scan[tid] += v;
+            __syncthreads();
         }
+        const int off = s_scan[tid] - c, tot = s_scan[kMergeThreads - 1];
+        for (int p0 = 0; p0 < tot; p0 += kMergeList) {
+            for (int i = 0; i < c; ++i) {
+                const int idx = off + i - p0;
+                if (idx >= 0 && idx < kMergeList) {
+                    s_bin[idx] = bins[g * cap + i];
+                    s_fail[idx] = failed[g * cap + i];
+                }
+            }
+            __syncthreads();
+            if (tid < M.bins) {
+                const int n = min(kMergeList, tot - p0);
+                for (int j = 0; j < n; ++j)
+                    if (s_bin[j] == tid) ema = __dadd_rn(__dmul_rn(keep, ema), __dmul_rn(gain, s_fail[j] ? 1.0 : 0.0));
+            }
+            __syncthreads();
+        }
+        __syncthreads();
     }
+    if (tid < M.bins) global_ema[tid] = ema;
 }
 
 __global__ void broadcast_ema_kernel(DevState St, int n_envs, int bins, const double* row) {
@@ -1367,13 +1406,106 @@ void launch_record_own(const DevModel& M, const DevState& St, int n, cudaStream_
 
 void launch_merge(const DevModel& M, const DevState& St, int n_local, const int* bins, const uint8_t* failed,
                   const int* counts, long long n_total, int cap, double* global_ema, cudaStream_t s) {
-    merge_kernel<<<1, 32, 0, s>>>(M, St, n_local, bins, failed, counts, n_total, cap, global_ema);
+    merge_kernel<<<1, kMergeThreads, 0, s>>>(M, bins, failed, counts, n_total, cap, global_ema);
     const int tot = n_local * M.bins;
     broadcast_ema_kernel<<<(tot + 255) / 256, 256, 0, s>>>(St, n_local, M.bins, global_ema);
 }
 
 void launch_broadcast_ema(const DevState& St, int n, int bins, const double* row, cudaStream_t s) {
     broadcast_ema_kernel<<<(n * bins + 255) / 256, 256, 0, s>>>(St, n, bins, row);
+}
+
+// ---- iteration-boundary reductions (SURVEY §8(e) block contents) ----------
+// Rollout statistics of one control step, added into stats[7] = {env-steps,
+// Σr, Σr², Σ episode length (done envs), episodes, failures, divergences}.
+// One block, fixed-order tree reduction: deterministic.
+__global__ void __launch_bounds__(1024) rollout_stats_kernel(DevState St, int n, const float* reward,
+                                                             const uint8_t* flags, double* stats) {
+    __shared__ double red[7][32];
+    double a[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+        const uint8_t f = flags[e];
+        if (f & (kFlagNotStepped | kFlagBadAction)) continue;
+        const double r = reward ? static_cast<double>(reward[e]) : 0.0;
+        a[0] += 1.0;
+        a[1] += r;
+        a[2] += r * r;
+        if (f & kFlagDone) {
+            a[3] += static_cast<double>(St.steps[e]);
+            a[4] += 1.0;
+        }
+        if (f & kFlagFailed) a[5] += 1.0;
+        if (f & kFlagDiverged) a[6] += 1.0;
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        double v = a[k];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[k][warp] = v;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            double v = lane < nw ? red[k][lane] : 0.0;
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) stats[k] += v;
+        }
+    }
+}
+
+// Column moments of an [n x D] f32 batch in f64 (RunningNorm::update's batch
+// terms, nn.cpp:246-256): pass 1 gives per row-chunk (mean, M2) per column
+// (two passes over the chunk, L2-resident); pass 2 merges the chunks in order
+// (Chan et al.), writing out = [n, mean[D], var[D]] (population variance).
+constexpr int kMomRows = 256;
+
+__global__ void obs_moments_part_kernel(const float* x, int n, int D, double* part) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+    if (c >= D) return;
+    const int r0 = k * kMomRows, r1 = min(n, r0 + kMomRows);
+    double s = 0.0;
+    for (int r = r0; r < r1; ++r) s += static_cast<double>(x[static_cast<size_t>(r) * D + c]);
+    const double mean = s / static_cast<double>(r1 - r0);
+    double m2 = 0.0;
+    for (int r = r0; r < r1; ++r) {
+        const double d = static_cast<double>(x[static_cast<size_t>(r) * D + c]) - mean;
+        m2 += d * d;
+    }
+    part[(static_cast<size_t>(k) * D + c) * 2] = mean;
+    part[(static_cast<size_t>(k) * D + c) * 2 + 1] = m2;
+}
+
+__global__ void obs_moments_merge_kernel(const double* part, int n, int D, int chunks, double* out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c == 0) out[0] = static_cast<double>(n);
+    if (c >= D) return;
+    double cnt = 0.0, mean = 0.0, m2 = 0.0;
+    for (int k = 0; k < chunks; ++k) {
+        const double nk = static_cast<double>(min(n - k * kMomRows, kMomRows));
+        const double mk = part[(static_cast<size_t>(k) * D + c) * 2], qk = part[(static_cast<size_t>(k) * D + c) * 2 + 1];
+        const double tot = cnt + nk, d = mk - mean;
+        mean += d * (nk / tot);
+        m2 += qk + d * d * (cnt * nk / tot);
+        cnt = tot;
+    }
+    out[1 + c] = mean;
+    out[1 + D + c] = n > 0 ? m2 / static_cast<double>(n) : 0.0;
+}
+
+void launch_rollout_stats(const DevState& St, int n, const float* reward, const uint8_t* flags, double* stats,
+                          cudaStream_t s) {
+    rollout_stats_kernel<<<1, 1024, 0, s>>>(St, n, reward, flags, stats);
+}
+
+int obs_moments_chunks(int n) { return (n + kMomRows - 1) / kMomRows; }
+
+void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t s) {
+    const int chunks = obs_moments_chunks(n);
+    if (chunks > 0) obs_moments_part_kernel<<<dim3((D + 127) / 128, chunks), 128, 0, s>>>(x, n, D, part);
+    obs_moments_merge_kernel<<<(D + 127) / 128, 128, 0, s>>>(part, n, D, chunks, out);
 }
 
 void launch_drain(const DevState& St, int n, int cap, int* bins, uint8_t* failed, int* counts, cudaStream_t s) {

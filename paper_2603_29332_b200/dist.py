@@ -126,6 +126,26 @@ def exchange(block: torch.Tensor, group=None):
     return out
 
 
+def running_norm_fold_t(count, mean, var, n, bmean, bvar):
+    """running_norm_fold on device tensors (0-d count / n), no host sync; the
+    count == 0 branch takes the batch moments exactly, as nn.cpp:257-262."""
+    tot = count + n
+    delta = bmean - mean
+    var_m = (var * count + bvar * n + delta * delta * (count * n / tot)) / tot
+    mean_m = mean + delta * (n / tot)
+    first = count == 0.0
+    keep = n == 0.0
+    mean = torch.where(keep, mean, torch.where(first, bmean, mean_m))
+    var = torch.where(keep, var, torch.where(first, bvar, var_m))
+    return torch.where(keep, count, tot), mean, var
+
+
+def init_norm_state(obs_dim, device):
+    """RunningNorm(dim) on the device: count 0, mean 0, var 1 (nn.hpp:88-93)."""
+    return (torch.zeros((), dtype=torch.float64, device=device), torch.zeros(obs_dim, dtype=torch.float64, device=device),
+            torch.ones(obs_dim, dtype=torch.float64, device=device))
+
+
 def merged_iteration(blocks, n_envs, cap, obs_dim, norm_state, ema, decay, merge_on_device=None):
     """Applies the rank-ordered merge to the gathered blocks.
 
@@ -133,12 +153,18 @@ def merged_iteration(blocks, n_envs, cap, obs_dim, norm_state, ema, decay, merge
     (an EnvBatch) is given, the outcome merge runs on the GPU
     (msk_gpu_merge_outcomes) and ``ema`` is ignored."""
     parts = [unpack_block(b, n_envs, cap, obs_dim) for b in blocks]
-    stats = torch.zeros(N_STATS, dtype=torch.float64)
     count, mean, var = norm_state
+    on_device = torch.is_tensor(mean)
+    stats = torch.zeros(N_STATS, dtype=torch.float64, device=mean.device if on_device else "cpu")
     for p in parts:  # rank order
-        stats += p["stats"].cpu()
-        nm = p["norm"].cpu().numpy()
-        count, mean, var = running_norm_fold(count, mean, var, nm[0], nm[1:1 + obs_dim], nm[1 + obs_dim:])
+        if on_device:  # fold on the device: no host round trip at the iteration boundary
+            stats += p["stats"]
+            nm = p["norm"]
+            count, mean, var = running_norm_fold_t(count, mean, var, nm[0], nm[1:1 + obs_dim], nm[1 + obs_dim:])
+        else:
+            stats += p["stats"].cpu()
+            nm = p["norm"].cpu().numpy()
+            count, mean, var = running_norm_fold(count, mean, var, nm[0], nm[1:1 + obs_dim], nm[1 + obs_dim:])
     bins = torch.cat([p["bins"] for p in parts])
     failed = torch.cat([p["failed"] for p in parts])
     counts = torch.cat([p["counts"] for p in parts])
@@ -153,7 +179,7 @@ def merged_iteration(blocks, n_envs, cap, obs_dim, norm_state, ema, decay, merge
 def iteration_exchange(env, rollout_stats: torch.Tensor, obs_batch: torch.Tensor, norm_state, cap=64, group=None):
     """One iteration boundary on a GPU rank: drain, pack, all_gather, ordered merge (device sampler)."""
     bins, failed, counts = env.drain_outcomes(cap)
-    norm = batch_moments(obs_batch)
+    norm = env.obs_moments(obs_batch)  # native f64 column moments (msk_gpu_obs_moments)
     block = pack_block(bins, failed, counts, rollout_stats.to(bins.device), norm, env.obs_dim)
     blocks = exchange(block, group)
     return merged_iteration(blocks, env.n, cap, env.obs_dim, norm_state, None, env.cfg.adaptive_decay,

@@ -122,3 +122,48 @@ def test_device_merge_bit_exact_with_host(assets):
     for e in range(3):
         assert np.array_equal(got[e], host)
     g.close()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available(), reason="needs a GPU")
+@pytest.mark.gpu
+def test_device_merge_large_bit_exact_with_host(assets):
+    """Chunked block-scan merge: > 1024 envs and > 4096 outcomes in one chunk."""
+    import paper_2603_29332_b200 as pk
+    from conftest import model_paths
+
+    mp_, cp = model_paths("arm2_m6")
+    g = pk.EnvBatch(mp_, cp, 2, cfg=pk.EnvConfig(adaptive_bins=BINS, adaptive_decay=DECAY))
+    ema0 = np.linspace(0.05, 0.3, BINS)
+    g.set_sampler(torch.as_tensor(ema0, device=g.device))
+    rng = np.random.default_rng(9)
+    n, cap = 5000, 8
+    counts = torch.as_tensor(rng.integers(0, cap + 3, n), dtype=torch.int32)  # some exceed cap (clamped)
+    bins = torch.as_tensor(rng.integers(0, BINS, (n, cap)), dtype=torch.int32)
+    failed = torch.as_tensor(rng.integers(0, 2, (n, cap)), dtype=torch.uint8)
+    g.merge_outcomes(bins.cuda(), failed.cuda(), counts.cuda())
+    host = mdist.merge_outcomes_host(ema0, bins, failed, counts, DECAY)
+    got = g.get_sampler().cpu().numpy()
+    assert np.array_equal(got[0], host) and np.array_equal(got[1], host)
+    g.close()
+
+
+def test_device_norm_fold_matches_host_fold():
+    """The on-device RunningNorm fold (no host sync) == the numpy fold, bit for bit,
+    including the first-batch branch (nn.cpp:257-262) and empty batches."""
+    import numpy as np
+    import torch
+
+    from paper_2603_29332_b200 import dist as mdist
+
+    rng = np.random.default_rng(5)
+    d = 7
+    host = (0.0, np.zeros(d), np.ones(d))
+    dev = mdist.init_norm_state(d, "cpu")
+    for n in (5, 0, 3, 11):
+        x = rng.normal(0, 2, (max(n, 1), d))[:n]
+        bm = mdist.batch_moments(torch.as_tensor(x)) if n else torch.cat([torch.zeros(1), torch.zeros(d), torch.ones(d)]).double()
+        b = bm.numpy()
+        host = mdist.running_norm_fold(*host, b[0], b[1:1 + d], b[1 + d:])
+        dev = mdist.running_norm_fold_t(*dev, bm[0], bm[1:1 + d], bm[1 + d:])
+        assert float(dev[0]) == host[0]
+        assert np.array_equal(dev[1].numpy(), host[1]) and np.array_equal(dev[2].numpy(), host[2])

@@ -453,3 +453,45 @@ def test_step_rewarded_matches_oracle(assets):
     torch.cuda.synchronize()
     assert to_np(out["flags"])[0] & pk.FLAG_NOT_STEPPED and to_np(rew)[0] == 7.0
     g.close()
+
+
+def test_iteration_reductions_match_torch(assets):
+    """msk_gpu_rollout_stats / msk_gpu_obs_moments vs plain torch f64 on the same step."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("walker5_m16")
+    n = 700
+    g = pk.EnvBatch(mp, cp, n, cfg=pk.EnvConfig(episode_horizon=3, rsi=True))
+    g.reset()
+    stats = torch.zeros(7, dtype=torch.float64, device=g.device)
+    for s in range(4):
+        a = torch.as_tensor(excitations(3, s, n, g.nm).astype(np.float32), device=g.device)
+        out = g.step(a)
+        st = g.get_state()["ints"]  # t_index, start, steps, done per env
+        g.rollout_stats(out["flags"], stats, reward=out["reward_aux"])
+        f = out["flags"].to(torch.int32)
+        done = (f & pk.FLAG_DONE) != 0
+        ok = (f & (pk.FLAG_NOT_STEPPED | pk.FLAG_BAD_ACTION)) == 0
+        r = out["reward_aux"].double()[ok]
+        steps = st[:, 2].double() if st.dim() == 2 else None
+        exp = torch.stack([ok.sum().double(), r.sum(), (r * r).sum(),
+                           (steps * done).sum() if steps is not None else torch.zeros((), device=g.device),
+                           done.sum().double(), ((f & pk.FLAG_FAILED) != 0).sum().double(),
+                           ((f & pk.FLAG_DIVERGED) != 0).sum().double()])
+        if s == 0:
+            acc = exp
+        else:
+            acc = acc + exp
+        g.reset(mask=out["flags"], mask_bits=pk.FLAG_DONE)
+    torch.cuda.synchronize()
+    assert torch.allclose(stats[[0, 1, 2, 4, 5, 6]], acc[[0, 1, 2, 4, 5, 6]], rtol=1e-12, atol=1e-9)
+    assert float(stats[4]) > 0  # horizon 3 -> episodes ended
+    obs = out["obs"]
+    m = g.obs_moments(obs)
+    x = obs.double()
+    assert float(m[0]) == n
+    assert torch.allclose(m[1:1 + g.obs_dim], x.mean(0), rtol=1e-12, atol=1e-12)
+    assert torch.allclose(m[1 + g.obs_dim:], x.var(0, unbiased=False), rtol=1e-9, atol=1e-12)
+    g.close()
