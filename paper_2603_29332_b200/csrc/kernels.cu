@@ -71,12 +71,28 @@ struct EnvSmem {
     unsigned hm;           // mask of this env's lanes
 };
 
-// Block prologue: copy the tree table into the head of shared memory.  Must be
-// reached by every thread of the block (it ends in __syncthreads).
+// Block prologue: stage the tree table (model constants of the tree passes)
+// into the head of shared memory with one TMA bulk copy (cp.async.bulk,
+// completion on an mbarrier).  Must be reached by every thread of the block.
 __device__ __forceinline__ void load_tree_table(unsigned char* smem, const DevModel& M) {
-    int4* dst = reinterpret_cast<int4*>(smem);
-    for (int i = threadIdx.x; i < M.tab_bytes / 16; i += blockDim.x) dst[i] = __ldg(M.tab_blob + i);
-    __syncthreads();
+    __shared__ __align__(8) uint64_t bar;
+    const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(&bar));
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(M.tab_bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+                     "l"(M.tab_blob), "r"(M.tab_bytes), "r"(b)
+                     : "memory");
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "TAB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+        "@!p bra TAB_WAIT_%=;\n\t}" ::"r"(b)
+        : "memory");
 }
 
 __device__ __forceinline__ EnvSmem carve(unsigned char* smem, int slot, const DevModel& M, int G, unsigned hm) {
