@@ -100,6 +100,27 @@ public:
     void step_host(const float* actions, float* observation, float* delta, float* reward_aux, uint8_t* flags) {
         check(msk_gpu_step_host(ctx_, actions, observation, delta, reward_aux, flags), ctx_);
     }
+    // Env::step(action, fn) with the built-in discriminator as fn (env.cpp:265-270):
+    // load D = Mlp(delta_dim, hidden, 1, Sigmoid) once, then step with a reward buffer.
+    void set_discriminator(const std::vector<double>& theta, int hidden) {
+        check(msk_gpu_set_discriminator(ctx_, theta.data(), static_cast<int64_t>(theta.size()), hidden), ctx_);
+    }
+    void step(const float* actions, const StepBuffers& out, float* reward, void* stream = nullptr) {
+        check(msk_gpu_step_rewarded(ctx_, actions, out.observation, out.delta, reward, out.reward_aux, out.flags,
+                                    out.muscle_power, out.contact_force, stream),
+              ctx_);
+    }
+    void step_host(const float* actions, float* observation, float* delta, float* reward, float* reward_aux,
+                   uint8_t* flags) {
+        check(msk_gpu_step_host_rewarded(ctx_, actions, observation, delta, reward, reward_aux, flags), ctx_);
+    }
+    // Mlp(shape, seed) initial parameters (nn.cpp:16-38), e.g. for a frozen D.
+    static std::vector<double> mlp_init(int in, int hidden, int out, uint64_t seed, double final_init_scale = 1.0) {
+        std::vector<double> theta(static_cast<size_t>(msk_mlp_param_count(in, hidden, out)));
+        if (msk_mlp_init(theta.data(), in, hidden, out, seed, final_init_scale) != MSK_OK)
+            throw ContractError("mlp_init: bad shape");
+        return theta;
+    }
     void observe(float* observation, void* stream = nullptr) {
         check(msk_gpu_observe(ctx_, observation, stream), ctx_);
     }

@@ -1,7 +1,8 @@
 // C++ host program driving the env-stepper through include/msk_gpu.hpp —
 // the "C++ host code calling CUDA through a thin C-ABI" of north_star.
 // Steps E whole-body envs with Philox excitations, auto-resets done envs,
-// and prints throughput and a checksum of the final observations.
+// computes the tracking reward with the built-in tensor-core discriminator,
+// and prints throughput, a checksum of the final observations and the mean reward.
 //
 //   build: make -C tools cpp_demo   (links paper_2603_29332_b200/libmsk_b200.so)
 //   run:   tools/cpp_demo <model.json> <clip.csv> [envs] [steps]
@@ -34,13 +35,17 @@ int main(int argc, char** argv) {
         cudaMalloc(&delta, sizeof(float) * E * env.delta_dim());
         cudaMalloc(&raux, sizeof(float) * E);
         cudaMalloc(&flags, E);
+        float* reward;
+        cudaMalloc(&reward, sizeof(float) * E);
+        // frozen tracking discriminator D = Mlp(delta_dim, 256, 1, Sigmoid), seed 7
+        env.set_discriminator(msk::gpu::EnvBatch::mlp_init(env.delta_dim(), 256, 1, 7), 256);
         env.reset(nullptr, 0xff, obs);
         msk::gpu::StepBuffers out{obs, delta, raux, flags};
         cudaDeviceSynchronize();
         const auto t0 = std::chrono::steady_clock::now();
         for (int s = 0; s < steps; ++s) {
             env.fill_excitations(0x5EED, static_cast<uint32_t>(s), actions);
-            env.step(actions, out);
+            env.step(actions, out, reward);  // Env::step(action, fn): reward = r(D(Δ)) + reward_aux
             env.reset(flags, MSK_FLAG_DONE);  // batched auto-reset
         }
         cudaDeviceSynchronize();
@@ -49,7 +54,13 @@ int main(int argc, char** argv) {
         cudaMemcpy(h.data(), obs, sizeof(float) * h.size(), cudaMemcpyDeviceToHost);
         double checksum = 0.0;
         for (float v : h) checksum += v;
-        std::printf("envs=%d steps=%d env-steps/s=%.0f obs_checksum=%.6e\n", E, steps, E * steps / secs, checksum);
+        std::vector<float> hr(static_cast<size_t>(E));
+        cudaMemcpy(hr.data(), reward, sizeof(float) * E, cudaMemcpyDeviceToHost);
+        double rsum = 0.0;
+        for (float v : hr) rsum += v;
+        std::printf("envs=%d steps=%d env-steps/s=%.0f obs_checksum=%.6e mean_reward=%.6f\n", E, steps,
+                    E * steps / secs, checksum, rsum / E);
+        cudaFree(reward);
         cudaFree(actions);
         cudaFree(obs);
         cudaFree(delta);
