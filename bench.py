@@ -242,6 +242,7 @@ def main():
     ap.add_argument("--ref-envs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-groups", type=int, default=2, help="env groups (contexts) in the e2e host-buffer loop")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     C = dict(CONFIGS[args.config])
@@ -348,35 +349,66 @@ def main():
     # e2e through the C-ABI host-buffer call (pinned host in/out)
     e2e = None
     if not args.no_e2e:
-        ha = torch.empty(E, env.nm, dtype=torch.float32, pin_memory=True)
-        env.fill_excitations(seed, 12345, actions)
-        ha.copy_(actions.cpu())
-        ho = torch.empty(E, env.obs_dim, dtype=torch.float32, pin_memory=True)
-        hd = torch.empty(E, env.delta_dim, dtype=torch.float32, pin_memory=True)
-        hr = torch.empty(E, dtype=torch.float32, pin_memory=True)
-        hf = torch.empty(E, dtype=torch.uint8, pin_memory=True)
-        hw = torch.empty(E, dtype=torch.float32, pin_memory=True) if C["disc"] else None
+        # End to end through the host-buffer C ABI, as an RL harness drives it:
+        # the envs of this GPU split into `groups` contexts (env groups), each
+        # stepped with msk_gpu_step_host_async + msk_gpu_host_wait, so one
+        # group's PCIe transfers overlap the other group's step.  Every step
+        # copies that step's actions in (pinned) and its obs/Δ/reward/flags out.
+        groups = max(1, args.e2e_groups)
+        eg = E // groups
+        envs_e = [pk.EnvBatch(mp, cp, eg, cfg=cfg, reward=rcfg, global_env_offset=rank * E + g * eg)
+                  for g in range(groups)]
+        bufs = []
+        for ge in envs_e:
+            ge.set_eval_mode(C["eval"])
+            if C["disc"]:
+                ge.set_discriminator(pk.mlp_init(ge.delta_dim, C["disc"][0], C["disc"][1]), C["disc"][0])
+            ge.reset()
+            a_dev = ge.fill_excitations(seed, 12345)
+            bufs.append(dict(
+                a=a_dev.cpu().pin_memory(), o=torch.empty(eg, ge.obs_dim, pin_memory=True),
+                d=torch.empty(eg, ge.delta_dim, pin_memory=True), r=torch.empty(eg, pin_memory=True),
+                f=torch.zeros(eg, dtype=torch.uint8, pin_memory=True),
+                w=torch.empty(eg, pin_memory=True) if C["disc"] else None))
+
+        def issue(g):
+            b = bufs[g]
+            envs_e[g].step_host_async(b["a"], b["o"], b["d"], b["r"], b["f"], reward_host=b["w"])
+
+        def collect(g):  # wait for the group's results (now in host memory), auto-reset done envs
+            envs_e[g].host_wait()
+            f = bufs[g]["f"]
+            if f.any():
+                envs_e[g].reset(mask=f.to(dev), mask_bits=pk.FLAG_DONE)
+                torch.cuda.synchronize()
+
         for _ in range(2):
-            env.step_host(ha, ho, hd, hr, hf, reward_host=hw)
-            env.reset(mask=hf.to(dev), mask_bits=pk.FLAG_DONE)
+            for g in range(groups):
+                issue(g)
+            for g in range(groups):
+                collect(g)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        tt = 0.0
         k2 = max(3, args.steps // 2)
-        for _ in range(k2):  # user loop: step through the host-buffer C ABI, auto-reset done envs
-            t0 = time.perf_counter()
-            env.step_host(ha, ho, hd, hr, hf, reward_host=hw)
-            if hf.any():
-                env.reset(mask=hf.to(dev, non_blocking=True), mask_bits=pk.FLAG_DONE)
-                torch.cuda.synchronize()
-            tt += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        for g in range(groups):
+            issue(g)
+        for it in range(k2):
+            for g in range(groups):
+                collect(g)
+                if it + 1 < k2:
+                    issue(g)
+        tt = time.perf_counter() - t0
         tv = torch.tensor([tt], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(tv, op=dist.ReduceOp.MAX)
-        e2e = {"value": E * world * k2 / float(tv[0]), "unit": "env-steps/s",
+        e2e = {"value": eg * groups * world * k2 / float(tv[0]), "unit": "env-steps/s",
                "h2d_bytes_per_step": E * env.nm * 4,
-               "d2h_bytes_per_step": E * (env.obs_dim + env.delta_dim + 1 + (1 if C["disc"] else 0)) * 4 + E}
+               "d2h_bytes_per_step": E * (env.obs_dim + env.delta_dim + 1 + (1 if C["disc"] else 0)) * 4 + E,
+               "api": f"msk_gpu_step_host_async/host_wait, {groups} env groups of {eg}"}
+        for ge in envs_e:
+            ge.close()
 
     disc = None
     if C["disc"]:  # the tensor-core kernel alone on this step's Δ (for its own roofline)

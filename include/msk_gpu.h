@@ -148,6 +148,13 @@ int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_ho
  * msk_gpu_step_rewarded); reward_host [E] required. */
 int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                                float* reward_host, float* reward_aux_host, uint8_t* flags_host);
+/* Asynchronous host-buffer step (reward_host nullable = plain step): enqueues
+ * the same pipeline and returns; the host buffers (pinned) must stay untouched
+ * until msk_gpu_host_wait.  Lets a harness double-buffer env groups (one
+ * context each) so one group's PCIe transfers overlap the other's step. */
+int msk_gpu_step_host_async(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                            float* reward_host, float* reward_aux_host, uint8_t* flags_host);
+int msk_gpu_host_wait(msk_gpu_ctx* ctx);
 
 int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream);
 int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream);

@@ -110,6 +110,8 @@ def lib():
         L.msk_gpu_step.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step_host.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_step_host_rewarded.argtypes = [_vp] * 7
+        L.msk_gpu_step_host_async.argtypes = [_vp] * 7
+        L.msk_gpu_host_wait.argtypes = [_vp]
         L.msk_gpu_rollout_stats.argtypes = [_vp] * 5
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
@@ -292,6 +294,15 @@ class EnvBatch:
             return
         self._ck(lib().msk_gpu_step_host(self.h, _p(actions_host), _p(obs_host), _p(delta_host),
                                          _p(reward_aux_host), _p(flags_host)))
+
+    def step_host_async(self, actions_host, obs_host=None, delta_host=None, reward_aux_host=None, flags_host=None,
+                        reward_host=None):
+        """Enqueue a host-buffer step and return; pair with host_wait() (buffers must be pinned)."""
+        self._ck(lib().msk_gpu_step_host_async(self.h, _p(actions_host), _p(obs_host), _p(delta_host),
+                                               _p(reward_host), _p(reward_aux_host), _p(flags_host)))
+
+    def host_wait(self):
+        self._ck(lib().msk_gpu_host_wait(self.h))
 
     def observe(self, obs=None, stream=None):
         obs = obs if obs is not None else self._empty(self.n, self.obs_dim)

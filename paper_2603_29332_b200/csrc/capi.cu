@@ -561,7 +561,7 @@ namespace {
 // pipeline: H2D(actions c) -> step(c) [-> D(c)] -> D2H(outputs c), chunks on
 // separate streams so chunk c's transfers overlap the other chunks' kernels.
 void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
-                    float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
+                    float* reward_host, float* reward_aux_host, uint8_t* flags_host, bool wait) {
     if (!actions_host) throw ConfigError("step_host: actions is null");
     if (reward_host && !ctx->disc.w1) throw ConfigError("step_host: reward requested but no discriminator set");
     const size_t E = static_cast<size_t>(ctx->n_envs);
@@ -614,7 +614,8 @@ void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host
         if (flags_host)
             ck(cudaMemcpyAsync(flags_host + e0, ctx->h_flags + e0, n, cudaMemcpyDeviceToHost, s), "D2H flags");
     }
-    for (int i = 0; i < ctx->host_streams; ++i) ck(cudaStreamSynchronize(ctx->hs[i]), "step_host sync");
+    if (wait)
+        for (int i = 0; i < ctx->host_streams; ++i) ck(cudaStreamSynchronize(ctx->hs[i]), "step_host sync");
 }
 
 }  // namespace
@@ -622,7 +623,7 @@ void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host
 int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                       float* reward_aux_host, uint8_t* flags_host) {
     return guarded(ctx, [&] {
-        step_host_impl(ctx, actions_host, obs_host, delta_host, nullptr, reward_aux_host, flags_host);
+        step_host_impl(ctx, actions_host, obs_host, delta_host, nullptr, reward_aux_host, flags_host, true);
     });
 }
 
@@ -630,7 +631,21 @@ int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, floa
                                float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
     return guarded(ctx, [&] {
         if (!reward_host) throw ConfigError("step_host_rewarded: reward is null");
-        step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host);
+        step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host, true);
+    });
+}
+
+int msk_gpu_step_host_async(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
+                            float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
+    return guarded(ctx, [&] {
+        step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host, false);
+    });
+}
+
+int msk_gpu_host_wait(msk_gpu_ctx* ctx) {
+    return guarded(ctx, [&] {
+        for (int i = 0; i < ctx->host_streams; ++i)
+            if (ctx->hs[i]) ck(cudaStreamSynchronize(ctx->hs[i]), "host_wait");
     });
 }
 
