@@ -320,6 +320,18 @@ def test_host_buffer_step_matches_device_step(assets):
     assert np.array_equal(ho.numpy(), dev["obs"])
     assert np.array_equal(hd.numpy(), dev["delta"])
     assert np.array_equal(hf.numpy(), dev["flags"])
+    # asynchronous variant (+ the discriminator reward): same results after host_wait
+    g.set_state(st)
+    from oracle.oracle import mlp_init
+
+    g.set_discriminator(mlp_init(g.delta_dim, 64, 7), 64)
+    ho.zero_()
+    hw = torch.empty(n).pin_memory()
+    g.step_host_async(ha, ho, hd, hr, hf, reward_host=hw)
+    g.host_wait()
+    assert np.array_equal(ho.numpy(), dev["obs"]) and np.array_equal(hf.numpy(), dev["flags"])
+    r_dev = to_np(g.discriminator_reward(torch.as_tensor(dev["delta"], device=g.device))) + dev["reward_aux"]
+    assert np.abs(hw.numpy() - r_dev).max() <= 1e-6
     g.close()
 
 
