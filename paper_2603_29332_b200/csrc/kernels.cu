@@ -446,12 +446,31 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
     }
     o += 3 * nk;
     const size_t mb = static_cast<size_t>(e) * nm;
-    for (int x = lane; x < nm; x += S.G) {  // reference slot x <- internal muscle m_int[x]
-        const size_t i = mb + __ldg(M.m_int + x);
-        obs_row[o + x] = St.act[i];
-        obs_row[o + nm + x] = St.fm[i];
-        obs_row[o + 2 * nm + x] = St.lm[i];
-        obs_row[o + 3 * nm + x] = St.vm[i];
+    // reference slot x <- internal muscle m_int[x]; 4 slots per lane in flight
+    // (all loads issued before the stores, which may alias them)
+    for (int x0 = 0; x0 < nm; x0 += 4 * S.G) {
+        float v[4][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int x = x0 + j * S.G + lane;
+            if (x < nm) {
+                const size_t i = mb + __ldg(M.m_int + x);
+                v[j][0] = St.act[i];
+                v[j][1] = St.fm[i];
+                v[j][2] = St.lm[i];
+                v[j][3] = St.vm[i];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int x = x0 + j * S.G + lane;
+            if (x < nm) {
+                obs_row[o + x] = v[j][0];
+                obs_row[o + nm + x] = v[j][1];
+                obs_row[o + 2 * nm + x] = v[j][2];
+                obs_row[o + 3 * nm + x] = v[j][3];
+            }
+        }
     }
     o += 4 * nm;
     const size_t t = static_cast<size_t>(t_index);
