@@ -211,6 +211,38 @@ int msk_gpu_validate(const char* model_json_path, const char* clip_csv_path, msk
 /* Measured FFMA throughput of `device` in TFLOP/s (FP32 roofline denominator). */
 int msk_gpu_fp32_peak_probe(int device, double* tflops);
 
+/* ---- on-device policy sampling (SPEC.md:371-393 sample_action) -------------
+ * a0 ~ N(mean(s), exp(log_std)) with mean = head_scale * Mlp_pi(norm(s)) +
+ * head_offset (Head::Affine, nn.hpp:10-19), then n_ode explicit-Euler steps of
+ * the flow field a += dt * Mlp_psi([phi(t), norm(s), a]) with
+ * phi(t) = [t, sin 2 pi t, cos 2 pi t, sin 4 pi t, cos 4 pi t];
+ * norm = RunningNorm::apply (nn.cpp:272-277).  Mlp_pi = Mlp(obs_dim, hidden,
+ * n_actions), Mlp_psi = Mlp(5 + obs_dim + n_actions, hidden, n_actions), flat
+ * f64 parameters in the nn.cpp:16-38 layout.  hidden: multiple of 64.  Every
+ * layer runs as a tcgen05 GEMM with bf16 operands and fp32 accumulation.
+ * Gaussian noise: Philox4x32-10 keyed by seed, counter (step, global env, ...). */
+typedef struct msk_policy msk_policy;
+int msk_policy_create(int32_t obs_dim, int32_t n_actions, int32_t hidden, const double* pi_theta,
+                      int64_t pi_n_params, double head_scale, double head_offset, const double* log_std,
+                      const double* psi_theta, int64_t psi_n_params, int32_t n_ode, double dt_ode, int32_t max_envs,
+                      int32_t device, msk_policy** out);
+void msk_policy_destroy(msk_policy* p);
+const char* msk_policy_last_error(const msk_policy* p);
+/* RunningNorm state (count 0 -> identity). */
+int msk_policy_set_norm(msk_policy* p, const double* mean, const double* var, double count);
+/* actions [n x n_actions] (device) = final a; a0 / logprob (nullable) = the
+ * Gaussian sample and its log-density (explore = 0: a0 = mean, logprob = 0). */
+int msk_policy_sample(msk_policy* p, const float* obs, int32_t n, int32_t explore, uint64_t seed, uint32_t step,
+                      int64_t global_env_offset, float* actions, float* a0, float* logprob, void* stream);
+/* Same, replayed from a CUDA graph (re-captured when any argument changes). */
+int msk_policy_sample_graph(msk_policy* p, const float* obs, int32_t n, int32_t explore, uint64_t seed,
+                            uint32_t step, int64_t global_env_offset, float* actions, float* a0, float* logprob,
+                            void* stream);
+int32_t msk_policy_time_features(double t, double* out5);
+/* Test hook: Y = act(X W^T + b) through one tiled tensor-core GEMM (epi 0 tanh, 1 linear). */
+int msk_gemm_test(const float* X, int32_t M, int32_t K, const double* W, const float* b, int32_t N, int32_t epi,
+                  float* Y);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,7 +14,7 @@ import ctypes as C
 import os
 from dataclasses import dataclass, field
 
-__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError", "mlp_init",
+__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError", "mlp_init", "Policy",
            "FLAG_DONE", "FLAG_FAILED", "FLAG_DIVERGED", "FLAG_NOT_STEPPED", "FLAG_BAD_ACTION"]
 
 LIB_PATH = os.environ.get("MSK_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmsk_b200.so")
@@ -33,6 +33,76 @@ def mlp_init(n_in, hidden, seed, n_out=1, final_init_scale=1.0):
     if lib().msk_mlp_init(theta.ctypes.data, n_in, hidden, n_out, C.c_uint64(seed), float(final_init_scale)) != 0:
         raise MskError(lib().msk_gpu_last_error(None).decode())
     return theta
+
+
+class Policy:
+    """On-device policy sampling (msk_policy_*): Gaussian π⁽⁰⁾ + flow-ODE ψ on the tensor cores.
+
+    pi_theta: Mlp(obs_dim, hidden, n_actions) flat f64 params; psi_theta: Mlp(5 + obs_dim +
+    n_actions, hidden, n_actions); log_std [n_actions]; head y = head_scale * z + head_offset."""
+
+    TIME_FEATURES = 5
+
+    def __init__(self, obs_dim, n_actions, hidden, pi_theta, log_std, psi_theta, n_ode=20, dt_ode=0.05,
+                 max_envs=4096, head_scale=1.0, head_offset=0.0, device=0):
+        import numpy as np
+        import torch
+
+        self.torch = torch
+        self.obs_dim, self.nm, self.hidden, self.n_ode, self.dt = obs_dim, n_actions, hidden, n_ode, dt_ode
+        self.max_envs = max_envs
+        self.device = torch.device("cuda", device)
+        self._keep = [np.ascontiguousarray(np.asarray(x, dtype=np.float64)) for x in (pi_theta, log_std, psi_theta)]
+        pi, ls, psi = self._keep
+        h = C.c_void_p()
+        rc = lib().msk_policy_create(obs_dim, n_actions, hidden, pi.ctypes.data, pi.size, head_scale, head_offset,
+                                     ls.ctypes.data, psi.ctypes.data, psi.size, n_ode, dt_ode, max_envs, device,
+                                     C.byref(h))
+        if rc != 0:
+            raise MskError(lib().msk_policy_last_error(None).decode())
+        self.h = h
+
+    def _ck(self, rc):
+        if rc != 0:
+            raise MskError(lib().msk_policy_last_error(self.h).decode())
+
+    def set_norm(self, mean, var, count):
+        import numpy as np
+
+        m = np.ascontiguousarray(mean, dtype=np.float64)
+        v = np.ascontiguousarray(var, dtype=np.float64)
+        self._ck(lib().msk_policy_set_norm(self.h, m.ctypes.data, v.ctypes.data, float(count)))
+
+    def sample(self, obs, explore=False, seed=0, step=0, global_env_offset=0, actions=None, a0=None, logprob=None,
+               graph=False, stream=None):
+        """Returns actions [n x n_actions] (device); a0 / logprob filled when given."""
+        torch = self.torch
+        n = obs.shape[0]
+        actions = actions if actions is not None else torch.empty(n, self.nm, device=self.device)
+        fn = lib().msk_policy_sample_graph if graph else lib().msk_policy_sample
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        self._ck(fn(self.h, _p(obs.contiguous()), n, int(bool(explore)), C.c_uint64(seed), C.c_uint32(step),
+                    int(global_env_offset), _p(actions), _p(a0), _p(logprob), s))
+        return actions
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().msk_policy_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def time_features(t):
+    import numpy as np
+
+    out = np.zeros(5)
+    lib().msk_policy_time_features(float(t), out.ctypes.data)
+    return out
 
 
 class MskError(RuntimeError):
@@ -113,6 +183,18 @@ def lib():
         L.msk_gpu_step_host_async.argtypes = [_vp] * 7
         L.msk_gpu_host_wait.argtypes = [_vp]
         L.msk_gpu_rollout_stats.argtypes = [_vp] * 5
+        L.msk_policy_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int64, C.c_double, C.c_double, _vp,
+                                        _vp, C.c_int64, C.c_int32, C.c_double, C.c_int32, C.c_int32, _vp]
+        L.msk_policy_destroy.argtypes = [_vp]
+        L.msk_policy_last_error.restype = C.c_char_p
+        L.msk_policy_last_error.argtypes = [_vp]
+        L.msk_policy_set_norm.argtypes = [_vp, _vp, _vp, C.c_double]
+        L.msk_policy_sample.argtypes = [_vp, _vp, C.c_int32, C.c_int32, C.c_uint64, C.c_uint32, C.c_int64, _vp, _vp,
+                                        _vp, _vp]
+        L.msk_policy_sample_graph.argtypes = L.msk_policy_sample.argtypes
+        L.msk_policy_time_features.restype = C.c_int32
+        L.msk_policy_time_features.argtypes = [C.c_double, _vp]
+        L.msk_gemm_test.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
         L.msk_mlp_param_count.restype = C.c_int64

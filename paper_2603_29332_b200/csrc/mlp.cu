@@ -1,0 +1,297 @@
+// Pipelined bf16 GEMM on the 5th-generation tensor cores with MLP epilogues:
+// the building block of the on-device policy (π⁽⁰⁾ mean MLP and the flow field
+// ψ) — one CTA per 128 x 256 output tile:
+//   warp 0   TMA producer: 1-D bulk copies of pre-tiled A (16 KB) and W (32 KB)
+//            K-blocks into a 4-stage shared-memory ring (mbarrier complete_tx);
+//   warp 1   allocates 256 TMEM columns; one thread issues 4 tcgen05.mma
+//            (M = 128, N = 256, K = 16) per K-block and commits each stage back
+//            to the producer, then the accumulator to the epilogue;
+//   warps 2-5 epilogue: tcgen05.ld of their TMEM lane quarter, bias (+ addend),
+//            tanh -> bf16 tiled (next layer's A), fp32 affine head, or the flow
+//            ODE update a += dt * ψ.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "mlp.cuh"
+
+namespace msk_b200 {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kABytes = kGemmBM * kGemmBK * 2;  // 16 KB
+constexpr int kWBytes = kGemmBN * kGemmBK * 2;  // 32 KB
+constexpr int kGemmThreads = 192;
+
+__host__ __device__ constexpr uint32_t blk_off(int r, int k) {  // inside a (rows x 64) block
+    return static_cast<uint32_t>(((r >> 3) * 8 + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
+}
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "GW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra GW_%=;\n\t}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(b))
+                 : "memory");
+}
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {  // LBO 128 B, SBO 1024 B, version 1, no swizzle
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>(128 >> 4) << 16) |
+           (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46);
+}
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kGemmBN >> 3) << 17) |
+                            (static_cast<uint32_t>(kGemmBM >> 4) << 24);
+
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float tanh_a(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ uint32_t bf2(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// 16 consecutive columns [n0, n0 + 16) of row m into a tiled bf16 image with
+// KB = K/64 column blocks (two 16-B stores).
+__device__ __forceinline__ void store_tiled16(void* img, int KB, int m, int n0, const float (&y)[16]) {
+    char* base = static_cast<char*>(img) + (static_cast<size_t>(m >> 7) * KB + (n0 >> 6)) * kABytes;
+    const int r = m & 127, k = n0 & 63;
+    uint4 lo = make_uint4(bf2(y[0], y[1]), bf2(y[2], y[3]), bf2(y[4], y[5]), bf2(y[6], y[7]));
+    uint4 hi = make_uint4(bf2(y[8], y[9]), bf2(y[10], y[11]), bf2(y[12], y[13]), bf2(y[14], y[15]));
+    *reinterpret_cast<uint4*>(base + blk_off(r, k)) = lo;
+    *reinterpret_cast<uint4*>(base + blk_off(r, k + 8)) = hi;
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    unsigned char* sA = smem;                                    // kStages x 16 KB
+    unsigned char* sW = smem + kStages * kABytes;                // kStages x 32 KB
+    uint64_t* full = reinterpret_cast<uint64_t*>(sW + kStages * kWBytes);
+    uint64_t* empty = full + kStages;
+    uint64_t* acc_full = empty + kStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mb = blockIdx.x, nb = blockIdx.y;
+    const int KB = pad_to(g.K, kGemmBK) / kGemmBK;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
+        }
+        bar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+    // inputs may be the previous kernel's outputs (programmatic dependent launch)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    if (warp == 0 && lane == 0) {  // TMA producer
+        const char* A = static_cast<const char*>(g.A) + static_cast<size_t>(mb) * KB * kABytes;
+        const char* W = static_cast<const char*>(g.W) + static_cast<size_t>(nb) * KB * kWBytes;
+        for (int kb = 0; kb < KB; ++kb) {
+            const int s = kb % kStages;
+            if (kb >= kStages) bar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+            bar_expect(&full[s], kABytes + kWBytes);
+            bulk(sA + s * kABytes, A + static_cast<size_t>(kb) * kABytes, kABytes, &full[s]);
+            bulk(sW + s * kWBytes, W + static_cast<size_t>(kb) * kWBytes, kWBytes, &full[s]);
+        }
+    } else if (warp == 1 && lane == 0) {  // MMA issuer
+        for (int kb = 0; kb < KB; ++kb) {
+            const int s = kb % kStages;
+            bar_wait(&full[s], (kb / kStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a0 = su32(sA + s * kABytes), w0 = su32(sW + s * kWBytes);
+#pragma unroll
+            for (int k = 0; k < kGemmBK / 16; ++k) {
+                const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                    "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc), "r"(acc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             su32(&empty[s]))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         su32(acc_full))
+                     : "memory");
+    } else if (warp >= 2) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31
+        bar_wait(acc_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
+        const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        const int n_out_pad = pad_to(EPI == kEpiOde ? g.n_valid : g.N, kGemmBK);  // tiled output width
+        for (int c = 0; c < kGemmBN; c += 16) {
+            const int n0 = nb * kGemmBN + c;
+            float v[16];
+            ld16(trow + c, v);
+            if (n0 >= (EPI == kEpiF32 ? g.n_valid : n_out_pad)) continue;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] += (g.bias && n0 + i < g.N) ? g.bias[n0 + i] : 0.0f;
+            if (EPI == kEpiTanhTiled) {
+                if (g.addend && m < g.M) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (n0 + i < g.N) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+                store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
+            } else if (EPI == kEpiF32) {
+                if (m < g.M) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (n0 + i < g.n_valid) {
+                            float y = fmaf(g.scale, v[i], g.offset);
+                            if (g.addend) y += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
+                            g.out_f[static_cast<size_t>(m) * g.ld_f + n0 + i] = y;
+                        }
+                }
+            } else {  // kEpiOde: a += dt * psi
+                float y[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    y[i] = 0.0f;
+                    if (m < g.M && n0 + i < g.n_valid) {
+                        float* a = g.out_f + static_cast<size_t>(m) * g.ld_f + n0 + i;
+                        y[i] = fmaf(g.dt, v[i], *a);
+                        *a = y[i];
+                    }
+                }
+                if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+__global__ void obs_to_tiled_kernel(const float* obs, int M, int D, int ld, const float* mean, const float* inv_sd,
+                                    void* out) {
+    // one thread per (row, 8-column chunk) of the padded [Mpad x Kpad] image
+    const int Kp = pad_to(D, kGemmBK), chunks = Kp / 8;
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    const int Mp = pad_to(M, kGemmBM);
+    if (t >= static_cast<long long>(Mp) * chunks) return;
+    const int m = static_cast<int>(t / chunks), k0 = static_cast<int>(t % chunks) * 8;
+    float y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int k = k0 + i;
+        float x = 0.0f;
+        if (m < M && k < D) {
+            x = obs[static_cast<size_t>(m) * ld + k];
+            if (mean) x = (x - mean[k]) * inv_sd[k];
+        }
+        y[i] = x;
+    }
+    char* base = static_cast<char*>(out) + (static_cast<size_t>(m >> 7) * (Kp / kGemmBK) + (k0 >> 6)) * kABytes;
+    *reinterpret_cast<uint4*>(base + blk_off(m & 127, k0 & 63)) =
+        make_uint4(bf2(y[0], y[1]), bf2(y[2], y[3]), bf2(y[4], y[5]), bf2(y[6], y[7]));
+}
+
+}  // namespace
+
+std::vector<uint16_t> pack_weights(const double* W, int rows, int cols, int c0, int nc) {
+    const int Np = pad_to(rows, kGemmBN), Kp = pad_to(nc, kGemmBK), KB = Kp / kGemmBK;
+    std::vector<uint16_t> img(static_cast<size_t>(Np) * Kp, 0);
+    for (int n = 0; n < rows; ++n)
+        for (int k = 0; k < nc; ++k) {
+            const __nv_bfloat16 b = __float2bfloat16_rn(static_cast<float>(W[static_cast<size_t>(c0 + k) * rows + n]));
+            uint16_t u;
+            std::memcpy(&u, &b, 2);
+            const size_t blk = static_cast<size_t>(n / kGemmBN) * KB + k / kGemmBK;
+            img[(blk * kWBytes + blk_off(n % kGemmBN, k % kGemmBK)) / 2] = u;
+        }
+    return img;
+}
+
+size_t gemm_smem_bytes() { return static_cast<size_t>(kStages) * (kABytes + kWBytes) + 256; }
+
+cudaError_t prepare_gemm() {
+    cudaError_t e;
+    const int bytes = static_cast<int>(gemm_smem_bytes());
+    if ((e = cudaFuncSetAttribute(gemm_kernel<kEpiTanhTiled>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute(gemm_kernel<kEpiF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
+    return cudaFuncSetAttribute(gemm_kernel<kEpiOde>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(pad_to(g.M, kGemmBM) / kGemmBM, pad_to(g.N, kGemmBN) / kGemmBN);
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = gemm_smem_bytes();
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    switch (epi) {
+        case kEpiTanhTiled: return cudaLaunchKernelEx(&cfg, gemm_kernel<kEpiTanhTiled>, g);
+        case kEpiF32: return cudaLaunchKernelEx(&cfg, gemm_kernel<kEpiF32>, g);
+        default: return cudaLaunchKernelEx(&cfg, gemm_kernel<kEpiOde>, g);
+    }
+}
+
+cudaError_t launch_obs_to_tiled(const float* obs, int M, int D, const float* mean, const float* inv_sd, void* out,
+                                cudaStream_t s) {
+    const long long n = static_cast<long long>(pad_to(M, kGemmBM)) * (pad_to(D, kGemmBK) / 8);
+    obs_to_tiled_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(obs, M, D, D, mean, inv_sd, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_f32_to_tiled(const float* x, int M, int D, int ld, void* out, cudaStream_t s) {
+    const long long n = static_cast<long long>(pad_to(M, kGemmBM)) * (pad_to(D, kGemmBK) / 8);
+    obs_to_tiled_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, M, D, ld, nullptr, nullptr, out);
+    return cudaGetLastError();
+}
+
+}  // namespace msk_b200

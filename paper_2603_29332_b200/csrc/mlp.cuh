@@ -1,0 +1,61 @@
+// Tiled bf16 GEMM on the tcgen05 tensor cores + MLP epilogues (see mlp.cu).
+//
+// Layouts ("tiled" = what the UMMA descriptors and 1-D TMA bulk copies read):
+//   activations A [M x K]: blocks of 128 rows x 64 K (16 KB) at
+//       ((mb * KB) + kb) * 16 KB, KB = K/64, rows/K padded with zeros;
+//   weights     W [N x K]: blocks of 256 rows x 64 K (32 KB) at
+//       ((nb * KB) + kb) * 32 KB;
+// inside a block element (r, k) sits at ((r/8)*8 + k/8)*128 + (r%8)*16 + (k%8)*2
+// (K-major core matrices, no swizzle: LBO = 128 B, SBO = 1024 B).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+namespace msk_b200 {
+
+constexpr int kGemmBM = 128, kGemmBN = 256, kGemmBK = 64;
+
+__host__ __device__ inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
+inline size_t tiled_a_bytes(int M, int K) { return static_cast<size_t>(pad_to(M, kGemmBM)) * pad_to(K, kGemmBK) * 2; }
+inline size_t tiled_w_bytes(int N, int K) { return static_cast<size_t>(pad_to(N, kGemmBN)) * pad_to(K, kGemmBK) * 2; }
+
+// Host: pack a column-major (Eigen/Mlp layout) f64 matrix W[rows x cols] — or a
+// column slice [c0, c0 + nc) of it — into the tiled bf16 weight image.
+std::vector<uint16_t> pack_weights(const double* W, int rows, int cols, int c0, int nc);
+
+enum GemmEpi : int {
+    kEpiTanhTiled = 0,  // out_a (tiled bf16, K = N) = tanh(acc + bias[n] + addend[m, n])
+    kEpiF32 = 1,        // out_f[m * ld + n] = acc + bias[n] (+ addend)           (n < n_valid)
+    kEpiOde = 2,        // a[m * ld + n] += dt * (acc + bias[n]); out_a = bf16 tiled copy of the new a
+};
+
+struct GemmArgs {
+    const void* A = nullptr;       // tiled activations
+    const void* W = nullptr;       // tiled weights
+    const float* bias = nullptr;   // [N] (nullable)
+    const float* addend = nullptr; // fp32 row-major [M x ld_add] (nullable)
+    int ld_add = 0;
+    void* out_a = nullptr;         // tiled bf16 output (K = N padded) for the next layer
+    float* out_f = nullptr;        // fp32 row-major output / ODE state
+    int ld_f = 0;
+    int M = 0, N = 0, K = 0;       // logical sizes (N, K padded internally)
+    int n_valid = 0;               // columns of out_f that are written
+    float dt = 0.0f;
+    float scale = 1.0f, offset = 0.0f;  // kEpiF32: affine head y = scale * z + offset
+};
+
+cudaError_t prepare_gemm();
+size_t gemm_smem_bytes();
+cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s);
+
+// obs f32 [M x D] -> normalised (RunningNorm::apply) bf16 tiled A [M x D]
+cudaError_t launch_obs_to_tiled(const float* obs, int M, int D, const float* mean, const float* inv_sd, void* out,
+                                cudaStream_t s);
+// f32 row-major [M x D] -> bf16 tiled
+cudaError_t launch_f32_to_tiled(const float* x, int M, int D, int ld, void* out, cudaStream_t s);
+
+}  // namespace msk_b200

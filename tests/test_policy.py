@@ -1,0 +1,126 @@
+"""On-device policy sampling vs the f64 oracle (oracle/policy.py).
+
+Tolerances (bf16 tensor-core operands, fp32 accumulation):
+  one GEMM layer  vs torch fp32 on the same bf16-rounded operands: rel 1e-4 (linear), 4e-3 abs (tanh -> bf16)
+  full sample (π⁽⁰⁾ + 20 flow steps) vs f64: |Δa| <= 2e-2 (measured ~5e-3, tools/policy_check.py)
+  SPEC.md:391-393 examples: ψ ≡ 0 -> a = a⁽⁰⁾ exactly; ψ ≡ c -> a = a⁽⁰⁾ + c (1e-5); deterministic repeatable.
+"""
+import numpy as np
+import pytest
+
+from oracle.oracle import mlp_init
+from oracle.policy import sample_action
+
+pytestmark = pytest.mark.gpu
+
+D, NM, H = 40, 24, 64
+
+
+def _bf16(x):
+    import torch
+
+    return torch.as_tensor(np.asarray(x, dtype=np.float32)).to(torch.bfloat16).float()
+
+
+@pytest.mark.parametrize("epi", [0, 1])
+def test_tiled_gemm_matches_torch(epi):
+    import ctypes as C
+
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    rng = np.random.default_rng(epi)
+    M, K, N = 300, 200, 300  # ragged in every dimension, two N tiles
+    X = rng.normal(0, 1, (M, K)).astype(np.float32)
+    W = rng.normal(0, 1 / np.sqrt(K), (N, K))
+    b = rng.normal(0, 0.1, N).astype(np.float32)
+    Wc = np.asfortranarray(W).ravel(order="F")  # column-major, as Mlp stores it
+    Y = np.zeros((M, N), dtype=np.float32)
+    rc = pk.lib().msk_gemm_test(X.ctypes.data, M, K, Wc.ctypes.data, b.ctypes.data, N, epi, Y.ctypes.data)
+    assert rc == 0
+    ref = (_bf16(X) @ _bf16(W).T + torch.as_tensor(b)).numpy()
+    if epi == 1:
+        assert np.abs(Y - ref).max() <= 1e-4 * max(1.0, np.abs(ref).max())
+    else:
+        assert np.abs(Y - np.tanh(ref)).max() <= 4e-3
+
+
+def _params(seed, psi_scale=0.3):
+    pi = mlp_init(D, H, seed, n_out=NM)
+    psi = mlp_init(5 + D + NM, H, seed + 1, n_out=NM, final_init_scale=psi_scale)
+    log_std = np.full(NM, -1.0)  # SPEC.md:372 init log-std
+    return pi, log_std, psi
+
+
+def _policy(pi, log_std, psi, **kw):
+    import paper_2603_29332_b200 as pk
+
+    return pk.Policy(D, NM, H, pi, log_std, psi, max_envs=512, **kw)
+
+
+def test_policy_deterministic_matches_oracle():
+    import torch
+
+    pi, ls, psi = _params(3)
+    p = _policy(pi, ls, psi, head_scale=0.5, head_offset=0.5)
+    rng = np.random.default_rng(0)
+    obs = rng.normal(0, 1, (200, D)).astype(np.float32)
+    mean, var = rng.normal(0, 0.2, D), rng.uniform(0.5, 2.0, D)
+    p.set_norm(mean, var, 100.0)
+    a = p.sample(torch.as_tensor(obs, device="cuda")).cpu().numpy()
+    ref, _, _ = sample_action(pi, ls, psi, obs, H, norm=(mean, var, 100.0), head_scale=0.5, head_offset=0.5)
+    err = np.abs(a - ref).max()
+    assert err <= 2e-2, err
+    # deterministic mode is repeatable, and the CUDA-graph replay is identical
+    b = p.sample(torch.as_tensor(obs, device="cuda")).cpu().numpy()
+    g = p.sample(torch.as_tensor(obs, device="cuda"), graph=True).cpu().numpy()
+    g2 = p.sample(torch.as_tensor(obs, device="cuda"), graph=True).cpu().numpy()
+    assert np.array_equal(a, b) and np.array_equal(a, g) and np.array_equal(g, g2)
+    p.close()
+
+
+def test_policy_spec_examples():
+    """ψ ≡ 0 -> a = a⁽⁰⁾; ψ ≡ c -> a = a⁽⁰⁾ + c."""
+    import torch
+
+    pi, ls, psi = _params(5)
+    zero = np.zeros_like(psi)
+    p = _policy(pi, ls, zero)
+    obs = torch.as_tensor(np.random.default_rng(1).normal(0, 1, (130, D)).astype(np.float32), device="cuda")
+    a0 = torch.empty(130, NM, device="cuda")
+    a = p.sample(obs, a0=a0)
+    assert torch.equal(a, a0)
+    p.close()
+    const = zero.copy()
+    c = np.linspace(-0.3, 0.4, NM)
+    const[-NM:] = c  # ψ head bias only
+    p = _policy(pi, ls, const)
+    a = p.sample(obs, a0=a0)
+    assert np.abs((a - a0).cpu().numpy() - c).max() <= 1e-5
+    p.close()
+
+
+def test_policy_explore_noise_and_logprob():
+    import torch
+
+    pi, ls, psi = _params(7)
+    p = _policy(pi, ls, np.zeros_like(psi))
+    n = 500
+    obs = torch.as_tensor(np.random.default_rng(2).normal(0, 1, (n, D)).astype(np.float32), device="cuda")
+    mean = p.sample(obs).clone()
+    a0 = torch.empty(n, NM, device="cuda")
+    lp = torch.empty(n, device="cuda")
+    a = p.sample(obs, explore=True, seed=11, step=3, a0=a0, logprob=lp)
+    eps = ((a0 - mean) / np.exp(-1.0)).cpu().numpy()
+    assert abs(eps.mean()) < 0.05 and abs(eps.std() - 1.0) < 0.05
+    ref_lp = np.sum(-0.5 * eps * eps + 1.0 - 0.5 * np.log(2 * np.pi), axis=1)
+    assert np.abs(lp.cpu().numpy() - ref_lp).max() <= 1e-3 * np.abs(ref_lp).max()
+    assert torch.equal(a, a0)  # ψ ≡ 0
+    # same (seed, step, env) -> same noise; another step -> different noise
+    a0b = torch.empty_like(a0)
+    p.sample(obs, explore=True, seed=11, step=3, a0=a0b)
+    assert torch.equal(a0, a0b)
+    p.sample(obs, explore=True, seed=11, step=4, a0=a0b)
+    assert not torch.equal(a0, a0b)
+    p.close()
