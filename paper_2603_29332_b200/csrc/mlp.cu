@@ -174,32 +174,64 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
             for (int i = 0; i < 16; ++i) v[i] += (g.bias && n0 + i < g.N) ? g.bias[n0 + i] : 0.0f;
             if (EPI == kEpiTanhTiled) {
                 if (g.addend && m < g.M) {
+                    const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
+                    if (n0 + 16 <= g.N) {  // 4 x 16-B loads of the thread's 64 contiguous bytes
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (n0 + i < g.N) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 t = *reinterpret_cast<const float4*>(ap + i);
+                            v[i] += t.x;
+                            v[i + 1] += t.y;
+                            v[i + 2] += t.z;
+                            v[i + 3] += t.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (n0 + i < g.N) v[i] += ap[i];
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
                 store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
             } else if (EPI == kEpiF32) {
                 if (m < g.M) {
+                    float* op = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (n0 + i < g.n_valid) {
-                            float y = fmaf(g.scale, v[i], g.offset);
-                            if (g.addend) y += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
-                            g.out_f[static_cast<size_t>(m) * g.ld_f + n0 + i] = y;
-                        }
+                    for (int i = 0; i < 16; ++i) {
+                        v[i] = fmaf(g.scale, v[i], g.offset);
+                        if (g.addend && n0 + i < g.n_valid) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
+                    }
+                    if (n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4)
+                            *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (n0 + i < g.n_valid) op[i] = v[i];
+                    }
                 }
             } else {  // kEpiOde: a += dt * psi
                 float y[16];
+                float* ap = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
+                if (m < g.M && n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {  // 16-B vector RMW
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    y[i] = 0.0f;
-                    if (m < g.M && n0 + i < g.n_valid) {
-                        float* a = g.out_f + static_cast<size_t>(m) * g.ld_f + n0 + i;
-                        y[i] = fmaf(g.dt, v[i], *a);
-                        *a = y[i];
+                    for (int i = 0; i < 16; i += 4) {
+                        const float4 t = *reinterpret_cast<const float4*>(ap + i);
+                        y[i] = fmaf(g.dt, v[i], t.x);
+                        y[i + 1] = fmaf(g.dt, v[i + 1], t.y);
+                        y[i + 2] = fmaf(g.dt, v[i + 2], t.z);
+                        y[i + 3] = fmaf(g.dt, v[i + 3], t.w);
+                        *reinterpret_cast<float4*>(ap + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        y[i] = 0.0f;
+                        if (m < g.M && n0 + i < g.n_valid) {
+                            y[i] = fmaf(g.dt, v[i], ap[i]);
+                            ap[i] = y[i];
+                        }
                     }
                 }
                 if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
