@@ -243,6 +243,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-groups", type=int, default=2, help="env groups (contexts) in the e2e host-buffer loop")
+    ap.add_argument("--policy-width", type=int, default=0,
+                    help="actions from the on-device flow policy of this hidden width (0: Philox excitations)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     C = dict(CONFIGS[args.config])
@@ -291,11 +293,22 @@ def main():
     # rollout stats (dist.py N_STATS): steps, sum r, sum r^2, sum episode length, episodes, failures, divergences
     stats = torch.zeros(pkd.N_STATS, dtype=torch.float64, device=dev)
 
+    policy = None
+    if args.policy_width:  # on-device policy: Gaussian π0 + 20-step flow ODE (frozen random-init Mlps)
+        W = args.policy_width
+        policy = pk.Policy(env.obs_dim, env.nm, W, pk.mlp_init(env.obs_dim, W, 1, n_out=env.nm, final_init_scale=0.01),
+                           [-1.0] * env.nm, pk.mlp_init(5 + env.obs_dim + env.nm, W, 2, n_out=env.nm,
+                                                        final_init_scale=0.01),
+                           n_ode=20, dt_ode=0.05, max_envs=E, head_offset=0.5)
+
     def one_step(s, ev=None):
-        """One control step of the workload; ev (optional) = [start, excitations, step, stats,
+        """One control step of the workload; ev (optional) = [start, actions, step, stats,
         exchange, reset] events recorded at the phase boundaries."""
         nonlocal norm_state
-        env.fill_excitations(seed, s, actions)
+        if policy is not None:
+            policy.sample(obs, explore=True, seed=seed, step=s, global_env_offset=rank * E, actions=actions, graph=True)
+        else:
+            env.fill_excitations(seed, s, actions)
         if ev:
             ev[1].record(stream)
         env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags, reward=reward)
@@ -310,7 +323,7 @@ def main():
             stats.zero_()
         if ev:
             ev[4].record(stream)
-        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=None)
+        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=obs if policy is not None else None)
         if ev:
             ev[5].record(stream)
 
@@ -339,7 +352,7 @@ def main():
     ms = sum(e[0].elapsed_time(e[5]) for e in evs)
     kms = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     phases = {name: sum(e[i].elapsed_time(e[i + 1]) for e in evs) / args.steps
-              for i, name in enumerate(["excitations", "step", "rollout_stats", "iteration_exchange", "reset"])}
+              for i, name in enumerate(["actions", "step", "rollout_stats", "iteration_exchange", "reset"])}
     t = torch.tensor([ms, kms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -466,6 +479,8 @@ def main():
             "config": {"workload": C["desc"] if args.model == C["model"] else f"{args.config} with model {args.model}",
                        "config": args.config, "envs_per_gpu": E, "global_envs": E * world,
                        "clip": CLIPS[args.model], "parallelism": f"env shards x{world}",
+                       "actions": (f"on-device policy: Gaussian pi0 + 20-step flow ODE, Mlp width {args.policy_width} "
+                                   "(tcgen05 GEMMs, CUDA graph)") if args.policy_width else "Philox excitations",
                        "l2": "flushed between timed steps"},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic,

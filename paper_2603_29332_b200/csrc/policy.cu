@@ -60,9 +60,13 @@ __device__ __forceinline__ void philox4(uint32_t c0, uint32_t c1, uint32_t c2, u
 
 // One warp per row: a⁽⁰⁾ = mean + exp(log_std)·ε (explore) or mean
 // (deterministic), Gaussian log-density of a⁽⁰⁾, bf16 tiled copy for ψ.
+__global__ void set_step_kernel(uint32_t* d_step, uint32_t step) { *d_step = step; }
+
 __global__ void sample_a0_kernel(int M, int nm, float* a, const float* log_std, int explore, uint64_t seed,
-                                 uint32_t step, long long env_offset, float* a0_out, float* logprob, void* a_tiled) {
+                                 const uint32_t* d_step, long long env_offset, float* a0_out, float* logprob,
+                                 void* a_tiled) {
     const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    const uint32_t step = *d_step;  // set per call before a (possibly graph-replayed) sample
     if (row >= pad_to(M, kGemmBM)) return;
     const int kp = pad_to(nm, kGemmBK);
     float lp = 0.0f;
@@ -135,6 +139,7 @@ struct msk_policy {
     // scratch
     void *s_t = nullptr, *a_t = nullptr, *h1 = nullptr, *h2 = nullptr;
     float* P = nullptr;
+    uint32_t* d_step = nullptr;  // noise counter of the current call (outside the graph)
     // graph cache (keyed by the call's pointers / sizes)
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
@@ -145,7 +150,6 @@ struct msk_policy {
         float* logprob;
         int n, explore;
         uint64_t seed;
-        uint32_t step;
         long long off;
     } key{};
     cudaStream_t cap_stream = nullptr;
@@ -187,8 +191,8 @@ std::vector<float> to_f32(const double* x, size_t n) {
 }
 
 // Enqueue one sample (all kernels) on stream s.
-void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_t seed, uint32_t step,
-                    long long env_offset, float* actions, float* a0_out, float* logprob, cudaStream_t s) {
+void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_t seed, long long env_offset,
+                    float* actions, float* a0_out, float* logprob, cudaStream_t s) {
     const int H = p->hidden, D = p->obs_dim, NM = p->nm;
     ckp(launch_obs_to_tiled(obs, n, D, p->norm ? p->norm_mean : nullptr, p->norm_inv_sd, p->s_t, s), "obs");
     GemmArgs g;
@@ -204,8 +208,8 @@ void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_
     hd.A = p->h1; hd.W = p->pw4; hd.bias = p->pb4; hd.N = NM; hd.K = H; hd.out_a = nullptr;
     hd.out_f = actions; hd.ld_f = NM; hd.n_valid = NM; hd.scale = p->head_scale; hd.offset = p->head_offset;
     ckp(launch_gemm(hd, kEpiF32, s), "pi4");
-    sample_a0_kernel<<<(pad_to(n, kGemmBM) + 7) / 8, 256, 0, s>>>(n, NM, actions, p->log_std, explore, seed, step,
-                                                                  env_offset, a0_out, logprob, p->a_t);
+    sample_a0_kernel<<<(pad_to(n, kGemmBM) + 7) / 8, 256, 0, s>>>(n, NM, actions, p->log_std, explore, seed,
+                                                                  p->d_step, env_offset, a0_out, logprob, p->a_t);
     ckp(cudaGetLastError(), "a0");
     // ψ: P = W1_s · s once, then N_ODE Euler steps
     GemmArgs pg;
@@ -303,6 +307,7 @@ int msk_policy_create(int32_t obs_dim, int32_t n_actions, int32_t hidden, const 
         p->P = p->dalloc<float>(static_cast<size_t>(pad_to(max_envs, kGemmBM)) * H);
         p->norm_mean = p->dalloc<float>(D);
         p->norm_inv_sd = p->dalloc<float>(D);
+        p->d_step = p->dalloc<uint32_t>(1);
         ckp(prepare_gemm(), "cudaFuncSetAttribute(gemm)");
         ckp(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking), "stream");
         *out = p;
@@ -355,7 +360,8 @@ int msk_policy_sample(msk_policy* p, const float* obs, int32_t n, int32_t explor
     try {
         if (!obs || !actions || n < 1 || n > p->max_envs) throw std::invalid_argument("policy_sample: bad arguments");
         ckp(cudaSetDevice(p->device), "cudaSetDevice");
-        enqueue_sample(p, obs, n, explore, seed, step, global_env_offset, actions, a0, logprob,
+        set_step_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(p->d_step, step);
+        enqueue_sample(p, obs, n, explore, seed, global_env_offset, actions, a0, logprob,
                        static_cast<cudaStream_t>(stream));
         return MSK_OK;
     } catch (const std::invalid_argument& ex) {
@@ -366,8 +372,9 @@ int msk_policy_sample(msk_policy* p, const float* obs, int32_t n, int32_t explor
 }
 
 // Same sample replayed from a CUDA graph (captured on first use and whenever
-// the pointers / sizes / seed / step change; the graph is relaunched as is
-// otherwise — one launch instead of ~4 N_ODE + 6).
+// the pointers / sizes / seed change; the per-call noise counter lives in
+// device memory, so a new step just relaunches the graph — one launch instead
+// of ~4 N_ODE + 6).
 int msk_policy_sample_graph(msk_policy* p, const float* obs, int32_t n, int32_t explore, uint64_t seed,
                             uint32_t step, int64_t global_env_offset, float* actions, float* a0, float* logprob,
                             void* stream) {
@@ -375,11 +382,11 @@ int msk_policy_sample_graph(msk_policy* p, const float* obs, int32_t n, int32_t 
     try {
         if (!obs || !actions || n < 1 || n > p->max_envs) throw std::invalid_argument("policy_sample: bad arguments");
         ckp(cudaSetDevice(p->device), "cudaSetDevice");
-        const msk_policy::Key k{obs, actions, a0, logprob, n, explore, seed, step, global_env_offset};
+        const msk_policy::Key k{obs, actions, a0, logprob, n, explore, seed, global_env_offset};
         if (!p->gexec || std::memcmp(&k, &p->key, sizeof k) != 0) {
             cudaGraph_t g = nullptr;
             ckp(cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal), "capture");
-            enqueue_sample(p, obs, n, explore, seed, step, global_env_offset, actions, a0, logprob, p->cap_stream);
+            enqueue_sample(p, obs, n, explore, seed, global_env_offset, actions, a0, logprob, p->cap_stream);
             ckp(cudaStreamEndCapture(p->cap_stream, &g), "end capture");
             if (p->gexec) {
                 cudaGraphExecUpdateResultInfo info;
@@ -394,6 +401,7 @@ int msk_policy_sample_graph(msk_policy* p, const float* obs, int32_t n, int32_t 
             p->graph = g;
             p->key = k;
         }
+        set_step_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(p->d_step, step);
         ckp(cudaGraphLaunch(p->gexec, static_cast<cudaStream_t>(stream)), "graph launch");
         return MSK_OK;
     } catch (const std::invalid_argument& ex) {
