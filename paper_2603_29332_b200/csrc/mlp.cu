@@ -102,6 +102,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
     uint64_t* empty = full + kStages;
     uint64_t* acc_full = empty + kStages;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    float* sbias = reinterpret_cast<float*>(smem + kStages * (kABytes + kWBytes) + 128);  // this tile's 256 biases
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mb = blockIdx.x, nb = blockIdx.y;
     const int KB = pad_to(g.K, kGemmBK) / kGemmBK;
@@ -160,6 +161,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
                          su32(acc_full))
                      : "memory");
     } else if (warp >= 2) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31
+        for (int i = threadIdx.x - 64; i < kGemmBN; i += kGemmThreads - 64) {  // stage the tile's biases
+            const int n = blockIdx.y * kGemmBN + i;
+            sbias[i] = (g.bias && n < g.N) ? g.bias[n] : 0.0f;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
         bar_wait(acc_full, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
@@ -171,7 +177,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
             ld16(trow + c, v);
             if (n0 >= (EPI == kEpiF32 ? g.n_valid : n_out_pad)) continue;
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += (g.bias && n0 + i < g.N) ? g.bias[n0 + i] : 0.0f;
+            for (int i = 0; i < 16; ++i) v[i] += sbias[c + i];
             if (EPI == kEpiTanhTiled) {
                 if (g.addend && m < g.M) {
                     const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
@@ -283,7 +289,7 @@ std::vector<uint16_t> pack_weights(const double* W, int rows, int cols, int c0, 
     return img;
 }
 
-size_t gemm_smem_bytes() { return static_cast<size_t>(kStages) * (kABytes + kWBytes) + 256; }
+size_t gemm_smem_bytes() { return static_cast<size_t>(kStages) * (kABytes + kWBytes) + 128 + kGemmBN * 4; }
 
 cudaError_t prepare_gemm() {
     cudaError_t e;
