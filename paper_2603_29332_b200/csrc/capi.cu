@@ -339,9 +339,13 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             for (int d = 0; d <= c.n_levels; ++d) blob[M.tab_off_lvs + d] = static_cast<unsigned char>(c.level_start[d]);
             M.tab_blob = reinterpret_cast<const int4*>(ctx->upload(blob));
         }
-        const int per_block = M.tab_bytes + envs_per_block() * M.smem_env_bytes;
-        if (per_block > static_cast<int>(prop.sharedMemPerBlockOptin))
-            throw ConfigError("model needs " + std::to_string(per_block) + " B of shared memory per block");
+        // as many env slots per block as shared memory allows (28 for the whole-body models)
+        const int avail = static_cast<int>(prop.sharedMemPerBlockOptin) - M.tab_bytes;
+        M.epb = std::min(envs_per_block(), avail / std::max(1, M.smem_env_bytes));
+        if (M.epb < 1)
+            throw ConfigError("model needs " + std::to_string(M.tab_bytes + M.smem_env_bytes) +
+                              " B of shared memory per env");
+        const int per_block = M.tab_bytes + M.epb * M.smem_env_bytes;
         ck(prepare_kernels(per_block), "cudaFuncSetAttribute");
 
         DevState& S = ctx->St;

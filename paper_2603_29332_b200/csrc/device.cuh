@@ -79,6 +79,7 @@ struct DevModel {
     const int* emg_map;
     // per-env smem layout (bytes from the warp's base)
     int smem_env_bytes, off_relcs, off_dqf, off_tau, off_root, off_union;
+    int epb;  // envs per block actually used (<= the compiled warps x envs-per-warp; fewer for big models)
     // block-shared tree table at the head of dynamic smem (bytes)
     const int4* tab_blob;
     int tab_bytes, tab_off_a, tab_off_in, tab_off_meta, tab_off_child, tab_off_lvl, tab_off_lvs;

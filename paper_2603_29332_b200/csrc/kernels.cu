@@ -119,6 +119,14 @@ __device__ __forceinline__ int link_dof(const DevModel& M, int l) {
     return l >= M.floating ? M.nrd + l - M.floating : -1;
 }
 
+#ifndef MSK_EPW_DEFAULT_UNROLL
+#if defined(MSK_EPW) && MSK_EPW == 2
+#define MSK_EPW_DEFAULT_UNROLL 2
+#else
+#define MSK_EPW_DEFAULT_UNROLL 1
+#endif
+#endif
+
 // ---- SFU helpers (flush-to-zero approximations; operands here are O(1)) ----
 __device__ __forceinline__ float ex2_ftz(float x) {
     float y;
@@ -608,34 +616,75 @@ __device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, in
     return F;
 }
 
+// Inputs of one muscle for the fast path (all loads issued before any math).
+template <int NSEG>
+struct MuscleIn {
+    float4 kc[NSEG];
+    float4 p0;
+    double2 pa, pb;
+    float u, a0, lm0;
+    int ext, nsc;
+};
+
+template <int NSEG>
+__device__ __forceinline__ void muscle_load(const DevModel& M, const DevState& St, const float* act_row, size_t mb,
+                                            int m, int chunk_last, MuscleIn<NSEG>& x) {
+    const int nm = M.nm;
+    // muscles are sorted by segment count: the warp's chunk pads to the count of
+    // its last muscle (a warp-uniform bound <= NSEG)
+    x.nsc = __ldg(M.m_meta + chunk_last) & 0xff;
+    x.ext = __ldg(M.m_meta + m) >> 9;
+#pragma unroll
+    for (int k = 0; k < NSEG; ++k)
+        if (k < x.nsc) x.kc[k] = ldc4(M.seg_kf + k * nm + m);
+    x.p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
+    x.pa = ldc2d(M.m_p1a + m);
+    x.pb = ldc2d(M.m_p1b + m);
+    x.u = fminf(fmaxf(act_row[x.ext], 0.0f), 1.0f);
+    x.a0 = St.act[mb + m];
+    x.lm0 = St.lm[mb + m];
+}
+
+template <int NSEG>
+__device__ __forceinline__ void muscle_compute(const EnvSmem& S, const DevState& St, size_t mb, float* pw, int m,
+                                               const MuscleIn<NSEG>& x) {
+    double L = 0.0;
+    float tq[NSEG];
+#pragma unroll
+    for (int k = 0; k < NSEG; ++k)
+        if (k < x.nsc) L += kseg(S, x.kc[k], __float_as_int(x.kc[k].w), tq[k]);
+    const float F = muscle_update(St, mb, m, x.ext, x.p0, x.pa, x.pb, x.u, x.a0, x.lm0, L, pw);
+#pragma unroll
+    for (int k = 0; k < NSEG; ++k)
+        if (k < x.nsc) S.un[__float_as_int(x.kc[k].w) >> 11] = -F * tq[k];
+}
+
+#ifndef MSK_MUSCLE_UNROLL
+#define MSK_MUSCLE_UNROLL (MSK_EPW_DEFAULT_UNROLL)
+#endif
+
 template <int NSEG>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
                                              const float* act_row, size_t mb, float* pw, int lane) {
     const int nm = M.nm;
     if constexpr (NSEG > 0) {
-        for (int m = lane; m < nm; m += S.G) {
-            // muscles are sorted by segment count: the warp's chunk pads to the
-            // count of its last muscle (a warp-uniform bound <= NSEG)
-            const int nsc = __ldg(M.m_meta + min(m - lane + S.G - 1, nm - 1)) & 0xff;
-            const int ext = __ldg(M.m_meta + m) >> 9;
-            float4 kc[NSEG];
-#pragma unroll
-            for (int k = 0; k < NSEG; ++k)
-                if (k < nsc) kc[k] = ldc4(M.seg_kf + k * nm + m);
-            const float4 p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
-            const double2 pa = ldc2d(M.m_p1a + m), pb = ldc2d(M.m_p1b + m);
-            const float u = fminf(fmaxf(act_row[ext], 0.0f), 1.0f);
-            const float a0 = St.act[mb + m];
-            const float lm0 = St.lm[mb + m];
-            double L = 0.0;
-            float tq[NSEG];
-#pragma unroll
-            for (int k = 0; k < NSEG; ++k)
-                if (k < nsc) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
-            const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw);
-#pragma unroll
-            for (int k = 0; k < NSEG; ++k)
-                if (k < nsc) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
+        if constexpr (MSK_MUSCLE_UNROLL == 2) {
+            // two muscles per lane per iteration, loads of both before the math of
+            // either: two independent dependency chains per lane
+            for (int m0 = lane; m0 < nm; m0 += 2 * S.G) {
+                const int m1 = m0 + S.G;
+                MuscleIn<NSEG> x0, x1;
+                muscle_load<NSEG>(M, St, act_row, mb, m0, min(m0 - lane + S.G - 1, nm - 1), x0);
+                if (m1 < nm) muscle_load<NSEG>(M, St, act_row, mb, m1, min(m1 - lane + S.G - 1, nm - 1), x1);
+                muscle_compute<NSEG>(S, St, mb, pw, m0, x0);
+                if (m1 < nm) muscle_compute<NSEG>(S, St, mb, pw, m1, x1);
+            }
+        } else {
+            for (int m = lane; m < nm; m += S.G) {
+                MuscleIn<NSEG> x;
+                muscle_load<NSEG>(M, St, act_row, mb, m, min(m - lane + S.G - 1, nm - 1), x);
+                muscle_compute<NSEG>(S, St, mb, pw, m, x);
+            }
         }
     } else {
         for (int m = lane; m < nm; m += S.G) {
@@ -708,9 +757,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     constexpr int G = 32 / EPW, QS = QSL * EPW;
     const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
     const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
-    const int le = (blockIdx.x * WPB + warp) * EPW + grp;  // env index local to this launch
+    const int slot = warp * EPW + grp;            // env slot of this block (< M.epb active)
+    const int le = blockIdx.x * M.epb + slot;     // env index local to this launch
     load_tree_table(smem, M);
-    if (le >= n_envs) return;
+    if (slot >= M.epb || le >= n_envs) return;
     const int e = env0 + le;
     const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq, nm = M.nm, nl = M.nl, nrd = M.nrd;
@@ -1034,10 +1084,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
     const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
     const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
-    const int e = (blockIdx.x * WPB + warp) * EPW + grp;
+    const int slot = warp * EPW + grp, e = blockIdx.x * M.epb + slot;
     // masked resets (the per-step auto-reset of done envs) usually select no env
     // of a block: skip the block before staging the tree table
-    const bool mine = e < n_envs && (!mask || (mask[e] & mask_bits));
+    const bool mine = slot < M.epb && e < n_envs && (!mask || (mask[e] & mask_bits));
     if (!__syncthreads_or(mine)) return;
     load_tree_table(smem, M);
     if (!mine) return;
@@ -1101,9 +1151,9 @@ __global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, Dev
     constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
     const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
     const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
-    const int e = (blockIdx.x * WPB + warp) * EPW + grp;
+    const int slot = warp * EPW + grp, e = blockIdx.x * M.epb + slot;
     load_tree_table(smem, M);
-    if (e >= n_envs) return;
+    if (slot >= M.epb || e >= n_envs) return;
     const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq;
     double qd[QS], dqd[QS];
@@ -1345,10 +1395,10 @@ double measure_fp32_peak_tflops() {
 #define MSK_EPW 1   // envs per warp: 1 (32 lanes per env) or 2 (16 lanes per env)
 #endif
 #ifndef MSK_WPB
-#define MSK_WPB 7   // warps per block
+#define MSK_WPB (28 / MSK_EPW)  // warps per block: one 896-thread block = 28 envs per SM
 #endif
 #ifndef MSK_MINB
-#define MSK_MINB (4 / MSK_EPW)  // blocks per SM: 28 envs resident -> 4096 envs in one wave
+#define MSK_MINB 1  // 28 envs resident per SM -> 4096 envs in one wave; one tree table per SM
 #endif
 constexpr int kEPW = MSK_EPW;
 constexpr int kWPB = MSK_WPB;
@@ -1367,7 +1417,7 @@ cudaError_t set_step_smem(int bytes) {
 }
 
 size_t block_smem(const DevModel& M) {
-    return static_cast<size_t>(M.tab_bytes) + static_cast<size_t>(kEnvsPerBlock) * M.smem_env_bytes;
+    return static_cast<size_t>(M.tab_bytes) + static_cast<size_t>(M.epb) * M.smem_env_bytes;
 }
 
 cudaError_t prepare_kernels(int smem_bytes_per_block) {
@@ -1391,7 +1441,7 @@ int envs_per_block() { return kEnvsPerBlock; }
 
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
                  float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s) {
-    const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
+    const int blocks = (n + M.epb - 1) / M.epb;
     const size_t smem = block_smem(M);
 #define MSK_STEP(NS, QSL)                                                                                  \
     step_kernel<kWPB, kMinB, NS, kEPW, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, \
@@ -1417,13 +1467,13 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
 
 void launch_reset(const DevModel& M, const DevState& St, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t s) {
-    const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
+    const int blocks = (n + M.epb - 1) / M.epb;
     reset_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, mode, mask, bits, frames_in,
                                                                                 obs, frames_out, bad);
 }
 
 void launch_observe(const DevModel& M, const DevState& St, int n, float* obs, float* delta, cudaStream_t s) {
-    const int blocks = (n + kEnvsPerBlock - 1) / kEnvsPerBlock;
+    const int blocks = (n + M.epb - 1) / M.epb;
     observe_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, obs, delta);
 }
 
