@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "mlp.cuh"
@@ -53,6 +54,24 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes,
                  "l"(src), "r"(bytes), "r"(su32(b))
                  : "memory");
 }
+// 1-D bulk copy of `bytes` into the same CTA-relative offset of every CTA in
+// ctaMask (TMA multicast), completing on each destination's mbarrier.
+__device__ __forceinline__ void bulk_mc(void* dst, const void* src, uint32_t bytes, uint64_t* b, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {  // LBO 128 B, SBO 1024 B, version 1, no swizzle
     return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>(128 >> 4) << 16) |
            (static_cast<uint64_t>(1024 >> 4) << 32) | (1ull << 46);
@@ -93,7 +112,11 @@ __device__ __forceinline__ void store_tiled16(void* img, int KB, int m, int n0, 
     *reinterpret_cast<uint4*>(base + blk_off(r, k + 8)) = hi;
 }
 
-template <int EPI>
+// CL > 1: a cluster of CL CTAs along M shares each weight K-block: CTA r loads
+// slice r of it and multicasts it to the whole cluster, so the per-SM weight
+// traffic drops by CL; every MMA commit frees the stage in all CTAs of the
+// cluster (multicast commit), which is what each producer waits for.
+template <int EPI, int CL>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
     extern __shared__ __align__(1024) unsigned char smem[];
     unsigned char* sA = smem;                                    // kStages x 16 KB
@@ -110,11 +133,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             bar_init(&full[s], 1);
-            bar_init(&empty[s], 1);
+            bar_init(&empty[s], CL);  // one release per cluster CTA's MMAs
         }
         bar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    if constexpr (CL > 1) cluster_sync();  // peers' barriers exist before any multicast
     if (warp == 1) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
                      : "memory");
@@ -130,12 +154,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
     if (warp == 0 && lane == 0) {  // TMA producer
         const char* A = static_cast<const char*>(g.A) + static_cast<size_t>(mb) * KB * kABytes;
         const char* W = static_cast<const char*>(g.W) + static_cast<size_t>(nb) * KB * kWBytes;
+        const uint32_t rank = CL > 1 ? cluster_rank() : 0;
+        constexpr uint32_t kSlice = kWBytes / CL;
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % kStages;
             if (kb >= kStages) bar_wait(&empty[s], ((kb / kStages) - 1) & 1);
             bar_expect(&full[s], kABytes + kWBytes);
             bulk(sA + s * kABytes, A + static_cast<size_t>(kb) * kABytes, kABytes, &full[s]);
-            bulk(sW + s * kWBytes, W + static_cast<size_t>(kb) * kWBytes, kWBytes, &full[s]);
+            if constexpr (CL == 1) {
+                bulk(sW + s * kWBytes, W + static_cast<size_t>(kb) * kWBytes, kWBytes, &full[s]);
+            } else {
+                bulk_mc(sW + s * kWBytes + rank * kSlice, W + static_cast<size_t>(kb) * kWBytes + rank * kSlice, kSlice,
+                        &full[s], static_cast<uint16_t>((1u << CL) - 1));
+            }
         }
     } else if (warp == 1 && lane == 0) {  // MMA issuer
         for (int kb = 0; kb < KB; ++kb) {
@@ -153,9 +184,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
                     "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc), "r"(acc)
                     : "memory");
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                             su32(&empty[s]))
-                         : "memory");
+            if constexpr (CL == 1) {
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                                 su32(&empty[s]))
+                             : "memory");
+            } else {  // stage s of this CTA is free: tell every producer in the cluster
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                    "%1;" ::"r"(su32(&empty[s])),
+                    "h"(static_cast<uint16_t>((1u << CL) - 1))
+                    : "memory");
+            }
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                          su32(acc_full))
@@ -246,6 +285,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still signal it
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
@@ -291,14 +331,40 @@ std::vector<uint16_t> pack_weights(const double* W, int rows, int cols, int c0, 
 
 size_t gemm_smem_bytes() { return static_cast<size_t>(kStages) * (kABytes + kWBytes) + 128 + kGemmBN * 4; }
 
+namespace {
+template <int EPI>
+cudaError_t prepare_epi(int bytes) {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(gemm_kernel<EPI, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+    if ((e = cudaFuncSetAttribute(gemm_kernel<EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
+    return cudaFuncSetAttribute(gemm_kernel<EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+template <int EPI>
+cudaError_t launch_epi(cudaLaunchConfig_t& cfg, int cl, const GemmArgs& g) {
+    switch (cl) {
+        case 4: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 4>, g);
+        case 2: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 2>, g);
+        default: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 1>, g);
+    }
+}
+}  // namespace
+
 cudaError_t prepare_gemm() {
     cudaError_t e;
     const int bytes = static_cast<int>(gemm_smem_bytes());
-    if ((e = cudaFuncSetAttribute(gemm_kernel<kEpiTanhTiled>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
-        return e;
-    if ((e = cudaFuncSetAttribute(gemm_kernel<kEpiF32>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
-        return e;
-    return cudaFuncSetAttribute(gemm_kernel<kEpiOde>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if ((e = prepare_epi<kEpiTanhTiled>(bytes))) return e;
+    if ((e = prepare_epi<kEpiF32>(bytes))) return e;
+    return prepare_epi<kEpiOde>(bytes);
+}
+
+// Weight-multicast cluster size for a grid with `mt` row tiles (MSK_GEMM_CLUSTER overrides).
+static int gemm_cluster(int mt) {
+    static const int forced = [] {
+        const char* v = std::getenv("MSK_GEMM_CLUSTER");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (forced == 1 || forced == 2 || forced == 4) return mt % forced == 0 ? forced : 1;
+    return mt % 4 == 0 ? 4 : (mt % 2 == 0 ? 2 : 1);
 }
 
 cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
@@ -307,15 +373,20 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = gemm_smem_bytes();
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    const int cl = gemm_cluster(static_cast<int>(cfg.gridDim.x));
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = cl;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     switch (epi) {
-        case kEpiTanhTiled: return cudaLaunchKernelEx(&cfg, gemm_kernel<kEpiTanhTiled>, g);
-        case kEpiF32: return cudaLaunchKernelEx(&cfg, gemm_kernel<kEpiF32>, g);
-        default: return cudaLaunchKernelEx(&cfg, gemm_kernel<kEpiOde>, g);
+        case kEpiTanhTiled: return launch_epi<kEpiTanhTiled>(cfg, cl, g);
+        case kEpiF32: return launch_epi<kEpiF32>(cfg, cl, g);
+        default: return launch_epi<kEpiOde>(cfg, cl, g);
     }
 }
 
