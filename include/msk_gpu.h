@@ -243,6 +243,26 @@ int32_t msk_policy_time_features(double t, double* out5);
 int msk_gemm_test(const float* X, int32_t M, int32_t K, const double* W, const float* b, int32_t N, int32_t epi,
                   float* Y);
 
+/* ---- on-device rollout buffer + GAE ----------------------
+ * h control steps x E envs, step-major: obs, a0, actions, logprob, reward,
+ * done (the step's flags; bit MSK_FLAG_DONE), value, delta.  msk_rollout_gae:
+ * delta_t = r_t + gamma V_{t+1} (1 - done_t) - V_t, A_t = delta_t + gamma lam
+ * (1 - done_t) A_{t+1} (V_h = bootstrap [E]), returns = A + V; normalize != 0
+ * standardises the advantages over the batch.  Outputs [h x E] (nullable). */
+typedef struct msk_rollout msk_rollout;
+int msk_rollout_create(int32_t n_envs, int32_t horizon, int32_t obs_dim, int32_t act_dim, int32_t delta_dim,
+                       int32_t device, msk_rollout** out);
+void msk_rollout_destroy(msk_rollout* r);
+const char* msk_rollout_last_error(const msk_rollout* r);
+/* Store step t (device buffers [E x dim], each nullable). */
+int msk_rollout_record(msk_rollout* r, int32_t t, const float* obs, const float* a0, const float* actions,
+                       const float* logprob, const float* reward, const uint8_t* flags, const float* value,
+                       const float* delta, void* stream);
+int msk_rollout_gae(msk_rollout* r, const float* bootstrap_value, float gamma, float lam, int32_t normalize,
+                    float* advantages, float* returns, void* stream);
+/* Device pointer of a stored field: 0 obs, 1 a0, 2 actions, 3 logprob, 4 reward, 5 done, 6 value, 7 delta. */
+void* msk_rollout_field(msk_rollout* r, int32_t field);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,3 +72,18 @@ def sample_action(pi_theta, log_std, psi_theta, obs, hidden, n_ode=20, dt=0.05, 
         phi = np.broadcast_to(time_features(k * dt), (n, 5))
         a = a + mlp_forward(psi, np.concatenate([phi, s, a], axis=1)) * dt
     return a, a0, logp
+
+
+def compute_gae(reward, done, value, bootstrap, gamma, lam):
+    """compute_gae, [h x E] arrays, f64: returns (advantages, returns)."""
+    reward, value = np.asarray(reward, np.float64), np.asarray(value, np.float64)
+    nd = 1.0 - (np.asarray(done) & 1).astype(np.float64)
+    h = reward.shape[0]
+    adv = np.zeros_like(reward)
+    next_v, next_a = np.asarray(bootstrap, np.float64), 0.0
+    for t in range(h - 1, -1, -1):
+        delta = reward[t] + gamma * next_v * nd[t] - value[t]
+        next_a = delta + gamma * lam * nd[t] * next_a
+        adv[t] = next_a
+        next_v = value[t]
+    return adv, adv + value

@@ -14,7 +14,7 @@ import ctypes as C
 import os
 from dataclasses import dataclass, field
 
-__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError", "mlp_init", "Policy",
+__all__ = ["EnvConfig", "RewardConfig", "RewardMode", "EnvBatch", "lib", "LIB_PATH", "MskError", "mlp_init", "Policy", "Rollout",
            "FLAG_DONE", "FLAG_FAILED", "FLAG_DIVERGED", "FLAG_NOT_STEPPED", "FLAG_BAD_ACTION"]
 
 LIB_PATH = os.environ.get("MSK_B200_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmsk_b200.so")
@@ -89,6 +89,52 @@ class Policy:
         if getattr(self, "h", None):
             lib().msk_policy_destroy(self.h)
             self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Rollout:
+    """On-device rollout buffer (h x E, step-major) + GAE (msk_rollout_*)."""
+
+    def __init__(self, n_envs, horizon, obs_dim, act_dim, delta_dim, device=0):
+        import torch
+
+        self.torch = torch
+        self.E, self.h = n_envs, horizon
+        h = C.c_void_p()
+        if lib().msk_rollout_create(n_envs, horizon, obs_dim, act_dim, delta_dim, device, C.byref(h)) != 0:
+            raise MskError(lib().msk_rollout_last_error(None).decode())
+        self.h_ = h
+        self.device = torch.device("cuda", device)
+
+    def _ck(self, rc):
+        if rc != 0:
+            raise MskError(lib().msk_rollout_last_error(self.h_).decode())
+
+    def record(self, t, obs=None, a0=None, actions=None, logprob=None, reward=None, flags=None, value=None,
+               delta=None, stream=None):
+        s = stream.cuda_stream if stream is not None else self.torch.cuda.current_stream(self.device).cuda_stream
+        self._ck(lib().msk_rollout_record(self.h_, int(t), _p(obs), _p(a0), _p(actions), _p(logprob), _p(reward),
+                                          _p(flags), _p(value), _p(delta), s))
+
+    def gae(self, bootstrap_value, gamma=0.99, lam=0.95, normalize=True, stream=None):
+        """(advantages, returns), each [h x E] float32 on the device."""
+        torch = self.torch
+        adv = torch.empty(self.h, self.E, device=self.device)
+        ret = torch.empty(self.h, self.E, device=self.device)
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        self._ck(lib().msk_rollout_gae(self.h_, _p(bootstrap_value.contiguous()), float(gamma), float(lam),
+                                       int(bool(normalize)), _p(adv), _p(ret), s))
+        return adv, ret
+
+    def close(self):
+        if getattr(self, "h_", None):
+            lib().msk_rollout_destroy(self.h_)
+            self.h_ = None
 
     def __del__(self):
         try:
@@ -195,6 +241,14 @@ def lib():
         L.msk_policy_time_features.restype = C.c_int32
         L.msk_policy_time_features.argtypes = [C.c_double, _vp]
         L.msk_gemm_test.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp, C.c_int32, C.c_int32, _vp]
+        L.msk_rollout_create.argtypes = [C.c_int32] * 6 + [_vp]
+        L.msk_rollout_destroy.argtypes = [_vp]
+        L.msk_rollout_last_error.restype = C.c_char_p
+        L.msk_rollout_last_error.argtypes = [_vp]
+        L.msk_rollout_record.argtypes = [_vp, C.c_int32] + [_vp] * 9
+        L.msk_rollout_gae.argtypes = [_vp, _vp, C.c_float, C.c_float, C.c_int32, _vp, _vp, _vp]
+        L.msk_rollout_field.restype = C.c_void_p
+        L.msk_rollout_field.argtypes = [_vp, C.c_int32]
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
         L.msk_mlp_param_count.restype = C.c_int64

@@ -124,3 +124,39 @@ def test_policy_explore_noise_and_logprob():
     p.sample(obs, explore=True, seed=11, step=4, a0=a0b)
     assert not torch.equal(a0, a0b)
     p.close()
+
+
+def test_rollout_gae_matches_oracle_and_spec():
+    """On-device GAE vs the f64 recursion; SPEC examples."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from oracle.policy import compute_gae
+
+    E, h = 300, 8
+    rng = np.random.default_rng(4)
+    r = rng.normal(0, 1, (h, E)).astype(np.float32)
+    v = rng.normal(0, 1, (h, E)).astype(np.float32)
+    boot = rng.normal(0, 1, E).astype(np.float32)
+    flags = (rng.uniform(0, 1, (h, E)) < 0.2).astype(np.uint8)  # bit 0 = done
+    ro = pk.Rollout(E, h, 3, 2, 1)
+    for t in range(h):
+        ro.record(t, reward=torch.as_tensor(r[t], device="cuda"), flags=torch.as_tensor(flags[t], device="cuda"),
+                  value=torch.as_tensor(v[t], device="cuda"))
+    bt = torch.as_tensor(boot, device="cuda")
+    adv, ret = ro.gae(bt, gamma=0.99, lam=0.95, normalize=False)
+    a_ref, r_ref = compute_gae(r, flags, v, boot, 0.99, 0.95)
+    assert np.abs(adv.cpu().numpy() - a_ref).max() <= 1e-4 * max(1.0, np.abs(a_ref).max())
+    assert np.abs(ret.cpu().numpy() - r_ref).max() <= 1e-4 * max(1.0, np.abs(r_ref).max())
+    # normalised advantages: zero mean, unit variance over the batch
+    adv_n, _ = ro.gae(bt, gamma=0.99, lam=0.95, normalize=True)
+    an = adv_n.cpu().numpy().astype(np.float64)
+    assert abs(an.mean()) < 1e-5 and abs(an.std() - 1.0) < 1e-4
+    # lambda = 0 -> TD residual; single done step -> A = r - V (SPEC.md:398-400)
+    adv0, _ = ro.gae(bt, gamma=0.99, lam=0.0, normalize=False)
+    nxt = np.concatenate([v[1:], boot[None]], 0)
+    td = r + 0.99 * nxt * (1 - (flags & 1)) - v
+    assert np.abs(adv0.cpu().numpy() - td).max() <= 1e-5
+    d = (flags[-1] & 1) == 1
+    assert np.abs(adv0.cpu().numpy()[-1][d] - (r[-1] - v[-1])[d]).max() <= 1e-6
+    ro.close()
