@@ -243,6 +243,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-groups", type=int, default=2, help="env groups (contexts) in the e2e host-buffer loop")
+    ap.add_argument("--rollout", action="store_true", help="record every step into the on-device rollout buffer "
+                    "and run GAE at each iteration boundary")
     ap.add_argument("--policy-width", type=int, default=0,
                     help="actions from the on-device flow policy of this hidden width (0: Philox excitations)")
     args = ap.parse_args()
@@ -301,12 +303,24 @@ def main():
                                                         final_init_scale=0.01),
                            n_ode=20, dt_ode=0.05, max_envs=E, head_offset=0.5)
 
+    rollout = None
+    if args.rollout:  # on-device rollout buffer of h = 8 steps + GAE at each iteration boundary
+        h_ro = C["exchange"] or 8
+        rollout = pk.Rollout(E, h_ro, env.obs_dim, env.nm, env.delta_dim)
+        ro_a0 = torch.empty(E, env.nm, device=dev)
+        ro_lp = torch.zeros(E, device=dev)
+        ro_v = torch.zeros(E, device=dev)  # no critic on this path: V = 0
+
     def one_step(s, ev=None):
         """One control step of the workload; ev (optional) = [start, actions, step, stats,
         exchange, reset] events recorded at the phase boundaries."""
         nonlocal norm_state
+        if rollout is not None:  # the observation the action is taken from
+            rollout.record(s % rollout.h, obs=obs)
         if policy is not None:
-            policy.sample(obs, explore=True, seed=seed, step=s, global_env_offset=rank * E, actions=actions, graph=True)
+            policy.sample(obs, explore=True, seed=seed, step=s, global_env_offset=rank * E, actions=actions,
+                          a0=ro_a0 if rollout is not None else None, logprob=ro_lp if rollout is not None else None,
+                          graph=True)
         else:
             env.fill_excitations(seed, s, actions)
         if ev:
@@ -314,6 +328,12 @@ def main():
         env.step(actions, obs=obs, delta=delta, reward_aux=raux, flags=flags, reward=reward)
         if ev:
             ev[2].record(stream)
+        if rollout is not None:
+            rollout.record(s % rollout.h, a0=ro_a0 if policy is not None else None, actions=actions,
+                           logprob=ro_lp, reward=reward if reward is not None else raux, flags=flags, value=ro_v,
+                           delta=delta)
+            if (s + 1) % rollout.h == 0:
+                rollout.gae(ro_v, gamma=0.99, lam=0.95, normalize=True)
         if C["exchange"]:
             env.rollout_stats(flags, stats, reward=reward if reward is not None else raux)
         if ev:
@@ -481,6 +501,7 @@ def main():
                        "clip": CLIPS[args.model], "parallelism": f"env shards x{world}",
                        "actions": (f"on-device policy: Gaussian pi0 + 20-step flow ODE, Mlp width {args.policy_width} "
                                    "(tcgen05 GEMMs, CUDA graph)") if args.policy_width else "Philox excitations",
+                       "rollout": "on-device buffer + GAE" if args.rollout else None,
                        "l2": "flushed between timed steps"},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic,
