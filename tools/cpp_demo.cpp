@@ -5,12 +5,16 @@
 // and prints throughput, a checksum of the final observations and the mean reward.
 //
 //   build: make -C tools cpp_demo   (links paper_2603_29332_b200/libmsk_b200.so)
-//   run:   tools/cpp_demo <model.json> <clip.csv> [envs] [steps]
+//   run:   tools/cpp_demo <model.json> <clip.csv> [envs] [steps] [policy_width]
+// With policy_width > 0 the actions come from the on-device flow policy
+// (msk_policy_*: Gaussian pi0 + 20-step flow ODE on the tensor cores) and every
+// step is recorded into the on-device rollout buffer, with GAE every 8 steps.
 #include <cuda_runtime.h>
 
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <stdexcept>
 #include <vector>
 
 #include "msk_gpu.hpp"
@@ -22,6 +26,7 @@ int main(int argc, char** argv) {
     }
     const int E = argc > 3 ? std::atoi(argv[3]) : 1024;
     const int steps = argc > 4 ? std::atoi(argv[4]) : 20;
+    const int width = argc > 5 ? std::atoi(argv[5]) : 0;
     try {
         msk::gpu::EnvConfig cfg;
         cfg.episode_horizon = 1000;
@@ -41,12 +46,46 @@ int main(int argc, char** argv) {
         env.set_discriminator(msk::gpu::EnvBatch::mlp_init(env.delta_dim(), 256, 1, 7), 256);
         env.reset(nullptr, 0xff, obs);
         msk::gpu::StepBuffers out{obs, delta, raux, flags};
+        // optional on-device policy + rollout buffer (C ABI)
+        msk_policy* pol = nullptr;
+        msk_rollout* ro = nullptr;
+        float *a0 = nullptr, *logp = nullptr, *value = nullptr, *adv = nullptr, *ret = nullptr;
+        const int horizon = 8;
+        if (width > 0) {
+            const int D = env.observation_dim(), NM = env.action_dim();
+            auto pi = msk::gpu::EnvBatch::mlp_init(D, width, NM, 1, 0.01);
+            auto psi = msk::gpu::EnvBatch::mlp_init(5 + D + NM, width, NM, 2, 0.01);
+            std::vector<double> log_std(NM, -1.0);
+            if (msk_policy_create(D, NM, width, pi.data(), static_cast<int64_t>(pi.size()), 1.0, 0.5, log_std.data(),
+                                  psi.data(), static_cast<int64_t>(psi.size()), 20, 0.05, E, 0, &pol) != MSK_OK)
+                throw std::runtime_error(msk_policy_last_error(nullptr));
+            if (msk_rollout_create(E, horizon, D, NM, env.delta_dim(), 0, &ro) != MSK_OK)
+                throw std::runtime_error(msk_rollout_last_error(nullptr));
+            cudaMalloc(&a0, sizeof(float) * E * NM);
+            cudaMalloc(&logp, sizeof(float) * E);
+            cudaMalloc(&value, sizeof(float) * E);
+            cudaMemset(value, 0, sizeof(float) * E);
+            cudaMalloc(&adv, sizeof(float) * E * horizon);
+            cudaMalloc(&ret, sizeof(float) * E * horizon);
+        }
         cudaDeviceSynchronize();
         const auto t0 = std::chrono::steady_clock::now();
         for (int s = 0; s < steps; ++s) {
-            env.fill_excitations(0x5EED, static_cast<uint32_t>(s), actions);
+            if (pol) {  // a = flow-refined Gaussian sample from the current observation
+                msk_rollout_record(ro, s % horizon, obs, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                   nullptr);
+                if (msk_policy_sample_graph(pol, obs, E, 1, 0x5EED, static_cast<uint32_t>(s), 0, actions, a0, logp,
+                                            nullptr) != MSK_OK)
+                    throw std::runtime_error(msk_policy_last_error(pol));
+            } else {
+                env.fill_excitations(0x5EED, static_cast<uint32_t>(s), actions);
+            }
             env.step(actions, out, reward);  // Env::step(action, fn): reward = r(D(Δ)) + reward_aux
-            env.reset(flags, MSK_FLAG_DONE);  // batched auto-reset
+            if (ro) {
+                msk_rollout_record(ro, s % horizon, nullptr, a0, actions, logp, reward, flags, value, delta, nullptr);
+                if ((s + 1) % horizon == 0) msk_rollout_gae(ro, value, 0.99f, 0.95f, 1, adv, ret, nullptr);
+            }
+            env.reset(flags, MSK_FLAG_DONE, pol ? obs : nullptr);  // batched auto-reset
         }
         cudaDeviceSynchronize();
         const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -58,9 +97,13 @@ int main(int argc, char** argv) {
         cudaMemcpy(hr.data(), reward, sizeof(float) * E, cudaMemcpyDeviceToHost);
         double rsum = 0.0;
         for (float v : hr) rsum += v;
-        std::printf("envs=%d steps=%d env-steps/s=%.0f obs_checksum=%.6e mean_reward=%.6f\n", E, steps,
-                    E * steps / secs, checksum, rsum / E);
+        std::printf("envs=%d steps=%d policy_width=%d env-steps/s=%.0f obs_checksum=%.6e mean_reward=%.6f\n", E,
+                    steps, width, E * steps / secs, checksum, rsum / E);
         cudaFree(reward);
+        if (pol) msk_policy_destroy(pol);
+        if (ro) msk_rollout_destroy(ro);
+        for (float* p : {a0, logp, value, adv, ret})
+            if (p) cudaFree(p);
         cudaFree(actions);
         cudaFree(obs);
         cudaFree(delta);
