@@ -119,14 +119,6 @@ __device__ __forceinline__ int link_dof(const DevModel& M, int l) {
     return l >= M.floating ? M.nrd + l - M.floating : -1;
 }
 
-#ifndef MSK_EPW_DEFAULT_UNROLL
-#if defined(MSK_EPW) && MSK_EPW == 2
-#define MSK_EPW_DEFAULT_UNROLL 2
-#else
-#define MSK_EPW_DEFAULT_UNROLL 1
-#endif
-#endif
-
 // ---- SFU helpers (flush-to-zero approximations; operands here are O(1)) ----
 __device__ __forceinline__ float ex2_ftz(float x) {
     float y;
@@ -145,26 +137,10 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 }
 constexpr float kLog2e = 1.4426950408889634f;
 
-// Read-only model-constant loads.  MSK_L1_KEEP marks them evict_last in L1 so
-// the per-env state stream does not push them out (A/B experiment).
-__device__ __forceinline__ float4 ldc4(const float4* p) {
-#ifdef MSK_L1_KEEP
-    float4 v;
-    asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ double2 ldc2d(const double2* p) {
-#ifdef MSK_L1_KEEP
-    double2 v;
-    asm("ld.global.nc.L1::evict_last.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
+// Read-only model-constant loads (non-coherent path; the tables never change
+// during a launch).
+__device__ __forceinline__ float4 ldc4(const float4* p) { return __ldg(p); }
+__device__ __forceinline__ double2 ldc2d(const double2* p) { return __ldg(p); }
 
 // ---- Hill-type muscle (muscle.cpp:9-40) -----------------------------------
 __device__ __forceinline__ float hill_fl(float l) {  // exp(-((l-1)/0.45)^2)
@@ -659,32 +635,15 @@ __device__ __forceinline__ void muscle_compute(const EnvSmem& S, const DevState&
         if (k < x.nsc) S.un[__float_as_int(x.kc[k].w) >> 11] = -F * tq[k];
 }
 
-#ifndef MSK_MUSCLE_UNROLL
-#define MSK_MUSCLE_UNROLL (MSK_EPW_DEFAULT_UNROLL)
-#endif
-
 template <int NSEG>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
                                              const float* act_row, size_t mb, float* pw, int lane) {
     const int nm = M.nm;
     if constexpr (NSEG > 0) {
-        if constexpr (MSK_MUSCLE_UNROLL == 2) {
-            // two muscles per lane per iteration, loads of both before the math of
-            // either: two independent dependency chains per lane
-            for (int m0 = lane; m0 < nm; m0 += 2 * S.G) {
-                const int m1 = m0 + S.G;
-                MuscleIn<NSEG> x0, x1;
-                muscle_load<NSEG>(M, St, act_row, mb, m0, min(m0 - lane + S.G - 1, nm - 1), x0);
-                if (m1 < nm) muscle_load<NSEG>(M, St, act_row, mb, m1, min(m1 - lane + S.G - 1, nm - 1), x1);
-                muscle_compute<NSEG>(S, St, mb, pw, m0, x0);
-                if (m1 < nm) muscle_compute<NSEG>(S, St, mb, pw, m1, x1);
-            }
-        } else {
-            for (int m = lane; m < nm; m += S.G) {
-                MuscleIn<NSEG> x;
-                muscle_load<NSEG>(M, St, act_row, mb, m, min(m - lane + S.G - 1, nm - 1), x);
-                muscle_compute<NSEG>(S, St, mb, pw, m, x);
-            }
+        for (int m = lane; m < nm; m += S.G) {
+            MuscleIn<NSEG> x;
+            muscle_load<NSEG>(M, St, act_row, mb, m, min(m - lane + S.G - 1, nm - 1), x);
+            muscle_compute<NSEG>(S, St, mb, pw, m, x);
         }
     } else {
         for (int m = lane; m < nm; m += S.G) {
