@@ -112,181 +112,302 @@ __device__ __forceinline__ void store_tiled16(void* img, int KB, int m, int n0, 
     *reinterpret_cast<uint4*>(base + blk_off(r, k + 8)) = hi;
 }
 
+// Epilogue of one 128 x 256 output tile (row tile mb, column tile nb) by the
+// four epilogue warps (2-5): warp w reads TMEM lanes 32 (w % 4) .. + 31.
+template <int EPI>
+__device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, float* sbias, uint64_t* acc_full,
+                                              int mb, int nb, int warp, int lane) {
+    for (int i = threadIdx.x - 64; i < kGemmBN; i += kGemmThreads - 64) {  // stage the tile's biases
+        const int n = nb * kGemmBN + i;
+        sbias[i] = (g.bias && n < g.N) ? g.bias[n] : 0.0f;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+    bar_wait(acc_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    const int n_out_pad = pad_to(EPI == kEpiOde ? g.n_valid : g.N, kGemmBK);  // tiled output width
+    for (int c = 0; c < kGemmBN; c += 16) {
+        const int n0 = nb * kGemmBN + c;
+        float v[16];
+        ld16(trow + c, v);
+        if (n0 >= (EPI == kEpiF32 ? g.n_valid : n_out_pad)) continue;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] += sbias[c + i];
+        if (EPI == kEpiTanhTiled) {
+            if (g.addend && m < g.M) {
+                const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
+                if (n0 + 16 <= g.N) {  // 4 x 16-B loads of the thread's 64 contiguous bytes
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4) {
+                        const float4 t = *reinterpret_cast<const float4*>(ap + i);
+                        v[i] += t.x;
+                        v[i + 1] += t.y;
+                        v[i + 2] += t.z;
+                        v[i + 3] += t.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (n0 + i < g.N) v[i] += ap[i];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+            store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
+        } else if (EPI == kEpiF32) {
+            if (m < g.M) {
+                float* op = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    v[i] = fmaf(g.scale, v[i], g.offset);
+                    if (g.addend && n0 + i < g.n_valid) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
+                }
+                if (n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (n0 + i < g.n_valid) op[i] = v[i];
+                }
+            }
+        } else {  // kEpiOde: a += dt * psi
+            float y[16];
+            float* ap = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
+            if (m < g.M && n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {  // 16-B vector RMW
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(ap + i);
+                    y[i] = fmaf(g.dt, v[i], t.x);
+                    y[i + 1] = fmaf(g.dt, v[i + 1], t.y);
+                    y[i + 2] = fmaf(g.dt, v[i + 2], t.z);
+                    y[i + 3] = fmaf(g.dt, v[i + 3], t.w);
+                    *reinterpret_cast<float4*>(ap + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    y[i] = 0.0f;
+                    if (m < g.M && n0 + i < g.n_valid) {
+                        y[i] = fmaf(g.dt, v[i], ap[i]);
+                        ap[i] = y[i];
+                    }
+                }
+            }
+            if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
+        }
+    }
+}
+
 // CL > 1: a cluster of CL CTAs along M shares each weight K-block: CTA r loads
 // slice r of it and multicasts it to the whole cluster, so the per-SM weight
 // traffic drops by CL; every MMA commit frees the stage in all CTAs of the
 // cluster (multicast commit), which is what each producer waits for.
 template <int EPI, int CL>
 __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
+extern __shared__ __align__(1024) unsigned char smem[];
+unsigned char* sA = smem;                                    // kStages x 16 KB
+unsigned char* sW = smem + kStages * kABytes;                // kStages x 32 KB
+uint64_t* full = reinterpret_cast<uint64_t*>(sW + kStages * kWBytes);
+uint64_t* empty = full + kStages;
+uint64_t* acc_full = empty + kStages;
+uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
+float* sbias = reinterpret_cast<float*>(smem + kStages * (kABytes + kWBytes) + 128);  // this tile's 256 biases
+const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+const int mb = blockIdx.x, nb = blockIdx.y;
+const int KB = pad_to(g.K, kGemmBK) / kGemmBK;
+
+if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+        bar_init(&full[s], 1);
+        bar_init(&empty[s], CL);  // one release per cluster CTA's MMAs
+    }
+    bar_init(acc_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+if constexpr (CL > 1) cluster_sync();  // peers' barriers exist before any multicast
+if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+__syncthreads();
+asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+const uint32_t tmem = *tslot;
+// inputs may be the previous kernel's outputs (programmatic dependent launch)
+asm volatile("griddepcontrol.wait;" ::: "memory");
+
+if (warp == 0 && lane == 0) {  // TMA producer
+    const char* A = static_cast<const char*>(g.A) + static_cast<size_t>(mb) * KB * kABytes;
+    const char* W = static_cast<const char*>(g.W) + static_cast<size_t>(nb) * KB * kWBytes;
+    const uint32_t rank = CL > 1 ? cluster_rank() : 0;
+    constexpr uint32_t kSlice = kWBytes / CL;
+    for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) bar_wait(&empty[s], ((kb / kStages) - 1) & 1);
+        bar_expect(&full[s], kABytes + kWBytes);
+        bulk(sA + s * kABytes, A + static_cast<size_t>(kb) * kABytes, kABytes, &full[s]);
+        if constexpr (CL == 1) {
+            bulk(sW + s * kWBytes, W + static_cast<size_t>(kb) * kWBytes, kWBytes, &full[s]);
+        } else {
+            bulk_mc(sW + s * kWBytes + rank * kSlice, W + static_cast<size_t>(kb) * kWBytes + rank * kSlice, kSlice,
+                    &full[s], static_cast<uint16_t>((1u << CL) - 1));
+        }
+    }
+} else if (warp == 1 && lane == 0) {  // MMA issuer
+    for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % kStages;
+        bar_wait(&full[s], (kb / kStages) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t a0 = su32(sA + s * kABytes), w0 = su32(sW + s * kWBytes);
+#pragma unroll
+        for (int k = 0; k < kGemmBK / 16; ++k) {
+            const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc), "r"(acc)
+                : "memory");
+        }
+        if constexpr (CL == 1) {
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             su32(&empty[s]))
+                         : "memory");
+        } else {  // stage s of this CTA is free: tell every producer in the cluster
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                "%1;" ::"r"(su32(&empty[s])),
+                "h"(static_cast<uint16_t>((1u << CL) - 1))
+                : "memory");
+        }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     su32(acc_full))
+                 : "memory");
+} else if (warp >= 2) {
+    gemm_epilogue<EPI>(g, tmem, sbias, acc_full, mb, nb, warp, lane);
+}
+asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+__syncthreads();
+if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still signal it
+if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+// CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs computes a
+// 256 x 256 tile with one M = 256 UMMA per K-step issued by the leader (rank 0).
+// Each CTA stages its own 128 rows of A and its own 128-row half of the weight
+// block (16 + 16 KB per K-block instead of 16 + 32 KB), so the bytes each SM
+// ingests per flop drop by 1.5x.  The peer's TMA completion is relayed to the
+// leader's stage barrier by a remote mbarrier arrive; the leader's MMA commits
+// are multicast to both CTAs (stage release, accumulator ready); each CTA's
+// TMEM holds its own 128 accumulator rows, so the epilogue is unchanged.
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kGemmBN >> 3) << 17) |
+                             (static_cast<uint32_t>((2 * kGemmBM) >> 4) << 24);
+
+__device__ __forceinline__ void bar_wait_cluster(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "GWC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra GWC_%=;\n\t}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm2_kernel(GemmArgs g) {
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char* sA = smem;                                    // kStages x 16 KB
-    unsigned char* sW = smem + kStages * kABytes;                // kStages x 32 KB
-    uint64_t* full = reinterpret_cast<uint64_t*>(sW + kStages * kWBytes);
+    constexpr int kWHalf = kWBytes / 2;                           // 128 weight rows x 64 K
+    unsigned char* sA = smem;                                     // kStages x 16 KB
+    unsigned char* sW = smem + kStages * kABytes;                 // kStages x 16 KB (this CTA's half)
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * (kABytes + kWBytes));
     uint64_t* empty = full + kStages;
     uint64_t* acc_full = empty + kStages;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
-    float* sbias = reinterpret_cast<float*>(smem + kStages * (kABytes + kWBytes) + 128);  // this tile's 256 biases
+    float* sbias = reinterpret_cast<float*>(smem + kStages * (kABytes + kWBytes) + 128);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int mb = blockIdx.x, nb = blockIdx.y;
     const int KB = pad_to(g.K, kGemmBK) / kGemmBK;
+    const uint32_t rank = cluster_rank();
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            bar_init(&full[s], 1);
-            bar_init(&empty[s], CL);  // one release per cluster CTA's MMAs
+            bar_init(&full[s], rank == 0 ? 2 : 1);  // leader: own TMA + the peer's relay
+            bar_init(&empty[s], 1);                 // the leader's (multicast) MMA commit
         }
         bar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    if constexpr (CL > 1) cluster_sync();  // peers' barriers exist before any multicast
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
+    cluster_sync();
+    if (warp == 1) {  // both CTAs: the pair's TMEM (same column base in each)
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
                      : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tslot;
-    // inputs may be the previous kernel's outputs (programmatic dependent launch)
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
-    if (warp == 0 && lane == 0) {  // TMA producer
+    if (warp == 0 && lane == 0) {  // TMA producer (both CTAs)
         const char* A = static_cast<const char*>(g.A) + static_cast<size_t>(mb) * KB * kABytes;
-        const char* W = static_cast<const char*>(g.W) + static_cast<size_t>(nb) * KB * kWBytes;
-        const uint32_t rank = CL > 1 ? cluster_rank() : 0;
-        constexpr uint32_t kSlice = kWBytes / CL;
+        const char* W = static_cast<const char*>(g.W) + static_cast<size_t>(nb) * KB * kWBytes + rank * kWHalf;
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % kStages;
             if (kb >= kStages) bar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-            bar_expect(&full[s], kABytes + kWBytes);
+            bar_expect(&full[s], kABytes + kWHalf);
             bulk(sA + s * kABytes, A + static_cast<size_t>(kb) * kABytes, kABytes, &full[s]);
-            if constexpr (CL == 1) {
-                bulk(sW + s * kWBytes, W + static_cast<size_t>(kb) * kWBytes, kWBytes, &full[s]);
-            } else {
-                bulk_mc(sW + s * kWBytes + rank * kSlice, W + static_cast<size_t>(kb) * kWBytes + rank * kSlice, kSlice,
-                        &full[s], static_cast<uint16_t>((1u << CL) - 1));
-            }
+            bulk(sW + s * kWHalf, W + static_cast<size_t>(kb) * kWBytes, kWHalf, &full[s]);
         }
-    } else if (warp == 1 && lane == 0) {  // MMA issuer
-        for (int kb = 0; kb < KB; ++kb) {
-            const int s = kb % kStages;
-            bar_wait(&full[s], (kb / kStages) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t a0 = su32(sA + s * kABytes), w0 = su32(sW + s * kWBytes);
+    } else if (warp == 1 && lane == 0) {
+        if (rank == 0) {  // MMA issuer for the pair
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % kStages;
+                bar_wait_cluster(&full[s], (kb / kStages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t a0 = su32(sA + s * kABytes), w0 = su32(sW + s * kWHalf);
 #pragma unroll
-            for (int k = 0; k < kGemmBK / 16; ++k) {
-                const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                for (int k = 0; k < kGemmBK / 16; ++k) {
+                    const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n\t.reg .pred p;\n\t"
+                        "setp.ne.b32 p, %4, 0;\n\t"
+                        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                        "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc2), "r"(acc)
+                        : "memory");
+                }
                 asm volatile(
-                    "{\n\t.reg .pred p;\n\t"
-                    "setp.ne.b32 p, %4, 0;\n\t"
-                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                    "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc), "r"(acc)
-                    : "memory");
-            }
-            if constexpr (CL == 1) {
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                                 su32(&empty[s]))
-                             : "memory");
-            } else {  // stage s of this CTA is free: tell every producer in the cluster
-                asm volatile(
-                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
                     "%1;" ::"r"(su32(&empty[s])),
-                    "h"(static_cast<uint16_t>((1u << CL) - 1))
+                    "h"(static_cast<uint16_t>(3))
                     : "memory");
             }
-        }
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         su32(acc_full))
-                     : "memory");
-    } else if (warp >= 2) {  // epilogue: warp w reads TMEM lanes 32 (w % 4) .. + 31
-        for (int i = threadIdx.x - 64; i < kGemmBN; i += kGemmThreads - 64) {  // stage the tile's biases
-            const int n = blockIdx.y * kGemmBN + i;
-            sbias[i] = (g.bias && n < g.N) ? g.bias[n] : 0.0f;
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
-        bar_wait(acc_full, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
-        const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
-        const int n_out_pad = pad_to(EPI == kEpiOde ? g.n_valid : g.N, kGemmBK);  // tiled output width
-        for (int c = 0; c < kGemmBN; c += 16) {
-            const int n0 = nb * kGemmBN + c;
-            float v[16];
-            ld16(trow + c, v);
-            if (n0 >= (EPI == kEpiF32 ? g.n_valid : n_out_pad)) continue;
-#pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] += sbias[c + i];
-            if (EPI == kEpiTanhTiled) {
-                if (g.addend && m < g.M) {
-                    const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
-                    if (n0 + 16 <= g.N) {  // 4 x 16-B loads of the thread's 64 contiguous bytes
-#pragma unroll
-                        for (int i = 0; i < 16; i += 4) {
-                            const float4 t = *reinterpret_cast<const float4*>(ap + i);
-                            v[i] += t.x;
-                            v[i + 1] += t.y;
-                            v[i + 2] += t.z;
-                            v[i + 3] += t.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (n0 + i < g.N) v[i] += ap[i];
-                    }
-                }
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
-                store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
-            } else if (EPI == kEpiF32) {
-                if (m < g.M) {
-                    float* op = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        v[i] = fmaf(g.scale, v[i], g.offset);
-                        if (g.addend && n0 + i < g.n_valid) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
-                    }
-                    if (n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {
-#pragma unroll
-                        for (int i = 0; i < 16; i += 4)
-                            *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (n0 + i < g.n_valid) op[i] = v[i];
-                    }
-                }
-            } else {  // kEpiOde: a += dt * psi
-                float y[16];
-                float* ap = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
-                if (m < g.M && n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {  // 16-B vector RMW
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        const float4 t = *reinterpret_cast<const float4*>(ap + i);
-                        y[i] = fmaf(g.dt, v[i], t.x);
-                        y[i + 1] = fmaf(g.dt, v[i + 1], t.y);
-                        y[i + 2] = fmaf(g.dt, v[i + 2], t.z);
-                        y[i + 3] = fmaf(g.dt, v[i + 3], t.w);
-                        *reinterpret_cast<float4*>(ap + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        y[i] = 0.0f;
-                        if (m < g.M && n0 + i < g.n_valid) {
-                            y[i] = fmaf(g.dt, v[i], ap[i]);
-                            ap[i] = y[i];
-                        }
-                    }
-                }
-                if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                    su32(acc_full)),
+                "h"(static_cast<uint16_t>(3))
+                : "memory");
+        } else {  // relay: this CTA's stage landed -> arrive on the leader's stage barrier
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % kStages;
+                bar_wait(&full[s], (kb / kStages) & 1);
+                uint32_t remote;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(&full[s])));
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
             }
         }
+    } else if (warp >= 2) {
+        gemm_epilogue<EPI>(g, tmem, sbias, acc_full, mb, nb, warp, lane);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still signal it
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    cluster_sync();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
 __global__ void obs_to_tiled_kernel(const float* obs, int M, int D, int ld, const float* mean, const float* inv_sd,
@@ -335,12 +456,14 @@ namespace {
 template <int EPI>
 cudaError_t prepare_epi(int bytes) {
     cudaError_t e;
+    if ((e = cudaFuncSetAttribute(gemm2_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
     if ((e = cudaFuncSetAttribute(gemm_kernel<EPI, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
     if ((e = cudaFuncSetAttribute(gemm_kernel<EPI, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes))) return e;
     return cudaFuncSetAttribute(gemm_kernel<EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 template <int EPI>
 cudaError_t launch_epi(cudaLaunchConfig_t& cfg, int cl, const GemmArgs& g) {
+    if (cl == -2) return cudaLaunchKernelEx(&cfg, gemm2_kernel<EPI>, g);
     switch (cl) {
         case 4: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 4>, g);
         case 2: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 2>, g);
@@ -373,7 +496,10 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = gemm_smem_bytes();
     cfg.stream = s;
-    const int cl = gemm_cluster(static_cast<int>(cfg.gridDim.x));
+    // MSK_GEMM_2CTA: CTA-pair UMMA (needs an even number of 128-row tiles)
+    static const bool pair = std::getenv("MSK_GEMM_2CTA") != nullptr;
+    const bool use2 = pair && cfg.gridDim.x % 2 == 0;
+    const int cl = use2 ? 2 : gemm_cluster(static_cast<int>(cfg.gridDim.x));
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
@@ -383,10 +509,11 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
     attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
+    const int sel = use2 ? -2 : cl;
     switch (epi) {
-        case kEpiTanhTiled: return launch_epi<kEpiTanhTiled>(cfg, cl, g);
-        case kEpiF32: return launch_epi<kEpiF32>(cfg, cl, g);
-        default: return launch_epi<kEpiOde>(cfg, cl, g);
+        case kEpiTanhTiled: return launch_epi<kEpiTanhTiled>(cfg, sel, g);
+        case kEpiF32: return launch_epi<kEpiF32>(cfg, sel, g);
+        default: return launch_epi<kEpiOde>(cfg, sel, g);
     }
 }
 
