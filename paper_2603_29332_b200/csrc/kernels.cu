@@ -675,6 +675,134 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
     }
 }
 
+// Articulated-body pass, leaves -> root (per link U = IA e0, D, Schur
+// complement, shift to the parent origin; children summed in fixed order).
+__device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int lane) {
+    for (int lev = M.n_levels - 1; lev >= 0; --lev) {
+        const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
+        for (int i = lane; i < n; i += S.G) {
+            const int l = S.tlvl[b + i];
+            const int meta = S.tmeta[l];
+            float* u = S.un + kLinkStride * l;
+            float2* u2 = reinterpret_cast<float2*>(u);
+            float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
+            float P2 = u[8];
+            const int c0 = (meta >> 16) & 0xff, c1 = c0 + ((meta >> 8) & 0xff);
+            for (int c = c0; c < c1; ++c) {
+                const float* uc = S.un + kLinkStride * S.tchild[c];
+                const float2* uc2 = reinterpret_cast<const float2*>(uc);
+                const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
+                r0.x += a0.x;
+                r0.y += a0.y;
+                r1.x += a1.x;
+                r1.y += a1.y;
+                r2.x += a2.x;
+                r2.y += a2.y;
+                r3.x += a3.x;
+                r3.y += a3.y;
+                P2 += uc[8];
+            }
+            const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
+            const float P0 = r3.x, P1 = r3.y;
+            const int dof = link_dof(M, l);
+            if (dof < 0) {  // floating root keeps its full articulated inertia
+                u2[0] = r0;
+                u2[1] = r1;
+                u2[2] = r2;
+                u2[3] = r3;
+                u[8] = P2;
+                continue;
+            }
+            // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
+            const float invD = 1.0f / I00;
+            const float t = S.tau[dof];
+            const float uu = (t - P0) * invD;               // u / D
+            const float U1 = I01 * invD, U2 = I02 * invD;   // U / D
+            const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
+            const float bb = fmaf(-I01, U2, I12);
+            const float cq = fmaf(-I02, U2, I22);
+            const float2 cv = u2[6];
+            // pa = pA + Ia c + U u / D   (pa[0] = tau)
+            const float q1 = fmaf(I01, uu, fmaf(a, cv.x, fmaf(bb, cv.y, P1)));
+            const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
+            u[9] = uu;
+            u2[5] = make_float2(U1, U2);
+            const int p = (meta & 0xff) - 1;
+            if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
+                const float4 kl = S.kin[l], kp = S.kin[p];
+                const float dx = kl.z - kp.z, dz = kl.w - kp.w;
+                const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
+                u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
+                u2[1] = make_float2(be, a);
+                u2[2] = make_float2(bb, cq);
+                u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
+                u[8] = q2;
+            }
+        }
+        __syncwarp(S.hm);
+    }
+
+}
+
+// Floating-root solve (3x3 Cholesky) + articulated-body pass, root -> leaves:
+// q̈ into S.tau.
+__device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, int lane) {
+    if (M.floating && lane == 0) {
+        float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky)
+        const float l00 = sqrtf(u[0]);
+        const float l10 = u[1] / l00, l20 = u[2] / l00;
+        const float l11 = sqrtf(u[3] - l10 * l10);
+        const float l21 = (u[4] - l20 * l10) / l11;
+        const float l22 = sqrtf(u[5] - l20 * l20 - l21 * l21);
+        const float y0 = -u[6] / l00;
+        const float y1 = (-u[7] - l10 * y0) / l11;
+        const float y2 = (-u[8] - l20 * y0 - l21 * y1) / l22;
+        const float x2 = y2 / l22;
+        const float x1 = (y1 - l21 * x2) / l11;
+        const float x0 = (y0 - l10 * x1 - l20 * x2) / l00;
+        u[0] = x0;
+        u[1] = x1;
+        u[2] = x2;
+        // spatial -> coordinate acceleration of the root (x, z, pitch)
+        const float wd = S.dqf[2];
+        S.tau[0] = fmaf(-wd, S.dqf[1], x1);
+        S.tau[1] = fmaf(wd, S.dqf[0], x2);
+        S.tau[2] = x0;
+    }
+    __syncwarp(S.hm);
+    for (int lev = 0; lev < M.n_levels; ++lev) {
+        const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
+        for (int i = lane; i < n; i += S.G) {
+            const int l = S.tlvl[b + i];
+            const int dof = link_dof(M, l);
+            if (dof < 0) continue;
+            float* u = S.un + kLinkStride * l;
+            const int p = (S.tmeta[l] & 0xff) - 1;
+            float2* u2 = reinterpret_cast<float2*>(u);
+            const float2 cv = u2[6];
+            float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
+            if (p >= 0) {
+                const float* up = S.un + kLinkStride * p;
+                const float2 a01 = reinterpret_cast<const float2*>(up)[0];
+                const float a2 = up[2];
+                const float4 kl = S.kin[l], kp = S.kin[p];
+                const float dx = kl.z - kp.z, dz = kl.w - kp.w;
+                A0 = a01.x;
+                A1 += fmaf(-a01.x, dz, a01.y);
+                A2 += fmaf(a01.x, dx, a2);
+            }
+            // q̈ = (u - U^T A) / D with U0 = D
+            const float2 U = u2[5];
+            const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
+            u2[0] = make_float2(A0 + qdd, A1);
+            u[2] = A2;
+            S.tau[dof] = qdd;
+        }
+        __syncwarp(S.hm);
+    }
+
+}
+
 // Loads an env's q, dq (f64) into the DOF-owning lanes.
 template <int QS>
 __device__ __forceinline__ void load_dofs(const DevModel& M, const EnvSmem& S, const double* q, const double* dq,
@@ -727,18 +855,20 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     const float* act_row = actions + static_cast<size_t>(le) * nm;
 
     // Contract checks of Env::step (env.cpp:207-210): env untouched on failure.
+    bool active = true;
     if (St.done[e]) {
         if (lane == 0 && flags) flags[le] = kFlagNotStepped;
-        return;
+        active = false;
     }
-    {
+    if (active) {
         bool bad = false;
         for (int m = lane; m < nm; m += S.G) bad |= !isfinite(act_row[m]);
         if (__any_sync(S.hm, bad)) {
             if (lane == 0 && flags) flags[le] = kFlagBadAction;
-            return;
+            active = false;
         }
     }
+    if (!active) return;
 
     double qd[QS], dqd[QS];
     load_dofs<QS>(M, S, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
@@ -794,129 +924,17 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         __syncwarp(S.hm);
 
         PHASE_MARK(1);
-        // ---- 3. FK + velocities + per-link articulated-body terms ----
-        tree_sweep<true>(M, S, lane, grf_row);
+        {
+            // ---- 3. FK + velocities + per-link articulated-body terms ----
+            tree_sweep<true>(M, S, lane, grf_row);
 
-        PHASE_MARK(2);
-        // ---- 4a. articulated-body pass, leaves -> root ----
-        for (int lev = M.n_levels - 1; lev >= 0; --lev) {
-            const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-            for (int i = lane; i < n; i += S.G) {
-                const int l = S.tlvl[b + i];
-                const int meta = S.tmeta[l];
-                float* u = S.un + kLinkStride * l;
-                float2* u2 = reinterpret_cast<float2*>(u);
-                float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
-                float P2 = u[8];
-                const int c0 = (meta >> 16) & 0xff, c1 = c0 + ((meta >> 8) & 0xff);
-                for (int c = c0; c < c1; ++c) {
-                    const float* uc = S.un + kLinkStride * S.tchild[c];
-                    const float2* uc2 = reinterpret_cast<const float2*>(uc);
-                    const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
-                    r0.x += a0.x;
-                    r0.y += a0.y;
-                    r1.x += a1.x;
-                    r1.y += a1.y;
-                    r2.x += a2.x;
-                    r2.y += a2.y;
-                    r3.x += a3.x;
-                    r3.y += a3.y;
-                    P2 += uc[8];
-                }
-                const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
-                const float P0 = r3.x, P1 = r3.y;
-                const int dof = link_dof(M, l);
-                if (dof < 0) {  // floating root keeps its full articulated inertia
-                    u2[0] = r0;
-                    u2[1] = r1;
-                    u2[2] = r2;
-                    u2[3] = r3;
-                    u[8] = P2;
-                    continue;
-                }
-                // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
-                const float invD = 1.0f / I00;
-                const float t = S.tau[dof];
-                const float uu = (t - P0) * invD;               // u / D
-                const float U1 = I01 * invD, U2 = I02 * invD;   // U / D
-                const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
-                const float bb = fmaf(-I01, U2, I12);
-                const float cq = fmaf(-I02, U2, I22);
-                const float2 cv = u2[6];
-                // pa = pA + Ia c + U u / D   (pa[0] = tau)
-                const float q1 = fmaf(I01, uu, fmaf(a, cv.x, fmaf(bb, cv.y, P1)));
-                const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
-                u[9] = uu;
-                u2[5] = make_float2(U1, U2);
-                const int p = (meta & 0xff) - 1;
-                if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
-                    const float4 kl = S.kin[l], kp = S.kin[p];
-                    const float dx = kl.z - kp.z, dz = kl.w - kp.w;
-                    const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
-                    u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
-                    u2[1] = make_float2(be, a);
-                    u2[2] = make_float2(bb, cq);
-                    u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
-                    u[8] = q2;
-                }
-            }
-            __syncwarp(S.hm);
-        }
+            PHASE_MARK(2);
+            // ---- 4a. articulated-body pass, leaves -> root ----
+            aba_up(M, S, lane);
 
-        PHASE_MARK(3);
-        // ---- 4b. root solve + articulated-body pass, root -> leaves ----
-        if (M.floating && lane == 0) {
-            float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky)
-            const float l00 = sqrtf(u[0]);
-            const float l10 = u[1] / l00, l20 = u[2] / l00;
-            const float l11 = sqrtf(u[3] - l10 * l10);
-            const float l21 = (u[4] - l20 * l10) / l11;
-            const float l22 = sqrtf(u[5] - l20 * l20 - l21 * l21);
-            const float y0 = -u[6] / l00;
-            const float y1 = (-u[7] - l10 * y0) / l11;
-            const float y2 = (-u[8] - l20 * y0 - l21 * y1) / l22;
-            const float x2 = y2 / l22;
-            const float x1 = (y1 - l21 * x2) / l11;
-            const float x0 = (y0 - l10 * x1 - l20 * x2) / l00;
-            u[0] = x0;
-            u[1] = x1;
-            u[2] = x2;
-            // spatial -> coordinate acceleration of the root (x, z, pitch)
-            const float wd = S.dqf[2];
-            S.tau[0] = fmaf(-wd, S.dqf[1], x1);
-            S.tau[1] = fmaf(wd, S.dqf[0], x2);
-            S.tau[2] = x0;
-        }
-        __syncwarp(S.hm);
-        for (int lev = 0; lev < M.n_levels; ++lev) {
-            const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-            for (int i = lane; i < n; i += S.G) {
-                const int l = S.tlvl[b + i];
-                const int dof = link_dof(M, l);
-                if (dof < 0) continue;
-                float* u = S.un + kLinkStride * l;
-                const int p = (S.tmeta[l] & 0xff) - 1;
-                float2* u2 = reinterpret_cast<float2*>(u);
-                const float2 cv = u2[6];
-                float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
-                if (p >= 0) {
-                    const float* up = S.un + kLinkStride * p;
-                    const float2 a01 = reinterpret_cast<const float2*>(up)[0];
-                    const float a2 = up[2];
-                    const float4 kl = S.kin[l], kp = S.kin[p];
-                    const float dx = kl.z - kp.z, dz = kl.w - kp.w;
-                    A0 = a01.x;
-                    A1 += fmaf(-a01.x, dz, a01.y);
-                    A2 += fmaf(a01.x, dx, a2);
-                }
-                // q̈ = (u - U^T A) / D with U0 = D
-                const float2 U = u2[5];
-                const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
-                u2[0] = make_float2(A0 + qdd, A1);
-                u[2] = A2;
-                S.tau[dof] = qdd;
-            }
-            __syncwarp(S.hm);
+            PHASE_MARK(3);
+            // ---- 4b. root solve + articulated-body pass, root -> leaves ----
+            aba_down(M, S, lane);
         }
 
         PHASE_MARK(4);
