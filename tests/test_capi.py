@@ -142,3 +142,30 @@ def test_host_mlp_init_matches_oracle_and_reference_rng():
     assert np.array_equal(big, mlp_init(102, 256, 7))
     assert np.array_equal(big[:512], g["big_head"]) and np.sum(big) == g["big_sum"][0]
     assert np.array_equal(pk.mlp_init(5, 32, 1, final_init_scale=0.0)[-33:], np.zeros(33))
+
+
+def test_new_entry_points_fail_cleanly_without_gpu_or_bad_args():
+    """Policy / rollout / discriminator entry points report errors (no crash) on
+    bad shapes, and on a host without a GPU report a CUDA error instead of
+    falling back to the CPU."""
+    import numpy as np
+
+    import paper_2603_29332_b200 as pk
+
+    L = pk.lib()
+    assert L.msk_mlp_param_count(0, 16, 1) < 0
+    th = np.zeros(4)
+    assert L.msk_mlp_init(th.ctypes.data, 0, 16, 1, 7, 1.0) != 0
+    h = C.c_void_p()
+    # hidden width not a multiple of 64 -> contract error (status 1) before any device work
+    pi = np.zeros(10)
+    rc = L.msk_policy_create(8, 4, 48, pi.ctypes.data, pi.size, 1.0, 0.0, pi.ctypes.data, pi.ctypes.data, pi.size,
+                             20, 0.05, 16, 0, C.byref(h))
+    assert rc == 1 and not h.value
+    assert b"multiple of 64" in L.msk_policy_last_error(None)
+    # wrong parameter count -> contract error
+    rc = L.msk_policy_create(8, 4, 64, pi.ctypes.data, pi.size, 1.0, 0.0, pi.ctypes.data, pi.ctypes.data, pi.size,
+                             20, 0.05, 16, 0, C.byref(h))
+    assert rc == 1 and b"parameter count" in L.msk_policy_last_error(None)
+    r = C.c_void_p()
+    assert L.msk_rollout_create(0, 8, 1, 1, 1, 0, C.byref(r)) != 0 and not r.value
