@@ -321,6 +321,9 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             t += c.nl;
             M.tab_off_lvs = t;
             t += c.n_levels + 1;
+            t = align16(t);
+            M.tab_off_work = t;  // per (level, slot < 32) work words of the tree passes
+            t += 4 * 32 * c.n_levels;
             M.tab_bytes = align16(t);
             std::vector<unsigned char> blob(M.tab_bytes, 0);
             auto put = [&](int at, const void* src, size_t n) { std::memcpy(blob.data() + at, src, n); };
@@ -337,6 +340,23 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
                 blob[M.tab_off_lvl + l] = static_cast<unsigned char>(c.level_links[l]);
             }
             for (int d = 0; d <= c.n_levels; ++d) blob[M.tab_off_lvs + d] = static_cast<unsigned char>(c.level_start[d]);
+            // work word of slot i of level d: link | (parent + 1) << 8 | child_off << 16 |
+            // nchild << 24 | has_sphere << 28 | valid << 31 (one shared load per level)
+            for (int d = 0; d < c.n_levels; ++d) {
+                const int b = c.level_start[d], n = c.level_start[d + 1] - b;
+                if (n > 32) throw ConfigError("model too wide: a tree level has more than 32 links");
+                for (int i = 0; i < n; ++i) {
+                    const int l = c.level_links[b + i];
+                    const int nchild = c.child_start[l + 1] - c.child_start[l];
+                    if (nchild > 15) throw ConfigError("model too wide: a link has more than 15 children");
+                    const int has_sph = c.sphere_start[l + 1] > c.sphere_start[l] ? 1 : 0;
+                    const uint32_t w = static_cast<uint32_t>(l) | (static_cast<uint32_t>(c.link_parent[l] + 1) << 8) |
+                                       (static_cast<uint32_t>(c.child_start[l]) << 16) |
+                                       (static_cast<uint32_t>(nchild) << 24) | (static_cast<uint32_t>(has_sph) << 28) |
+                                       (1u << 31);
+                    put(M.tab_off_work + 4 * (32 * d + i), &w, 4);
+                }
+            }
             M.tab_blob = reinterpret_cast<const int4*>(ctx->upload(blob));
         }
         // as many env slots per block as shared memory allows (28 for the whole-body models)

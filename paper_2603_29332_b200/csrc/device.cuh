@@ -82,7 +82,7 @@ struct DevModel {
     int epb;  // envs per block actually used (<= the compiled warps x envs-per-warp; fewer for big models)
     // block-shared tree table at the head of dynamic smem (bytes)
     const int4* tab_blob;
-    int tab_bytes, tab_off_a, tab_off_in, tab_off_meta, tab_off_child, tab_off_lvl, tab_off_lvs;
+    int tab_bytes, tab_off_a, tab_off_in, tab_off_meta, tab_off_child, tab_off_lvl, tab_off_lvs, tab_off_work;
 };
 
 // Per-env mutable state (device pointers, env-major rows).

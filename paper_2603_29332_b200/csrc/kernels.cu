@@ -67,6 +67,7 @@ struct EnvSmem {
     const uint8_t* tchild; // child lists
     const uint8_t* tlvl;   // links grouped by depth
     const uint8_t* tlvs;   // level starts
+    const uint32_t* twork; // [level][32] work words (see capi.cu): link, parent, children, sphere flag
     int G;                 // lanes per env (32 or 16)
     unsigned hm;           // mask of this env's lanes
 };
@@ -112,8 +113,15 @@ __device__ __forceinline__ EnvSmem carve(unsigned char* smem, int slot, const De
     s.tchild = smem + M.tab_off_child;
     s.tlvl = smem + M.tab_off_lvl;
     s.tlvs = smem + M.tab_off_lvs;
+    s.twork = reinterpret_cast<const uint32_t*>(smem + M.tab_off_work);
     return s;
 }
+
+// Work word fields (capi.cu tree table): valid slots are packed at the front of a level.
+__device__ __forceinline__ int ww_link(uint32_t w) { return static_cast<int>(w & 0xff); }
+__device__ __forceinline__ int ww_parent(uint32_t w) { return static_cast<int>((w >> 8) & 0xff) - 1; }
+__device__ __forceinline__ int ww_child0(uint32_t w) { return static_cast<int>((w >> 16) & 0xff); }
+__device__ __forceinline__ int ww_nchild(uint32_t w) { return static_cast<int>((w >> 24) & 0xf); }
 
 __device__ __forceinline__ int link_dof(const DevModel& M, int l) {
     return l >= M.floating ? M.nrd + l - M.floating : -1;
@@ -275,11 +283,11 @@ __device__ __forceinline__ void publish_dofs(const DevModel& M, const EnvSmem& S
 template <bool kFull>
 __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, int lane, float* grf) {
     for (int lev = 0; lev < M.n_levels; ++lev) {
-        const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-        for (int i = lane; i < n; i += S.G) {
-            const int l = S.tlvl[b + i];
+        for (int i = lane; i < 32; i += S.G) {
+            const uint32_t ww = S.twork[32 * lev + i];
+            if (!(ww >> 31)) break;
+            const int l = ww_link(ww);
             const int dof = link_dof(M, l);
-            const int meta = S.tmeta[l];
             const float4 la = S.ta[l];
             float c, s, ox, oz, w = 0.0f, vx = 0.0f, vz = 0.0f;
             if (dof < 0) {  // floating root: origin (0,0) relative, pitch q2
@@ -293,7 +301,7 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
                     vz = S.dqf[1];
                 }
             } else {
-                const int p = (meta & 0xff) - 1;
+                const int p = ww_parent(ww);
                 const double2 rd = S.relcs[dof];
                 const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
                 if (p >= 0) {
@@ -331,7 +339,7 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
             const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
             const float mg = m * M.gravity;
             float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
-            if (meta >> 24) {  // link carries contact spheres
+            if ((ww >> 28) & 1) {  // link carries contact spheres
                 const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
                 float gx = 0.0f, gz = 0.0f;
                 for (int sp = s0; sp < s1; ++sp) {
@@ -679,15 +687,15 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
 // complement, shift to the parent origin; children summed in fixed order).
 __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int lane) {
     for (int lev = M.n_levels - 1; lev >= 0; --lev) {
-        const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-        for (int i = lane; i < n; i += S.G) {
-            const int l = S.tlvl[b + i];
-            const int meta = S.tmeta[l];
+        for (int i = lane; i < 32; i += S.G) {
+            const uint32_t ww = S.twork[32 * lev + i];
+            if (!(ww >> 31)) break;
+            const int l = ww_link(ww);
             float* u = S.un + kLinkStride * l;
             float2* u2 = reinterpret_cast<float2*>(u);
             float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
             float P2 = u[8];
-            const int c0 = (meta >> 16) & 0xff, c1 = c0 + ((meta >> 8) & 0xff);
+            const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
             for (int c = c0; c < c1; ++c) {
                 const float* uc = S.un + kLinkStride * S.tchild[c];
                 const float2* uc2 = reinterpret_cast<const float2*>(uc);
@@ -727,7 +735,7 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
             const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
             u[9] = uu;
             u2[5] = make_float2(U1, U2);
-            const int p = (meta & 0xff) - 1;
+            const int p = ww_parent(ww);
             if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
                 const float4 kl = S.kin[l], kp = S.kin[p];
                 const float dx = kl.z - kp.z, dz = kl.w - kp.w;
@@ -771,13 +779,14 @@ __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, in
     }
     __syncwarp(S.hm);
     for (int lev = 0; lev < M.n_levels; ++lev) {
-        const int b = S.tlvs[lev], n = S.tlvs[lev + 1] - b;
-        for (int i = lane; i < n; i += S.G) {
-            const int l = S.tlvl[b + i];
+        for (int i = lane; i < 32; i += S.G) {
+            const uint32_t ww = S.twork[32 * lev + i];
+            if (!(ww >> 31)) break;
+            const int l = ww_link(ww);
             const int dof = link_dof(M, l);
             if (dof < 0) continue;
             float* u = S.un + kLinkStride * l;
-            const int p = (S.tmeta[l] & 0xff) - 1;
+            const int p = ww_parent(ww);
             float2* u2 = reinterpret_cast<float2*>(u);
             const float2 cv = u2[6];
             float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
