@@ -242,7 +242,7 @@ def main():
     ap.add_argument("--ref-envs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-groups", type=int, default=2, help="env groups (contexts) in the e2e host-buffer loop")
+    ap.add_argument("--e2e-groups", type=int, default=4, help="env groups (contexts) in the e2e host-buffer loop")
     ap.add_argument("--rollout", action="store_true", help="record every step into the on-device rollout buffer "
                     "and run GAE at each iteration boundary")
     ap.add_argument("--policy-width", type=int, default=0,
@@ -253,6 +253,8 @@ def main():
     args.model = args.model or C["model"]
     args.envs = args.envs or C["envs"]
     args.C = C
+    if C["exchange"]:  # the first iteration boundary (allocations) falls inside the warm-up
+        args.warmup = max(args.warmup, C["exchange"] + 1)
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -394,6 +396,7 @@ def main():
         bufs = []
         for ge in envs_e:
             ge.set_eval_mode(C["eval"])
+            ge.set_host_pipeline(1, 1)  # one chunk per group: the groups themselves pipeline
             if C["disc"]:
                 ge.set_discriminator(pk.mlp_init(ge.delta_dim, C["disc"][0], C["disc"][1]), C["disc"][0])
             ge.reset()

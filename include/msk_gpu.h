@@ -155,6 +155,10 @@ int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, floa
 int msk_gpu_step_host_async(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                             float* reward_host, float* reward_aux_host, uint8_t* flags_host);
 int msk_gpu_host_wait(msk_gpu_ctx* ctx);
+/* Shape of the host-buffer pipeline: env chunks per call and streams (default
+ * 4 x 4, best for one synchronous context; 1 chunk per context is best when a
+ * harness double-buffers several contexts with msk_gpu_step_host_async). */
+int msk_gpu_set_host_pipeline(msk_gpu_ctx* ctx, int32_t chunks, int32_t streams);
 
 int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream);
 int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream);

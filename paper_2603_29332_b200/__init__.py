@@ -228,6 +228,7 @@ def lib():
         L.msk_gpu_step_host_rewarded.argtypes = [_vp] * 7
         L.msk_gpu_step_host_async.argtypes = [_vp] * 7
         L.msk_gpu_host_wait.argtypes = [_vp]
+        L.msk_gpu_set_host_pipeline.argtypes = [_vp, C.c_int32, C.c_int32]
         L.msk_gpu_rollout_stats.argtypes = [_vp] * 5
         L.msk_policy_create.argtypes = [C.c_int32, C.c_int32, C.c_int32, _vp, C.c_int64, C.c_double, C.c_double, _vp,
                                         _vp, C.c_int64, C.c_int32, C.c_double, C.c_int32, C.c_int32, _vp]
@@ -439,6 +440,10 @@ class EnvBatch:
 
     def host_wait(self):
         self._ck(lib().msk_gpu_host_wait(self.h))
+
+    def set_host_pipeline(self, chunks, streams):
+        """Env chunks and streams of the host-buffer pipeline."""
+        self._ck(lib().msk_gpu_set_host_pipeline(self.h, int(chunks), int(streams)))
 
     def observe(self, obs=None, stream=None):
         obs = obs if obs is not None else self._empty(self.n, self.obs_dim)

@@ -83,6 +83,7 @@ struct msk_gpu_ctx {
     // host-buffer path
     cudaStream_t hs[kMaxHostStreams] = {};
     int host_chunks = 4, host_streams = 4;
+    int pipe_chunks = 0, pipe_streams = 0;  // msk_gpu_set_host_pipeline before the first host step
     float* h_actions = nullptr;  // device staging
     float* h_obs = nullptr;
     float* h_delta = nullptr;
@@ -391,6 +392,10 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         S.power_scratch = rw.mode == 2 ? ctx->dalloc<float>(E * c.nm) : nullptr;
         ctx->global_ema = ctx->dalloc<double>(M.bins);
         ctx->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
+        // obs-moment partials for a whole batch, allocated up front (no allocation,
+        // hence no implicit sync, at the first iteration boundary)
+        ctx->mom_cap = static_cast<size_t>(obs_moments_chunks(n_envs)) * ctx->obs_dim * 2;
+        ctx->mom_part = ctx->dalloc<double>(ctx->mom_cap);
         ctx->delta_dim = 3 + c.nj + 2 * c.nk;
 
         launch_seed(S, n_envs, base_seed + static_cast<uint64_t>(global_env_offset), nullptr);
@@ -591,8 +596,9 @@ void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host
     const size_t E = static_cast<size_t>(ctx->n_envs);
     const int nm = ctx->cm.nm;
     if (!ctx->hs[0]) {
-        ctx->host_chunks = host_knob("MSK_HOST_CHUNKS", 4, 1, 64);
-        ctx->host_streams = host_knob("MSK_HOST_STREAMS", 4, 1, kMaxHostStreams);
+        ctx->host_chunks = ctx->pipe_chunks ? ctx->pipe_chunks : host_knob("MSK_HOST_CHUNKS", 4, 1, 64);
+        ctx->host_streams =
+            ctx->pipe_streams ? ctx->pipe_streams : host_knob("MSK_HOST_STREAMS", 4, 1, kMaxHostStreams);
         for (int i = 0; i < ctx->host_streams; ++i)
             ck(cudaStreamCreateWithFlags(&ctx->hs[i], cudaStreamNonBlocking), "stream");
         ctx->h_actions = ctx->dalloc<float>(E * nm);
@@ -663,6 +669,24 @@ int msk_gpu_step_host_async(msk_gpu_ctx* ctx, const float* actions_host, float* 
                             float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
     return guarded(ctx, [&] {
         step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host, false);
+    });
+}
+
+int msk_gpu_set_host_pipeline(msk_gpu_ctx* ctx, int32_t chunks, int32_t streams) {
+    return guarded(ctx, [&] {
+        if (chunks < 1 || chunks > 64 || streams < 1 || streams > kMaxHostStreams)
+            throw ConfigError("set_host_pipeline: chunks in [1, 64], streams in [1, 8]");
+        for (int i = 0; i < ctx->host_streams; ++i)
+            if (ctx->hs[i]) ck(cudaStreamSynchronize(ctx->hs[i]), "set_host_pipeline");
+        if (!ctx->hs[0]) {  // not yet initialised: the first host step creates the streams
+            ctx->pipe_chunks = chunks;
+            ctx->pipe_streams = streams;
+            return;
+        }
+        for (int i = ctx->host_streams; i < streams; ++i)
+            ck(cudaStreamCreateWithFlags(&ctx->hs[i], cudaStreamNonBlocking), "stream");
+        ctx->host_chunks = chunks;
+        ctx->host_streams = std::max(ctx->host_streams, streams);
     });
 }
 
