@@ -332,6 +332,13 @@ def test_host_buffer_step_matches_device_step(assets):
     assert np.array_equal(ho.numpy(), dev["obs"]) and np.array_equal(hf.numpy(), dev["flags"])
     r_dev = to_np(g.discriminator_reward(torch.as_tensor(dev["delta"], device=g.device))) + dev["reward_aux"]
     assert np.abs(hw.numpy() - r_dev).max() <= 1e-6
+    # other pipeline shapes (one chunk / many chunks on 3 streams) give the same step
+    for chunks, streams in ((1, 1), (5, 3)):
+        g.set_state(st)
+        g.set_host_pipeline(chunks, streams)
+        ho.zero_()
+        g.step_host(ha, ho, hd, hr, hf)
+        assert np.array_equal(ho.numpy(), dev["obs"]) and np.array_equal(hf.numpy(), dev["flags"])
     g.close()
 
 
