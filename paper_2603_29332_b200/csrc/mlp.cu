@@ -152,8 +152,13 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
                         if (n0 + i < g.N) v[i] += ap[i];
                 }
             }
+            if (n0 + 16 <= g.N) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+                for (int i = 0; i < 16; ++i) v[i] = tanh_a(v[i]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+            }
             store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
         } else if (EPI == kEpiF32) {
             if (m < g.M) {
@@ -486,8 +491,8 @@ static int gemm_cluster(int mt) {
         const char* v = std::getenv("MSK_GEMM_CLUSTER");
         return v ? std::atoi(v) : 0;
     }();
-    if (forced == 1 || forced == 2 || forced == 4) return mt % forced == 0 ? forced : 1;
-    return mt % 4 == 0 ? 4 : (mt % 2 == 0 ? 2 : 1);
+    if (forced == 2 || forced == 4) return mt % forced == 0 ? forced : 1;
+    return 1;  // measured: weight multicast saves L2 traffic but no time at these sizes
 }
 
 cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
