@@ -123,6 +123,11 @@ __device__ __forceinline__ int ww_parent(uint32_t w) { return static_cast<int>((
 __device__ __forceinline__ int ww_child0(uint32_t w) { return static_cast<int>((w >> 16) & 0xff); }
 __device__ __forceinline__ int ww_nchild(uint32_t w) { return static_cast<int>((w >> 24) & 0xf); }
 
+// Origin (x, z) half of a link's frame record {cos, sin, x, z}: an 8-B load.
+__device__ __forceinline__ float2 frame_origin(const EnvSmem& S, int l) {
+    return reinterpret_cast<const float2*>(S.kin + l)[1];
+}
+
 __device__ __forceinline__ int link_dof(const DevModel& M, int l) {
     return l >= M.floating ? M.nrd + l - M.floating : -1;
 }
@@ -737,8 +742,8 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
             u2[5] = make_float2(U1, U2);
             const int p = ww_parent(ww);
             if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
-                const float4 kl = S.kin[l], kp = S.kin[p];
-                const float dx = kl.z - kp.z, dz = kl.w - kp.w;
+                const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
+                const float dx = ol.x - op.x, dz = ol.y - op.y;
                 const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
                 u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
                 u2[1] = make_float2(be, a);
@@ -794,8 +799,8 @@ __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, in
                 const float* up = S.un + kLinkStride * p;
                 const float2 a01 = reinterpret_cast<const float2*>(up)[0];
                 const float a2 = up[2];
-                const float4 kl = S.kin[l], kp = S.kin[p];
-                const float dx = kl.z - kp.z, dz = kl.w - kp.w;
+                const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
+                const float dx = ol.x - op.x, dz = ol.y - op.y;
                 A0 = a01.x;
                 A1 += fmaf(-a01.x, dz, a01.y);
                 A2 += fmaf(a01.x, dx, a2);
