@@ -552,3 +552,77 @@ def test_full_size_batch_sampled_envs_match_oracle(assets):
         assert np.abs(sg["act"][e] - so["act"][0]).max() <= 1e-5
         assert to_np(out["flags"])[e] == oo["flags"][0]
     g.close()
+
+
+# Muscles whose segments are NOT parent-child: exercises the generic muscle
+# path (world-frame via points, per-joint pairs of skeleton.cpp:147-170) that
+# the generated whole-body models never hit.
+GENERAL_EXTRA = {
+    "walker5_m16": [("bi_l", [[0, [0.10, -0.05]], [2, [0.05, -0.10]]]),           # pelvis -> shank
+                    ("cross", [[1, [0.02, -0.10]], [3, [0.02, -0.10]]]),          # thigh -> thigh
+                    ("tri_r", [[0, [0.08, -0.02]], [3, [0.04, -0.12]], [2, [0.03, -0.05]]])],
+    "arm2_m6": [("tether", [[-1, [0.10, 0.05]], [1, [0.05, -0.02]]]),             # world -> forearm
+                ("span", [[0, [0.02, 0.03]], [-1, [0.30, -0.20]], [1, [0.10, 0.02]]])],
+}
+
+
+def _general_segment_model(tmp_path, name):
+    import json
+
+    from oracle.oracle import OracleModel
+
+    mp, cp = model_paths(name)
+    m = json.load(open(mp))
+    base = dict(m["muscles"][0])
+    extra = GENERAL_EXTRA[name]
+    for name, vias in extra:
+        mu = dict(base, name=name, via_points=vias, f_max=300.0, tendon_slack=0.0)
+        m["muscles"].append(mu)
+    path = tmp_path / f"{name}_general.json"
+    path.write_text(json.dumps(m))
+    # slack so that each new muscle starts near its optimal fibre length at the clip's first frame
+    om = OracleModel(str(path))
+    q0 = np.loadtxt(cp, delimiter=",", skiprows=1, max_rows=1)[1:1 + om.nq]
+    for k in range(len(extra)):
+        i = len(m["muscles"]) - len(extra) + k
+        L = om.mtu_length(q0, i)
+        m["muscles"][i]["tendon_slack"] = max(0.0, L - m["muscles"][i]["l_opt"])
+    path.write_text(json.dumps(m))
+    return str(path), cp
+
+
+@pytest.mark.parametrize("name", sorted(GENERAL_EXTRA))
+def test_general_segments_parity(assets, tmp_path, name):
+    import torch
+
+    mp, cp = _general_segment_model(tmp_path, name)
+    n = 6
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    fmax = o.model.d["m_fmax"]
+    frames = (np.arange(n) * 37 + 5) % (o.frames - 2)
+    for trial in range(3):
+        g.reset_to_frame(frames + trial)
+        o.reset_to_frame(frames + trial)
+        torch.cuda.synchronize()
+        s = o.get_state()
+        rng = np.random.default_rng(trial)
+        s["dq"] = s["dq"] + rng.normal(0, 0.3, s["dq"].shape)
+        s["act"] = rng.uniform(0, 1, s["act"].shape)
+        s = f32_state(s)
+        o.set_state(s)
+        g.set_state(s)
+        a = excitations(300 + trial, 0, n, g.nm).astype(np.float32)
+        og, oo = step_both(g, o, a)
+        sg, so = gpu_state(g), o.get_state()
+        for e in range(n):
+            for k in ("q", "dq"):
+                err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
+                _note(name + "_general", k + " (tol 1e-5)", err)
+                assert err <= 1e-5, (trial, e, k, err)
+        _note(name + "_general", "f_m rel f_max (tol 1e-4)", force_err(sg["f_m"], so["f_m"], fmax))
+        assert force_err(sg["f_m"], so["f_m"], fmax) <= 1e-4
+        assert np.abs(og["delta"] - oo["delta"]).max() <= 1e-5
+        assert np.array_equal(og["flags"], oo["flags"])
+    g.close()
