@@ -106,6 +106,16 @@ def test_single_step_parity(assets, name):
         assert np.array_equal(og["flags"], oo["flags"])
         assert np.array_equal(sg["ints"], so["ints"])
         assert np.allclose(sg["t"], so["t"], rtol=0, atol=1e-12)
+        # per-link ground reaction forces (StepInfo::grf_per_link, skeleton.cpp:323-325) and
+        # muscle power (skeleton.cpp:308-309), relative to the batch's scale
+        grf_g = og["contact_force"].reshape(n, -1)
+        grf_o = np.asarray(oo["grf"]).reshape(n, -1)
+        gscale = max(1.0, np.abs(grf_o).max())
+        _note(name, "grf rel (tol 1e-3)", np.abs(grf_g - grf_o).max() / gscale)
+        assert np.abs(grf_g - grf_o).max() <= 1e-3 * gscale
+        pscale = max(1.0, np.abs(oo["power"]).max())
+        _note(name, "muscle power rel (tol 1e-4)", np.abs(og["muscle_power"] - oo["power"]).max() / pscale)
+        assert np.abs(og["muscle_power"] - oo["power"]).max() <= 1e-4 * pscale
     g.close()
 
 
@@ -625,4 +635,67 @@ def test_general_segments_parity(assets, tmp_path, name):
         assert force_err(sg["f_m"], so["f_m"], fmax) <= 1e-4
         assert np.abs(og["delta"] - oo["delta"]).max() <= 1e-5
         assert np.array_equal(og["flags"], oo["flags"])
+    g.close()
+
+
+def _lowest_sphere_bottom(o, model_path, q):
+    """min over contact spheres of (sphere centre z - radius), world frame (oracle FK)."""
+    import ctypes as C
+    import json
+
+    from oracle.oracle import _dp, _ptr, lib
+
+    m = json.load(open(model_path))
+    nl, nj = len(m["links"]), len(m["joints"])
+    org, ang, anc = np.zeros(2 * nl), np.zeros(nl), np.zeros(2 * nj)
+    L = lib()
+    L.om_forward_kinematics.argtypes = [C.c_void_p, _dp, _dp, _dp, _dp]
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    L.om_forward_kinematics(C.addressof(o.model.s), _ptr(q, _dp), _ptr(org, _dp), _ptr(ang, _dp), _ptr(anc, _dp))
+    z = []
+    for sp in m["contacts"]["spheres"]:
+        l, (x, dz), r = sp["link"], sp["offset"], sp["radius"]
+        z.append(org[2 * l + 1] + np.sin(ang[l]) * x + np.cos(ang[l]) * dz - r)
+    return min(z)
+
+
+@pytest.mark.parametrize("name", ["wb700", "walker5_m16"])
+def test_contact_parity(assets, name):
+    """Penalty ground contact active (root lowered so the foot spheres
+    penetrate): contact wrenches in the dynamics and per-link GRF outputs
+    (skeleton.cpp:235-262, 323-325) match the oracle."""
+    import torch
+
+    n = 4
+    mp, cp = model_paths(name)
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    if not o.model.d["n_spheres"]:
+        pytest.skip("model has no contact spheres")
+    g.reset_to_frame(np.arange(n) * 7 + 3)
+    o.reset_to_frame(np.arange(n) * 7 + 3)
+    torch.cuda.synchronize()
+    s = o.get_state()
+    # lower each body so its lowest contact sphere penetrates 1-4 cm (oracle FK)
+    for e in range(n):
+        s["q"][e, 1] -= _lowest_sphere_bottom(o, mp, s["q"][e]) + np.linspace(0.01, 0.04, n)[e]
+    s["dq"][:, 1] -= 0.2
+    s = f32_state(s)
+    o.set_state(s)
+    g.set_state(s)
+    a = excitations(42, 0, n, g.nm).astype(np.float32)
+    og, oo = step_both(g, o, a)
+    grf_o = np.asarray(oo["grf"]).reshape(n, -1)
+    assert np.abs(grf_o).max() > 1.0, "no contact happened"
+    grf_g = og["contact_force"].reshape(n, -1)
+    scale = np.abs(grf_o).max()
+    _note(name, "grf in contact rel (tol 1e-3)", np.abs(grf_g - grf_o).max() / scale)
+    assert np.abs(grf_g - grf_o).max() <= 1e-3 * scale
+    sg, so = gpu_state(g), o.get_state()
+    for e in range(n):
+        for k in ("q", "dq"):
+            err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
+            _note(name, k + " in contact (tol 1e-5)", err)
+            assert err <= 1e-5, (e, k, err)
     g.close()
