@@ -149,6 +149,23 @@ def world_point(origin, angle, link, local):
     return origin[link] + rot(angle[link]) @ np.array(local, dtype=float)
 
 
+def ground_offset(model: Model, q):
+    """Clip-pipeline ground correction (SPEC.md clip pipeline: minimum foot
+    height across the entire sequence): shift the root height so the lowest
+    contact-sphere bottom over the whole clip touches z = 0."""
+    if not model.floating or not model.spheres:
+        return q
+    low = np.inf
+    for row in q:
+        origin, angle, _ = fk(model, row)
+        for sp in model.spheres:
+            p = world_point(origin, angle, sp["link"], sp["offset"])
+            low = min(low, p[1] - sp["radius"])
+    q = q.copy()
+    q[:, 1] -= low
+    return q
+
+
 def key_body_state(model, origin, angle):
     pos, ang = [], []
     for l in model.key_bodies:
@@ -668,7 +685,7 @@ def generate(out_dir, which=None):
         written.append(mp)
         for cname, fn in clips:
             cp = os.path.join(out_dir, f"{name}_{cname}.csv")
-            write_clip(cp, model, fn(model))
+            write_clip(cp, model, ground_offset(model, fn(model)))
             written.append(cp)
     return written
 
