@@ -388,6 +388,7 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
 }
 
 // Key-body COM (absolute) and unreduced frame angle (skeleton.cpp:346-357).
+template <bool kAngle = true>
 __device__ __forceinline__ void key_body(const DevModel& M, const EnvSmem& S, const double* qsm, int k,
                                          double& x, double& z, double& ang) {
     const int l = __ldg(M.key_bodies + k);
@@ -396,7 +397,7 @@ __device__ __forceinline__ void key_body(const DevModel& M, const EnvSmem& S, co
     x = static_cast<double>(fmaf(kl.x, c, kl.z));
     z = static_cast<double>(fmaf(kl.y, c, kl.w));
     double a = 0.0;
-    int cur = l;
+    int cur = kAngle ? l : -1;  // the angle walks the path to the root: only when asked for
     while (cur >= 0) {
         const int dof = link_dof(M, cur);
         if (dof < 0) {
@@ -498,7 +499,7 @@ __device__ bool write_delta(const DevModel& M, const EnvSmem& S, const double* q
     bool far = false;
     for (int k = lane; k < nk; k += S.G) {
         double x, z, a;
-        key_body(M, S, qsm, k, x, z, a);
+        key_body<false>(M, S, qsm, k, x, z, a);
         const double dx = x - M.clip_kp[t * 2 * nk + 2 * k];
         const double dz = z - M.clip_kp[t * 2 * nk + 2 * k + 1];
         if (drow) {
