@@ -247,6 +247,9 @@ def main():
                     "and run GAE at each iteration boundary")
     ap.add_argument("--policy-width", type=int, default=0,
                     help="actions from the on-device flow policy of this hidden width (0: Philox excitations)")
+    ap.add_argument("--disc-train", default="", choices=["", "fp32", "tf32"],
+                    help="train the reward discriminator on the device once per rollout iteration (needs --rollout "
+                         "and a config with D): one Adam step on the iteration's h*E Delta rows, then publish")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     C = dict(CONFIGS[args.config])
@@ -312,6 +315,14 @@ def main():
         ro_a0 = torch.empty(E, env.nm, device=dev)
         ro_lp = torch.zeros(E, device=dev)
         ro_v = torch.zeros(E, device=dev)  # no critic on this path: V = 0
+    trainer = None
+    if args.disc_train:  # SPEC.md:412-421 on the rollout's Δ, lr 3e-5, λ = 10
+        if not (rollout is not None and C["disc"]):
+            raise SystemExit("--disc-train needs --rollout and a config with a discriminator (c4)")
+        width, dseed = C["disc"]
+        trainer = pk.DiscTrainer(env.delta_dim, width, pk.mlp_init(env.delta_dim, width, dseed), lr=3e-5,
+                                 grad_penalty=10.0, max_rows=rollout.h * E, math=1 if args.disc_train == "tf32" else 0)
+        ro_delta = rollout.field(7, env.delta_dim)
 
     def one_step(s, ev=None):
         """One control step of the workload; ev (optional) = [start, actions, step, stats,
@@ -343,6 +354,9 @@ def main():
         if C["exchange"] and (s + 1) % C["exchange"] == 0:  # iteration boundary (h control steps)
             _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state)
             stats.zero_()
+        if trainer is not None and (s + 1) % rollout.h == 0:  # D update on the iteration's Δ, then publish
+            trainer.step(ro_delta)
+            trainer.publish(env)
         if ev:
             ev[4].record(stream)
         env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=obs if policy is not None else None)
@@ -505,6 +519,9 @@ def main():
                        "actions": (f"on-device policy: Gaussian pi0 + 20-step flow ODE, Mlp width {args.policy_width} "
                                    "(tcgen05 GEMMs, CUDA graph)") if args.policy_width else "Philox excitations",
                        "rollout": "on-device buffer + GAE" if args.rollout else None,
+                       **({"disc_train": f"one Adam step per iteration on h*E Delta rows ({args.disc_train} cuBLAS "
+                                         "GEMMs) + device publish, inside the iteration_exchange phase"}
+                          if args.disc_train else {}),
                        "l2": "flushed between timed steps"},
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic,

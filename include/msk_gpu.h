@@ -130,6 +130,35 @@ int msk_mlp_init(double* theta, int32_t in, int32_t hidden, int32_t out, uint64_
 int msk_gpu_clear_discriminator(msk_gpu_ctx* ctx);
 /* reward[i] = r(D(delta_i)) for n rows of delta [n x delta_dim]. */
 int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n, float* reward, void* stream);
+/* ---- discriminator training step (SPEC.md:412-421 train_discriminator) ------
+ * One Adam step (nn.cpp:224-240: β1 0.9, β2 0.999, ε 1e-8; a non-finite
+ * gradient skips the step) on
+ *   loss = -log clamp(D(0)) - mean_i log(1 - clamp(D(Δ_i))) + λ mean_i ||∇_Δ D(Δ_i)||²
+ * (clamp to [1e-4, 1 - 1e-4]; gradient penalty at the sampled Δ),
+ * the gradient from Mlp::backward (nn.cpp:80-129) and
+ * Mlp::gradient_penalty_backward (nn.cpp:131-222).  The learner's absent
+ * train_discriminator (learn.cpp) is the interface replaced.  Master θ
+ * (nn.cpp:16-38 layout) and Adam moments live on the device in f64; GEMMs in
+ * cuBLAS with math 0 = FP32, 1 = TF32 tensor cores.  delta: [rows x ld] f32 device rows (the
+ * rollout's Δ), rows <= max_rows.  loss (device, nullable): {total, logistic,
+ * mean penalty} at the pre-step parameters. */
+typedef struct msk_disc_trainer msk_disc_trainer;
+int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, int64_t n_params, double lr,
+                            double grad_penalty, int32_t max_rows, int32_t math, int32_t device,
+                            msk_disc_trainer** out);
+void msk_disc_trainer_destroy(msk_disc_trainer* t);
+const char* msk_disc_trainer_last_error(const msk_disc_trainer* t);
+int msk_disc_train_step(msk_disc_trainer* t, const float* delta, int32_t rows, int32_t ld, double* loss,
+                        void* stream);
+/* Loss and dloss/dθ (f32, [n_params], device) without the Adam step. */
+int msk_disc_trainer_gradient(msk_disc_trainer* t, const float* delta, int32_t rows, int32_t ld, float* grad,
+                              double* loss, void* stream);
+/* Synchronises; copies θ (f64, host) and the Adam step / skip counts. */
+int msk_disc_trainer_get_params(msk_disc_trainer* t, double* theta, int64_t* adam_steps, int64_t* adam_skipped);
+/* Refreshes ctx's reward discriminator (set earlier with the same shape) from
+ * the trainer's θ on the device, stream-ordered (no host round trip). */
+int msk_disc_trainer_publish(msk_disc_trainer* t, msk_gpu_ctx* ctx, void* stream);
+
 /* Env::step(action, fn) with fn = the discriminator reward: msk_gpu_step plus
  * reward [E] = r(D(delta)) + reward_aux for stepped envs, 0 for diverged ones
  * (StepResult::reward stays 0, env.cpp:267-268), untouched for envs flagged

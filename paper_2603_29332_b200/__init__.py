@@ -30,8 +30,9 @@ def mlp_init(n_in, hidden, seed, n_out=1, final_init_scale=1.0):
     if n < 0:
         raise ValueError("bad Mlp shape")
     theta = np.zeros(n)
-    if lib().msk_mlp_init(theta.ctypes.data, n_in, hidden, n_out, C.c_uint64(seed), float(final_init_scale)) != 0:
-        raise MskError(lib().msk_gpu_last_error(None).decode())
+    rc = lib().msk_mlp_init(theta.ctypes.data, n_in, hidden, n_out, C.c_uint64(seed), float(final_init_scale))
+    if rc != 0:
+        raise MskError(rc, lib().msk_gpu_last_error(None).decode())
     return theta
 
 
@@ -59,12 +60,12 @@ class Policy:
                                      ls.ctypes.data, psi.ctypes.data, psi.size, n_ode, dt_ode, max_envs, device,
                                      C.byref(h))
         if rc != 0:
-            raise MskError(lib().msk_policy_last_error(None).decode())
+            raise MskError(rc, lib().msk_policy_last_error(None).decode())
         self.h = h
 
     def _ck(self, rc):
         if rc != 0:
-            raise MskError(lib().msk_policy_last_error(self.h).decode())
+            raise MskError(rc, lib().msk_policy_last_error(self.h).decode())
 
     def set_norm(self, mean, var, count):
         import numpy as np
@@ -106,14 +107,15 @@ class Rollout:
         self.torch = torch
         self.E, self.h = n_envs, horizon
         h = C.c_void_p()
-        if lib().msk_rollout_create(n_envs, horizon, obs_dim, act_dim, delta_dim, device, C.byref(h)) != 0:
-            raise MskError(lib().msk_rollout_last_error(None).decode())
+        rc = lib().msk_rollout_create(n_envs, horizon, obs_dim, act_dim, delta_dim, device, C.byref(h))
+        if rc != 0:
+            raise MskError(rc, lib().msk_rollout_last_error(None).decode())
         self.h_ = h
         self.device = torch.device("cuda", device)
 
     def _ck(self, rc):
         if rc != 0:
-            raise MskError(lib().msk_rollout_last_error(self.h_).decode())
+            raise MskError(rc, lib().msk_rollout_last_error(self.h_).decode())
 
     def record(self, t, obs=None, a0=None, actions=None, logprob=None, reward=None, flags=None, value=None,
                delta=None, stream=None):
@@ -131,6 +133,15 @@ class Rollout:
                                        int(bool(normalize)), _p(adv), _p(ret), s))
         return adv, ret
 
+    def field(self, index, cols, dtype=None):
+        """Device tensor view [h * E x cols] of a stored field (msk_rollout_field:
+        0 obs, 1 a0, 2 actions, 3 logprob, 4 reward, 5 done, 6 value, 7 delta)."""
+        torch = self.torch
+        dtype = dtype or torch.float32
+        ptr = lib().msk_rollout_field(self.h_, int(index))
+        n = self.h * self.E * cols
+        return _wrap_device(ptr, n, dtype, self.device).view(self.h * self.E, cols)
+
     def close(self):
         if getattr(self, "h_", None):
             lib().msk_rollout_destroy(self.h_)
@@ -141,6 +152,88 @@ class Rollout:
             self.close()
         except Exception:
             pass
+
+
+class DiscTrainer:
+    """Discriminator training step on the device (msk_disc_trainer_*; SPEC.md:412-421
+    train_discriminator): one Adam step (nn.cpp:224-240) on
+    -log clamp(D(0)) - mean log(1 - clamp(D(Δ))) + λ mean ||∇_Δ D(Δ)||².
+    math: 0 FP32 GEMMs, 1 TF32 tensor-core GEMMs."""
+
+    def __init__(self, n_in, hidden, theta, lr=3e-5, grad_penalty=10.0, max_rows=4096, math=0, device=0):
+        import numpy as np
+        import torch
+
+        self.torch = torch
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        self.n_in, self.hidden, self.n_params = n_in, hidden, len(theta)
+        h = C.c_void_p()
+        rc = lib().msk_disc_trainer_create(n_in, hidden, theta.ctypes.data, len(theta), float(lr),
+                                           float(grad_penalty), int(max_rows), int(math), device, C.byref(h))
+        if rc != 0:
+            raise MskError(rc, lib().msk_disc_trainer_last_error(None).decode())
+        self.h_ = h
+        self.device = torch.device("cuda", device)
+        self.loss = torch.zeros(3, dtype=torch.float64, device=self.device)
+
+    def _ck(self, rc):
+        if rc != 0:
+            raise MskError(rc, lib().msk_disc_trainer_last_error(self.h_).decode())
+
+    def _s(self, stream):
+        return stream.cuda_stream if stream is not None else self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def step(self, delta, stream=None):
+        """One update on delta [rows x ld] (f32, device); returns the device loss
+        tensor {total, logistic, mean penalty} at the pre-step parameters."""
+        self._ck(lib().msk_disc_train_step(self.h_, _p(delta), delta.shape[0], delta.stride(0), _p(self.loss),
+                                           self._s(stream)))
+        return self.loss
+
+    def gradient(self, delta, stream=None):
+        """(grad [n_params] f32, loss [3] f64) at the current parameters, no update."""
+        g = self.torch.empty(self.n_params, dtype=self.torch.float32, device=self.device)
+        self._ck(lib().msk_disc_trainer_gradient(self.h_, _p(delta), delta.shape[0], delta.stride(0), _p(g),
+                                                 _p(self.loss), self._s(stream)))
+        return g, self.loss
+
+    def params(self):
+        """(theta f64 numpy, adam_steps, adam_skipped); synchronises."""
+        import numpy as np
+
+        th = np.zeros(self.n_params)
+        st, sk = C.c_int64(), C.c_int64()
+        self._ck(lib().msk_disc_trainer_get_params(self.h_, th.ctypes.data, C.byref(st), C.byref(sk)))
+        return th, st.value, sk.value
+
+    def publish(self, env, stream=None):
+        """Refresh env's reward discriminator from this trainer's θ on the device."""
+        env._ck(lib().msk_disc_trainer_publish(self.h_, env.h, self._s(stream)))
+
+    def close(self):
+        if getattr(self, "h_", None):
+            lib().msk_disc_trainer_destroy(self.h_)
+            self.h_ = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device(ptr, n, dtype, device):
+    """A torch tensor viewing n elements of library-owned device memory (no copy)."""
+    import torch
+
+    class _Arr:  # __cuda_array_interface__ v3
+        pass
+
+    typestr = {torch.float32: "<f4", torch.uint8: "|u1", torch.float64: "<f8", torch.int32: "<i4"}[dtype]
+    a = _Arr()
+    a.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False), "version": 3,
+                                  "strides": None}
+    return torch.as_tensor(a, device=device)
 
 
 def time_features(t):
@@ -271,6 +364,15 @@ def lib():
         L.msk_gpu_rng_raw.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp]
         L.msk_gpu_fill_excitations.argtypes = [_vp, C.c_uint64, C.c_uint32, _vp, _vp]
         L.msk_gpu_launch_count.restype = C.c_int64
+        L.msk_disc_trainer_create.argtypes = [C.c_int32, C.c_int32, _vp, C.c_int64, C.c_double, C.c_double,
+                                              C.c_int32, C.c_int32, C.c_int32, _vp]
+        L.msk_disc_trainer_destroy.argtypes = [_vp]
+        L.msk_disc_trainer_last_error.restype = C.c_char_p
+        L.msk_disc_trainer_last_error.argtypes = [_vp]
+        L.msk_disc_train_step.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp]
+        L.msk_disc_trainer_gradient.argtypes = [_vp, _vp, C.c_int32, C.c_int32, _vp, _vp, _vp]
+        L.msk_disc_trainer_get_params.argtypes = [_vp, _vp, _vp, _vp]
+        L.msk_disc_trainer_publish.argtypes = [_vp, _vp, _vp]
         L.msk_gpu_launch_count.argtypes = [_vp]
         for name in ("msk_gpu_create", "msk_gpu_dims", "msk_gpu_set_eval_mode", "msk_gpu_reset",
                      "msk_gpu_reset_to_frame", "msk_gpu_step", "msk_gpu_step_host", "msk_gpu_observe",

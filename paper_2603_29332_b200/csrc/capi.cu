@@ -507,7 +507,6 @@ int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_p
         d.w2 = up(h.w2.data(), h.w2.size() * 2);
         d.w3 = up(h.w3.data(), h.w3.size() * 2);
         d.bias = static_cast<const float*>(up(h.bias.data(), h.bias.size() * 4));
-        d.b4 = h.b4;
         ck(prepare_disc(d), "cudaFuncSetAttribute(disc)");
         ctx->disc = d;
         if (!ctx->r_delta) {
@@ -552,6 +551,19 @@ int msk_gpu_clear_discriminator(msk_gpu_ctx* ctx) {
         for (void* p : ctx->disc_allocs) cudaFree(p);
         ctx->disc_allocs.clear();
         ctx->disc = DiscDev{};
+    });
+}
+
+int msk_disc_trainer_publish(msk_disc_trainer* trainer, msk_gpu_ctx* ctx, void* stream) {
+    return guarded(ctx, [&] {
+        if (!trainer) throw ConfigError("disc_trainer_publish: trainer is null");
+        int din = 0, hidden = 0;
+        const double* theta = disc_trainer_theta(trainer, &din, &hidden);
+        if (!ctx->disc.w1) throw ConfigError("disc_trainer_publish: set a discriminator of the same shape first");
+        if (din != ctx->disc.din || hidden != ctx->disc.hidden)
+            throw ConfigError("disc_trainer_publish: trainer shape differs from the context's discriminator");
+        ck(launch_disc_repack(theta, ctx->disc, as_stream(stream)), "disc repack");
+        ctx->count();
     });
 }
 

@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) z = fmaf(tanh_fast(v[i] + sb[2 * H + c + i]), sb[3 * H + c + i], z);
     }
-    z += P.b4;
+    z += __ldg(P.bias + 4 * H);  // b4
     const int row = row0 + r;
     if (row < n) {
         float d = 1.0f / (1.0f + __expf(-z));
@@ -295,8 +295,8 @@ DiscHost build_disc_images(const double* theta, long long n_params, int din, int
     o += H;
     const double* w4 = theta + o;  // 1 x H
     o += H;
-    h.b4 = static_cast<float>(theta[o]);
-    h.bias.resize(4 * static_cast<size_t>(H));
+    h.bias.resize(4 * static_cast<size_t>(H) + 1);
+    h.bias[4 * static_cast<size_t>(H)] = static_cast<float>(theta[o]);  // b4
     for (int i = 0; i < H; ++i) {
         h.bias[i] = static_cast<float>(b1[i]);
         h.bias[H + i] = static_cast<float>(b2[i]);
@@ -325,6 +325,49 @@ cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, con
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, disc_reward_kernel, P, delta, ld, n, raux, flags, reward);
+}
+
+// Device-side refresh of the images from f64 parameters (same layout as
+// build_disc_images): used when the discriminator is trained on the device.
+__global__ void disc_repack_kernel(const double* __restrict__ theta, int din, int H, int K1, __nv_bfloat16* w1,
+                                   __nv_bfloat16* w2, __nv_bfloat16* w3, float* bias) {
+    const long long o1 = static_cast<long long>(H) * din + H, o2 = o1 + static_cast<long long>(H) * H + H,
+                    o3 = o2 + static_cast<long long>(H) * H + H;
+    const long long n1 = static_cast<long long>(H) * K1, n2 = static_cast<long long>(H) * H;
+    for (long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; t < n1 + 2 * n2 + 4 * H + 1;
+         t += static_cast<long long>(gridDim.x) * blockDim.x) {
+        if (t < n1) {  // W1 (H x din, zero-padded to K1)
+            const int r = static_cast<int>(t % H), k = static_cast<int>(t / H);
+            const double v = k < din ? theta[static_cast<long long>(k) * H + r] : 0.0;
+            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(w1) + img_off(r, k, K1)) =
+                __float2bfloat16_rn(static_cast<float>(v));
+        } else if (t < n1 + 2 * n2) {  // W2, W3 (H x H)
+            const long long u = t - n1;
+            const int which = static_cast<int>(u / n2);
+            const long long e = u % n2;
+            const int r = static_cast<int>(e % H), k = static_cast<int>(e / H);
+            const double v = theta[(which ? o2 : o1) + static_cast<long long>(k) * H + r];
+            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(which ? w3 : w2) + img_off(r, k, H)) =
+                __float2bfloat16_rn(static_cast<float>(v));
+        } else {  // b1 | b2 | b3 | w4 | b4
+            const int i = static_cast<int>(t - n1 - 2 * n2), part = i / H, c = i % H;
+            const long long src = part == 0 ? static_cast<long long>(H) * din + c
+                                  : part == 1 ? o1 + static_cast<long long>(H) * H + c
+                                  : part == 2 ? o2 + static_cast<long long>(H) * H + c
+                                  : part == 3 ? o3 + c
+                                              : o3 + H;
+            bias[i] = static_cast<float>(theta[src]);
+        }
+    }
+}
+
+cudaError_t launch_disc_repack(const double* theta, const DiscDev& P, cudaStream_t s) {
+    disc_repack_kernel<<<296, 256, 0, s>>>(theta, P.din, P.hidden, P.k1,
+                                           static_cast<__nv_bfloat16*>(const_cast<void*>(P.w1)),
+                                           static_cast<__nv_bfloat16*>(const_cast<void*>(P.w2)),
+                                           static_cast<__nv_bfloat16*>(const_cast<void*>(P.w3)),
+                                           const_cast<float*>(P.bias));
+    return cudaGetLastError();
 }
 
 }  // namespace msk_b200

@@ -13,8 +13,7 @@ namespace msk_b200 {
 struct DiscHost {
     int din = 0, hidden = 0, k1 = 0;  // k1 = din rounded up to the MMA K step (16)
     std::vector<uint16_t> w1, w2, w3;  // bf16 K-major core-matrix images (H x k1, H x H, H x H)
-    std::vector<float> bias;           // b1 | b2 | b3 | w4 (4 H floats)
-    float b4 = 0.0f;
+    std::vector<float> bias;           // b1 | b2 | b3 | w4 | b4 (4 H + 1 floats)
 };
 
 // Device view passed to the kernel by value.
@@ -24,8 +23,7 @@ struct DiscDev {
     const void* w1 = nullptr;
     const void* w2 = nullptr;
     const void* w3 = nullptr;
-    const float* bias = nullptr;
-    float b4 = 0.0f;
+    const float* bias = nullptr;  // b1 | b2 | b3 | w4 | b4
 };
 
 DiscHost build_disc_images(const double* theta, long long n_params, int din, int hidden);
@@ -36,4 +34,13 @@ cudaError_t prepare_disc(const DiscDev& P);
 cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, const float* raux,
                         const uint8_t* flags, float* reward, cudaStream_t s, bool pdl);
 
+// Rewrites P's images in place from f64 Mlp parameters on the device (same
+// din / hidden), e.g. after a device training step (disc_train.cu).
+cudaError_t launch_disc_repack(const double* theta, const DiscDev& P, cudaStream_t s);
+
 }  // namespace msk_b200
+
+struct msk_disc_trainer;
+namespace msk_b200 {
+const double* disc_trainer_theta(const msk_disc_trainer* t, int* din, int* hidden);
+}

@@ -1,0 +1,230 @@
+"""Discriminator training step — oracle pins
+on CPU, device step vs the f64 oracle on the GPU.
+
+Oracle (oracle/disc_train.py) pins: finite-difference gradient checks of the
+loss (rel < 1e-5), the penalty equals ||dD/dΔ||², SPEC.md:419-420's
+examples, the SPEC.md:418 training example, Adam's non-finite skip (nn.cpp:229-232).
+
+Device tolerances (tests marked gpu), gradient norm-wise per parameter block
+(floor 1e-2 of the whole gradient's norm):
+  math 0 (FP32): rel 1e-4; math 1 (TF32): rel 2e-2
+  loss: rel 1e-5 (FP32), 1e-3 (TF32)
+  θ after 3 Adam steps: ||θ_gpu − θ_ref|| ≤ 1e-2 ||θ_ref − θ_0||
+  published reward discriminator: as the bf16 reward path, 3e-3 max(1, |r|)
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle.disc_train import Adam, disc_loss_grad, gradient_penalty_backward, mlp_forward_cache, train_discriminator
+from oracle.oracle import disc_reward, mlp_init
+
+
+def _fd_check(theta, din, H, delta, lam, idx, eps=1e-6):
+    g = disc_loss_grad(theta, din, H, delta, lam)[3]
+    worst = 0.0
+    for i in idx:
+        tp, tm = theta.copy(), theta.copy()
+        tp[i] += eps
+        tm[i] -= eps
+        fd = (disc_loss_grad(tp, din, H, delta, lam)[0] - disc_loss_grad(tm, din, H, delta, lam)[0]) / (2 * eps)
+        worst = max(worst, abs(fd - g[i]) / max(1e-6, abs(fd) + abs(g[i])))
+    return worst
+
+
+@pytest.mark.parametrize("lam", [0.0, 10.0])
+def test_oracle_gradient_matches_finite_differences(lam):
+    din, H = 7, 16
+    theta = mlp_init(din, H, 7)
+    rng = np.random.default_rng(1)
+    delta = rng.normal(0, 0.5, (6, din))
+    idx = rng.choice(len(theta), 60, replace=False)
+    assert _fd_check(theta, din, H, delta, lam, idx) < 1e-5
+
+
+def test_oracle_penalty_is_squared_input_gradient():
+    din, H = 5, 16
+    theta = mlp_init(din, H, 3)
+    x = np.random.default_rng(2).normal(0, 1, (4, din))
+    pen = gradient_penalty_backward(mlp_forward_cache(theta, din, H, x), np.zeros(len(theta)), din, H)
+    eps, gx = 1e-6, np.zeros_like(x)
+    for j in range(din):
+        xp, xm = x.copy(), x.copy()
+        xp[:, j] += eps
+        xm[:, j] -= eps
+        gx[:, j] = (mlp_forward_cache(theta, din, H, xp)["y"][:, 0] - mlp_forward_cache(theta, din, H, xm)["y"][:, 0]) / (2 * eps)
+    assert np.allclose(pen, (gx ** 2).sum(1), rtol=1e-7)
+
+
+def test_oracle_spec_examples():
+    """zero-initialised head -> D = 0.5 everywhere, loss = 2 log 2
+    (penalty 0: the input gradient vanishes with w4 = 0); λ = 0 -> pure logistic terms."""
+    din, H = 9, 32
+    th0 = mlp_init(din, H, 7, final_init_scale=0.0)
+    delta = np.random.default_rng(3).normal(0, 1, (16, din))
+    loss, logistic, pen, _ = disc_loss_grad(th0, din, H, delta, 10.0)
+    assert abs(loss - 2 * np.log(2)) < 1e-14 and pen == 0.0
+    th = mlp_init(din, H, 7)
+    l0, lg0, p0, _ = disc_loss_grad(th, din, H, delta, 0.0)
+    assert l0 == lg0 and p0 == 0.0
+    l1, lg1, p1, _ = disc_loss_grad(th, din, H, delta, 10.0)
+    assert lg1 == lg0 and abs(l1 - (lg1 + 10.0 * p1)) < 1e-14 and p1 > 0
+
+
+def test_oracle_training_separates_zero_from_large_delta():
+    """after training on a batch with large ||Δ||, D(0) > D(Δ_typical)."""
+    din, H = 6, 16
+    theta = mlp_init(din, H, 11)
+    rng = np.random.default_rng(4)
+    delta = rng.normal(0, 2.0, (64, din))
+    adam = Adam(len(theta), 1e-2)
+    for _ in range(60):
+        train_discriminator(theta, din, H, delta, 10.0, adam)
+    c0 = mlp_forward_cache(theta, din, H, np.zeros((1, din)))["y"][0, 0]
+    cd = mlp_forward_cache(theta, din, H, delta)["y"][:, 0]
+    assert adam.step_count == 60 and c0 > np.median(cd)
+
+
+def test_oracle_adam_skips_non_finite_gradient():
+    th = np.ones(4)
+    a = Adam(4, 0.1)
+    assert not a.step(th, np.array([1.0, np.nan, 0.0, 0.0]))
+    assert a.skipped == 1 and a.step_count == 0 and np.all(th == 1.0)
+    assert a.step(th, np.array([1.0, -1.0, 0.0, 2.0]))
+    # first Adam step moves each parameter by lr * sign(g) (bias-corrected m / sqrt(v))
+    assert np.allclose(th, [0.9, 1.1, 1.0, 0.9], atol=1e-7)
+
+
+def test_trainer_entry_points_fail_cleanly():
+    """Bad shapes -> status 1 before any device work; without a GPU -> status 3, no CPU fallback."""
+    import paper_2603_29332_b200 as pk
+
+    L = pk.lib()
+    h = C.c_void_p()
+    th = np.zeros(10)
+    rc = L.msk_disc_trainer_create(5, 16, th.ctypes.data, th.size, 1e-3, 10.0, 64, 1, 0, C.byref(h))
+    assert rc == 1 and not h.value and b"parameter count" in L.msk_disc_trainer_last_error(None)
+    th = mlp_init(5, 16, 7)
+    rc = L.msk_disc_trainer_create(5, 16, th.ctypes.data, th.size, 1e-3, 10.0, 64, 7, 0, C.byref(h))
+    assert rc == 1 and b"math" in L.msk_disc_trainer_last_error(None)
+    assert L.msk_disc_train_step(None, None, 1, 5, None, None) == 1
+    import torch
+
+    if not torch.cuda.is_available():
+        rc = L.msk_disc_trainer_create(5, 16, th.ctypes.data, th.size, 1e-3, 10.0, 64, 1, 0, C.byref(h))
+        assert rc == 3 and not h.value
+
+
+# ---------------------------------------------------------------- GPU ----
+def _blocks(din, H):
+    o, out = 0, []
+    for r, c in [(H, din), (H, H), (H, H), (1, H)]:
+        out.append((o, o + r * c))
+        out.append((o + r * c, o + r * c + r))
+        o += r * c + r
+    return out
+
+
+def _block_rel(g, ref, din, H):
+    """Worst per-block error relative to max(||block||, 1e-2 ||grad||): the scalar
+    b4 gradient is a cancelling sum (D(Δ) terms vs the D(0) term) of f32 adjoints."""
+    floor = 1e-2 * np.linalg.norm(ref)
+    return max(np.linalg.norm(g[a:b] - ref[a:b]) / max(np.linalg.norm(ref[a:b]), floor) for a, b in _blocks(din, H))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("math,tol_g,tol_l", [(0, 1e-4, 1e-5), (1, 2e-2, 1e-3)])
+@pytest.mark.parametrize("din,H,B", [(9, 16, 37), (102, 256, 1000)])
+def test_device_gradient_matches_oracle(math, tol_g, tol_l, din, H, B):
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    theta = mlp_init(din, H, 7)
+    rng = np.random.default_rng(din + B)
+    delta = (rng.normal(0, 0.3, (B, din))).astype(np.float32)
+    loss, logistic, pen, gref = disc_loss_grad(theta, din, H, delta.astype(np.float64), 10.0)
+    tr = pk.DiscTrainer(din, H, theta, lr=1e-3, grad_penalty=10.0, max_rows=B, math=math)
+    g, lv = tr.gradient(torch.as_tensor(delta, device="cuda"))
+    g, lv = g.cpu().numpy().astype(np.float64), lv.cpu().numpy()
+    assert _block_rel(g, gref, din, H) <= tol_g
+    assert abs(lv[0] - loss) <= tol_l * abs(loss)
+    assert abs(lv[1] - logistic) <= tol_l * abs(logistic)
+    assert abs(lv[2] - pen) <= max(tol_l, 1e-3 if math == 1 else 1e-4) * abs(pen)
+    tr.close()
+
+
+@pytest.mark.gpu
+def test_device_gradient_ragged_rows_and_ld():
+    """A Δ view with a row stride larger than its width (a rollout buffer slice), fewer rows than max_rows."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    din, H, B = 20, 32, 77
+    theta = mlp_init(din, H, 5)
+    full = torch.randn(B, din + 13, device="cuda") * 0.4
+    view = full[:, :din]
+    gref = disc_loss_grad(theta, din, H, view.cpu().double().numpy(), 10.0)[3]
+    tr = pk.DiscTrainer(din, H, theta, max_rows=500, math=0)
+    g, _ = tr.gradient(view)
+    assert _block_rel(g.cpu().double().numpy(), gref, din, H) <= 1e-4
+    tr.close()
+
+
+@pytest.mark.gpu
+def test_device_adam_steps_match_oracle_and_publish():
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from conftest import ensure_assets, model_paths
+
+    ensure_assets()
+    mp, cp = model_paths("wb700")
+    env = pk.EnvBatch(mp, cp, 8)
+    din, H, B, lr = env.delta_dim, 256, 2048, 1e-3
+    theta0 = mlp_init(din, H, 7)
+    rng = np.random.default_rng(9)
+    batches = [(rng.normal(0, 0.2, (B, din))).astype(np.float32) for _ in range(3)]
+    th_ref, adam = theta0.copy(), Adam(len(theta0), lr)
+    tr = pk.DiscTrainer(din, H, theta0, lr=lr, grad_penalty=10.0, max_rows=B, math=0)
+    for d in batches:
+        l_ref = train_discriminator(th_ref, din, H, d.astype(np.float64), 10.0, adam)[0]
+        lv = tr.step(torch.as_tensor(d, device="cuda")).cpu().numpy()
+        assert abs(lv[0] - l_ref) <= 1e-5 * abs(l_ref)
+    th, steps, skipped = tr.params()
+    assert steps == 3 and skipped == 0
+    assert np.linalg.norm(th - th_ref) <= 1e-2 * np.linalg.norm(th_ref - theta0)
+    # publish into the env's reward discriminator (device repack) == set_discriminator(θ)
+    env.set_discriminator(theta0, H)
+    tr.publish(env)
+    dx = torch.as_tensor(batches[0][:64], device="cuda")
+    r = env.discriminator_reward(dx).cpu().numpy()
+    ref = disc_reward(th, din, H, batches[0][:64].astype(np.float64))
+    assert np.max(np.abs(r - ref) / np.maximum(1.0, np.abs(ref))) <= 3e-3
+    env.set_discriminator(th, H)
+    r2 = env.discriminator_reward(dx).cpu().numpy()
+    assert np.array_equal(r, r2)
+    tr.close()
+    env.close()
+
+
+@pytest.mark.gpu
+def test_device_non_finite_delta_skips_the_update():
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    din, H = 9, 16
+    theta = mlp_init(din, H, 7)
+    tr = pk.DiscTrainer(din, H, theta, max_rows=16)
+    d = torch.zeros(16, din, device="cuda")
+    d[3, 2] = float("nan")
+    tr.step(d)
+    th, steps, skipped = tr.params()
+    assert steps == 0 and skipped == 1 and np.array_equal(th, theta)
+    tr.step(torch.zeros(16, din, device="cuda"))
+    th, steps, skipped = tr.params()
+    assert steps == 1 and skipped == 1 and not np.array_equal(th, theta)
+    tr.close()
