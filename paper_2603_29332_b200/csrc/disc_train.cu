@@ -43,21 +43,33 @@
 namespace {
 
 constexpr double kClampLo = 1e-4, kClampHi = 1.0 - 1e-4;
+// Column-wise elementwise kernels: grid (row blocks, columns), 256 threads,
+// 4 rows per thread (coalesced along the column-major rows, 4 loads in flight).
+constexpr int kRowsPerThread = 4, kRowsPerBlock = 256 * kRowsPerThread;
 
-// X2 bottom half: primal input rows (Δ, then one zero row).
+// X2 bottom half: primal input rows (Δ, then one zero row) — a 32 x 32 tile
+// transpose through shared memory (row-major Δ in, column-major X out).
 __global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld, int din, int R, float* X2) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    const int j = blockIdx.y;
-    if (i >= R) return;
-    X2[static_cast<size_t>(j) * 2 * R + R + i] = i < B ? delta[static_cast<size_t>(i) * ld + j] : 0.0f;
+    __shared__ float tile[32][33];
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int i = i0 + r, j = j0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < B && j < din) ? delta[static_cast<size_t>(i) * ld + j] : 0.0f;
+    }
+    __syncthreads();
+    for (int c = threadIdx.y; c < 32; c += 8) {
+        const int j = j0 + c, i = i0 + threadIdx.x;
+        if (j < din && i < R) X2[static_cast<size_t>(j) * 2 * R + R + i] = tile[threadIdx.x][c];
+    }
 }
 
 // x = tanh(x + b[col]) over a column-major block (rows x cols, leading dim ld).
 __global__ void bias_tanh_kernel(float* x, int rows, int cols, int ld, const float* __restrict__ b) {
-    const size_t n = static_cast<size_t>(rows) * cols;
-    for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
-         t += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(t % rows), j = static_cast<int>(t / rows);
+    const int j = blockIdx.y;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
+        if (i >= rows) break;
         float* p = x + static_cast<size_t>(j) * ld + i;
         *p = tanhf(*p + b[j]);
     }
@@ -88,10 +100,11 @@ __global__ void head_kernel(const float* __restrict__ z4, const float* __restric
 // d3 = (d4 ⊗ w4) ∘ (1 - H3²)   (nn.cpp:161)
 __global__ void d3_kernel(const float* __restrict__ d4, const float* __restrict__ w4, const float* __restrict__ H3,
                           int ldh, int R, int H, float* d3) {
-    const size_t n = static_cast<size_t>(R) * H;
-    for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
-         t += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(t % R), j = static_cast<int>(t / R);
+    const int j = blockIdx.y;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
+        if (i >= R) break;
         const float h = H3[static_cast<size_t>(j) * ldh + i];
         d3[static_cast<size_t>(j) * R + i] = d4[i] * w4[j] * (1.0f - h * h);
     }
@@ -100,10 +113,11 @@ __global__ void d3_kernel(const float* __restrict__ d4, const float* __restrict_
 // out = x ∘ (1 - H²), x and out [R x H] (ld lx / lo), H read with leading dim ldh.
 __global__ void gate_kernel(const float* x, int lx, const float* __restrict__ Hm, int ldh, int R, int H, float* out,
                             int lo) {
-    const size_t n = static_cast<size_t>(R) * H;
-    for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
-         t += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(t % R), j = static_cast<int>(t / R);
+    const int j = blockIdx.y;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
+        if (i >= R) break;
         const float h = Hm[static_cast<size_t>(j) * ldh + i];
         out[static_cast<size_t>(j) * lo + i] = x[static_cast<size_t>(j) * lx + i] * (1.0f - h * h);
     }
@@ -129,11 +143,12 @@ __global__ void head2_kernel(const float* __restrict__ d4, const float* __restri
 template <bool OUTER>
 __global__ void rev_elem_kernel(float* S, const float* __restrict__ V, const float* __restrict__ w4,
                                 const float* __restrict__ Hm, int ldh, const float* __restrict__ Z, int R, int H) {
-    const size_t n = static_cast<size_t>(R) * H;
     const size_t ld = 2 * static_cast<size_t>(R);
-    for (size_t t = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; t < n;
-         t += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(t % R), j = static_cast<int>(t / R);
+    const int j = blockIdx.y;
+#pragma unroll
+    for (int k = 0; k < kRowsPerThread; ++k) {
+        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
+        if (i >= R) break;
         float bu, bh;
         if constexpr (OUTER) {
             bu = V[i] * w4[j];
@@ -312,8 +327,8 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     float *gW0 = g, *gb0 = g + static_cast<long long>(H) * din, *gW1 = g + t->o1,
           *gb1 = g + t->o1 + static_cast<long long>(H) * H, *gW2 = g + t->o2,
           *gb2 = g + t->o2 + static_cast<long long>(H) * H, *gw4 = g + t->o3, *gb3 = g + t->o3 + H;
-    const size_t RH = static_cast<size_t>(R) * H;
     const int gR = (R + 255) / 256;
+    const dim3 eg((R + kRowsPerBlock - 1) / kRowsPerBlock, H);
     float *Xb = t->X2 + R, *Xt = t->X2;  // primal / tangent halves
     float* Ab[4];
     float* At[4];
@@ -323,31 +338,31 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     }
 
     // ---- forward (nn.cpp:54-73) ----
-    pack_input_kernel<<<dim3(gR, din), 256, 0, s>>>(delta, B, ld, din, R, t->X2);
+    pack_input_kernel<<<dim3((R + 31) / 32, (din + 31) / 32), dim3(32, 8), 0, s>>>(delta, B, ld, din, R, t->X2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, din, Xb, R2, W0, H, Ab[1], R2);
-    bias_tanh_kernel<<<grid_for(RH), 256, 0, s>>>(Ab[1], R, H, R2, b0);
+    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[1], R, H, R2, b0);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, Ab[1], R2, W1, H, Ab[2], R2);
-    bias_tanh_kernel<<<grid_for(RH), 256, 0, s>>>(Ab[2], R, H, R2, b1);
+    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[2], R, H, R2, b1);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, Ab[2], R2, W2, H, Ab[3], R2);
-    bias_tanh_kernel<<<grid_for(RH), 256, 0, s>>>(Ab[3], R, H, R2, b2);
+    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[3], R, H, R2, b2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, 1, H, Ab[3], R2, w4, 1, t->z4, R);
     head_kernel<<<gR, 256, 0, s>>>(t->z4, b3, B, R, t->d4, t->dd4, t->dz4, t->lrow);
 
     // ---- input gradient g = dy/dx (nn.cpp:161-164) ----
-    d3_kernel<<<grid_for(RH), 256, 0, s>>>(t->d4, w4, Ab[3], R2, R, H, t->T1);
+    d3_kernel<<<eg, 256, 0, s>>>(t->d4, w4, Ab[3], R2, R, H, t->T1);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, R, H, H, t->T1, R, W2, H, t->T2, R);
-    gate_kernel<<<grid_for(RH), 256, 0, s>>>(t->T2, R, Ab[2], R2, R, H, t->T2, R);
+    gate_kernel<<<eg, 256, 0, s>>>(t->T2, R, Ab[2], R2, R, H, t->T2, R);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, R, H, H, t->T2, R, W1, H, t->T1, R);
-    gate_kernel<<<grid_for(RH), 256, 0, s>>>(t->T1, R, Ab[1], R2, R, H, t->T1, R);
+    gate_kernel<<<eg, 256, 0, s>>>(t->T1, R, Ab[1], R2, R, H, t->T1, R);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, R, din, H, t->T1, R, W0, H, Xt, R2);
 
     // ---- forward tangent along g (nn.cpp:167-171) ----
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, din, Xt, R2, W0, H, t->Z[1], R);
-    gate_kernel<<<grid_for(RH), 256, 0, s>>>(t->Z[1], R, Ab[1], R2, R, H, At[1], R2);
+    gate_kernel<<<eg, 256, 0, s>>>(t->Z[1], R, Ab[1], R2, R, H, At[1], R2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, At[1], R2, W1, H, t->Z[2], R);
-    gate_kernel<<<grid_for(RH), 256, 0, s>>>(t->Z[2], R, Ab[2], R2, R, H, At[2], R2);
+    gate_kernel<<<eg, 256, 0, s>>>(t->Z[2], R, Ab[2], R2, R, H, At[2], R2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, At[2], R2, W2, H, t->Z[3], R);
-    gate_kernel<<<grid_for(RH), 256, 0, s>>>(t->Z[3], R, Ab[3], R2, R, H, At[3], R2);
+    gate_kernel<<<eg, 256, 0, s>>>(t->Z[3], R, Ab[3], R2, R, H, At[3], R2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, 1, H, At[3], R2, w4, 1, t->zeta4, R);
     head2_kernel<<<gR, 256, 0, s>>>(t->d4, t->dd4, t->zeta4, t->dz4, B, R, static_cast<float>(t->lam / B), t->V,
                                     t->prow);
@@ -355,17 +370,17 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     // ---- reverse pass over [tangent; primal] (nn.cpp:186-221 + nn.cpp:98-128) ----
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, 1, H, static_cast<int>(R2), t->V, R2, t->A[3], R2, gw4, 1);
     colsum_kernel<<<1, 256, 0, s>>>(t->V + R, R, 0, gb3);
-    rev_elem_kernel<true><<<grid_for(RH), 256, 0, s>>>(t->S1, t->V, w4, Ab[3], R2, t->Z[3], R, H);
+    rev_elem_kernel<true><<<eg, 256, 0, s>>>(t->S1, t->V, w4, Ab[3], R2, t->Z[3], R, H);
     // layer 2
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, H, static_cast<int>(R2), t->S1, R2, t->A[2], R2, gW2, H);
     colsum_kernel<<<H, 256, 0, s>>>(t->S1 + R, R, R2, gb2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(R2), H, H, t->S1, R2, W2, H, t->S2, R2);
-    rev_elem_kernel<false><<<grid_for(RH), 256, 0, s>>>(t->S2, nullptr, nullptr, Ab[2], R2, t->Z[2], R, H);
+    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S2, nullptr, nullptr, Ab[2], R2, t->Z[2], R, H);
     // layer 1
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, H, static_cast<int>(R2), t->S2, R2, t->A[1], R2, gW1, H);
     colsum_kernel<<<H, 256, 0, s>>>(t->S2 + R, R, R2, gb1);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(R2), H, H, t->S2, R2, W1, H, t->S1, R2);
-    rev_elem_kernel<false><<<grid_for(RH), 256, 0, s>>>(t->S1, nullptr, nullptr, Ab[1], R2, t->Z[1], R, H);
+    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S1, nullptr, nullptr, Ab[1], R2, t->Z[1], R, H);
     // layer 0
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, din, static_cast<int>(R2), t->S1, R2, t->X2, R2, gW0, H);
     colsum_kernel<<<H, 256, 0, s>>>(t->S1 + R, R, R2, gb0);
