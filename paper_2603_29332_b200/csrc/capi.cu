@@ -623,8 +623,9 @@ void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host
     const int chunks = static_cast<int>(std::min<size_t>(ctx->host_chunks, E));
     const size_t per = (E + chunks - 1) / chunks;
     for (int c = 0; c < chunks; ++c) {
-        const size_t e0 = c * per, n = std::min(per, E - e0);
-        if (n == 0) break;
+        const size_t e0 = c * per;
+        if (e0 >= E) break;  // ragged E: ceil-sized chunks can run out before `chunks`
+        const size_t n = std::min(per, E - e0);
         cudaStream_t s = ctx->hs[c % ctx->host_streams];
         ck(cudaMemcpyAsync(ctx->h_actions + e0 * nm, actions_host + e0 * nm, n * nm * sizeof(float),
                            cudaMemcpyHostToDevice, s),

@@ -342,8 +342,9 @@ def test_host_buffer_step_matches_device_step(assets):
     assert np.array_equal(ho.numpy(), dev["obs"]) and np.array_equal(hf.numpy(), dev["flags"])
     r_dev = to_np(g.discriminator_reward(torch.as_tensor(dev["delta"], device=g.device))) + dev["reward_aux"]
     assert np.abs(hw.numpy() - r_dev).max() <= 1e-6
-    # other pipeline shapes (one chunk / many chunks on 3 streams) give the same step
-    for chunks, streams in ((1, 1), (5, 3)):
+    # other pipeline shapes (one chunk / many chunks on 3 streams) give the same step;
+    # 12 chunks of ceil(37/12) = 4 envs run out after 10 (ragged tail, no overrun)
+    for chunks, streams in ((1, 1), (5, 3), (12, 4)):
         g.set_state(st)
         g.set_host_pipeline(chunks, streams)
         ho.zero_()
@@ -698,4 +699,99 @@ def test_contact_parity(assets, name):
             err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
             _note(name, k + " in contact (tol 1e-5)", err)
             assert err <= 1e-5, (e, k, err)
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["arm2_m6", "walker5_m16", "wb700"])
+def test_observe_tracking_error_and_force_state_to_reference(assets, name):
+    """Env::observe / tracking_error (env.cpp:129-193) on a stepped state, then
+    Env::force_state_to_reference (env.cpp:123-127): the continuous state becomes
+    make_initial_state at the CURRENT frame (t_index / start / steps / done kept),
+    so the tracking error vanishes — compared with the oracle's
+    reset_to_frame(t_index) for the continuous part."""
+    import torch
+
+    n = _envs(name) + 2
+    mp, cp = model_paths(name)
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    frames = (np.arange(n) * 37 + 5) % (o.frames - 10)
+    g.reset_to_frame(frames)
+    o.reset_to_frame(frames)
+    sync_from_oracle(g, o)
+    for k in range(3):
+        step_both(g, o, excitations(77, k, n, g.nm).astype(np.float32))
+        sync_from_oracle(g, o)  # keep both on the same (f32-rounded) trajectory
+    obs_g, d_g = to_np(g.observe()), to_np(g.tracking_error())
+    obs_o, d_o = o.observe(), o.tracking_error()
+    blocks = obs_block_errors(g, obs_g, obs_o)
+    assert max(v for k, v in blocks.items() if k != "f_m") <= 1e-4, blocks
+    assert np.abs(d_g - d_o).max() <= 1e-5
+    assert np.abs(d_o).max() > 1e-3  # a non-trivial tracking error before the reset
+    ints_before = gpu_state(g)["ints"].copy()
+    g.force_state_to_reference()
+    torch.cuda.synchronize()
+    sg = gpu_state(g)
+    assert np.array_equal(sg["ints"], ints_before)  # t_index, start, steps, done untouched
+    t_index = ints_before[:, 0]
+    o.reset_to_frame(t_index)
+    so = o.get_state()
+    for k in ("q", "dq", "t"):
+        assert np.abs(sg[k] - so[k]).max() <= 1e-12 * max(1.0, np.abs(so[k]).max()), k
+    assert np.abs(sg["act"] - so["act"]).max() <= 1e-7
+    assert force_err(sg["f_m"], so["f_m"], o.model.d["m_fmax"]) <= 1e-4
+    d_g = to_np(g.tracking_error())
+    assert np.abs(o.tracking_error()).max() <= 1e-9
+    assert np.abs(d_g).max() <= 1e-5, np.abs(d_g).max()
+    g.close()
+
+
+@pytest.mark.parametrize("name,n", [("arm2_m6", 5), ("walker5_m16", 29), ("wb700", 31)])
+def test_outputs_stay_inside_caller_buffers(assets, name, n):
+    """Out-of-bounds write check (compute-sanitizer is not available on the GPU
+    pool): every caller-owned output of step / rewarded step / reset / observe /
+    tracking_error / drain is a view into a larger buffer whose guard bytes on both
+    sides must survive, for ragged env counts (not multiples of the block's env
+    slots or of 32)."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from oracle.oracle import mlp_init
+
+    mp, cp = model_paths(name)
+    g = pk.EnvBatch(mp, cp, n, cfg=pk.EnvConfig(episode_horizon=3),
+                    reward=pk.RewardConfig(mode=pk.RewardMode.ImitationPower))
+    g.set_discriminator(mlp_init(g.delta_dim, 32, 7), 32)
+    GUARD = 4096
+    bufs = []
+
+    def guarded(*shape, dtype=torch.float32):
+        numel = int(np.prod(shape))
+        esz = torch.empty((), dtype=dtype).element_size()
+        raw = torch.full(((numel * esz + 2 * GUARD * esz),), 0x5A, dtype=torch.uint8, device="cuda")
+        view = raw[GUARD * esz:GUARD * esz + numel * esz].view(dtype).view(*shape)
+        bufs.append((raw, GUARD * esz, numel * esz))
+        return view
+
+    obs = guarded(n, g.obs_dim)
+    delta = guarded(n, g.delta_dim)
+    raux, rew = guarded(n), guarded(n)
+    flags = guarded(n, dtype=torch.uint8)
+    power = guarded(n, g.nm)
+    grf = guarded(n, g.n_links, 2)
+    starts = guarded(n, dtype=torch.int32)
+    g.reset(obs=obs, start_frames=starts)
+    a = g.fill_excitations(5, 0)
+    for s in range(4):  # horizon 3: episodes end and auto-reset inside the loop
+        g.step(a, obs=obs, delta=delta, reward_aux=raux, flags=flags, muscle_power=power, contact_force=grf,
+               reward=rew)
+        g.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=obs, start_frames=starts)
+    g.observe(obs=obs)
+    g.tracking_error(delta=delta)
+    g.discriminator_reward(delta, reward=rew)
+    torch.cuda.synchronize()
+    for raw, off, nbytes in bufs:
+        head, tail = raw[:off], raw[off + nbytes:]
+        assert bool((head == 0x5A).all()) and bool((tail == 0x5A).all())
     g.close()
