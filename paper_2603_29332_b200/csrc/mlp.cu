@@ -25,7 +25,10 @@ namespace {
 constexpr int kStages = 4;
 constexpr int kABytes = kGemmBM * kGemmBK * 2;  // 16 KB
 constexpr int kWBytes = kGemmBN * kGemmBK * 2;  // 32 KB
-constexpr int kGemmThreads = 192;
+// warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: epilogue (two warps per
+// TMEM lane quarter, each converting one 128-column half of the tile)
+constexpr int kGemmThreads = 320;
+constexpr int kEpiWarps = (kGemmThreads - 64) / 32;
 
 __host__ __device__ constexpr uint32_t blk_off(int r, int k) {  // inside a (rows x 64) block
     return static_cast<uint32_t>(((r >> 3) * 8 + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
@@ -91,6 +94,21 @@ __device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void ld32(uint32_t taddr, float (&v)[2][16]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i >> 4][i & 15] = __uint_as_float(r[i]);
+}
+
 __device__ __forceinline__ float tanh_a(float x) {
     float y;
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -112,8 +130,88 @@ __device__ __forceinline__ void store_tiled16(void* img, int KB, int m, int n0, 
     *reinterpret_cast<uint4*>(base + blk_off(r, k + 8)) = hi;
 }
 
+// Bias / activation / store of 16 consecutive accumulator columns [n0, n0 + 16)
+// of output row m (sb = the tile's staged biases of those columns).
+template <int EPI>
+__device__ __forceinline__ void epi16(const GemmArgs& g, int m, int n0, int n_out_pad, const float* sb,
+                                      float (&v)[16]) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += sb[i];
+    if (EPI == kEpiTanhTiled) {
+        if (g.addend && m < g.M) {
+            const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
+            if (n0 + 16 <= g.N) {  // 4 x 16-B loads of the thread's 64 contiguous bytes
+#pragma unroll
+                for (int i = 0; i < 16; i += 4) {
+                    const float4 t = *reinterpret_cast<const float4*>(ap + i);
+                    v[i] += t.x;
+                    v[i + 1] += t.y;
+                    v[i + 2] += t.z;
+                    v[i + 3] += t.w;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (n0 + i < g.N) v[i] += ap[i];
+            }
+        }
+        if (n0 + 16 <= g.N) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = tanh_a(v[i]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+        }
+        store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
+    } else if (EPI == kEpiF32) {
+        if (m < g.M) {
+            float* op = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                v[i] = fmaf(g.scale, v[i], g.offset);
+                if (g.addend && n0 + i < g.n_valid) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
+            }
+            if (n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (n0 + i < g.n_valid) op[i] = v[i];
+            }
+        }
+    } else {  // kEpiOde: a += dt * psi
+        float y[16];
+        float* ap = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
+        if (m < g.M && n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {  // 16-B vector RMW
+#pragma unroll
+            for (int i = 0; i < 16; i += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(ap + i);
+                y[i] = fmaf(g.dt, v[i], t.x);
+                y[i + 1] = fmaf(g.dt, v[i + 1], t.y);
+                y[i + 2] = fmaf(g.dt, v[i + 2], t.z);
+                y[i + 3] = fmaf(g.dt, v[i + 3], t.w);
+                *reinterpret_cast<float4*>(ap + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                y[i] = 0.0f;
+                if (m < g.M && n0 + i < g.n_valid) {
+                    y[i] = fmaf(g.dt, v[i], ap[i]);
+                    ap[i] = y[i];
+                }
+            }
+        }
+        if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
+    }
+}
+
 // Epilogue of one 128 x 256 output tile (row tile mb, column tile nb) by the
-// four epilogue warps (2-5): warp w reads TMEM lanes 32 (w % 4) .. + 31.
+// eight epilogue warps (2-9): warp w reads TMEM lanes 32 (w % 4) .. + 31 (the
+// hardware's lane-quarter rule) and columns [128 h, 128 h + 128), h = (w - 2) / 4,
+// 32 columns per TMEM load (one wait per load).
 template <int EPI>
 __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, float* sbias, uint64_t* acc_full,
                                               int mb, int nb, int warp, int lane) {
@@ -121,88 +219,21 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
         const int n = nb * kGemmBN + i;
         sbias[i] = (g.bias && n < g.N) ? g.bias[n] : 0.0f;
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");  // epilogue warps only
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // epilogue warps only
     bar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
+    const int c_lo = ((warp - 2) / 4) * (kGemmBN / 2), c_hi = c_lo + kGemmBN / 2;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int n_out_pad = pad_to(EPI == kEpiOde ? g.n_valid : g.N, kGemmBK);  // tiled output width
-    for (int c = 0; c < kGemmBN; c += 16) {
+    const int n_end = EPI == kEpiF32 ? g.n_valid : n_out_pad;
+    for (int c = c_lo; c < c_hi; c += 32) {
         const int n0 = nb * kGemmBN + c;
-        float v[16];
-        ld16(trow + c, v);
-        if (n0 >= (EPI == kEpiF32 ? g.n_valid : n_out_pad)) continue;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] += sbias[c + i];
-        if (EPI == kEpiTanhTiled) {
-            if (g.addend && m < g.M) {
-                const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
-                if (n0 + 16 <= g.N) {  // 4 x 16-B loads of the thread's 64 contiguous bytes
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4) {
-                        const float4 t = *reinterpret_cast<const float4*>(ap + i);
-                        v[i] += t.x;
-                        v[i + 1] += t.y;
-                        v[i + 2] += t.z;
-                        v[i + 3] += t.w;
-                    }
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (n0 + i < g.N) v[i] += ap[i];
-                }
-            }
-            if (n0 + 16 <= g.N) {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = tanh_a(v[i]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
-            }
-            store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
-        } else if (EPI == kEpiF32) {
-            if (m < g.M) {
-                float* op = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    v[i] = fmaf(g.scale, v[i], g.offset);
-                    if (g.addend && n0 + i < g.n_valid) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
-                }
-                if (n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {
-#pragma unroll
-                    for (int i = 0; i < 16; i += 4)
-                        *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (n0 + i < g.n_valid) op[i] = v[i];
-                }
-            }
-        } else {  // kEpiOde: a += dt * psi
-            float y[16];
-            float* ap = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
-            if (m < g.M && n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {  // 16-B vector RMW
-#pragma unroll
-                for (int i = 0; i < 16; i += 4) {
-                    const float4 t = *reinterpret_cast<const float4*>(ap + i);
-                    y[i] = fmaf(g.dt, v[i], t.x);
-                    y[i + 1] = fmaf(g.dt, v[i + 1], t.y);
-                    y[i + 2] = fmaf(g.dt, v[i + 2], t.z);
-                    y[i + 3] = fmaf(g.dt, v[i + 3], t.w);
-                    *reinterpret_cast<float4*>(ap + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    y[i] = 0.0f;
-                    if (m < g.M && n0 + i < g.n_valid) {
-                        y[i] = fmaf(g.dt, v[i], ap[i]);
-                        ap[i] = y[i];
-                    }
-                }
-            }
-            if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
-        }
+        if (n0 >= n_end) break;  // columns past the valid / padded output width
+        float v[2][16];
+        ld32(trow + c, v);
+        epi16<EPI>(g, m, n0, n_out_pad, sbias + c, v[0]);
+        if (n0 + 16 < n_end) epi16<EPI>(g, m, n0 + 16, n_out_pad, sbias + c + 16, v[1]);
     }
 }
 
