@@ -428,9 +428,9 @@ def main():
         def collect(g):  # wait for the group's results (now in host memory), auto-reset done envs
             envs_e[g].host_wait()
             f = bufs[g]["f"]
-            if f.any():
-                envs_e[g].reset(mask=f.to(dev), mask_bits=pk.FLAG_DONE)
-                torch.cuda.synchronize()
+            if f.any():  # the reset runs on torch's stream: wait for it alone (not for the other groups)
+                envs_e[g].reset(mask=f.to(dev, non_blocking=True), mask_bits=pk.FLAG_DONE)
+                torch.cuda.current_stream(dev).synchronize()
 
         for _ in range(2):
             for g in range(groups):
