@@ -497,11 +497,22 @@ def main():
                     "flops_per_env_step": cm["flops_per_env_step"], "peak_source": "measured FFMA probe"}
         except Exception as ex:  # pragma: no cover
             fp32 = {"error": str(ex)}
-        traffic = None
+        traffic, issue = None, None
         tp = os.path.join(ROOT, "profiles", "step_kernel_traffic.json")
-        if os.path.exists(tp):
-            with open(tp) as f:
-                traffic = json.load(f).get("bytes_per_launch")
+        if os.path.exists(tp) and args.config == "c2" and args.model == C["model"] and E == C["envs"]:
+            with open(tp) as f:  # the committed ncu --set full capture of this kernel on this workload
+                prof = json.load(f)
+            traffic = prof.get("bytes_per_launch")
+            met = prof.get("metrics", {})
+            try:  # the binding resource: instruction issue slots (SURVEY §8(d) "FP32-issue bound")
+                inst = float(met["smsp__inst_executed.sum"][0])
+                issue = {"issue_slot_frac": float(met["smsp__issue_active.avg.pct_of_peak_sustained_active"][0]) / 100,
+                         "warp_inst_per_env_substep": inst / (E * 10),
+                         "l1tex_frac": float(met["l1tex__throughput.avg.pct_of_peak_sustained_active"][0]) / 100,
+                         "fma_pipe_frac": float(met["sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"][0])
+                         / 100, "source": "ncu --set full, profiles/step_kernel_traffic.json"}
+            except (KeyError, ValueError):
+                issue = None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
@@ -526,7 +537,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved_gbs / hbm_peak, "traffic": traffic,
                          "bytes_per_env_step": cm["bytes_per_env_step"], "step_kernel_ms": kms,
-                         "note": "path is FP32-issue bound (SURVEY §8(d)); see fp32", "fp32": fp32},
+                         "note": "path is FP32-issue bound (SURVEY §8(d)); see fp32 and issue", "fp32": fp32,
+                         **({"issue": issue} if issue else {})},
             "cpu_baseline": cpu,
             "e2e": e2e,
             **({"disc_kernel": dict(disc, achieved_tflops=disc["flops_per_launch"] / (disc["ms"] * 1e-3) / 1e12,

@@ -390,6 +390,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         S.out_failed = ctx->dalloc<uint8_t>(E * S.out_cap);
         S.out_count = ctx->dalloc<int>(E);
         S.power_scratch = rw.mode == 2 ? ctx->dalloc<float>(E * c.nm) : nullptr;
+        S.reset_list = ctx->dalloc<int>(E + 1);
         ctx->global_ema = ctx->dalloc<double>(M.bins);
         ctx->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
         // obs-moment partials for a whole batch, allocated up front (no allocation,

@@ -1076,11 +1076,14 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
     const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
     const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
-    const int slot = warp * EPW + grp, e = blockIdx.x * M.epb + slot;
-    // masked resets (the per-step auto-reset of done envs) usually select no env
-    // of a block: skip the block before staging the tree table
-    const bool mine = slot < M.epb && e < n_envs && (!mask || (mask[e] & mask_bits));
-    if (!__syncthreads_or(mine)) return;
+    // masked resets (the per-step auto-reset of done envs) run over the compacted
+    // list of selected envs (St.reset_list, see launch_reset), so the selected
+    // envs fill the first blocks and every later block exits at once
+    const int slot = warp * EPW + grp, k = blockIdx.x * M.epb + slot;
+    const int n_sel = mask ? St.reset_list[0] : n_envs;
+    if (blockIdx.x * M.epb >= n_sel) return;
+    const bool mine = slot < M.epb && k < n_sel;
+    const int e = mine ? (mask ? St.reset_list[1 + k] : k) : 0;
     load_tree_table(smem, M);
     if (!mine) return;
     const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
@@ -1162,6 +1165,40 @@ __global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, Dev
 // ============================================================================
 // small per-env kernels
 // ============================================================================
+// list[0] = number of envs e < n with mask[e] & bits, list[1..] = those envs in
+// increasing order (one block: per 1024-env chunk a block-wide prefix count).
+constexpr int kCompactThreads = 1024;
+__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint8_t* mask, uint8_t bits, int n,
+                                                                  int* list) {
+    __shared__ int warp_off[kCompactThreads / 32];
+    __shared__ int base, chunk_tot;
+    if (threadIdx.x == 0) base = 0;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int c0 = 0; c0 < n; c0 += kCompactThreads) {
+        const int e = c0 + threadIdx.x;
+        const bool sel = e < n && (mask[e] & bits);
+        const unsigned b = __ballot_sync(0xffffffffu, sel);
+        if (lane == 0) warp_off[warp] = __popc(b);
+        __syncthreads();
+        if (warp == 0) {  // exclusive scan of the 32 warp counts
+            const int v = warp_off[lane];
+            int x = v;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            warp_off[lane] = x - v;
+            if (lane == 31) chunk_tot = x;
+        }
+        __syncthreads();
+        if (sel) list[1 + base + warp_off[warp] + __popc(b & ((1u << lane) - 1))] = e;
+        __syncthreads();
+        if (threadIdx.x == 0) base += chunk_tot;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) list[0] = base;
+}
+
 __global__ void seed_kernel(DevState St, int n_envs, uint64_t base_seed) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n_envs) return;
@@ -1459,6 +1496,7 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
 
 void launch_reset(const DevModel& M, const DevState& St, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t s) {
+    if (mask) compact_kernel<<<1, kCompactThreads, 0, s>>>(mask, bits, n, St.reset_list);
     const int blocks = (n + M.epb - 1) / M.epb;
     reset_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, mode, mask, bits, frames_in,
                                                                                 obs, frames_out, bad);
