@@ -200,6 +200,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.n_pairs = c.n_pairs;
         M.frames = clip.frames;
         M.n_emg = clip.n_emg;
+        if (ec.adaptive_bins > 1024) throw ConfigError("env: adaptive_bins > 1024 not supported on the device");
         M.bins = std::max(1, ec.adaptive_bins);
         M.gravity = c.gravity;
         M.k_lim = c.k_lim;

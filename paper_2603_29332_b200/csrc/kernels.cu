@@ -1249,8 +1249,9 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(DevModel M, const 
     __shared__ int s_bin[kMergeList];
     __shared__ uint8_t s_fail[kMergeList];
     __shared__ int s_scan[kMergeThreads];
-    const int tid = threadIdx.x;
-    double ema = tid < M.bins ? global_ema[tid] : 0.0;
+    __shared__ double s_ema[kMergeThreads];  // bins <= 1024
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < M.bins) s_ema[tid] = global_ema[tid];
     const double keep = M.decay, gain = __dsub_rn(1.0, M.decay);
     for (long long base = 0; base < n_total; base += kMergeThreads) {
         const long long g = base + tid;
@@ -1273,16 +1274,30 @@ __global__ void __launch_bounds__(kMergeThreads) merge_kernel(DevModel M, const 
                 }
             }
             __syncthreads();
-            if (tid < M.bins) {
-                const int n = min(kMergeList, tot - p0);
-                for (int j = 0; j < n; ++j)
-                    if (s_bin[j] == tid) ema = __dadd_rn(__dmul_rn(keep, ema), __dmul_rn(gain, s_fail[j] ? 1.0 : 0.0));
+            // warp w owns bins w, w + 32, ...: it finds its bin's outcomes 32 list
+            // entries at a time (ballot) and applies them in list order, so each
+            // bin's EMA sees exactly the sequential order of AdaptiveSampler::record
+            const int n = min(kMergeList, tot - p0);
+            for (int b = warp; b < M.bins; b += kMergeThreads / 32) {
+                double ema = s_ema[b];
+                for (int j0 = 0; j0 < n; j0 += 32) {
+                    const int j = j0 + lane;
+                    const bool hit = j < n && s_bin[j] == b;
+                    unsigned mk = __ballot_sync(0xffffffffu, hit);
+                    const unsigned fm = __ballot_sync(0xffffffffu, hit && s_fail[j]);
+                    while (mk) {
+                        const int i = __ffs(mk) - 1;
+                        mk &= mk - 1;
+                        ema = __dadd_rn(__dmul_rn(keep, ema), __dmul_rn(gain, (fm >> i) & 1 ? 1.0 : 0.0));
+                    }
+                }
+                if (lane == 0) s_ema[b] = ema;
             }
             __syncthreads();
         }
         __syncthreads();
     }
-    if (tid < M.bins) global_ema[tid] = ema;
+    if (tid < M.bins) global_ema[tid] = s_ema[tid];
 }
 
 __global__ void broadcast_ema_kernel(DevState St, int n_envs, int bins, const double* row) {
