@@ -362,7 +362,8 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             M.tab_blob = reinterpret_cast<const int4*>(ctx->upload(blob));
         }
         // as many env slots per block as shared memory allows (28 for the whole-body models)
-        const int avail = static_cast<int>(prop.sharedMemPerBlockOptin) - M.tab_bytes;
+        // (minus the reset kernel's static env list, kResetRange ints)
+        const int avail = static_cast<int>(prop.sharedMemPerBlockOptin) - M.tab_bytes - 1088;
         M.epb = std::min(envs_per_block(), avail / std::max(1, M.smem_env_bytes));
         if (M.epb < 1)
             throw ConfigError("model needs " + std::to_string(M.tab_bytes + M.smem_env_bytes) +
@@ -391,7 +392,6 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         S.out_failed = ctx->dalloc<uint8_t>(E * S.out_cap);
         S.out_count = ctx->dalloc<int>(E);
         S.power_scratch = rw.mode == 2 ? ctx->dalloc<float>(E * c.nm) : nullptr;
-        S.reset_list = ctx->dalloc<int>(E + 1);
         ctx->global_ema = ctx->dalloc<double>(M.bins);
         ctx->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
         // obs-moment partials for a whole batch, allocated up front (no allocation,

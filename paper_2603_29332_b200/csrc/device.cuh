@@ -106,7 +106,6 @@ struct DevState {
     int* out_count;   // E
     int out_cap;
     float* power_scratch;  // E x nm (reward mode 2 without a caller buffer)
-    int* reset_list;       // E + 1: [0] count, then the env indices of a masked reset (compacted)
 };
 
 }  // namespace msk_b200

@@ -1067,26 +1067,13 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
 // ============================================================================
 enum ResetMode : int { kResetSample = 0, kResetFrame = 1, kResetForce = 2, kResetInit = 3 };
 
-template <int WPB, int MINB, int EPW>
-__global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevState St, int n_envs, int mode,
-                                                               const uint8_t* mask, uint8_t mask_bits,
-                                                               const int* frames_in, float* obs, int* frames_out,
-                                                               uint8_t* bad) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr int G = 32 / EPW, QS = kMaxQSlots * EPW;
-    const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
-    const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
-    // masked resets (the per-step auto-reset of done envs) run over the compacted
-    // list of selected envs (St.reset_list, see launch_reset), so the selected
-    // envs fill the first blocks and every later block exits at once
-    const int slot = warp * EPW + grp, k = blockIdx.x * M.epb + slot;
-    const int n_sel = mask ? St.reset_list[0] : n_envs;
-    if (blockIdx.x * M.epb >= n_sel) return;
-    const bool mine = slot < M.epb && k < n_sel;
-    const int e = mine ? (mask ? St.reset_list[1 + k] : k) : 0;
-    load_tree_table(smem, M);
-    if (!mine) return;
-    const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
+// Env::reset / reset_to_frame / force_state_to_reference / construction of env e
+// by one warp (env slot S): frame choice, make_initial_state, observe.
+template <int EPW>
+__device__ __forceinline__ void reset_env(const DevModel& M, const DevState& St, const EnvSmem& S, int e, int mode,
+                                          const int* frames_in, float* obs, int* frames_out, uint8_t* bad,
+                                          int lane) {
+    constexpr int QS = kMaxQSlots * EPW;
     const int nq = M.nq;
     int frame = 0;
     if (mode == kResetSample) {
@@ -1096,7 +1083,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
         frame = frames_in[e];
         if (frame < 0 || frame >= M.frames - 1) {  // ContractError in env.cpp:96-97
             if (lane == 0 && bad) bad[e] = 1;
-            return;
+            return;  // (this env only)
         }
         if (lane == 0 && bad) bad[e] = 0;
     } else if (mode == kResetForce) {
@@ -1139,6 +1126,49 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     }
 }
 
+// Each block owns a contiguous range of at most kResetRange envs: it compacts
+// the range's selected envs (mask & mask_bits; all when mask is null) in shared
+// memory and its env slots work through them.  A masked auto-reset that selects
+// a few envs per range thus runs in one wave over <= 148 blocks, instead of
+// scheduling every block of the env grid (one per SM, 28 env slots of smem).
+constexpr int kResetRange = 256;
+
+template <int WPB, int MINB, int EPW>
+__global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevState St, int n_envs, int range,
+                                                               int mode, const uint8_t* mask, uint8_t mask_bits,
+                                                               const int* frames_in, float* obs, int* frames_out,
+                                                               uint8_t* bad) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_list[kResetRange];
+    __shared__ int s_cnt;
+    constexpr int G = 32 / EPW;
+    const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) / G, lane = threadIdx.x & (G - 1);
+    const unsigned hm = EPW == 1 ? 0xffffffffu : (0xffffu << (16 * grp));
+    const int e0 = blockIdx.x * range, n_range = min(range, n_envs - e0);
+    if (threadIdx.x == 0) s_cnt = 0;
+    __syncthreads();
+    {
+        const int t = threadIdx.x, wl = threadIdx.x & 31;
+        const bool sel = t < n_range && (!mask || (mask[e0 + t] & mask_bits));
+        const unsigned b = __ballot_sync(0xffffffffu, sel);
+        int base = 0;
+        if (wl == 0 && b) base = atomicAdd(&s_cnt, __popc(b));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (sel) s_list[base + __popc(b & ((1u << wl) - 1))] = e0 + t;
+    }
+    __syncthreads();
+    const int cnt = s_cnt;
+    if (cnt == 0) return;
+    load_tree_table(smem, M);
+    const int slot = warp * EPW + grp;
+    if (slot >= M.epb) return;
+    const EnvSmem S = carve(smem, slot, M, G, hm);
+    for (int k = slot; k < cnt; k += M.epb) {
+        reset_env<EPW>(M, St, S, s_list[k], mode, frames_in, obs, frames_out, bad, lane);
+        __syncwarp(hm);
+    }
+}
+
 template <int WPB, int MINB, int EPW>
 __global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, DevState St, int n_envs, float* obs,
                                                                  float* delta) {
@@ -1165,40 +1195,6 @@ __global__ void __launch_bounds__(WPB * 32, MINB) observe_kernel(DevModel M, Dev
 // ============================================================================
 // small per-env kernels
 // ============================================================================
-// list[0] = number of envs e < n with mask[e] & bits, list[1..] = those envs in
-// increasing order (one block: per 1024-env chunk a block-wide prefix count).
-constexpr int kCompactThreads = 1024;
-__global__ void __launch_bounds__(kCompactThreads) compact_kernel(const uint8_t* mask, uint8_t bits, int n,
-                                                                  int* list) {
-    __shared__ int warp_off[kCompactThreads / 32];
-    __shared__ int base, chunk_tot;
-    if (threadIdx.x == 0) base = 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int c0 = 0; c0 < n; c0 += kCompactThreads) {
-        const int e = c0 + threadIdx.x;
-        const bool sel = e < n && (mask[e] & bits);
-        const unsigned b = __ballot_sync(0xffffffffu, sel);
-        if (lane == 0) warp_off[warp] = __popc(b);
-        __syncthreads();
-        if (warp == 0) {  // exclusive scan of the 32 warp counts
-            const int v = warp_off[lane];
-            int x = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
-            }
-            warp_off[lane] = x - v;
-            if (lane == 31) chunk_tot = x;
-        }
-        __syncthreads();
-        if (sel) list[1 + base + warp_off[warp] + __popc(b & ((1u << lane) - 1))] = e;
-        __syncthreads();
-        if (threadIdx.x == 0) base += chunk_tot;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) list[0] = base;
-}
-
 __global__ void seed_kernel(DevState St, int n_envs, uint64_t base_seed) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n_envs) return;
@@ -1511,10 +1507,17 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
 
 void launch_reset(const DevModel& M, const DevState& St, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t s) {
-    if (mask) compact_kernel<<<1, kCompactThreads, 0, s>>>(mask, bits, n, St.reset_list);
-    const int blocks = (n + M.epb - 1) / M.epb;
-    reset_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, mode, mask, bits, frames_in,
-                                                                                obs, frames_out, bad);
+    static const int sms = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    // one wave of blocks when the ranges allow it, ranges of <= kResetRange envs
+    const int blocks = std::max(std::min((n + M.epb - 1) / M.epb, sms), (n + kResetRange - 1) / kResetRange);
+    const int range = (n + blocks - 1) / blocks;
+    reset_kernel<kWPB, kMinB, kEPW><<<blocks, kWPB * 32, block_smem(M), s>>>(M, St, n, range, mode, mask, bits,
+                                                                                frames_in, obs, frames_out, bad);
 }
 
 void launch_observe(const DevModel& M, const DevState& St, int n, float* obs, float* delta, cudaStream_t s) {

@@ -9,3 +9,5 @@ CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu_launch.log 2>&1; echo ncu1 rc=$?
 timeout 300 $CMD > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -f -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
 tail -2 gpurun_out/pytest_gpu.log; tail -1 gpurun_out/bench.log; tail -1 gpurun_out/bench_ref.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke rc=$?; tail -4 gpurun_out/smoke.log
+CFGS="c3 c4 c5" bash tools/_gpu_configs.sh > gpurun_out/configs.log 2>&1; echo configs rc=$?
