@@ -795,3 +795,42 @@ def test_outputs_stay_inside_caller_buffers(assets, name, n):
         head, tail = raw[:off], raw[off + nbytes:]
         assert bool((head == 0x5A).all()) and bool((tail == 0x5A).all())
     g.close()
+
+
+def test_reset_ranges_larger_than_the_block(assets):
+    """More envs than one wave of env slots (148 x 28): each reset block owns a
+    range of envs and its env slots loop over the range's selected envs.  RSI
+    start frames (full and masked resets), the reset state and the RNG streams
+    equal the oracle's for every env."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("arm2_m6")
+    n = 9001
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=5, rsi=True, adaptive_bins=7))
+    ema = np.random.default_rng(5).uniform(0, 1, (n, 7))
+    g.set_sampler(torch.as_tensor(ema, device=g.device))
+    o.set_sampler(ema)
+    sf = torch.empty(n, dtype=torch.int32, device=g.device)
+    g.reset(start_frames=sf)
+    _, fo = o.reset()
+    torch.cuda.synchronize()
+    assert np.array_equal(to_np(sf), fo)
+    rng = np.random.default_rng(6)
+    for r in range(3):  # sparse and dense masked resets (the auto-reset path)
+        sel = rng.random(n) < (0.02, 0.5, 0.97)[r]
+        mask = torch.as_tensor(sel.astype(np.uint8) * pk.FLAG_DONE, device=g.device)
+        sf.fill_(-1)
+        g.reset(mask=mask, mask_bits=pk.FLAG_DONE, start_frames=sf)
+        _, fo = o.reset(mask=sel)
+        torch.cuda.synchronize()
+        got = to_np(sf)
+        assert np.array_equal(got[sel], np.asarray(fo)[sel]), r
+        assert np.all(got[~sel] == -1), r  # unselected envs untouched
+    sg, so = gpu_state(g), o.get_state()
+    assert np.array_equal(sg["ints"], so["ints"])
+    assert np.array_equal(sg["q"], so["q"]) and np.array_equal(sg["dq"], so["dq"])
+    for e in (0, 4143, 4144, 9000):
+        assert np.array_equal(to_np(g.rng_raw(e, 8)).view(np.uint64), o.rng_raw(e, 8))
+    g.close()
