@@ -152,4 +152,48 @@ private:
     msk_dims dims_{};
 };
 
+// train_discriminator on the device: one Adam step per call
+// on rows of Δ (e.g. the rollout buffer's), then publish() refreshes the
+// EnvBatch's reward discriminator (same shape) without a host round trip.
+class DiscTrainer {
+public:
+    DiscTrainer(int in, int hidden, const std::vector<double>& theta, double lr, double grad_penalty, int max_rows,
+                bool tf32 = true, int device = 0)
+        : n_(theta.size()) {
+        const int st = msk_disc_trainer_create(in, hidden, theta.data(), static_cast<int64_t>(theta.size()), lr,
+                                               grad_penalty, max_rows, tf32 ? 1 : 0, device, &t_);
+        if (st != MSK_OK) {
+            const std::string msg = msk_disc_trainer_last_error(nullptr);
+            if (st == MSK_ERR_CONTRACT) throw ContractError(msg);
+            throw CudaError(msg);
+        }
+    }
+    ~DiscTrainer() { msk_disc_trainer_destroy(t_); }
+    DiscTrainer(const DiscTrainer&) = delete;
+    DiscTrainer& operator=(const DiscTrainer&) = delete;
+
+    // loss (device, nullable): {total, logistic, mean penalty} before the step
+    void step(const float* delta, int rows, int ld, double* loss = nullptr, void* stream = nullptr) {
+        ck(msk_disc_train_step(t_, delta, rows, ld, loss, stream));
+    }
+    void publish(EnvBatch& env, void* stream = nullptr) {
+        check(msk_disc_trainer_publish(t_, env.handle(), stream), env.handle());
+    }
+    std::vector<double> params(int64_t* adam_steps = nullptr, int64_t* skipped = nullptr) {
+        std::vector<double> th(n_);
+        ck(msk_disc_trainer_get_params(t_, th.data(), adam_steps, skipped));
+        return th;
+    }
+
+private:
+    void ck(int st) {
+        if (st == MSK_OK) return;
+        const std::string msg = msk_disc_trainer_last_error(t_);
+        if (st == MSK_ERR_CONTRACT) throw ContractError(msg);
+        throw CudaError(msg);
+    }
+    size_t n_ = 0;
+    msk_disc_trainer* t_ = nullptr;
+};
+
 }  // namespace msk::gpu

@@ -8,12 +8,15 @@
 //   run:   tools/cpp_demo <model.json> <clip.csv> [envs] [steps] [policy_width]
 // With policy_width > 0 the actions come from the on-device flow policy
 // (msk_policy_*: Gaussian pi0 + 20-step flow ODE on the tensor cores) and every
-// step is recorded into the on-device rollout buffer, with GAE every 8 steps.
+// step is recorded into the on-device rollout buffer; every 8 steps GAE runs and
+// the discriminator takes one training step on the iteration's Δ rows
+// (msk_disc_trainer_*), published into the reward path.
 #include <cuda_runtime.h>
 
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <stdexcept>
 #include <vector>
 
@@ -49,6 +52,8 @@ int main(int argc, char** argv) {
         // optional on-device policy + rollout buffer (C ABI)
         msk_policy* pol = nullptr;
         msk_rollout* ro = nullptr;
+        std::unique_ptr<msk::gpu::DiscTrainer> dtrain;
+        double* dloss = nullptr;
         float *a0 = nullptr, *logp = nullptr, *value = nullptr, *adv = nullptr, *ret = nullptr;
         const int horizon = 8;
         if (width > 0) {
@@ -67,10 +72,12 @@ int main(int argc, char** argv) {
             cudaMemset(value, 0, sizeof(float) * E);
             cudaMalloc(&adv, sizeof(float) * E * horizon);
             cudaMalloc(&ret, sizeof(float) * E * horizon);
+            dtrain = std::make_unique<msk::gpu::DiscTrainer>(
+                env.delta_dim(), 256, msk::gpu::EnvBatch::mlp_init(env.delta_dim(), 256, 1, 7), 3e-5, 10.0,
+                E * horizon);
+            cudaMalloc(&dloss, 3 * sizeof(double));
         }
-        cudaDeviceSynchronize();
-        const auto t0 = std::chrono::steady_clock::now();
-        for (int s = 0; s < steps; ++s) {
+        auto one_step = [&](int s) {
             if (pol) {  // a = flow-refined Gaussian sample from the current observation
                 msk_rollout_record(ro, s % horizon, obs, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                    nullptr);
@@ -83,10 +90,20 @@ int main(int argc, char** argv) {
             env.step(actions, out, reward);  // Env::step(action, fn): reward = r(D(Δ)) + reward_aux
             if (ro) {
                 msk_rollout_record(ro, s % horizon, nullptr, a0, actions, logp, reward, flags, value, delta, nullptr);
-                if ((s + 1) % horizon == 0) msk_rollout_gae(ro, value, 0.99f, 0.95f, 1, adv, ret, nullptr);
+                if ((s + 1) % horizon == 0) {
+                    msk_rollout_gae(ro, value, 0.99f, 0.95f, 1, adv, ret, nullptr);
+                    dtrain->step(static_cast<const float*>(msk_rollout_field(ro, 7)), E * horizon, env.delta_dim(),
+                                 dloss);
+                    dtrain->publish(env);
+                }
             }
             env.reset(flags, MSK_FLAG_DONE, pol ? obs : nullptr);  // batched auto-reset
-        }
+        };
+        // one untimed iteration: graph capture, cuBLAS / module first-use costs
+        for (int s = 0; s < horizon; ++s) one_step(s);
+        cudaDeviceSynchronize();
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int s = horizon; s < horizon + steps; ++s) one_step(s);
         cudaDeviceSynchronize();
         const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         std::vector<float> h(static_cast<size_t>(E) * env.observation_dim());
@@ -97,9 +114,13 @@ int main(int argc, char** argv) {
         cudaMemcpy(hr.data(), reward, sizeof(float) * E, cudaMemcpyDeviceToHost);
         double rsum = 0.0;
         for (float v : hr) rsum += v;
-        std::printf("envs=%d steps=%d policy_width=%d env-steps/s=%.0f obs_checksum=%.6e mean_reward=%.6f\n", E,
-                    steps, width, E * steps / secs, checksum, rsum / E);
+        double lh[3] = {0, 0, 0};
+        if (dloss) cudaMemcpy(lh, dloss, sizeof(lh), cudaMemcpyDeviceToHost);
+        std::printf("envs=%d steps=%d policy_width=%d env-steps/s=%.0f obs_checksum=%.6e mean_reward=%.6f "
+                    "disc_loss=%.6f\n",
+                    E, steps, width, E * steps / secs, checksum, rsum / E, lh[0]);
         cudaFree(reward);
+        if (dloss) cudaFree(dloss);
         if (pol) msk_policy_destroy(pol);
         if (ro) msk_rollout_destroy(ro);
         for (float* p : {a0, logp, value, adv, ret})
