@@ -49,7 +49,7 @@ constexpr int kRowsPerThread = 4, kRowsPerBlock = 256 * kRowsPerThread;
 
 // X2 bottom half: primal input rows (Δ, then one zero row) — a 32 x 32 tile
 // transpose through shared memory (row-major Δ in, column-major X out).
-__global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld, int din, int R, float* X2) {
+__global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld, int din, int R, int Rp, float* X2) {
     __shared__ float tile[32][33];
     const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += 8) {
@@ -59,19 +59,22 @@ __global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld
     __syncthreads();
     for (int c = threadIdx.y; c < 32; c += 8) {
         const int j = j0 + c, i = i0 + threadIdx.x;
-        if (j < din && i < R) X2[static_cast<size_t>(j) * 2 * R + R + i] = tile[threadIdx.x][c];
+        if (j < din && i < Rp) X2[static_cast<size_t>(j) * 2 * Rp + Rp + i] = tile[threadIdx.x][c];
     }
 }
 
-// x = tanh(x + b[col]) over a column-major block (rows x cols, leading dim ld).
-__global__ void bias_tanh_kernel(float* x, int rows, int cols, int ld, const float* __restrict__ b) {
+// The column-wise kernels cover rows [0, Rp) of a half and write 0 to the
+// padding rows [R, Rp), so every GEMM over a padded extent sees zeros there.
+
+// x = tanh(x + b[col]) over a column-major block (leading dim ld).
+__global__ void bias_tanh_kernel(float* x, int R, int Rp, int ld, const float* __restrict__ b) {
     const int j = blockIdx.y;
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; ++k) {
         const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= rows) break;
+        if (i >= Rp) break;
         float* p = x + static_cast<size_t>(j) * ld + i;
-        *p = tanhf(*p + b[j]);
+        *p = i < R ? tanhf(*p + b[j]) : 0.0f;
     }
 }
 
@@ -99,40 +102,44 @@ __global__ void head_kernel(const float* __restrict__ z4, const float* __restric
 
 // d3 = (d4 ⊗ w4) ∘ (1 - H3²)   (nn.cpp:161)
 __global__ void d3_kernel(const float* __restrict__ d4, const float* __restrict__ w4, const float* __restrict__ H3,
-                          int ldh, int R, int H, float* d3) {
+                          int ldh, int R, int Rp, float* d3, int ldd) {
     const int j = blockIdx.y;
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; ++k) {
         const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= R) break;
+        if (i >= Rp) break;
         const float h = H3[static_cast<size_t>(j) * ldh + i];
-        d3[static_cast<size_t>(j) * R + i] = d4[i] * w4[j] * (1.0f - h * h);
+        d3[static_cast<size_t>(j) * ldd + i] = i < R ? d4[i] * w4[j] * (1.0f - h * h) : 0.0f;
     }
 }
 
 // out = x ∘ (1 - H²), x and out [R x H] (ld lx / lo), H read with leading dim ldh.
-__global__ void gate_kernel(const float* x, int lx, const float* __restrict__ Hm, int ldh, int R, int H, float* out,
+__global__ void gate_kernel(const float* x, int lx, const float* __restrict__ Hm, int ldh, int R, int Rp, float* out,
                             int lo) {
     const int j = blockIdx.y;
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; ++k) {
         const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= R) break;
+        if (i >= Rp) break;
         const float h = Hm[static_cast<size_t>(j) * ldh + i];
-        out[static_cast<size_t>(j) * lo + i] = x[static_cast<size_t>(j) * lx + i] * (1.0f - h * h);
+        out[static_cast<size_t>(j) * lo + i] = i < R ? x[static_cast<size_t>(j) * lx + i] * (1.0f - h * h) : 0.0f;
     }
 }
 
 // Penalty + head adjoints (nn.cpp:172, 187-188 with the logistic dz4 added to b_z4):
-// V[i] = b_ζ4 = 2 w d4, V[R + i] = b_z4 = 2 w dd4 ζ4 + dz4, w = λ/B on Δ rows, 0 on the zero row.
+// V[i] = b_ζ4 = 2 w d4, V[Rp + i] = b_z4 = 2 w dd4 ζ4 + dz4, w = λ/B on Δ rows, 0 on the zero row.
 __global__ void head2_kernel(const float* __restrict__ d4, const float* __restrict__ dd4,
-                             const float* __restrict__ zeta4, const float* __restrict__ dz4, int B, int R, float lamB,
-                             float* V, double* prow) {
+                             const float* __restrict__ zeta4, const float* __restrict__ dz4, int B, int R, int Rp,
+                             float lamB, float* V, double* prow) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= R) return;
+    if (i >= Rp) return;
+    if (i >= R) {
+        V[i] = V[Rp + i] = 0.0f;
+        return;
+    }
     const float w = i < B ? lamB : 0.0f;
     V[i] = 2.0f * w * d4[i];
-    V[R + i] = 2.0f * w * dd4[i] * zeta4[i] + dz4[i];
+    V[Rp + i] = 2.0f * w * dd4[i] * zeta4[i] + dz4[i];
     prow[i] = i < B ? static_cast<double>(d4[i]) * zeta4[i] / B : 0.0;
 }
 
@@ -142,27 +149,32 @@ __global__ void head2_kernel(const float* __restrict__ d4, const float* __restri
 //   b_ζ = G ∘ b_u,  b_h += -2 H ∘ ζ ∘ b_u,  b_z = G ∘ b_h   (G = 1 - H²)
 template <bool OUTER>
 __global__ void rev_elem_kernel(float* S, const float* __restrict__ V, const float* __restrict__ w4,
-                                const float* __restrict__ Hm, int ldh, const float* __restrict__ Z, int R, int H) {
-    const size_t ld = 2 * static_cast<size_t>(R);
+                                const float* __restrict__ Hm, int ldh, const float* __restrict__ Z, int R, int Rp,
+                                int H) {
+    const size_t ld = 2 * static_cast<size_t>(Rp);
     const int j = blockIdx.y;
 #pragma unroll
     for (int k = 0; k < kRowsPerThread; ++k) {
         const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= R) break;
+        if (i >= Rp) break;
+        if (i >= R) {
+            S[j * ld + i] = S[j * ld + Rp + i] = 0.0f;
+            continue;
+        }
         float bu, bh;
         if constexpr (OUTER) {
             bu = V[i] * w4[j];
-            bh = V[R + i] * w4[j];
+            bh = V[Rp + i] * w4[j];
         } else {
             bu = S[j * ld + i];
-            bh = S[j * ld + R + i];
+            bh = S[j * ld + Rp + i];
         }
         const float h = Hm[static_cast<size_t>(j) * ldh + i];
-        const float z = Z[static_cast<size_t>(j) * R + i];
+        const float z = Z[static_cast<size_t>(j) * Rp + i];
         const float g = 1.0f - h * h;
         bh = fmaf(-2.0f * h * z, bu, bh);
         S[j * ld + i] = g * bu;
-        S[j * ld + R + i] = g * bh;
+        S[j * ld + Rp + i] = g * bh;
     }
 }
 
@@ -316,8 +328,11 @@ void gemm(msk_disc_trainer* t, cublasOperation_t ta, cublasOperation_t tb, int m
 
 // Loss and dloss/dθ (into t->grad) for B rows of Δ at the current parameters.
 void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaStream_t s) {
-    const int H = t->H, din = t->din, R = B + 1;
-    const long long R2 = 2LL * R;
+    // R rows (B Δ rows + the zero row) stored with Rp = R rounded up to 4 rows per
+    // half, so every leading dimension and half offset is 16-B aligned (the
+    // aligned cuBLAS kernels); padding rows stay zero in every stacked buffer
+    const int H = t->H, din = t->din, R = B + 1, Rp = (R + 3) & ~3;
+    const long long R2 = 2LL * Rp;
     ckb(cublasSetStream(t->blas, s), "cublasSetStream");
     const float* th = t->theta32;
     const float *W0 = th, *b0 = th + static_cast<long long>(H) * din, *W1 = th + t->o1,
@@ -327,63 +342,63 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     float *gW0 = g, *gb0 = g + static_cast<long long>(H) * din, *gW1 = g + t->o1,
           *gb1 = g + t->o1 + static_cast<long long>(H) * H, *gW2 = g + t->o2,
           *gb2 = g + t->o2 + static_cast<long long>(H) * H, *gw4 = g + t->o3, *gb3 = g + t->o3 + H;
-    const int gR = (R + 255) / 256;
-    const dim3 eg((R + kRowsPerBlock - 1) / kRowsPerBlock, H);
-    float *Xb = t->X2 + R, *Xt = t->X2;  // primal / tangent halves
+    const int gR = (Rp + 255) / 256;
+    const dim3 eg((Rp + kRowsPerBlock - 1) / kRowsPerBlock, H);
+    float *Xb = t->X2 + Rp, *Xt = t->X2;  // primal / tangent halves
     float* Ab[4];
     float* At[4];
     for (int l = 1; l <= 3; ++l) {
         At[l] = t->A[l];
-        Ab[l] = t->A[l] + R;
+        Ab[l] = t->A[l] + Rp;
     }
 
     // ---- forward (nn.cpp:54-73) ----
-    pack_input_kernel<<<dim3((R + 31) / 32, (din + 31) / 32), dim3(32, 8), 0, s>>>(delta, B, ld, din, R, t->X2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, din, Xb, R2, W0, H, Ab[1], R2);
-    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[1], R, H, R2, b0);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, Ab[1], R2, W1, H, Ab[2], R2);
-    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[2], R, H, R2, b1);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, Ab[2], R2, W2, H, Ab[3], R2);
-    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[3], R, H, R2, b2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, 1, H, Ab[3], R2, w4, 1, t->z4, R);
+    pack_input_kernel<<<dim3((Rp + 31) / 32, (din + 31) / 32), dim3(32, 8), 0, s>>>(delta, B, ld, din, R, Rp, t->X2);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, din, Xb, R2, W0, H, Ab[1], R2);
+    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[1], R, Rp, R2, b0);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, Ab[1], R2, W1, H, Ab[2], R2);
+    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[2], R, Rp, R2, b1);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, Ab[2], R2, W2, H, Ab[3], R2);
+    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[3], R, Rp, R2, b2);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, 1, H, Ab[3], R2, w4, 1, t->z4, Rp);
     head_kernel<<<gR, 256, 0, s>>>(t->z4, b3, B, R, t->d4, t->dd4, t->dz4, t->lrow);
 
     // ---- input gradient g = dy/dx (nn.cpp:161-164) ----
-    d3_kernel<<<eg, 256, 0, s>>>(t->d4, w4, Ab[3], R2, R, H, t->T1);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, R, H, H, t->T1, R, W2, H, t->T2, R);
-    gate_kernel<<<eg, 256, 0, s>>>(t->T2, R, Ab[2], R2, R, H, t->T2, R);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, R, H, H, t->T2, R, W1, H, t->T1, R);
-    gate_kernel<<<eg, 256, 0, s>>>(t->T1, R, Ab[1], R2, R, H, t->T1, R);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, R, din, H, t->T1, R, W0, H, Xt, R2);
+    d3_kernel<<<eg, 256, 0, s>>>(t->d4, w4, Ab[3], R2, R, Rp, t->T1, Rp);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, Rp, H, H, t->T1, Rp, W2, H, t->T2, Rp);
+    gate_kernel<<<eg, 256, 0, s>>>(t->T2, Rp, Ab[2], R2, R, Rp, t->T2, Rp);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, Rp, H, H, t->T2, Rp, W1, H, t->T1, Rp);
+    gate_kernel<<<eg, 256, 0, s>>>(t->T1, Rp, Ab[1], R2, R, Rp, t->T1, Rp);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, Rp, din, H, t->T1, Rp, W0, H, Xt, R2);
 
     // ---- forward tangent along g (nn.cpp:167-171) ----
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, din, Xt, R2, W0, H, t->Z[1], R);
-    gate_kernel<<<eg, 256, 0, s>>>(t->Z[1], R, Ab[1], R2, R, H, At[1], R2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, At[1], R2, W1, H, t->Z[2], R);
-    gate_kernel<<<eg, 256, 0, s>>>(t->Z[2], R, Ab[2], R2, R, H, At[2], R2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, H, H, At[2], R2, W2, H, t->Z[3], R);
-    gate_kernel<<<eg, 256, 0, s>>>(t->Z[3], R, Ab[3], R2, R, H, At[3], R2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, R, 1, H, At[3], R2, w4, 1, t->zeta4, R);
-    head2_kernel<<<gR, 256, 0, s>>>(t->d4, t->dd4, t->zeta4, t->dz4, B, R, static_cast<float>(t->lam / B), t->V,
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, din, Xt, R2, W0, H, t->Z[1], Rp);
+    gate_kernel<<<eg, 256, 0, s>>>(t->Z[1], Rp, Ab[1], R2, R, Rp, At[1], R2);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, At[1], R2, W1, H, t->Z[2], Rp);
+    gate_kernel<<<eg, 256, 0, s>>>(t->Z[2], Rp, Ab[2], R2, R, Rp, At[2], R2);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, At[2], R2, W2, H, t->Z[3], Rp);
+    gate_kernel<<<eg, 256, 0, s>>>(t->Z[3], Rp, Ab[3], R2, R, Rp, At[3], R2);
+    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, 1, H, At[3], R2, w4, 1, t->zeta4, Rp);
+    head2_kernel<<<gR, 256, 0, s>>>(t->d4, t->dd4, t->zeta4, t->dz4, B, R, Rp, static_cast<float>(t->lam / B), t->V,
                                     t->prow);
 
     // ---- reverse pass over [tangent; primal] (nn.cpp:186-221 + nn.cpp:98-128) ----
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, 1, H, static_cast<int>(R2), t->V, R2, t->A[3], R2, gw4, 1);
-    colsum_kernel<<<1, 256, 0, s>>>(t->V + R, R, 0, gb3);
-    rev_elem_kernel<true><<<eg, 256, 0, s>>>(t->S1, t->V, w4, Ab[3], R2, t->Z[3], R, H);
+    colsum_kernel<<<1, 256, 0, s>>>(t->V + Rp, R, 0, gb3);
+    rev_elem_kernel<true><<<eg, 256, 0, s>>>(t->S1, t->V, w4, Ab[3], R2, t->Z[3], R, Rp, H);
     // layer 2
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, H, static_cast<int>(R2), t->S1, R2, t->A[2], R2, gW2, H);
-    colsum_kernel<<<H, 256, 0, s>>>(t->S1 + R, R, R2, gb2);
+    colsum_kernel<<<H, 256, 0, s>>>(t->S1 + Rp, R, R2, gb2);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(R2), H, H, t->S1, R2, W2, H, t->S2, R2);
-    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S2, nullptr, nullptr, Ab[2], R2, t->Z[2], R, H);
+    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S2, nullptr, nullptr, Ab[2], R2, t->Z[2], R, Rp, H);
     // layer 1
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, H, static_cast<int>(R2), t->S2, R2, t->A[1], R2, gW1, H);
-    colsum_kernel<<<H, 256, 0, s>>>(t->S2 + R, R, R2, gb1);
+    colsum_kernel<<<H, 256, 0, s>>>(t->S2 + Rp, R, R2, gb1);
     gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(R2), H, H, t->S2, R2, W1, H, t->S1, R2);
-    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S1, nullptr, nullptr, Ab[1], R2, t->Z[1], R, H);
+    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S1, nullptr, nullptr, Ab[1], R2, t->Z[1], R, Rp, H);
     // layer 0
     gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, din, static_cast<int>(R2), t->S1, R2, t->X2, R2, gW0, H);
-    colsum_kernel<<<H, 256, 0, s>>>(t->S1 + R, R, R2, gb0);
+    colsum_kernel<<<H, 256, 0, s>>>(t->S1 + Rp, R, R2, gb0);
 
     loss_kernel<<<1, 1024, 0, s>>>(t->lrow, t->prow, R, t->lam, t->loss);
     ckc(cudaGetLastError(), "disc train kernels");
@@ -447,7 +462,7 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
         t->bad = talloc<int>(t, 1);
         ckc(cudaMemcpy(t->theta, theta, P * sizeof(double), cudaMemcpyHostToDevice), "upload theta");
         to_f32_kernel<<<grid_for(P), 256>>>(t->theta, P, t->theta32);
-        const size_t R = static_cast<size_t>(max_rows) + 1, RH = R * H;
+        const size_t R = (static_cast<size_t>(max_rows) + 1 + 3) & ~static_cast<size_t>(3), RH = R * H;  // padded
         t->X2 = talloc<float>(t, 2 * R * din);
         for (int l = 1; l <= 3; ++l) {
             t->A[l] = talloc<float>(t, 2 * RH);

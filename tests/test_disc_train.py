@@ -156,6 +156,26 @@ def test_device_gradient_matches_oracle(math, tol_g, tol_l, din, H, B):
 
 
 @pytest.mark.gpu
+def test_device_gradient_after_a_larger_batch():
+    """Row counts change between calls (B = 999 then 37, 38, 40): the padded
+    layout must not pick up rows a previous, larger batch left behind."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    din, H = 9, 16
+    theta = mlp_init(din, H, 3)
+    tr = pk.DiscTrainer(din, H, theta, max_rows=1000, math=0)
+    tr.gradient(torch.randn(999, din, device="cuda"))
+    for B in (37, 38, 40):
+        d = torch.randn(B, din, device="cuda") * 0.3
+        gref = disc_loss_grad(theta, din, H, d.cpu().double().numpy(), 10.0)[3]
+        g, _ = tr.gradient(d)
+        assert _block_rel(g.cpu().double().numpy(), gref, din, H) <= 1e-4, B
+    tr.close()
+
+
+@pytest.mark.gpu
 def test_device_gradient_ragged_rows_and_ld():
     """A Δ view with a row stride larger than its width (a rollout buffer slice), fewer rows than max_rows."""
     import torch
