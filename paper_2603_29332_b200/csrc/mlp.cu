@@ -130,80 +130,96 @@ __device__ __forceinline__ void store_tiled16(void* img, int KB, int m, int n0, 
     *reinterpret_cast<uint4*>(base + blk_off(r, k + 8)) = hi;
 }
 
+// Epilogues read at most one f32 source per output element: the addend (tanh
+// layers with an addend, the affine head) or the running value they update
+// (kEpiTanhAcc's sum, kEpiOde's action).  It is loaded 32 columns ahead into
+// registers, so its (L2) latency overlaps the MMA tail and the TMEM loads.
+template <int EPI>
+__device__ __forceinline__ const float* epi_src(const GemmArgs& g, int m, int& ld) {
+    if (m >= g.M) return nullptr;
+    if (EPI == kEpiTanhAcc || EPI == kEpiOde) {
+        ld = g.ld_f;
+        return g.out_f;
+    }
+    ld = g.ld_add;
+    return g.addend;
+}
+template <int EPI>
+__device__ __forceinline__ int epi_limit(const GemmArgs& g) {
+    return (EPI == kEpiF32 || EPI == kEpiOde) ? g.n_valid : g.N;
+}
+
+// 32 source values of row m at columns [n0, n0 + 32) (0 outside the valid range).
+__device__ __forceinline__ void load_src32(const float* row, int n0, int limit, bool vec, float (&x)[32]) {
+    if (!row) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = 0.0f;
+        return;
+    }
+    if (vec && n0 + 32 <= limit) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            const float4 t = *reinterpret_cast<const float4*>(row + n0 + i);
+            x[i] = t.x;
+            x[i + 1] = t.y;
+            x[i + 2] = t.z;
+            x[i + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) x[i] = n0 + i < limit ? row[n0 + i] : 0.0f;
+    }
+}
+
+__device__ __forceinline__ void store_f16cols(float* op, int n0, int limit, bool vec, const float* v) {
+    if (vec && n0 + 16 <= limit) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(op + n0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (n0 + i < limit) op[n0 + i] = v[i];
+    }
+}
+
 // Bias / activation / store of 16 consecutive accumulator columns [n0, n0 + 16)
-// of output row m (sb = the tile's staged biases of those columns).
+// of output row m (sb = the tile's staged biases of those columns, src = the
+// preloaded f32 source values of those columns).
 template <int EPI>
 __device__ __forceinline__ void epi16(const GemmArgs& g, int m, int n0, int n_out_pad, const float* sb,
-                                      float (&v)[16]) {
+                                      const float* src, float (&v)[16]) {
+    constexpr bool kTanh = EPI == kEpiTanhTiled || EPI == kEpiTanhPre || EPI == kEpiTanhAcc;
+    float* orow = (m < g.M && g.out_f) ? g.out_f + static_cast<size_t>(m) * g.ld_f : nullptr;
+    const bool vec = (g.ld_f & 3) == 0;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] += sb[i];
-    if (EPI == kEpiTanhTiled) {
-        if (g.addend && m < g.M) {
-            const float* ap = g.addend + static_cast<size_t>(m) * g.ld_add + n0;
-            if (n0 + 16 <= g.N) {  // 4 x 16-B loads of the thread's 64 contiguous bytes
+    for (int i = 0; i < 16; ++i) v[i] = EPI == kEpiTanhPre ? fmaf(g.scale, v[i], sb[i]) : v[i] + sb[i];
+    if (kTanh) {
+        if (EPI != kEpiTanhAcc) {  // addend (0 when absent)
 #pragma unroll
-                for (int i = 0; i < 16; i += 4) {
-                    const float4 t = *reinterpret_cast<const float4*>(ap + i);
-                    v[i] += t.x;
-                    v[i + 1] += t.y;
-                    v[i + 2] += t.z;
-                    v[i + 3] += t.w;
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (n0 + i < g.N) v[i] += ap[i];
-            }
+            for (int i = 0; i < 16; ++i) v[i] += src[i];
         }
-        if (n0 + 16 <= g.N) {
+        if (EPI == kEpiTanhPre && orow) store_f16cols(orow, n0, g.N, vec, v);  // f32 pre-activation
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = tanh_a(v[i]);
-        } else {
+        for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+        if (EPI == kEpiTanhAcc && orow) {  // running f32 sum of the activations
+            float y[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
+            for (int i = 0; i < 16; ++i) y[i] = src[i] + v[i];
+            store_f16cols(orow, n0, g.N, vec, y);
         }
         store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
     } else if (EPI == kEpiF32) {
-        if (m < g.M) {
-            float* op = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
+        if (orow) {
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                v[i] = fmaf(g.scale, v[i], g.offset);
-                if (g.addend && n0 + i < g.n_valid) v[i] += g.addend[static_cast<size_t>(m) * g.ld_add + n0 + i];
-            }
-            if (n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {
-#pragma unroll
-                for (int i = 0; i < 16; i += 4)
-                    *reinterpret_cast<float4*>(op + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (n0 + i < g.n_valid) op[i] = v[i];
-            }
+            for (int i = 0; i < 16; ++i) v[i] = fmaf(g.scale, v[i], g.offset) + src[i];
+            store_f16cols(orow, n0, g.n_valid, vec, v);
         }
     } else {  // kEpiOde: a += dt * psi
         float y[16];
-        float* ap = g.out_f + static_cast<size_t>(m) * g.ld_f + n0;
-        if (m < g.M && n0 + 16 <= g.n_valid && (g.ld_f & 3) == 0) {  // 16-B vector RMW
 #pragma unroll
-            for (int i = 0; i < 16; i += 4) {
-                const float4 t = *reinterpret_cast<const float4*>(ap + i);
-                y[i] = fmaf(g.dt, v[i], t.x);
-                y[i + 1] = fmaf(g.dt, v[i + 1], t.y);
-                y[i + 2] = fmaf(g.dt, v[i + 2], t.z);
-                y[i + 3] = fmaf(g.dt, v[i + 3], t.w);
-                *reinterpret_cast<float4*>(ap + i) = make_float4(y[i], y[i + 1], y[i + 2], y[i + 3]);
-            }
-        } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                y[i] = 0.0f;
-                if (m < g.M && n0 + i < g.n_valid) {
-                    y[i] = fmaf(g.dt, v[i], ap[i]);
-                    ap[i] = y[i];
-                }
-            }
-        }
+        for (int i = 0; i < 16; ++i) y[i] = (orow && n0 + i < g.n_valid) ? fmaf(g.dt, v[i], src[i]) : 0.0f;
+        if (orow) store_f16cols(orow, n0, g.n_valid, vec, y);
         if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
     }
 }
@@ -219,21 +235,31 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
         const int n = nb * kGemmBN + i;
         sbias[i] = (g.bias && n < g.N) ? g.bias[n] : 0.0f;
     }
+    const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
+    const int c_lo = ((warp - 2) / 4) * (kGemmBN / 2), c_hi = c_lo + kGemmBN / 2;
+    int lds = 0;
+    const float* sp = epi_src<EPI>(g, m, lds);
+    const float* srow = sp ? sp + static_cast<size_t>(m) * lds : nullptr;
+    const int limit = epi_limit<EPI>(g);
+    const bool svec = (lds & 3) == 0;
+    float cur[32], nxt[32];
+    load_src32(srow, nb * kGemmBN + c_lo, limit, svec, cur);  // overlaps the MMA tail
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // epilogue warps only
     bar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
-    const int c_lo = ((warp - 2) / 4) * (kGemmBN / 2), c_hi = c_lo + kGemmBN / 2;
     const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
     const int n_out_pad = pad_to(EPI == kEpiOde ? g.n_valid : g.N, kGemmBK);  // tiled output width
     const int n_end = EPI == kEpiF32 ? g.n_valid : n_out_pad;
     for (int c = c_lo; c < c_hi; c += 32) {
         const int n0 = nb * kGemmBN + c;
         if (n0 >= n_end) break;  // columns past the valid / padded output width
+        if (c + 32 < c_hi) load_src32(srow, n0 + 32, limit, svec, nxt);
         float v[2][16];
         ld32(trow + c, v);
-        epi16<EPI>(g, m, n0, n_out_pad, sbias + c, v[0]);
-        if (n0 + 16 < n_end) epi16<EPI>(g, m, n0 + 16, n_out_pad, sbias + c + 16, v[1]);
+        epi16<EPI>(g, m, n0, n_out_pad, sbias + c, cur, v[0]);
+        if (n0 + 16 < n_end) epi16<EPI>(g, m, n0 + 16, n_out_pad, sbias + c + 16, cur + 16, v[1]);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) cur[i] = nxt[i];
     }
 }
 
@@ -513,6 +539,8 @@ cudaError_t prepare_gemm() {
     const int bytes = static_cast<int>(gemm_smem_bytes());
     if ((e = prepare_epi<kEpiTanhTiled>(bytes))) return e;
     if ((e = prepare_epi<kEpiF32>(bytes))) return e;
+    if ((e = prepare_epi<kEpiTanhPre>(bytes))) return e;
+    if ((e = prepare_epi<kEpiTanhAcc>(bytes))) return e;
     return prepare_epi<kEpiOde>(bytes);
 }
 
@@ -549,6 +577,8 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
     switch (epi) {
         case kEpiTanhTiled: return launch_epi<kEpiTanhTiled>(cfg, sel, g);
         case kEpiF32: return launch_epi<kEpiF32>(cfg, sel, g);
+        case kEpiTanhPre: return launch_epi<kEpiTanhPre>(cfg, sel, g);
+        case kEpiTanhAcc: return launch_epi<kEpiTanhAcc>(cfg, sel, g);
         default: return launch_epi<kEpiOde>(cfg, sel, g);
     }
 }

@@ -31,6 +31,8 @@ enum GemmEpi : int {
     kEpiTanhTiled = 0,  // out_a (tiled bf16, K = N) = tanh(acc + bias[n] + addend[m, n])
     kEpiF32 = 1,        // out_f[m * ld + n] = acc + bias[n] (+ addend)           (n < n_valid)
     kEpiOde = 2,        // a[m * ld + n] += dt * (acc + bias[n]); out_a = bf16 tiled copy of the new a
+    kEpiTanhPre = 3,    // z = scale * acc + bias[n] + addend[m, n]: out_f = z (f32), out_a = tanh(z) (tiled)
+    kEpiTanhAcc = 4,    // y = tanh(acc + bias[n]): out_a = y (tiled), out_f[m, n] += y (f32 running sum)
 };
 
 struct GemmArgs {

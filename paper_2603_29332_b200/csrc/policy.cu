@@ -6,10 +6,17 @@
 //     a⁽ᵏ⁺¹⁾ = a⁽ᵏ⁾ + ψ(k·dt, s, a⁽ᵏ⁾)·dt,  k = 0 … N_ODE − 1.
 // Every layer is one tcgen05 GEMM (mlp.cu).  ψ's first layer is split by
 // input block: the observation part W1_s·s is computed once per control step
-// (it does not change along the ODE), the time part b1 + W1_t·φ(t_k) is a
-// per-k bias precomputed on the host, so each ODE step costs
-// [a]·W1_aᵀ + 3 more layers.  The whole sample (π⁽⁰⁾, noise, N_ODE × 4 GEMMs)
-// is captured once into a CUDA graph and replayed.
+// (it does not change along the ODE) and the time part b1 + W1_t·φ(t_k) is a
+// per-k bias precomputed on the host.  ψ depends on a only through its
+// first-layer pre-activation z_k = W1_a a_k + W1_s s + b1 + W1_t φ(t_k), and
+// a_{k+1} − a_k = dt (W4 h3_k + b4), so
+//     z_{k+1} = z_k + dt (W1_a W4) h3_k + dt W1_a b4 + W1_t (φ(t_{k+1}) − φ(t_k))
+//     a_N     = a_0 + dt W4 (Σ_k h3_k) + N dt b4
+// with W1_a W4 (H x H) formed once in f64 on the host.  An ODE step is then
+// three H x H layers (z update, layer 2, layer 3 — the z update keeps z in
+// f32, layer 3 also accumulates Σ h3 in f32) and the action head runs once
+// after the last step: 3 N + 1 GEMMs instead of 4 N.  The whole sample (π⁽⁰⁾,
+// noise, the ODE) is captured once into a CUDA graph and replayed.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -134,11 +141,15 @@ struct msk_policy {
     void *qw1s = nullptr, *qw1a = nullptr, *qw2 = nullptr, *qw3 = nullptr, *qw4 = nullptr;
     float *pb1 = nullptr, *pb2 = nullptr, *pb3 = nullptr, *pb4 = nullptr, *log_std = nullptr;
     float *qc = nullptr, *qb2 = nullptr, *qb3 = nullptr, *qb4 = nullptr;  // qc: [n_ode x H] time biases
+    void* qm = nullptr;      // W1_a W4 (H x H), tiled bf16
+    float* qd = nullptr;     // [n_ode - 1 x H]: dt W1_a b4 + W1_t (φ(t_{k+1}) − φ(t_k))
+    float* qhb = nullptr;    // [NM]: N dt b4 / dt = N b4 (the head GEMM scales by dt)
     float *norm_mean = nullptr, *norm_inv_sd = nullptr;
     bool norm = false;
     // scratch
     void *s_t = nullptr, *a_t = nullptr, *h1 = nullptr, *h2 = nullptr;
     float* P = nullptr;
+    float *z1 = nullptr, *hsum = nullptr;  // f32 [rows x H]: ψ layer-1 pre-activation, Σ_k h3_k
     uint32_t* d_step = nullptr;  // noise counter of the current call (outside the graph)
     // graph cache (keyed by the call's pointers / sizes)
     cudaGraphExec_t gexec = nullptr;
@@ -211,27 +222,39 @@ void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_
     sample_a0_kernel<<<(pad_to(n, kGemmBM) + 7) / 8, 256, 0, s>>>(n, NM, actions, p->log_std, explore, seed,
                                                                   p->d_step, env_offset, a0_out, logprob, p->a_t);
     ckp(cudaGetLastError(), "a0");
-    // ψ: P = W1_s · s once, then N_ODE Euler steps
+    // ψ: P = W1_s · s once, then N_ODE Euler steps in the z-recurrence form
     GemmArgs pg;
     pg.M = n; pg.A = p->s_t; pg.W = p->qw1s; pg.N = H; pg.K = D; pg.out_f = p->P; pg.ld_f = H; pg.n_valid = H;
     ckp(launch_gemm(pg, kEpiF32, s), "psiP");
+    if (p->n_ode == 0) return;
+    GemmArgs z;  // z_0 = W1_a a_0 + P + b1 + W1_t φ(0)
+    z.M = n; z.A = p->a_t; z.W = p->qw1a; z.bias = p->qc; z.addend = p->P; z.ld_add = H; z.N = H; z.K = NM;
+    z.out_a = p->h1; z.out_f = p->z1; z.ld_f = H;
+    ckp(launch_gemm(z, kEpiTanhPre, s), "psi1");
+    ckp(cudaMemsetAsync(p->hsum, 0, sizeof(float) * static_cast<size_t>(pad_to(n, kGemmBM)) * H, s), "hsum");
+    void *x = p->h1, *y = p->h2;  // x: tanh(z_k)
     for (int k = 0; k < p->n_ode; ++k) {
         GemmArgs q;
-        q.M = n;
-        q.A = p->a_t; q.W = p->qw1a; q.bias = p->qc + static_cast<size_t>(k) * H; q.addend = p->P; q.ld_add = H;
-        q.N = H; q.K = NM; q.out_a = p->h1;
-        ckp(launch_gemm(q, kEpiTanhTiled, s), "psi1");
-        q.addend = nullptr;
-        q.A = p->h1; q.W = p->qw2; q.bias = p->qb2; q.K = H; q.out_a = p->h2;
+        q.M = n; q.N = H; q.K = H;
+        q.A = x; q.W = p->qw2; q.bias = p->qb2; q.out_a = y;
         ckp(launch_gemm(q, kEpiTanhTiled, s), "psi2");
-        q.A = p->h2; q.W = p->qw3; q.bias = p->qb3; q.out_a = p->h1;
-        ckp(launch_gemm(q, kEpiTanhTiled, s), "psi3");
-        GemmArgs u;
-        u.M = n; u.A = p->h1; u.W = p->qw4; u.bias = p->qb4; u.N = NM; u.K = H;
-        u.out_f = actions; u.ld_f = NM; u.n_valid = NM; u.dt = static_cast<float>(p->dt);
-        u.out_a = (k + 1 < p->n_ode) ? p->a_t : nullptr;
-        ckp(launch_gemm(u, kEpiOde, s), "psi4");
+        q.A = y; q.W = p->qw3; q.bias = p->qb3; q.out_a = x; q.out_f = p->hsum; q.ld_f = H;
+        ckp(launch_gemm(q, kEpiTanhAcc, s), "psi3");
+        if (k + 1 < p->n_ode) {  // z_{k+1} = z_k + dt (W1_a W4) h3_k + qd_k
+            GemmArgs u;
+            u.M = n; u.N = H; u.K = H; u.A = x; u.W = p->qm; u.bias = p->qd + static_cast<size_t>(k) * H;
+            u.addend = p->z1; u.ld_add = H; u.out_f = p->z1; u.ld_f = H; u.out_a = y;
+            u.scale = static_cast<float>(p->dt);
+            ckp(launch_gemm(u, kEpiTanhPre, s), "psi1");
+            std::swap(x, y);
+        }
     }
+    // a_N = a_0 + dt (W4 Σ_k h3_k + N b4), in place on the action buffer
+    ckp(launch_f32_to_tiled(p->hsum, n, H, H, y, s), "hsum tiles");
+    GemmArgs fh;
+    fh.M = n; fh.A = y; fh.W = p->qw4; fh.bias = p->qhb; fh.N = NM; fh.K = H; fh.out_f = actions; fh.ld_f = NM;
+    fh.n_valid = NM; fh.scale = static_cast<float>(p->dt); fh.addend = actions; fh.ld_add = NM;
+    ckp(launch_gemm(fh, kEpiF32, s), "psi4");
 }
 
 }  // namespace
@@ -297,14 +320,46 @@ int msk_policy_create(int32_t obs_dim, int32_t n_actions, int32_t hidden, const 
         p->qb2 = p->upload(to_f32(t, H)); t += H;
         p->qw3 = p->upload(pack_weights(t, H, H, 0, H)); t += static_cast<size_t>(H) * H;
         p->qb3 = p->upload(to_f32(t, H)); t += H;
+        const double* W4 = t;  // NM x H, column-major
         p->qw4 = p->upload(pack_weights(t, NM, H, 0, H)); t += static_cast<size_t>(NM) * H;
+        const double* b4 = t;
         p->qb4 = p->upload(to_f32(t, NM));
+        {  // z-recurrence constants (see the header): W1_a W4, W1_a b4, time-bias differences
+            const double* W1a = W1 + static_cast<size_t>(kTimeFeatures + D) * H;  // column a of W1_a at W1a + a H
+            std::vector<double> Mq(static_cast<size_t>(H) * H, 0.0), v(H, 0.0);
+            for (int kk = 0; kk < H; ++kk)
+                for (int a = 0; a < NM; ++a) {
+                    const double w4 = W4[static_cast<size_t>(kk) * NM + a];
+                    const double* col = W1a + static_cast<size_t>(a) * H;
+                    double* out = Mq.data() + static_cast<size_t>(kk) * H;
+                    for (int i = 0; i < H; ++i) out[i] += col[i] * w4;
+                }
+            for (int a = 0; a < NM; ++a)
+                for (int i = 0; i < H; ++i) v[i] += W1a[static_cast<size_t>(a) * H + i] * b4[a];
+            p->qm = p->upload(pack_weights(Mq.data(), H, H, 0, H));
+            std::vector<float> qd(static_cast<size_t>(std::max(1, n_ode - 1)) * H);
+            for (int k = 0; k + 1 < n_ode; ++k)
+                for (int i = 0; i < H; ++i) {
+                    double dtime = 0.0;  // W1_t (φ(t_{k+1}) − φ(t_k))
+                    double f0[kTimeFeatures], f1[kTimeFeatures];
+                    time_features(k * dt_ode, f0);
+                    time_features((k + 1) * dt_ode, f1);
+                    for (int j = 0; j < kTimeFeatures; ++j) dtime += W1[static_cast<size_t>(j) * H + i] * (f1[j] - f0[j]);
+                    qd[static_cast<size_t>(k) * H + i] = static_cast<float>(dt_ode * v[i] + dtime);
+                }
+            p->qd = p->upload(qd);
+            std::vector<float> hb(NM);
+            for (int a = 0; a < NM; ++a) hb[a] = static_cast<float>(n_ode * b4[a]);
+            p->qhb = p->upload(hb);
+        }
         // scratch
         p->s_t = p->dalloc<char>(tiled_a_bytes(max_envs, D));
         p->a_t = p->dalloc<char>(tiled_a_bytes(max_envs, NM));
         p->h1 = p->dalloc<char>(tiled_a_bytes(max_envs, H));
         p->h2 = p->dalloc<char>(tiled_a_bytes(max_envs, H));
         p->P = p->dalloc<float>(static_cast<size_t>(pad_to(max_envs, kGemmBM)) * H);
+        p->z1 = p->dalloc<float>(static_cast<size_t>(pad_to(max_envs, kGemmBM)) * H);
+        p->hsum = p->dalloc<float>(static_cast<size_t>(pad_to(max_envs, kGemmBM)) * H);
         p->norm_mean = p->dalloc<float>(D);
         p->norm_inv_sd = p->dalloc<float>(D);
         p->d_step = p->dalloc<uint32_t>(1);
