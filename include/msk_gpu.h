@@ -295,6 +295,17 @@ int msk_rollout_gae(msk_rollout* r, const float* bootstrap_value, float gamma, f
                     float* advantages, float* returns, void* stream);
 /* Device pointer of a stored field: 0 obs, 1 a0, 2 actions, 3 logprob, 4 reward, 5 done, 6 value, 7 delta. */
 void* msk_rollout_field(msk_rollout* r, int32_t field);
+/* PPO minibatching ("epochs over shuffled minibatches"; the
+ * learner's minibatch loop, learn.cpp, is absent): epoch `epoch`'s shuffle of
+ * the h*E records is a keyed Feistel bijection of [0, h*E) (seed, epoch) —
+ * deterministic, no sort; minibatch `index` holds records
+ * perm(index*mb_size + j), j < mb_size (the last one may be short).  Gathers
+ * the stored obs / a0 / actions / logprob / value and the last GAE's
+ * advantages / returns into caller buffers [mb_size x dim] (each nullable);
+ * record_ids (nullable) receives the record indices (t*E + env). */
+int msk_rollout_minibatch(msk_rollout* r, uint64_t seed, int32_t epoch, int32_t index, int32_t mb_size,
+                          float* obs, float* a0, float* actions, float* logprob, float* advantages, float* returns,
+                          float* value, int32_t* record_ids, void* stream);
 
 #ifdef __cplusplus
 }

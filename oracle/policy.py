@@ -87,3 +87,47 @@ def compute_gae(reward, done, value, bootstrap, gamma, lam):
         adv[t] = next_a
         next_v = value[t]
     return adv, adv + value
+
+
+# ---- PPO minibatch shuffle (rollout.cu msk_rollout_minibatch) -------------
+def _mix32(x):
+    x = np.uint64(x) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(16)
+    x = (x * np.uint64(0x7FEB352D)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(15)
+    x = (x * np.uint64(0x846CA68B)) & np.uint64(0xFFFFFFFF)
+    x ^= x >> np.uint64(16)
+    return int(x)
+
+
+def minibatch_key(seed, epoch):
+    """splitmix64 of (seed, epoch), as msk_rollout_minibatch."""
+    M = (1 << 64) - 1
+    z = (seed + 0x9E3779B97F4A7C15 * (epoch + 1)) & M
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+    return z ^ (z >> 31)
+
+
+def feistel_permutation(n, key):
+    """The epoch shuffle: perm[i] for i < n (4-round Feistel on an even-bit
+    domain >= n, cycle-walked into [0, n))."""
+    bits = 2
+    while (1 << bits) < n:
+        bits += 2
+    hb = bits // 2
+    mask = (1 << hb) - 1
+    out = np.empty(n, dtype=np.int64)
+    for i in range(n):
+        x = i
+        while True:
+            left, right = x >> hb, x & mask
+            for rnd in range(4):
+                k = ((key >> (16 * rnd)) ^ (0x9E3779B9 * (rnd + 1))) & 0xFFFFFFFF
+                t = left ^ (_mix32(right ^ k) & mask)
+                left, right = right, t
+            x = (left << hb) | right
+            if x < n:
+                break
+        out[i] = x
+    return out

@@ -133,6 +133,22 @@ class Rollout:
                                        int(bool(normalize)), _p(adv), _p(ret), s))
         return adv, ret
 
+    def minibatch(self, seed, epoch, index, mb_size, obs_dim, act_dim, stream=None):
+        """PPO minibatch `index` of epoch `epoch` (msk_rollout_minibatch): dict of
+        device tensors obs, a0, actions, logprob, advantages, returns, value, record_ids."""
+        torch = self.torch
+        n = self.h * self.E
+        rows = max(0, min(mb_size, n - index * mb_size))
+        f = lambda *shape: torch.empty(*shape, device=self.device)  # noqa: E731
+        out = dict(obs=f(rows, obs_dim), a0=f(rows, act_dim), actions=f(rows, act_dim), logprob=f(rows),
+                   advantages=f(rows), returns=f(rows), value=f(rows),
+                   record_ids=torch.empty(rows, dtype=torch.int32, device=self.device))
+        s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        self._ck(lib().msk_rollout_minibatch(self.h_, C.c_uint64(seed), int(epoch), int(index), int(mb_size),
+                                             *[_p(out[k]) for k in ("obs", "a0", "actions", "logprob", "advantages",
+                                                                   "returns", "value", "record_ids")], s))
+        return out
+
     def field(self, index, cols, dtype=None):
         """Device tensor view [h * E x cols] of a stored field (msk_rollout_field:
         0 obs, 1 a0, 2 actions, 3 logprob, 4 reward, 5 done, 6 value, 7 delta)."""
@@ -341,6 +357,7 @@ def lib():
         L.msk_rollout_last_error.argtypes = [_vp]
         L.msk_rollout_record.argtypes = [_vp, C.c_int32] + [_vp] * 9
         L.msk_rollout_gae.argtypes = [_vp, _vp, C.c_float, C.c_float, C.c_int32, _vp, _vp, _vp]
+        L.msk_rollout_minibatch.argtypes = [_vp, C.c_uint64, C.c_int32, C.c_int32, C.c_int32] + [_vp] * 9
         L.msk_rollout_field.restype = C.c_void_p
         L.msk_rollout_field.argtypes = [_vp, C.c_int32]
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]

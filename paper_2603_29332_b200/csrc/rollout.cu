@@ -74,6 +74,79 @@ __global__ void __launch_bounds__(1024) normalize_kernel(long long n, float* adv
     for (long long i = threadIdx.x; i < n; i += blockDim.x) adv[i] = static_cast<float>((adv[i] - mean) * inv);
 }
 
+// ---- PPO minibatching (epochs over shuffled minibatches) ----
+// The epoch's shuffle is a keyed bijection of [0, n): a 4-round Feistel
+// network on the smallest even-bit-width domain >= n, cycle-walked into
+// [0, n) (format-preserving, no sort, O(1) per record, deterministic in
+// (seed, epoch)).
+__device__ __forceinline__ uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+__host__ __device__ inline int feistel_half_bits(long long n) {
+    int bits = 2;
+    while ((1ll << bits) < n) bits += 2;
+    return bits / 2;
+}
+
+__device__ __forceinline__ uint32_t feistel_perm(uint32_t x, long long n, int hb, uint64_t key) {
+    const uint32_t mask = (1u << hb) - 1u;
+    do {
+        uint32_t l = x >> hb, r = x & mask;
+#pragma unroll
+        for (int round = 0; round < 4; ++round) {
+            const uint32_t k = static_cast<uint32_t>(key >> (16 * round)) ^ (0x9E3779B9u * (round + 1));
+            const uint32_t t = l ^ (mix32(r ^ k) & mask);
+            l = r;
+            r = t;
+        }
+        x = (l << hb) | r;
+    } while (x >= static_cast<uint32_t>(n));
+    return x;
+}
+
+struct MbOut {
+    float *obs, *a0, *act, *logp, *adv, *ret, *value;
+    int* ids;
+};
+
+// One warp per minibatch row: record id, then the row copies (16-B vectors
+// when the row width allows).
+__global__ void minibatch_kernel(long long n, int hb, uint64_t key, long long first, int rows, int obs_dim,
+                                 int act_dim, const float* obs, const float* a0, const float* act,
+                                 const float* logp, const float* adv, const float* ret, const float* value,
+                                 MbOut o) {
+    const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (j >= rows) return;
+    const uint32_t i = feistel_perm(static_cast<uint32_t>(first + j), n, hb, key);
+    auto copy_row = [&](float* dst, const float* src, int dim) {
+        if (!dst || dim == 0) return;
+        const float* sp = src + static_cast<size_t>(i) * dim;
+        float* dp = dst + static_cast<size_t>(j) * dim;
+        if ((dim & 3) == 0) {
+            for (int c = lane; c < dim / 4; c += 32)
+                reinterpret_cast<float4*>(dp)[c] = reinterpret_cast<const float4*>(sp)[c];
+        } else {
+            for (int c = lane; c < dim; c += 32) dp[c] = sp[c];
+        }
+    };
+    copy_row(o.obs, obs, obs_dim);
+    copy_row(o.a0, a0, act_dim);
+    copy_row(o.act, act, act_dim);
+    if (lane == 0) {
+        if (o.logp) o.logp[j] = logp[i];
+        if (o.adv) o.adv[j] = adv[i];
+        if (o.ret) o.ret[j] = ret[i];
+        if (o.value) o.value[j] = value[i];
+        if (o.ids) o.ids[j] = static_cast<int>(i);
+    }
+}
+
 }  // namespace
 
 struct msk_rollout {
@@ -196,6 +269,37 @@ int msk_rollout_gae(msk_rollout* r, const float* bootstrap_value, float gamma, f
         const size_t n = static_cast<size_t>(r->E) * r->h;
         copy_rows(advantages, r->adv, n * 4, s);
         copy_rows(returns, r->ret, n * 4, s);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
+        return MSK_OK;
+    } catch (const std::invalid_argument& ex) {
+        return rfail(r, ex.what());
+    } catch (const std::exception& ex) {
+        return rfail(r, ex.what(), MSK_ERR_CUDA);
+    }
+}
+
+int msk_rollout_minibatch(msk_rollout* r, uint64_t seed, int32_t epoch, int32_t index, int32_t mb_size,
+                          float* obs, float* a0, float* actions, float* logprob, float* advantages, float* returns,
+                          float* value, int32_t* record_ids, void* stream) {
+    if (!r) return rfail(nullptr, "null rollout");
+    try {
+        const long long n = static_cast<long long>(r->E) * r->h;
+        if (n >= (1ll << 31)) throw std::invalid_argument("rollout_minibatch: more than 2^31 records");
+        if (mb_size < 1 || index < 0 || static_cast<long long>(index) * mb_size >= n)
+            throw std::invalid_argument("rollout_minibatch: minibatch out of range");
+        cudaSetDevice(r->device);
+        const long long first = static_cast<long long>(index) * mb_size;
+        const int rows = static_cast<int>(std::min<long long>(mb_size, n - first));
+        // key: (seed, epoch) mixed on the host (splitmix64)
+        uint64_t z = seed + 0x9E3779B97F4A7C15ull * (static_cast<uint64_t>(epoch) + 1);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const MbOut o{obs, a0, actions, logprob, advantages, returns, value, record_ids};
+        minibatch_kernel<<<(rows + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+            n, feistel_half_bits(n), z, first, rows, r->obs_dim, r->act_dim, r->obs, r->a0, r->act, r->logp,
+            r->adv, r->ret, r->value, o);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw std::runtime_error(cudaGetErrorString(e));
         return MSK_OK;

@@ -169,3 +169,16 @@ def test_new_entry_points_fail_cleanly_without_gpu_or_bad_args():
     assert rc == 1 and b"parameter count" in L.msk_policy_last_error(None)
     r = C.c_void_p()
     assert L.msk_rollout_create(0, 8, 1, 1, 1, 0, C.byref(r)) != 0 and not r.value
+
+
+def test_minibatch_oracle_is_a_bijection():
+    """The oracle's Feistel shuffle (rollout.cu msk_rollout_minibatch) permutes
+    [0, n) for ragged n, and depends on (seed, epoch)."""
+    import numpy as np
+
+    from oracle.policy import feistel_permutation, minibatch_key
+
+    for n in (1, 2, 3, 7, 296, 1000, 4097):
+        p = feistel_permutation(n, minibatch_key(5, 0))
+        assert np.array_equal(np.sort(p), np.arange(n))
+    assert not np.array_equal(feistel_permutation(500, minibatch_key(5, 0)), feistel_permutation(500, minibatch_key(5, 1)))

@@ -160,3 +160,51 @@ def test_rollout_gae_matches_oracle_and_spec():
     d = (flags[-1] & 1) == 1
     assert np.abs(adv0.cpu().numpy()[-1][d] - (r[-1] - v[-1])[d]).max() <= 1e-6
     ro.close()
+
+
+def test_rollout_minibatches_are_a_keyed_permutation():
+    """PPO minibatching (msk_rollout_minibatch): every epoch's minibatches
+    partition the h*E records (a permutation equal to the oracle's Feistel
+    shuffle, deterministic in (seed, epoch), different across epochs) and
+    gather exactly the stored rows and the last GAE's advantages / returns."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from oracle.policy import feistel_permutation, minibatch_key
+
+    E, h, D, NA = 37, 8, 12, 5  # 296 records, ragged last minibatch
+    ro = pk.Rollout(E, h, D, NA, 1)
+    rng = np.random.default_rng(8)
+    obs = rng.normal(0, 1, (h, E, D)).astype(np.float32)
+    act = rng.normal(0, 1, (h, E, NA)).astype(np.float32)
+    rew = rng.normal(0, 1, (h, E)).astype(np.float32)
+    val = rng.normal(0, 1, (h, E)).astype(np.float32)
+    for t in range(h):
+        ro.record(t, obs=torch.as_tensor(obs[t], device="cuda"), a0=torch.as_tensor(act[t] * 2, device="cuda"),
+                  actions=torch.as_tensor(act[t], device="cuda"), logprob=torch.as_tensor(rew[t] * 3, device="cuda"),
+                  reward=torch.as_tensor(rew[t], device="cuda"),
+                  flags=torch.zeros(E, dtype=torch.uint8, device="cuda"), value=torch.as_tensor(val[t], device="cuda"))
+    adv, ret = ro.gae(torch.zeros(E, device="cuda"), normalize=True)
+    adv, ret = adv.cpu().numpy().reshape(-1), ret.cpu().numpy().reshape(-1)
+    n, mb = h * E, 50
+    orders = []
+    for epoch in (0, 1):
+        ids = []
+        for b in range((n + mb - 1) // mb):
+            out = {k: v.cpu().numpy() for k, v in ro.minibatch(11, epoch, b, mb, D, NA).items()}
+            i = out["record_ids"].astype(np.int64)
+            ids.append(i)
+            assert np.array_equal(out["obs"], obs.reshape(n, D)[i])
+            assert np.array_equal(out["actions"], act.reshape(n, NA)[i])
+            assert np.array_equal(out["a0"], 2 * act.reshape(n, NA)[i])
+            assert np.array_equal(out["logprob"], 3 * rew.reshape(n)[i])
+            assert np.array_equal(out["value"], val.reshape(n)[i])
+            assert np.array_equal(out["advantages"], adv[i]) and np.array_equal(out["returns"], ret[i])
+        order = np.concatenate(ids)
+        assert np.array_equal(np.sort(order), np.arange(n))
+        assert np.array_equal(order, feistel_permutation(n, minibatch_key(11, epoch)))
+        orders.append(order)
+    assert not np.array_equal(orders[0], orders[1])
+    again = ro.minibatch(11, 1, 0, mb, D, NA)["record_ids"].cpu().numpy()
+    assert np.array_equal(again, orders[1][:mb])
+    ro.close()
