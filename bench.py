@@ -352,7 +352,7 @@ def main():
         if ev:
             ev[3].record(stream)
         if C["exchange"] and (s + 1) % C["exchange"] == 0:  # iteration boundary (h control steps)
-            _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state)
+            _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state, cap=C["exchange"])
             stats.zero_()
         if trainer is not None and (s + 1) % rollout.h == 0:  # D update on the iteration's Δ, then publish
             trainer.step(ro_delta)

@@ -5,9 +5,12 @@ envs [r*E, (r+1)*E) (seeds base + global index, so any sharding gives
 identical per-env results).  Once per rollout iteration every rank packs a
 fixed-size block
 
-    outcome bins  int32 [E, cap]   (Env::drain_episode_outcomes, env.cpp:200-204)
-    outcome failed int32 [E, cap]
+    outcome bins  int16 [E, cap]   (Env::drain_episode_outcomes, env.cpp:200-204)
+    outcome failed uint8 [E, cap]
     outcome counts int32 [E]
+
+(cap = the iteration's h control steps: an env ends at most one episode per
+step, so h slots hold every outcome of an iteration; 3 bytes per slot)
     rollout stats  float64 [7]     (n_steps, Σr, Σr², Σ episode length, episodes, failures, divergences)
     obs moments    float64 [1 + 2 D]  (count, mean[D], population var[D] of this rank's batch)
 
@@ -35,7 +38,7 @@ N_STATS = 7
 
 def block_layout(n_envs: int, cap: int, obs_dim: int):
     """Byte offsets of the per-rank block."""
-    sizes = [("bins", 4 * n_envs * cap), ("failed", 4 * n_envs * cap), ("counts", 4 * n_envs),
+    sizes = [("bins", 2 * n_envs * cap), ("failed", n_envs * cap), ("counts", 4 * n_envs),
              ("stats", 8 * N_STATS), ("norm", 8 * (1 + 2 * obs_dim))]
     off, lay = 0, {}
     for name, nbytes in sizes:
@@ -56,8 +59,8 @@ def pack_block(bins, failed, counts, stats, norm, obs_dim):
         o, nb = lay[name]
         buf[o:o + nb] = t.contiguous().view(torch.uint8).reshape(-1)
 
-    put("bins", bins.to(torch.int32))
-    put("failed", failed.to(torch.int32))
+    put("bins", bins.to(torch.int16))
+    put("failed", failed.to(torch.uint8))
     put("counts", counts.to(torch.int32))
     put("stats", stats.to(torch.float64))
     put("norm", norm.to(torch.float64))
@@ -71,7 +74,7 @@ def unpack_block(buf, n_envs, cap, obs_dim):
         o, nb = lay[name]
         return buf[o:o + nb].view(dtype).reshape(shape)
 
-    return dict(bins=get("bins", torch.int32, (n_envs, cap)), failed=get("failed", torch.int32, (n_envs, cap)),
+    return dict(bins=get("bins", torch.int16, (n_envs, cap)), failed=get("failed", torch.uint8, (n_envs, cap)),
                 counts=get("counts", torch.int32, (n_envs,)), stats=get("stats", torch.float64, (N_STATS,)),
                 norm=get("norm", torch.float64, (1 + 2 * obs_dim,)))
 
@@ -165,7 +168,7 @@ def merged_iteration(blocks, n_envs, cap, obs_dim, norm_state, ema, decay, merge
             stats += p["stats"].cpu()
             nm = p["norm"].cpu().numpy()
             count, mean, var = running_norm_fold(count, mean, var, nm[0], nm[1:1 + obs_dim], nm[1 + obs_dim:])
-    bins = torch.cat([p["bins"] for p in parts])
+    bins = torch.cat([p["bins"] for p in parts]).to(torch.int32)
     failed = torch.cat([p["failed"] for p in parts])
     counts = torch.cat([p["counts"] for p in parts])
     if merge_on_device is not None:
