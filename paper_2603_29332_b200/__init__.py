@@ -45,11 +45,12 @@ class Policy:
     TIME_FEATURES = 5
 
     def __init__(self, obs_dim, n_actions, hidden, pi_theta, log_std, psi_theta, n_ode=20, dt_ode=0.05,
-                 max_envs=4096, head_scale=1.0, head_offset=0.0, device=0):
+                 max_envs=4096, head_scale=1.0, head_offset=0.0, device=None):
         import numpy as np
         import torch
 
         self.torch = torch
+        device = torch.cuda.current_device() if device is None else device
         self.obs_dim, self.nm, self.hidden, self.n_ode, self.dt = obs_dim, n_actions, hidden, n_ode, dt_ode
         self.max_envs = max_envs
         self.device = torch.device("cuda", device)
@@ -101,10 +102,11 @@ class Policy:
 class Rollout:
     """On-device rollout buffer (h x E, step-major) + GAE (msk_rollout_*)."""
 
-    def __init__(self, n_envs, horizon, obs_dim, act_dim, delta_dim, device=0):
+    def __init__(self, n_envs, horizon, obs_dim, act_dim, delta_dim, device=None):
         import torch
 
         self.torch = torch
+        device = torch.cuda.current_device() if device is None else device
         self.E, self.h = n_envs, horizon
         h = C.c_void_p()
         rc = lib().msk_rollout_create(n_envs, horizon, obs_dim, act_dim, delta_dim, device, C.byref(h))
@@ -176,11 +178,12 @@ class DiscTrainer:
     -log clamp(D(0)) - mean log(1 - clamp(D(Δ))) + λ mean ||∇_Δ D(Δ)||².
     math: 0 FP32 GEMMs, 1 TF32 tensor-core GEMMs."""
 
-    def __init__(self, n_in, hidden, theta, lr=3e-5, grad_penalty=10.0, max_rows=4096, math=0, device=0):
+    def __init__(self, n_in, hidden, theta, lr=3e-5, grad_penalty=10.0, max_rows=4096, math=0, device=None):
         import numpy as np
         import torch
 
         self.torch = torch
+        device = torch.cuda.current_device() if device is None else device
         theta = np.ascontiguousarray(theta, dtype=np.float64)
         self.n_in, self.hidden, self.n_params = n_in, hidden, len(theta)
         h = C.c_void_p()
