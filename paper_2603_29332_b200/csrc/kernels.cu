@@ -23,6 +23,8 @@
 // so a step is bit-reproducible.
 #include <cuda_runtime.h>
 
+#include <stdexcept>
+
 #include <cstdint>
 
 #include "device.cuh"
@@ -1351,10 +1353,10 @@ __global__ void set_ints_kernel(DevState St, int n_envs, const int* ints) {
 // Philox4x32-10 excitations, one thread per (env, group of 4 muscles).
 __global__ void excitation_kernel(int n_envs, int nm, long long env_offset, uint64_t seed, uint32_t step,
                                   float* out) {
-    const int groups = (nm + 3) / 4;
-    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-    if (i >= static_cast<long long>(n_envs) * groups) return;
-    const int e = static_cast<int>(i / groups), g = static_cast<int>(i % groups);
+    const int groups = (nm + 3) / 4;  // (n_envs * groups < 2^31: checked by the launcher)
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_envs * groups) return;
+    const int e = i / groups, g = i - e * groups;
     uint32_t c0 = step, c1 = static_cast<uint32_t>(env_offset + e), c2 = static_cast<uint32_t>(g), c3 = 0;
     uint32_t k0 = static_cast<uint32_t>(seed), k1 = static_cast<uint32_t>(seed >> 32);
 #pragma unroll
@@ -1371,10 +1373,18 @@ __global__ void excitation_kernel(int n_envs, int nm, long long env_offset, uint
     }
     const uint32_t r4[4] = {c0, c1, c2, c3};
     float* row = out + static_cast<size_t>(e) * nm;
+    constexpr float kScale = 1.0f / 16777216.0f;
+    if ((nm & 3) == 0) {  // rows start 16-B aligned: one vector store
+        reinterpret_cast<float4*>(row)[g] = make_float4(static_cast<float>(r4[0] >> 8) * kScale,
+                                                        static_cast<float>(r4[1] >> 8) * kScale,
+                                                        static_cast<float>(r4[2] >> 8) * kScale,
+                                                        static_cast<float>(r4[3] >> 8) * kScale);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int m = 4 * g + k;
-        if (m < nm) row[m] = static_cast<float>(r4[k] >> 8) * (1.0f / 16777216.0f);
+        if (m < nm) row[m] = static_cast<float>(r4[k] >> 8) * kScale;
     }
 }
 
@@ -1662,6 +1672,7 @@ void launch_set_ints(const DevState& St, int n, const int* ints, cudaStream_t s)
 void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint32_t step, float* out,
                         cudaStream_t s) {
     const long long tot = static_cast<long long>(n) * ((nm + 3) / 4);
+    if (tot >= (1ll << 31)) throw std::runtime_error("fill_excitations: batch too large");
     excitation_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(n, nm, env_offset, seed, step, out);
 }
 
