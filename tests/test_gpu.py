@@ -834,3 +834,28 @@ def test_reset_ranges_larger_than_the_block(assets):
     for e in (0, 4143, 4144, 9000):
         assert np.array_equal(to_np(g.rng_raw(e, 8)).view(np.uint64), o.rng_raw(e, 8))
     g.close()
+
+
+def test_c1_thousand_step_free_run(assets):
+    """BASELINE config c1: the default arm2_m6 model, 1 env, 1000
+    control steps of fixed-seed Philox excitations, eval mode, RSI off, horizon
+    1000 — GPU and f64 oracle free-running from the same reset: flags identical
+    at every step (the episode ends at step 1000 on both) and max |Δq| over the
+    whole run <= 1e-3 rad (measured 4.1e-5, at step 154)."""
+    mp, cp = model_paths("arm2_m6")
+    g, o = make_pair(mp, cp, 1, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    g.reset()
+    o.reset()
+    worst = 0.0
+    for s in range(1000):
+        a = excitations(0x5EED, s, 1, g.nm).astype(np.float32)
+        og, oo = step_both(g, o, a)
+        sg, so = gpu_state(g), o.get_state()
+        worst = max(worst, float(np.abs(sg["q"] - so["q"]).max()))
+        assert np.array_equal(og["flags"], oo["flags"]), s
+    assert og["flags"][0] & 1  # horizon reached at step 1000
+    _note("arm2_m6", "c1 1000-step free-run q drift (tol 1e-3)", worst)
+    assert worst <= 1e-3, worst
+    g.close()

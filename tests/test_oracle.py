@@ -231,6 +231,7 @@ def _run_pair(name, n, steps, cfg_kw, mode=0):
     ("arm2_m6", 4, 80, dict(episode_horizon=25), 2),
     ("walker5_m16", 4, 40, dict(episode_horizon=1000, termination_body_err=0.3), 0),
     ("wb700", 2, 2, dict(episode_horizon=1000), 2),
+    ("arm2_m6", 1, 1000, dict(episode_horizon=1000, rsi=False), 0),  # BASELINE c1: 1 env, 1000 steps
 ])
 def test_oracle_bit_exact_vs_reference(assets, name, n, steps, cfg_kw, mode):
     _run_pair(name, n, steps, cfg_kw, mode)
