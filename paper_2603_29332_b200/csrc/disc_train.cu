@@ -20,14 +20,18 @@
 //   * each weight gradient is one GEMM over the stacked 2R rows,
 //     gW_l = [b_ζ; b_z]ᵀ [u; H] (the reference's two products in one);
 //   * bias gradients: fixed-order column sums in f64; Adam in f64 with the
-//     reference's non-finite-gradient skip evaluated on the device.
+//     reference's non-finite-gradient skip evaluated on the device;
+//   * each half of a stacked matrix is padded to Rp = R rounded up to 4 rows
+//     (16-B aligned leading dimensions and half offsets, so cuBLAS picks its
+//     sm100 tcgen05 kernels); the column kernels write zeros into the padding
+//     and the GEMMs run over the padded extents.
 // The GEMMs are plain library GEMMs (cuBLAS, f32 data) in the math mode the
 // caller picks: FP32 (default) or TF32 tensor cores.  Only cuBLAS 12.0-level
 // entry points are used: the process may already hold torch's bundled
 // libcublas.so.12, which then serves these symbols (the BF16x9 FP32 emulation
-// of cuBLAS 12.9 is therefore not used).  Elementwise / reduction work is fused into the
-// kernels below.  This is the learner side of the loop, launched once per
-// rollout iteration; the stepping path never calls it.
+// of cuBLAS 12.9 is therefore not used).  Elementwise / reduction work is
+// fused into the kernels below.  This is the learner side of the loop,
+// launched once per rollout iteration; the stepping path never calls it.
 #include <cublas_v2.h>
 #include <cuda_runtime.h>
 
