@@ -176,17 +176,15 @@ __device__ __forceinline__ float mtu_force(float act, float l, float v, float fm
     return fmax * (act * hill_fl(l) * hill_fv(v) + hill_fp(l));
 }
 
-// sqrt of a non-negative f64 from the approximate f64 rsqrt seed (MUFU on the
-// high word, ~23 bits) plus one f64 Newton correction (~46 bits); also returns
-// the f32 reciprocal length.  (Conversions f32 <-> f64 cost more than DMUL on
-// this part: the f64 seed replaced an f32 rsqrt + two conversions, +0.4 %.)  x is clamped
+// sqrt of a non-negative f64 from the f32 rsqrt seed plus one f64 Newton
+// correction (~46 bits); also returns the f32 reciprocal length.  x is clamped
 // at ~1e-30 through its high word (one integer max; negative rounding noise has
 // the sign bit set and clamps too) so degenerate/padding segments stay finite.
 __device__ __forceinline__ double sqrt_d(double x, float& inv) {
     x = __hiloint2double(max(__double2hiint(x), 0x39B4484B), __double2loint(x));
-    double rd;  // f64 MUFU seed (high word): no f64 -> f32 -> f64 conversion round trip
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rd) : "d"(x));
-    inv = static_cast<float>(rd);
+    const float r = rsqrt_ftz(static_cast<float>(x));
+    inv = r;
+    const double rd = static_cast<double>(r);
     const double s = x * rd;
     return fma(fma(-s, s, x), 0.5 * rd, s);
 }
