@@ -219,6 +219,19 @@ int msk_gpu_record_own_outcomes(msk_gpu_ctx* ctx, void* stream);
  * step, episodes, failures, divergences} over the envs stepped (flags from
  * msk_gpu_step; reward nullable); deterministic single-block reduction. */
 int msk_gpu_rollout_stats(msk_gpu_ctx* ctx, const float* reward, const uint8_t* flags, double* stats, void* stream);
+/* One rollout-iteration boundary of this rank (the C++ form of
+ * paper_2603_29332_b200/dist.py iteration_exchange): drains the episode
+ * outcomes (cap slots per env: the iteration's h steps), takes this rank's
+ * rollout stats (stats_in [7] f64, see msk_gpu_rollout_stats) and the f64
+ * column moments of obs [E x obs_dim], all-gathers the fixed-size block over
+ * nccl_comm (an ncclComm_t; NULL = single rank; NCCL is loaded at run time
+ * from libnccl.so.2), then applies the identical rank-ordered merge on the
+ * device: outcomes into the replicated sampler (SPEC.md:296 order), stats
+ * summed in rank order into stats_out [7] (nullable), and the observation
+ * normaliser norm_state [1 + 2 obs_dim] = {count, mean, var} (f64, in/out)
+ * folded rank by rank as RunningNorm::update (nn.cpp:246-270). */
+int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, const float* obs,
+                               const double* stats_in, double* norm_state, double* stats_out, void* stream);
 /* Batch moments of obs [n x obs_dim] (RunningNorm::update's batch mean and
  * population variance, nn.cpp:246-256) in f64: out = [n, mean[D], var[D]]. */
 int msk_gpu_obs_moments(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream);

@@ -135,6 +135,12 @@ public:
         check(msk_gpu_drain_outcomes(ctx_, bins, failed, counts, cap, stream), ctx_);
     }
     void record_own_outcomes(void* stream = nullptr) { check(msk_gpu_record_own_outcomes(ctx_, stream), ctx_); }
+    // Rollout-iteration boundary of this rank (drain, stats, obs moments, NCCL
+    // all-gather over nccl_comm = an ncclComm_t or nullptr, rank-ordered merge).
+    void iteration_exchange(int cap, const float* obs, const double* stats_in, double* norm_state,
+                            double* stats_out = nullptr, void* nccl_comm = nullptr, void* stream = nullptr) {
+        check(msk_gpu_iteration_exchange(ctx_, nccl_comm, cap, obs, stats_in, norm_state, stats_out, stream), ctx_);
+    }
     void fill_excitations(uint64_t seed, uint32_t step, float* actions, void* stream = nullptr) {
         check(msk_gpu_fill_excitations(ctx_, seed, step, actions, stream), ctx_);
     }

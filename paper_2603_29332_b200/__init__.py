@@ -364,6 +364,7 @@ def lib():
         L.msk_rollout_field.restype = C.c_void_p
         L.msk_rollout_field.argtypes = [_vp, C.c_int32]
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
+        L.msk_gpu_iteration_exchange.argtypes = [_vp, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
         L.msk_mlp_param_count.restype = C.c_int64
         L.msk_mlp_param_count.argtypes = [C.c_int32, C.c_int32, C.c_int32]
@@ -644,6 +645,18 @@ class EnvBatch:
                                                            device=self.device)
         self._ck(lib().msk_gpu_obs_moments(self.h, _p(obs.contiguous()), int(n), _p(out), self._s(stream)))
         return out
+
+    def iteration_exchange(self, cap, obs, stats, norm, stats_out=None, nccl_comm=None, stream=None):
+        """msk_gpu_iteration_exchange: drain + stats + obs moments, all-gather over
+        nccl_comm (an ncclComm_t as int; None = single rank), rank-ordered merge on the
+        device.  norm: f64 [1 + 2 obs_dim] device tensor {count, mean, var}, updated
+        in place; returns stats_out (f64 [7])."""
+        torch = self.torch
+        stats_out = stats_out if stats_out is not None else torch.empty(7, dtype=torch.float64, device=self.device)
+        self._ck(lib().msk_gpu_iteration_exchange(self.h, C.c_void_p(nccl_comm) if nccl_comm else None, int(cap),
+                                                  _p(obs.contiguous()), _p(stats), _p(norm), _p(stats_out),
+                                                  self._s(stream)))
+        return stats_out
 
     def rng_raw(self, env, n, stream=None):
         out = self._empty(n, dtype=self.torch.int64)  # raw u64 bits; view as uint64 on the host

@@ -1,5 +1,7 @@
 // C ABI (include/msk_gpu.h): context ownership, device tables, launches.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -40,6 +42,10 @@ int obs_moments_chunks(int n);
 void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t);
 void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint32_t step, float* out,
                         cudaStream_t);
+void launch_merge_block(const DevModel& M, const int* bins, const uint8_t* failed, const int* counts, long long n,
+                        int cap, double* global_ema, cudaStream_t s);
+void launch_exchange_fold(const unsigned char* gathered, size_t block_bytes, int world, size_t off_stats,
+                          size_t off_mom, int D, double* norm, double* stats_out, cudaStream_t s);
 double measure_fp32_peak_tflops();
 }  // namespace msk_b200
 
@@ -96,6 +102,10 @@ struct msk_gpu_ctx {
     // device discriminator (msk_gpu_set_discriminator)
     DiscDev disc{};
     std::vector<void*> disc_allocs;
+    // iteration exchange (msk_gpu_iteration_exchange): this rank's block and the gathered blocks
+    unsigned char* x_block = nullptr;
+    unsigned char* x_gathered = nullptr;
+    size_t x_block_bytes = 0, x_gathered_bytes = 0;
     float* r_delta = nullptr;  // scratch when the caller passes no Δ / reward_aux / flags
     float* r_raux = nullptr;
     uint8_t* r_flags = nullptr;
@@ -422,6 +432,8 @@ void msk_gpu_destroy(msk_gpu_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
+    if (ctx->x_block) cudaFree(ctx->x_block);
+    if (ctx->x_gathered) cudaFree(ctx->x_gathered);
     for (void* p : ctx->allocs) cudaFree(p);
     for (void* p : ctx->disc_allocs) cudaFree(p);
     for (auto& s : ctx->hs)
@@ -867,6 +879,95 @@ int msk_gpu_merge_outcomes(msk_gpu_ctx* ctx, const int32_t* bins, const uint8_t*
         launch_merge(ctx->M, ctx->St, ctx->n_envs, bins, failed, counts, n_envs_total, cap, ctx->global_ema,
                      as_stream(stream));
         ctx->count(2);
+        ctx->check_launch();
+    });
+}
+
+}  // extern "C"
+
+namespace {
+// NCCL is resolved at run time (dlopen of libnccl.so.2, e.g. the copy the
+// process already holds), so the library has no link-time NCCL dependency.
+struct NcclApi {
+    decltype(&ncclAllGather) all_gather = nullptr;
+    decltype(&ncclCommCount) count = nullptr;
+    bool ok = false;
+};
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return a;
+        a.all_gather = reinterpret_cast<decltype(&ncclAllGather)>(dlsym(h, "ncclAllGather"));
+        a.count = reinterpret_cast<decltype(&ncclCommCount)>(dlsym(h, "ncclCommCount"));
+        a.ok = a.all_gather && a.count;
+        return a;
+    }();
+    return api;
+}
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+extern "C" {
+
+int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, const float* obs,
+                               const double* stats_in, double* norm_state, double* stats_out, void* stream) {
+    return guarded(ctx, [&] {
+        if (cap < 1 || !obs || !stats_in || !norm_state) throw ConfigError("iteration_exchange: bad arguments");
+        cudaStream_t s = as_stream(stream);
+        const size_t E = ctx->n_envs, D = ctx->obs_dim;
+        // block: bins i32 [E cap] | failed u8 [E cap] | counts i32 [E] | stats f64 [7] | moments f64 [1 + 2D]
+        const size_t off_failed = align_up(4 * E * cap, 16), off_counts = align_up(off_failed + E * cap, 16);
+        const size_t off_stats = align_up(off_counts + 4 * E, 16), off_mom = align_up(off_stats + 8 * 7, 16);
+        const size_t bytes = align_up(off_mom + 8 * (1 + 2 * D), 16);
+        int world = 1;
+        if (nccl_comm) {
+            if (!nccl_api().ok) throw CudaFail("iteration_exchange: libnccl.so.2 not loadable");
+            if (nccl_api().count(static_cast<ncclComm_t>(nccl_comm), &world) != ncclSuccess)
+                throw CudaFail("iteration_exchange: ncclCommCount failed");
+        }
+        if (bytes != ctx->x_block_bytes) {
+            if (ctx->x_block) cudaFree(ctx->x_block);
+            ck(cudaMalloc(&ctx->x_block, bytes), "cudaMalloc");
+            ctx->x_block_bytes = bytes;
+        }
+        if (world > 1 && bytes * world != ctx->x_gathered_bytes) {
+            if (ctx->x_gathered) cudaFree(ctx->x_gathered);
+            ck(cudaMalloc(&ctx->x_gathered, bytes * world), "cudaMalloc");
+            ctx->x_gathered_bytes = bytes * world;
+        }
+        unsigned char* b = ctx->x_block;
+        launch_drain(ctx->St, ctx->n_envs, cap, reinterpret_cast<int*>(b), b + off_failed,
+                     reinterpret_cast<int*>(b + off_counts), s);
+        ck(cudaMemcpyAsync(b + off_stats, stats_in, 8 * 7, cudaMemcpyDeviceToDevice, s), "stats");
+        const size_t need = static_cast<size_t>(obs_moments_chunks(ctx->n_envs)) * D * 2;
+        if (need > ctx->mom_cap) {
+            ctx->mom_part = ctx->dalloc<double>(need);
+            ctx->mom_cap = need;
+        }
+        launch_obs_moments(obs, ctx->n_envs, static_cast<int>(D), ctx->mom_part, reinterpret_cast<double*>(b + off_mom),
+                           s);
+        unsigned char* g = b;
+        if (world > 1) {
+            if (nccl_api().all_gather(b, ctx->x_gathered, bytes, ncclUint8, static_cast<ncclComm_t>(nccl_comm), s) !=
+                ncclSuccess)
+                throw CudaFail("iteration_exchange: ncclAllGather failed");
+            g = ctx->x_gathered;
+        }
+        // identical rank-ordered merge on every rank: outcomes (global env order =
+        // rank order, then env, then time) into the replicated sampler, stats and
+        // observation moments folded in rank order
+        ck(cudaMemcpyAsync(ctx->global_ema, ctx->St.ema, sizeof(double) * ctx->M.bins, cudaMemcpyDeviceToDevice, s),
+           "ema");
+        for (int r = 0; r < world; ++r) {
+            const unsigned char* br = g + r * bytes;
+            launch_merge_block(ctx->M, reinterpret_cast<const int*>(br), br + off_failed,
+                               reinterpret_cast<const int*>(br + off_counts), static_cast<long long>(E), cap,
+                               ctx->global_ema, s);
+        }
+        launch_broadcast_ema(ctx->St, ctx->n_envs, ctx->M.bins, ctx->global_ema, s);
+        launch_exchange_fold(g, bytes, world, off_stats, off_mom, static_cast<int>(D), norm_state, stats_out, s);
+        ctx->count(5 + world);
         ctx->check_launch();
     });
 }

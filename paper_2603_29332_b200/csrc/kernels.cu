@@ -1554,6 +1554,67 @@ void launch_merge(const DevModel& M, const DevState& St, int n_local, const int*
     broadcast_ema_kernel<<<(tot + 255) / 256, 256, 0, s>>>(St, n_local, M.bins, global_ema);
 }
 
+// One rank's outcome block into the running global EMA (no broadcast): the
+// per-rank form of launch_merge for blocks gathered rank by rank.
+void launch_merge_block(const DevModel& M, const int* bins, const uint8_t* failed, const int* counts, long long n,
+                        int cap, double* global_ema, cudaStream_t s) {
+    merge_kernel<<<1, kMergeThreads, 0, s>>>(M, bins, failed, counts, n, cap, global_ema);
+}
+
+// Rank-ordered iteration merge of the gathered blocks' statistics and
+// observation moments (dist.py merged_iteration, RunningNorm::update
+// nn.cpp:246-270), with the same IEEE operation order as the torch path (no
+// contraction): stats_out[k] = sum over ranks in order; norm = (count, mean[D],
+// var[D]) folded rank by rank.  One block; threads over D.
+__global__ void exchange_fold_kernel(const unsigned char* gathered, size_t block_bytes, int world, size_t off_stats,
+                                     size_t off_mom, int D, double* norm, double* stats_out) {
+    if (stats_out && threadIdx.x < 7) {
+        double acc = 0.0;
+        for (int r = 0; r < world; ++r)
+            acc = __dadd_rn(acc, reinterpret_cast<const double*>(gathered + r * block_bytes + off_stats)[threadIdx.x]);
+        stats_out[threadIdx.x] = acc;
+    }
+    __shared__ double c0;
+    if (threadIdx.x == 0) c0 = norm[0];
+    __syncthreads();  // everyone has the pre-fold count before norm[0] is rewritten
+    const double count0 = c0;
+    if (threadIdx.x == 0) {  // the folded count (the same for every column)
+        double count = count0;
+        for (int r = 0; r < world; ++r) {
+            const double n = reinterpret_cast<const double*>(gathered + r * block_bytes + off_mom)[0];
+            if (n != 0.0) count = __dadd_rn(count, n);
+        }
+        norm[0] = count;
+    }
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        double count = count0, mean = norm[1 + d], var = norm[1 + D + d];
+        for (int r = 0; r < world; ++r) {
+            const double* m = reinterpret_cast<const double*>(gathered + r * block_bytes + off_mom);
+            const double n = m[0], bmean = m[1 + d], bvar = m[1 + D + d];
+            if (n == 0.0) continue;
+            const double tot = __dadd_rn(count, n);
+            if (count == 0.0) {
+                mean = bmean;
+                var = bvar;
+            } else {
+                const double delta = __dsub_rn(bmean, mean);
+                const double a = __dadd_rn(__dmul_rn(var, count), __dmul_rn(bvar, n));
+                const double b = __dmul_rn(__dmul_rn(delta, delta), __ddiv_rn(__dmul_rn(count, n), tot));
+                var = __ddiv_rn(__dadd_rn(a, b), tot);
+                mean = __dadd_rn(mean, __dmul_rn(delta, __ddiv_rn(n, tot)));
+            }
+            count = tot;
+        }
+        norm[1 + d] = mean;
+        norm[1 + D + d] = var;
+    }
+}
+
+void launch_exchange_fold(const unsigned char* gathered, size_t block_bytes, int world, size_t off_stats,
+                          size_t off_mom, int D, double* norm, double* stats_out, cudaStream_t s) {
+    exchange_fold_kernel<<<1, 1024, 0, s>>>(gathered, block_bytes, world, off_stats, off_mom, D, norm, stats_out);
+}
+
 void launch_broadcast_ema(const DevState& St, int n, int bins, const double* row, cudaStream_t s) {
     broadcast_ema_kernel<<<(n * bins + 255) / 256, 256, 0, s>>>(St, n, bins, row);
 }

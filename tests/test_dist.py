@@ -167,3 +167,63 @@ def test_device_norm_fold_matches_host_fold():
         dev = mdist.running_norm_fold_t(*dev, bm[0], bm[1:1 + d], bm[1 + d:])
         assert float(dev[0]) == host[0]
         assert np.array_equal(dev[1].numpy(), host[1]) and np.array_equal(dev[2].numpy(), host[2])
+
+
+@pytest.mark.gpu
+def test_native_iteration_exchange_matches_python_path(assets):
+    """msk_gpu_iteration_exchange (the C++-host form of the iteration boundary)
+    equals dist.iteration_exchange bit for bit: summed stats, folded observation
+    normaliser and the merged sampler; also through a 1-rank NCCL communicator."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    import paper_2603_29332_b200.dist as pkd
+    from conftest import model_paths
+
+    mp, cp = model_paths("wb700")
+    E, h = 96, 8
+    envs = [pk.EnvBatch(mp, cp, E, cfg=pk.EnvConfig(episode_horizon=3, rsi=True)) for _ in range(3)]
+    stats = [torch.zeros(pkd.N_STATS, dtype=torch.float64, device="cuda") for _ in envs]
+    obs = [torch.empty(E, envs[0].obs_dim, device="cuda") for _ in envs]
+    for g, ob in zip(envs, obs):
+        g.set_eval_mode(False)
+        g.reset(obs=ob)
+    for it in range(2):
+        for s in range(h):
+            for g, st, ob in zip(envs, stats, obs):
+                out = g.step(g.fill_excitations(3, it * h + s), obs=ob)
+                g.rollout_stats(out["flags"], st, reward=out["reward_aux"])
+                g.reset(mask=out["flags"], mask_bits=pk.FLAG_DONE)
+        torch.cuda.synchronize()
+        if it == 0:
+            norms = [pkd.init_norm_state(envs[0].obs_dim, "cuda") for _ in envs]
+            flat = [torch.cat([n[0].reshape(1), n[1], n[2]]) for n in norms[1:]]
+        ref_stats, norms[0], _ = pkd.iteration_exchange(envs[0], stats[0], obs[0], norms[0], cap=h)
+        s1 = envs[1].iteration_exchange(h, obs[1], stats[1], flat[0])
+        comm = C.c_void_p()
+        if it == 1:  # a one-rank NCCL communicator through the dlopen'ed NCCL
+            class UniqueId(C.Structure):  # ncclUniqueId, passed by value
+                _fields_ = [("internal", C.c_char * 128)]
+
+            nccl = C.CDLL("libnccl.so.2")
+            nccl.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, UniqueId, C.c_int]
+            uid = UniqueId()
+            assert nccl.ncclGetUniqueId(C.byref(uid)) == 0
+            assert nccl.ncclCommInitRank(C.byref(comm), 1, uid, 0) == 0
+        s2 = envs[2].iteration_exchange(h, obs[2], stats[2], flat[1], nccl_comm=comm.value)
+        torch.cuda.synchronize()
+        for so in (s1, s2):
+            assert torch.equal(so.cpu(), ref_stats.cpu())
+        ref_flat = torch.cat([norms[0][0].reshape(1), norms[0][1], norms[0][2]]).cpu()
+        for f in flat:
+            assert torch.equal(f.cpu(), ref_flat), it
+        e0 = envs[0].get_sampler().cpu()
+        for g in envs[1:]:
+            assert torch.equal(g.get_sampler().cpu(), e0)
+        for st in stats:
+            st.zero_()
+    for g in envs:
+        g.close()
