@@ -54,6 +54,18 @@ int main(int argc, char** argv) {
         msk_rollout* ro = nullptr;
         std::unique_ptr<msk::gpu::DiscTrainer> dtrain;
         double* dloss = nullptr;
+        // iteration boundary (msk_gpu_iteration_exchange; nccl_comm = nullptr: one rank)
+        double *stats = nullptr, *stats_out = nullptr, *norm = nullptr;
+        const int D = env.observation_dim();
+        cudaMalloc(&stats, 7 * sizeof(double));
+        cudaMalloc(&stats_out, 7 * sizeof(double));
+        cudaMalloc(&norm, (1 + 2 * D) * sizeof(double));
+        cudaMemset(stats, 0, 7 * sizeof(double));
+        {
+            std::vector<double> n0(1 + 2 * D, 0.0);
+            for (int i = 0; i < D; ++i) n0[1 + D + i] = 1.0;  // RunningNorm(dim): count 0, mean 0, var 1
+            cudaMemcpy(norm, n0.data(), n0.size() * sizeof(double), cudaMemcpyHostToDevice);
+        }
         float *a0 = nullptr, *logp = nullptr, *value = nullptr, *adv = nullptr, *ret = nullptr;
         const int horizon = 8;
         if (width > 0) {
@@ -88,6 +100,11 @@ int main(int argc, char** argv) {
                 env.fill_excitations(0x5EED, static_cast<uint32_t>(s), actions);
             }
             env.step(actions, out, reward);  // Env::step(action, fn): reward = r(D(Δ)) + reward_aux
+            msk_gpu_rollout_stats(env.handle(), reward, flags, stats, nullptr);
+            if ((s + 1) % horizon == 0) {  // drain, stats, obs moments, (all-gather), ordered merge
+                env.iteration_exchange(horizon, obs, stats, norm, stats_out);
+                cudaMemsetAsync(stats, 0, 7 * sizeof(double));
+            }
             if (ro) {
                 msk_rollout_record(ro, s % horizon, nullptr, a0, actions, logp, reward, flags, value, delta, nullptr);
                 if ((s + 1) % horizon == 0) {
@@ -114,11 +131,16 @@ int main(int argc, char** argv) {
         cudaMemcpy(hr.data(), reward, sizeof(float) * E, cudaMemcpyDeviceToHost);
         double rsum = 0.0;
         for (float v : hr) rsum += v;
-        double lh[3] = {0, 0, 0};
+        double lh[3] = {0, 0, 0}, so[7] = {0}, ncount = 0.0;
         if (dloss) cudaMemcpy(lh, dloss, sizeof(lh), cudaMemcpyDeviceToHost);
+        cudaMemcpy(so, stats_out, sizeof(so), cudaMemcpyDeviceToHost);
+        cudaMemcpy(&ncount, norm, sizeof(double), cudaMemcpyDeviceToHost);
         std::printf("envs=%d steps=%d policy_width=%d env-steps/s=%.0f obs_checksum=%.6e mean_reward=%.6f "
-                    "disc_loss=%.6f\n",
-                    E, steps, width, E * steps / secs, checksum, rsum / E, lh[0]);
+                    "disc_loss=%.6f last_iteration_steps=%.0f norm_count=%.0f\n",
+                    E, steps, width, E * steps / secs, checksum, rsum / E, lh[0], so[0], ncount);
+        cudaFree(stats);
+        cudaFree(stats_out);
+        cudaFree(norm);
         cudaFree(reward);
         if (dloss) cudaFree(dloss);
         if (pol) msk_policy_destroy(pol);
