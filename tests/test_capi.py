@@ -182,3 +182,14 @@ def test_minibatch_oracle_is_a_bijection():
         p = feistel_permutation(n, minibatch_key(5, 0))
         assert np.array_equal(np.sort(p), np.arange(n))
     assert not np.array_equal(feistel_permutation(500, minibatch_key(5, 0)), feistel_permutation(500, minibatch_key(5, 1)))
+
+
+def test_exchange_and_minibatch_entry_points_fail_cleanly():
+    """msk_gpu_iteration_exchange / msk_rollout_minibatch report contract errors
+    (status 1) on null contexts and bad arguments — no crash, no CPU fallback."""
+    import paper_2603_29332_b200 as pk
+
+    L = pk.lib()
+    assert L.msk_gpu_iteration_exchange(None, None, 8, None, None, None, None, None) == 1
+    assert L.msk_rollout_minibatch(None, 1, 0, 0, 8, *([None] * 8), None) == 1
+    assert b"null" in L.msk_rollout_last_error(None)
