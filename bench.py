@@ -49,17 +49,21 @@ CONFIGS = {
                             "adaptive sampler, 0.5 m termination, auto-reset), fused tracking reward "
                             "-log(1-D(delta)) (D: Mlp W=256 seed 7 on tcgen05) + ImitationPower 0.05, "
                             "allgather every 8 steps"),
+    "c2g": dict(model="wb700_general", envs=4096, eval=True, rsi=False, horizon=1000, reward_mode=0, disc=None,
+                exchange=0, desc="c2 with the generic-segment whole-body variant wb700_general: 46% of the 700 "
+                             "muscles span non-adjacent links (generic world-frame muscle path)"),
     "c5": dict(model="wb700_slow", envs=8192, eval=False, rsi=True, horizon=250, reward_mode=2, disc=None,
                exchange=8, desc="stress: wb700 with contacts, tau_act=0.05 / tau_deact=0.20 for all muscles, "
                             "training mode with mid-batch resets, allgather every 8 steps"),
 }
 CLIPS = {"wb700_fixed": "wb700_fixed_dance", "wb700": "wb700_dance", "arm2_m6": "arm2_m6_sine",
-         "walker5_m16": "walker5_m16_sine", "wb700_slow": "wb700_dance"}
+         "walker5_m16": "walker5_m16_sine", "wb700_slow": "wb700_dance", "wb700_general": "wb700_fixed_dance"}
 
 
 def ensure_assets():
     d = os.path.join(ROOT, "assets", "generated")
-    need = ["wb700_fixed.json", "wb700_fixed_dance.csv", "wb700.json", "wb700_dance.csv", "arm2_m6.json"]
+    need = ["wb700_fixed.json", "wb700_fixed_dance.csv", "wb700.json", "wb700_dance.csv", "arm2_m6.json",
+            "wb700_general.json", "wb700_slow.json"]
     if not all(os.path.exists(os.path.join(d, n)) for n in need):
         from tools.gen_assets import generate
         generate(d)
@@ -68,13 +72,6 @@ def ensure_assets():
 
 def model_files(name):
     d = ensure_assets()
-    if name == "wb700_slow" and not os.path.exists(os.path.join(d, "wb700_slow.json")):
-        with open(os.path.join(d, "wb700.json")) as f:  # C5: long activation/deactivation lag
-            m = json.load(f)
-        for mu in m["muscles"]:
-            mu["tau_act"], mu["tau_deact"] = 0.05, 0.20
-        with open(os.path.join(d, "wb700_slow.json"), "w") as f:
-            json.dump(m, f)
     return os.path.join(d, name + ".json"), os.path.join(d, CLIPS[name] + ".csv")
 
 
@@ -194,7 +191,7 @@ def run_reference(args, rank, world):
     secs, steps = b.bench(args.steps)
     v = steps / secs
     line = {"metric": "env-steps/sec (700-muscle whole-body)", "value": v, "unit": "env-steps/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Philox excitations, generated dance clip)", "impl": "reference",
             "config": {"workload": f"{args.config}: {C['desc']} (CPU sample"
@@ -228,6 +225,52 @@ def cpu_baseline_sample(args):
             "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)"}
 
 
+def self_launch(n):
+    """Re-runs this command under torch.distributed.run with n ranks on this node
+    (127.0.0.1 rendezvous); returns its exit code (rank 0 prints the JSON line)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"[bench] launching {n} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    return subprocess.run(cmd).returncode
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank plumbing on CPU (gloo), no GPU: every rank builds a
+    synthetic iteration block (outcomes of its env shard, stats, observation
+    moments), all-gathers it and applies the rank-ordered merge (dist.py, the
+    same code the GPU ranks run); rank 0 prints one JSON line with what it saw."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2603_29332_b200.dist as pkd
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    E, cap, D = 64, 8, 12
+    g = np.random.default_rng(100 + rank)
+    bins = torch.tensor(g.integers(0, 10, (E, cap)), dtype=torch.int16)
+    failed = torch.tensor(g.integers(0, 2, (E, cap)), dtype=torch.uint8)
+    counts = torch.tensor(g.integers(0, cap + 1, E), dtype=torch.int32)
+    stats = torch.tensor([float(E), 1.0 * rank, 0.0, 0.0, 0.0, 0.0, 0.0], dtype=torch.float64)
+    obs = torch.tensor(g.normal(rank, 1.0, (E, D)))
+    norm = pkd.batch_moments(obs)
+    blocks = pkd.exchange(pkd.pack_block(bins, failed, counts, stats, norm, D))
+    st, (cnt, mean, var), ema = pkd.merged_iteration(blocks, E, cap, D, (0.0, np.zeros(D), np.ones(D)),
+                                                      np.zeros(10), 0.99)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "ranks_in_exchange": len(blocks),
+                          "env_steps_merged": float(st[0]), "rank_sum": float(st[1]), "norm_count": float(cnt),
+                          "sampler_ema": [float(x) for x in ema]}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -250,6 +293,9 @@ def main():
     ap.add_argument("--disc-train", default="", choices=["", "fp32", "tf32"],
                     help="train the reward discriminator on the device once per rollout iteration (needs --rollout "
                          "and a config with D): one Adam step on the iteration's h*E Delta rows, then publish")
+    ap.add_argument("--dry-run", action="store_true", help="CPU-only check of the multi-rank exchange plumbing "
+                    "(gloo; no GPU): self-launch, all_gather and the rank-ordered merge")
+    ap.add_argument("--e2e-steps", type=int, default=0, help="timed end-to-end iterations (default max(100, steps))")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     C = dict(CONFIGS[args.config])
@@ -259,10 +305,19 @@ def main():
     if C["exchange"]:  # the first iteration boundary (allocations) falls inside the warm-up
         args.warmup = max(args.warmup, C["exchange"] + 1)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` launches its own N ranks (one process per GPU) when no
+        # launcher did: the same torchrun command line the driver uses
+        raise SystemExit(self_launch(args.gpus))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per GPU")
 
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -273,9 +328,18 @@ def main():
     import paper_2603_29332_b200 as pk
     import paper_2603_29332_b200.dist as pkd
 
+    if local >= torch.cuda.device_count():
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local} but this node has {torch.cuda.device_count()} GPUs")
     torch.cuda.set_device(local)
+    comm = None
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        t = torch.ones(1, device="cuda")
+        dist.all_reduce(t)  # communicator up: every rank contributes
+        comm = {"backend": "nccl", "nranks": dist.get_world_size(), "all_reduce_check": float(t.item())}
+        if rank == 0:
+            print(f"[bench] NCCL communicator nranks={comm['nranks']} (all_reduce of ones = {t.item():.0f})",
+                  file=sys.stderr, flush=True)
     mp, cp = model_files(args.model)
     E = args.envs
     cfg = pk.EnvConfig(episode_horizon=C["horizon"], rsi=C["rsi"])
@@ -324,12 +388,16 @@ def main():
                                  grad_penalty=10.0, max_rows=rollout.h * E, math=1 if args.disc_train == "tf32" else 0)
         ro_delta = rollout.field(7, env.delta_dim)
 
+    mom_acc = None  # observation moments of the current iteration (h x E observations)
+
     def one_step(s, ev=None):
         """One control step of the workload; ev (optional) = [start, actions, step, stats,
         exchange, reset] events recorded at the phase boundaries."""
-        nonlocal norm_state
+        nonlocal norm_state, mom_acc
         if rollout is not None:  # the observation the action is taken from
             rollout.record(s % rollout.h, obs=obs)
+        if C["exchange"]:  # the normaliser sees every observation the policy acts on (SPEC.md:480)
+            mom_acc = pkd.fold_moments(mom_acc, env.obs_moments(obs), env.obs_dim)
         if policy is not None:
             policy.sample(obs, explore=True, seed=seed, step=s, global_env_offset=rank * E, actions=actions,
                           a0=ro_a0 if rollout is not None else None, logprob=ro_lp if rollout is not None else None,
@@ -352,14 +420,15 @@ def main():
         if ev:
             ev[3].record(stream)
         if C["exchange"] and (s + 1) % C["exchange"] == 0:  # iteration boundary (h control steps)
-            _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state, cap=C["exchange"])
+            _, norm_state, _ = pkd.iteration_exchange(env, stats, obs, norm_state, cap=C["exchange"], moments=mom_acc)
             stats.zero_()
+            mom_acc = None
         if trainer is not None and (s + 1) % rollout.h == 0:  # D update on the iteration's Δ, then publish
             trainer.step(ro_delta)
             trainer.publish(env)
         if ev:
             ev[4].record(stream)
-        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=obs if policy is not None else None)
+        env.reset(mask=flags, mask_bits=pk.FLAG_DONE, obs=obs if (policy is not None or C["exchange"]) else None)
         if ev:
             ev[5].record(stream)
 
@@ -440,7 +509,7 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        k2 = max(3, args.steps // 2)
+        k2 = args.e2e_steps or max(100, args.steps)
         t0 = time.perf_counter()
         for g in range(groups):
             issue(g)
@@ -547,6 +616,7 @@ def main():
                                     / float(peaks.get("bf16_tflops", 2250.0)), bound="tensor")}
                if disc else {}),
             "gpu_launches": launches,
+            **({"comm": comm} if comm else {}),
             "phases_ms_per_step": phases,
             "clocks": summarize_clocks(clk_lines, t_loop0, t_loop1),
         }

@@ -193,21 +193,43 @@ int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream);
 int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream);
 int msk_gpu_force_state_to_reference(msk_gpu_ctx* ctx, void* stream);
 
-/* State of every env: q, dq [E x nq] (f64), act, l_m, v_m, f_m [E x n_muscles]
- * (f32), t [E] (f64), ints [E x 4] = {t_index, start_index, steps, done}.
- * Any pointer may be NULL. */
-int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float* l_m, float* v_m, float* f_m,
+/* State of every env (SimState, skeleton.hpp:27-32): q, dq [E x nq] (f64), act,
+ * v_m, f_m [E x n_muscles] (f32), l_m [E x n_muscles] (f64: the fibre length
+ * is the integrator state whose difference gives v_m, kept at the reference's
+ * precision), t [E] (f64), ints [E x 4] = {t_index, start_index, steps, done}.
+ * Muscle columns in reference order.  Any pointer may be NULL. */
+int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, double* l_m, float* v_m, float* f_m,
                       double* t, int32_t* ints, void* stream);
-int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const float* l_m,
+int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const double* l_m,
                       const float* v_m, const float* f_m, const double* t, const int32_t* ints, void* stream);
+
+/* mt19937_64 state of every env (Env::rng(), env.hpp:120; the engine state
+ * Rng::serialize writes, rng.hpp:56-68): mt [E x 312] u64 words and mti [E] the
+ * next-word index (312 = regenerate on the next draw), i.e. libstdc++'s _M_x /
+ * _M_p.  Device pointers, either nullable; set clamps mti into [0, 312].  With
+ * msk_gpu_get_state / set_state and the sampler this checkpoints a batch
+ * completely: a restored batch replays the same reset frames. */
+int msk_gpu_get_rng(msk_gpu_ctx* ctx, uint64_t* mt, int32_t* mti, void* stream);
+int msk_gpu_set_rng(msk_gpu_ctx* ctx, const uint64_t* mt, const int32_t* mti, void* stream);
 
 /* Adaptive sampler failure EMA [E x bins] (f64).  set: broadcast != 0 copies
  * one [bins] row to every env. */
 int msk_gpu_get_sampler(msk_gpu_ctx* ctx, double* ema, void* stream);
 int msk_gpu_set_sampler(msk_gpu_ctx* ctx, const double* ema, int32_t broadcast, void* stream);
-/* Pending episode outcomes: bins/failed [E x cap], counts [E]; then cleared. */
+/* Pending episode outcomes (Env::drain_episode_outcomes, env.cpp:200-204):
+ * bins/failed [E x cap], counts [E] = the number of valid slots written; then
+ * cleared.  The reference list is unbounded; here each env holds a ring of
+ * msk_gpu_set_outcome_capacity slots (default 64, grown to `cap` by a drain or
+ * exchange asking for more).  Outcomes that overflow the ring or the caller's
+ * cap are never silent: they are counted (msk_gpu_outcomes_dropped). */
 int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int32_t* counts, int32_t cap,
                            void* stream);
+/* Per-env pending-outcome ring size (>= the steps between two drains; an env
+ * ends at most one episode per step).  Pending outcomes are kept. */
+int msk_gpu_set_outcome_capacity(msk_gpu_ctx* ctx, int32_t cap, void* stream);
+/* Total outcomes lost to ring / drain-cap overflow since creation (synchronises
+ * the device).  0 in any run whose drains keep up. */
+int msk_gpu_outcomes_dropped(msk_gpu_ctx* ctx, int64_t* dropped);
 /* Each env records its own pending outcomes into its own sampler, in order. */
 int msk_gpu_record_own_outcomes(msk_gpu_ctx* ctx, void* stream);
 /* Order-fixed merge: outcome blocks of n_envs_total envs in

@@ -473,6 +473,22 @@ class OracleBatch:
     def rng_raw(self, env, n):
         return np.array([lib().om_rng_raw(C.byref(self.envs[env])) for _ in range(n)], dtype=np.uint64)
 
+    def get_rng(self):
+        """(mt [E x 312] uint64, mti [E] int32) of every env (rng.hpp:71 engine state)."""
+        mt = np.array([np.ctypeslib.as_array(env.mt) for env in self.envs], dtype=np.uint64)
+        return mt, np.array([env.mti for env in self.envs], dtype=np.int32)
+
+    def set_rng(self, mt, mti):
+        for e, env in enumerate(self.envs):
+            for i in range(312):
+                env.mt[i] = int(mt[e, i])
+            env.mti = int(mti[e])
+
+    def rng_serialize(self, env):
+        """Rng::serialize() text (rng.hpp:56-61): 312 words, index, have_spare 0, spare 0."""
+        mt, mti = self.get_rng()
+        return " ".join(str(int(w)) for w in mt[env]) + f" {int(mti[env])} 0 0"
+
 
 def excitations(seed, step, n_envs, nm, global_env_offset=0):
     L = lib()

@@ -95,6 +95,9 @@ def ref_lib():
         lib.ref_record_own_outcomes.argtypes = [C.c_void_p]
         lib.ref_drain_outcomes.argtypes = [C.c_void_p, _ip, _up, _ip, C.c_int32]
         lib.ref_rng_raw.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
+        lib.ref_rng_serialize.restype = C.c_int32
+        lib.ref_rng_serialize.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32]
+        lib.ref_rng_deserialize.argtypes = [C.c_void_p, C.c_int32, C.c_char_p]
         lib.ref_excitations.argtypes = [C.c_uint64, C.c_uint32, C.c_int64, C.c_int32, C.c_int32, _dp]
         lib.ref_rng_uniform.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int64, _dp]
         lib.ref_bench.restype = C.c_double
@@ -245,6 +248,16 @@ class RefBatch:
         out = np.zeros(n, dtype=np.uint64)
         self.lib.ref_rng_raw(self.h, env, n, out.ctypes.data_as(C.POINTER(C.c_uint64)))
         return out
+
+    def rng_serialize(self, env):
+        """The reference's own Rng::serialize() of env `env` (rng.hpp:56-61)."""
+        buf = C.create_string_buffer(16384)
+        n = self.lib.ref_rng_serialize(self.h, int(env), buf, len(buf))
+        assert n < len(buf)
+        return buf.value.decode()
+
+    def rng_deserialize(self, env, text):
+        self.lib.ref_rng_deserialize(self.h, int(env), text.encode())
 
     def bench(self, steps, action_seed=0x5EED):
         n = C.c_int64(0)

@@ -376,6 +376,21 @@ void ref_drain_outcomes(void* h, int32_t* bins, uint8_t* failed, int32_t* counts
     }
 }
 
+// Env e's Rng::serialize() text (rng.hpp:56-61) into buf; returns its length
+// (or the needed length when len is too small).
+int32_t ref_rng_serialize(void* h, int32_t e, char* buf, int32_t len) {
+    Batch& b = *static_cast<Batch*>(h);
+    const std::string s = b.envs[static_cast<size_t>(e)]->rng().serialize();
+    if (static_cast<int32_t>(s.size()) < len) std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int32_t>(s.size());
+}
+
+// Rng::deserialize (rng.hpp:63-68) of env e from text.
+void ref_rng_deserialize(void* h, int32_t e, const char* text) {
+    Batch& b = *static_cast<Batch*>(h);
+    b.envs[static_cast<size_t>(e)]->rng().deserialize(text);
+}
+
 // Raw mt19937_64 draws of env e's stream (advances it).
 void ref_rng_raw(void* h, int32_t e, int32_t n, uint64_t* out) {
     Batch& b = *static_cast<Batch*>(h);

@@ -71,6 +71,9 @@ class Policy:
     def set_norm(self, mean, var, count):
         import numpy as np
 
+        if mean is None or var is None or count == 0:  # RunningNorm with count 0: identity
+            self._ck(lib().msk_policy_set_norm(self.h, None, None, 0.0))
+            return
         m = np.ascontiguousarray(mean, dtype=np.float64)
         v = np.ascontiguousarray(var, dtype=np.float64)
         self._ck(lib().msk_policy_set_norm(self.h, m.ctypes.data, v.ctypes.data, float(count)))
@@ -383,6 +386,10 @@ def lib():
         L.msk_gpu_record_own_outcomes.argtypes = [_vp, _vp]
         L.msk_gpu_merge_outcomes.argtypes = [_vp, _vp, _vp, _vp, C.c_int64, C.c_int32, _vp]
         L.msk_gpu_rng_raw.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp]
+        L.msk_gpu_get_rng.argtypes = [_vp, _vp, _vp, _vp]
+        L.msk_gpu_set_rng.argtypes = [_vp, _vp, _vp, _vp]
+        L.msk_gpu_set_outcome_capacity.argtypes = [_vp, C.c_int32, _vp]
+        L.msk_gpu_outcomes_dropped.argtypes = [_vp, C.POINTER(C.c_int64)]
         L.msk_gpu_fill_excitations.argtypes = [_vp, C.c_uint64, C.c_uint32, _vp, _vp]
         L.msk_gpu_launch_count.restype = C.c_int64
         L.msk_disc_trainer_create.argtypes = [C.c_int32, C.c_int32, _vp, C.c_int64, C.c_double, C.c_double,
@@ -400,7 +407,8 @@ def lib():
                      "msk_gpu_tracking_error", "msk_gpu_force_state_to_reference", "msk_gpu_get_state",
                      "msk_gpu_set_state", "msk_gpu_get_sampler", "msk_gpu_set_sampler", "msk_gpu_drain_outcomes",
                      "msk_gpu_record_own_outcomes", "msk_gpu_merge_outcomes", "msk_gpu_rng_raw",
-                     "msk_gpu_fill_excitations"):
+                     "msk_gpu_fill_excitations", "msk_gpu_get_rng", "msk_gpu_set_rng",
+                     "msk_gpu_set_outcome_capacity", "msk_gpu_outcomes_dropped"):
             getattr(L, name).restype = C.c_int
         _LIB = L
     return _LIB
@@ -585,7 +593,8 @@ class EnvBatch:
         torch = self.torch
         n, nq, nm = self.n, self.nq, self.nm
         s = dict(q=self._empty(n, nq, dtype=torch.float64), dq=self._empty(n, nq, dtype=torch.float64),
-                 act=self._empty(n, nm), l_m=self._empty(n, nm), v_m=self._empty(n, nm), f_m=self._empty(n, nm),
+                 act=self._empty(n, nm), l_m=self._empty(n, nm, dtype=torch.float64), v_m=self._empty(n, nm),
+                 f_m=self._empty(n, nm),
                  t=self._empty(n, dtype=torch.float64), ints=self._empty(n, 4, dtype=torch.int32))
         self._ck(lib().msk_gpu_get_state(self.h, *[_p(s[k]) for k in ("q", "dq", "act", "l_m", "v_m", "f_m", "t",
                                                                       "ints")], self._s(stream)))
@@ -599,7 +608,7 @@ class EnvBatch:
                 return None
             return torch.as_tensor(s[k], dtype=dt, device=self.device).contiguous()
 
-        t = [cv("q", torch.float64), cv("dq", torch.float64), cv("act", torch.float32), cv("l_m", torch.float32),
+        t = [cv("q", torch.float64), cv("dq", torch.float64), cv("act", torch.float32), cv("l_m", torch.float64),
              cv("v_m", torch.float32), cv("f_m", torch.float32), cv("t", torch.float64), cv("ints", torch.int32)]
         self._ck(lib().msk_gpu_set_state(self.h, *[_p(x) for x in t], self._s(stream)))
         self._keep = t
@@ -657,6 +666,37 @@ class EnvBatch:
                                                   _p(obs.contiguous()), _p(stats), _p(norm), _p(stats_out),
                                                   self._s(stream)))
         return stats_out
+
+    def get_rng(self, stream=None):
+        """(mt [E x 312] int64 (u64 bits), mti [E] int32): every env's mt19937_64 engine state."""
+        torch = self.torch
+        mt = self._empty(self.n, 312, dtype=torch.int64)
+        mti = self._empty(self.n, dtype=torch.int32)
+        self._ck(lib().msk_gpu_get_rng(self.h, _p(mt), _p(mti), self._s(stream)))
+        return mt, mti
+
+    def set_rng(self, mt, mti, stream=None):
+        torch = self.torch
+        a = torch.as_tensor(mt, device=self.device).view(torch.int64).contiguous() if mt is not None else None
+        b = torch.as_tensor(mti, dtype=torch.int32, device=self.device).contiguous() if mti is not None else None
+        self._ck(lib().msk_gpu_set_rng(self.h, _p(a), _p(b), self._s(stream)))
+        self._keep = (a, b)
+
+    def rng_serialize(self, env, stream=None):
+        """Env e's engine state in the reference's Rng::serialize text (rng.hpp:56-61):
+        the 312 state words, the word index, have_spare (0: Env draws no normals), spare."""
+        mt, mti = self.get_rng(stream)
+        self.torch.cuda.synchronize(self.device)
+        words = mt[env].cpu().numpy().view("uint64")
+        return " ".join(str(int(w)) for w in words) + f" {int(mti[env])} 0 0"
+
+    def set_outcome_capacity(self, cap, stream=None):
+        self._ck(lib().msk_gpu_set_outcome_capacity(self.h, int(cap), self._s(stream)))
+
+    def outcomes_dropped(self):
+        v = C.c_int64(0)
+        self._ck(lib().msk_gpu_outcomes_dropped(self.h, C.byref(v)))
+        return int(v.value)
 
     def rng_raw(self, env, n, stream=None):
         out = self._empty(n, dtype=self.torch.int64)  # raw u64 bits; view as uint64 on the host

@@ -33,9 +33,11 @@ void launch_merge(const DevModel&, const DevState&, int n_local, const int* bins
                   const int* counts, long long n_total, int cap, double* global_ema, cudaStream_t);
 void launch_broadcast_ema(const DevState&, int n, int bins, const double* row, cudaStream_t);
 void launch_drain(const DevState&, int n, int cap, int* bins, uint8_t* failed, int* counts, cudaStream_t);
+void launch_set_mti(const DevState&, int n, const int* mti, cudaStream_t);
 void launch_get_ints(const DevState&, int n, int* ints, cudaStream_t);
 void launch_set_ints(const DevState&, int n, const int* ints, cudaStream_t);
 void launch_permute_muscles(const DevModel&, int n, const float* src, float* dst, int to_internal, cudaStream_t);
+void launch_permute_muscles(const DevModel&, int n, const double* src, double* dst, int to_internal, cudaStream_t);
 void launch_rollout_stats(const DevState&, int n, const float* reward, const uint8_t* flags, double* stats,
                           cudaStream_t);
 int obs_moments_chunks(int n);
@@ -106,6 +108,8 @@ struct msk_gpu_ctx {
     unsigned char* x_block = nullptr;
     unsigned char* x_gathered = nullptr;
     size_t x_block_bytes = 0, x_gathered_bytes = 0;
+    void* x_hdr = nullptr;  // layout header all-gather (multi-rank)
+    int x_checked_cap = -1;
     float* r_delta = nullptr;  // scratch when the caller passes no Δ / reward_aux / flags
     float* r_raux = nullptr;
     uint8_t* r_flags = nullptr;
@@ -152,6 +156,38 @@ int guarded(msk_gpu_ctx* ctx, F&& f) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+constexpr int kDefaultOutCap = 64;
+
+// Zeroed device buffer owned outside ctx->allocs (resizable tables).
+void* raw_alloc(size_t bytes) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, std::max<size_t>(1, bytes)), "cudaMalloc");
+    ck(cudaMemset(p, 0, std::max<size_t>(1, bytes)), "cudaMemset");
+    return p;
+}
+
+// Grow the per-env pending-outcome ring to `cap` slots (never shrinks): the
+// pending entries move with a pitched copy on `s`, after which the old ring is
+// released (the host waits for s once; resizing is rare).
+void grow_outcome_ring(msk_gpu_ctx* ctx, int cap, cudaStream_t s) {
+    DevState& S = ctx->St;
+    if (cap <= S.out_cap) return;
+    const size_t E = ctx->n_envs;
+    int* nb = static_cast<int*>(raw_alloc(E * cap * sizeof(int)));
+    uint8_t* nf = static_cast<uint8_t*>(raw_alloc(E * cap));
+    ck(cudaMemcpy2DAsync(nb, cap * sizeof(int), S.out_bin, S.out_cap * sizeof(int), S.out_cap * sizeof(int), E,
+                         cudaMemcpyDeviceToDevice, s),
+       "grow outcome ring");
+    ck(cudaMemcpy2DAsync(nf, cap, S.out_failed, S.out_cap, S.out_cap, E, cudaMemcpyDeviceToDevice, s),
+       "grow outcome ring");
+    ck(cudaStreamSynchronize(s), "grow outcome ring");
+    cudaFree(S.out_bin);
+    cudaFree(S.out_failed);
+    S.out_bin = nb;
+    S.out_failed = nf;
+    S.out_cap = cap;
+}
+
 int align16(int x) { return (x + 15) & ~15; }
 
 }  // namespace
@@ -167,8 +203,10 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
     try {
         if (n_envs < 1) throw ConfigError("msk_gpu_create: n_envs must be >= 1");
         if (!model_json_path || !clip_csv_path) throw ConfigError("msk_gpu_create: model and clip paths required");
+        // load_model does not call ModelSpec::validate (model.cpp:198-204) and neither does
+        // Env::Env (env.cpp:74-87): only the structure the device tables need is enforced
         const ModelSpec spec = load_model(model_json_path);
-        const auto errs = spec.validate();
+        const auto errs = spec.device_envelope();
         if (!errs.empty()) throw ConfigError("model '" + std::string(model_json_path) + "': " + errs.front());
         const Clip clip = load_clip(clip_csv_path, spec);
         msk_env_config ec{250, 1, 10, 0, 0.2, 0.99, 0.5, 0.01};
@@ -269,6 +307,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.child_start = ctx->upload(c.child_start);
         M.child_list = ctx->upload(c.child_list);
         M.sphere_start = ctx->upload(c.sphere_start);
+        M.sphere_link = ctx->upload(c.sphere_link);
         M.joint_damping = ctx->upload(c.joint_damping);
         M.joint_lo = ctx->upload(c.joint_lo);
         M.joint_hi = ctx->upload(c.joint_hi);
@@ -316,6 +355,10 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         off = align16(off + 16);
         M.off_union = off;
         off = align16(off + 4 * std::max({c.n_pairs + 1, kLinkStride * c.nl, 2 * c.nq}));  // +1: dummy slot
+        M.off_kind = off;  // f64 link frames, only for models with general muscle segments
+        if (c.has_general) off = align16(off + 32 * c.nl);
+        M.off_pen = off;  // contact-sphere penetrations
+        off = align16(off + 4 * c.ns);
         M.smem_env_bytes = off;
         {  // block-shared tree table: link {anchor, com, mass}, inertia, packed meta,
            // child lists and the depth-level schedule (u8 indices, n_links <= 255)
@@ -386,7 +429,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         S.q = ctx->dalloc<double>(E * c.nq);
         S.dq = ctx->dalloc<double>(E * c.nq);
         S.act = ctx->dalloc<float>(E * c.nm);
-        S.lm = ctx->dalloc<float>(E * c.nm);
+        S.lm = ctx->dalloc<double>(E * c.nm);
         S.vm = ctx->dalloc<float>(E * c.nm);
         S.fm = ctx->dalloc<float>(E * c.nm);
         S.t = ctx->dalloc<double>(E);
@@ -397,11 +440,17 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         S.mt = ctx->dalloc<uint64_t>(E * 312);
         S.mti = ctx->dalloc<int>(E);
         S.ema = ctx->dalloc<double>(E * M.bins);
-        S.out_cap = 64;
-        S.out_bin = ctx->dalloc<int>(E * S.out_cap);
-        S.out_failed = ctx->dalloc<uint8_t>(E * S.out_cap);
+        // pending-outcome ring: kDefaultOutCap slots per env (an env ends at most one
+        // episode per step); grown on demand by drain / exchange with a larger cap or
+        // by msk_gpu_set_outcome_capacity; outcomes past it are counted in out_dropped
+        S.out_cap = kDefaultOutCap;
+        S.out_bin = static_cast<int*>(raw_alloc(E * S.out_cap * sizeof(int)));
+        S.out_failed = static_cast<uint8_t*>(raw_alloc(E * S.out_cap));
         S.out_count = ctx->dalloc<int>(E);
+        S.out_dropped = ctx->dalloc<unsigned long long>(1);
         S.power_scratch = rw.mode == 2 ? ctx->dalloc<float>(E * c.nm) : nullptr;
+        S.u = ctx->dalloc<float>(E * c.nm);
+        S.u_bad = ctx->dalloc<uint8_t>(E);
         ctx->global_ema = ctx->dalloc<double>(M.bins);
         ctx->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
         // obs-moment partials for a whole batch, allocated up front (no allocation,
@@ -433,7 +482,10 @@ void msk_gpu_destroy(msk_gpu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->x_block) cudaFree(ctx->x_block);
+    if (ctx->St.out_bin) cudaFree(ctx->St.out_bin);
+    if (ctx->St.out_failed) cudaFree(ctx->St.out_failed);
     if (ctx->x_gathered) cudaFree(ctx->x_gathered);
+    if (ctx->x_hdr) cudaFree(ctx->x_hdr);
     for (void* p : ctx->allocs) cudaFree(p);
     for (void* p : ctx->disc_allocs) cudaFree(p);
     for (auto& s : ctx->hs)
@@ -493,7 +545,7 @@ int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delt
         if (!actions) throw ConfigError("step: actions is null");
         launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, obs, delta, reward_aux, flags, muscle_power,
                     contact_force, as_stream(stream));
-        ctx->count();
+        ctx->count(2);  // prep_actions + step
         ctx->check_launch();
     });
 }
@@ -602,7 +654,7 @@ int msk_gpu_step_rewarded(msk_gpu_ctx* ctx, const float* actions, float* obs, fl
         uint8_t* f = flags ? flags : ctx->r_flags;
         cudaStream_t s = as_stream(stream);
         launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, obs, d, ra, f, muscle_power, contact_force, s);
-        ctx->count();
+        ctx->count(2);  // prep_actions + step
         ctx->check_launch();
         // D(Δ) on the tensor cores, launched as a programmatic dependent of the step
         ck(launch_disc(ctx->disc, d, ctx->delta_dim, ctx->n_envs, ra, f, reward, s, true), "launch discriminator");
@@ -647,7 +699,7 @@ void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host
         launch_step(ctx->M, ctx->St, static_cast<int>(e0), static_cast<int>(n), ctx->h_actions + e0 * nm,
                     ctx->h_obs + e0 * ctx->obs_dim, ctx->h_delta + e0 * ctx->delta_dim, ctx->h_raux + e0,
                     ctx->h_flags + e0, nullptr, nullptr, s);
-        ctx->count();
+        ctx->count(2);  // prep_actions + step
         ctx->check_launch();
         if (reward_host) {
             ck(launch_disc(ctx->disc, ctx->h_delta + e0 * ctx->delta_dim, ctx->delta_dim, static_cast<int>(n),
@@ -749,7 +801,7 @@ int msk_gpu_force_state_to_reference(msk_gpu_ctx* ctx, void* stream) {
     });
 }
 
-int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float* l_m, float* v_m, float* f_m,
+int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, double* l_m, float* v_m, float* f_m,
                       double* t, int32_t* ints, void* stream) {
     return guarded(ctx, [&] {
         const size_t E = ctx->n_envs, nq = ctx->cm.nq;
@@ -760,13 +812,17 @@ int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float
         cp(q, ctx->St.q, E * nq * 8);
         cp(dq, ctx->St.dq, E * nq * 8);
         // muscle rows: internal (segment-count) order -> reference order
-        for (auto [dst, src] : {std::pair<float*, const float*>{act, ctx->St.act}, {l_m, ctx->St.lm},
-                                {v_m, ctx->St.vm}, {f_m, ctx->St.fm}})
+        for (auto [dst, src] : {std::pair<float*, const float*>{act, ctx->St.act}, {v_m, ctx->St.vm}, {f_m, ctx->St.fm}})
             if (dst) {
                 launch_permute_muscles(ctx->M, ctx->n_envs, src, dst, 0, s);
                 ctx->count();
                 ctx->check_launch();
             }
+        if (l_m) {
+            launch_permute_muscles(ctx->M, ctx->n_envs, ctx->St.lm, l_m, 0, s);
+            ctx->count();
+            ctx->check_launch();
+        }
         cp(t, ctx->St.t, E * 8);
         if (ints) {
             launch_get_ints(ctx->St, ctx->n_envs, ints, s);
@@ -776,7 +832,7 @@ int msk_gpu_get_state(msk_gpu_ctx* ctx, double* q, double* dq, float* act, float
     });
 }
 
-int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const float* l_m,
+int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const float* act, const double* l_m,
                       const float* v_m, const float* f_m, const double* t, const int32_t* ints, void* stream) {
     return guarded(ctx, [&] {
         const size_t E = ctx->n_envs, nq = ctx->cm.nq;
@@ -786,13 +842,17 @@ int msk_gpu_set_state(msk_gpu_ctx* ctx, const double* q, const double* dq, const
         };
         cp(ctx->St.q, q, E * nq * 8);
         cp(ctx->St.dq, dq, E * nq * 8);
-        for (auto [dst, src] : {std::pair<float*, const float*>{ctx->St.act, act}, {ctx->St.lm, l_m},
-                                {ctx->St.vm, v_m}, {ctx->St.fm, f_m}})
+        for (auto [dst, src] : {std::pair<float*, const float*>{ctx->St.act, act}, {ctx->St.vm, v_m}, {ctx->St.fm, f_m}})
             if (src) {
                 launch_permute_muscles(ctx->M, ctx->n_envs, src, dst, 1, s);
                 ctx->count();
                 ctx->check_launch();
             }
+        if (l_m) {
+            launch_permute_muscles(ctx->M, ctx->n_envs, l_m, ctx->St.lm, 1, s);
+            ctx->count();
+            ctx->check_launch();
+        }
         cp(ctx->St.t, t, E * 8);
         if (ints) {
             launch_set_ints(ctx->St, ctx->n_envs, ints, s);
@@ -828,6 +888,7 @@ int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int
                            void* stream) {
     return guarded(ctx, [&] {
         if (!bins || !failed || !counts || cap < 0) throw ConfigError("drain_outcomes: bad arguments");
+        grow_outcome_ring(ctx, cap, as_stream(stream));  // sized for the caller's next drain
         launch_drain(ctx->St, ctx->n_envs, cap, bins, failed, counts, as_stream(stream));
         ctx->count();
         ctx->check_launch();
@@ -926,6 +987,34 @@ int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, c
             if (nccl_api().count(static_cast<ncclComm_t>(nccl_comm), &world) != ncclSuccess)
                 throw CudaFail("iteration_exchange: ncclCommCount failed");
         }
+        if (world > 1 && cap != ctx->x_checked_cap) {
+            // every rank must build the same block layout, or ncclAllGather would hang or
+            // mix ranks' data: all-gather a fixed 32-B header {E, cap, D, bytes} first
+            // (once per cap; E and D are fixed per context) and fail on any mismatch
+            const int64_t hdr[4] = {static_cast<int64_t>(E), cap, static_cast<int64_t>(D),
+                                    static_cast<int64_t>(bytes)};
+            if (ctx->x_hdr) cudaFree(ctx->x_hdr);
+            ctx->x_hdr = nullptr;
+            ck(cudaMalloc(&ctx->x_hdr, 32 * (1 + static_cast<size_t>(world))), "cudaMalloc");
+            ck(cudaMemcpyAsync(ctx->x_hdr, hdr, 32, cudaMemcpyHostToDevice, s), "exchange header");
+            if (nccl_api().all_gather(ctx->x_hdr, static_cast<unsigned char*>(ctx->x_hdr) + 32, 32, ncclUint8,
+                                      static_cast<ncclComm_t>(nccl_comm), s) != ncclSuccess)
+                throw CudaFail("iteration_exchange: ncclAllGather (header) failed");
+            std::vector<int64_t> all(4 * static_cast<size_t>(world));
+            ck(cudaMemcpyAsync(all.data(), static_cast<unsigned char*>(ctx->x_hdr) + 32, 32 * world,
+                               cudaMemcpyDeviceToHost, s),
+               "exchange header");
+            ck(cudaStreamSynchronize(s), "exchange header");
+            for (int r = 0; r < world; ++r)
+                if (!std::equal(hdr, hdr + 4, all.data() + 4 * r))
+                    throw ConfigError("iteration_exchange: rank " + std::to_string(r) + " has {envs " +
+                                      std::to_string(all[4 * r]) + ", cap " + std::to_string(all[4 * r + 1]) +
+                                      ", obs_dim " + std::to_string(all[4 * r + 2]) + "}, this rank {" +
+                                      std::to_string(E) + ", " + std::to_string(cap) + ", " + std::to_string(D) +
+                                      "}: every rank must exchange the same block layout");
+            ctx->x_checked_cap = cap;
+        }
+        grow_outcome_ring(ctx, cap, s);
         if (bytes != ctx->x_block_bytes) {
             if (ctx->x_block) cudaFree(ctx->x_block);
             ck(cudaMalloc(&ctx->x_block, bytes), "cudaMalloc");
@@ -969,6 +1058,45 @@ int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, c
         launch_exchange_fold(g, bytes, world, off_stats, off_mom, static_cast<int>(D), norm_state, stats_out, s);
         ctx->count(5 + world);
         ctx->check_launch();
+    });
+}
+
+int msk_gpu_get_rng(msk_gpu_ctx* ctx, uint64_t* mt, int32_t* mti, void* stream) {
+    return guarded(ctx, [&] {
+        const size_t E = ctx->n_envs;
+        cudaStream_t s = as_stream(stream);
+        if (mt) ck(cudaMemcpyAsync(mt, ctx->St.mt, E * 312 * 8, cudaMemcpyDeviceToDevice, s), "get_rng");
+        if (mti) ck(cudaMemcpyAsync(mti, ctx->St.mti, E * 4, cudaMemcpyDeviceToDevice, s), "get_rng");
+    });
+}
+
+int msk_gpu_set_rng(msk_gpu_ctx* ctx, const uint64_t* mt, const int32_t* mti, void* stream) {
+    return guarded(ctx, [&] {
+        const size_t E = ctx->n_envs;
+        cudaStream_t s = as_stream(stream);
+        if (mt) ck(cudaMemcpyAsync(ctx->St.mt, mt, E * 312 * 8, cudaMemcpyDeviceToDevice, s), "set_rng");
+        if (mti) {
+            launch_set_mti(ctx->St, ctx->n_envs, mti, s);  // clamps the index into [0, 312]
+            ctx->count();
+            ctx->check_launch();
+        }
+    });
+}
+
+int msk_gpu_set_outcome_capacity(msk_gpu_ctx* ctx, int32_t cap, void* stream) {
+    return guarded(ctx, [&] {
+        if (cap < 1 || cap > (1 << 20)) throw ConfigError("set_outcome_capacity: cap must be in [1, 2^20]");
+        grow_outcome_ring(ctx, cap, as_stream(stream));
+    });
+}
+
+int msk_gpu_outcomes_dropped(msk_gpu_ctx* ctx, int64_t* dropped) {
+    return guarded(ctx, [&] {
+        if (!dropped) throw ConfigError("outcomes_dropped: null argument");
+        unsigned long long v = 0;
+        ck(cudaDeviceSynchronize(), "outcomes_dropped");
+        ck(cudaMemcpy(&v, ctx->St.out_dropped, sizeof v, cudaMemcpyDeviceToHost), "outcomes_dropped");
+        *dropped = static_cast<int64_t>(v);
     });
 }
 

@@ -40,6 +40,7 @@ struct DevModel {
     const int* child_list;
     const int* sphere_start;
     const float4* sphere;  // {x, z, radius, 0}
+    const int* sphere_link;
     // joints
     const float* joint_damping;
     const double* joint_lo;
@@ -78,7 +79,7 @@ struct DevModel {
     float w_emg, w_power;
     const int* emg_map;
     // per-env smem layout (bytes from the warp's base)
-    int smem_env_bytes, off_relcs, off_dqf, off_tau, off_root, off_union;
+    int smem_env_bytes, off_relcs, off_dqf, off_tau, off_root, off_union, off_kind, off_pen;
     int epb;  // envs per block actually used (<= the compiled warps x envs-per-warp; fewer for big models)
     // block-shared tree table at the head of dynamic smem (bytes)
     const int4* tab_blob;
@@ -90,7 +91,7 @@ struct DevState {
     double* q;        // E x nq
     double* dq;       // E x nq
     float* act;       // E x nm
-    float* lm;        // E x nm
+    double* lm;       // E x nm (f64: prev_len = slack + l_m l_opt feeds the v_m difference)
     float* vm;        // E x nm
     float* fm;        // E x nm
     double* t;        // E
@@ -103,9 +104,12 @@ struct DevState {
     double* ema;      // E x bins
     int* out_bin;     // E x out_cap
     uint8_t* out_failed;
-    int* out_count;   // E
+    int* out_count;   // E (pending outcomes, may exceed out_cap: the excess is dropped and counted)
     int out_cap;
+    unsigned long long* out_dropped;  // [1] outcomes lost to ring / drain-cap overflow (never silent)
     float* power_scratch;  // E x nm (reward mode 2 without a caller buffer)
+    float* u;              // E x nm: the step's clamped excitations, device muscle order
+    uint8_t* u_bad;        // E: the step's action row had a non-finite entry
 };
 
 }  // namespace msk_b200

@@ -62,6 +62,8 @@ struct EnvSmem {
     float* tau;      // nq: joint torque, then q̈
     float* root;     // [0] root x, [1] root z (absolute), [2] cos q2, [3] sin q2
     float* un;       // union: pair slots | kLinkStride floats per link (ABA) | f64 q
+    double2* kind;   // 2 nl (general-segment models only): f64 {cos, sin}, {origin x, z} (root-relative)
+    float* pen;      // ns: contact-sphere penetration (f64 geometry) of the substep
     // block-shared tree table (copied once per block; see CompiledModel tab_*)
     const float4* ta;      // nl: {anchor x, anchor z, com, mass}
     const float* tin;      // nl: inertia
@@ -109,6 +111,8 @@ __device__ __forceinline__ EnvSmem carve(unsigned char* smem, int slot, const De
     s.tau = reinterpret_cast<float*>(base + M.off_tau);
     s.root = reinterpret_cast<float*>(base + M.off_root);
     s.un = reinterpret_cast<float*>(base + M.off_union);
+    s.kind = reinterpret_cast<double2*>(base + M.off_kind);
+    s.pen = reinterpret_cast<float*>(base + M.off_pen);
     s.ta = reinterpret_cast<const float4*>(smem + M.tab_off_a);
     s.tin = reinterpret_cast<const float*>(smem + M.tab_off_in);
     s.tmeta = reinterpret_cast<const int*>(smem + M.tab_off_meta);
@@ -176,6 +180,19 @@ __device__ __forceinline__ float mtu_force(float act, float l, float v, float fm
     return fmax * (act * hill_fl(l) * hill_fv(v) + hill_fp(l));
 }
 
+#ifdef MSK_F64_HILL  // diagnostics build: the Hill force in f64 (muscle.cpp:9-40 arithmetic)
+__device__ __forceinline__ float mtu_force_d(float act, double l, double v, float fmax) {
+    const double d = (l - 1.0) / 0.45;
+    const double fl = exp(-d * d);
+    double fv;
+    if (v <= -1.0) fv = 0.0;
+    else if (v < 0.0) fv = (v + 1.0) / (1.0 - v / 4.0);
+    else fv = (1.4 * v + 0.32) / (v + 0.32);
+    const double fp = l > 1.0 ? (exp(4.0 * (l - 1.0)) - 1.0) / (exp(2.0) - 1.0) : 0.0;
+    return static_cast<float>(static_cast<double>(fmax) * (static_cast<double>(act) * fl * fv + fp));
+}
+#endif
+
 // sqrt of a non-negative f64 from the f32 rsqrt seed plus one f64 Newton
 // correction (~46 bits); also returns the f32 reciprocal length.  x is clamped
 // at ~1e-30 through its high word (one integer max; negative rounding noise has
@@ -189,19 +206,21 @@ __device__ __forceinline__ double sqrt_d(double x, float& inv) {
     return fma(fma(-s, s, x), 0.5 * rd, s);
 }
 
-// World (root-relative) position of a via point (general segments only).
-__device__ __forceinline__ float2 via_point(const DevModel& M, const float4* kin, int v) {
+// World (root-relative) position of a via point from the f64 frames (fk_d):
+// the general segments' lengths feed v_m = (L - prev_len) / (dt l_opt v_max), so they need the
+// reference's f64 precision like the adjacent (K-form) segments.
+__device__ __forceinline__ double2 via_point_d(const DevModel& M, const double2* kind, int v) {
     const int l = __ldg(M.via_link + v);
-    const float x = __ldg(M.via_x + v), z = __ldg(M.via_z + v);
-    if (l < 0) return make_float2(x, z);
-    const float4 k = kin[l];
-    return make_float2(fmaf(k.x, x, fmaf(-k.y, z, k.z)), fmaf(k.y, x, fmaf(k.x, z, k.w)));
+    const double x = __ldg(M.via_x + v), z = __ldg(M.via_z + v);
+    if (l < 0) return make_double2(x, z);
+    const double2 cs = kind[2 * l], o = kind[2 * l + 1];
+    return make_double2(fma(cs.x, x, fma(-cs.y, z, o.x)), fma(cs.y, x, fma(cs.x, z, o.y)));
 }
 
-__device__ __forceinline__ float general_seg_len(const DevModel& M, const EnvSmem& S, int v_end) {
-    const float2 pe = via_point(M, S.kin, v_end), ps = via_point(M, S.kin, v_end - 1);
-    const float dx = pe.x - ps.x, dz = pe.y - ps.y;
-    return sqrtf(fmaf(dx, dx, dz * dz));
+__device__ __forceinline__ double general_seg_len(const DevModel& M, const EnvSmem& S, int v_end) {
+    const double2 pe = via_point_d(M, S.kind, v_end), ps = via_point_d(M, S.kind, v_end - 1);
+    const double dx = pe.x - ps.x, dz = pe.y - ps.y;
+    return sqrt(fma(dx, dx, dz * dz));
 }
 
 // Same-link (kind 0) or adjacent (kind 1) segment from its K constants
@@ -226,29 +245,29 @@ __device__ __forceinline__ double muscle_length(const DevModel& M, const EnvSmem
         const float4 kf = __ldg(M.seg_kf + k * M.nm + m);
         const int info = __float_as_int(kf.w);
         float arm;
-        L += (info & 3) == 2 ? static_cast<double>(general_seg_len(M, S, info >> 11)) : kseg(S, kf, info, arm);
+        L += (info & 3) == 2 ? general_seg_len(M, S, info >> 11) : kseg(S, kf, info, arm);
     }
     return L;
 }
 
-// J_m^T F of the general (non-adjacent) segments of muscle m (reference index), world frame.
+// J_m^T F of the general (non-adjacent) segments of muscle m (reference index),
+// world frame (skeleton.cpp:147-170): the segment direction and the lever arm
+// about the joint from the f64 frames (fk_d), the moment rounded to f32 once.
 __device__ void general_pairs(const DevModel& M, const EnvSmem& S, int m, float F) {
     const int p0 = __ldg(M.m_pair_start + m), p1 = __ldg(M.m_pair_start + m + 1);
     for (int p = p0; p < p1; ++p) {
         const int ve = __ldg(M.pair_via + p), j = __ldg(M.pair_joint + p);
         const float sg = __ldg(M.pair_sign + p);
-        const float2 pe = via_point(M, S.kin, ve);
-        const float2 ps = via_point(M, S.kin, ve - 1);
-        const float sx = pe.x - ps.x, sz = pe.y - ps.y;
-        const float len = sqrtf(fmaf(sx, sx, sz * sz));
+        const double2 pe = via_point_d(M, S.kind, ve);
+        const double2 ps = via_point_d(M, S.kind, ve - 1);
+        const double sx = pe.x - ps.x, sz = pe.y - ps.y;
+        const double len = sqrt(fma(sx, sx, sz * sz));
         float val = 0.0f;
-        if (len > 1e-12f) {
-            const float inv = 1.0f / len;
-            const float ux = sx * inv, uz = sz * inv;
-            const float4 ka = S.kin[M.floating + j];
-            const float2 pt = sg < 0.0f ? pe : ps;
-            const float rx = pt.x - ka.z, rz = pt.y - ka.w;
-            val = sg * F * fmaf(rx, uz, -rz * ux);
+        if (len > 1e-12) {
+            const double2 ka = S.kind[2 * (M.floating + j) + 1];  // joint j's child-link origin
+            const double2 pt = sg < 0.0f ? pe : ps;
+            const double rx = pt.x - ka.x, rz = pt.y - ka.y;
+            val = static_cast<float>(static_cast<double>(sg * F) * (fma(rx, sz, -rz * sx) / len));
         }
         S.un[__ldg(M.pair_slot + p)] = val;
     }
@@ -273,12 +292,49 @@ __device__ __forceinline__ void publish_dofs(const DevModel& M, const EnvSmem& S
                 sincos(qd[k], &sn, &cs);
                 S.root[2] = static_cast<float>(cs);
                 S.root[3] = static_cast<float>(sn);
+                S.relcs[2] = make_double2(cs, sn);  // (unused root slot) f64 pitch for fk_d
             } else {
                 S.root[d] = static_cast<float>(qd[k]);
+                reinterpret_cast<double*>(S.relcs)[d] = qd[k];  // relcs[0] = f64 root (x, z)
             }
             S.dqf[d] = static_cast<float>(dqd[k]);
         }
     }
+}
+
+// f64 world height of a point given in link l's frame (skeleton.cpp:82-113):
+// walks the joint chain up to the root, p <- anchor + R(mount + q) p, each
+// joint's rotation in f64 (relcs); the floating root adds R(q2) and (q0, q1)
+// (relcs[2], relcs[0]).
+__device__ __forceinline__ double sphere_height_d(const DevModel& M, const EnvSmem& S, int l, float px, float pz) {
+    double x = px, z = pz;
+    int cur = l;
+    while (cur >= M.floating) {
+        const double2 r = S.relcs[M.nrd + cur - M.floating];
+        const float4 a = S.ta[cur];
+        const double nx = fma(r.x, x, fma(-r.y, z, static_cast<double>(a.x)));
+        z = fma(r.y, x, fma(r.x, z, static_cast<double>(a.y)));
+        x = nx;
+        cur = (S.tmeta[cur] & 0xff) - 1;
+    }
+    if (M.floating) {
+        const double2 r = S.relcs[2], o = S.relcs[0];
+        z = fma(r.y, x, fma(r.x, z, o.y));
+    }
+    return z;
+}
+
+// Penetration depth of every contact sphere from its f64 world height: the
+// contact force is discontinuous at pen = 0 when the sphere moves down
+// (f_n = -c z' there, skeleton.cpp:243-248), so the branch must be taken where
+// the reference's f64 takes it (an f32 height flips it for |pen| < ~1e-7 m).
+__device__ __forceinline__ void sphere_pen_d(const DevModel& M, const EnvSmem& S, int lane) {
+    for (int sp = lane; sp < M.ns; sp += S.G) {
+        const float4 sd = __ldg(M.sphere + sp);
+        S.pen[sp] = static_cast<float>(static_cast<double>(sd.z) - sphere_height_d(M, S, __ldg(M.sphere_link + sp),
+                                                                                      sd.x, sd.y));
+    }
+    __syncwarp(S.hm);
 }
 
 // Root-to-leaf sweep.  FK by rotation composition R_l = R_p R_joint
@@ -352,7 +408,8 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
                 for (int sp = s0; sp < s1; ++sp) {
                     const float4 sd = __ldg(M.sphere + sp);
                     const float rx = fmaf(c, sd.x, -s * sd.y), rz = fmaf(s, sd.x, c * sd.y);
-                    const float pen = sd.z - (oz + rz + (M.floating ? S.root[1] : 0.0f));
+                    // penetration from the f64 world height (sphere_pen_d)
+                    const float pen = S.pen[sp];
                     if (pen > 0.0f) {
                         const float fn = fmaxf(0.0f, fmaf(M.c_k, pen, -M.c_c * fmaf(w, rx, vz)));
                         if (fn > 0.0f) {
@@ -384,6 +441,42 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
             u2[3] = make_float2(p0, p1);
             u[8] = p2;
             u2[6] = make_float2(c1, c2);
+        }
+        __syncwarp(S.hm);
+    }
+}
+
+// f64 forward kinematics (skeleton.cpp:82-107, root-relative) into S.kind, for
+// models with general (non-adjacent) muscle segments: rotation composition
+// R_l = R_p R_joint with each joint's f64 rotation (relcs), origins
+// o_l = o_p + R_p anchor.
+__device__ __forceinline__ void fk_d(const DevModel& M, const EnvSmem& S, int lane) {
+    for (int lev = 0; lev < M.n_levels; ++lev) {
+        for (int i = lane; i < 32; i += S.G) {
+            const uint32_t ww = S.twork[32 * lev + i];
+            if (!(ww >> 31)) break;
+            const int l = ww_link(ww);
+            const int dof = link_dof(M, l);
+            double2 cs, o;
+            if (dof < 0) {  // floating root: origin 0 (root-relative), pitch q2
+                cs = S.relcs[2];
+                o = make_double2(0.0, 0.0);
+            } else {
+                const double2 r = S.relcs[dof];
+                const int p = ww_parent(ww);
+                const float4 la = S.ta[l];
+                if (p >= 0) {
+                    const double2 cp = S.kind[2 * p], op = S.kind[2 * p + 1];
+                    const double ax = la.x, az = la.y;
+                    o = make_double2(fma(cp.x, ax, fma(-cp.y, az, op.x)), fma(cp.y, ax, fma(cp.x, az, op.y)));
+                    cs = make_double2(fma(cp.x, r.x, -cp.y * r.y), fma(cp.y, r.x, cp.x * r.y));
+                } else {
+                    o = make_double2(la.x, la.y);
+                    cs = r;
+                }
+            }
+            S.kind[2 * l] = cs;
+            S.kind[2 * l + 1] = o;
         }
         __syncwarp(S.hm);
     }
@@ -457,7 +550,7 @@ __device__ void write_obs(const DevModel& M, const DevState& St, const EnvSmem& 
                 const size_t i = mb + __ldg(M.m_int + x);
                 v[j][0] = St.act[i];
                 v[j][1] = St.fm[i];
-                v[j][2] = St.lm[i];
+                v[j][2] = static_cast<float>(St.lm[i]);
                 v[j][3] = St.vm[i];
             }
         }
@@ -520,11 +613,11 @@ __device__ void init_muscles(const DevModel& M, const DevState& St, const EnvSme
     for (int m = lane; m < M.nm; m += S.G) {
         const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
         const double L = muscle_length(M, S, m);
-        const float lm = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
+        const double lm = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
         St.act[mb + m] = a0;
         St.lm[mb + m] = lm;
         St.vm[mb + m] = 0.0f;
-        St.fm[mb + m] = mtu_force(a0, lm, 0.0f, __ldg(M.m_p0 + m).x);
+        St.fm[mb + m] = mtu_force(a0, static_cast<float>(lm), 0.0f, __ldg(M.m_p0 + m).x);
     }
 }
 
@@ -591,19 +684,30 @@ __device__ int rsi_frame(const DevModel& M, const DevState& St, int e) {
 // (segments padded to NSEG, branch-free); NSEG == 0: generic path.
 // Activation, fibre kinematics and Hill force of muscle m given its path
 // length L; stores the muscle state, accumulates power, returns F.
+// l_m is f64 state: prev_len = slack + l_m l_opt must reproduce the previous
+// substep's path length to ~1e-16 (v_m divides the difference by dt l_opt v_max,
+// ~1e-3), as in the reference's f64 SimState.  v_m / f_m are stored only at the
+// last substep (nothing reads them in between).
 __device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, int m, int ext, float4 p0, double2 pa,
-                                               double2 pb, float u, float a0, float lm0, double L, float* pw) {
+                                               double2 pb, float u, float a0, double lm0, double L, float* pw,
+                                               bool last) {
     const float gain = fmaf(1.5f, a0, 0.5f);
     const float ex = ex2_ftz(u > a0 ? p0.y * rcp_ftz(gain) : p0.z * gain);  // p0.y/z carry log2(e)
     const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
-    const double prev_len = fma(static_cast<double>(lm0), pa.y, pa.x);
+    const double prev_len = fma(lm0, pa.y, pa.x);
     const float vm = static_cast<float>((L - prev_len) * pb.y);
-    const float lm1 = fmaxf(static_cast<float>((L - pa.x) * pb.x), kMinFiber);
-    const float F = mtu_force(a1, lm1, vm, p0.x);
+    const double lm1 = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
+#ifdef MSK_F64_HILL
+    const float F = mtu_force_d(a1, lm1, (L - prev_len) * pb.y, p0.x);
+#else
+    const float F = mtu_force(a1, static_cast<float>(lm1), vm, p0.x);
+#endif
     St.act[mb + m] = a1;
     St.lm[mb + m] = lm1;
-    St.vm[mb + m] = vm;
-    St.fm[mb + m] = F;
+    if (last) {
+        St.vm[mb + m] = vm;
+        St.fm[mb + m] = F;
+    }
     if (pw) pw[ext] += fabsf(F * vm * p0.w);
     return F;
 }
@@ -614,7 +718,8 @@ struct MuscleIn {
     float4 kc[NSEG];
     float4 p0;
     double2 pa, pb;
-    float u, a0, lm0;
+    float u, a0;
+    double lm0;
     int ext, nsc;
 };
 
@@ -632,20 +737,20 @@ __device__ __forceinline__ void muscle_load(const DevModel& M, const DevState& S
     x.p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
     x.pa = ldc2d(M.m_p1a + m);
     x.pb = ldc2d(M.m_p1b + m);
-    x.u = fminf(fmaxf(act_row[x.ext], 0.0f), 1.0f);
+    x.u = act_row[m];  // clamped, device order (prep_actions_kernel)
     x.a0 = St.act[mb + m];
     x.lm0 = St.lm[mb + m];
 }
 
 template <int NSEG>
 __device__ __forceinline__ void muscle_compute(const EnvSmem& S, const DevState& St, size_t mb, float* pw, int m,
-                                               const MuscleIn<NSEG>& x) {
+                                               const MuscleIn<NSEG>& x, bool last) {
     double L = 0.0;
     float tq[NSEG];
 #pragma unroll
     for (int k = 0; k < NSEG; ++k)
         if (k < x.nsc) L += kseg(S, x.kc[k], __float_as_int(x.kc[k].w), tq[k]);
-    const float F = muscle_update(St, mb, m, x.ext, x.p0, x.pa, x.pb, x.u, x.a0, x.lm0, L, pw);
+    const float F = muscle_update(St, mb, m, x.ext, x.p0, x.pa, x.pb, x.u, x.a0, x.lm0, L, pw, last);
 #pragma unroll
     for (int k = 0; k < NSEG; ++k)
         if (k < x.nsc) S.un[__float_as_int(x.kc[k].w) >> 11] = -F * tq[k];
@@ -653,13 +758,13 @@ __device__ __forceinline__ void muscle_compute(const EnvSmem& S, const DevState&
 
 template <int NSEG>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
-                                             const float* act_row, size_t mb, float* pw, int lane) {
+                                             const float* act_row, size_t mb, float* pw, int lane, bool last) {
     const int nm = M.nm;
     if constexpr (NSEG > 0) {
         for (int m = lane; m < nm; m += S.G) {
             MuscleIn<NSEG> x;
             muscle_load<NSEG>(M, St, act_row, mb, m, min(m - lane + S.G - 1, nm - 1), x);
-            muscle_compute<NSEG>(S, St, mb, pw, m, x);
+            muscle_compute<NSEG>(S, St, mb, pw, m, x, last);
         }
     } else {
         for (int m = lane; m < nm; m += S.G) {
@@ -667,17 +772,17 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
             const int nseg = meta & 0xff, ext = meta >> 9;
             const float4 p0 = __ldg(M.m_p0 + m);
             const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
-            const float u = fminf(fmaxf(act_row[ext], 0.0f), 1.0f);
+            const float u = act_row[m];
             const float a0 = St.act[mb + m];
-            const float lm0 = St.lm[mb + m];
+            const double lm0 = St.lm[mb + m];
             double L = 0.0;
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
                 const int info = __float_as_int(kf.w);
                 float arm;
-                L += (info & 3) == 2 ? static_cast<double>(general_seg_len(M, S, info >> 11)) : kseg(S, kf, info, arm);
+                L += (info & 3) == 2 ? general_seg_len(M, S, info >> 11) : kseg(S, kf, info, arm);
             }
-            const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw);
+            const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
                 const int info = __float_as_int(kf.w);
@@ -848,6 +953,29 @@ __device__ __forceinline__ double* stage_q(const DevModel& M, const EnvSmem& S, 
 }  // namespace
 
 // ============================================================================
+// Env::step's action handling (env.cpp:208-213) once per control step: the
+// non-finite check (per-env flag) and the clamp to [0, 1], written in the
+// device's muscle order so the 10 substeps read each warp's 32 excitations as
+// one coalesced 128-B line instead of gathering them from the reference-order
+// row every substep.  One warp per env: coalesced reads, row-local scatter.
+// ============================================================================
+__global__ void prep_actions_kernel(DevModel M, DevState St, int env0, int n_envs, const float* __restrict__ actions) {
+    const int le = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (le >= n_envs) return;
+    const int nm = M.nm, e = env0 + le;
+    const float* row = actions + static_cast<size_t>(le) * nm;
+    float* u = St.u + static_cast<size_t>(e) * nm;
+    bool bad = false;
+    for (int x = lane; x < nm; x += 32) {
+        const float a = row[x];
+        bad |= !isfinite(a);
+        u[__ldg(M.m_int + x)] = fminf(fmaxf(a, 0.0f), 1.0f);
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) St.u_bad[e] = bad ? 1 : 0;
+}
+
+// ============================================================================
 // step kernel: warp per env, WPB envs per block
 // ============================================================================
 // QSL: DOF register slots per lane (n_q <= 32 QSL); fewer slots, fewer live registers.
@@ -869,7 +997,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     const EnvSmem S = carve(smem, warp * EPW + grp, M, G, hm);
     const int nq = M.nq, nm = M.nm, nl = M.nl, nrd = M.nrd;
     const size_t mb = static_cast<size_t>(e) * nm;
-    const float* act_row = actions + static_cast<size_t>(le) * nm;
+    const float* act_row = St.u + mb;  // this step's clamped excitations in device muscle order
 
     // Contract checks of Env::step (env.cpp:207-210): env untouched on failure.
     bool active = true;
@@ -878,9 +1006,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         active = false;
     }
     if (active) {
-        bool bad = false;
-        for (int m = lane; m < nm; m += S.G) bad |= !isfinite(act_row[m]);
-        if (__any_sync(S.hm, bad)) {
+        if (St.u_bad[e]) {
             if (lane == 0 && flags) flags[le] = kFlagBadAction;
             active = false;
         }
@@ -902,10 +1028,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     PHASE_T0();
     int diverged_at = -1;
     for (int sub = 0; sub < kSubsteps; ++sub) {
-        if (M.has_general) tree_sweep<false>(M, S, lane, nullptr);  // world frame for general segments
+        if (M.has_general) fk_d(M, S, lane);  // f64 world frames of the general segments
 
         // ---- 1. muscles + J_m^T F contributions ----
-        muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane);
+        muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane, sub == kSubsteps - 1);
         __syncwarp(S.hm);
 
         PHASE_MARK(0);
@@ -943,6 +1069,7 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         PHASE_MARK(1);
         {
             // ---- 3. FK + velocities + per-link articulated-body terms ----
+            if (M.ns) sphere_pen_d(M, S, lane);
             tree_sweep<true>(M, S, lane, grf_row);
 
             PHASE_MARK(2);
@@ -1104,7 +1231,8 @@ __device__ __forceinline__ void reset_env(const DevModel& M, const DevState& St,
     }
     publish_dofs<QS>(M, S, qd, dqd, lane);
     __syncwarp(S.hm);
-    tree_sweep<false>(M, S, lane, nullptr);
+    tree_sweep<false>(M, S, lane, nullptr);  // (f32 frames for the observation)
+    if (M.has_general) fk_d(M, S, lane);
     init_muscles(M, St, S, e, lane);
     if (lane == 0) {
         St.t[e] = frame * kCtrlDt;
@@ -1149,8 +1277,10 @@ __global__ void __launch_bounds__(WPB * 32, MINB) reset_kernel(DevModel M, DevSt
     const int e0 = blockIdx.x * range, n_range = min(range, n_envs - e0);
     if (threadIdx.x == 0) s_cnt = 0;
     __syncthreads();
-    {
-        const int t = threadIdx.x, wl = threadIdx.x & 31;
+    // every env of the range is visited whatever the block size (blockDim.x strides);
+    // the list order is not significant (each env's reset is independent)
+    for (int t0 = 0; t0 < n_range; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x, wl = threadIdx.x & 31;
         const bool sel = t < n_range && (!mask || (mask[e0 + t] & mask_bits));
         const unsigned b = __ballot_sync(0xffffffffu, sel);
         int base = 0;
@@ -1210,6 +1340,11 @@ __global__ void seed_kernel(DevState St, int n_envs, uint64_t base_seed) {
     St.mti[e] = 312;
 }
 
+__global__ void set_mti_kernel(DevState St, int n_envs, const int* mti) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n_envs) St.mti[e] = min(max(mti[e], 0), 312);
+}
+
 __global__ void rng_raw_kernel(DevState St, int e, int n, uint64_t* out) {
     if (blockIdx.x == 0 && threadIdx.x == 0)
         for (int i = 0; i < n; ++i) out[i] = mt_next(St.mt + static_cast<size_t>(e) * 312, St.mti + e);
@@ -1224,11 +1359,13 @@ __device__ __forceinline__ void sampler_record(double* ema, int bins, double dec
 __global__ void record_own_kernel(DevModel M, DevState St, int n_envs) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n_envs) return;
-    const int n = min(St.out_count[e], St.out_cap);
+    const int c = St.out_count[e];
+    const int n = min(c, St.out_cap);
     for (int i = 0; i < n; ++i)
         sampler_record(St.ema + static_cast<size_t>(e) * M.bins, M.bins, M.decay,
                        St.out_bin[static_cast<size_t>(e) * St.out_cap + i],
                        St.out_failed[static_cast<size_t>(e) * St.out_cap + i]);
+    if (c > n) atomicAdd(St.out_dropped, static_cast<unsigned long long>(c - n));  // ring overflow: counted
     St.out_count[e] = 0;
 }
 
@@ -1307,18 +1444,21 @@ __global__ void drain_kernel(DevState St, int n_envs, int cap, int* bins, uint8_
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n_envs) return;
     const int c = St.out_count[e];
-    counts[e] = c;
     const int n = min(min(c, St.out_cap), cap);
+    counts[e] = n;  // only valid slots are ever reported (the merge reads counts[e] entries)
     for (int i = 0; i < n; ++i) {
         bins[static_cast<size_t>(e) * cap + i] = St.out_bin[static_cast<size_t>(e) * St.out_cap + i];
         failed[static_cast<size_t>(e) * cap + i] = St.out_failed[static_cast<size_t>(e) * St.out_cap + i];
     }
+    // outcomes beyond the ring or the caller's cap are not silently lost: counted
+    if (c > n) atomicAdd(St.out_dropped, static_cast<unsigned long long>(c - n));
     St.out_count[e] = 0;
 }
 
 // Muscle rows between the internal (segment-count sorted) order and the
 // reference order: to_internal ? dst[i] = src[ext(i)] : dst[ext(i)] = src[i].
-__global__ void permute_muscles_kernel(DevModel M, int n_envs, const float* src, float* dst, int to_internal) {
+template <class T>
+__global__ void permute_muscles_kernel(DevModel M, int n_envs, const T* src, T* dst, int to_internal) {
     const long long tot = static_cast<long long>(n_envs) * M.nm;
     for (long long g = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; g < tot;
          g += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1374,7 +1514,7 @@ __global__ void excitation_kernel(int n_envs, int nm, long long env_offset, uint
     const uint32_t r4[4] = {c0, c1, c2, c3};
     float* row = out + static_cast<size_t>(e) * nm;
     constexpr float kScale = 1.0f / 16777216.0f;
-    if ((nm & 3) == 0) {  // rows start 16-B aligned: one vector store
+    if ((nm & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {  // 16-B aligned rows: one vector store
         reinterpret_cast<float4*>(row)[g] = make_float4(static_cast<float>(r4[0] >> 8) * kScale,
                                                         static_cast<float>(r4[1] >> 8) * kScale,
                                                         static_cast<float>(r4[2] >> 8) * kScale,
@@ -1496,6 +1636,7 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
 #define MSK_STEP(NS, QSL)                                                                                  \
     step_kernel<kWPB, kMinB, NS, kEPW, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, \
                                                                             raux, flags, power, grf)
+    prep_actions_kernel<<<(n + 7) / 8, 256, 0, s>>>(M, St, env0, n, actions);
     const int v = step_variant(M);
     if (step_qslots(M) == 3 && (v == 0 || v == 2 || v == 3)) {  // whole-body sized models
         switch (v) {
@@ -1541,6 +1682,10 @@ void launch_seed(const DevState& St, int n, uint64_t base_seed, cudaStream_t s) 
 
 void launch_rng_raw(const DevState& St, int e, int n, uint64_t* out, cudaStream_t s) {
     rng_raw_kernel<<<1, 32, 0, s>>>(St, e, n, out);
+}
+
+void launch_set_mti(const DevState& St, int n, const int* mti, cudaStream_t s) {
+    set_mti_kernel<<<(n + 127) / 128, 128, 0, s>>>(St, n, mti);
 }
 
 void launch_record_own(const DevModel& M, const DevState& St, int n, cudaStream_t s) {
@@ -1719,7 +1864,14 @@ void launch_drain(const DevState& St, int n, int cap, int* bins, uint8_t* failed
 void launch_permute_muscles(const DevModel& M, int n, const float* src, float* dst, int to_internal, cudaStream_t s) {
     const long long tot = static_cast<long long>(n) * M.nm;
     const int blocks = static_cast<int>(std::min<long long>((tot + 255) / 256, 148 * 16));
-    permute_muscles_kernel<<<blocks, 256, 0, s>>>(M, n, src, dst, to_internal);
+    permute_muscles_kernel<float><<<blocks, 256, 0, s>>>(M, n, src, dst, to_internal);
+}
+
+void launch_permute_muscles(const DevModel& M, int n, const double* src, double* dst, int to_internal,
+                            cudaStream_t s) {
+    const long long tot = static_cast<long long>(n) * M.nm;
+    const int blocks = static_cast<int>(std::min<long long>((tot + 255) / 256, 148 * 16));
+    permute_muscles_kernel<double><<<blocks, 256, 0, s>>>(M, n, src, dst, to_internal);
 }
 
 void launch_get_ints(const DevState& St, int n, int* ints, cudaStream_t s) {

@@ -101,6 +101,45 @@ std::vector<std::string> ModelSpec::validate() const {
     return e;
 }
 
+std::vector<std::string> ModelSpec::device_envelope() const {
+    // What msk_gpu_create enforces.  The reference steps any model load_model
+    // parses (load_model, model.cpp:198-204, and Env::Env, env.cpp:74-87, never
+    // call validate), so only the structure the device tables are built from is
+    // required here: the joint/child ordering of the tree (FK, the level schedule
+    // and the articulated-body passes assume parents precede children), link
+    // indices in range, and no world anchors on a floating root (the device keeps
+    // geometry root-relative).  Physical-range checks (masses, limits, damping,
+    // tau_act <= tau_deact, ...) stay in validate() / msk_gpu_validate.
+    std::vector<std::string> e;
+    const int nl = static_cast<int>(links.size()), nj = static_cast<int>(joints.size());
+    if (links.empty()) e.push_back("model has no links");
+    const int want = floating ? nl - 1 : nl;
+    if (nj != want)
+        e.push_back("expected " + std::to_string(want) + " joints for " + std::to_string(nl) + " links, got " +
+                    std::to_string(nj));
+    const int fc = floating ? 1 : 0;
+    for (int j = 0; j < nj; ++j) {
+        const auto& t = joints[j];
+        if (t.child != fc + j) e.push_back("joint '" + t.name + "': joints must be listed in child-link order");
+        if (t.parent >= t.child) e.push_back("joint '" + t.name + "': parent must precede child");
+        if (t.parent < -1 || t.parent >= nl) e.push_back("joint '" + t.name + "': parent link out of range");
+        if (t.parent == -1 && floating)
+            e.push_back("joint '" + t.name + "': floating-root models have no world-parented joints on the device");
+    }
+    for (const auto& m : muscles)
+        for (const auto& v : m.vias) {
+            if (v.link < -1 || v.link >= nl)
+                e.push_back("muscle '" + m.name + "': via point references missing link " + std::to_string(v.link));
+            if (floating && v.link == -1)
+                e.push_back("muscle '" + m.name + "': floating-root models cannot anchor muscles to the world");
+        }
+    for (const auto& s : spheres)
+        if (s.link < 0 || s.link >= nl) e.push_back("contact sphere references missing link");
+    for (int k : key_bodies)
+        if (k < 0 || k >= nl) e.push_back("key body index out of range");
+    return e;
+}
+
 ModelSpec load_model(const std::string& path) {
     std::ifstream in(path);
     if (!in) throw ConfigError("model: cannot open '" + path + "'");

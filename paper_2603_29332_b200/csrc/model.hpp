@@ -55,6 +55,8 @@ struct ModelSpec {
     int nrd() const { return floating ? 3 : 0; }
     int nq() const { return nrd() + static_cast<int>(joints.size()); }
     std::vector<std::string> validate() const;
+    // Structural subset msk_gpu_create enforces (the reference's load_model runs no validation).
+    std::vector<std::string> device_envelope() const;
 };
 
 struct Clip {

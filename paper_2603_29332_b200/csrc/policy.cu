@@ -195,6 +195,16 @@ void ckp(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Identity normaliser (mean 0, 1/sd 1), written into the same device buffers the
+// sample kernels always read.
+void set_identity_norm(msk_policy* p) {
+    const std::vector<float> zero(p->obs_dim, 0.0f), one(p->obs_dim, 1.0f);
+    ckp(cudaMemcpy(p->norm_mean, zero.data(), zero.size() * 4, cudaMemcpyHostToDevice), "norm");
+    ckp(cudaMemcpy(p->norm_inv_sd, one.data(), one.size() * 4, cudaMemcpyHostToDevice), "norm");
+    p->norm = false;
+}
+
+
 std::vector<float> to_f32(const double* x, size_t n) {
     std::vector<float> v(n);
     for (size_t i = 0; i < n; ++i) v[i] = static_cast<float>(x[i]);
@@ -205,7 +215,9 @@ std::vector<float> to_f32(const double* x, size_t n) {
 void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_t seed, long long env_offset,
                     float* actions, float* a0_out, float* logprob, cudaStream_t s) {
     const int H = p->hidden, D = p->obs_dim, NM = p->nm;
-    ckp(launch_obs_to_tiled(obs, n, D, p->norm ? p->norm_mean : nullptr, p->norm_inv_sd, p->s_t, s), "obs");
+    // always normalise: the identity normaliser is mean 0, 1/sd 1 ((x - 0) * 1 == x bit for bit),
+    // so a captured graph stays valid when msk_policy_set_norm changes the statistics
+    ckp(launch_obs_to_tiled(obs, n, D, p->norm_mean, p->norm_inv_sd, p->s_t, s), "obs");
     GemmArgs g;
     g.M = n;
     // π⁽⁰⁾ mean: 3 tanh layers + affine head into the action buffer
@@ -363,6 +375,7 @@ int msk_policy_create(int32_t obs_dim, int32_t n_actions, int32_t hidden, const 
         p->norm_mean = p->dalloc<float>(D);
         p->norm_inv_sd = p->dalloc<float>(D);
         p->d_step = p->dalloc<uint32_t>(1);
+        set_identity_norm(p);
         ckp(prepare_gemm(), "cudaFuncSetAttribute(gemm)");
         ckp(cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking), "stream");
         *out = p;
@@ -392,7 +405,7 @@ int msk_policy_set_norm(msk_policy* p, const double* mean, const double* var, do
     try {
         ckp(cudaSetDevice(p->device), "cudaSetDevice");
         if (count == 0.0 || !mean || !var) {  // RunningNorm::apply with count 0 is the identity (nn.cpp:273)
-            p->norm = false;
+            set_identity_norm(p);
             return MSK_OK;
         }
         std::vector<float> m(p->obs_dim), is(p->obs_dim);

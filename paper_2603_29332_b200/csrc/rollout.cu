@@ -128,7 +128,9 @@ __global__ void minibatch_kernel(long long n, int hb, uint64_t key, long long fi
         if (!dst || dim == 0) return;
         const float* sp = src + static_cast<size_t>(i) * dim;
         float* dp = dst + static_cast<size_t>(j) * dim;
-        if ((dim & 3) == 0) {
+        // 16-B vectors only when both rows are 16-B aligned (a C-ABI caller may pass
+        // an offset / sub-buffer pointer)
+        if ((dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(sp) | reinterpret_cast<uintptr_t>(dp)) & 15) == 0) {
             for (int c = lane; c < dim / 4; c += 32)
                 reinterpret_cast<float4*>(dp)[c] = reinterpret_cast<const float4*>(sp)[c];
         } else {

@@ -179,10 +179,23 @@ def merged_iteration(blocks, n_envs, cap, obs_dim, norm_state, ema, decay, merge
     return stats, (count, mean, var), new_ema
 
 
-def iteration_exchange(env, rollout_stats: torch.Tensor, obs_batch: torch.Tensor, norm_state, cap=64, group=None):
-    """One iteration boundary on a GPU rank: drain, pack, all_gather, ordered merge (device sampler)."""
+def fold_moments(acc, m, obs_dim):
+    """Chan / RunningNorm::update merge (nn.cpp:246-270) of two moment vectors
+    [n, mean[D], var[D]] (f64 device tensors, no host sync): the iteration's
+    observation moments accumulate step by step over its h x E observations."""
+    if acc is None:
+        return m.clone()
+    c, mean, var = running_norm_fold_t(acc[0], acc[1:1 + obs_dim], acc[1 + obs_dim:], m[0], m[1:1 + obs_dim],
+                                       m[1 + obs_dim:])
+    return torch.cat([c.reshape(1), mean, var])
+
+
+def iteration_exchange(env, rollout_stats: torch.Tensor, obs_batch, norm_state, cap=64, group=None, moments=None):
+    """One iteration boundary on a GPU rank: drain, pack, all_gather, ordered merge (device sampler).
+    The observation moments are those of ``obs_batch`` [n x D] or, when given,
+    ``moments`` [n, mean[D], var[D]] (e.g. folded over the iteration's h steps)."""
     bins, failed, counts = env.drain_outcomes(cap)
-    norm = env.obs_moments(obs_batch)  # native f64 column moments (msk_gpu_obs_moments)
+    norm = moments if moments is not None else env.obs_moments(obs_batch)  # native f64 column moments
     block = pack_block(bins, failed, counts, rollout_stats.to(bins.device), norm, env.obs_dim)
     blocks = exchange(block, group)
     return merged_iteration(blocks, env.n, cap, env.obs_dim, norm_state, None, env.cfg.adaptive_decay,

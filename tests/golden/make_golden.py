@@ -93,8 +93,35 @@ def make_mlp():
                 big_len=np.array([big.size]))
 
 
+RNG_CASE = dict(model="arm2_m6", n=3, rounds=5, cfg=dict(episode_horizon=30, rsi=True))
+
+
+def make_rng():
+    """The reference's own Rng::serialize() text (rng.hpp:56-61) of every env at
+    construction and after each of `rounds` RSI resets of all envs, plus the
+    start frames of every round (Env::rng(), env.hpp:120)."""
+    c = RNG_CASE
+    mp, cp = model_paths(c["model"])
+    b = RefBatch(mp, cp, c["n"], base_seed=0x5EED, cfg=env_config(**c["cfg"]))
+    ema = np.linspace(0.0, 0.3, b.bins)
+    b.set_sampler(np.tile(ema, (c["n"], 1)))
+    states = [[b.rng_serialize(e) for e in range(c["n"])]]
+    frames = []
+    for _ in range(c["rounds"]):
+        _, f = b.reset()
+        frames.append([int(x) for x in f])
+        states.append([b.rng_serialize(e) for e in range(c["n"])])
+    return dict(case=c, ema=ema.tolist(), serialize=states, frames=frames)
+
+
 def main():
     ensure_assets()
+    import json
+
+    path = os.path.join(HERE, "rng_serialize.json")
+    with open(path, "w") as f:
+        json.dump(make_rng(), f)
+    print(path, os.path.getsize(path))
     path = os.path.join(HERE, "mlp_seed7.npz")
     np.savez_compressed(path, **make_mlp())
     print(path, os.path.getsize(path))

@@ -1,10 +1,12 @@
 """GPU parity tests: the sm_100a path (through the C ABI) vs the oracle.
 
-Tolerances (north_star: "rel <= 1e-4 on forces, <= 1e-5 on q/qdot"), for ONE
-control step (10 substeps) from identical state and excitations:
-  q, q̇        max|Δ| <= 1e-5 * max(1, max|ref|)      (per env, norm-wise)
+Tolerances (north_star: "rel <= 1e-4 on forces, <= 1e-5 on q/qdot"; SURVEY.md
+§8(c)), for ONE control step (10 substeps) from identical state and excitations:
+  q           |Δ| <= max(1e-5 |ref|, 1e-6)           (per element)
+  q̇           max|Δ| <= 1e-5 max|ref| (per env) and |Δ| <= 2e-4 max(|ref|, 0.05)
+              per element (parity_util.py: why the per-element bound is 2e-4)
   activation  max|Δ| <= 1e-6
-  muscle force |ΔF| <= 1e-4 * max(|F|, f_max)        (per muscle)
+  muscle force |ΔF| <= 1e-4 * max(|F|, 1e-3 f_max)   (per muscle)
   Δ (tracking error) max|Δ| <= 1e-5 m / rad
   observation max|Δ| <= 1e-4 * max(1, max|ref block|) (per env and obs block)
   flags, t_index, steps, start frames, RNG draws, sampler: bit-exact.
@@ -17,8 +19,8 @@ import pytest
 
 from conftest import model_paths
 from golden_cases import CASES
-from parity_util import (f32_state, force_err, gpu_state, make_pair, obs_block_errors, step_both, sync_from_oracle,
-                         to_np)
+from parity_util import (dq_norm_ratio, dq_ratio, f32_state, f_ratio, f_rel, force_err, gpu_state, make_pair,
+                         obs_block_errors, q_ratio, step_both, sync_from_oracle, to_np)
 from oracle.oracle import excitations
 
 pytestmark = pytest.mark.gpu
@@ -47,6 +49,37 @@ def _parity_report():
 
         with open(path, "w") as f:
             json.dump(REPORT, f, indent=1, sort_keys=True)
+
+
+def _check_step(name, sg, so, fmax, rows=None):
+    """SURVEY §8(c) single-step tolerances on a GPU/oracle state pair (rows: the
+    GPU rows that correspond to the oracle's envs); ratios (<= 1 passes) and the
+    true relative force error go into the parity report."""
+    take = (lambda x: x[rows]) if rows is not None else (lambda x: x)
+
+    def check(label, a, b, r, rel, floor):
+        _note(name, label, r)
+        if r > 1.0:
+            rr = np.abs(a - b) / np.maximum(rel * np.abs(b), floor)
+            e, i = np.unravel_index(np.argmax(rr), rr.shape)
+            raise AssertionError(f"{name} {label}: ratio {r:.3g} at row {e} dof {i}: gpu {a[e, i]!r} ref {b[e, i]!r}; "
+                                 f"row max |d| {np.abs(a[e] - b[e]).max():.3g}")
+
+    q, dq = take(sg["q"]), take(sg["dq"])
+    check("q ratio (|d| <= max(1e-5|ref|, 1e-6) per element)", q, so["q"], q_ratio(q, so["q"]), 1e-5, 1e-6)
+    _note(name, "dq survey ratio (1e-5|ref|, 1e-6 floor; reported, not asserted)", q_ratio(dq, so["dq"]))
+    check("dq ratio (|d| <= 2e-4 max(|ref|, 0.05) per element)", dq, so["dq"], dq_ratio(dq, so["dq"]), 2e-4, 1e-5)
+    rn = dq_norm_ratio(dq, so["dq"])
+    _note(name, "dq norm ratio (max|d| <= 1e-5 max|ref| per env)", rn)
+    assert rn <= 1.0, (name, "dq norm-wise", rn)
+    act = np.abs(take(sg["act"]) - so["act"]).max()
+    _note(name, "act (tol 1e-6)", act)
+    assert act <= 1e-6, (name, act)
+    fr = f_ratio(take(sg["f_m"]), so["f_m"], fmax)
+    _note(name, "f_m ratio (|dF| <= 1e-4 max(|F|, 1e-3 f_max))", fr)
+    _note(name, "f_m true rel err (|F| >= 1e-3 f_max)", f_rel(take(sg["f_m"]), so["f_m"], fmax))
+    _note(name, "f_m rel f_max", force_err(take(sg["f_m"]), so["f_m"], fmax))
+    assert fr <= 1.0, (name, fr)
 
 
 def _envs(name):
@@ -87,16 +120,8 @@ def test_single_step_parity(assets, name):
         a = excitations(1000 + trial, 0, n, g.nm).astype(np.float32)
         og, oo = step_both(g, o, a)
         sg, so = gpu_state(g), o.get_state()
-        for e in range(n):
-            for k in ("q", "dq"):
-                err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
-                _note(name, k + " (tol 1e-5)", err)
-                assert err <= 1e-5, (name, trial, e, k, err)
-        _note(name, "act (tol 1e-6)", np.abs(sg["act"] - so["act"]).max())
-        _note(name, "f_m rel f_max (tol 1e-4)", force_err(sg["f_m"], so["f_m"], fmax))
+        _check_step(name, sg, so, fmax)
         _note(name, "delta (tol 1e-5)", np.abs(og["delta"] - oo["delta"]).max())
-        assert np.abs(sg["act"] - so["act"]).max() <= 1e-6
-        assert force_err(sg["f_m"], so["f_m"], fmax) <= 1e-4, force_err(sg["f_m"], so["f_m"], fmax)
         assert np.abs(og["delta"] - oo["delta"]).max() <= 1e-5
         blocks = obs_block_errors(g, og["obs"], oo["obs"])
         _note(name, "obs blocks except f_m (tol 1e-4)", max(v for k, v in blocks.items() if k != "f_m"))
@@ -527,41 +552,142 @@ def test_iteration_reductions_match_torch(assets):
     g.close()
 
 
-def test_full_size_batch_sampled_envs_match_oracle(assets):
-    """BASELINE config size (4096 envs, training-mode RSI): sampled global env
-    indices (0, 1, E-1 and random ones) of the full GPU batch match the oracle
-    run on those envs alone (parity on a sampled subset) —
-    start frames bit-exact, state within the single-step tolerances."""
+def _gpu_rows(g, rows):
+    """The state of the given envs only (gathered on the device)."""
+    import torch
+
+    s = g.get_state()
+    idx = torch.as_tensor(rows, dtype=torch.long, device=g.device)
+    out = {k: to_np(v.index_select(0, idx)) for k, v in s.items()}
+    return {k: (v.astype(np.float64) if k != "ints" else v) for k, v in out.items()}
+
+
+# BASELINE.json configs at their full per-GPU batch size (SURVEY §8(c): parity
+# on a sampled subset of global env indices, the oracle running those envs alone):
+#   name: (model, envs, EnvConfig, reward mode, discriminator (W, seed) or None, eval, steps, h)
+SCALE_CASES = {
+    "c2_wb700_fixed_4096": ("wb700_fixed", 4096, dict(episode_horizon=1000, rsi=False), 0, None, True, 4, 0),
+    "c4_wb700_16384": ("wb700", 16384, dict(episode_horizon=250, rsi=True), 2, (256, 7), False, 12, 8),
+    "c5_wb700_slow_8192": ("wb700_slow", 8192, dict(episode_horizon=250, rsi=True), 2, None, False, 12, 8),
+    "c2g_wb700_general_4096": ("wb700_general", 4096, dict(episode_horizon=1000, rsi=False), 0, None, True, 4, 0),
+}
+
+
+@pytest.mark.parametrize("case", sorted(SCALE_CASES))
+def test_full_size_batch_sampled_envs_match_oracle(assets, case):
+    """A whole BASELINE batch steps on the GPU (training configs: RSI resets,
+    adaptive sampler, termination, auto-reset of done envs, the fused D(Δ)
+    reward and an iteration boundary with the ordered sampler merge).  Global
+    envs 0, 1, E-1 and 13 random ones are replayed by the oracle alone, each
+    step from the GPU's pre-step state: every step must meet the single-step
+    tolerances, flags / start frames / drained outcomes are bit-exact, and the
+    device's merged sampler equals the host merge of every env's outcomes."""
     import torch
 
     import paper_2603_29332_b200 as pk
-    from oracle.oracle import OracleBatch
+    import paper_2603_29332_b200.dist as pkd
+    from oracle.oracle import OracleBatch, disc_reward, mlp_init
     from oracle.ref import env_config
 
-    mp, cp = model_paths("wb700_fixed")
-    E = 4096
-    g = pk.EnvBatch(mp, cp, E, cfg=pk.EnvConfig(episode_horizon=1000, rsi=True))
-    g.reset()
-    a = torch.empty(E, g.nm, device=g.device)
-    for s in range(2):
-        g.fill_excitations(0x5EED, s, a)
-        out = g.step(a)
-    torch.cuda.synchronize()
-    sg = gpu_state(g)
+    model, E, cfg_kw, mode, disc, ev, steps, h = SCALE_CASES[case]
+    mp, cp = model_paths(model)
+    g = pk.EnvBatch(mp, cp, E, cfg=pk.EnvConfig(**cfg_kw), reward=pk.RewardConfig(mode=mode))
+    g.set_eval_mode(ev)
     rng = np.random.default_rng(11)
-    sample = [0, 1, E - 1] + sorted(rng.choice(np.arange(2, E - 1), 5, replace=False).tolist())
+    sample = [0, 1, E - 1] + sorted(rng.choice(np.arange(2, E - 1), 13, replace=False).tolist())
+    orc = {}
     for e in sample:
-        o = OracleBatch(mp, cp, 1, cfg=env_config(episode_horizon=1000, rsi=True), global_env_offset=e)
-        o.reset()
-        # the oracle steps in f64 from the same start; compare after two control steps
-        for s in range(2):
-            oo = o.step(excitations(0x5EED, s, 1, g.nm, global_env_offset=e))
-        so = o.get_state()
-        assert int(sg["ints"][e, 1]) == int(so["ints"][0, 1])  # RSI start frame, bit-exact
-        q_err = np.abs(sg["q"][e] - so["q"][0]).max() / max(1.0, np.abs(so["q"][0]).max())
-        assert q_err <= 1e-4, (e, q_err)
-        assert np.abs(sg["act"][e] - so["act"][0]).max() <= 1e-5
-        assert to_np(out["flags"])[e] == oo["flags"][0]
+        o = OracleBatch(mp, cp, 1, cfg=env_config(**cfg_kw), reward_mode=mode, global_env_offset=e)
+        o.set_eval_mode(ev)
+        orc[e] = o
+    fmax = orc[0].model.d["m_fmax"]
+    theta = None
+    if disc:
+        theta = mlp_init(g.delta_dim, disc[0], disc[1])
+        g.set_discriminator(theta, disc[0])
+    sf = torch.full((E,), -1, dtype=torch.int32, device=g.device)
+    g.reset(start_frames=sf)
+    sfn = to_np(sf)
+    for e, o in orc.items():
+        _, f = o.reset()
+        assert int(f[0]) == int(sfn[e]), (case, "initial RSI frame", e)
+    a = torch.empty(E, g.nm, device=g.device)
+    reward = torch.zeros(E, device=g.device)
+    n_done = n_resets = n_ties = 0
+    for s in range(steps):
+        pre = _gpu_rows(g, sample)
+        for k, (e, o) in enumerate(orc.items()):  # single-step protocol: same pre-step state
+            o.set_state(f32_state({kk: v[k:k + 1] for kk, v in pre.items()}) | {"ints": pre["ints"][k:k + 1]})
+        g.fill_excitations(0x5EED, s, a)
+        out = g.step(a, reward=reward if disc else None, want_power=True)
+        post = _gpu_rows(g, sample)
+        fl, rw = to_np(out["flags"]), to_np(reward)
+        # Contact ties: the clip's global-minimum frame puts a sphere exactly on the
+        # ground (SPEC.md:570, ground_offset: min height 0 within 1e-12 m); there the
+        # reference's contact force is discontinuous (f_n = max(0, k pen - c z'),
+        # skeleton.cpp:243-248) and its branch is decided by the last bit of its own
+        # libm/FK rounding.  Such env-steps are rounding-ambiguous in the reference
+        # itself: counted and reported, not compared (they must stay rare).
+        tie = np.zeros(len(sample), dtype=bool)
+        if orc[0].model.d["n_spheres"]:
+            for k, (e, o) in enumerate(orc.items()):
+                tie[k] = abs(_lowest_sphere_bottom(o, mp, pre["q"][k])) < 1e-9
+        n_ties += int(tie.sum())
+        oo = {e: o.step(excitations(0x5EED, s, 1, g.nm, global_env_offset=e)) for e, o in orc.items()}
+        so = {kk: np.concatenate([o.get_state()[kk] for o in orc.values()]) for kk in post}
+        keep = [k for k, e in enumerate(sample) if not tie[k]]
+        ks = [sample[k] for k in keep]
+        assert np.array_equal(fl[ks], np.concatenate([oo[e]["flags"] for e in ks])), (case, s)
+        live = [k for k in keep if not (fl[sample[k]] & pk.FLAG_DIVERGED)]
+        _check_step(case, {kk: v[live] for kk, v in post.items()}, {kk: v[live] for kk, v in so.items()}, fmax)
+        assert np.array_equal(post["ints"][keep], so["ints"][keep]), (case, s)
+        aux = np.concatenate([oo[e]["reward_aux"] for e in ks])
+        assert np.abs(to_np(out["reward_aux"])[ks] - aux).max() <= 1e-4 * max(1.0, np.abs(aux).max())
+        if disc:  # reward = r(D(Δ)) + reward_aux, D on the oracle's own Δ (f64)
+            ref = np.array([disc_reward(theta, g.delta_dim, disc[0], oo[e]["delta"])[0] for e in ks]) + aux
+            ref = np.where(fl[ks] & pk.FLAG_DIVERGED, 0.0, ref)
+            err = float(np.max(np.abs(rw[ks] - ref) / np.maximum(1.0, np.abs(ref))))
+            _note(case, "D reward rel (tol 3e-3)", err)
+            assert err <= 3e-3, (case, s, err)
+        done = (fl & pk.FLAG_DONE) > 0
+        n_done += int(done.sum())
+        if h and (s + 1) % h == 0:  # iteration boundary: drain -> ordered merge -> replicated sampler
+            ema0 = to_np(g.get_sampler())[0].copy()
+            bins, failed, counts = g.drain_outcomes(h)
+            b_n, f_n, c_n = to_np(bins), to_np(failed), to_np(counts)
+            for k, (e, o) in enumerate(orc.items()):
+                ob, of, oc = o.drain_outcomes(h)
+                if n_ties:  # a tied env-step may end an episode on one side only
+                    continue
+                assert int(oc[0]) == int(c_n[e]), (case, s, e)
+                assert np.array_equal(ob[0, :oc[0]], b_n[e, :oc[0]]) and np.array_equal(of[0, :oc[0]], f_n[e, :oc[0]])
+            g.merge_outcomes(bins, failed, counts)
+            host = pkd.merge_outcomes_host(ema0, b_n, f_n, c_n, cfg_kw.get("adaptive_decay", 0.99))
+            dev = to_np(g.get_sampler())
+            assert np.array_equal(dev, np.tile(host, (E, 1))), (case, "merged sampler")
+            for o in orc.values():
+                o.set_sampler(host[None, :])
+        if done.any():  # auto-reset of done envs (RSI from the current sampler)
+            sf.fill_(-1)
+            g.reset(mask=out["flags"], mask_bits=pk.FLAG_DONE, start_frames=sf)
+            sfn = to_np(sf)
+            after = _gpu_rows(g, sample)
+            for k, (e, o) in enumerate(orc.items()):
+                if done[e]:  # (after a tie too: the oracle's RNG follows the GPU's resets)
+                    _, f = o.reset()
+                    n_resets += 1
+                    assert int(f[0]) == int(sfn[e]), (case, s, "reset frame", e)
+                    # make_initial_state at the sampled frame (skeleton.cpp:264-284)
+                    st = o.get_state()
+                    assert np.array_equal(after["ints"][k:k + 1], st["ints"])
+                    assert q_ratio(after["q"][k], st["q"][0]) <= 1.0 and q_ratio(after["dq"][k], st["dq"][0]) <= 1.0
+                    assert np.abs(after["act"][k] - st["act"][0]).max() <= 1e-7
+                    assert f_ratio(after["f_m"][k:k + 1], st["f_m"], fmax) <= 1.0
+    _note(case, "episodes ended in the batch", n_done)
+    _note(case, "sampled-env resets replayed", n_resets)
+    _note(case, "contact-tie env-steps (not compared)", n_ties)
+    assert n_ties <= 2, (case, n_ties)
+    assert g.outcomes_dropped() == 0
     g.close()
 
 
@@ -627,13 +753,7 @@ def test_general_segments_parity(assets, tmp_path, name):
         a = excitations(300 + trial, 0, n, g.nm).astype(np.float32)
         og, oo = step_both(g, o, a)
         sg, so = gpu_state(g), o.get_state()
-        for e in range(n):
-            for k in ("q", "dq"):
-                err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
-                _note(name + "_general", k + " (tol 1e-5)", err)
-                assert err <= 1e-5, (trial, e, k, err)
-        _note(name + "_general", "f_m rel f_max (tol 1e-4)", force_err(sg["f_m"], so["f_m"], fmax))
-        assert force_err(sg["f_m"], so["f_m"], fmax) <= 1e-4
+        _check_step(name + "_general", sg, so, fmax)
         assert np.abs(og["delta"] - oo["delta"]).max() <= 1e-5
         assert np.array_equal(og["flags"], oo["flags"])
     g.close()
@@ -694,11 +814,7 @@ def test_contact_parity(assets, name):
     _note(name, "grf in contact rel (tol 1e-3)", np.abs(grf_g - grf_o).max() / scale)
     assert np.abs(grf_g - grf_o).max() <= 1e-3 * scale
     sg, so = gpu_state(g), o.get_state()
-    for e in range(n):
-        for k in ("q", "dq"):
-            err = np.abs(sg[k][e] - so[k][e]).max() / max(1.0, np.abs(so[k][e]).max())
-            _note(name, k + " in contact (tol 1e-5)", err)
-            assert err <= 1e-5, (e, k, err)
+    _check_step(name + " in contact", sg, so, o.model.d["m_fmax"])
     g.close()
 
 
@@ -859,3 +975,116 @@ def test_c1_thousand_step_free_run(assets):
     _note("arm2_m6", "c1 1000-step free-run q drift (tol 1e-3)", worst)
     assert worst <= 1e-3, worst
     g.close()
+
+
+# ---- boundary: RNG checkpoint, outcome ring, model acceptance ----------
+def test_rng_state_matches_reference_serialize_and_checkpoint_roundtrip(assets):
+    """msk_gpu_get_rng equals the reference's Rng::serialize() (rng.hpp:56-61) at
+    construction and after each RSI reset round (golden made by oracle/_ref); a
+    saved {rng, sampler, state} restored later replays identical start frames."""
+    import json
+
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    gd = json.load(open(os.path.join(HERE, "golden", "rng_serialize.json")))
+    c = gd["case"]
+    mp, cp = model_paths(c["model"])
+    g = pk.EnvBatch(mp, cp, c["n"], cfg=pk.EnvConfig(**c["cfg"]))
+    g.set_sampler(torch.as_tensor(np.tile(np.array(gd["ema"]), (c["n"], 1)), device=g.device))
+    assert [g.rng_serialize(e) for e in range(c["n"])] == gd["serialize"][0]
+    sf = torch.empty(c["n"], dtype=torch.int32, device=g.device)
+    for r in range(c["rounds"]):
+        g.reset(start_frames=sf)
+        torch.cuda.synchronize()
+        assert to_np(sf).tolist() == gd["frames"][r]
+        assert [g.rng_serialize(e) for e in range(c["n"])] == gd["serialize"][r + 1]
+    # checkpoint / restore
+    mt, mti = [x.clone() for x in g.get_rng()]
+    ema = g.get_sampler().clone()
+    first = []
+    for _ in range(200):  # > 156 resets: crosses a 312-word regeneration of the engine
+        g.reset(start_frames=sf)
+        first.append(to_np(sf).copy())
+    g.set_rng(mt, mti)
+    g.set_sampler(ema)
+    for k in range(200):
+        g.reset(start_frames=sf)
+        assert np.array_equal(to_np(sf), first[k]), k
+    g.close()
+
+
+def test_outcome_ring_overflow_is_counted_and_capacity_grows(assets):
+    """More pending outcomes than ring slots are counted, never silently lost
+    (the reference list is unbounded, env.cpp:195-204); a larger capacity keeps them all."""
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("arm2_m6")
+    n = 5
+    g = pk.EnvBatch(mp, cp, n, cfg=pk.EnvConfig(episode_horizon=1, rsi=False))
+    a = torch.full((n, g.nm), 0.3, device=g.device)
+
+    def episodes(k):  # horizon 1: every step ends an episode
+        for _ in range(k):
+            g.reset()
+            g.step(a)
+
+    episodes(70)
+    bins, failed, counts = g.drain_outcomes(64)
+    torch.cuda.synchronize()
+    assert to_np(counts).tolist() == [64] * n
+    assert g.outcomes_dropped() == 6 * n
+    g.set_outcome_capacity(100)
+    episodes(70)
+    bins, failed, counts = g.drain_outcomes(100)
+    torch.cuda.synchronize()
+    assert to_np(counts).tolist() == [70] * n
+    assert g.outcomes_dropped() == 6 * n  # nothing new lost
+    # a drain asking for fewer slots than pending: the rest is counted
+    episodes(10)
+    _, _, counts = g.drain_outcomes(4)
+    torch.cuda.synchronize()
+    assert to_np(counts).tolist() == [4] * n
+    assert g.outcomes_dropped() == 6 * n + 6 * n
+    g.close()
+
+
+def test_create_accepts_models_the_reference_steps(assets, tmp_path):
+    """load_model / Env::Env run no ModelSpec::validate (model.cpp:198-204,
+    env.cpp:74-87): a model with tau_act > tau_deact and inverted joint limits
+    is stepped, and matches the oracle; structural errors are still refused."""
+    import json
+
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    mp, cp = model_paths("arm2_m6")
+    js = json.load(open(mp))
+    for m in js["muscles"]:
+        m["tau_act"], m["tau_deact"] = 0.08, 0.02  # validate() would refuse this
+    js["joints"][1]["limits"] = [0.5, -0.5]
+    p = tmp_path / "relaxed.json"
+    p.write_text(json.dumps(js))
+    n = 3
+    g, o = make_pair(str(p), cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    fr = np.array([5, 50, 300])
+    g.reset_to_frame(fr)
+    o.reset_to_frame(fr)
+    sync_from_oracle(g, o)
+    for s in range(3):
+        a = excitations(9, s, n, g.nm).astype(np.float32)
+        og, oo = step_both(g, o, a)
+        sg, so = gpu_state(g), o.get_state()
+        assert np.array_equal(og["flags"], oo["flags"])
+        assert np.abs(sg["q"] - so["q"]).max() <= 1e-5 * max(1.0, np.abs(so["q"]).max())
+        assert np.abs(sg["act"] - so["act"]).max() <= 1e-6
+    g.close()
+    js["joints"][1]["parent"] = 1  # a cycle: the device tables cannot be built
+    p.write_text(json.dumps(js))
+    with pytest.raises(pk.MskError, match="parent must precede child"):
+        pk.EnvBatch(str(p), cp, 1)
+    torch.cuda.synchronize()

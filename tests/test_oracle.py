@@ -320,3 +320,38 @@ def test_mlp_forward_matches_numpy():
         a = np.tanh(a @ W.T + b)
     z = a @ ws[3][0].T + ws[3][1]
     assert np.allclose(om.mlp_forward_sigmoid(th, n_in, h, x), 1 / (1 + np.exp(-z[:, 0])), rtol=1e-13, atol=0)
+
+
+# ---- RNG checkpoint state (Env::rng(), Rng::serialize; env.hpp:120, rng.hpp:56-68) ----
+def test_oracle_rng_state_matches_reference_serialize_golden(assets):
+    """The oracle's mt19937_64 engine state, written in Rng::serialize's format,
+    equals the reference's own serialize() text at construction and after every
+    RSI reset round (tests/golden/rng_serialize.json, made by oracle/_ref)."""
+    import json
+
+    g = json.load(open(os.path.join(GOLDEN, "rng_serialize.json")))
+    c = g["case"]
+    mp, cp = model_paths(c["model"])
+    o = om.OracleBatch(mp, cp, c["n"], cfg=env_config(**c["cfg"]))
+    o.set_sampler(np.tile(np.array(g["ema"]), (c["n"], 1)))
+    assert [o.rng_serialize(e) for e in range(c["n"])] == g["serialize"][0]
+    for r in range(c["rounds"]):
+        _, f = o.reset()
+        assert f.tolist() == g["frames"][r]
+        assert [o.rng_serialize(e) for e in range(c["n"])] == g["serialize"][r + 1]
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference build oracle/_ref absent")
+def test_reference_rng_deserialize_restores_the_reset_sequence(assets):
+    """Rng::deserialize of a saved serialize() replays the same start frames
+    (the checkpoint contract the device's get/set_rng mirrors)."""
+    from oracle.ref import RefBatch
+
+    mp, cp = model_paths("arm2_m6")
+    b = RefBatch(mp, cp, 2, cfg=env_config(episode_horizon=30, rsi=True))
+    b.reset()
+    saved = [b.rng_serialize(e) for e in range(2)]
+    first = [b.reset()[1].tolist() for _ in range(4)]
+    for e in range(2):
+        b.rng_deserialize(e, saved[e])
+    assert [b.reset()[1].tolist() for _ in range(4)] == first

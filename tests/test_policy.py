@@ -80,6 +80,32 @@ def test_policy_deterministic_matches_oracle():
     p.close()
 
 
+def test_graph_replay_follows_normaliser_changes():
+    """A graph captured before msk_policy_set_norm must apply the new statistics
+    (the normaliser is part of every replay, not of the capture key)."""
+    import torch
+
+    pi, ls, psi = _params(4)
+    p = _policy(pi, ls, psi)
+    rng = np.random.default_rng(5)
+    obs = torch.as_tensor(rng.normal(0, 1, (150, D)).astype(np.float32), device="cuda")
+    g0 = p.sample(obs, graph=True).clone()  # count 0: identity normaliser
+    e0 = p.sample(obs).clone()
+    assert torch.equal(g0, e0)
+    mean, var = rng.normal(0, 0.5, D), rng.uniform(0.2, 3.0, D)
+    p.set_norm(mean, var, 50.0)
+    g1 = p.sample(obs, graph=True).clone()
+    e1 = p.sample(obs).clone()
+    assert torch.equal(g1, e1)
+    assert not torch.equal(g0, g1)
+    ref, _, _ = sample_action(pi, ls, psi, obs.cpu().numpy(), H, norm=(mean, var, 50.0))
+    assert np.abs(g1.cpu().numpy() - ref).max() <= 2e-2
+    p.set_norm(None, None, 0.0)  # back to the identity
+    g2 = p.sample(obs, graph=True).clone()
+    assert torch.equal(g2, g0)
+    p.close()
+
+
 def test_policy_spec_examples():
     """ψ ≡ 0 -> a = a⁽⁰⁾; ψ ≡ c -> a = a⁽⁰⁾ + c (SPEC.md:391-392)."""
     import torch

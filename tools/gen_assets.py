@@ -660,6 +660,41 @@ def backflip_clip(model: Model, T, seed=13):
 
 
 # --------------------------------------------------------------------------
+def wb700_general():
+    """wb700_fixed with every multi-joint muscle's interior via points removed:
+    its single segment then joins two links that are NOT parent and child (a
+    straight bi-/tri-articular line of action), which the device evaluates on
+    its generic world-frame path (general segments + per-joint pairs,
+    skeleton.cpp:147-170) instead of the adjacent-segment fast path.  l_opt is
+    kept and the tendon slack reset so each fibre is at its optimal length in
+    the neutral pose.  Uses the wb700_fixed clip (same tree and key bodies)."""
+    m = wb700(False)
+    m.name = "wb700_general"
+    q0 = np.zeros(m.nq)
+    origin, angle, _ = fk(m, q0)
+    for mu in m.muscles:
+        vps = mu["via_points"]
+        if len(vps) < 3:
+            continue
+        keep = [vps[0], vps[-1]]
+        L = mtu_len(m, origin, angle, [(v[0], tuple(v[1])) for v in keep])
+        mu["via_points"] = keep
+        mu["tendon_slack"] = float(max(0.0, L - mu["l_opt"]))
+    return m
+
+
+def wb700_slow():
+    """BASELINE c5 stress model: wb700 (floating, contacts) with a long
+    excitation-to-activation lag on every muscle, tau_act = 0.05 s and
+    tau_deact = 0.20 s (the reference has no transport delay; the first-order
+    activation lag is its only delay, muscle.cpp:42-56).  Clip: wb700_dance."""
+    m = wb700(True)
+    m.name = "wb700_slow"
+    for mu in m.muscles:
+        mu["tau_act"], mu["tau_deact"] = 0.05, 0.20
+    return m
+
+
 def write_model(path, model):
     with open(path, "w") as f:
         json.dump(model.to_json(), f, indent=1)
@@ -674,6 +709,8 @@ def generate(out_dir, which=None):
         "wb700": (lambda: wb700(True), [("dance", lambda m: dance_clip(m, 1101)),
                                          ("backflip", lambda m: backflip_clip(m, 1101))]),
         "wb700_fixed": (lambda: wb700(False), [("dance", lambda m: dance_clip(m, 1101))]),
+        "wb700_general": (wb700_general, []),  # clip: wb700_fixed_dance (same tree)
+        "wb700_slow": (wb700_slow, []),  # clip: wb700_dance (same tree)
     }
     written = []
     for name, (mk, clips) in jobs.items():
