@@ -172,6 +172,20 @@ def summarize_clocks(lines, t0=None, t1=None):
 
 
 # ----------------------------------------------------------------------------
+def cpu_model():
+    """Host CPU model name and logical core count (for the CPU-arm lines)."""
+    name = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    name = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"model": name, "logical_cpus": os.cpu_count()}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path (oracle/_ref) on the host cores."""
     if rank != 0:
@@ -181,7 +195,7 @@ def run_reference(args, rank, world):
     mp, cp = model_files(args.model)
     C = args.C
     threads = args.cpu_threads or os.cpu_count() or 1
-    n_envs = args.ref_envs or max(threads, 8)
+    n_envs = args.ref_envs or 8 * threads  # E_cpu = 8 x cores
     cfg = env_config(episode_horizon=C["horizon"], rsi=C["rsi"])
     b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads, reward_mode=C["reward_mode"])
     b.set_eval_mode(C["eval"])
@@ -199,7 +213,8 @@ def run_reference(args, rank, world):
                        "config": args.config, "envs": n_envs,
                        "parallelism": f"{threads} host threads (ThreadPool::parallel_chunks)"},
             "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "reference",
-                             "sample": f"{n_envs} envs x {args.steps} control steps"},
+                             "sample": f"{n_envs} envs x {args.steps} control steps ({secs:.1f} s)",
+                             "cpu": cpu_model()},
             "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -211,7 +226,7 @@ def cpu_baseline_sample(args):
     mp, cp = model_files(args.model)
     C = args.C
     threads = args.cpu_threads or os.cpu_count() or 1
-    n_envs = max(threads, 8)
+    n_envs = 8 * threads  # E_cpu = 8 x cores
     b = RefBatch(mp, cp, n_envs, cfg=env_config(episode_horizon=C["horizon"], rsi=C["rsi"]), threads=threads,
                  reward_mode=C["reward_mode"])
     b.set_eval_mode(C["eval"])
@@ -222,7 +237,7 @@ def cpu_baseline_sample(args):
     k = max(1, min(5000, int(args.cpu_seconds / max(per_step, 1e-3))))
     secs, steps = b.bench(k)
     return {"value": steps / secs, "unit": "env-steps/s", "cores": threads, "kind": "reference",
-            "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)"}
+            "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)", "cpu": cpu_model()}
 
 
 def self_launch(n):
@@ -281,7 +296,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="envs per GPU (default: the config's)")
     ap.add_argument("--model", default="", help="override the config's model")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--ref-envs", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

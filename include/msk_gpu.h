@@ -189,6 +189,14 @@ int msk_gpu_host_wait(msk_gpu_ctx* ctx);
  * harness double-buffers several contexts with msk_gpu_step_host_async). */
 int msk_gpu_set_host_pipeline(msk_gpu_ctx* ctx, int32_t chunks, int32_t streams);
 
+/* Diagnostics / parity: advance every active env's continuous state (q, q̇,
+ * muscles, t) by n_substeps (1..9) 2 ms substeps of msk::step's loop body
+ * (skeleton.cpp:295-329) with the given excitations, WITHOUT the env epilogue
+ * (no t_index / observation / termination).  Lets a test compare forces and
+ * accelerations from an identical state before they feed back into the state. */
+int msk_gpu_substeps(msk_gpu_ctx* ctx, const float* actions, int32_t n_substeps, float* muscle_power,
+                     float* contact_force, void* stream);
+
 int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream);
 int msk_gpu_tracking_error(msk_gpu_ctx* ctx, float* delta, void* stream);
 int msk_gpu_force_state_to_reference(msk_gpu_ctx* ctx, void* stream);

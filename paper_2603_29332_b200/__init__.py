@@ -387,6 +387,7 @@ def lib():
         L.msk_gpu_merge_outcomes.argtypes = [_vp, _vp, _vp, _vp, C.c_int64, C.c_int32, _vp]
         L.msk_gpu_rng_raw.argtypes = [_vp, C.c_int32, C.c_int32, _vp, _vp]
         L.msk_gpu_get_rng.argtypes = [_vp, _vp, _vp, _vp]
+        L.msk_gpu_substeps.argtypes = [_vp, _vp, C.c_int32, _vp, _vp, _vp]
         L.msk_gpu_set_rng.argtypes = [_vp, _vp, _vp, _vp]
         L.msk_gpu_set_outcome_capacity.argtypes = [_vp, C.c_int32, _vp]
         L.msk_gpu_outcomes_dropped.argtypes = [_vp, C.POINTER(C.c_int64)]
@@ -408,7 +409,7 @@ def lib():
                      "msk_gpu_set_state", "msk_gpu_get_sampler", "msk_gpu_set_sampler", "msk_gpu_drain_outcomes",
                      "msk_gpu_record_own_outcomes", "msk_gpu_merge_outcomes", "msk_gpu_rng_raw",
                      "msk_gpu_fill_excitations", "msk_gpu_get_rng", "msk_gpu_set_rng",
-                     "msk_gpu_set_outcome_capacity", "msk_gpu_outcomes_dropped"):
+                     "msk_gpu_set_outcome_capacity", "msk_gpu_outcomes_dropped", "msk_gpu_substeps"):
             getattr(L, name).restype = C.c_int
         _LIB = L
     return _LIB
@@ -666,6 +667,11 @@ class EnvBatch:
                                                   _p(obs.contiguous()), _p(stats), _p(norm), _p(stats_out),
                                                   self._s(stream)))
         return stats_out
+
+    def substeps(self, actions, n_substeps, stream=None):
+        """msk_gpu_substeps: n (< 10) substeps of the continuous state, no env epilogue (parity diagnostics)."""
+        a = actions if actions.dtype == self.torch.float32 and actions.is_contiguous() else actions.float().contiguous()
+        self._ck(lib().msk_gpu_substeps(self.h, _p(a), int(n_substeps), None, None, self._s(stream)))
 
     def get_rng(self, stream=None):
         """(mt [E x 312] int64 (u64 bits), mti [E] int32): every env's mt19937_64 engine state."""

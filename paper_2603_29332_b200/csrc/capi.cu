@@ -22,7 +22,7 @@ namespace msk_b200 {
 cudaError_t prepare_kernels(int smem_bytes_per_block);
 int envs_per_block();
 void launch_step(const DevModel&, const DevState&, int env0, int n, const float* actions, float* obs, float* delta,
-                 float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t);
+                 float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t, int n_substeps = kSubsteps);
 void launch_reset(const DevModel&, const DevState&, int n, int mode, const uint8_t* mask, uint8_t bits,
                   const int* frames_in, float* obs, int* frames_out, uint8_t* bad, cudaStream_t);
 void launch_observe(const DevModel&, const DevState&, int n, float* obs, float* delta, cudaStream_t);
@@ -546,6 +546,18 @@ int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delt
         launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, obs, delta, reward_aux, flags, muscle_power,
                     contact_force, as_stream(stream));
         ctx->count(2);  // prep_actions + step
+        ctx->check_launch();
+    });
+}
+
+int msk_gpu_substeps(msk_gpu_ctx* ctx, const float* actions, int32_t n_substeps, float* muscle_power,
+                     float* contact_force, void* stream) {
+    return guarded(ctx, [&] {
+        if (!actions || n_substeps < 1 || n_substeps >= kSubsteps)
+            throw ConfigError("substeps: actions required and 1 <= n_substeps < 10");
+        launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, nullptr, nullptr, nullptr, nullptr, muscle_power,
+                    contact_force, as_stream(stream), n_substeps);
+        ctx->count(2);
         ctx->check_launch();
     });
 }

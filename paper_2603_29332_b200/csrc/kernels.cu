@@ -983,7 +983,9 @@ template <int WPB, int MINB, int NSEG, int EPW, int QSL>
 __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevState St, int env0, int n_envs,
                                                               const float* __restrict__ actions, float* obs,
                                                               float* delta, float* reward_aux, uint8_t* flags,
-                                                              float* power, float* grf) {
+                                                              float* power, float* grf, int n_substeps) {
+    // n_substeps: kSubsteps for Env::step; fewer only for the msk_gpu_substeps
+    // diagnostic (state advanced by that many substeps, no env epilogue)
     extern __shared__ __align__(16) unsigned char smem[];
     static_assert(QSL >= 1 && QSL <= kMaxQSlots, "DOF slots");
     constexpr int G = 32 / EPW, QS = QSL * EPW;
@@ -1027,11 +1029,11 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
 
     PHASE_T0();
     int diverged_at = -1;
-    for (int sub = 0; sub < kSubsteps; ++sub) {
+    for (int sub = 0; sub < n_substeps; ++sub) {
         if (M.has_general) fk_d(M, S, lane);  // f64 world frames of the general segments
 
         // ---- 1. muscles + J_m^T F contributions ----
-        muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane, sub == kSubsteps - 1);
+        muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane, sub == n_substeps - 1);
         __syncwarp(S.hm);
 
         PHASE_MARK(0);
@@ -1112,12 +1114,13 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
             St.dq[static_cast<size_t>(e) * nq + d] = dqd[k];
         }
     }
-    const int n_sub = diverged_at >= 0 ? diverged_at + 1 : kSubsteps;
+    const int n_sub = diverged_at >= 0 ? diverged_at + 1 : n_substeps;
     if (lane == 0) {
         double t = St.t[e];
         for (int s = 0; s < n_sub; ++s) t += kSimDt;
         St.t[e] = t;
     }
+    if (n_substeps != kSubsteps) return;  // msk_gpu_substeps: continuous state only
     const int obs_dim = 3 * nq + 6 * M.nk + 4 * nm;
     const int ddim = 3 + M.nj + 2 * M.nk;
     float* obs_row = obs ? obs + static_cast<size_t>(le) * obs_dim : nullptr;
@@ -1630,12 +1633,13 @@ cudaError_t prepare_kernels(int smem_bytes_per_block) {
 int envs_per_block() { return kEnvsPerBlock; }
 
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
-                 float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s) {
+                 float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s,
+                 int n_substeps) {
     const int blocks = (n + M.epb - 1) / M.epb;
     const size_t smem = block_smem(M);
 #define MSK_STEP(NS, QSL)                                                                                  \
     step_kernel<kWPB, kMinB, NS, kEPW, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, \
-                                                                            raux, flags, power, grf)
+                                                                            raux, flags, power, grf, n_substeps)
     prep_actions_kernel<<<(n + 7) / 8, 256, 0, s>>>(M, St, env0, n, actions);
     const int v = step_variant(M);
     if (step_qslots(M) == 3 && (v == 0 || v == 2 || v == 3)) {  // whole-body sized models

@@ -55,7 +55,8 @@ def main():
     with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as f:
         json.dump(js, f)
         pert = f.name
-    worst, rels, norm = 0.0, [], 0.0
+    worst, rels, norm, fr = 0.0, [], 0.0, 0.0
+    fmax = np.array([mu["f_max"] for mu in json.load(open(mp))["muscles"]])
     for trial in range(3):
         a = one(mp, cp, 3, 0, eps, trial)
         b = one(pert, cp, 3, 0, eps, trial)
@@ -63,11 +64,15 @@ def main():
         worst = max(worst, float((d / np.maximum(1e-5 * np.abs(a["dq"]), 1e-6)).max()))
         rels.append((d / np.maximum(np.abs(a["dq"]), 1e-3)).ravel())
         norm = max(norm, float((d.max(axis=1) / np.abs(a["dq"]).max(axis=1)).max()))
+        # end-of-step muscle forces vs the SURVEY bound 1e-4 max(|F|, 1e-3 f_max), minus the
+        # perturbation itself (b's forces are scaled by its f_max)
+        fb = b["f_m"] * (fmax / np.array([mu["f_max"] for mu in js["muscles"]]))[None, :]
+        fr = max(fr, float((np.abs(a["f_m"] - fb) / (1e-4 * np.maximum(np.abs(a["f_m"]), 1e-3 * fmax))).max()))
     os.unlink(pert)
     r = np.concatenate(rels)
     print(f"{name}: force perturbation eps {eps:.1e} -> per-element q̇ ratio (1e-5 rel, 1e-6 floor) worst "
           f"{worst:.2f}; |Δq̇|/max(|q̇|,1e-3) quantiles 50% {np.quantile(r, .5):.2e} 99% {np.quantile(r, .99):.2e} "
-          f"max {r.max():.2e}; norm-wise max|Δq̇|/max|q̇| {norm:.2e}")
+          f"max {r.max():.2e}; norm-wise max|Δq̇|/max|q̇| {norm:.2e}; end-of-step force ratio {fr:.2f}")
 
 
 if __name__ == "__main__":

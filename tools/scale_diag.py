@@ -55,6 +55,10 @@ def main():
             oo = o.step(excitations(0x5EED, s, 1, g.nm, global_env_offset=e))
             so = o.get_state()
             rq, rd = q_ratio(post["q"][k], so["q"][0]), q_ratio(post["dq"][k], so["dq"][0])
+            dd_ = np.abs(post["dq"][k] - so["dq"][0])
+            i_ = int(np.argmax(dd_ / np.maximum(1e-3 * np.abs(so["dq"][0]), 5e-5)))
+            print(f"  step {s} env {e}: max|q̇| {np.abs(so['dq'][0]).max():.3g} (dof {int(np.argmax(np.abs(so['dq'][0])))}),"
+                  f" worst dof {i_}: |d| {dd_[i_]:.3g} ref {so['dq'][0][i_]:.4g}; max|d| {dd_.max():.3g}")
             if rq > 1 or rd > 1:
                 grf_o = np.asarray(oo["grf"]).reshape(-1)
                 dd = np.abs(cf[e].reshape(-1) - grf_o)
