@@ -21,6 +21,7 @@
 namespace msk_b200 {
 cudaError_t prepare_kernels(int smem_bytes_per_block);
 int envs_per_block();
+int lanes_per_env();
 void launch_step(const DevModel&, const DevState&, int env0, int n, const float* actions, float* obs, float* delta,
                  float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t, int n_substeps = kSubsteps);
 void launch_reset(const DevModel&, const DevState&, int n, int mode, const uint8_t* mask, uint8_t bits,
@@ -298,6 +299,22 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         }
         M.max_seg = c.max_seg;
         M.has_general = c.has_general;
+        {  // chunk runs by padded segment count (muscles are sorted by it): a lane group's
+           // chunk of G consecutive muscles pads to the count of its last muscle
+            const int G = lanes_per_env();
+            std::vector<int> chunk_ns;
+            for (int m0 = 0; m0 < c.nm; m0 += G) chunk_ns.push_back(c.pk_meta[std::min(m0 + G, c.nm) - 1] & 0xff);
+            for (int k = 0; k <= 5; ++k) {
+                int m = c.nm;
+                for (size_t ch = 0; ch < chunk_ns.size(); ++ch)
+                    if (chunk_ns[ch] >= k) {
+                        m = static_cast<int>(ch) * G;
+                        break;
+                    }
+                M.seg_run[k] = k == 5 ? c.nm : m;
+            }
+            M.seg_run[0] = 0;
+        }
         M.link_parent = ctx->upload(c.link_parent);
         M.link_dof = ctx->upload(c.link_dof);
         M.link_inertia = ctx->upload(c.link_inertia);

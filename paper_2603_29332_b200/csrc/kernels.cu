@@ -713,47 +713,39 @@ __device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, in
 }
 
 // Inputs of one muscle for the fast path (all loads issued before any math).
-template <int NSEG>
-struct MuscleIn {
-    float4 kc[NSEG];
-    float4 p0;
-    double2 pa, pb;
-    float u, a0;
-    double lm0;
-    int ext, nsc;
-};
-
-template <int NSEG>
-__device__ __forceinline__ void muscle_load(const DevModel& M, const DevState& St, const float* act_row, size_t mb,
-                                            int m, int chunk_last, MuscleIn<NSEG>& x) {
+// One muscle of a chunk whose muscles all have (at most) NS segments — NS is
+// a compile-time constant: the segment loop unrolls without predicates (padding
+// segments have K = 0 and write the dummy slot) and the per-segment smem
+// address arithmetic is shared.
+template <int NS>
+__device__ __forceinline__ void muscle_one(const DevModel& M, const DevState& St, const EnvSmem& S,
+                                           const float* act_row, size_t mb, float* pw, int m, bool last) {
     const int nm = M.nm;
-    // muscles are sorted by segment count: the warp's chunk pads to the count of
-    // its last muscle (a warp-uniform bound <= NSEG)
-    x.nsc = __ldg(M.m_meta + chunk_last) & 0xff;
-    x.ext = __ldg(M.m_meta + m) >> 9;
+    float4 kc[NS > 0 ? NS : 1];
 #pragma unroll
-    for (int k = 0; k < NSEG; ++k)
-        if (k < x.nsc) x.kc[k] = ldc4(M.seg_kf + k * nm + m);
-    x.p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
-    x.pa = ldc2d(M.m_p1a + m);
-    x.pb = ldc2d(M.m_p1b + m);
-    x.u = act_row[m];  // clamped, device order (prep_actions_kernel)
-    x.a0 = St.act[mb + m];
-    x.lm0 = St.lm[mb + m];
+    for (int k = 0; k < NS; ++k) kc[k] = ldc4(M.seg_kf + k * nm + m);
+    const float4 p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
+    const double2 pa = ldc2d(M.m_p1a + m), pb = ldc2d(M.m_p1b + m);
+    const float u = act_row[m];  // clamped, device order (prep_actions_kernel)
+    const float a0 = St.act[mb + m];
+    const double lm0 = St.lm[mb + m];
+    const int ext = pw ? (__ldg(M.m_meta + m) >> 9) : 0;  // reference index: power output only
+    double L = 0.0;
+    float tq[NS > 0 ? NS : 1];
+#pragma unroll
+    for (int k = 0; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
+    const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
+#pragma unroll
+    for (int k = 0; k < NS; ++k) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
 }
 
-template <int NSEG>
-__device__ __forceinline__ void muscle_compute(const EnvSmem& S, const DevState& St, size_t mb, float* pw, int m,
-                                               const MuscleIn<NSEG>& x, bool last) {
-    double L = 0.0;
-    float tq[NSEG];
-#pragma unroll
-    for (int k = 0; k < NSEG; ++k)
-        if (k < x.nsc) L += kseg(S, x.kc[k], __float_as_int(x.kc[k].w), tq[k]);
-    const float F = muscle_update(St, mb, m, x.ext, x.p0, x.pa, x.pb, x.u, x.a0, x.lm0, L, pw, last);
-#pragma unroll
-    for (int k = 0; k < NSEG; ++k)
-        if (k < x.nsc) S.un[__float_as_int(x.kc[k].w) >> 11] = -F * tq[k];
+// Muscles [m0, m1) (whole chunks of the lane group, muscles sorted by segment
+// count) with NS segments each.
+template <int NS>
+__device__ __forceinline__ void muscle_run(const DevModel& M, const DevState& St, const EnvSmem& S,
+                                           const float* act_row, size_t mb, float* pw, int lane, bool last, int m0,
+                                           int m1) {
+    for (int m = m0 + lane; m < m1; m += S.G) muscle_one<NS>(M, St, S, act_row, mb, pw, m, last);
 }
 
 template <int NSEG>
@@ -761,11 +753,12 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
                                              const float* act_row, size_t mb, float* pw, int lane, bool last) {
     const int nm = M.nm;
     if constexpr (NSEG > 0) {
-        for (int m = lane; m < nm; m += S.G) {
-            MuscleIn<NSEG> x;
-            muscle_load<NSEG>(M, St, act_row, mb, m, min(m - lane + S.G - 1, nm - 1), x);
-            muscle_compute<NSEG>(S, St, mb, pw, m, x, last);
-        }
+        // runs of chunks by padded segment count (M.seg_run, muscle units): 0, 1, ..., NSEG
+        muscle_run<0>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[0], M.seg_run[1]);
+        if constexpr (NSEG >= 1) muscle_run<1>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[1], M.seg_run[2]);
+        if constexpr (NSEG >= 2) muscle_run<2>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[2], M.seg_run[3]);
+        if constexpr (NSEG >= 3) muscle_run<3>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[3], M.seg_run[4]);
+        if constexpr (NSEG >= 4) muscle_run<4>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[4], M.seg_run[5]);
     } else {
         for (int m = lane; m < nm; m += S.G) {
             const int meta = __ldg(M.m_meta + m);
@@ -1631,6 +1624,7 @@ cudaError_t prepare_kernels(int smem_bytes_per_block) {
 }
 
 int envs_per_block() { return kEnvsPerBlock; }
+int lanes_per_env() { return 32 / kEPW; }
 
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
                  float* delta, float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t s,
