@@ -166,11 +166,13 @@ __device__ __forceinline__ float hill_fl(float l) {  // exp(-((l-1)/0.45)^2)
     const float d = l - 1.0f;
     return ex2_ftz(d * d * (-kLog2e / (0.45f * 0.45f)));
 }
-__device__ __forceinline__ float hill_fv(float v) {
-    if (v <= -1.0f) return 0.0f;
-    if (v < 0.0f) return (v + 1.0f) * rcp_ftz(fmaf(-0.25f, v, 1.0f));
+__device__ __forceinline__ float hill_fv(float v) {  // branch-free: one reciprocal, selects
     constexpr float c = 0.32f;  // (1.4 - 1) / (1 + 1/4)
-    return fmaf(1.4f, v, c) * rcp_ftz(v + c);
+    const bool neg = v < 0.0f;
+    const float num = neg ? v + 1.0f : fmaf(1.4f, v, c);
+    const float den = neg ? fmaf(-0.25f, v, 1.0f) : v + c;
+    const float fv = num * rcp_ftz(den);
+    return v <= -1.0f ? 0.0f : fv;
 }
 __device__ __forceinline__ float hill_fp(float l) {  // (exp(4(l-1)) - 1) / (e^2 - 1)
     if (l <= 1.0f) return 0.0f;
@@ -688,7 +690,20 @@ __device__ int rsi_frame(const DevModel& M, const DevState& St, int e) {
 // substep's path length to ~1e-16 (v_m divides the difference by dt l_opt v_max,
 // ~1e-3), as in the reference's f64 SimState.  v_m / f_m are stored only at the
 // last substep (nothing reads them in between).
-__device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, int m, int ext, float4 p0, double2 pa,
+// This env's muscle rows (device order), formed once per run of the muscle phase.
+struct MuscleRows {
+    const float* u;  // the step's clamped excitations
+    float* act;
+    double* lm;
+    float* vm;
+    float* fm;
+};
+
+__device__ __forceinline__ MuscleRows muscle_rows(const DevState& St, const float* act_row, size_t mb) {
+    return MuscleRows{act_row, St.act + mb, St.lm + mb, St.vm + mb, St.fm + mb};
+}
+
+__device__ __forceinline__ float muscle_update(const MuscleRows& R, int m, int ext, float4 p0, double2 pa,
                                                double2 pb, float u, float a0, double lm0, double L, float* pw,
                                                bool last) {
     const float gain = fmaf(1.5f, a0, 0.5f);
@@ -702,11 +717,11 @@ __device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, in
 #else
     const float F = mtu_force(a1, static_cast<float>(lm1), vm, p0.x);
 #endif
-    St.act[mb + m] = a1;
-    St.lm[mb + m] = lm1;
+    R.act[m] = a1;
+    R.lm[m] = lm1;
     if (last) {
-        St.vm[mb + m] = vm;
-        St.fm[mb + m] = F;
+        R.vm[m] = vm;
+        R.fm[m] = F;
     }
     if (pw) pw[ext] += fabsf(F * vm * p0.w);
     return F;
@@ -718,23 +733,23 @@ __device__ __forceinline__ float muscle_update(const DevState& St, size_t mb, in
 // segments have K = 0 and write the dummy slot) and the per-segment smem
 // address arithmetic is shared.
 template <int NS>
-__device__ __forceinline__ void muscle_one(const DevModel& M, const DevState& St, const EnvSmem& S,
-                                           const float* act_row, size_t mb, float* pw, int m, bool last) {
+__device__ __forceinline__ void muscle_one(const DevModel& M, const MuscleRows& R, const EnvSmem& S, float* pw, int m,
+                                           bool last) {
     const int nm = M.nm;
     float4 kc[NS > 0 ? NS : 1];
 #pragma unroll
     for (int k = 0; k < NS; ++k) kc[k] = ldc4(M.seg_kf + k * nm + m);
     const float4 p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
     const double2 pa = ldc2d(M.m_p1a + m), pb = ldc2d(M.m_p1b + m);
-    const float u = act_row[m];  // clamped, device order (prep_actions_kernel)
-    const float a0 = St.act[mb + m];
-    const double lm0 = St.lm[mb + m];
+    const float u = R.u[m];  // clamped, device order (prep_actions_kernel)
+    const float a0 = R.act[m];
+    const double lm0 = R.lm[m];
     const int ext = pw ? (__ldg(M.m_meta + m) >> 9) : 0;  // reference index: power output only
     double L = 0.0;
     float tq[NS > 0 ? NS : 1];
 #pragma unroll
     for (int k = 0; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
-    const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
+    const float F = muscle_update(R, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
 #pragma unroll
     for (int k = 0; k < NS; ++k) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
 }
@@ -745,7 +760,9 @@ template <int NS>
 __device__ __forceinline__ void muscle_run(const DevModel& M, const DevState& St, const EnvSmem& S,
                                            const float* act_row, size_t mb, float* pw, int lane, bool last, int m0,
                                            int m1) {
-    for (int m = m0 + lane; m < m1; m += S.G) muscle_one<NS>(M, St, S, act_row, mb, pw, m, last);
+    if (m0 + lane >= m1) return;
+    const MuscleRows R = muscle_rows(St, act_row, mb);
+    for (int m = m0 + lane; m < m1; m += S.G) muscle_one<NS>(M, R, S, pw, m, last);
 }
 
 template <int NSEG>
@@ -765,9 +782,10 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
             const int nseg = meta & 0xff, ext = meta >> 9;
             const float4 p0 = __ldg(M.m_p0 + m);
             const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
-            const float u = act_row[m];
-            const float a0 = St.act[mb + m];
-            const double lm0 = St.lm[mb + m];
+            const MuscleRows R = muscle_rows(St, act_row, mb);
+            const float u = R.u[m];
+            const float a0 = R.act[m];
+            const double lm0 = R.lm[m];
             double L = 0.0;
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
@@ -775,7 +793,7 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
                 float arm;
                 L += (info & 3) == 2 ? general_seg_len(M, S, info >> 11) : kseg(S, kf, info, arm);
             }
-            const float F = muscle_update(St, mb, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
+            const float F = muscle_update(R, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
             for (int k = 0; k < nseg; ++k) {
                 const float4 kf = __ldg(M.seg_kf + k * nm + m);
                 const int info = __float_as_int(kf.w);
@@ -828,7 +846,7 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
                 continue;
             }
             // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
-            const float invD = 1.0f / I00;
+            const float invD = rcp_ftz(I00);  // (IEEE 1/x costs a range check + slow-path call)
             const float t = S.tau[dof];
             const float uu = (t - P0) * invD;               // u / D
             const float U1 = I01 * invD, U2 = I02 * invD;   // U / D
@@ -862,18 +880,18 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
 // q̈ into S.tau.
 __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, int lane) {
     if (M.floating && lane == 0) {
-        float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky)
-        const float l00 = sqrtf(u[0]);
-        const float l10 = u[1] / l00, l20 = u[2] / l00;
-        const float l11 = sqrtf(u[3] - l10 * l10);
-        const float l21 = (u[4] - l20 * l10) / l11;
-        const float l22 = sqrtf(u[5] - l20 * l20 - l21 * l21);
-        const float y0 = -u[6] / l00;
-        const float y1 = (-u[7] - l10 * y0) / l11;
-        const float y2 = (-u[8] - l20 * y0 - l21 * y1) / l22;
-        const float x2 = y2 / l22;
-        const float x1 = (y1 - l21 * x2) / l11;
-        const float x0 = (y0 - l10 * x1 - l20 * x2) / l00;
+        float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky with reciprocal pivots)
+        const float i00 = rsqrt_ftz(u[0]);
+        const float l10 = u[1] * i00, l20 = u[2] * i00;
+        const float i11 = rsqrt_ftz(u[3] - l10 * l10);
+        const float l21 = (u[4] - l20 * l10) * i11;
+        const float i22 = rsqrt_ftz(u[5] - l20 * l20 - l21 * l21);
+        const float y0 = -u[6] * i00;
+        const float y1 = (-u[7] - l10 * y0) * i11;
+        const float y2 = (-u[8] - l20 * y0 - l21 * y1) * i22;
+        const float x2 = y2 * i22;
+        const float x1 = (y1 - l21 * x2) * i11;
+        const float x0 = (y0 - l10 * x1 - l20 * x2) * i00;
         u[0] = x0;
         u[1] = x1;
         u[2] = x2;
