@@ -121,8 +121,13 @@ int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delt
  * D = Mlp(in = delta_dim, hidden, out = 1, Head::Sigmoid) given by its flat f64
  * parameters in the reference layout (nn.cpp:16-38: W1 b1 W2 b2 W3 b3 W4 b4,
  * W column-major).  hidden: multiple of 16 in [16, 256].  Evaluated on the
- * tcgen05 tensor cores with bf16 operands and fp32 accumulation. */
+ * tcgen05 tensor cores with fp32 accumulation; by default every operand is
+ * split as hi + lo bf16 (3 MMAs per product, accurate tanh/exp/log): fp32-class,
+ * ~1e-6 relative to the f64 Mlp (tests: <= 1e-5).  msk_gpu_set_discriminator_mode(ctx, 1)
+ * selects the bf16-operand fast mode (~3e-3). */
 int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_params, int32_t hidden);
+/* 0: fp32-class split-bf16 (default); 1: bf16 operands (fast). */
+int msk_gpu_set_discriminator_mode(msk_gpu_ctx* ctx, int32_t mode);
 /* Host helpers for the parameter blob: Mlp(in, hidden, out) parameter count and
  * the Mlp(shape, seed) initialisation (nn.cpp:16-38, msk::Rng = mt19937_64). */
 int64_t msk_mlp_param_count(int32_t in, int32_t hidden, int32_t out);

@@ -369,6 +369,7 @@ def lib():
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_iteration_exchange.argtypes = [_vp, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
+        L.msk_gpu_set_discriminator_mode.argtypes = [_vp, C.c_int32]
         L.msk_mlp_param_count.restype = C.c_int64
         L.msk_mlp_param_count.argtypes = [C.c_int32, C.c_int32, C.c_int32]
         L.msk_mlp_init.argtypes = [_vp, C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_double]
@@ -510,6 +511,10 @@ class EnvBatch:
         th = np.ascontiguousarray(np.asarray(theta, dtype=np.float64))
         self._ck(lib().msk_gpu_set_discriminator(self.h, th.ctypes.data, th.size, int(hidden)))
         self._disc = True
+
+    def set_discriminator_mode(self, fast):
+        """False (default): fp32-class split-bf16 operands; True: bf16 operands (fast)."""
+        self._ck(lib().msk_gpu_set_discriminator_mode(self.h, 1 if fast else 0))
 
     def clear_discriminator(self):
         self._ck(lib().msk_gpu_clear_discriminator(self.h))

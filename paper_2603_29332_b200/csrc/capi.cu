@@ -105,6 +105,7 @@ struct msk_gpu_ctx {
     // device discriminator (msk_gpu_set_discriminator)
     DiscDev disc{};
     std::vector<void*> disc_allocs;
+    bool disc_fast = false;  // msk_gpu_set_discriminator_mode: bf16 fast mode instead of split-bf16
     // iteration exchange (msk_gpu_iteration_exchange): this rank's block and the gathered blocks
     unsigned char* x_block = nullptr;
     unsigned char* x_gathered = nullptr;
@@ -579,6 +580,14 @@ int msk_gpu_substeps(msk_gpu_ctx* ctx, const float* actions, int32_t n_substeps,
     });
 }
 
+int msk_gpu_set_discriminator_mode(msk_gpu_ctx* ctx, int32_t mode) {
+    return guarded(ctx, [&] {
+        if (mode != 0 && mode != 1) throw ConfigError("set_discriminator_mode: mode must be 0 (fp32-class) or 1 (bf16)");
+        ctx->disc_fast = mode == 1;
+        ctx->disc.precise = ctx->disc_fast ? 0 : 1;
+    });
+}
+
 int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_params, int32_t hidden) {
     return guarded(ctx, [&] {
         if (!theta) throw ConfigError("set_discriminator: theta is null");
@@ -602,6 +611,13 @@ int msk_gpu_set_discriminator(msk_gpu_ctx* ctx, const double* theta, int64_t n_p
         d.w2 = up(h.w2.data(), h.w2.size() * 2);
         d.w3 = up(h.w3.data(), h.w3.size() * 2);
         d.bias = static_cast<const float*>(up(h.bias.data(), h.bias.size() * 4));
+        d.c_hi[0] = up(h.c1_hi.data(), h.c1_hi.size() * 2);
+        d.c_lo[0] = up(h.c1_lo.data(), h.c1_lo.size() * 2);
+        d.c_hi[1] = up(h.c2_hi.data(), h.c2_hi.size() * 2);
+        d.c_lo[1] = up(h.c2_lo.data(), h.c2_lo.size() * 2);
+        d.c_hi[2] = up(h.c3_hi.data(), h.c3_hi.size() * 2);
+        d.c_lo[2] = up(h.c3_lo.data(), h.c3_lo.size() * 2);
+        d.precise = ctx->disc_fast ? 0 : 1;
         ck(prepare_disc(d), "cudaFuncSetAttribute(disc)");
         ctx->disc = d;
         if (!ctx->r_delta) {

@@ -247,10 +247,192 @@ __global__ void __launch_bounds__(kThreads, 1)
                      : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// fp32-class mode (split bf16): every operand x = hi + lo with hi = bf16(x),
+// lo = bf16(x - hi) (16 significant bits), and each product A W^T is formed
+// as A_hi W_hi + A_hi W_lo + A_lo W_hi on the tensor cores with fp32
+// accumulation in TMEM (the dropped A_lo W_lo term and the residual of the
+// split are ~2^-16 relative); tanh / exp / log are the accurate fp32 ones.
+// The activations (A hi / lo, 128 x K) stay in shared memory; the weights are
+// streamed in K16 chunks (hi + lo, N x 16 each) through a 4-stage TMA ring, one
+// thread issuing the bulk copies and the MMAs (3 per chunk, commit per chunk
+// frees its stage).
+// ---------------------------------------------------------------------------
+constexpr int kRing = 4;
+
+// element (r, kk) of a K16 chunk image (N rows x 16 K): two 8-K core-matrix columns
+__host__ __device__ constexpr uint32_t chunk_off(int r, int kk) {
+    return static_cast<uint32_t>(((r >> 3) * 2 + (kk >> 3)) * 128 + (r & 7) * 16 + (kk & 7) * 2);
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem, uint64_t da, uint64_t dw, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(da), "l"(dw), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bfloat16& lo) {
+    hi = __float2bfloat16_rn(x);
+    lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    disc_reward_precise_kernel(DiscDev P, const float* __restrict__ delta, int ld, int n, const float* __restrict__ raux,
+                               const uint8_t* __restrict__ flags, float* __restrict__ reward) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int H = P.hidden, K1 = P.k1, Kmax = K1 > H ? K1 : H;
+    const uint32_t chunk_bytes = static_cast<uint32_t>(H) * 32;   // N x 16 bf16
+    char* sa_hi = reinterpret_cast<char*>(smem);                     // 128 x Kmax bf16
+    char* sa_lo = sa_hi + kTileM * Kmax * 2;
+    char* ring = sa_lo + kTileM * Kmax * 2;                          // kRing x (hi | lo) chunks
+    float* sb = reinterpret_cast<float*>(ring + kRing * 2 * chunk_bytes);  // b1 b2 b3 w4
+    uint64_t* full = reinterpret_cast<uint64_t*>(sb + 4 * H);      // [kRing]
+    uint64_t* empty = full + kRing;                                  // [kRing]
+    uint64_t* done = empty + kRing;                                  // [1] layer's MMAs complete
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int row0 = blockIdx.x * kTileM;
+
+    if (tid == 0) {
+        for (int i = 0; i < kRing; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(P.tmem_cols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    for (int i = tid; i < 4 * H; i += kThreads) sb[i] = P.bias[i];
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // ring bookkeeping (thread 0 only): chunks consumed from each stage so far.  A
+    // stage's n-th load completes full[] phase n and its n-th commit empty[] phase
+    // n; a stage is refilled only after its last commit, so no phase is skipped.
+    uint32_t uses[kRing] = {0, 0, 0, 0};
+    auto load_chunk = [&](int layer, int c, int st) {
+        mbar_expect_tx(&full[st], 2 * chunk_bytes);
+        bulk_g2s(ring + (2 * st) * chunk_bytes, static_cast<const char*>(P.c_hi[layer]) + c * chunk_bytes, chunk_bytes,
+                 &full[st]);
+        bulk_g2s(ring + (2 * st + 1) * chunk_bytes, static_cast<const char*>(P.c_lo[layer]) + c * chunk_bytes,
+                 chunk_bytes, &full[st]);
+    };
+    if (tid == 0)  // the first layer's leading chunks do not depend on Δ
+        for (int c = 0; c < kRing && c < K1 / 16; ++c) load_chunk(0, c, c);
+
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // Δ = the previous kernel's output
+    for (int i = tid; i < kTileM * K1; i += kThreads) {
+        const int r = i / K1, k = i - r * K1, row = row0 + r;
+        const float x = (row < n && k < P.din) ? delta[static_cast<size_t>(row) * ld + k] : 0.0f;
+        __nv_bfloat16 hi, lo;
+        split_bf16(x, hi, lo);
+        *reinterpret_cast<__nv_bfloat16*>(sa_hi + img_off(r, k, K1)) = hi;
+        *reinterpret_cast<__nv_bfloat16*>(sa_lo + img_off(r, k, K1)) = lo;
+    }
+    proxy_fence();
+    __syncthreads();
+
+    const int r = warp * 32 + lane;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    const uint32_t idesc = instr_desc(H);
+    uint32_t done_phase = 0;
+    for (int layer = 0; layer < 3; ++layer) {
+        const int K = layer == 0 ? K1 : H, nch = K / 16;
+        if (tid == 0) {
+            if (layer > 0)  // stages are free (the previous layer's MMAs completed)
+                for (int c = 0; c < kRing && c < nch; ++c) load_chunk(layer, c, c);
+            const uint32_t a_hi = smem_u32(sa_hi), a_lo = smem_u32(sa_lo), sbo = static_cast<uint32_t>(K >> 3) * 128;
+            for (int c = 0; c < nch; ++c) {
+                const int st = c % kRing;
+                mbar_wait(&full[st], uses[st] & 1);
+                ++uses[st];
+                tc_fence_after();
+                const uint32_t w_hi = smem_u32(ring + (2 * st) * chunk_bytes), w_lo = w_hi + chunk_bytes;
+                const uint64_t dah = smem_desc(a_hi + 256 * c, 128, sbo), dal = smem_desc(a_lo + 256 * c, 128, sbo);
+                const uint64_t dwh = smem_desc(w_hi, 128, 256), dwl = smem_desc(w_lo, 128, 256);
+                mma_f16(tmem, dal, dwh, idesc, c > 0);  // small terms first
+                mma_f16(tmem, dah, dwl, idesc, 1);
+                mma_f16(tmem, dah, dwh, idesc, 1);
+                mma_commit(&empty[st]);
+                // refill the previous chunk's stage once its MMAs are done (this
+                // chunk's MMAs are already queued behind them)
+                if (c > 0 && c - 1 + kRing < nch) {
+                    const int sp = (c - 1) % kRing;
+                    mbar_wait(&empty[sp], (uses[sp] - 1) & 1);
+                    load_chunk(layer, c - 1 + kRing, sp);
+                }
+            }
+            mma_commit(done);
+        }
+        mbar_wait(done, done_phase);
+        done_phase ^= 1;
+        tc_fence_after();
+        if (layer < 2) {
+            for (int c = 0; c < H; c += 16) {  // tanh(acc + b) -> split bf16 A for the next layer (K = H)
+                float v[16];
+                tmem_ld16(trow + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    __nv_bfloat16 hi, lo;
+                    split_bf16(tanhf(v[i] + sb[layer * H + c + i]), hi, lo);
+                    *reinterpret_cast<__nv_bfloat16*>(sa_hi + img_off(r, c + i, H)) = hi;
+                    *reinterpret_cast<__nv_bfloat16*>(sa_lo + img_off(r, c + i, H)) = lo;
+                }
+            }
+            proxy_fence();
+            tc_fence_before();
+            __syncthreads();
+            tc_fence_after();
+        }
+    }
+    float z = 0.0f;
+    for (int c = 0; c < H; c += 16) {
+        float v[16];
+        tmem_ld16(trow + c, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) z = fmaf(tanhf(v[i] + sb[2 * H + c + i]), sb[3 * H + c + i], z);
+    }
+    z += __ldg(P.bias + 4 * H);
+    const int row = row0 + r;
+    if (row < n) {
+        float d = 1.0f / (1.0f + expf(-z));
+        d = fminf(fmaxf(d, 1e-4f), 1.0f - 1e-4f);
+        const float rw = -log1pf(-d);
+        if (!flags) {
+            reward[row] = rw;
+        } else {
+            const uint8_t f = flags[row];
+            if (!(f & kFlagSkip)) reward[row] = (f & kFlagDiverged) ? 0.0f : rw + (raux ? raux[row] : 0.0f);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(P.tmem_cols)
+                     : "memory");
+}
+
 }  // namespace
 
 size_t disc_smem_bytes(const DiscDev& P) {
     const int Kmax = std::max(P.k1, P.hidden);
+    if (P.precise)  // A hi + lo, the weight ring, biases, barriers
+        return 2 * static_cast<size_t>(kTileM) * Kmax * 2 + static_cast<size_t>(kRing) * 2 * P.hidden * 32 +
+               16 * P.hidden + 128;
     return static_cast<size_t>(kTileM) * Kmax * 2 + static_cast<size_t>(P.hidden) * Kmax * 2 + 16 * P.hidden + 64;
 }
 
@@ -280,15 +462,33 @@ DiscHost build_disc_images(const double* theta, long long n_params, int din, int
             }
         return img;
     };
+    // split-bf16 chunked images: chunk c of a K-column image = rows x 16 K (chunk_off)
+    auto chunked = [&](const double* W, int rows, int cols, int K, std::vector<uint16_t>& hi,
+                       std::vector<uint16_t>& lo) {
+        hi.assign(static_cast<size_t>(rows) * K, 0);
+        lo.assign(static_cast<size_t>(rows) * K, 0);
+        for (int r = 0; r < rows; ++r)
+            for (int k = 0; k < cols; ++k) {
+                const float x = static_cast<float>(W[static_cast<size_t>(k) * rows + r]);
+                const __nv_bfloat16 bh = __float2bfloat16_rn(x);
+                const __nv_bfloat16 bl = __float2bfloat16_rn(x - __bfloat162float(bh));
+                const size_t at = (static_cast<size_t>(k >> 4) * rows * 16 * 2 + chunk_off(r, k & 15)) / 2;
+                std::memcpy(&hi[at], &bh, 2);
+                std::memcpy(&lo[at], &bl, 2);
+            }
+    };
     long long o = 0;
+    chunked(theta + o, H, din, K1, h.c1_hi, h.c1_lo);
     h.w1 = image(theta + o, H, din, K1);
     o += static_cast<long long>(H) * din;
     const double* b1 = theta + o;
     o += H;
+    chunked(theta + o, H, H, H, h.c2_hi, h.c2_lo);
     h.w2 = image(theta + o, H, H, H);
     o += static_cast<long long>(H) * H;
     const double* b2 = theta + o;
     o += H;
+    chunked(theta + o, H, H, H, h.c3_hi, h.c3_lo);
     h.w3 = image(theta + o, H, H, H);
     o += static_cast<long long>(H) * H;
     const double* b3 = theta + o;
@@ -307,8 +507,14 @@ DiscHost build_disc_images(const double* theta, long long n_params, int din, int
 }
 
 cudaError_t prepare_disc(const DiscDev& P) {
-    return cudaFuncSetAttribute(disc_reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(disc_smem_bytes(P)));
+    DiscDev q = P;
+    q.precise = 0;
+    cudaError_t e = cudaFuncSetAttribute(disc_reward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(disc_smem_bytes(q)));
+    if (e != cudaSuccess) return e;
+    q.precise = 1;
+    return cudaFuncSetAttribute(disc_reward_precise_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(disc_smem_bytes(q)));
 }
 
 cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, const float* raux,
@@ -324,13 +530,27 @@ cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, con
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
+    if (P.precise) return cudaLaunchKernelEx(&cfg, disc_reward_precise_kernel, P, delta, ld, n, raux, flags, reward);
     return cudaLaunchKernelEx(&cfg, disc_reward_kernel, P, delta, ld, n, raux, flags, reward);
 }
 
 // Device-side refresh of the images from f64 parameters (same layout as
 // build_disc_images): used when the discriminator is trained on the device.
-__global__ void disc_repack_kernel(const double* __restrict__ theta, int din, int H, int K1, __nv_bfloat16* w1,
-                                   __nv_bfloat16* w2, __nv_bfloat16* w3, float* bias) {
+// One weight element into both image sets: the bf16 core-matrix image (fast
+// mode) and the split hi / lo K16-chunk images (fp32-class mode).
+__device__ __forceinline__ void put_weight(const DiscDev& P, int layer, int r, int k, int K, int rows, double v) {
+    const float x = static_cast<float>(v);
+    char* fast = reinterpret_cast<char*>(const_cast<void*>(layer == 0 ? P.w1 : layer == 1 ? P.w2 : P.w3));
+    *reinterpret_cast<__nv_bfloat16*>(fast + img_off(r, k, K)) = __float2bfloat16_rn(x);
+    const __nv_bfloat16 hi = __float2bfloat16_rn(x), lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+    const size_t at = static_cast<size_t>(k >> 4) * rows * 32 + chunk_off(r, k & 15);
+    *reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(const_cast<void*>(P.c_hi[layer])) + at) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(const_cast<void*>(P.c_lo[layer])) + at) = lo;
+}
+
+__global__ void disc_repack_kernel(const double* __restrict__ theta, DiscDev P) {
+    const int din = P.din, H = P.hidden, K1 = P.k1;
+    float* bias = const_cast<float*>(P.bias);
     const long long o1 = static_cast<long long>(H) * din + H, o2 = o1 + static_cast<long long>(H) * H + H,
                     o3 = o2 + static_cast<long long>(H) * H + H;
     const long long n1 = static_cast<long long>(H) * K1, n2 = static_cast<long long>(H) * H;
@@ -339,16 +559,14 @@ __global__ void disc_repack_kernel(const double* __restrict__ theta, int din, in
         if (t < n1) {  // W1 (H x din, zero-padded to K1)
             const int r = static_cast<int>(t % H), k = static_cast<int>(t / H);
             const double v = k < din ? theta[static_cast<long long>(k) * H + r] : 0.0;
-            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(w1) + img_off(r, k, K1)) =
-                __float2bfloat16_rn(static_cast<float>(v));
+            put_weight(P, 0, r, k, K1, H, v);
         } else if (t < n1 + 2 * n2) {  // W2, W3 (H x H)
             const long long u = t - n1;
             const int which = static_cast<int>(u / n2);
             const long long e = u % n2;
             const int r = static_cast<int>(e % H), k = static_cast<int>(e / H);
             const double v = theta[(which ? o2 : o1) + static_cast<long long>(k) * H + r];
-            *reinterpret_cast<__nv_bfloat16*>(reinterpret_cast<char*>(which ? w3 : w2) + img_off(r, k, H)) =
-                __float2bfloat16_rn(static_cast<float>(v));
+            put_weight(P, 1 + which, r, k, H, H, v);
         } else {  // b1 | b2 | b3 | w4 | b4
             const int i = static_cast<int>(t - n1 - 2 * n2), part = i / H, c = i % H;
             const long long src = part == 0 ? static_cast<long long>(H) * din + c
@@ -362,11 +580,7 @@ __global__ void disc_repack_kernel(const double* __restrict__ theta, int din, in
 }
 
 cudaError_t launch_disc_repack(const double* theta, const DiscDev& P, cudaStream_t s) {
-    disc_repack_kernel<<<296, 256, 0, s>>>(theta, P.din, P.hidden, P.k1,
-                                           static_cast<__nv_bfloat16*>(const_cast<void*>(P.w1)),
-                                           static_cast<__nv_bfloat16*>(const_cast<void*>(P.w2)),
-                                           static_cast<__nv_bfloat16*>(const_cast<void*>(P.w3)),
-                                           const_cast<float*>(P.bias));
+    disc_repack_kernel<<<296, 256, 0, s>>>(theta, P);
     return cudaGetLastError();
 }
 

@@ -14,6 +14,9 @@ struct DiscHost {
     int din = 0, hidden = 0, k1 = 0;  // k1 = din rounded up to the MMA K step (16)
     std::vector<uint16_t> w1, w2, w3;  // bf16 K-major core-matrix images (H x k1, H x H, H x H)
     std::vector<float> bias;           // b1 | b2 | b3 | w4 | b4 (4 H + 1 floats)
+    // fp32-class (split-bf16) mode: W = hi + lo (both bf16), each layer's image in
+    // K16-chunk-major order (chunk c = rows x 16 K, contiguous) for the streamed ring
+    std::vector<uint16_t> c1_hi, c1_lo, c2_hi, c2_lo, c3_hi, c3_lo;
 };
 
 // Device view passed to the kernel by value.
@@ -24,6 +27,9 @@ struct DiscDev {
     const void* w2 = nullptr;
     const void* w3 = nullptr;
     const float* bias = nullptr;  // b1 | b2 | b3 | w4 | b4
+    int precise = 1;  // 1: split-bf16 operands (hi + lo), accurate tanh: fp32-class; 0: bf16 fast mode
+    const void* c_hi[3] = {nullptr, nullptr, nullptr};  // chunked split images (see DiscHost)
+    const void* c_lo[3] = {nullptr, nullptr, nullptr};
 };
 
 DiscHost build_disc_images(const double* theta, long long n_params, int din, int hidden);
