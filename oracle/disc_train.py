@@ -16,11 +16,14 @@ Functions follow the reference line by line:
 The clamp's derivative is taken as 0 outside [1e-4, 1 - 1e-4] (its subgradient);
 learn.cpp, which would compose these calls, is absent from the reference.
 
-Parity status: nn.cpp cannot be compiled here (it needs Eigen's Map / rowwise /
-array API, which the oracle's Eigen shim does not provide), so this
-restatement is pinned by finite-difference gradient checks (SPEC.md:775,
-"all gradient checks rel. err < 1e-5") and by SPEC.md:419-420's examples, not by
-a reference binary.
+Parity status: pinned to the reference itself — nn.cpp is compiled unchanged
+into oracle/_ref (the Eigen shim provides its Map / Array / rowwise / colwise
+API) and Mlp::forward / backward / gradient_penalty_backward, Adam::step and
+RunningNorm agree with these functions to <= 1e-12 relative
+(tests/test_disc_train.py, and tests/golden/nn_reference.npz where
+/root/reference is absent); finite-difference gradient checks
+and SPEC.md:419-420's examples are kept.  The composition into the loss
+(train_discriminator) follows SPEC.md:412-421, learn.cpp being absent.
 """
 import numpy as np
 

@@ -95,6 +95,18 @@ def ref_lib():
         lib.ref_record_own_outcomes.argtypes = [C.c_void_p]
         lib.ref_drain_outcomes.argtypes = [C.c_void_p, _ip, _up, _ip, C.c_int32]
         lib.ref_rng_raw.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_uint64)]
+        P = C.POINTER
+        lib.ref_mlp_init.restype = C.c_int64
+        lib.ref_mlp_init.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_uint64, C.c_double, _dp]
+        lib.ref_mlp_forward.argtypes = [_dp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                        C.c_double, _dp, C.c_int32, _dp]
+        lib.ref_mlp_backward.argtypes = [_dp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_double,
+                                         C.c_double, _dp, C.c_int32, _dp, _dp, _dp]
+        lib.ref_mlp_gp_backward.argtypes = [_dp, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _dp, C.c_int32, _dp,
+                                            _dp]
+        lib.ref_adam_step.restype = C.c_int32
+        lib.ref_adam_step.argtypes = [_dp, _dp, C.c_int64, C.c_double, _dp, _dp, P(C.c_int64), P(C.c_int64)]
+        lib.ref_running_norm.argtypes = [_dp, C.c_int32, C.c_int32, _dp, _dp, _dp, _dp]
         lib.ref_rng_serialize.restype = C.c_int32
         lib.ref_rng_serialize.argtypes = [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32]
         lib.ref_rng_deserialize.argtypes = [C.c_void_p, C.c_int32, C.c_char_p]
@@ -306,3 +318,78 @@ def rng_uniform(seed, lo, hi, n):
     out = np.zeros(n)
     ref_lib().ref_rng_uniform(C.c_uint64(seed), float(lo), float(hi), int(n), out.ctypes.data_as(_dp))
     return out
+
+
+# ---- the reference's nn.cpp (Mlp / Adam / RunningNorm), nn.cpp:16-284 ----------
+HEAD_LINEAR, HEAD_SIGMOID, HEAD_AFFINE = 0, 1, 2
+
+
+def _d(a):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a, a.ctypes.data_as(_dp)
+
+
+def ref_mlp_init(n_in, hidden, n_out, seed, final_init_scale=1.0):
+    L = ref_lib()
+    n = L.ref_mlp_init(n_in, hidden, n_out, C.c_uint64(seed), final_init_scale, None)
+    th = np.zeros(n)
+    L.ref_mlp_init(n_in, hidden, n_out, C.c_uint64(seed), final_init_scale, th.ctypes.data_as(_dp))
+    return th
+
+
+def ref_mlp_forward(theta, n_in, hidden, n_out, X, head=HEAD_SIGMOID, affine=(1.0, 0.0)):
+    th, pth = _d(theta)
+    x, px = _d(np.atleast_2d(X))
+    y = np.zeros((x.shape[0], n_out))
+    ref_lib().ref_mlp_forward(pth, th.size, n_in, hidden, n_out, head, affine[0], affine[1], px, x.shape[0],
+                              y.ctypes.data_as(_dp))
+    return y
+
+
+def ref_mlp_backward(theta, n_in, hidden, n_out, X, upstream, head=HEAD_SIGMOID, affine=(1.0, 0.0)):
+    """(grad [n], input_grad [B x in]) of Mlp::backward from a zero gradient."""
+    th, pth = _d(theta)
+    x, px = _d(np.atleast_2d(X))
+    up, pup = _d(np.atleast_2d(upstream))
+    g = np.zeros(th.size)
+    ig = np.zeros(x.shape)
+    ref_lib().ref_mlp_backward(pth, th.size, n_in, hidden, n_out, head, affine[0], affine[1], px, x.shape[0], pup,
+                               g.ctypes.data_as(_dp), ig.ctypes.data_as(_dp))
+    return g, ig
+
+
+def ref_mlp_gp_backward(theta, n_in, hidden, X, head=HEAD_SIGMOID):
+    """(grad [n], penalty [B]) of Mlp::gradient_penalty_backward from a zero gradient."""
+    th, pth = _d(theta)
+    x, px = _d(np.atleast_2d(X))
+    g = np.zeros(th.size)
+    pen = np.zeros(x.shape[0])
+    ref_lib().ref_mlp_gp_backward(pth, th.size, n_in, hidden, head, px, x.shape[0], g.ctypes.data_as(_dp),
+                                  pen.ctypes.data_as(_dp))
+    return g, pen
+
+
+class RefAdam:
+    """Adam::step (nn.cpp:224-240) with the state held here."""
+
+    def __init__(self, n, lr):
+        self.lr, self.m, self.v = lr, np.zeros(n), np.zeros(n)
+        self.step_count, self.skipped = C.c_int64(0), C.c_int64(0)
+
+    def step(self, params, grad):
+        g, pg = _d(grad)
+        ok = ref_lib().ref_adam_step(params.ctypes.data_as(_dp), pg, params.size, self.lr, self.m.ctypes.data_as(_dp),
+                                     self.v.ctypes.data_as(_dp), C.byref(self.step_count), C.byref(self.skipped))
+        return bool(ok)
+
+
+def ref_running_norm(X, count, mean, var):
+    """RunningNorm::update(X) then apply(X) (nn.cpp:246-277): (count, mean, var, Y)."""
+    x, px = _d(np.atleast_2d(X))
+    c = np.array([count], dtype=np.float64)
+    m = np.array(mean, dtype=np.float64)
+    v = np.array(var, dtype=np.float64)
+    y = np.zeros(x.shape)
+    ref_lib().ref_running_norm(px, x.shape[0], x.shape[1], c.ctypes.data_as(_dp), m.ctypes.data_as(_dp),
+                               v.ctypes.data_as(_dp), y.ctypes.data_as(_dp))
+    return float(c[0]), m, v, y

@@ -114,9 +114,31 @@ def make_rng():
     return dict(case=c, ema=ema.tolist(), serialize=states, frames=frames)
 
 
+def make_nn():
+    """The reference's own nn.cpp (Mlp::forward / backward / gradient_penalty_backward)
+    on a fixed small case (tests/test_disc_train.py::_nn_case)."""
+    from oracle.oracle import mlp_init
+    from oracle.ref import ref_mlp_backward, ref_mlp_forward, ref_mlp_gp_backward
+
+    din, H, B = 9, 16, 7
+    rng = np.random.default_rng(11)
+    theta = mlp_init(din, H, 3)
+    theta = theta + rng.normal(0, 0.05, theta.shape)
+    X = rng.normal(0, 0.8, (B, din))
+    up = rng.normal(0, 1.0, (B, 1))
+    gb, ig = ref_mlp_backward(theta, din, H, 1, X, up)
+    gp, pen = ref_mlp_gp_backward(theta, din, H, X)
+    return dict(shape=np.array([din, H]), theta=theta, X=X, up=up, y=ref_mlp_forward(theta, din, H, 1, X),
+                grad_backward=gb, input_grad=ig, grad_penalty=gp, penalty=pen)
+
+
 def main():
     ensure_assets()
     import json
+
+    path = os.path.join(HERE, "nn_reference.npz")
+    np.savez_compressed(path, **make_nn())
+    print(path, os.path.getsize(path))
 
     path = os.path.join(HERE, "rng_serialize.json")
     with open(path, "w") as f:

@@ -248,3 +248,98 @@ def test_device_non_finite_delta_skips_the_update():
     th, steps, skipped = tr.params()
     assert steps == 1 and skipped == 1 and not np.array_equal(th, theta)
     tr.close()
+
+
+# ---- pins against the reference's own nn.cpp (oracle/_ref, compiled from ----
+# /root/reference/proj/src/nn.cpp against the Eigen shim; golden fixture made
+# from it for machines without /root/reference) --------------------------------
+import os  # noqa: E402
+
+from oracle.ref import REF_SO  # noqa: E402
+
+HAVE_REF = os.path.exists(REF_SO)
+GOLDEN_NN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "nn_reference.npz")
+
+
+def _rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.max(np.abs(a - b)) / max(1e-300, np.max(np.abs(b))))
+
+
+def _nn_case(din=9, H=16, B=7, seed=11):
+    rng = np.random.default_rng(seed)
+    theta = mlp_init(din, H, 3)
+    theta = theta + rng.normal(0, 0.05, theta.shape)  # non-zero biases
+    X = rng.normal(0, 0.8, (B, din))
+    up = rng.normal(0, 1.0, (B, 1))
+    return theta, X, up
+
+
+def _oracle_nn(theta, X, up, din, H):
+    c = mlp_forward_cache(theta, din, H, X)
+    from oracle.disc_train import mlp_backward
+
+    g_b = np.zeros(theta.size)
+    ig = mlp_backward(c, up, g_b, din, H, input_grad=True)
+    g_p = np.zeros(theta.size)
+    pen = gradient_penalty_backward(c, g_p, din, H)
+    return c["y"], g_b, ig, g_p, pen
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference build oracle/_ref absent")
+@pytest.mark.parametrize("din,H,B", [(9, 16, 7), (102, 64, 33)])
+def test_oracle_mlp_matches_reference_nn_cpp(din, H, B):
+    """Mlp::forward / Mlp::backward / Mlp::gradient_penalty_backward of the
+    REFERENCE (nn.cpp:54-222) equal the oracle restatement (oracle/disc_train.py)
+    to f64 rounding (different summation order only)."""
+    from oracle.ref import ref_mlp_backward, ref_mlp_forward, ref_mlp_gp_backward, ref_mlp_init
+
+    assert np.array_equal(ref_mlp_init(din, H, 1, 3), mlp_init(din, H, 3))  # Mlp(shape, seed)
+    theta, X, up = _nn_case(din, H, B)
+    y, g_b, ig, g_p, pen = _oracle_nn(theta, X, up, din, H)
+    assert _rel(y, ref_mlp_forward(theta, din, H, 1, X)) <= 1e-14
+    rg, rig = ref_mlp_backward(theta, din, H, 1, X, up)
+    assert _rel(g_b, rg) <= 1e-12 and _rel(ig, rig) <= 1e-12
+    rgp, rpen = ref_mlp_gp_backward(theta, din, H, X)
+    assert _rel(g_p, rgp) <= 1e-12 and _rel(pen, rpen) <= 1e-12
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference build oracle/_ref absent")
+def test_oracle_adam_and_running_norm_match_reference():
+    """Adam::step (nn.cpp:224-240, incl. the non-finite skip) and RunningNorm
+    update/apply (nn.cpp:246-277) of the reference vs the oracles."""
+    from oracle.ref import RefAdam, ref_running_norm
+
+    import paper_2603_29332_b200.dist as pkd
+    from oracle.policy import running_norm_apply
+
+    rng = np.random.default_rng(2)
+    n = 50
+    p_o, p_r = rng.normal(0, 1, n), None
+    p_r = p_o.copy()
+    a_o, a_r = Adam(n, 3e-3), RefAdam(n, 3e-3)
+    for k in range(4):
+        g = rng.normal(0, 1, n)
+        if k == 2:
+            g[5] = np.nan  # skipped by both
+        assert a_o.step(p_o, g) == a_r.step(p_r, g)
+    assert _rel(p_o, p_r) <= 1e-15 and a_o.skipped == a_r.skipped.value == 1
+    cnt, mean, var = 0.0, np.zeros(6), np.ones(6)
+    for k in range(3):
+        X = rng.normal(k, 1.0 + k, (20 + k, 6))
+        rc, rm, rv, ry = ref_running_norm(X, cnt, mean, var)
+        m = pkd.batch_moments(__import__("torch").as_tensor(X)).numpy()
+        cnt, mean, var = pkd.running_norm_fold(cnt, mean, var, m[0], m[1:7], m[7:])
+        assert cnt == rc and _rel(mean, rm) <= 1e-14 and _rel(var, rv) <= 1e-13
+        assert _rel(running_norm_apply(X, mean, var, cnt), ry) <= 1e-13
+
+
+def test_oracle_mlp_reproduces_reference_golden():
+    """The same pins from the committed fixture (made by the reference build,
+    tests/golden/make_golden.py) where /root/reference is absent."""
+    g = np.load(GOLDEN_NN)
+    din, H = int(g["shape"][0]), int(g["shape"][1])
+    y, g_b, ig, g_p, pen = _oracle_nn(g["theta"], g["X"], g["up"], din, H)
+    assert _rel(y, g["y"]) <= 1e-14
+    assert _rel(g_b, g["grad_backward"]) <= 1e-12 and _rel(ig, g["input_grad"]) <= 1e-12
+    assert _rel(g_p, g["grad_penalty"]) <= 1e-12 and _rel(pen, g["penalty"]) <= 1e-12

@@ -355,3 +355,26 @@ def test_reference_rng_deserialize_restores_the_reset_sequence(assets):
     for e in range(2):
         b.rng_deserialize(e, saved[e])
     assert [b.reset()[1].tolist() for _ in range(4)] == first
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference build oracle/_ref absent")
+def test_discriminator_and_policy_mlps_match_reference_nn_cpp():
+    """The reward oracle's Mlp (om_mlp_forward_sigmoid, the D(Δ) of every GPU reward
+    test) and the policy oracle's Mlp (oracle/policy.py, Head::Affine) equal the
+    reference's own Mlp::forward (nn.cpp:54-73) to f64 rounding."""
+    from oracle.policy import mlp_forward, mlp_layers
+    from oracle.ref import HEAD_AFFINE, ref_mlp_forward
+
+    rng = np.random.default_rng(4)
+    for din, H in ((9, 16), (102, 256)):
+        th = om.mlp_init(din, H, 7) + rng.normal(0, 0.02, om.mlp_param_count(din, H))
+        X = rng.normal(0, 1.0, (11, din))
+        ref = ref_mlp_forward(th, din, H, 1, X)[:, 0]
+        assert np.max(np.abs(om.mlp_forward_sigmoid(th, din, H, X) - ref)) <= 1e-14
+        r_ref = -np.log(1.0 - np.clip(ref, 1e-4, 1.0 - 1e-4))  # SPEC.md:423-429
+        assert np.max(np.abs(om.disc_reward(th, din, H, X) - r_ref)) <= 1e-13
+    th = om.mlp_init(40, 64, 3, n_out=24)
+    X = rng.normal(0, 1.0, (9, 40))
+    y = 0.5 * mlp_forward(mlp_layers(th, 40, 64, 24), X) + 0.25
+    ref = ref_mlp_forward(th, 40, 64, 24, X, head=HEAD_AFFINE, affine=(0.5, 0.25))
+    assert np.max(np.abs(y - ref)) <= 1e-13 * max(1.0, np.abs(ref).max())
