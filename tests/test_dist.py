@@ -225,5 +225,8 @@ def test_native_iteration_exchange_matches_python_path(assets):
             assert torch.equal(g.get_sampler().cpu(), e0)
         for st in stats:
             st.zero_()
+        if comm.value:
+            nccl.ncclCommDestroy.argtypes = [C.c_void_p]
+            assert nccl.ncclCommDestroy(comm) == 0
     for g in envs:
         g.close()
