@@ -305,7 +305,7 @@ def main():
                     "and run GAE at each iteration boundary")
     ap.add_argument("--policy-width", type=int, default=0,
                     help="actions from the on-device flow policy of this hidden width (0: Philox excitations)")
-    ap.add_argument("--disc-train", default="", choices=["", "fp32", "tf32"],
+    ap.add_argument("--disc-train", default="", choices=["", "fp32", "bf16"],
                     help="train the reward discriminator on the device once per rollout iteration (needs --rollout "
                          "and a config with D): one Adam step on the iteration's h*E Delta rows, then publish")
     ap.add_argument("--dry-run", action="store_true", help="CPU-only check of the multi-rank exchange plumbing "
@@ -400,7 +400,7 @@ def main():
             raise SystemExit("--disc-train needs --rollout and a config with a discriminator (c4)")
         width, dseed = C["disc"]
         trainer = pk.DiscTrainer(env.delta_dim, width, pk.mlp_init(env.delta_dim, width, dseed), lr=3e-5,
-                                 grad_penalty=10.0, max_rows=rollout.h * E, math=1 if args.disc_train == "tf32" else 0)
+                                 grad_penalty=10.0, max_rows=rollout.h * E, math=1 if args.disc_train == "bf16" else 0)
         ro_delta = rollout.field(7, env.delta_dim)
 
     mom_acc = None  # observation moments of the current iteration (h x E observations)
@@ -614,7 +614,7 @@ def main():
                        "actions": (f"on-device policy: Gaussian pi0 + 20-step flow ODE, Mlp width {args.policy_width} "
                                    "(tcgen05 GEMMs, CUDA graph)") if args.policy_width else "Philox excitations",
                        "rollout": "on-device buffer + GAE" if args.rollout else None,
-                       **({"disc_train": f"one Adam step per iteration on h*E Delta rows ({args.disc_train} cuBLAS "
+                       **({"disc_train": f"one Adam step per iteration on h*E Delta rows ({args.disc_train} tcgen05 "
                                          "GEMMs) + device publish, inside the iteration_exchange phase"}
                           if args.disc_train else {}),
                        "l2": "flushed between timed steps"},

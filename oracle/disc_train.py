@@ -179,6 +179,58 @@ def disc_loss_grad(theta, n_in, hidden, delta, lam):
     return logistic + lam * pen_mean, logistic, pen_mean, grad
 
 
+def bias_adjoint_rows(theta, n_in, hidden, delta, lam):
+    """Per-row bias adjoints of dloss/dθ (the rows whose column sums are the
+    bias gradients of disc_loss_grad): [b0 rows, b1 rows, b2 rows, b4 rows], each
+    [(B + 1) x out], Δ rows first, then the D(0) row.  Used to state the
+    conditioning of the bias gradients (Σ_r |row| vs |Σ_r row|: the D(0) term
+    cancels most of the Δ terms), nn.cpp:98-128 and 186-221 row by row."""
+    delta = np.asarray(delta, dtype=np.float64)
+    B = delta.shape[0]
+    L = mlp_layers(theta, n_in, hidden, 1)
+    W = [l[0] for l in L]
+
+    def logistic_rows(c, upstream):
+        y = c["y"]
+        dz4 = upstream * y * (1.0 - y)
+        dz3 = (dz4 @ W[3]) * (1.0 - c["h3"] ** 2)
+        dz2 = (dz3 @ W[2]) * (1.0 - c["h2"] ** 2)
+        dz1 = (dz2 @ W[1]) * (1.0 - c["h1"] ** 2)
+        return [dz1, dz2, dz3, dz4]
+
+    c0 = mlp_forward_cache(theta, n_in, hidden, np.zeros((1, n_in)))
+    y0 = c0["y"][0, 0]
+    z0 = logistic_rows(c0, np.array([[-1.0 / y0 if CLAMP_LO < y0 < CLAMP_HI else 0.0]]))
+    c = mlp_forward_cache(theta, n_in, hidden, delta)
+    y = c["y"][:, 0]
+    inside = (y > CLAMP_LO) & (y < CLAMP_HI)
+    zr = logistic_rows(c, (np.where(inside, 1.0 / (1.0 - y), 0.0) / B)[:, None])
+    if lam != 0.0:
+        d4 = y * (1.0 - y)
+        dd4 = d4 * (1.0 - 2.0 * y)
+        h1, h2, h3 = c["h1"], c["h2"], c["h3"]
+        g1, g2, g3 = 1.0 - h1 ** 2, 1.0 - h2 ** 2, 1.0 - h3 ** 2
+        d3 = (d4[:, None] * W[3]) * g3
+        d1 = (((d3 @ W[2]) * g2) @ W[1]) * g1
+        zeta1 = (d1 @ W[0]) @ W[0].T
+        u1 = g1 * zeta1
+        zeta2 = u1 @ W[1].T
+        u2 = g2 * zeta2
+        zeta3 = u2 @ W[2].T
+        zeta4 = ((g3 * zeta3) @ W[3].T)[:, 0]
+        w = lam / B
+        b_u3, b_h3 = (w * 2.0 * d4)[:, None] * W[3], (w * 2.0 * dd4 * zeta4)[:, None] * W[3]
+        b_z4 = (w * 2.0 * dd4 * zeta4)[:, None]
+        b_zeta3, b_z3 = g3 * b_u3, g3 * (b_h3 - 2.0 * h3 * zeta3 * b_u3)
+        b_u2, b_h2 = b_zeta3 @ W[2], b_z3 @ W[2]
+        b_zeta2, b_z2 = g2 * b_u2, g2 * (b_h2 - 2.0 * h2 * zeta2 * b_u2)
+        b_u1, b_h1 = b_zeta2 @ W[1], b_z2 @ W[1]
+        b_z1 = g1 * (b_h1 - 2.0 * h1 * zeta1 * b_u1)
+        for k, pz in enumerate([b_z1, b_z2, b_z3, b_z4]):
+            zr[k] = zr[k] + pz
+    return [np.vstack([a, b]) for a, b in zip(zr, z0)]
+
+
 def train_discriminator(theta, n_in, hidden, delta, lam, adam):
     """One update: returns (loss, logistic, penalty) at the
     pre-update parameters; theta is updated in place by adam."""

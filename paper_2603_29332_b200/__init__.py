@@ -179,7 +179,7 @@ class DiscTrainer:
     """Discriminator training step on the device (msk_disc_trainer_*; SPEC.md:412-421
     train_discriminator): one Adam step (nn.cpp:224-240) on
     -log clamp(D(0)) - mean log(1 - clamp(D(Δ))) + λ mean ||∇_Δ D(Δ)||².
-    math: 0 FP32 GEMMs, 1 TF32 tensor-core GEMMs."""
+    math: 0 fp32-class (split-bf16 tcgen05 GEMMs, 3 MMAs per product), 1 bf16 tcgen05 GEMMs."""
 
     def __init__(self, n_in, hidden, theta, lr=3e-5, grad_penalty=10.0, max_rows=4096, math=0, device=None):
         import numpy as np

@@ -7,32 +7,42 @@
 // with master parameters θ in the reference's flat layout (nn.cpp:16-38, W
 // column-major) and the Adam moments in f64 on the device.
 //
-// Structure (all activations column-major, R = B + 1 rows: the B Δ rows plus
-// the zero input of the D(0) term as the last row):
-//   * forward  H_l = tanh(H_{l-1} W_lᵀ + b_l), y = sigmoid(H_3 w_4 + b_4)
-//     (nn.cpp:54-73);
+// The reference composes Mlp::backward (nn.cpp:80-129) for the logistic terms
+// with Mlp::gradient_penalty_backward (nn.cpp:131-222: input gradient g, its
+// forward tangent, then a reverse pass through primal + tangent).  Here, over
+// R = B + 1 rows (the B Δ rows plus the zero input of the D(0) term):
+//   * forward   H_l = tanh(H_{l-1} W_lᵀ + b_l), y = sigmoid(H_3 w_4 + b_4)
 //   * input gradient g = dy/dx (d-chain) and its forward tangent ζ_l, u_l
-//     (nn.cpp:157-171);
-//   * ONE reverse pass carrying [tangent; primal] adjoints stacked as 2R-row
-//     matrices: the logistic loss's upstream (Mlp::backward, nn.cpp:80-129)
-//     enters the primal adjoint of the head, so it rides the gradient-penalty
-//     reverse pass (nn.cpp:173-221) — both are linear in the head adjoint;
-//   * each weight gradient is one GEMM over the stacked 2R rows,
-//     gW_l = [b_ζ; b_z]ᵀ [u; H] (the reference's two products in one);
-//   * bias gradients: fixed-order column sums in f64; Adam in f64 with the
-//     reference's non-finite-gradient skip evaluated on the device;
-//   * each half of a stacked matrix is padded to Rp = R rounded up to 4 rows
-//     (16-B aligned leading dimensions and half offsets, so cuBLAS picks its
-//     sm100 tcgen05 kernels); the column kernels write zeros into the padding
-//     and the GEMMs run over the padded extents.
-// The GEMMs are plain library GEMMs (cuBLAS, f32 data) in the math mode the
-// caller picks: FP32 (default) or TF32 tensor cores.  Only cuBLAS 12.0-level
-// entry points are used: the process may already hold torch's bundled
-// libcublas.so.12, which then serves these symbols (the BF16x9 FP32 emulation
-// of cuBLAS 12.9 is therefore not used).  Elementwise / reduction work is
-// fused into the kernels below.  This is the learner side of the loop,
-// launched once per rollout iteration; the stepping path never calls it.
-#include <cublas_v2.h>
+//   * ONE reverse pass carrying [tangent; primal] adjoints: the logistic
+//     loss's head adjoint enters the primal adjoint of the penalty's reverse
+//     pass (both are linear in the head adjoint);
+//   * weight gradients gW_l = b_ζᵀ u + b_zᵀ H (one split-K GEMM over 2R rows),
+//     bias gradients as column sums of the primal adjoints.
+//
+// Every product is a hand-written tcgen05 GEMM (no cuBLAS):
+//   * operands live in HBM as "split images": x = hi + lo, both bf16, in
+//     128 x 128 blocks of 8 x 8 core matrices ordered column-group-major, so the
+//     SAME image is a K-major operand (row GEMMs, K = columns) and an MN-major
+//     operand (weight-gradient GEMMs, K = rows);
+//   * fp32-class mode (math 0): three MMAs per product (lo·hi + hi·lo + hi·hi,
+//     fp32 TMEM accumulation), ~2^-17 relative operands; fast mode (math 1):
+//     hi·hi only (bf16 operands);
+//   * row GEMMs (M = 128 rows per CTA, N = the layer width ≤ 256 in two
+//     128-column MMAs, K in 32-column stages through a 4-stage bulk-copy ring)
+//     fuse every elementwise step into the epilogue: bias + tanh, the sigmoid
+//     head (row dot product, clamped logs, d4 / dd4 / logistic adjoint), the
+//     gates ∘(1 - H²), the penalty head, and the reverse elementwise step; the
+//     reverse GEMMs compute tangent and primal rows of the same tile in one CTA
+//     (two TMEM accumulators sharing each weight stage) so that step pairs them;
+//   * column sums (bias gradients, w4 gradient) are per-warp butterfly
+//     reductions in the epilogues, reduced later in a fixed order;
+//   * weight-gradient GEMMs split K = 2R over ~148 CTAs (MN-major operands from
+//     1 KB bulk-copy pieces), fp32 partials reduced in a fixed order in f64.
+// Everything is deterministic (no atomics).  This is the learner side of the
+// loop, launched once per rollout iteration; the stepping path never calls it.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -46,148 +56,690 @@
 
 namespace {
 
+using bf16 = __nv_bfloat16;
 constexpr double kClampLo = 1e-4, kClampHi = 1.0 - 1e-4;
-// Column-wise elementwise kernels: grid (row blocks, columns), 256 threads,
-// 4 rows per thread (coalesced along the column-major rows, 4 loads in flight).
-constexpr int kRowsPerThread = 4, kRowsPerBlock = 256 * kRowsPerThread;
 
-// X2 bottom half: primal input rows (Δ, then one zero row) — a 32 x 32 tile
-// transpose through shared memory (row-major Δ in, column-major X out).
-__global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld, int din, int R, int Rp, float* X2) {
-    __shared__ float tile[32][33];
-    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const int i = i0 + r, j = j0 + threadIdx.x;
-        tile[r][threadIdx.x] = (i < B && j < din) ? delta[static_cast<size_t>(i) * ld + j] : 0.0f;
+// ---- split images -----------------------------------------------------------
+// [rows_p x cols_p] (both multiples of 128) as 128 x 128 blocks of 16384
+// elements, block (rb, cb) at rb * (cols_p / 128) + cb; inside a block the 8 x 8
+// core matrices (8 rows x 8 consecutive columns = 128 B) are column-group-major:
+// core (rg, cg) at (cg * 16 + rg) * 128 B.
+__host__ __device__ __forceinline__ size_t iofs(int r, int c, int cols_p) {
+    return (static_cast<size_t>(r >> 7) * (cols_p >> 7) + (c >> 7)) * 16384 +
+           static_cast<size_t>((((c & 127) >> 3) << 4) + ((r & 127) >> 3)) * 64 + (r & 7) * 8 + (c & 7);
+}
+
+struct Img {
+    bf16* hi = nullptr;
+    bf16* lo = nullptr;
+    int cols_p = 0;
+};
+
+__device__ __forceinline__ uint32_t pack2(bf16 a, bf16 b) {
+    return static_cast<uint32_t>(__bfloat16_as_ushort(a)) | (static_cast<uint32_t>(__bfloat16_as_ushort(b)) << 16);
+}
+
+// 8 consecutive columns of one row: x = hi + lo.
+__device__ __forceinline__ void store8(const Img& im, int r, int c, const float* v) {
+    uint32_t h[4], l[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const bf16 a = __float2bfloat16_rn(v[2 * i]), b = __float2bfloat16_rn(v[2 * i + 1]);
+        h[i] = pack2(a, b);
+        l[i] = pack2(__float2bfloat16_rn(v[2 * i] - __bfloat162float(a)),
+                     __float2bfloat16_rn(v[2 * i + 1] - __bfloat162float(b)));
     }
+    const size_t o = iofs(r, c, im.cols_p);
+    *reinterpret_cast<uint4*>(im.hi + o) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(im.lo + o) = make_uint4(l[0], l[1], l[2], l[3]);
+}
+__device__ __forceinline__ void load8(const Img& im, int r, int c, float* v) {
+    const size_t o = iofs(r, c, im.cols_p);
+    const uint4 h = *reinterpret_cast<const uint4*>(im.hi + o), l = *reinterpret_cast<const uint4*>(im.lo + o);
+    const uint32_t hw[4] = {h.x, h.y, h.z, h.w}, lw[4] = {l.x, l.y, l.z, l.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = __uint_as_float(hw[i] << 16) + __uint_as_float(lw[i] << 16);
+        v[2 * i + 1] = __uint_as_float(hw[i] & 0xffff0000u) + __uint_as_float(lw[i] & 0xffff0000u);
+    }
+}
+__device__ __forceinline__ void store32(const Img& im, int r, int c, const float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) store8(im, r, c + 8 * j, v + 8 * j);
+}
+__device__ __forceinline__ void load32(const Img& im, int r, int c, float (&v)[32]) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) load8(im, r, c + 8 * j, v + 8 * j);
+}
+
+// ---- tcgen05 / bulk-copy helpers ------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "DTW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra DTW_%=;\n\t}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(b))
+                 : "memory");
+}
+// shared-memory matrix descriptor, no swizzle: LBO = K-group stride, SBO = MN-group stride
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return static_cast<uint64_t>((addr >> 4) & 0x3FFF) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16) |
+           (static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+}
+// kind::f16: D f32, A/B bf16, M = 128, N = 128; mn = 1 -> both operands MN-major
+__host__ __device__ constexpr uint32_t idesc128(int mn) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(mn) << 15) | (static_cast<uint32_t>(mn) << 16) |
+           (static_cast<uint32_t>(128 >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// Column sums over the 32 rows (lanes) of a warp for 32 columns: butterfly
+// reduce-scatter (31 shuffles), lane l ends with column l; written to dst[lane].
+__device__ __forceinline__ void colsum32(float (&x)[32], float* dst, int lane) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const float send = up ? x[i] : x[i + o];
+            const float keep = up ? x[i + o] : x[i];
+            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    dst[lane] = x[0];
+}
+
+// ---- row GEMMs: C[128-row tile x N] = A[tile x K] · Wᵀ, N ≤ 256 ------------------
+// Persistent: each CTA loops over units (a 128-row tile, or for the dual reverse
+// GEMMs a (tile, 128-column half) pair); two TMEM accumulator buffers, so the
+// epilogue of one unit overlaps the mainloop of the next.
+constexpr int kRowEpiWarps = 16;                      // 4 per TMEM lane quarter, one column slice each
+constexpr int kRowThreads = 64 + 32 * kRowEpiWarps;   // + warp 0 bulk-copy producer, warp 1 MMA issuer
+constexpr int kKC = 32;                               // K columns per pipeline stage
+constexpr int kChunk = 128 * kKC * 2;                 // 8 KB: one image's 128-row x 32-column slice (contiguous)
+constexpr int kRowStages = 4;
+constexpr int kRowStageBytes = 6 * kChunk;            // A (hi, lo) x 1-2 halves + B (hi, lo) x 1-2 blocks
+constexpr size_t kRowSmem = static_cast<size_t>(kRowStages) * kRowStageBytes + 256 + (2 * 4 * 128 + 2 * 256) * 4;
+
+enum Epi : int {
+    kEpiTanh = 0,  // out0 = tanh(acc + bias)
+    kEpiHead,      // out0 = H3 = tanh(acc + bias); head row scalars; out1 = d3 = d4 w4 ∘ (1 - H3²)
+    kEpiGate,      // out0 = acc ∘ (1 - h²)
+    kEpiPlain,     // out0 = acc
+    kEpiGate2,     // out1 = z = acc, out0 = acc ∘ (1 - h²)
+    kEpiTHead,     // penalty head: zeta4, V; out0 = S_t, out1 = S_p (layer-3 reverse step); w4 / b column sums
+    kEpiRev        // dual: bu = acc_t, bh = acc_p -> out0 = S_t, out1 = S_p (reverse step); b column sums
+};
+
+struct RowArgs {
+    const bf16* a_hi[2] = {nullptr, nullptr};  // A images (kEpiRev: [0] tangent rows, [1] primal rows)
+    const bf16* a_lo[2] = {nullptr, nullptr};
+    int a_cols = 0;                      // K (multiple of 128)
+    const bf16* w_hi = nullptr;          // weight image: rows = N, cols = K
+    const bf16* w_lo = nullptr;
+    int nb = 1;                          // N / 128
+    int n_valid = 0;                     // valid output columns (bias / w4 length)
+    int rows = 0;                        // valid rows R
+    int tiles = 0;                       // 128-row tiles
+    int passes = 3;
+    const float* bias = nullptr;         // [N]
+    const float* w4 = nullptr;           // head weights [N]
+    const float* b4 = nullptr;           // head bias
+    Img h, z;                            // gate activations, pre-gate tangent
+    Img out[2];
+    float *d4 = nullptr, *dd4 = nullptr, *dz4 = nullptr, *vh = nullptr;
+    double *lrow = nullptr, *prow = nullptr;
+    float* colpart[2] = {nullptr, nullptr};  // [tiles * 4 x ldc] per-warp column sums
+    int ldc = 0;
+    int B = 0;
+    float lamB = 0.0f;
+};
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void store16(const Img& im, int r, int c, const float (&v)[16]) {
+    store8(im, r, c, v);
+    store8(im, r, c + 8, v + 8);
+}
+__device__ __forceinline__ void load16(const Img& im, int r, int c, float (&v)[16]) {
+    load8(im, r, c, v);
+    load8(im, r, c + 8, v + 8);
+}
+// Column sums over the 32 rows (lanes) of a warp for 16 columns: butterfly
+// reduce-scatter over lane bits 3..0, then the two lane halves combined; lanes
+// 0-15 write dst[lane] (fixed order: deterministic).
+__device__ __forceinline__ void colsum16(float (&x)[16], float* dst, int lane) {
+#pragma unroll
+    for (int o = 8; o >= 1; o >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const float send = up ? x[i] : x[i + o];
+            const float keep = up ? x[i + o] : x[i];
+            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+    }
+    x[0] += __shfl_xor_sync(0xffffffffu, x[0], 16);
+    if (lane < 16) dst[lane] = x[0];
+}
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kRowEpiWarps) : "memory"); }
+
+// One unit's epilogue by one epilogue warp: TMEM lane quarter q (rows), column
+// slice j (a quarter of the unit's columns), 16 columns per TMEM load.
+template <int EPI>
+__device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tacc, float* sdot, const float* sb,
+                                                  const float* sw, int mb, int nh, int q, int j, int lane) {
+    constexpr bool kDual = EPI == kEpiRev;
+    const int rt = q * 32 + lane, r = mb * 128 + rt;
+    const bool valid = r < g.rows;
+    const int ncols = kDual ? 128 : g.nb * 128, sl = ncols >> 2, c_lo = j * sl, c_hi = c_lo + sl;
+    const int obase = kDual ? nh * 128 : 0;  // output column of accumulator column 0
+    const uint32_t tl = tacc + (static_cast<uint32_t>(q * 32) << 16);
+    float* cp0 = g.colpart[0] ? g.colpart[0] + static_cast<size_t>(mb * 4 + q) * g.ldc : nullptr;
+    float* cp1 = g.colpart[1] ? g.colpart[1] + static_cast<size_t>(mb * 4 + q) * g.ldc : nullptr;
+    float v[16], x[16];
+
+    if constexpr (EPI == kEpiTanh || EPI == kEpiGate || EPI == kEpiPlain || EPI == kEpiGate2) {
+        for (int c = c_lo; c < c_hi; c += 16) {
+            tmem_ld16(tl + c, v);
+            if (EPI == kEpiTanh) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = valid ? tanhf(v[i] + sb[c + i]) : 0.0f;
+                store16(g.out[0], r, c, v);
+            } else if (EPI == kEpiPlain) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = valid ? v[i] : 0.0f;
+                store16(g.out[0], r, c, v);
+            } else {
+                load16(g.h, r, c, x);
+                if (EPI == kEpiGate2) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = valid ? v[i] : 0.0f;
+                    store16(g.out[1], r, c, v);
+                }
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = valid ? v[i] * (1.0f - x[i] * x[i]) : 0.0f;
+                store16(g.out[0], r, c, v);
+            }
+        }
+    } else if constexpr (EPI == kEpiHead) {
+        // pass 1: H3 and the row dot product z4 = H3 · w4
+        float dot = 0.0f;
+        for (int c = c_lo; c < c_hi; c += 16) {
+            tmem_ld16(tl + c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                v[i] = valid ? tanhf(v[i] + sb[c + i]) : 0.0f;
+                dot = fmaf(v[i], sw[c + i], dot);
+            }
+            store16(g.out[0], r, c, v);
+        }
+        sdot[j * 128 + rt] = dot;
+        epi_bar();
+        const float z4 = (sdot[rt] + sdot[128 + rt]) + (sdot[256 + rt] + sdot[384 + rt]);
+        // sigmoid head + clamped logs (nn.cpp:66-68) in f64
+        const double y = 1.0 / (1.0 + exp(-(static_cast<double>(z4) + g.b4[0])));
+        const double yc = fmin(fmax(y, kClampLo), kClampHi);
+        const bool inside = y > kClampLo && y < kClampHi;
+        const double d = y * (1.0 - y);
+        const float d4 = valid ? static_cast<float>(d) : 0.0f;
+        if (valid && j == 0) {
+            g.d4[r] = d4;
+            g.dd4[r] = static_cast<float>(d * (1.0 - 2.0 * y));
+            if (r < g.B) {  // -(1/B) log(1 - clamp(y)): upstream 1 / (B (1 - y)) -> dz4 = y / B
+                g.dz4[r] = inside ? static_cast<float>(y / g.B) : 0.0f;
+                g.lrow[r] = -log(1.0 - yc) / g.B;
+            } else {  // -log clamp(D(0)): upstream -1 / y -> dz4 = -(1 - y)
+                g.dz4[r] = inside ? static_cast<float>(-(1.0 - y)) : 0.0f;
+                g.lrow[r] = -log(yc);
+            }
+        }
+        // pass 2: d3 = d4 w4 ∘ (1 - H3²)  (nn.cpp:161)
+        for (int c = c_lo; c < c_hi; c += 16) {
+            tmem_ld16(tl + c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float h = tanhf(v[i] + sb[c + i]);
+                v[i] = valid ? d4 * sw[c + i] * (1.0f - h * h) : 0.0f;
+            }
+            store16(g.out[1], r, c, v);
+        }
+    } else if constexpr (EPI == kEpiTHead) {
+        // pass 1: u3 = ζ3 ∘ (1 - H3²), zeta4 = u3 · w4  (nn.cpp:167-171)
+        float dot = 0.0f;
+        for (int c = c_lo; c < c_hi; c += 16) {
+            tmem_ld16(tl + c, v);
+            load16(g.h, r, c, x);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) dot = fmaf(v[i] * (1.0f - x[i] * x[i]), sw[c + i], dot);
+        }
+        sdot[j * 128 + rt] = dot;
+        epi_bar();
+        const float zeta4 = (sdot[rt] + sdot[128 + rt]) + (sdot[256 + rt] + sdot[384 + rt]);
+        // penalty + head adjoints (nn.cpp:172, 187-188; the logistic dz4 rides b_z4)
+        float vu = 0.0f, vhv = 0.0f;
+        if (valid) {
+            const float w = r < g.B ? g.lamB : 0.0f, d4 = g.d4[r];
+            vu = 2.0f * w * d4;
+            vhv = 2.0f * w * g.dd4[r] * zeta4 + g.dz4[r];
+            if (j == 0) {
+                g.vh[r] = vhv;
+                g.prow[r] = r < g.B ? static_cast<double>(d4) * zeta4 / g.B : 0.0;
+            }
+        }
+        // pass 2: layer-3 reverse step and the w4 / b2 column sums
+        for (int c = c_lo; c < c_hi; c += 16) {
+            tmem_ld16(tl + c, v);
+            load16(g.h, r, c, x);
+            float st[16], sp[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float h = x[i], gt = 1.0f - h * h, w4 = sw[c + i];
+                const float bu = vu * w4, bh = fmaf(-2.0f * h * v[i], bu, vhv * w4);
+                st[i] = gt * bu;
+                sp[i] = gt * bh;
+                x[i] = fmaf(vu, v[i] * gt, vhv * h);  // gw4 term: b_ζ4 u3 + b_z4 H3
+            }
+            store16(g.out[0], r, c, st);
+            store16(g.out[1], r, c, sp);
+            colsum16(x, cp0 + c, lane);
+            colsum16(sp, cp1 + c, lane);
+        }
+    } else {  // kEpiRev: accumulator columns [0, 128) tangent rows (b_u), [128, 256) primal rows (b_h)
+        for (int c = c_lo; c < c_hi; c += 16) {
+            float bh[16], zt[16];
+            const int oc = obase + c;
+            tmem_ld16(tl + c, v);
+            tmem_ld16(tl + 128 + c, bh);
+            load16(g.h, r, oc, x);
+            load16(g.z, r, oc, zt);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const float h = x[i], gt = 1.0f - h * h;
+                const float b2 = fmaf(-2.0f * h * zt[i], v[i], bh[i]);
+                v[i] = valid ? gt * v[i] : 0.0f;
+                bh[i] = valid ? gt * b2 : 0.0f;
+            }
+            store16(g.out[0], r, oc, v);
+            store16(g.out[1], r, oc, bh);
+            colsum16(bh, cp0 + oc, lane);
+        }
+    }
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(kRowThreads, 1) row_gemm_kernel(const RowArgs g) {
+    constexpr bool kDual = EPI == kEpiRev;
+    constexpr int kA = kDual ? 2 : 1;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kRowStages * kRowStageBytes);
+    uint64_t* empty = full + kRowStages;
+    uint64_t* acc_full = empty + kRowStages;  // [2]
+    uint64_t* acc_empty = acc_full + 2;       // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    float* sdot = reinterpret_cast<float*>(smem + kRowStages * kRowStageBytes + 256);  // [2][4][128] row partial dots
+    float* sb = sdot + 2 * 4 * 128;                                                     // [256] bias
+    float* sw = sb + 256;                                                               // [256] head weights
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int KC = g.a_cols / kKC, kblk = g.a_cols >> 7;
+    const int nbu = kDual ? 1 : g.nb;                        // B blocks per unit
+    const int units = kDual ? g.tiles * g.nb : g.tiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kRowStages; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            bar_init(&acc_full[b], 1);
+            bar_init(&acc_empty[b], kRowEpiWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    for (int c = threadIdx.y; c < 32; c += 8) {
-        const int j = j0 + c, i = i0 + threadIdx.x;
-        if (j < din && i < Rp) X2[static_cast<size_t>(j) * 2 * Rp + Rp + i] = tile[threadIdx.x][c];
-    }
-}
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
 
-// The column-wise kernels cover rows [0, Rp) of a half and write 0 to the
-// padding rows [R, Rp), so every GEMM over a padded extent sees zeros there.
-
-// x = tanh(x + b[col]) over a column-major block (leading dim ld).
-__global__ void bias_tanh_kernel(float* x, int R, int Rp, int ld, const float* __restrict__ b) {
-    const int j = blockIdx.y;
+    // stage slots: A (hi, lo) per half, then B (hi, lo) per 128-column block
+    if (warp == 0 && lane == 0) {
+        const bool lo = g.passes == 3;
+        const uint32_t bytes = static_cast<uint32_t>((kA + nbu) * (lo ? 2 : 1) * kChunk);
+        int gk = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            const int mb = kDual ? u / g.nb : u, n0 = kDual ? u % g.nb : 0;
+            for (int kc = 0; kc < KC; ++kc, ++gk) {
+                const int s = gk % kRowStages;
+                if (gk >= kRowStages) bar_wait(&empty[s], ((gk / kRowStages) - 1) & 1);
+                unsigned char* st = smem + s * kRowStageBytes;
+                bar_expect(&full[s], bytes);
+                const size_t aoff = (static_cast<size_t>(mb) * kblk + (kc >> 2)) * 16384 + (kc & 3) * 4096;
 #pragma unroll
-    for (int k = 0; k < kRowsPerThread; ++k) {
-        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= Rp) break;
-        float* p = x + static_cast<size_t>(j) * ld + i;
-        *p = i < R ? tanhf(*p + b[j]) : 0.0f;
-    }
-}
-
-// Head (nn.cpp:66-68 sigmoid; SPEC.md:416 clamped logs): y, head' (d4), head'' (dd4),
-// the logistic loss's head adjoint dz4 (Mlp::backward's dz4 = upstream * y (1 - y)),
-// and the per-row logistic loss term.
-__global__ void head_kernel(const float* __restrict__ z4, const float* __restrict__ b3, int B, int R, float* d4,
-                            float* dd4, float* dz4, double* lrow) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= R) return;
-    const double y = 1.0 / (1.0 + exp(-(static_cast<double>(z4[i]) + b3[0])));
-    const double yc = fmin(fmax(y, kClampLo), kClampHi);
-    const bool inside = y > kClampLo && y < kClampHi;
-    const double d = y * (1.0 - y);
-    d4[i] = static_cast<float>(d);
-    dd4[i] = static_cast<float>(d * (1.0 - 2.0 * y));
-    if (i < B) {  // -(1/B) log(1 - clamp(y)): upstream 1 / (B (1 - y))
-        dz4[i] = inside ? static_cast<float>(y / B) : 0.0f;
-        lrow[i] = -log(1.0 - yc) / B;
-    } else {  // -log clamp(D(0)): upstream -1 / y
-        dz4[i] = inside ? static_cast<float>(-(1.0 - y)) : 0.0f;
-        lrow[i] = -log(yc);
-    }
-}
-
-// d3 = (d4 ⊗ w4) ∘ (1 - H3²)   (nn.cpp:161)
-__global__ void d3_kernel(const float* __restrict__ d4, const float* __restrict__ w4, const float* __restrict__ H3,
-                          int ldh, int R, int Rp, float* d3, int ldd) {
-    const int j = blockIdx.y;
-#pragma unroll
-    for (int k = 0; k < kRowsPerThread; ++k) {
-        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= Rp) break;
-        const float h = H3[static_cast<size_t>(j) * ldh + i];
-        d3[static_cast<size_t>(j) * ldd + i] = i < R ? d4[i] * w4[j] * (1.0f - h * h) : 0.0f;
-    }
-}
-
-// out = x ∘ (1 - H²), x and out [R x H] (ld lx / lo), H read with leading dim ldh.
-__global__ void gate_kernel(const float* x, int lx, const float* __restrict__ Hm, int ldh, int R, int Rp, float* out,
-                            int lo) {
-    const int j = blockIdx.y;
-#pragma unroll
-    for (int k = 0; k < kRowsPerThread; ++k) {
-        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= Rp) break;
-        const float h = Hm[static_cast<size_t>(j) * ldh + i];
-        out[static_cast<size_t>(j) * lo + i] = i < R ? x[static_cast<size_t>(j) * lx + i] * (1.0f - h * h) : 0.0f;
-    }
-}
-
-// Penalty + head adjoints (nn.cpp:172, 187-188 with the logistic dz4 added to b_z4):
-// V[i] = b_ζ4 = 2 w d4, V[Rp + i] = b_z4 = 2 w dd4 ζ4 + dz4, w = λ/B on Δ rows, 0 on the zero row.
-__global__ void head2_kernel(const float* __restrict__ d4, const float* __restrict__ dd4,
-                             const float* __restrict__ zeta4, const float* __restrict__ dz4, int B, int R, int Rp,
-                             float lamB, float* V, double* prow) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= Rp) return;
-    if (i >= R) {
-        V[i] = V[Rp + i] = 0.0f;
-        return;
-    }
-    const float w = i < B ? lamB : 0.0f;
-    V[i] = 2.0f * w * d4[i];
-    V[Rp + i] = 2.0f * w * dd4[i] * zeta4[i] + dz4[i];
-    prow[i] = i < B ? static_cast<double>(d4[i]) * zeta4[i] / B : 0.0;
-}
-
-// Layer-3 adjoints from the head: [b_u3; b_h3] = V ⊗ w4, then the elementwise
-// step below (nn.cpp:191-195).
-// rev_elem: S = [b_u; b_h] (2R x H) -> [b_ζ; b_z] with
-//   b_ζ = G ∘ b_u,  b_h += -2 H ∘ ζ ∘ b_u,  b_z = G ∘ b_h   (G = 1 - H²)
-template <bool OUTER>
-__global__ void rev_elem_kernel(float* S, const float* __restrict__ V, const float* __restrict__ w4,
-                                const float* __restrict__ Hm, int ldh, const float* __restrict__ Z, int R, int Rp,
-                                int H) {
-    const size_t ld = 2 * static_cast<size_t>(Rp);
-    const int j = blockIdx.y;
-#pragma unroll
-    for (int k = 0; k < kRowsPerThread; ++k) {
-        const int i = blockIdx.x * kRowsPerBlock + k * 256 + threadIdx.x;
-        if (i >= Rp) break;
-        if (i >= R) {
-            S[j * ld + i] = S[j * ld + Rp + i] = 0.0f;
-            continue;
+                for (int a = 0; a < kA; ++a) {
+                    bulk(st + (2 * a) * kChunk, g.a_hi[a] + aoff, kChunk, &full[s]);
+                    if (lo) bulk(st + (2 * a + 1) * kChunk, g.a_lo[a] + aoff, kChunk, &full[s]);
+                }
+                for (int n = 0; n < nbu; ++n) {
+                    const size_t woff = (static_cast<size_t>(n0 + n) * kblk + (kc >> 2)) * 16384 + (kc & 3) * 4096;
+                    bulk(st + (2 * kA + 2 * n) * kChunk, g.w_hi + woff, kChunk, &full[s]);
+                    if (lo) bulk(st + (2 * kA + 2 * n + 1) * kChunk, g.w_lo + woff, kChunk, &full[s]);
+                }
+            }
         }
-        float bu, bh;
-        if constexpr (OUTER) {
-            bu = V[i] * w4[j];
-            bh = V[Rp + i] * w4[j];
-        } else {
-            bu = S[j * ld + i];
-            bh = S[j * ld + Rp + i];
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t id = idesc128(0);
+        int gk = 0, it = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const int buf = it & 1;
+            if (it >= 2) bar_wait(&acc_empty[buf], ((it >> 1) - 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t tb = tmem + buf * 256;
+            for (int kc = 0; kc < KC; ++kc, ++gk) {
+                const int s = gk % kRowStages;
+                bar_wait(&full[s], (gk / kRowStages) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t st = su32(smem + s * kRowStageBytes);
+#pragma unroll
+                for (int ks = 0; ks < kKC / 16; ++ks) {
+#pragma unroll
+                    for (int a = 0; a < kA; ++a) {
+                        const uint64_t ah = sdesc(st + (2 * a) * kChunk + ks * 4096, 2048, 128);
+                        const uint64_t al = sdesc(st + (2 * a + 1) * kChunk + ks * 4096, 2048, 128);
+                        for (int n = 0; n < nbu; ++n) {
+                            const uint64_t bh = sdesc(st + (2 * kA + 2 * n) * kChunk + ks * 4096, 2048, 128);
+                            const uint64_t bl = sdesc(st + (2 * kA + 2 * n + 1) * kChunk + ks * 4096, 2048, 128);
+                            const uint32_t tm = tb + (a + n) * 128;
+                            const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+                            if (g.passes == 3) {  // small terms first
+                                mma(tm, al, bh, id, acc);
+                                mma(tm, ah, bl, id, 1u);
+                                mma(tm, ah, bh, id, 1u);
+                            } else {
+                                mma(tm, ah, bh, id, acc);
+                            }
+                        }
+                    }
+                }
+                commit(&empty[s]);
+            }
+            commit(&acc_full[buf]);
         }
-        const float h = Hm[static_cast<size_t>(j) * ldh + i];
-        const float z = Z[static_cast<size_t>(j) * Rp + i];
-        const float g = 1.0f - h * h;
-        bh = fmaf(-2.0f * h * z, bu, bh);
-        S[j * ld + i] = g * bu;
-        S[j * ld + Rp + i] = g * bh;
+    } else if (warp >= 2) {
+        // bias / head weights, zero past the valid columns (padding stays 0)
+        for (int c = threadIdx.x - 64; c < 256; c += 32 * kRowEpiWarps) {
+            sb[c] = (g.bias && c < g.n_valid) ? g.bias[c] : 0.0f;
+            sw[c] = (g.w4 && c < g.n_valid) ? g.w4[c] : 0.0f;
+        }
+        epi_bar();
+        const int q = warp & 3, j = (warp - 2) >> 2;
+        int it = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
+            const int buf = it & 1;
+            bar_wait(&acc_full[buf], (it >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            row_unit_epilogue<EPI>(g, tmem + buf * 256, sdot + buf * 512, sb, sw, kDual ? u / g.nb : u,
+                                   kDual ? u % g.nb : 0, q, j, lane);
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[buf])) : "memory");
+        }
     }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
 }
 
-// out[j] = Σ_i x[j * ld + i], i < rows — fixed-order f64 sum, one block per column.
-__global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ x, int rows, size_t ld, float* out) {
+// ---- weight-gradient GEMMs: gW[o, i] = Σ_r S_t[r,o] A_t[r,i] + S_p[r,o] A_p[r,i] ---
+// CTA (o-tile, split) accumulates its share of the 32-row chunks of both halves
+// in TMEM (M = 128 o, N = 128 i per MMA, both operands MN-major) and writes an
+// fp32 partial [split][i][o] (o contiguous = the θ layout of W).  A chunk of an
+// image (32 rows x 128 columns, 16 column groups of 512 B, 2 KB apart in the
+// block) is ONE 5-D TMA tensor copy (see img_tmap), landing with column groups
+// 512 B apart: MN-group stride (SBO) 512 B, K-group (row-group) stride 128 B.
+constexpr int kWgThreads = 192;  // warp 0 TMA producer, warp 1 MMA issuer, warps 2-5 epilogue
+constexpr int kWgRows = 32;
+constexpr int kWgBlk = 16 * 512;           // 8 KB: 128 columns x 32 rows
+constexpr int kWgStages = 4;
+constexpr int kWgStageBytes = 6 * kWgBlk;  // S hi/lo + A hi/lo for <= 2 column blocks
+constexpr size_t kWgSmem = static_cast<size_t>(kWgStages) * kWgStageBytes + 256;
+
+struct alignas(64) WgMaps {
+    CUtensorMap s[2][2];  // [half][hi, lo]
+    CUtensorMap a[2][2];
+};
+
+struct WgArgs {
+    int s_cols = 0;  // M extent (o), multiple of 128
+    int a_cols = 0;  // N extent (i), 128 or 256
+    int chunks = 0;  // 32-row chunks per half
+    int splits = 1;
+    int passes = 3;
+    float* part = nullptr;
+};
+
+__device__ __forceinline__ void tma5(void* dst, const CUtensorMap* map, int c1, int c3, int c4, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, "
+        "%6}], [%7];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c1), "r"(0), "r"(c3), "r"(c4), "r"(su32(b))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(kWgThreads, 1) wgrad_kernel(const __grid_constant__ WgMaps maps, const WgArgs g) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kWgStages * kWgStageBytes);
+    uint64_t* empty = full + kWgStages;
+    uint64_t* acc_full = empty + kWgStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ot = blockIdx.x, sp = blockIdx.y, nb = g.a_cols >> 7;
+    const int total = 2 * g.chunks;
+    const int t0 = static_cast<int>(static_cast<long long>(sp) * total / g.splits);
+    const int t1 = static_cast<int>(static_cast<long long>(sp + 1) * total / g.splits);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kWgStages; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
+        }
+        bar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0 && lane == 0) {
+        const bool lo = g.passes == 3;
+        const uint32_t bytes = static_cast<uint32_t>((1 + nb) * (lo ? 2 : 1) * kWgBlk);
+        for (int t = t0; t < t1; ++t) {
+            const int k = t - t0, s = k % kWgStages;
+            if (k >= kWgStages) bar_wait(&empty[s], ((k / kWgStages) - 1) & 1);
+            bar_expect(&full[s], bytes);
+            const int half = t >= g.chunks ? 1 : 0, row0 = (t - half * g.chunks) * kWgRows;
+            const int rb = row0 >> 7, qt = (row0 >> 5) & 3;
+            unsigned char* st = smem + s * kWgStageBytes;
+            // slots: 0 S_hi, 1 S_lo, 2 + 2n A_hi(n), 3 + 2n A_lo(n)
+            tma5(st, &maps.s[half][0], qt, ot, rb, &full[s]);
+            if (lo) tma5(st + kWgBlk, &maps.s[half][1], qt, ot, rb, &full[s]);
+            for (int n = 0; n < nb; ++n) {
+                tma5(st + (2 + 2 * n) * kWgBlk, &maps.a[half][0], qt, n, rb, &full[s]);
+                if (lo) tma5(st + (3 + 2 * n) * kWgBlk, &maps.a[half][1], qt, n, rb, &full[s]);
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t id = idesc128(1);
+        for (int t = t0; t < t1; ++t) {
+            const int k = t - t0, s = k % kWgStages;
+            bar_wait(&full[s], (k / kWgStages) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t st = su32(smem + s * kWgStageBytes);
+#pragma unroll
+            for (int ks = 0; ks < kWgRows / 16; ++ks) {
+                const uint64_t sh = sdesc(st + ks * 256, 128, 512), sl = sdesc(st + kWgBlk + ks * 256, 128, 512);
+                for (int n = 0; n < nb; ++n) {
+                    const uint64_t ah = sdesc(st + (2 + 2 * n) * kWgBlk + ks * 256, 128, 512);
+                    const uint64_t al = sdesc(st + (3 + 2 * n) * kWgBlk + ks * 256, 128, 512);
+                    const uint32_t tm = tmem + n * 128, acc = (k > 0 || ks > 0) ? 1u : 0u;
+                    if (g.passes == 3) {
+                        mma(tm, sl, ah, id, acc);
+                        mma(tm, sh, al, id, 1u);
+                        mma(tm, sh, ah, id, 1u);
+                    } else {
+                        mma(tm, sh, ah, id, acc);
+                    }
+                }
+            }
+            commit(&empty[s]);
+        }
+        commit(acc_full);
+    } else if (warp >= 2) {
+        const int q = warp & 3, o = ot * 128 + q * 32 + lane;
+        bar_wait(acc_full, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16);
+        float* dst = g.part + static_cast<size_t>(sp) * g.a_cols * g.s_cols + o;
+        const bool empty_range = t1 <= t0;
+        for (int c = 0; c < g.a_cols; c += 32) {
+            float v[32];
+            tmem_ld32(tl + c, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) dst[static_cast<size_t>(c + i) * g.s_cols] = empty_range ? 0.0f : v[i];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
+// ---- small kernels ---------------------------------------------------------------
+// X image rows [0, rows_p): Δ rows, then the zero row (D(0) term), zeros after;
+// one thread per (row, 8-column group).
+__global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld, int din, int rows_p, Img X) {
+    const int groups = X.cols_p >> 3;
+    const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<long long>(rows_p) * groups) return;
+    const int r = static_cast<int>(t / groups), c0 = static_cast<int>(t % groups) * 8;
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int c = c0 + i;
+        v[i] = (r < B && c < din) ? delta[static_cast<size_t>(r) * ld + c] : 0.0f;
+    }
+    store8(X, r, c0, v);
+}
+
+// Weight images from the f64 master parameters: fwd (rows = out, cols = in) and
+// bwd (rows = in, cols = out) of each hidden layer W (out x in, column-major in θ).
+struct WPack {
+    const double* W[3];
+    int out[3], in[3];
+    Img fwd[3], bwd[3];
+};
+__global__ void pack_weights_kernel(WPack P) {
+    const int l = blockIdx.y >> 1, tr = blockIdx.y & 1;
+    const Img& im = tr ? P.bwd[l] : P.fwd[l];
+    const int rows_p = tr ? ((P.in[l] + 127) & ~127) : ((P.out[l] + 127) & ~127);
+    const int groups = im.cols_p >> 3;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= rows_p * groups) return;
+    const int n = t / groups, k0 = (t % groups) * 8;
+    uint32_t h[4], lw[4];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+        double w[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int k = k0 + i + j;
+            const int o = tr ? k : n, c = tr ? n : k;  // W[o, c]
+            w[j] = (o < P.out[l] && c < P.in[l]) ? P.W[l][static_cast<size_t>(c) * P.out[l] + o] : 0.0;
+        }
+        const bf16 a = __double2bfloat16(w[0]), b = __double2bfloat16(w[1]);
+        h[i / 2] = pack2(a, b);
+        lw[i / 2] = pack2(__double2bfloat16(w[0] - static_cast<double>(__bfloat162float(a))),
+                          __double2bfloat16(w[1] - static_cast<double>(__bfloat162float(b))));
+    }
+    const size_t o = iofs(n, k0, im.cols_p);
+    *reinterpret_cast<uint4*>(im.hi + o) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(im.lo + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+}
+
+// grad_W[i * out + o] = Σ_s part[s][i][o] (fixed order, f64)
+__global__ void wg_reduce_kernel(const float* __restrict__ part, int splits, int a_cols, int s_cols, int n_in,
+                                 int n_out, float* gW) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_in * n_out) return;
+    const int i = t / n_out, o = t % n_out;
+    double s = 0.0;
+    for (int k = 0; k < splits; ++k) s += part[(static_cast<size_t>(k) * a_cols + i) * s_cols + o];
+    gW[t] = static_cast<float>(s);
+}
+
+// out[j] = Σ_rows colpart[row][j]: one block per column, fixed-order f64 tree.
+__global__ void __launch_bounds__(256) colred_kernel(const float* __restrict__ cp, int rows, int ldc, float* out) {
     __shared__ double red[8];
     const int j = blockIdx.x;
     double s = 0.0;
-    for (int i = threadIdx.x; i < rows; i += 256) s += x[j * ld + i];
+    for (int i = threadIdx.x; i < rows; i += 256) s += cp[static_cast<size_t>(i) * ldc + j];
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
     __syncthreads();
@@ -198,34 +750,51 @@ __global__ void __launch_bounds__(256) colsum_kernel(const float* __restrict__ x
     }
 }
 
-// loss[0] = total, loss[1] = logistic, loss[2] = mean penalty (f64, fixed order).
-__global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ lrow, const double* __restrict__ prow,
-                                                    int R, double lam, double* loss) {
-    __shared__ double red[2][32];
-    double a = 0.0, b = 0.0;
-    for (int i = threadIdx.x; i < R; i += 1024) {
+// Row reductions of the loss terms and the head-bias gradient, fixed order:
+// block b sums rows [b R / nb, (b + 1) R / nb) into part[b] = {Σ lrow, Σ prow, Σ b_z4};
+// loss_final then sums the blocks in order: loss = {total, logistic, mean penalty},
+// gb4 = Σ b_z4.
+constexpr int kLossBlocks = 148;
+__global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict__ lrow,
+                                                        const double* __restrict__ prow, const float* __restrict__ vh,
+                                                        int R, double* part) {
+    __shared__ double red[3][8];
+    const int i0 = static_cast<int>(static_cast<long long>(blockIdx.x) * R / gridDim.x);
+    const int i1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * R / gridDim.x);
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int i = i0 + threadIdx.x; i < i1; i += 256) {
         a += lrow[i];
         b += prow[i];
+        c += vh[i];
     }
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         b += __shfl_xor_sync(0xffffffffu, b, o);
+        c += __shfl_xor_sync(0xffffffffu, c, o);
     }
     if ((threadIdx.x & 31) == 0) {
         red[0][threadIdx.x >> 5] = a;
         red[1][threadIdx.x >> 5] = b;
+        red[2][threadIdx.x >> 5] = c;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double s = 0.0, p = 0.0;
-        for (int w = 0; w < 32; ++w) {
-            s += red[0][w];
-            p += red[1][w];
-        }
-        loss[0] = s + lam * p;
-        loss[1] = s;
-        loss[2] = p;
+    if (threadIdx.x < 3) {
+        double t = 0.0;
+        for (int w = 0; w < 8; ++w) t += red[threadIdx.x][w];
+        part[blockIdx.x * 3 + threadIdx.x] = t;
     }
+}
+__global__ void loss_final_kernel(const double* __restrict__ part, int nb, double lam, double* loss, float* gb4) {
+    double s = 0.0, p = 0.0, g = 0.0;
+    for (int k = 0; k < nb; ++k) {
+        s += part[3 * k];
+        p += part[3 * k + 1];
+        g += part[3 * k + 2];
+    }
+    loss[0] = s + lam * p;
+    loss[1] = s;
+    loss[2] = p;
+    *gb4 = static_cast<float>(g);
 }
 
 __global__ void finite_kernel(const float* __restrict__ g, long long n, int* bad) {
@@ -277,6 +846,7 @@ int grid_for(size_t n) { return static_cast<int>(std::min<size_t>((n + 255) / 25
 
 struct msk_disc_trainer {
     int device = 0, din = 0, H = 0, max_rows = 0, math = 0;
+    int Hp = 0, Dp = 0, rows_p = 0;  // padded widths, padded row capacity (multiple of 128)
     long long P = 0;
     long long o1 = 0, o2 = 0, o3 = 0;  // offsets of W1, W2, W3 (= w4) in θ
     double lr = 0.0, lam = 0.0;
@@ -284,12 +854,16 @@ struct msk_disc_trainer {
     float *theta32 = nullptr, *grad = nullptr;
     long long* counts = nullptr;  // {Adam step_count, skipped}
     int* bad = nullptr;
-    // activations / adjoints (column-major; R = max_rows + 1)
-    float *X2 = nullptr, *A[4] = {}, *Z[4] = {}, *T1 = nullptr, *T2 = nullptr, *S1 = nullptr, *S2 = nullptr;
-    float *z4 = nullptr, *d4 = nullptr, *dd4 = nullptr, *dz4 = nullptr, *zeta4 = nullptr, *V = nullptr;
-    double *lrow = nullptr, *prow = nullptr, *loss = nullptr;
-    cublasHandle_t blas = nullptr;
+    // split images (see iofs)
+    Img X, Xt, H1, H2, H3, D3, T2, T1, At1, At2, Z1, Z2, St, Sp, Ut, Up;
+    Img Wf[3], Wb[3];
+    float *d4 = nullptr, *dd4 = nullptr, *dz4 = nullptr, *vh = nullptr;
+    double *lrow = nullptr, *prow = nullptr, *loss = nullptr, *lpart = nullptr;
+    float* colpart[4] = {};  // gw4, gb2, gb1, gb0 per-warp column sums
+    float* part[3] = {};     // weight-gradient partials
+    int splits[3] = {1, 1, 1};
     std::vector<void*> allocs;
+    std::vector<std::pair<const void*, CUtensorMap>> maps;  // weight-gradient operand views of the image planes
     std::string err;
 };
 
@@ -305,9 +879,6 @@ int dtfail(msk_disc_trainer* t, const std::string& m, int code = MSK_ERR_CONTRAC
 void ckc(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
-void ckb(cublasStatus_t s, const char* what) {
-    if (s != CUBLAS_STATUS_SUCCESS) throw std::runtime_error(std::string(what) + ": cuBLAS status " + std::to_string(s));
-}
 
 template <class T>
 T* talloc(msk_disc_trainer* t, size_t n) {
@@ -318,93 +889,239 @@ T* talloc(msk_disc_trainer* t, size_t n) {
     return static_cast<T*>(p);
 }
 
-cublasComputeType_t compute_type(int math) { return math == 1 ? CUBLAS_COMPUTE_32F_FAST_TF32 : CUBLAS_COMPUTE_32F; }
+// 5-D tensor map of one plane of a split image for the weight-gradient GEMMs, in
+// 4-byte units: {128 (4 row groups = 512 B), 4 row quarters, 16 column groups,
+// column blocks, row blocks}; box {128, 1, 16, 1, 1} = a 32-row x 128-column chunk.
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+CUtensorMap img_tmap(const bf16* plane, int rows_p, int cols_p) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        ckc(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q), "cuTensorMapEncodeTiled");
+        if (!fn || q != cudaDriverEntryPointSuccess) throw std::runtime_error("cuTensorMapEncodeTiled unavailable");
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    CUtensorMap m;
+    const cuuint64_t dims[5] = {128, 4, 16, static_cast<cuuint64_t>(cols_p >> 7), static_cast<cuuint64_t>(rows_p >> 7)};
+    const cuuint64_t strides[4] = {512, 2048, 32768, 32768ull * (cols_p >> 7)};  // bytes, dims 1..4
+    const cuuint32_t box[5] = {128, 1, 16, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, const_cast<bf16*>(plane), dims, strides, box,
+                                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return m;
+}
 
-// C (m x n, ldc) = op(A) op(B), column-major f32.
-void gemm(msk_disc_trainer* t, cublasOperation_t ta, cublasOperation_t tb, int m, int n, int k, const float* A,
-          long long lda, const float* B, long long ldb, float* C, long long ldc) {
-    const float one = 1.0f, zero = 0.0f;
-    ckb(cublasGemmEx(t->blas, ta, tb, m, n, k, &one, A, CUDA_R_32F, static_cast<int>(lda), B, CUDA_R_32F,
-                     static_cast<int>(ldb), &zero, C, CUDA_R_32F, static_cast<int>(ldc), compute_type(t->math),
-                     CUBLAS_GEMM_DEFAULT),
-        "cublasGemmEx");
+Img img_alloc(msk_disc_trainer* t, int rows_p, int cols_p) {
+    Img im;
+    im.cols_p = cols_p;
+    im.hi = talloc<bf16>(t, static_cast<size_t>(rows_p) * cols_p);
+    im.lo = talloc<bf16>(t, static_cast<size_t>(rows_p) * cols_p);
+    t->maps.emplace_back(im.hi, img_tmap(im.hi, rows_p, cols_p));
+    t->maps.emplace_back(im.lo, img_tmap(im.lo, rows_p, cols_p));
+    return im;
+}
+
+bool g_prepared = false;
+template <int EPI>
+void prep_row() {
+    ckc(cudaFuncSetAttribute(row_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(kRowSmem)),
+        "cudaFuncSetAttribute");
+}
+int g_sms = 148;
+void prepare_kernels() {
+    if (g_prepared) return;
+    prep_row<kEpiTanh>();
+    prep_row<kEpiHead>();
+    prep_row<kEpiGate>();
+    prep_row<kEpiPlain>();
+    prep_row<kEpiGate2>();
+    prep_row<kEpiTHead>();
+    prep_row<kEpiRev>();
+    int dev = 0;
+    ckc(cudaGetDevice(&dev), "cudaGetDevice");
+    ckc(cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev), "cudaDeviceGetAttribute");
+    ckc(cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kWgSmem)),
+        "cudaFuncSetAttribute");
+    g_prepared = true;
+}
+
+template <int EPI>
+void row(RowArgs a, int tiles, cudaStream_t s) {
+    a.tiles = tiles;
+    const int units = EPI == kEpiRev ? tiles * a.nb : tiles;
+    row_gemm_kernel<EPI><<<std::min(units, g_sms), kRowThreads, kRowSmem, s>>>(a);
+}
+
+RowArgs rargs(const msk_disc_trainer* t, const Img& A, const Img& W, int n_out, int rows) {
+    RowArgs a;
+    a.a_hi[0] = A.hi;
+    a.a_lo[0] = A.lo;
+    a.a_cols = A.cols_p;
+    a.w_hi = W.hi;
+    a.w_lo = W.lo;
+    a.nb = n_out >> 7;
+    a.n_valid = t->H;  // bias / w4 length (only the hidden-width epilogues read them)
+    a.rows = rows;
+    a.passes = t->math == 0 ? 3 : 1;
+    return a;
+}
+
+const CUtensorMap& tmap_of(const msk_disc_trainer* t, const void* plane) {
+    for (const auto& m : t->maps)
+        if (m.first == plane) return m.second;
+    throw std::runtime_error("disc_train: no tensor map for an image plane");
+}
+
+void wgrad(const msk_disc_trainer* t, const Img& S0, const Img& S1, const Img& A0, const Img& A1, int chunks,
+           int splits, float* part, cudaStream_t s) {
+    WgMaps m;
+    const Img* ims[4] = {&S0, &S1, &A0, &A1};
+    for (int k = 0; k < 4; ++k) {
+        CUtensorMap* dst = k < 2 ? m.s[k] : m.a[k - 2];
+        dst[0] = tmap_of(t, ims[k]->hi);
+        dst[1] = tmap_of(t, ims[k]->lo);
+    }
+    WgArgs w;
+    w.s_cols = S0.cols_p;
+    w.a_cols = A0.cols_p;
+    w.chunks = chunks;
+    w.splits = splits;
+    w.passes = t->math == 0 ? 3 : 1;
+    w.part = part;
+    wgrad_kernel<<<dim3(S0.cols_p >> 7, splits), kWgThreads, kWgSmem, s>>>(m, w);
+}
+
+// splits of a weight-gradient GEMM: ~one wave of CTAs over the o-tiles
+int wg_splits(int o_tiles, int total_chunks) { return std::max(1, std::min((148 + o_tiles - 1) / o_tiles, total_chunks)); }
+
+void pack_weights(msk_disc_trainer* t, cudaStream_t s) {
+    WPack P;
+    const long long off[3] = {0, t->o1, t->o2};
+    for (int l = 0; l < 3; ++l) {
+        P.W[l] = t->theta + off[l];
+        P.out[l] = t->H;
+        P.in[l] = l == 0 ? t->din : t->H;
+        P.fwd[l] = t->Wf[l];
+        P.bwd[l] = t->Wb[l];
+    }
+    const int maxn = std::max(t->Hp, t->Dp) * (std::max(t->Hp, t->Dp) >> 3);
+    pack_weights_kernel<<<dim3((maxn + 255) / 256, 6), 256, 0, s>>>(P);
 }
 
 // Loss and dloss/dθ (into t->grad) for B rows of Δ at the current parameters.
 void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaStream_t s) {
-    // R rows (B Δ rows + the zero row) stored with Rp = R rounded up to 4 rows per
-    // half, so every leading dimension and half offset is 16-B aligned (the
-    // aligned cuBLAS kernels); padding rows stay zero in every stacked buffer
-    const int H = t->H, din = t->din, R = B + 1, Rp = (R + 3) & ~3;
-    const long long R2 = 2LL * Rp;
-    ckb(cublasSetStream(t->blas, s), "cublasSetStream");
+    const int H = t->H, din = t->din, R = B + 1, tiles = (R + 127) / 128, rows_p = tiles * 128;
+    const int chunks = (R + kWgRows - 1) / kWgRows;
     const float* th = t->theta32;
-    const float *W0 = th, *b0 = th + static_cast<long long>(H) * din, *W1 = th + t->o1,
-                *b1 = th + t->o1 + static_cast<long long>(H) * H, *W2 = th + t->o2,
-                *b2 = th + t->o2 + static_cast<long long>(H) * H, *w4 = th + t->o3, *b3 = th + t->o3 + H;
+    const float *b0 = th + static_cast<long long>(H) * din, *b1 = th + t->o1 + static_cast<long long>(H) * H,
+                *b2 = th + t->o2 + static_cast<long long>(H) * H, *w4 = th + t->o3, *b4 = th + t->o3 + H;
     float* g = t->grad;
     float *gW0 = g, *gb0 = g + static_cast<long long>(H) * din, *gW1 = g + t->o1,
           *gb1 = g + t->o1 + static_cast<long long>(H) * H, *gW2 = g + t->o2,
-          *gb2 = g + t->o2 + static_cast<long long>(H) * H, *gw4 = g + t->o3, *gb3 = g + t->o3 + H;
-    const int gR = (Rp + 255) / 256;
-    const dim3 eg((Rp + kRowsPerBlock - 1) / kRowsPerBlock, H);
-    float *Xb = t->X2 + Rp, *Xt = t->X2;  // primal / tangent halves
-    float* Ab[4];
-    float* At[4];
-    for (int l = 1; l <= 3; ++l) {
-        At[l] = t->A[l];
-        Ab[l] = t->A[l] + Rp;
+          *gb2 = g + t->o2 + static_cast<long long>(H) * H, *gw4 = g + t->o3, *gb4 = g + t->o3 + H;
+    const int Hp = t->Hp, Dp = t->Dp;
+
+    {
+        const long long n = static_cast<long long>(rows_p) * (Dp >> 3);
+        pack_input_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(delta, B, ld, din, rows_p, t->X);
     }
-
-    // ---- forward (nn.cpp:54-73) ----
-    pack_input_kernel<<<dim3((Rp + 31) / 32, (din + 31) / 32), dim3(32, 8), 0, s>>>(delta, B, ld, din, R, Rp, t->X2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, din, Xb, R2, W0, H, Ab[1], R2);
-    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[1], R, Rp, R2, b0);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, Ab[1], R2, W1, H, Ab[2], R2);
-    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[2], R, Rp, R2, b1);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, Ab[2], R2, W2, H, Ab[3], R2);
-    bias_tanh_kernel<<<eg, 256, 0, s>>>(Ab[3], R, Rp, R2, b2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, 1, H, Ab[3], R2, w4, 1, t->z4, Rp);
-    head_kernel<<<gR, 256, 0, s>>>(t->z4, b3, B, R, t->d4, t->dd4, t->dz4, t->lrow);
-
+    // ---- forward (nn.cpp:54-73) + head (nn.cpp:66-68) ----
+    RowArgs a = rargs(t, t->X, t->Wf[0], Hp, R);
+    a.bias = b0;
+    a.out[0] = t->H1;
+    row<kEpiTanh>(a, tiles, s);
+    a = rargs(t, t->H1, t->Wf[1], Hp, R);
+    a.bias = b1;
+    a.out[0] = t->H2;
+    row<kEpiTanh>(a, tiles, s);
+    a = rargs(t, t->H2, t->Wf[2], Hp, R);
+    a.bias = b2;
+    a.w4 = w4;
+    a.b4 = b4;
+    a.out[0] = t->H3;
+    a.out[1] = t->D3;
+    a.d4 = t->d4;
+    a.dd4 = t->dd4;
+    a.dz4 = t->dz4;
+    a.lrow = t->lrow;
+    a.B = B;
+    row<kEpiHead>(a, tiles, s);
     // ---- input gradient g = dy/dx (nn.cpp:161-164) ----
-    d3_kernel<<<eg, 256, 0, s>>>(t->d4, w4, Ab[3], R2, R, Rp, t->T1, Rp);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, Rp, H, H, t->T1, Rp, W2, H, t->T2, Rp);
-    gate_kernel<<<eg, 256, 0, s>>>(t->T2, Rp, Ab[2], R2, R, Rp, t->T2, Rp);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, Rp, H, H, t->T2, Rp, W1, H, t->T1, Rp);
-    gate_kernel<<<eg, 256, 0, s>>>(t->T1, Rp, Ab[1], R2, R, Rp, t->T1, Rp);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, Rp, din, H, t->T1, Rp, W0, H, Xt, R2);
-
+    a = rargs(t, t->D3, t->Wb[2], Hp, R);
+    a.h = t->H2;
+    a.out[0] = t->T2;
+    row<kEpiGate>(a, tiles, s);
+    a = rargs(t, t->T2, t->Wb[1], Hp, R);
+    a.h = t->H1;
+    a.out[0] = t->T1;
+    row<kEpiGate>(a, tiles, s);
+    a = rargs(t, t->T1, t->Wb[0], Dp, R);
+    a.out[0] = t->Xt;
+    row<kEpiPlain>(a, tiles, s);
     // ---- forward tangent along g (nn.cpp:167-171) ----
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, din, Xt, R2, W0, H, t->Z[1], Rp);
-    gate_kernel<<<eg, 256, 0, s>>>(t->Z[1], Rp, Ab[1], R2, R, Rp, At[1], R2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, At[1], R2, W1, H, t->Z[2], Rp);
-    gate_kernel<<<eg, 256, 0, s>>>(t->Z[2], Rp, Ab[2], R2, R, Rp, At[2], R2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, H, H, At[2], R2, W2, H, t->Z[3], Rp);
-    gate_kernel<<<eg, 256, 0, s>>>(t->Z[3], Rp, Ab[3], R2, R, Rp, At[3], R2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_T, Rp, 1, H, At[3], R2, w4, 1, t->zeta4, Rp);
-    head2_kernel<<<gR, 256, 0, s>>>(t->d4, t->dd4, t->zeta4, t->dz4, B, R, Rp, static_cast<float>(t->lam / B), t->V,
-                                    t->prow);
-
+    a = rargs(t, t->Xt, t->Wf[0], Hp, R);
+    a.h = t->H1;
+    a.out[0] = t->At1;
+    a.out[1] = t->Z1;
+    row<kEpiGate2>(a, tiles, s);
+    a = rargs(t, t->At1, t->Wf[1], Hp, R);
+    a.h = t->H2;
+    a.out[0] = t->At2;
+    a.out[1] = t->Z2;
+    row<kEpiGate2>(a, tiles, s);
+    a = rargs(t, t->At2, t->Wf[2], Hp, R);
+    a.h = t->H3;
+    a.w4 = w4;
+    a.d4 = t->d4;
+    a.dd4 = t->dd4;
+    a.dz4 = t->dz4;
+    a.vh = t->vh;
+    a.prow = t->prow;
+    a.B = B;
+    a.lamB = static_cast<float>(t->lam / B);
+    a.out[0] = t->St;
+    a.out[1] = t->Sp;
+    a.colpart[0] = t->colpart[0];
+    a.colpart[1] = t->colpart[1];
+    a.ldc = Hp;
+    row<kEpiTHead>(a, tiles, s);
     // ---- reverse pass over [tangent; primal] (nn.cpp:186-221 + nn.cpp:98-128) ----
-    gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, 1, H, static_cast<int>(R2), t->V, R2, t->A[3], R2, gw4, 1);
-    colsum_kernel<<<1, 256, 0, s>>>(t->V + Rp, R, 0, gb3);
-    rev_elem_kernel<true><<<eg, 256, 0, s>>>(t->S1, t->V, w4, Ab[3], R2, t->Z[3], R, Rp, H);
-    // layer 2
-    gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, H, static_cast<int>(R2), t->S1, R2, t->A[2], R2, gW2, H);
-    colsum_kernel<<<H, 256, 0, s>>>(t->S1 + Rp, R, R2, gb2);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(R2), H, H, t->S1, R2, W2, H, t->S2, R2);
-    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S2, nullptr, nullptr, Ab[2], R2, t->Z[2], R, Rp, H);
-    // layer 1
-    gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, H, static_cast<int>(R2), t->S2, R2, t->A[1], R2, gW1, H);
-    colsum_kernel<<<H, 256, 0, s>>>(t->S2 + Rp, R, R2, gb1);
-    gemm(t, CUBLAS_OP_N, CUBLAS_OP_N, static_cast<int>(R2), H, H, t->S2, R2, W1, H, t->S1, R2);
-    rev_elem_kernel<false><<<eg, 256, 0, s>>>(t->S1, nullptr, nullptr, Ab[1], R2, t->Z[1], R, Rp, H);
-    // layer 0
-    gemm(t, CUBLAS_OP_T, CUBLAS_OP_N, H, din, static_cast<int>(R2), t->S1, R2, t->X2, R2, gW0, H);
-    colsum_kernel<<<H, 256, 0, s>>>(t->S1 + Rp, R, R2, gb0);
-
-    loss_kernel<<<1, 1024, 0, s>>>(t->lrow, t->prow, R, t->lam, t->loss);
+    wgrad(t, t->St, t->Sp, t->At2, t->H2, chunks, t->splits[2], t->part[2], s);
+    a = rargs(t, t->St, t->Wb[2], Hp, R);
+    a.a_hi[1] = t->Sp.hi;
+    a.a_lo[1] = t->Sp.lo;
+    a.h = t->H2;
+    a.z = t->Z2;
+    a.out[0] = t->Ut;
+    a.out[1] = t->Up;
+    a.colpart[0] = t->colpart[2];
+    a.ldc = Hp;
+    row<kEpiRev>(a, tiles, s);
+    wgrad(t, t->Ut, t->Up, t->At1, t->H1, chunks, t->splits[1], t->part[1], s);
+    a = rargs(t, t->Ut, t->Wb[1], Hp, R);
+    a.a_hi[1] = t->Up.hi;
+    a.a_lo[1] = t->Up.lo;
+    a.h = t->H1;
+    a.z = t->Z1;
+    a.out[0] = t->St;
+    a.out[1] = t->Sp;
+    a.colpart[0] = t->colpart[3];
+    a.ldc = Hp;
+    row<kEpiRev>(a, tiles, s);
+    wgrad(t, t->St, t->Sp, t->Xt, t->X, chunks, t->splits[0], t->part[0], s);
+    // ---- fixed-order reductions into the θ-layout gradient ----
+    wg_reduce_kernel<<<(H * din + 255) / 256, 256, 0, s>>>(t->part[0], t->splits[0], Dp, Hp, din, H, gW0);
+    wg_reduce_kernel<<<(H * H + 255) / 256, 256, 0, s>>>(t->part[1], t->splits[1], Hp, Hp, H, H, gW1);
+    wg_reduce_kernel<<<(H * H + 255) / 256, 256, 0, s>>>(t->part[2], t->splits[2], Hp, Hp, H, H, gW2);
+    colred_kernel<<<H, 256, 0, s>>>(t->colpart[0], tiles * 4, Hp, gw4);
+    colred_kernel<<<H, 256, 0, s>>>(t->colpart[1], tiles * 4, Hp, gb2);
+    colred_kernel<<<H, 256, 0, s>>>(t->colpart[2], tiles * 4, Hp, gb1);
+    colred_kernel<<<H, 256, 0, s>>>(t->colpart[3], tiles * 4, Hp, gb0);
+    const int lb = std::min(kLossBlocks, R);
+    loss_part_kernel<<<lb, 256, 0, s>>>(t->lrow, t->prow, t->vh, R, t->lpart);
+    loss_final_kernel<<<1, 1, 0, s>>>(t->lpart, lb, t->lam, t->loss, gb4);
     ckc(cudaGetLastError(), "disc train kernels");
 }
 
@@ -434,7 +1151,10 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
     auto t = new msk_disc_trainer();
     try {
         if (n_in < 1 || hidden < 1 || max_rows < 1) throw std::invalid_argument("disc_trainer: bad dimensions");
-        if (math < 0 || math > 1) throw std::invalid_argument("disc_trainer: math must be 0 (FP32) or 1 (TF32)");
+        if (n_in > 256 || hidden > 256)
+            throw std::invalid_argument("disc_trainer: input width and hidden width must be <= 256");
+        if (math < 0 || math > 1)
+            throw std::invalid_argument("disc_trainer: math must be 0 (fp32-class split-bf16) or 1 (bf16)");
         if (!theta) throw std::invalid_argument("disc_trainer: theta is null");
         if (!(lr > 0.0) || !(grad_penalty >= 0.0)) throw std::invalid_argument("disc_trainer: need lr > 0, λ >= 0");
         const long long H = hidden, din = n_in;
@@ -446,6 +1166,7 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
         int major = 0;
         ckc(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device), "cudaDeviceGetAttribute");
         if (major != 10) throw std::runtime_error("disc_trainer: needs an sm_100 device");
+        prepare_kernels();
         t->device = device;
         t->din = n_in;
         t->H = hidden;
@@ -457,6 +1178,8 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
         t->o3 = t->o2 + H * H + H;
         t->lr = lr;
         t->lam = grad_penalty;
+        t->Hp = static_cast<int>((H + 127) & ~127LL);
+        t->Dp = static_cast<int>((din + 127) & ~127LL);
         t->theta = talloc<double>(t, P);
         t->m = talloc<double>(t, P);
         t->v = talloc<double>(t, P);
@@ -466,22 +1189,31 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
         t->bad = talloc<int>(t, 1);
         ckc(cudaMemcpy(t->theta, theta, P * sizeof(double), cudaMemcpyHostToDevice), "upload theta");
         to_f32_kernel<<<grid_for(P), 256>>>(t->theta, P, t->theta32);
-        const size_t R = (static_cast<size_t>(max_rows) + 1 + 3) & ~static_cast<size_t>(3), RH = R * H;  // padded
-        t->X2 = talloc<float>(t, 2 * R * din);
-        for (int l = 1; l <= 3; ++l) {
-            t->A[l] = talloc<float>(t, 2 * RH);
-            t->Z[l] = talloc<float>(t, RH);
+        const int tiles = (max_rows + 1 + 127) / 128, rows_p = tiles * 128;
+        t->rows_p = rows_p;
+        const int Hp = t->Hp, Dp = t->Dp;
+        t->X = img_alloc(t, rows_p, Dp);
+        t->Xt = img_alloc(t, rows_p, Dp);
+        for (Img* im : {&t->H1, &t->H2, &t->H3, &t->D3, &t->T2, &t->T1, &t->At1, &t->At2, &t->Z1, &t->Z2, &t->St,
+                        &t->Sp, &t->Ut, &t->Up})
+            *im = img_alloc(t, rows_p, Hp);
+        for (int l = 0; l < 3; ++l) {
+            const int inp = l == 0 ? Dp : Hp;
+            t->Wf[l] = img_alloc(t, Hp, inp);
+            t->Wb[l] = img_alloc(t, inp, Hp);
         }
-        t->T1 = talloc<float>(t, RH);
-        t->T2 = talloc<float>(t, RH);
-        t->S1 = talloc<float>(t, 2 * RH);
-        t->S2 = talloc<float>(t, 2 * RH);
-        for (float** p : {&t->z4, &t->d4, &t->dd4, &t->dz4, &t->zeta4}) *p = talloc<float>(t, R);
-        t->V = talloc<float>(t, 2 * R);
-        t->lrow = talloc<double>(t, R);
-        t->prow = talloc<double>(t, R);
+        for (float** p : {&t->d4, &t->dd4, &t->dz4, &t->vh}) *p = talloc<float>(t, rows_p);
+        t->lrow = talloc<double>(t, rows_p);
+        t->prow = talloc<double>(t, rows_p);
         t->loss = talloc<double>(t, 3);
-        ckb(cublasCreate(&t->blas), "cublasCreate");
+        t->lpart = talloc<double>(t, 3 * kLossBlocks);
+        for (int k = 0; k < 4; ++k) t->colpart[k] = talloc<float>(t, static_cast<size_t>(tiles) * 4 * Hp);
+        const int total = 2 * ((max_rows + 1 + kWgRows - 1) / kWgRows);
+        for (int l = 0; l < 3; ++l) {
+            t->splits[l] = wg_splits(Hp >> 7, total);
+            t->part[l] = talloc<float>(t, static_cast<size_t>(t->splits[l]) * (l == 0 ? Dp : Hp) * Hp);
+        }
+        pack_weights(t, nullptr);
         ckc(cudaDeviceSynchronize(), "disc_trainer init");
         *out = t;
         return MSK_OK;
@@ -500,7 +1232,6 @@ void msk_disc_trainer_destroy(msk_disc_trainer* t) {
     if (!t) return;
     cudaSetDevice(t->device);
     cudaDeviceSynchronize();
-    if (t->blas) cublasDestroy(t->blas);
     for (void* p : t->allocs) cudaFree(p);
     delete t;
 }
@@ -537,6 +1268,7 @@ int msk_disc_train_step(msk_disc_trainer* t, const float* delta, int32_t rows, i
         adam_kernel<<<grid_for(t->P), 256, 0, s>>>(t->grad, t->P, t->bad, t->counts, t->lr, 0.9, 0.999, 1e-8,
                                                    t->theta, t->m, t->v, t->theta32);
         adam_commit_kernel<<<1, 1, 0, s>>>(t->bad, t->counts);
+        pack_weights(t, s);  // the GEMM images of the new θ
         ckc(cudaGetLastError(), "adam");
         if (loss) ckc(cudaMemcpyAsync(loss, t->loss, 24, cudaMemcpyDeviceToDevice, s), "copy loss");
         return MSK_OK;

@@ -45,7 +45,7 @@ def main():
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
     f = flops(B, din, H)
-    print(json.dumps({"rows": B, "din": din, "hidden": H, "math": ["fp32", "tf32"][math], "ms_per_step": ms,
+    print(json.dumps({"rows": B, "din": din, "hidden": H, "math": ["fp32-class split-bf16", "bf16"][math], "ms_per_step": ms,
                       "gflop_per_step": f / 1e9, "tflops": f / (ms * 1e-3) / 1e12,
                       "loss": tr.loss.cpu().tolist()}))
     tr.close()
