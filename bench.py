@@ -199,6 +199,10 @@ def run_reference(args, rank, world):
     cfg = env_config(episode_horizon=C["horizon"], rsi=C["rsi"])
     b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads, reward_mode=C["reward_mode"])
     b.set_eval_mode(C["eval"])
+    if C["disc"]:  # Env::step(action, fn) with the reference's own Mlp as fn (same θ as the GPU arm)
+        import paper_2603_29332_b200 as pk
+
+        b.set_discriminator(pk.mlp_init(b.delta_dim, C["disc"][0], C["disc"][1]), C["disc"][0])
     b.reset()
     for _ in range(args.warmup):
         b.bench(1)
@@ -209,7 +213,7 @@ def run_reference(args, rank, world):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Philox excitations, generated dance clip)", "impl": "reference",
             "config": {"workload": f"{args.config}: {C['desc']} (CPU sample"
-                                   + ("; D(Δ) reward not included: the reference's Mlp needs Eigen)" if C["disc"] else ")"),
+                                   + ("; D(Δ) reward by the reference's own Mlp::forward_one)" if C["disc"] else ")"),
                        "config": args.config, "envs": n_envs,
                        "parallelism": f"{threads} host threads (ThreadPool::parallel_chunks)"},
             "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "reference",
@@ -230,6 +234,10 @@ def cpu_baseline_sample(args):
     b = RefBatch(mp, cp, n_envs, cfg=env_config(episode_horizon=C["horizon"], rsi=C["rsi"]), threads=threads,
                  reward_mode=C["reward_mode"])
     b.set_eval_mode(C["eval"])
+    if C["disc"]:
+        import paper_2603_29332_b200 as pk
+
+        b.set_discriminator(pk.mlp_init(b.delta_dim, C["disc"][0], C["disc"][1]), C["disc"][0])
     b.reset()
     b.bench(1)
     secs, steps = b.bench(1)

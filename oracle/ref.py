@@ -114,6 +114,8 @@ def ref_lib():
         lib.ref_rng_uniform.argtypes = [C.c_uint64, C.c_double, C.c_double, C.c_int64, _dp]
         lib.ref_bench.restype = C.c_double
         lib.ref_bench.argtypes = [C.c_void_p, C.c_int32, C.c_uint64, C.POINTER(C.c_int64)]
+        lib.ref_set_discriminator.argtypes = [C.c_void_p, _dp, C.c_int64, C.c_int32]
+        lib.ref_set_discriminator.restype = C.c_int32
         for fn in ("ref_force_length_active", "ref_force_velocity", "ref_force_passive", "ref_wrap_angle"):
             getattr(lib, fn).restype = C.c_double
             getattr(lib, fn).argtypes = [C.c_double]
@@ -270,6 +272,13 @@ class RefBatch:
 
     def rng_deserialize(self, env, text):
         self.lib.ref_rng_deserialize(self.h, int(env), text.encode())
+
+    def set_discriminator(self, theta, hidden):
+        """ref_bench's tracking reward: the reference's Mlp(dΔ, hidden, 1, Sigmoid) with theta."""
+        theta = np.ascontiguousarray(theta, dtype=np.float64)
+        rc = self.lib.ref_set_discriminator(self.h, _ptr(theta, _dp), theta.size, hidden)
+        if rc != 0:
+            raise ValueError("ref_set_discriminator: parameter count mismatch")
 
     def bench(self, steps, action_seed=0x5EED):
         n = C.c_int64(0)

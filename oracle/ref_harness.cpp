@@ -19,6 +19,7 @@
 #include "msk/errors.hpp"
 #include "msk/model.hpp"
 #include "msk/muscle.hpp"
+#include "msk/nn.hpp"
 #include "msk/reference.hpp"
 #include "msk/skeleton.hpp"
 #include "msk/thread_pool.hpp"
@@ -87,6 +88,7 @@ struct Batch {
     std::vector<std::unique_ptr<msk::Env>> envs;
     std::unique_ptr<msk::ThreadPool> pool;
     int obs_dim = 0, delta_dim = 0;
+    std::unique_ptr<msk::Mlp> disc;  // tracking-reward discriminator for ref_bench (optional)
 };
 
 void set_err(char* err, int n, const std::string& msg) {
@@ -416,6 +418,26 @@ void ref_excitations(uint64_t seed, uint32_t step, int64_t global_env_offset, in
 // Timed CPU loop: `steps` control steps of every env with Philox actions,
 // done envs reset before their next step (the batched-harness convention).
 // Returns wall seconds; *env_steps receives the number of env-steps taken.
+// The reference's own Mlp(in = dΔ, hidden, 1, Head::Sigmoid) with parameters
+// theta (nn.cpp:16-38 flat layout) as ref_bench's tracking reward; null clears it.
+int32_t ref_set_discriminator(void* h, const double* theta, int64_t n, int32_t hidden) {
+    Batch& b = *static_cast<Batch*>(h);
+    if (!theta) {
+        b.disc.reset();
+        return 0;
+    }
+    msk::MlpShape sh;
+    sh.in = b.delta_dim;
+    sh.hidden = hidden;
+    sh.out = 1;
+    sh.head = msk::Head::Sigmoid;
+    auto m = std::make_unique<msk::Mlp>(sh, 0);
+    if (m->param_count() != n) return 1;
+    for (int64_t i = 0; i < n; ++i) m->params()[i] = theta[i];
+    b.disc = std::move(m);
+    return 0;
+}
+
 double ref_bench(void* h, int32_t steps, uint64_t action_seed, int64_t* env_steps) {
     Batch& b = *static_cast<Batch*>(h);
     const int n = static_cast<int>(b.envs.size());
@@ -428,7 +450,13 @@ double ref_bench(void* h, int32_t steps, uint64_t action_seed, int64_t* env_step
             msk::Env& env = *b.envs[static_cast<size_t>(e)];
             if (env.done()) env.reset();
             for (int m = 0; m < nm; ++m) a[m] = excitation(action_seed, step_ctr, static_cast<uint32_t>(e), m);
-            env.step(a);
+            if (b.disc)  // Env::step(action, fn), fn = reward_from_discriminator
+                env.step(a, [&](const Eigen::VectorXd& d) {
+                    const double y = b.disc->forward_one(d)[0];
+                    return -std::log(1.0 - std::min(std::max(y, 1e-4), 1.0 - 1e-4));
+                });
+            else
+                env.step(a);
             ++counts[static_cast<size_t>(e)];
         }
     };

@@ -342,14 +342,11 @@ __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tac
                 g.lrow[r] = -log(yc);
             }
         }
-        // pass 2: d3 = d4 w4 ∘ (1 - H3²)  (nn.cpp:161)
+        // pass 2: d3 = d4 w4 ∘ (1 - H3²)  (nn.cpp:161), H3 read back (L2) from pass 1's image
         for (int c = c_lo; c < c_hi; c += 16) {
-            tmem_ld16(tl + c, v);
+            load16(g.out[0], r, c, x);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const float h = tanhf(v[i] + sb[c + i]);
-                v[i] = valid ? d4 * sw[c + i] * (1.0f - h * h) : 0.0f;
-            }
+            for (int i = 0; i < 16; ++i) v[i] = valid ? d4 * sw[c + i] * (1.0f - x[i] * x[i]) : 0.0f;
             store16(g.out[1], r, c, v);
         }
     } else if constexpr (EPI == kEpiTHead) {
@@ -723,30 +720,47 @@ __global__ void pack_weights_kernel(WPack P) {
     *reinterpret_cast<uint4*>(im.lo + o) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
 }
 
-// grad_W[i * out + o] = Σ_s part[s][i][o] (fixed order, f64)
-__global__ void wg_reduce_kernel(const float* __restrict__ part, int splits, int a_cols, int s_cols, int n_in,
-                                 int n_out, float* gW) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n_in * n_out) return;
-    const int i = t / n_out, o = t % n_out;
-    double s = 0.0;
-    for (int k = 0; k < splits; ++k) s += part[(static_cast<size_t>(k) * a_cols + i) * s_cols + o];
-    gW[t] = static_cast<float>(s);
-}
-
-// out[j] = Σ_rows colpart[row][j]: one block per column, fixed-order f64 tree.
-__global__ void __launch_bounds__(256) colred_kernel(const float* __restrict__ cp, int rows, int ldc, float* out) {
-    __shared__ double red[8];
-    const int j = blockIdx.x;
-    double s = 0.0;
-    for (int i = threadIdx.x; i < rows; i += 256) s += cp[static_cast<size_t>(i) * ldc + j];
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += red[w];
-        out[j] = static_cast<float>(t);
+// All fixed-order gradient reductions in one launch (blockIdx.y = job):
+//   jobs 0-2: grad_W[i * out + o] = Σ_s part[s][i][o] (f64; four interleaved
+//             partial sums combined in a fixed order), one thread per element;
+//   jobs 3-6: out[j] = Σ_rows colpart[row][j], 32 columns per block.
+struct RedJobs {
+    const float* part[3];
+    int splits[3], a_cols[3], n_in[3];
+    float* gW[3];
+    const float* cp[4];
+    float* cout[4];
+    int s_cols, n_out, cp_rows, ldc;
+};
+__global__ void __launch_bounds__(256) grad_reduce_kernel(const RedJobs J) {
+    const int job = blockIdx.y;
+    if (job < 3) {
+        const int t = blockIdx.x * 256 + threadIdx.x;
+        if (t >= J.n_in[job] * J.n_out) return;
+        const int i = t / J.n_out, o = t % J.n_out;
+        const float* p = J.part[job] + static_cast<size_t>(i) * J.s_cols + o;
+        const size_t st = static_cast<size_t>(J.a_cols[job]) * J.s_cols;
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        int k = 0;
+        for (; k + 3 < J.splits[job]; k += 4)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s[u] += p[(k + u) * st];
+        for (; k < J.splits[job]; ++k) s[0] += p[k * st];
+        J.gW[job][t] = static_cast<float>((s[0] + s[1]) + (s[2] + s[3]));
+    } else {  // 32 columns per block: lanes = columns (coalesced rows), warps = row strides
+        __shared__ double red[8][32];
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, j = blockIdx.x * 32 + lane;
+        if (blockIdx.x * 32 >= J.n_out) return;
+        double s = 0.0;
+        if (j < J.n_out)
+            for (int r = w; r < J.cp_rows; r += 8) s += J.cp[job - 3][static_cast<size_t>(r) * J.ldc + j];
+        red[w][lane] = s;
+        __syncthreads();
+        if (w == 0 && j < J.n_out) {
+            double t = 0.0;
+            for (int k = 0; k < 8; ++k) t += red[k][lane];
+            J.cout[job - 3][j] = static_cast<float>(t);
+        }
     }
 }
 
@@ -785,16 +799,24 @@ __global__ void __launch_bounds__(256) loss_part_kernel(const double* __restrict
     }
 }
 __global__ void loss_final_kernel(const double* __restrict__ part, int nb, double lam, double* loss, float* gb4) {
+    const int lane = threadIdx.x;  // one warp: lane-strided sums, fixed butterfly
     double s = 0.0, p = 0.0, g = 0.0;
-    for (int k = 0; k < nb; ++k) {
+    for (int k = lane; k < nb; k += 32) {
         s += part[3 * k];
         p += part[3 * k + 1];
         g += part[3 * k + 2];
     }
-    loss[0] = s + lam * p;
-    loss[1] = s;
-    loss[2] = p;
-    *gb4 = static_cast<float>(g);
+    for (int o = 16; o > 0; o >>= 1) {
+        s += __shfl_xor_sync(0xffffffffu, s, o);
+        p += __shfl_xor_sync(0xffffffffu, p, o);
+        g += __shfl_xor_sync(0xffffffffu, g, o);
+    }
+    if (lane == 0) {
+        loss[0] = s + lam * p;
+        loss[1] = s;
+        loss[2] = p;
+        *gb4 = static_cast<float>(g);
+    }
 }
 
 __global__ void finite_kernel(const float* __restrict__ g, long long n, int* bad) {
@@ -1112,16 +1134,31 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     row<kEpiRev>(a, tiles, s);
     wgrad(t, t->St, t->Sp, t->Xt, t->X, chunks, t->splits[0], t->part[0], s);
     // ---- fixed-order reductions into the θ-layout gradient ----
-    wg_reduce_kernel<<<(H * din + 255) / 256, 256, 0, s>>>(t->part[0], t->splits[0], Dp, Hp, din, H, gW0);
-    wg_reduce_kernel<<<(H * H + 255) / 256, 256, 0, s>>>(t->part[1], t->splits[1], Hp, Hp, H, H, gW1);
-    wg_reduce_kernel<<<(H * H + 255) / 256, 256, 0, s>>>(t->part[2], t->splits[2], Hp, Hp, H, H, gW2);
-    colred_kernel<<<H, 256, 0, s>>>(t->colpart[0], tiles * 4, Hp, gw4);
-    colred_kernel<<<H, 256, 0, s>>>(t->colpart[1], tiles * 4, Hp, gb2);
-    colred_kernel<<<H, 256, 0, s>>>(t->colpart[2], tiles * 4, Hp, gb1);
-    colred_kernel<<<H, 256, 0, s>>>(t->colpart[3], tiles * 4, Hp, gb0);
+    {
+        RedJobs J;
+        float* gws[3] = {gW0, gW1, gW2};
+        for (int l = 0; l < 3; ++l) {
+            J.part[l] = t->part[l];
+            J.splits[l] = t->splits[l];
+            J.a_cols[l] = l == 0 ? Dp : Hp;
+            J.n_in[l] = l == 0 ? din : H;
+            J.gW[l] = gws[l];
+        }
+        float* couts[4] = {gw4, gb2, gb1, gb0};
+        for (int k = 0; k < 4; ++k) {
+            J.cp[k] = t->colpart[k];
+            J.cout[k] = couts[k];
+        }
+        J.s_cols = Hp;
+        J.n_out = H;
+        J.cp_rows = tiles * 4;
+        J.ldc = Hp;
+        const int bx = std::max((std::max(din, H) * H + 255) / 256, (H + 31) / 32);
+        grad_reduce_kernel<<<dim3(bx, 7), 256, 0, s>>>(J);
+    }
     const int lb = std::min(kLossBlocks, R);
     loss_part_kernel<<<lb, 256, 0, s>>>(t->lrow, t->prow, t->vh, R, t->lpart);
-    loss_final_kernel<<<1, 1, 0, s>>>(t->lpart, lb, t->lam, t->loss, gb4);
+    loss_final_kernel<<<1, 32, 0, s>>>(t->lpart, lb, t->lam, t->loss, gb4);
     ckc(cudaGetLastError(), "disc train kernels");
 }
 

@@ -378,3 +378,20 @@ def test_discriminator_and_policy_mlps_match_reference_nn_cpp():
     y = 0.5 * mlp_forward(mlp_layers(th, 40, 64, 24), X) + 0.25
     ref = ref_mlp_forward(th, 40, 64, 24, X, head=HEAD_AFFINE, affine=(0.5, 0.25))
     assert np.max(np.abs(y - ref)) <= 1e-13 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SO), reason="reference build oracle/_ref absent")
+def test_reference_bench_with_discriminator_reward():
+    """The CPU arm's c4 tracking reward: the reference's own Mlp (Head::Sigmoid) as
+    Env::step's TrackingRewardFn; a wrong parameter count is refused."""
+    from oracle.oracle import mlp_init
+    from oracle.ref import RefBatch, env_config
+
+    mp, cp = model_paths("arm2_m6")
+    b = RefBatch(mp, cp, 2, cfg=env_config(episode_horizon=50, rsi=True), threads=1)
+    with pytest.raises(ValueError):
+        b.set_discriminator(np.zeros(5), 16)
+    b.set_discriminator(mlp_init(b.delta_dim, 16, 7), 16)
+    b.reset()
+    secs, steps = b.bench(3)
+    assert steps == 6 and secs > 0
