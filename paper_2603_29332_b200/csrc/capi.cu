@@ -22,6 +22,7 @@ namespace msk_b200 {
 cudaError_t prepare_kernels(int smem_bytes_per_block);
 int envs_per_block();
 int lanes_per_env();
+int step_envs_per_warp();
 void launch_step(const DevModel&, const DevState&, int env0, int n, const float* actions, float* obs, float* delta,
                  float* raux, uint8_t* flags, float* power, float* grf, cudaStream_t, int n_substeps = kSubsteps);
 void launch_reset(const DevModel&, const DevState&, int n, int mode, const uint8_t* mask, uint8_t bits,
@@ -436,6 +437,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         // (minus the reset kernel's static env list, kResetRange ints)
         const int avail = static_cast<int>(prop.sharedMemPerBlockOptin) - M.tab_bytes - 1088;
         M.epb = std::min(envs_per_block(), avail / std::max(1, M.smem_env_bytes));
+        M.epb -= M.epb % step_envs_per_warp();  // the env-vectorised step kernel fills whole warps
         if (M.epb < 1)
             throw ConfigError("model needs " + std::to_string(M.tab_bytes + M.smem_env_bytes) +
                               " B of shared memory per env");

@@ -23,6 +23,7 @@
 // so a step is bit-reproducible.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <stdexcept>
 
 #include <cstdint>
@@ -820,6 +821,7 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
             float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
             float P2 = u[8];
             const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
+#pragma unroll 1  // mostly one child: an unrolled 4/2/1 cascade costs more branches than it saves (A/B +1.8 %)
             for (int c = c0; c < c1; ++c) {
                 const float* uc = S.un + kLinkStride * S.tchild[c];
                 const float2* uc2 = reinterpret_cast<const float2*>(uc);
@@ -959,6 +961,105 @@ __device__ __forceinline__ double* stage_q(const DevModel& M, const EnvSmem& S, 
     }
     __syncwarp(S.hm);
     return qsm;
+}
+
+// Env epilogue of a control step (env.cpp:214-262): state write-back, then for a
+// diverged env zeroed outputs and the failure flag, else Δ, observation,
+// reward_aux, termination and the episode outcome.  Shared by the step kernels.
+template <int QS>
+__device__ __forceinline__ void step_epilogue(const DevModel& M, const DevState& St, const EnvSmem& S, int e, int le,
+                                              const double (&qd)[QS], const double (&dqd)[QS], int diverged_at,
+                                              int n_substeps, float* obs, float* delta, float* reward_aux,
+                                              uint8_t* flags, float* power, float* grf_row, float* pw, int lane) {
+    const int nq = M.nq, nm = M.nm, nl = M.nl;
+    const size_t mb = static_cast<size_t>(e) * nm;
+    // ---- write back the simulation state ----
+#pragma unroll
+    for (int k = 0; k < QS; ++k) {
+        const int d = lane + S.G * k;
+        if (d < nq) {
+            St.q[static_cast<size_t>(e) * nq + d] = qd[k];
+            St.dq[static_cast<size_t>(e) * nq + d] = dqd[k];
+        }
+    }
+    const int n_sub = diverged_at >= 0 ? diverged_at + 1 : n_substeps;
+    if (lane == 0) {
+        double t = St.t[e];
+        for (int s = 0; s < n_sub; ++s) t += kSimDt;
+        St.t[e] = t;
+    }
+    if (n_substeps != kSubsteps) return;  // msk_gpu_substeps: continuous state only
+    const int obs_dim = 3 * nq + 6 * M.nk + 4 * nm;
+    const int ddim = 3 + M.nj + 2 * M.nk;
+    float* obs_row = obs ? obs + static_cast<size_t>(le) * obs_dim : nullptr;
+    float* drow = delta ? delta + static_cast<size_t>(le) * ddim : nullptr;
+
+    if (diverged_at >= 0) {  // env.cpp:214-229
+        if (obs_row)
+            for (int i = lane; i < obs_dim; i += S.G) obs_row[i] = 0.0f;
+        if (drow)
+            for (int i = lane; i < ddim; i += S.G) drow[i] = 0.0f;
+        if (power)
+            for (int m = lane; m < nm; m += S.G) power[static_cast<size_t>(le) * nm + m] = 0.0f;
+        if (grf_row)
+            for (int i = lane; i < 2 * nl; i += S.G) grf_row[i] = 0.0f;
+        if (lane == 0) {
+            if (reward_aux) reward_aux[le] = 0.0f;
+            if (flags) flags[le] = kFlagDone | kFlagFailed | kFlagDiverged;
+            St.done[e] = 1;
+            const int c = St.out_count[e];
+            if (c < St.out_cap) {
+                St.out_bin[static_cast<size_t>(e) * St.out_cap + c] = phase_bin(M, St.start[e]);
+                St.out_failed[static_cast<size_t>(e) * St.out_cap + c] = 1;
+            }
+            St.out_count[e] = c + 1;
+        }
+        return;
+    }
+
+    // ---- env epilogue (env.cpp:231-262) ----
+    const int t_index = St.t_index[e] + 1;
+    const int steps = St.steps[e] + 1;
+    tree_sweep<false>(M, S, lane, nullptr);
+    const double* qsm = stage_q<QS>(M, S, qd, lane);
+    const bool far = write_delta(M, S, qsm, t_index, drow, lane);
+    if (obs_row) write_obs(M, St, S, qsm, e, t_index, obs_row, lane);
+
+    float aux = 0.0f;
+    if (M.reward_mode == 1 && M.n_emg > 0) {
+        float s = 0.0f;
+        for (int ch = lane; ch < M.n_emg_ch; ch += S.G) {
+            const float d = static_cast<float>(M.clip_emg[static_cast<size_t>(t_index) * M.n_emg + ch]) -
+                            St.act[mb + __ldg(M.emg_map + ch)];
+            s = fmaf(d, d, s);
+        }
+        for (int o = S.G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(S.hm, s, o);
+        aux = M.n_emg_ch > 0 ? M.w_emg * (-s / static_cast<float>(M.n_emg_ch)) : 0.0f;
+    } else if (M.reward_mode == 2) {
+        float s = 0.0f;
+        for (int m = lane; m < nm; m += S.G) s += pw[m];
+        for (int o = S.G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(S.hm, s, o);
+        aux = M.w_power * (-s / static_cast<float>(max(1, nm)));
+    }
+    if (lane == 0) {
+        const bool failed = !M.eval_mode && far;
+        const bool horizon = steps >= M.horizon || t_index >= M.frames - 1;
+        uint8_t f = 0;
+        if (failed || horizon) {
+            f = kFlagDone | (failed ? kFlagFailed : 0);
+            St.done[e] = 1;
+            const int c = St.out_count[e];
+            if (c < St.out_cap) {
+                St.out_bin[static_cast<size_t>(e) * St.out_cap + c] = phase_bin(M, St.start[e]);
+                St.out_failed[static_cast<size_t>(e) * St.out_cap + c] = failed ? 1 : 0;
+            }
+            St.out_count[e] = c + 1;
+        }
+        St.t_index[e] = t_index;
+        St.steps[e] = steps;
+        if (flags) flags[le] = f;
+        if (reward_aux) reward_aux[le] = aux;
+    }
 }
 
 }  // namespace
@@ -1116,93 +1217,491 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
     }
 
     PHASE_MARK(5);
-    // ---- write back the simulation state ----
+    step_epilogue<QS>(M, St, S, e, le, qd, dqd, diverged_at, n_substeps, obs, delta, reward_aux, flags, power, grf_row,
+                      pw, lane);
+}
+
+// ============================================================================
+// step kernel, NE envs per thread ("env-vectorised"): every lane of a warp
+// advances NE environments at once — muscle constants, tree tables, work words,
+// loop control and address arithmetic are shared by the NE envs, and each
+// thread carries NE independent dependency chains (ILP instead of warps).
+// Same arithmetic per env as step_kernel (bit-identical results); a block is
+// WPB warps x NE env slots (slot = warp * NE + k).
+// ============================================================================
+namespace {
+
+template <int NE>
+struct EnvRowsN {
+    MuscleRows R[NE];
+    float* pw[NE];
+    bool live[NE];
+};
+
+// One muscle (device index m, NS segments) for the NE envs.
+template <int NS, int NE>
+__device__ __forceinline__ void muscle_one_n(const DevModel& M, const EnvRowsN<NE>& V, const EnvSmem (&S)[NE], int m,
+                                             bool last) {
+    const int nm = M.nm;
+    float4 kc[NS > 0 ? NS : 1];
 #pragma unroll
-    for (int k = 0; k < QS; ++k) {
-        const int d = lane + S.G * k;
-        if (d < nq) {
-            St.q[static_cast<size_t>(e) * nq + d] = qd[k];
-            St.dq[static_cast<size_t>(e) * nq + d] = dqd[k];
-        }
+    for (int k = 0; k < NS; ++k) kc[k] = ldc4(M.seg_kf + k * nm + m);
+    const float4 p0 = ldc4(M.m_p0 + m);
+    const double2 pa = ldc2d(M.m_p1a + m), pb = ldc2d(M.m_p1b + m);
+    bool anypw = false;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) anypw |= V.pw[e] != nullptr;
+    const int ext = anypw ? (__ldg(M.m_meta + m) >> 9) : 0;
+    float u[NE], a0[NE];
+    double lm0[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        u[e] = V.R[e].u[m];
+        a0[e] = V.R[e].act[m];
+        lm0[e] = V.R[e].lm[m];
     }
-    const int n_sub = diverged_at >= 0 ? diverged_at + 1 : n_substeps;
-    if (lane == 0) {
-        double t = St.t[e];
-        for (int s = 0; s < n_sub; ++s) t += kSimDt;
-        St.t[e] = t;
-    }
-    if (n_substeps != kSubsteps) return;  // msk_gpu_substeps: continuous state only
-    const int obs_dim = 3 * nq + 6 * M.nk + 4 * nm;
-    const int ddim = 3 + M.nj + 2 * M.nk;
-    float* obs_row = obs ? obs + static_cast<size_t>(le) * obs_dim : nullptr;
-    float* drow = delta ? delta + static_cast<size_t>(le) * ddim : nullptr;
-
-    if (diverged_at >= 0) {  // env.cpp:214-229
-        if (obs_row)
-            for (int i = lane; i < obs_dim; i += S.G) obs_row[i] = 0.0f;
-        if (drow)
-            for (int i = lane; i < ddim; i += S.G) drow[i] = 0.0f;
-        if (power)
-            for (int m = lane; m < nm; m += S.G) power[static_cast<size_t>(le) * nm + m] = 0.0f;
-        if (grf_row)
-            for (int i = lane; i < 2 * nl; i += S.G) grf_row[i] = 0.0f;
-        if (lane == 0) {
-            if (reward_aux) reward_aux[le] = 0.0f;
-            if (flags) flags[le] = kFlagDone | kFlagFailed | kFlagDiverged;
-            St.done[e] = 1;
-            const int c = St.out_count[e];
-            if (c < St.out_cap) {
-                St.out_bin[static_cast<size_t>(e) * St.out_cap + c] = phase_bin(M, St.start[e]);
-                St.out_failed[static_cast<size_t>(e) * St.out_cap + c] = 1;
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+        double L = 0.0;
+        float tq[NS > 0 ? NS : 1];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) L += kseg(S[e], kc[k], __float_as_int(kc[k].w), tq[k]);
+        // activation + fibre kinematics + Hill force (muscle_update), state stores gated by live
+        const float gain = fmaf(1.5f, a0[e], 0.5f);
+        const float ex = ex2_ftz(u[e] > a0[e] ? p0.y * rcp_ftz(gain) : p0.z * gain);
+        const float a1 = fminf(fmaxf(fmaf(a0[e] - u[e], ex, u[e]), 0.0f), 1.0f);
+        const double prev_len = fma(lm0[e], pa.y, pa.x);
+        const float vm = static_cast<float>((L - prev_len) * pb.y);
+        const double lm1 = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
+        const float F = mtu_force(a1, static_cast<float>(lm1), vm, p0.x);
+        if (V.live[e]) {
+            V.R[e].act[m] = a1;
+            V.R[e].lm[m] = lm1;
+            if (last) {
+                V.R[e].vm[m] = vm;
+                V.R[e].fm[m] = F;
             }
-            St.out_count[e] = c + 1;
+            if (V.pw[e]) V.pw[e][ext] += fabsf(F * vm * p0.w);
         }
-        return;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) S[e].un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
     }
+}
 
-    // ---- env epilogue (env.cpp:231-262) ----
-    const int t_index = St.t_index[e] + 1;
-    const int steps = St.steps[e] + 1;
-    tree_sweep<false>(M, S, lane, nullptr);
-    const double* qsm = stage_q<QS>(M, S, qd, lane);
-    const bool far = write_delta(M, S, qsm, t_index, drow, lane);
-    if (obs_row) write_obs(M, St, S, qsm, e, t_index, obs_row, lane);
+template <int NS, int NE>
+__device__ __forceinline__ void muscle_run_n(const DevModel& M, const EnvRowsN<NE>& V, const EnvSmem (&S)[NE], int lane,
+                                             bool last, int m0, int m1) {
+    if (m0 + lane >= m1) return;
+    for (int m = m0 + lane; m < m1; m += 32) muscle_one_n<NS, NE>(M, V, S, m, last);
+}
 
-    float aux = 0.0f;
-    if (M.reward_mode == 1 && M.n_emg > 0) {
-        float s = 0.0f;
-        for (int ch = lane; ch < M.n_emg_ch; ch += S.G) {
-            const float d = static_cast<float>(M.clip_emg[static_cast<size_t>(t_index) * M.n_emg + ch]) -
-                            St.act[mb + __ldg(M.emg_map + ch)];
-            s = fmaf(d, d, s);
-        }
-        for (int o = S.G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(S.hm, s, o);
-        aux = M.n_emg_ch > 0 ? M.w_emg * (-s / static_cast<float>(M.n_emg_ch)) : 0.0f;
-    } else if (M.reward_mode == 2) {
-        float s = 0.0f;
-        for (int m = lane; m < nm; m += S.G) s += pw[m];
-        for (int o = S.G >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(S.hm, s, o);
-        aux = M.w_power * (-s / static_cast<float>(max(1, nm)));
+template <int NSEG, int NE>
+__device__ __forceinline__ void muscle_phase_n(const DevModel& M, const DevState& St, const EnvSmem (&S)[NE],
+                                               const EnvRowsN<NE>& V, const size_t (&mb)[NE], int lane, bool last) {
+    if constexpr (NSEG > 0) {
+        muscle_run_n<0, NE>(M, V, S, lane, last, M.seg_run[0], M.seg_run[1]);
+        if constexpr (NSEG >= 1) muscle_run_n<1, NE>(M, V, S, lane, last, M.seg_run[1], M.seg_run[2]);
+        if constexpr (NSEG >= 2) muscle_run_n<2, NE>(M, V, S, lane, last, M.seg_run[2], M.seg_run[3]);
+        if constexpr (NSEG >= 3) muscle_run_n<3, NE>(M, V, S, lane, last, M.seg_run[3], M.seg_run[4]);
+        if constexpr (NSEG >= 4) muscle_run_n<4, NE>(M, V, S, lane, last, M.seg_run[4], M.seg_run[5]);
+    } else {  // generic segments: the single-env path per live env
+#pragma unroll
+        for (int e = 0; e < NE; ++e)
+            if (V.live[e]) muscle_phase<0>(M, St, S[e], V.R[e].u, mb[e], V.pw[e], lane, last);
     }
-    if (lane == 0) {
-        const bool failed = !M.eval_mode && far;
-        const bool horizon = steps >= M.horizon || t_index >= M.frames - 1;
-        uint8_t f = 0;
-        if (failed || horizon) {
-            f = kFlagDone | (failed ? kFlagFailed : 0);
-            St.done[e] = 1;
-            const int c = St.out_count[e];
-            if (c < St.out_cap) {
-                St.out_bin[static_cast<size_t>(e) * St.out_cap + c] = phase_bin(M, St.start[e]);
-                St.out_failed[static_cast<size_t>(e) * St.out_cap + c] = failed ? 1 : 0;
+}
+
+// Root-to-leaf sweep (tree_sweep<true>) for NE envs: the link's table entries,
+// work word and parent index are read once.
+template <int NE>
+__device__ __forceinline__ void tree_sweep_n(const DevModel& M, const EnvSmem (&S)[NE], int lane, float* const (&grf)[NE]) {
+    const EnvSmem& S0 = S[0];
+    for (int lev = 0; lev < M.n_levels; ++lev) {
+        const uint32_t ww = S0.twork[32 * lev + lane];
+        if (ww >> 31) {
+            const int l = ww_link(ww);
+            const int dof = link_dof(M, l);
+            const int p = ww_parent(ww);
+            const float4 la = S0.ta[l];
+            const float m = la.w, I = S0.tin[l], mg = m * M.gravity;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                float c, s, ox, oz, w, vx = 0.0f, vz = 0.0f;
+                if (dof < 0) {  // floating root: origin (0,0) relative, pitch q2
+                    c = S[e].root[2];
+                    s = S[e].root[3];
+                    ox = 0.0f;
+                    oz = 0.0f;
+                    w = S[e].dqf[2];
+                    vx = S[e].dqf[0];
+                    vz = S[e].dqf[1];
+                } else {
+                    const double2 rd = S[e].relcs[dof];
+                    const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
+                    w = S[e].dqf[dof];
+                    if (p >= 0) {
+                        const float4 kp = S[e].kin[p];
+                        ox = fmaf(kp.x, la.x, fmaf(-kp.y, la.y, kp.z));
+                        oz = fmaf(kp.y, la.x, fmaf(kp.x, la.y, kp.w));
+                        c = fmaf(kp.x, cr, -kp.y * sr);
+                        s = fmaf(kp.y, cr, kp.x * sr);
+                        const float* up = S[e].un + kLinkStride * p;
+                        const float2 wv = reinterpret_cast<const float2*>(up)[5];  // parent (omega, v_x)
+                        w += wv.x;
+                        vx = fmaf(-wv.x, oz - kp.w, wv.y);
+                        vz = fmaf(wv.x, ox - kp.z, up[9]);
+                    } else {
+                        ox = la.x;
+                        oz = la.y;
+                        c = cr;
+                        s = sr;
+                    }
+                }
+                S[e].kin[l] = make_float4(c, s, ox, oz);
+                float* u = S[e].un + kLinkStride * l;
+                reinterpret_cast<float2*>(u)[5] = make_float2(w, vx);
+                u[9] = vz;
+                const float cx = la.z * c, cz = la.z * s;
+                const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
+                const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
+                float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
+                if ((ww >> 28) & 1) {  // link carries contact spheres
+                    const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
+                    float gx = 0.0f, gz = 0.0f;
+                    for (int sp = s0; sp < s1; ++sp) {
+                        const float4 sd = __ldg(M.sphere + sp);
+                        const float rx = fmaf(c, sd.x, -s * sd.y), rz = fmaf(s, sd.x, c * sd.y);
+                        const float pen = S[e].pen[sp];
+                        if (pen > 0.0f) {
+                            const float fn = fmaxf(0.0f, fmaf(M.c_k, pen, -M.c_c * fmaf(w, rx, vz)));
+                            if (fn > 0.0f) {
+                                const float qz = rz - sd.z;
+                                const float ft = -M.c_mu * fn * tanhf(fmaf(-w, qz, vx) * M.inv_c_vs);
+                                p0 -= fmaf(rx, fn, -qz * ft);
+                                p1 -= ft;
+                                p2 -= fn;
+                                gx += ft * 0.1f;
+                                gz += fn * 0.1f;
+                            }
+                        }
+                    }
+                    if (grf[e]) {
+                        grf[e][2 * l] += gx;
+                        grf[e][2 * l + 1] += gz;
+                    }
+                }
+                float c1 = 0.0f, c2 = 0.0f;
+                if (dof >= 0) {
+                    const float qdot = S[e].dqf[dof];
+                    c1 = qdot * vz;
+                    c2 = -qdot * vx;
+                }
+                float2* u2 = reinterpret_cast<float2*>(u);
+                u2[0] = make_float2(i00, i01);
+                u2[1] = make_float2(i02, m);
+                u2[2] = make_float2(0.0f, m);
+                u2[3] = make_float2(p0, p1);
+                u[8] = p2;
+                u2[6] = make_float2(c1, c2);
             }
-            St.out_count[e] = c + 1;
         }
-        St.t_index[e] = t_index;
-        St.steps[e] = steps;
-        if (flags) flags[le] = f;
-        if (reward_aux) reward_aux[le] = aux;
+        __syncwarp();
     }
+}
+
+// Articulated-body pass, leaves -> root (aba_up) for NE envs.
+template <int NE>
+__device__ __forceinline__ void aba_up_n(const DevModel& M, const EnvSmem (&S)[NE], int lane) {
+    const EnvSmem& S0 = S[0];
+    for (int lev = M.n_levels - 1; lev >= 0; --lev) {
+        const uint32_t ww = S0.twork[32 * lev + lane];
+        if (ww >> 31) {
+            const int l = ww_link(ww);
+            const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
+            const int dof = link_dof(M, l);
+            const int p = ww_parent(ww);
+            float dx = 0.0f, dz = 0.0f;
+#pragma unroll
+            for (int e = 0; e < NE; ++e) {
+                float* u = S[e].un + kLinkStride * l;
+                float2* u2 = reinterpret_cast<float2*>(u);
+                float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
+                float P2 = u[8];
+#pragma unroll 1
+                for (int c = c0; c < c1; ++c) {
+                    const float* uc = S[e].un + kLinkStride * S0.tchild[c];
+                    const float2* uc2 = reinterpret_cast<const float2*>(uc);
+                    const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
+                    r0.x += a0.x;
+                    r0.y += a0.y;
+                    r1.x += a1.x;
+                    r1.y += a1.y;
+                    r2.x += a2.x;
+                    r2.y += a2.y;
+                    r3.x += a3.x;
+                    r3.y += a3.y;
+                    P2 += uc[8];
+                }
+                if (dof < 0) {  // floating root keeps its full articulated inertia
+                    u2[0] = r0;
+                    u2[1] = r1;
+                    u2[2] = r2;
+                    u2[3] = r3;
+                    u[8] = P2;
+                    continue;
+                }
+                const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
+                const float P0 = r3.x, P1 = r3.y;
+                const float invD = rcp_ftz(I00);
+                const float t = S[e].tau[dof];
+                const float uu = (t - P0) * invD;
+                const float U1 = I01 * invD, U2 = I02 * invD;
+                const float a = fmaf(-I01, U1, I11);
+                const float bb = fmaf(-I01, U2, I12);
+                const float cq = fmaf(-I02, U2, I22);
+                const float2 cv = u2[6];
+                const float q1 = fmaf(I01, uu, fmaf(a, cv.x, fmaf(bb, cv.y, P1)));
+                const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
+                u[9] = uu;
+                u2[5] = make_float2(U1, U2);
+                if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
+                    const float2 ol = frame_origin(S[e], l), op = frame_origin(S[e], p);
+                    dx = ol.x - op.x;
+                    dz = ol.y - op.y;
+                    const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
+                    u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
+                    u2[1] = make_float2(be, a);
+                    u2[2] = make_float2(bb, cq);
+                    u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
+                    u[8] = q2;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// Floating-root solve + articulated-body pass, root -> leaves (aba_down) for NE envs.
+template <int NE>
+__device__ __forceinline__ void aba_down_n(const DevModel& M, const EnvSmem (&S)[NE], int lane) {
+    if (M.floating && lane < NE) {  // one lane per env: the 3x3 root solve
+#pragma unroll
+        for (int e = 0; e < NE; ++e) {
+            if (e != lane) continue;
+            float* u = S[e].un;
+            const float i00 = rsqrt_ftz(u[0]);
+            const float l10 = u[1] * i00, l20 = u[2] * i00;
+            const float i11 = rsqrt_ftz(u[3] - l10 * l10);
+            const float l21 = (u[4] - l20 * l10) * i11;
+            const float i22 = rsqrt_ftz(u[5] - l20 * l20 - l21 * l21);
+            const float y0 = -u[6] * i00;
+            const float y1 = (-u[7] - l10 * y0) * i11;
+            const float y2 = (-u[8] - l20 * y0 - l21 * y1) * i22;
+            const float x2 = y2 * i22;
+            const float x1 = (y1 - l21 * x2) * i11;
+            const float x0 = (y0 - l10 * x1 - l20 * x2) * i00;
+            u[0] = x0;
+            u[1] = x1;
+            u[2] = x2;
+            const float wd = S[e].dqf[2];
+            S[e].tau[0] = fmaf(-wd, S[e].dqf[1], x1);
+            S[e].tau[1] = fmaf(wd, S[e].dqf[0], x2);
+            S[e].tau[2] = x0;
+        }
+    }
+    __syncwarp();
+    const EnvSmem& S0 = S[0];
+    for (int lev = 0; lev < M.n_levels; ++lev) {
+        const uint32_t ww = S0.twork[32 * lev + lane];
+        if (ww >> 31) {
+            const int l = ww_link(ww);
+            const int dof = link_dof(M, l);
+            const int p = ww_parent(ww);
+            if (dof >= 0) {
+#pragma unroll
+                for (int e = 0; e < NE; ++e) {
+                    float* u = S[e].un + kLinkStride * l;
+                    float2* u2 = reinterpret_cast<float2*>(u);
+                    const float2 cv = u2[6];
+                    float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
+                    if (p >= 0) {
+                        const float* up = S[e].un + kLinkStride * p;
+                        const float2 a01 = reinterpret_cast<const float2*>(up)[0];
+                        const float a2 = up[2];
+                        const float2 ol = frame_origin(S[e], l), op = frame_origin(S[e], p);
+                        const float dx = ol.x - op.x, dz = ol.y - op.y;
+                        A0 = a01.x;
+                        A1 += fmaf(-a01.x, dz, a01.y);
+                        A2 += fmaf(a01.x, dx, a2);
+                    }
+                    const float2 U = u2[5];
+                    const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
+                    u2[0] = make_float2(A0 + qdd, A1);
+                    u[2] = A2;
+                    S[e].tau[dof] = qdd;
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+template <int WPB, int NE, int NSEG, int QSL>
+__global__ void __launch_bounds__(WPB * 32, 1) stepn_kernel(DevModel M, DevState St, int env0, int n_envs,
+                                                             const float* __restrict__ actions, float* obs,
+                                                             float* delta, float* reward_aux, uint8_t* flags,
+                                                             float* power, float* grf, int n_substeps) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    static_assert(QSL >= 1 && QSL <= kMaxQSlots, "DOF slots");
+    constexpr int QS = QSL;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    load_tree_table(smem, M);
+    const int slot0 = warp * NE;
+    if (slot0 >= M.epb) return;
+    const int nq = M.nq, nm = M.nm, nl = M.nl, nrd = M.nrd;
+    EnvSmem S[NE];
+    EnvRowsN<NE> V;
+    int le[NE], ev[NE];
+    size_t mb[NE];
+    bool exists[NE];
+    float* grf_row[NE];
+    int n_live = 0;
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        const int slot = min(slot0 + k, M.epb - 1);
+        S[k] = carve(smem, slot, M, 32, 0xffffffffu);
+        le[k] = blockIdx.x * M.epb + slot0 + k;
+        exists[k] = slot0 + k < M.epb && le[k] < n_envs;
+        ev[k] = env0 + (exists[k] ? le[k] : min(le[0], n_envs - 1));  // loads of a missing env use a real row
+        mb[k] = static_cast<size_t>(ev[k]) * nm;
+        bool act = exists[k];
+        if (act && St.done[ev[k]]) {  // contract checks of Env::step (env.cpp:207-210)
+            if (lane == 0 && flags) flags[le[k]] = kFlagNotStepped;
+            act = false;
+        }
+        if (act && St.u_bad[ev[k]]) {
+            if (lane == 0 && flags) flags[le[k]] = kFlagBadAction;
+            act = false;
+        }
+        V.live[k] = act;
+        n_live += act;
+        V.R[k] = muscle_rows(St, St.u + mb[k], mb[k]);
+        V.pw[k] = power ? power + static_cast<size_t>(exists[k] ? le[k] : 0) * nm
+                        : (M.reward_mode == 2 ? St.power_scratch + mb[k] : nullptr);
+        grf_row[k] = (grf && exists[k]) ? grf + static_cast<size_t>(le[k]) * 2 * nl : nullptr;
+    }
+    if (n_live == 0) return;
+    bool stepped[NE];
+    double qd[NE][QS], dqd[NE][QS];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+        stepped[k] = V.live[k];
+        if (!V.live[k]) {  // not stepped: its caller rows stay untouched
+            V.pw[k] = nullptr;
+            grf_row[k] = nullptr;
+        }
+        load_dofs<QS>(M, S[k], St.q + static_cast<size_t>(ev[k]) * nq, St.dq + static_cast<size_t>(ev[k]) * nq, qd[k],
+                      dqd[k], lane);
+        publish_dofs<QS>(M, S[k], qd[k], dqd[k], lane);
+        if (V.live[k] && V.pw[k])
+            for (int m = lane; m < nm; m += 32) V.pw[k][m] = 0.0f;
+        if (grf_row[k])
+            for (int i = lane; i < 2 * nl; i += 32) grf_row[k][i] = 0.0f;
+    }
+    __syncwarp();
+
+    int diverged_at[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) diverged_at[k] = -1;
+    for (int sub = 0; sub < n_substeps; ++sub) {
+        if (M.has_general)
+#pragma unroll
+            for (int k = 0; k < NE; ++k) fk_d(M, S[k], lane);
+
+        // ---- 1. muscles + J_m^T F contributions ----
+        muscle_phase_n<NSEG, NE>(M, St, S, V, mb, lane, sub == n_substeps - 1);
+        __syncwarp();
+
+        // ---- 2. joint torques: fixed-order slot sums, damping, limits ----
+#pragma unroll
+        for (int kq = 0; kq < QS; ++kq) {
+            const int d = lane + 32 * kq;
+            if (d >= nrd && d < nq) {
+                const int j = d - nrd;
+                const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
+                const float damp = __ldg(M.joint_damping + j);
+                const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
+#pragma unroll
+                for (int k = 0; k < NE; ++k) {
+                    const float* un = S[k].un;
+                    float t = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
+                    int s = s0;
+                    for (; s + 3 < s1; s += 4) {
+                        t += un[s];
+                        t1 += un[s + 1];
+                        t2 += un[s + 2];
+                        t3 += un[s + 3];
+                    }
+                    for (; s < s1; ++s) t += un[s];
+                    t = (t + t1) + (t2 + t3);
+                    t -= damp * static_cast<float>(dqd[k][kq]);
+                    if (qd[k][kq] > hi)
+                        t -= static_cast<float>(M.k_lim_d * (qd[k][kq] - hi));
+                    else if (qd[k][kq] < lo)
+                        t -= static_cast<float>(M.k_lim_d * (qd[k][kq] - lo));
+                    S[k].tau[d] = t;
+                }
+            }
+        }
+        __syncwarp();
+
+        // ---- 3. FK + velocities + per-link articulated-body terms ----
+        if (M.ns)
+#pragma unroll
+            for (int k = 0; k < NE; ++k) sphere_pen_d(M, S[k], lane);
+        tree_sweep_n<NE>(M, S, lane, grf_row);
+        // ---- 4. articulated-body passes ----
+        aba_up_n<NE>(M, S, lane);
+        aba_down_n<NE>(M, S, lane);
+
+        // ---- 5. semi-implicit Euler (f64) + divergence check ----
+        bool bad[NE];
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            bad[k] = false;
+            if (!V.live[k]) continue;
+#pragma unroll
+            for (int kq = 0; kq < QS; ++kq) {
+                const int d = lane + 32 * kq;
+                if (d < nq) {
+                    dqd[k][kq] += static_cast<double>(S[k].tau[d]) * kSimDt;
+                    qd[k][kq] += dqd[k][kq] * kSimDt;
+                    bad[k] |= !isfinite(qd[k][kq]) || !isfinite(dqd[k][kq]);
+                }
+            }
+        }
+        __syncwarp();
+        int alive = 0;
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+            if (V.live[k]) publish_dofs<QS>(M, S[k], qd[k], dqd[k], lane);
+            if (V.live[k] && __any_sync(0xffffffffu, bad[k])) {
+                diverged_at[k] = sub;
+                V.live[k] = false;  // frozen at the diverging substep (msk::step throws there)
+            }
+            alive += V.live[k];
+        }
+        __syncwarp();
+        if (alive == 0) break;
+    }
+
+#pragma unroll
+    for (int k = 0; k < NE; ++k)
+        if (stepped[k])
+            step_epilogue<QS>(M, St, S[k], ev[k], le[k], qd[k], dqd[k], diverged_at[k], n_substeps, obs, delta,
+                              reward_aux, flags, power, grf_row[k], V.pw[k], lane);
 }
 
 // ============================================================================
@@ -1614,8 +2113,26 @@ int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 &
 // DOF register slots per lane: 3 covers n_q <= 96 (the whole-body models), else 4.
 int step_qslots(const DevModel& M) { return M.nq <= 96 ? 3 : kMaxQSlots; }
 
+// Envs per thread of the step kernel (MSK_NE: 1 = step_kernel, the default; 2 or 4 =
+// stepn_kernel, opt-in: 15 % fewer instructions at NE = 2 but half the warps per SM,
+// and the 128-register cap of 4 warps per SM partition leaves no room for the ILP
+// that would hide the per-env dependency chains — measured 0.628 / 0.870 ms vs 0.551 ms).
+int step_ne() {
+    static const int ne = [] {
+        const char* v = std::getenv("MSK_NE");
+        const int x = v ? std::atoi(v) : 1;
+        return (x == 1 || x == 2 || x == 4) ? x : 1;
+    }();
+    return kEPW == 1 ? ne : 1;
+}
+
 template <int NSEG, int QSL>
 cudaError_t set_step_smem(int bytes) {
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(stepn_kernel<14, 2, NSEG, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute(stepn_kernel<7, 4, NSEG, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
     return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG, kEPW, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 bytes);
 }
@@ -1642,6 +2159,7 @@ cudaError_t prepare_kernels(int smem_bytes_per_block) {
 }
 
 int envs_per_block() { return kEnvsPerBlock; }
+int step_envs_per_warp() { return step_ne(); }
 int lanes_per_env() { return 32 / kEPW; }
 
 void launch_step(const DevModel& M, const DevState& St, int env0, int n, const float* actions, float* obs,
@@ -1649,9 +2167,19 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
                  int n_substeps) {
     const int blocks = (n + M.epb - 1) / M.epb;
     const size_t smem = block_smem(M);
-#define MSK_STEP(NS, QSL)                                                                                  \
-    step_kernel<kWPB, kMinB, NS, kEPW, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, \
-                                                                            raux, flags, power, grf, n_substeps)
+    const int ne = step_ne();
+#define MSK_STEP(NS, QSL)                                                                                          \
+    do {                                                                                                           \
+        if (ne == 2)                                                                                               \
+            stepn_kernel<14, 2, NS, QSL><<<blocks, 14 * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux,  \
+                                                                         flags, power, grf, n_substeps);           \
+        else if (ne == 4)                                                                                          \
+            stepn_kernel<7, 4, NS, QSL><<<blocks, 7 * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux,    \
+                                                                       flags, power, grf, n_substeps);             \
+        else                                                                                                       \
+            step_kernel<kWPB, kMinB, NS, kEPW, QSL><<<blocks, kWPB * 32, smem, s>>>(                               \
+                M, St, env0, n, actions, obs, delta, raux, flags, power, grf, n_substeps);                         \
+    } while (0)
     prep_actions_kernel<<<(n + 7) / 8, 256, 0, s>>>(M, St, env0, n, actions);
     const int v = step_variant(M);
     if (step_qslots(M) == 3 && (v == 0 || v == 2 || v == 3)) {  // whole-body sized models

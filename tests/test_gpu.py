@@ -1209,3 +1209,20 @@ def test_create_accepts_models_the_reference_steps(assets, tmp_path):
     with pytest.raises(pk.MskError, match="parent must precede child"):
         pk.EnvBatch(str(p), cp, 1)
     torch.cuda.synchronize()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ne", [2, 4])
+def test_env_vectorised_step_kernel_parity(ne):
+    """The opt-in env-vectorised step kernel (MSK_NE = 2 / 4: each thread advances
+    NE envs) runs the same per-env arithmetic: smoke()'s oracle checks in a fresh
+    process (MSK_NE is read once per process).  The whole of this file also passes
+    under MSK_NE=2 and MSK_NE=4 (ragged batch sizes included; profiles/r02)."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=root,
+                       env={**os.environ, "MSK_NE": str(ne)}, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "smoke wb700" in r.stdout

@@ -22,6 +22,6 @@ for f in "$tmp"/*.cu; do
   objs+=("${f%.cu}.o")
 done
 g++ -std=c++17 -O2 -fPIC -I$JSON_INC -c "$tmp/model.cpp" -o "$tmp/model_cpp.o"
-nvcc $ARCH -shared -o variants/$name.so "${objs[@]}" "$tmp/model_cpp.o" -lcudart -lcublas
+nvcc $ARCH -shared -o variants/$name.so "${objs[@]}" "$tmp/model_cpp.o" -lcudart -ldl
 rm -rf "$tmp"
 echo "built variants/$name.so"
