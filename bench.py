@@ -567,8 +567,10 @@ def main():
         torch.cuda.synchronize()
         dms = e0.elapsed_time(e1) / reps
         flops = 2.0 * (env.delta_dim * width + 2 * width * width + width) * E
-        disc = {"kernel": "disc_reward_kernel (tcgen05 kind::f16, bf16 operands, fp32 TMEM accumulate)",
-                "width": width, "ms": dms, "flops_per_launch": flops}
+        disc = {"kernel": "disc_reward_precise_kernel (tcgen05 kind::f16, split-bf16 operands hi+lo, 3 MMAs per "
+                          "product, fp32 TMEM accumulate: fp32-class, the default mode)",
+                "width": width, "ms": dms, "flops_per_launch": flops,
+                "note": "flops counted once per product (the algorithmic count); the tensor cores execute 3x"}
 
     if rank == 0:
         cm = cost_model(mp)

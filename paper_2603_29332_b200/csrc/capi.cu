@@ -1,5 +1,6 @@
 // C ABI (include/msk_gpu.h): context ownership, device tables, launches.
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
@@ -19,6 +20,12 @@
 #include "model.hpp"
 
 namespace msk_b200 {
+
+// NVTX range over a C-ABI call (header-only NVTX v3: a no-op unless a profiler is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 cudaError_t prepare_kernels(int smem_bytes_per_block);
 int envs_per_block();
 int lanes_per_env();
@@ -541,6 +548,7 @@ int msk_gpu_set_eval_mode(msk_gpu_ctx* ctx, int32_t eval_mode) {
 
 int msk_gpu_reset(msk_gpu_ctx* ctx, const uint8_t* mask, uint8_t mask_bits, float* obs, int32_t* start_frames,
                   void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_reset");
     return guarded(ctx, [&] {
         launch_reset(ctx->M, ctx->St, ctx->n_envs, 0, mask, mask ? mask_bits : 0, nullptr, obs, start_frames, nullptr,
                      as_stream(stream));
@@ -561,6 +569,7 @@ int msk_gpu_reset_to_frame(msk_gpu_ctx* ctx, const int32_t* frames, const uint8_
 
 int msk_gpu_step(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward_aux, uint8_t* flags,
                  float* muscle_power, float* contact_force, void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_step");
     return guarded(ctx, [&] {
         if (!actions) throw ConfigError("step: actions is null");
         launch_step(ctx->M, ctx->St, 0, ctx->n_envs, actions, obs, delta, reward_aux, flags, muscle_power,
@@ -681,6 +690,7 @@ int msk_disc_trainer_publish(msk_disc_trainer* trainer, msk_gpu_ctx* ctx, void* 
 }
 
 int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n, float* reward, void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_discriminator_reward");
     return guarded(ctx, [&] {
         if (!ctx->disc.w1) throw ConfigError("discriminator_reward: no discriminator set");
         if (!delta || !reward || n < 0) throw ConfigError("discriminator_reward: bad arguments");
@@ -693,6 +703,7 @@ int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n
 int msk_gpu_step_rewarded(msk_gpu_ctx* ctx, const float* actions, float* obs, float* delta, float* reward,
                           float* reward_aux, uint8_t* flags, float* muscle_power, float* contact_force,
                           void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_step_rewarded");
     return guarded(ctx, [&] {
         if (!actions || !reward) throw ConfigError("step_rewarded: actions and reward are required");
         if (!ctx->disc.w1) throw ConfigError("step_rewarded: no discriminator set");
@@ -778,6 +789,7 @@ void step_host_impl(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host
 
 int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                       float* reward_aux_host, uint8_t* flags_host) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_step_host");
     return guarded(ctx, [&] {
         step_host_impl(ctx, actions_host, obs_host, delta_host, nullptr, reward_aux_host, flags_host, true);
     });
@@ -785,6 +797,7 @@ int msk_gpu_step_host(msk_gpu_ctx* ctx, const float* actions_host, float* obs_ho
 
 int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                                float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_step_host_rewarded");
     return guarded(ctx, [&] {
         if (!reward_host) throw ConfigError("step_host_rewarded: reward is null");
         step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host, true);
@@ -793,6 +806,7 @@ int msk_gpu_step_host_rewarded(msk_gpu_ctx* ctx, const float* actions_host, floa
 
 int msk_gpu_step_host_async(msk_gpu_ctx* ctx, const float* actions_host, float* obs_host, float* delta_host,
                             float* reward_host, float* reward_aux_host, uint8_t* flags_host) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_step_host_async");
     return guarded(ctx, [&] {
         step_host_impl(ctx, actions_host, obs_host, delta_host, reward_host, reward_aux_host, flags_host, false);
     });
@@ -824,6 +838,7 @@ int msk_gpu_host_wait(msk_gpu_ctx* ctx) {
 }
 
 int msk_gpu_observe(msk_gpu_ctx* ctx, float* obs, void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_observe");
     return guarded(ctx, [&] {
         launch_observe(ctx->M, ctx->St, ctx->n_envs, obs, nullptr, as_stream(stream));
         ctx->count();
@@ -933,6 +948,7 @@ int msk_gpu_set_sampler(msk_gpu_ctx* ctx, const double* ema, int32_t broadcast, 
 
 int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int32_t* counts, int32_t cap,
                            void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_drain_outcomes");
     return guarded(ctx, [&] {
         if (!bins || !failed || !counts || cap < 0) throw ConfigError("drain_outcomes: bad arguments");
         grow_outcome_ring(ctx, cap, as_stream(stream));  // sized for the caller's next drain
@@ -944,6 +960,7 @@ int msk_gpu_drain_outcomes(msk_gpu_ctx* ctx, int32_t* bins, uint8_t* failed, int
 
 int msk_gpu_rollout_stats(msk_gpu_ctx* ctx, const float* reward, const uint8_t* flags, double* stats,
                           void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_rollout_stats");
     return guarded(ctx, [&] {
         if (!flags || !stats) throw ConfigError("rollout_stats: flags and stats are required");
         launch_rollout_stats(ctx->St, ctx->n_envs, reward, flags, stats, as_stream(stream));
@@ -953,6 +970,7 @@ int msk_gpu_rollout_stats(msk_gpu_ctx* ctx, const float* reward, const uint8_t* 
 }
 
 int msk_gpu_obs_moments(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_obs_moments");
     return guarded(ctx, [&] {
         if (!obs || !out || n < 0) throw ConfigError("obs_moments: bad arguments");
         const size_t need = static_cast<size_t>(obs_moments_chunks(n)) * ctx->obs_dim * 2;
@@ -1020,6 +1038,7 @@ extern "C" {
 
 int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, const float* obs,
                                const double* stats_in, double* norm_state, double* stats_out, void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_iteration_exchange");
     return guarded(ctx, [&] {
         if (cap < 1 || !obs || !stats_in || !norm_state) throw ConfigError("iteration_exchange: bad arguments");
         cudaStream_t s = as_stream(stream);

@@ -44,6 +44,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1295,6 +1296,10 @@ int msk_disc_trainer_gradient(msk_disc_trainer* t, const float* delta, int32_t r
 
 int msk_disc_train_step(msk_disc_trainer* t, const float* delta, int32_t rows, int32_t ld, double* loss,
                         void* stream) {
+    nvtxRangePushA("msk_disc_train_step");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop_;
     if (!t) return dtfail(nullptr, "null disc trainer");
     try {
         check_rows(t, delta, rows, ld);
