@@ -143,8 +143,10 @@ int msk_gpu_discriminator_reward(msk_gpu_ctx* ctx, const float* delta, int32_t n
  * the gradient from Mlp::backward (nn.cpp:80-129) and
  * Mlp::gradient_penalty_backward (nn.cpp:131-222).  The learner's absent
  * train_discriminator (learn.cpp) is the interface replaced.  Master θ
- * (nn.cpp:16-38 layout) and Adam moments live on the device in f64; GEMMs in
- * cuBLAS with math 0 = FP32, 1 = TF32 tensor cores.  delta: [rows x ld] f32 device rows (the
+ * (nn.cpp:16-38 layout) and Adam moments live on the device in f64; every GEMM
+ * is the library's own tcgen05 kernel: math 0 = fp32-class (split-bf16 operands,
+ * 3 MMAs per product), 1 = bf16 operands.  n_in, hidden <= 256.
+ * delta: [rows x ld] f32 device rows (the
  * rollout's Δ), rows <= max_rows.  loss (device, nullable): {total, logistic,
  * mean penalty} at the pre-step parameters. */
 typedef struct msk_disc_trainer msk_disc_trainer;
