@@ -9,6 +9,8 @@
 //   warps 2-5 epilogue: tcgen05.ld of their TMEM lane quarter, bias (+ addend),
 //            tanh -> bf16 tiled (next layer's A), fp32 affine head, or the flow
 //            ODE update a += dt * ψ.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -134,6 +136,8 @@ __device__ __forceinline__ void store_tiled16(void* img, int KB, int m, int n0, 
 // layers with an addend, the affine head) or the running value they update
 // (kEpiTanhAcc's sum, kEpiOde's action).  It is loaded 32 columns ahead into
 // registers, so its (L2) latency overlaps the MMA tail and the TMEM loads.
+// Row-major sources are addressed by row pointer; F4 sources (g.f4_rows > 0) by
+// (base, m).
 template <int EPI>
 __device__ __forceinline__ const float* epi_src(const GemmArgs& g, int m, int& ld) {
     if (m >= g.M) return nullptr;
@@ -150,7 +154,22 @@ __device__ __forceinline__ int epi_limit(const GemmArgs& g) {
 }
 
 // 32 source values of row m at columns [n0, n0 + 32) (0 outside the valid range).
-__device__ __forceinline__ void load_src32(const float* row, int n0, int limit, bool vec, float (&x)[32]) {
+// f4 > 0: base is an F4 buffer (see GemmArgs::f4_rows), row is unused.
+__device__ __forceinline__ void load_src32(const float* row, const float* base, int f4, int m, int n0, int limit,
+                                           bool vec, float (&x)[32]) {
+    if (f4 > 0 && base) {
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+            float4 t = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            if (n0 + i < limit)
+                t = *reinterpret_cast<const float4*>(base + (static_cast<size_t>((n0 + i) >> 2) * f4 + m) * 4);
+            x[i] = t.x;
+            x[i + 1] = t.y;
+            x[i + 2] = t.z;
+            x[i + 3] = t.w;
+        }
+        return;
+    }
     if (!row) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) x[i] = 0.0f;
@@ -171,7 +190,18 @@ __device__ __forceinline__ void load_src32(const float* row, int n0, int limit, 
     }
 }
 
-__device__ __forceinline__ void store_f16cols(float* op, int n0, int limit, bool vec, const float* v) {
+// 16 columns [n0, n0 + 16) of row m into an f32 output: row-major (op = row
+// pointer) or F4 (base, m).
+__device__ __forceinline__ void store_f16cols(float* op, float* base, int f4, int m, int n0, int limit, bool vec,
+                                              const float* v) {
+    if (f4 > 0) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+            if (n0 + i < limit)
+                *reinterpret_cast<float4*>(base + (static_cast<size_t>((n0 + i) >> 2) * f4 + m) * 4) =
+                    make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        return;
+    }
     if (vec && n0 + 16 <= limit) {
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
@@ -190,7 +220,8 @@ template <int EPI>
 __device__ __forceinline__ void epi16(const GemmArgs& g, int m, int n0, int n_out_pad, const float* sb,
                                       const float* src, float (&v)[16]) {
     constexpr bool kTanh = EPI == kEpiTanhTiled || EPI == kEpiTanhPre || EPI == kEpiTanhAcc;
-    float* orow = (m < g.M && g.out_f) ? g.out_f + static_cast<size_t>(m) * g.ld_f : nullptr;
+    const int f4 = g.f4_rows;
+    float* orow = (m < g.M && g.out_f) ? (f4 > 0 ? g.out_f : g.out_f + static_cast<size_t>(m) * g.ld_f) : nullptr;
     const bool vec = (g.ld_f & 3) == 0;
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = EPI == kEpiTanhPre ? fmaf(g.scale, v[i], sb[i]) : v[i] + sb[i];
@@ -199,27 +230,27 @@ __device__ __forceinline__ void epi16(const GemmArgs& g, int m, int n0, int n_ou
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] += src[i];
         }
-        if (EPI == kEpiTanhPre && orow) store_f16cols(orow, n0, g.N, vec, v);  // f32 pre-activation
+        if (EPI == kEpiTanhPre && orow) store_f16cols(orow, g.out_f, f4, m, n0, g.N, vec, v);  // f32 pre-activation
 #pragma unroll
         for (int i = 0; i < 16; ++i) v[i] = n0 + i < g.N ? tanh_a(v[i]) : 0.0f;
         if (EPI == kEpiTanhAcc && orow) {  // running f32 sum of the activations
             float y[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) y[i] = src[i] + v[i];
-            store_f16cols(orow, n0, g.N, vec, y);
+            store_f16cols(orow, g.out_f, f4, m, n0, g.N, vec, y);
         }
         store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, v);
     } else if (EPI == kEpiF32) {
         if (orow) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = fmaf(g.scale, v[i], g.offset) + src[i];
-            store_f16cols(orow, n0, g.n_valid, vec, v);
+            store_f16cols(orow, g.out_f, f4, m, n0, g.n_valid, vec, v);
         }
     } else {  // kEpiOde: a += dt * psi
         float y[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) y[i] = (orow && n0 + i < g.n_valid) ? fmaf(g.dt, v[i], src[i]) : 0.0f;
-        if (orow) store_f16cols(orow, n0, g.n_valid, vec, y);
+        if (orow) store_f16cols(orow, g.out_f, f4, m, n0, g.n_valid, vec, y);
         if (g.out_a) store_tiled16(g.out_a, n_out_pad / kGemmBK, m, n0, y);
     }
 }
@@ -239,11 +270,12 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
     const int c_lo = ((warp - 2) / 4) * (kGemmBN / 2), c_hi = c_lo + kGemmBN / 2;
     int lds = 0;
     const float* sp = epi_src<EPI>(g, m, lds);
-    const float* srow = sp ? sp + static_cast<size_t>(m) * lds : nullptr;
+    const int f4 = g.f4_rows;
+    const float* srow = (sp && f4 <= 0) ? sp + static_cast<size_t>(m) * lds : nullptr;
     const int limit = epi_limit<EPI>(g);
     const bool svec = (lds & 3) == 0;
     float cur[32], nxt[32];
-    load_src32(srow, nb * kGemmBN + c_lo, limit, svec, cur);  // overlaps the MMA tail
+    load_src32(srow, sp, f4, m, nb * kGemmBN + c_lo, limit, svec, cur);  // overlaps the MMA tail
     asm volatile("bar.sync 1, %0;" ::"n"(kEpiWarps * 32) : "memory");  // epilogue warps only
     bar_wait(acc_full, 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -253,7 +285,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
     for (int c = c_lo; c < c_hi; c += 32) {
         const int n0 = nb * kGemmBN + c;
         if (n0 >= n_end) break;  // columns past the valid / padded output width
-        if (c + 32 < c_hi) load_src32(srow, n0 + 32, limit, svec, nxt);
+        if (c + 32 < c_hi) load_src32(srow, sp, f4, m, n0 + 32, limit, svec, nxt);
         float v[2][16];
         ld32(trow + c, v);
         epi16<EPI>(g, m, n0, n_out_pad, sbias + c, cur, v[0]);
@@ -363,12 +395,15 @@ if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 2
 // 256 x 256 tile with one M = 256 UMMA per K-step issued by the leader (rank 0).
 // Each CTA stages its own 128 rows of A and its own 128-row half of the weight
 // block (16 + 16 KB per K-block instead of 16 + 32 KB), so the bytes each SM
-// ingests per flop drop by 1.5x.  The peer's TMA completion is relayed to the
-// leader's stage barrier by a remote mbarrier arrive; the leader's MMA commits
-// are multicast to both CTAs (stage release, accumulator ready); each CTA's
-// TMEM holds its own 128 accumulator rows, so the epilogue is unchanged.
+// ingests per flop drop by 1.5x.  Both CTAs' copies are 2-D TMA tensor loads
+// with .cta_group::2 whose completion is counted on the LEADER's stage barrier
+// (the barrier address with the peer bit cleared); the leader's producer
+// expects the pair's bytes.  The leader's MMA commits are multicast to both
+// CTAs (stage release, accumulator ready); each CTA's TMEM holds its own 128
+// accumulator rows, so the epilogue is unchanged.
 constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(kGemmBN >> 3) << 17) |
                              (static_cast<uint32_t>((2 * kGemmBM) >> 4) << 24);
+constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;
 
 __device__ __forceinline__ void bar_wait_cluster(uint64_t* b, uint32_t parity) {
     asm volatile(
@@ -379,9 +414,19 @@ __device__ __forceinline__ void bar_wait_cluster(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// 16 KB chunk (row coordinate y of a [rows x 2 KB] view of a tiled image) into
+// this CTA's smem, completing on the pair leader's barrier.
+__device__ __forceinline__ void tma_pair(void* dst, const CUtensorMap* map, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(y), "r"(su32(bar) & kPeerBitMask)
+        : "memory");
+}
 
 template <int EPI>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm2_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapW, GemmArgs g) {
     extern __shared__ __align__(1024) unsigned char smem[];
     constexpr int kWHalf = kWBytes / 2;                           // 128 weight rows x 64 K
     unsigned char* sA = smem;                                     // kStages x 16 KB
@@ -398,8 +443,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm2_kernel(GemmArgs g) {
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            bar_init(&full[s], rank == 0 ? 2 : 1);  // leader: own TMA + the peer's relay
-            bar_init(&empty[s], 1);                 // the leader's (multicast) MMA commit
+            bar_init(&full[s], 1);   // leader: its producer's expect_tx arrival (+ both CTAs' bytes)
+            bar_init(&empty[s], 1);  // the leader's (multicast) MMA commit
         }
         bar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -417,52 +462,42 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm2_kernel(GemmArgs g) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp == 0 && lane == 0) {  // TMA producer (both CTAs)
-        const char* A = static_cast<const char*>(g.A) + static_cast<size_t>(mb) * KB * kABytes;
-        const char* W = static_cast<const char*>(g.W) + static_cast<size_t>(nb) * KB * kWBytes + rank * kWHalf;
+        const int ya = mb * KB * (kABytes / 2048);
+        const int yw = nb * KB * (kWBytes / 2048) + static_cast<int>(rank) * (kWHalf / 2048);
         for (int kb = 0; kb < KB; ++kb) {
             const int s = kb % kStages;
             if (kb >= kStages) bar_wait(&empty[s], ((kb / kStages) - 1) & 1);
-            bar_expect(&full[s], kABytes + kWHalf);
-            bulk(sA + s * kABytes, A + static_cast<size_t>(kb) * kABytes, kABytes, &full[s]);
-            bulk(sW + s * kWHalf, W + static_cast<size_t>(kb) * kWBytes, kWHalf, &full[s]);
+            if (rank == 0) bar_expect(&full[s], 2 * (kABytes + kWHalf));
+            tma_pair(sA + s * kABytes, &mapA, ya + kb * (kABytes / 2048), &full[s]);
+            tma_pair(sW + s * kWHalf, &mapW, yw + kb * (kWBytes / 2048), &full[s]);
         }
-    } else if (warp == 1 && lane == 0) {
-        if (rank == 0) {  // MMA issuer for the pair
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % kStages;
-                bar_wait_cluster(&full[s], (kb / kStages) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a0 = su32(sA + s * kABytes), w0 = su32(sW + s * kWHalf);
+    } else if (warp == 1 && lane == 0 && rank == 0) {  // MMA issuer for the pair
+        for (int kb = 0; kb < KB; ++kb) {
+            const int s = kb % kStages;
+            bar_wait_cluster(&full[s], (kb / kStages) & 1);  // both CTAs' bytes landed
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t a0 = su32(sA + s * kABytes), w0 = su32(sW + s * kWHalf);
 #pragma unroll
-                for (int k = 0; k < kGemmBK / 16; ++k) {
-                    const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
-                    asm volatile(
-                        "{\n\t.reg .pred p;\n\t"
-                        "setp.ne.b32 p, %4, 0;\n\t"
-                        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                        "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc2), "r"(acc)
-                        : "memory");
-                }
+            for (int k = 0; k < kGemmBK / 16; ++k) {
+                const uint32_t acc = (kb > 0 || k > 0) ? 1u : 0u;
                 asm volatile(
-                    "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
-                    "%1;" ::"r"(su32(&empty[s])),
-                    "h"(static_cast<uint16_t>(3))
+                    "{\n\t.reg .pred p;\n\t"
+                    "setp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                    "l"(sdesc(a0 + 256 * k)), "l"(sdesc(w0 + 256 * k)), "r"(kIdesc2), "r"(acc)
                     : "memory");
             }
             asm volatile(
-                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-                    su32(acc_full)),
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                "%1;" ::"r"(su32(&empty[s])),
                 "h"(static_cast<uint16_t>(3))
                 : "memory");
-        } else {  // relay: this CTA's stage landed -> arrive on the leader's stage barrier
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % kStages;
-                bar_wait(&full[s], (kb / kStages) & 1);
-                uint32_t remote;
-                asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(su32(&full[s])));
-                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-            }
         }
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                su32(acc_full)),
+            "h"(static_cast<uint16_t>(3))
+            : "memory");
     } else if (warp >= 2) {
         gemm_epilogue<EPI>(g, tmem, sbias, acc_full, mb, nb, warp, lane);
     }
@@ -472,8 +507,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm2_kernel(GemmArgs g) {
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
+// 2-D tensor map over a tiled image viewed as [bytes / 2 KB] rows of 256 u64:
+// one 16 KB box = 8 rows (a 128-row A block or a 128-row weight half-block).
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+bool tile_map(const void* base, size_t bytes, CUtensorMap* m) {
+    if (!g_encode) {
+        cudaDriverEntryPointQueryResult q;
+        void* fn = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn ||
+            q != cudaDriverEntryPointSuccess)
+            return false;
+        g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {256, static_cast<cuuint64_t>(bytes / 2048)};
+    const cuuint64_t strides[1] = {2048};
+    const cuuint32_t box[2] = {256, 8}, estr[2] = {1, 1};
+    return g_encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 __global__ void obs_to_tiled_kernel(const float* obs, int M, int D, int ld, const float* mean, const float* inv_sd,
-                                    void* out) {
+                                    void* out, int f4) {
     // one thread per (row, 8-column chunk) of the padded [Mpad x Kpad] image
     const int Kp = pad_to(D, kGemmBK), chunks = Kp / 8;
     const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
@@ -486,7 +541,7 @@ __global__ void obs_to_tiled_kernel(const float* obs, int M, int D, int ld, cons
         const int k = k0 + i;
         float x = 0.0f;
         if (m < M && k < D) {
-            x = obs[static_cast<size_t>(m) * ld + k];
+            x = f4 > 0 ? obs[(static_cast<size_t>(k >> 2) * f4 + m) * 4 + (k & 3)] : obs[static_cast<size_t>(m) * ld + k];
             if (mean) x = (x - mean[k]) * inv_sd[k];
         }
         y[i] = x;
@@ -524,8 +579,8 @@ cudaError_t prepare_epi(int bytes) {
     return cudaFuncSetAttribute(gemm_kernel<EPI, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 template <int EPI>
-cudaError_t launch_epi(cudaLaunchConfig_t& cfg, int cl, const GemmArgs& g) {
-    if (cl == -2) return cudaLaunchKernelEx(&cfg, gemm2_kernel<EPI>, g);
+cudaError_t launch_epi(cudaLaunchConfig_t& cfg, int cl, const GemmArgs& g, const CUtensorMap* maps) {
+    if (cl == -2) return cudaLaunchKernelEx(&cfg, gemm2_kernel<EPI>, maps[0], maps[1], g);
     switch (cl) {
         case 4: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 4>, g);
         case 2: return cudaLaunchKernelEx(&cfg, gemm_kernel<EPI, 2>, g);
@@ -560,9 +615,14 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = gemm_smem_bytes();
     cfg.stream = s;
-    // MSK_GEMM_2CTA: CTA-pair UMMA (needs an even number of 128-row tiles)
+    // MSK_GEMM_2CTA: CTA pairs (cta_group::2, needs an even number of row tiles).  Opt-in:
+    // measured 14.2 vs 13.4 us per K = 1024 layer at 4096 rows — halving the bytes each SM
+    // ingests does not pay, the layer is bound by fill / epilogue, not operand ingest.
     static const bool pair = std::getenv("MSK_GEMM_2CTA") != nullptr;
-    const bool use2 = pair && cfg.gridDim.x % 2 == 0;
+    CUtensorMap maps[2];
+    bool use2 = pair && cfg.gridDim.x % 2 == 0;
+    if (use2)
+        use2 = tile_map(g.A, tiled_a_bytes(g.M, g.K), &maps[0]) && tile_map(g.W, tiled_w_bytes(g.N, g.K), &maps[1]);
     const int cl = use2 ? 2 : gemm_cluster(static_cast<int>(cfg.gridDim.x));
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -575,24 +635,25 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s) {
     cfg.numAttrs = 2;
     const int sel = use2 ? -2 : cl;
     switch (epi) {
-        case kEpiTanhTiled: return launch_epi<kEpiTanhTiled>(cfg, sel, g);
-        case kEpiF32: return launch_epi<kEpiF32>(cfg, sel, g);
-        case kEpiTanhPre: return launch_epi<kEpiTanhPre>(cfg, sel, g);
-        case kEpiTanhAcc: return launch_epi<kEpiTanhAcc>(cfg, sel, g);
-        default: return launch_epi<kEpiOde>(cfg, sel, g);
+        case kEpiTanhTiled: return launch_epi<kEpiTanhTiled>(cfg, sel, g, maps);
+        case kEpiF32: return launch_epi<kEpiF32>(cfg, sel, g, maps);
+        case kEpiTanhPre: return launch_epi<kEpiTanhPre>(cfg, sel, g, maps);
+        case kEpiTanhAcc: return launch_epi<kEpiTanhAcc>(cfg, sel, g, maps);
+        default: return launch_epi<kEpiOde>(cfg, sel, g, maps);
     }
 }
 
 cudaError_t launch_obs_to_tiled(const float* obs, int M, int D, const float* mean, const float* inv_sd, void* out,
                                 cudaStream_t s) {
     const long long n = static_cast<long long>(pad_to(M, kGemmBM)) * (pad_to(D, kGemmBK) / 8);
-    obs_to_tiled_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(obs, M, D, D, mean, inv_sd, out);
+    obs_to_tiled_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(obs, M, D, D, mean, inv_sd, out, 0);
     return cudaGetLastError();
 }
 
-cudaError_t launch_f32_to_tiled(const float* x, int M, int D, int ld, void* out, cudaStream_t s) {
+cudaError_t launch_f32_to_tiled(const float* x, int M, int D, int ld, void* out, cudaStream_t s, int f4_rows) {
     const long long n = static_cast<long long>(pad_to(M, kGemmBM)) * (pad_to(D, kGemmBK) / 8);
-    obs_to_tiled_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, M, D, ld, nullptr, nullptr, out);
+    obs_to_tiled_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(x, M, D, ld, nullptr, nullptr, out,
+                                                                               f4_rows);
     return cudaGetLastError();
 }
 

@@ -48,6 +48,10 @@ struct GemmArgs {
     int n_valid = 0;               // columns of out_f that are written
     float dt = 0.0f;
     float scale = 1.0f, offset = 0.0f;  // kEpiF32: affine head y = scale * z + offset
+    // > 0: out_f and addend are internal f32 buffers in the F4 layout [N/4][f4_rows][4]
+    // (element (m, n) at ((n / 4) * f4_rows + m) * 4 + n % 4): a warp's 32 rows x one
+    // float4 are 512 contiguous bytes in the row-per-thread epilogue.  0: row-major.
+    int f4_rows = 0;
 };
 
 cudaError_t prepare_gemm();
@@ -57,7 +61,7 @@ cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s);
 // obs f32 [M x D] -> normalised (RunningNorm::apply) bf16 tiled A [M x D]
 cudaError_t launch_obs_to_tiled(const float* obs, int M, int D, const float* mean, const float* inv_sd, void* out,
                                 cudaStream_t s);
-// f32 row-major [M x D] -> bf16 tiled
-cudaError_t launch_f32_to_tiled(const float* x, int M, int D, int ld, void* out, cudaStream_t s);
+// f32 row-major [M x D] -> bf16 tiled (f4_rows > 0: x in the F4 layout of GemmArgs)
+cudaError_t launch_f32_to_tiled(const float* x, int M, int D, int ld, void* out, cudaStream_t s, int f4_rows = 0);
 
 }  // namespace msk_b200

@@ -235,13 +235,16 @@ void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_
                                                                   p->d_step, env_offset, a0_out, logprob, p->a_t);
     ckp(cudaGetLastError(), "a0");
     // ψ: P = W1_s · s once, then N_ODE Euler steps in the z-recurrence form
+    // internal f32 buffers (P, z1, hsum) in the F4 layout (coalesced row-per-thread epilogues)
+    const int f4 = (H % 4 == 0) ? pad_to(n, kGemmBM) : 0;
     GemmArgs pg;
     pg.M = n; pg.A = p->s_t; pg.W = p->qw1s; pg.N = H; pg.K = D; pg.out_f = p->P; pg.ld_f = H; pg.n_valid = H;
+    pg.f4_rows = f4;
     ckp(launch_gemm(pg, kEpiF32, s), "psiP");
     if (p->n_ode == 0) return;
     GemmArgs z;  // z_0 = W1_a a_0 + P + b1 + W1_t φ(0)
     z.M = n; z.A = p->a_t; z.W = p->qw1a; z.bias = p->qc; z.addend = p->P; z.ld_add = H; z.N = H; z.K = NM;
-    z.out_a = p->h1; z.out_f = p->z1; z.ld_f = H;
+    z.out_a = p->h1; z.out_f = p->z1; z.ld_f = H; z.f4_rows = f4;
     ckp(launch_gemm(z, kEpiTanhPre, s), "psi1");
     ckp(cudaMemsetAsync(p->hsum, 0, sizeof(float) * static_cast<size_t>(pad_to(n, kGemmBM)) * H, s), "hsum");
     void *x = p->h1, *y = p->h2;  // x: tanh(z_k)
@@ -250,19 +253,20 @@ void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_
         q.M = n; q.N = H; q.K = H;
         q.A = x; q.W = p->qw2; q.bias = p->qb2; q.out_a = y;
         ckp(launch_gemm(q, kEpiTanhTiled, s), "psi2");
-        q.A = y; q.W = p->qw3; q.bias = p->qb3; q.out_a = x; q.out_f = p->hsum; q.ld_f = H;
+        q.A = y; q.W = p->qw3; q.bias = p->qb3; q.out_a = x; q.out_f = p->hsum; q.ld_f = H; q.f4_rows = f4;
         ckp(launch_gemm(q, kEpiTanhAcc, s), "psi3");
         if (k + 1 < p->n_ode) {  // z_{k+1} = z_k + dt (W1_a W4) h3_k + qd_k
             GemmArgs u;
             u.M = n; u.N = H; u.K = H; u.A = x; u.W = p->qm; u.bias = p->qd + static_cast<size_t>(k) * H;
             u.addend = p->z1; u.ld_add = H; u.out_f = p->z1; u.ld_f = H; u.out_a = y;
             u.scale = static_cast<float>(p->dt);
+            u.f4_rows = f4;
             ckp(launch_gemm(u, kEpiTanhPre, s), "psi1");
             std::swap(x, y);
         }
     }
     // a_N = a_0 + dt (W4 Σ_k h3_k + N b4), in place on the action buffer
-    ckp(launch_f32_to_tiled(p->hsum, n, H, H, y, s), "hsum tiles");
+    ckp(launch_f32_to_tiled(p->hsum, n, H, H, y, s, f4), "hsum tiles");
     GemmArgs fh;
     fh.M = n; fh.A = y; fh.W = p->qw4; fh.bias = p->qhb; fh.N = NM; fh.K = H; fh.out_f = actions; fh.ld_f = NM;
     fh.n_valid = NM; fh.scale = static_cast<float>(p->dt); fh.addend = actions; fh.ld_add = NM;
