@@ -422,10 +422,17 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             }
             for (int d = 0; d <= c.n_levels; ++d) blob[M.tab_off_lvs + d] = static_cast<unsigned char>(c.level_start[d]);
             // work word of slot i of level d: link | (parent + 1) << 8 | child_off << 16 |
-            // nchild << 24 | has_sphere << 28 | valid << 31 (one shared load per level)
+            // nchild << 24 | has_sphere << 28 | simple level << 29 | valid << 31 (one shared load per level)
             for (int d = 0; d < c.n_levels; ++d) {
                 const int b = c.level_start[d], n = c.level_start[d + 1] - b;
                 if (n > 32) throw ConfigError("model too wide: a tree level has more than 32 links");
+                // bit 29: the level is "simple" — every link has a parent link and a joint DOF
+                // (no root, no child of the fixed base), so the passes skip those branches
+                bool simple = true;
+                for (int i = 0; i < n; ++i) {
+                    const int l = c.level_links[b + i];
+                    simple = simple && c.link_parent[l] >= 0 && l >= c.floating;
+                }
                 for (int i = 0; i < n; ++i) {
                     const int l = c.level_links[b + i];
                     const int nchild = c.child_start[l + 1] - c.child_start[l];
@@ -434,7 +441,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
                     const uint32_t w = static_cast<uint32_t>(l) | (static_cast<uint32_t>(c.link_parent[l] + 1) << 8) |
                                        (static_cast<uint32_t>(c.child_start[l]) << 16) |
                                        (static_cast<uint32_t>(nchild) << 24) | (static_cast<uint32_t>(has_sph) << 28) |
-                                       (1u << 31);
+                                       (static_cast<uint32_t>(simple) << 29) | (1u << 31);
                     put(M.tab_off_work + 4 * (32 * d + i), &w, 4);
                 }
             }

@@ -340,6 +340,105 @@ __device__ __forceinline__ void sphere_pen_d(const DevModel& M, const EnvSmem& S
     __syncwarp(S.hm);
 }
 
+// One link of the root-to-leaf sweep (tree_sweep).  kSimple: the level has no
+// root and no child of the fixed base (work-word bit 29), so the link has a
+// parent and a joint DOF = l + nrd - floating.
+template <bool kFull, bool kSimple>
+__device__ __forceinline__ void sweep_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff, float* grf) {
+    const int l = ww_link(ww);
+    const int dof = kSimple ? l + dofoff : link_dof(M, l);
+    const float4 la = S.ta[l];
+    float c, s, ox, oz, w = 0.0f, vx = 0.0f, vz = 0.0f;
+    if (!kSimple && dof < 0) {  // floating root: origin (0,0) relative, pitch q2
+        c = S.root[2];
+        s = S.root[3];
+        ox = 0.0f;
+        oz = 0.0f;
+        if (kFull) {
+            w = S.dqf[2];
+            vx = S.dqf[0];
+            vz = S.dqf[1];
+        }
+    } else {
+        const int p = ww_parent(ww);
+        const double2 rd = S.relcs[dof];
+        const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
+        if (kSimple || p >= 0) {
+            const float4 kp = S.kin[p];
+            ox = fmaf(kp.x, la.x, fmaf(-kp.y, la.y, kp.z));
+            oz = fmaf(kp.y, la.x, fmaf(kp.x, la.y, kp.w));
+            c = fmaf(kp.x, cr, -kp.y * sr);
+            s = fmaf(kp.y, cr, kp.x * sr);
+            if (kFull) {
+                const float* up = S.un + kLinkStride * p;
+                const float2 wv = reinterpret_cast<const float2*>(up)[5];  // parent (omega, v_x)
+                w = wv.x + S.dqf[dof];
+                vx = fmaf(-wv.x, oz - kp.w, wv.y);
+                vz = fmaf(wv.x, ox - kp.z, up[9]);
+            }
+        } else {
+            ox = la.x;
+            oz = la.y;
+            c = cr;
+            s = sr;
+            if (kFull) w = S.dqf[dof];
+        }
+    }
+    S.kin[l] = make_float4(c, s, ox, oz);
+    if (!kFull) return;
+    float* u = S.un + kLinkStride * l;
+    // link record (14 floats): [0..5] articulated inertia, [6..8] bias force,
+    // [9] u/D, [10..11] U1/D, U2/D, [12..13] c; velocity (omega, v_x | v_z)
+    // lives in [10..11 | 9] during this sweep only
+    reinterpret_cast<float2*>(u)[5] = make_float2(w, vx);
+    u[9] = vz;
+    const float m = la.w, I = S.tin[l];
+    const float cx = la.z * c, cz = la.z * s;
+    const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
+    const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
+    const float mg = m * M.gravity;
+    float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
+    if ((ww >> 28) & 1) {  // link carries contact spheres
+        const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
+        float gx = 0.0f, gz = 0.0f;
+        for (int sp = s0; sp < s1; ++sp) {
+            const float4 sd = __ldg(M.sphere + sp);
+            const float rx = fmaf(c, sd.x, -s * sd.y), rz = fmaf(s, sd.x, c * sd.y);
+            // penetration from the f64 world height (sphere_pen_d)
+            const float pen = S.pen[sp];
+            if (pen > 0.0f) {
+                const float fn = fmaxf(0.0f, fmaf(M.c_k, pen, -M.c_c * fmaf(w, rx, vz)));
+                if (fn > 0.0f) {
+                    const float qz = rz - sd.z;  // contact point relative to the origin
+                    const float ft = -M.c_mu * fn * tanhf(fmaf(-w, qz, vx) * M.inv_c_vs);
+                    p0 -= fmaf(rx, fn, -qz * ft);
+                    p1 -= ft;
+                    p2 -= fn;
+                    gx += ft * 0.1f;
+                    gz += fn * 0.1f;
+                }
+            }
+        }
+        if (grf) {
+            grf[2 * l] += gx;
+            grf[2 * l + 1] += gz;
+        }
+    }
+    float c1 = 0.0f, c2 = 0.0f;
+    if (dof >= 0) {  // c = V x S qdot at the joint: (0, qdot v_z, -qdot v_x)
+        const float qdot = S.dqf[dof];
+        c1 = qdot * vz;
+        c2 = -qdot * vx;
+    }
+    float2* u2 = reinterpret_cast<float2*>(u);  // 8-B aligned (stride 14 floats)
+    u2[0] = make_float2(i00, i01);
+    u2[1] = make_float2(i02, m);
+    u2[2] = make_float2(0.0f, m);
+    u2[3] = make_float2(p0, p1);
+    u[8] = p2;
+    u2[6] = make_float2(c1, c2);
+}
+
 // Root-to-leaf sweep.  FK by rotation composition R_l = R_p R_joint
 // (skeleton.cpp:82-107, root-relative); with kFull also velocity kinematics
 // (skeleton.cpp:43-72) and each link's own articulated-body terms: spatial
@@ -348,102 +447,15 @@ __device__ __forceinline__ void sphere_pen_d(const DevModel& M, const EnvSmem& S
 // substep (sphere_force / 10, skeleton.cpp:323-325) accumulates into grf.
 template <bool kFull>
 __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, int lane, float* grf) {
+    const int dofoff = M.nrd - M.floating;
     for (int lev = 0; lev < M.n_levels; ++lev) {
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
             if (!(ww >> 31)) break;
-            const int l = ww_link(ww);
-            const int dof = link_dof(M, l);
-            const float4 la = S.ta[l];
-            float c, s, ox, oz, w = 0.0f, vx = 0.0f, vz = 0.0f;
-            if (dof < 0) {  // floating root: origin (0,0) relative, pitch q2
-                c = S.root[2];
-                s = S.root[3];
-                ox = 0.0f;
-                oz = 0.0f;
-                if (kFull) {
-                    w = S.dqf[2];
-                    vx = S.dqf[0];
-                    vz = S.dqf[1];
-                }
-            } else {
-                const int p = ww_parent(ww);
-                const double2 rd = S.relcs[dof];
-                const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
-                if (p >= 0) {
-                    const float4 kp = S.kin[p];
-                    ox = fmaf(kp.x, la.x, fmaf(-kp.y, la.y, kp.z));
-                    oz = fmaf(kp.y, la.x, fmaf(kp.x, la.y, kp.w));
-                    c = fmaf(kp.x, cr, -kp.y * sr);
-                    s = fmaf(kp.y, cr, kp.x * sr);
-                    if (kFull) {
-                        const float* up = S.un + kLinkStride * p;
-                        const float2 wv = reinterpret_cast<const float2*>(up)[5];  // parent (omega, v_x)
-                        w = wv.x + S.dqf[dof];
-                        vx = fmaf(-wv.x, oz - kp.w, wv.y);
-                        vz = fmaf(wv.x, ox - kp.z, up[9]);
-                    }
-                } else {
-                    ox = la.x;
-                    oz = la.y;
-                    c = cr;
-                    s = sr;
-                    if (kFull) w = S.dqf[dof];
-                }
-            }
-            S.kin[l] = make_float4(c, s, ox, oz);
-            if (!kFull) continue;
-            float* u = S.un + kLinkStride * l;
-            // link record (14 floats): [0..5] articulated inertia, [6..8] bias force,
-            // [9] u/D, [10..11] U1/D, U2/D, [12..13] c; velocity (omega, v_x | v_z)
-            // lives in [10..11 | 9] during this sweep only
-            reinterpret_cast<float2*>(u)[5] = make_float2(w, vx);
-            u[9] = vz;
-            const float m = la.w, I = S.tin[l];
-            const float cx = la.z * c, cz = la.z * s;
-            const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
-            const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
-            const float mg = m * M.gravity;
-            float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
-            if ((ww >> 28) & 1) {  // link carries contact spheres
-                const int s0 = __ldg(M.sphere_start + l), s1 = __ldg(M.sphere_start + l + 1);
-                float gx = 0.0f, gz = 0.0f;
-                for (int sp = s0; sp < s1; ++sp) {
-                    const float4 sd = __ldg(M.sphere + sp);
-                    const float rx = fmaf(c, sd.x, -s * sd.y), rz = fmaf(s, sd.x, c * sd.y);
-                    // penetration from the f64 world height (sphere_pen_d)
-                    const float pen = S.pen[sp];
-                    if (pen > 0.0f) {
-                        const float fn = fmaxf(0.0f, fmaf(M.c_k, pen, -M.c_c * fmaf(w, rx, vz)));
-                        if (fn > 0.0f) {
-                            const float qz = rz - sd.z;  // contact point relative to the origin
-                            const float ft = -M.c_mu * fn * tanhf(fmaf(-w, qz, vx) * M.inv_c_vs);
-                            p0 -= fmaf(rx, fn, -qz * ft);
-                            p1 -= ft;
-                            p2 -= fn;
-                            gx += ft * 0.1f;
-                            gz += fn * 0.1f;
-                        }
-                    }
-                }
-                if (grf) {
-                    grf[2 * l] += gx;
-                    grf[2 * l + 1] += gz;
-                }
-            }
-            float c1 = 0.0f, c2 = 0.0f;
-            if (dof >= 0) {  // c = V x S qdot at the joint: (0, qdot v_z, -qdot v_x)
-                const float qdot = S.dqf[dof];
-                c1 = qdot * vz;
-                c2 = -qdot * vx;
-            }
-            float2* u2 = reinterpret_cast<float2*>(u);  // 8-B aligned (stride 14 floats)
-            u2[0] = make_float2(i00, i01);
-            u2[1] = make_float2(i02, m);
-            u2[2] = make_float2(0.0f, m);
-            u2[3] = make_float2(p0, p1);
-            u[8] = p2;
-            u2[6] = make_float2(c1, c2);
+            if ((ww >> 29) & 1)
+                sweep_link<kFull, true>(M, S, ww, dofoff, grf);
+            else
+                sweep_link<kFull, false>(M, S, ww, dofoff, grf);
         }
         __syncwarp(S.hm);
     }
@@ -810,77 +822,115 @@ __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& 
 
 // Articulated-body pass, leaves -> root (per link U = IA e0, D, Schur
 // complement, shift to the parent origin; children summed in fixed order).
+template <bool kSimple>
+__device__ __forceinline__ void aba_up_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff) {
+    const int l = ww_link(ww);
+    float* u = S.un + kLinkStride * l;
+    float2* u2 = reinterpret_cast<float2*>(u);
+    float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
+    float P2 = u[8];
+    const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
+#pragma unroll 1  // mostly one child: an unrolled 4/2/1 cascade costs more branches than it saves (A/B +1.8 %)
+    for (int c = c0; c < c1; ++c) {
+        const float* uc = S.un + kLinkStride * S.tchild[c];
+        const float2* uc2 = reinterpret_cast<const float2*>(uc);
+        const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
+        r0.x += a0.x;
+        r0.y += a0.y;
+        r1.x += a1.x;
+        r1.y += a1.y;
+        r2.x += a2.x;
+        r2.y += a2.y;
+        r3.x += a3.x;
+        r3.y += a3.y;
+        P2 += uc[8];
+    }
+    const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
+    const float P0 = r3.x, P1 = r3.y;
+    const int dof = kSimple ? l + dofoff : link_dof(M, l);
+    if (!kSimple && dof < 0) {  // floating root keeps its full articulated inertia
+        u2[0] = r0;
+        u2[1] = r1;
+        u2[2] = r2;
+        u2[3] = r3;
+        u[8] = P2;
+        return;
+    }
+    // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
+    const float invD = rcp_ftz(I00);  // (IEEE 1/x costs a range check + slow-path call)
+    const float t = S.tau[dof];
+    const float uu = (t - P0) * invD;               // u / D
+    const float U1 = I01 * invD, U2 = I02 * invD;   // U / D
+    const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
+    const float bb = fmaf(-I01, U2, I12);
+    const float cq = fmaf(-I02, U2, I22);
+    const float2 cv = u2[6];
+    // pa = pA + Ia c + U u / D   (pa[0] = tau)
+    const float q1 = fmaf(I01, uu, fmaf(a, cv.x, fmaf(bb, cv.y, P1)));
+    const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
+    u[9] = uu;
+    u2[5] = make_float2(U1, U2);
+    const int p = ww_parent(ww);
+    if (kSimple || p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
+        const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
+        const float dx = ol.x - op.x, dz = ol.y - op.y;
+        const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
+        u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
+        u2[1] = make_float2(be, a);
+        u2[2] = make_float2(bb, cq);
+        u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
+        u[8] = q2;
+    }
+}
+
 __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int lane) {
+    const int dofoff = M.nrd - M.floating;
     for (int lev = M.n_levels - 1; lev >= 0; --lev) {
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
             if (!(ww >> 31)) break;
-            const int l = ww_link(ww);
-            float* u = S.un + kLinkStride * l;
-            float2* u2 = reinterpret_cast<float2*>(u);
-            float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
-            float P2 = u[8];
-            const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
-#pragma unroll 1  // mostly one child: an unrolled 4/2/1 cascade costs more branches than it saves (A/B +1.8 %)
-            for (int c = c0; c < c1; ++c) {
-                const float* uc = S.un + kLinkStride * S.tchild[c];
-                const float2* uc2 = reinterpret_cast<const float2*>(uc);
-                const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
-                r0.x += a0.x;
-                r0.y += a0.y;
-                r1.x += a1.x;
-                r1.y += a1.y;
-                r2.x += a2.x;
-                r2.y += a2.y;
-                r3.x += a3.x;
-                r3.y += a3.y;
-                P2 += uc[8];
-            }
-            const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
-            const float P0 = r3.x, P1 = r3.y;
-            const int dof = link_dof(M, l);
-            if (dof < 0) {  // floating root keeps its full articulated inertia
-                u2[0] = r0;
-                u2[1] = r1;
-                u2[2] = r2;
-                u2[3] = r3;
-                u[8] = P2;
-                continue;
-            }
-            // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
-            const float invD = rcp_ftz(I00);  // (IEEE 1/x costs a range check + slow-path call)
-            const float t = S.tau[dof];
-            const float uu = (t - P0) * invD;               // u / D
-            const float U1 = I01 * invD, U2 = I02 * invD;   // U / D
-            const float a = fmaf(-I01, U1, I11);            // Ia = IA - U U^T / D
-            const float bb = fmaf(-I01, U2, I12);
-            const float cq = fmaf(-I02, U2, I22);
-            const float2 cv = u2[6];
-            // pa = pA + Ia c + U u / D   (pa[0] = tau)
-            const float q1 = fmaf(I01, uu, fmaf(a, cv.x, fmaf(bb, cv.y, P1)));
-            const float q2 = fmaf(I02, uu, fmaf(bb, cv.x, fmaf(cq, cv.y, P2)));
-            u[9] = uu;
-            u2[5] = make_float2(U1, U2);
-            const int p = ww_parent(ww);
-            if (p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
-                const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
-                const float dx = ol.x - op.x, dz = ol.y - op.y;
-                const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
-                u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
-                u2[1] = make_float2(be, a);
-                u2[2] = make_float2(bb, cq);
-                u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
-                u[8] = q2;
-            }
+            if ((ww >> 29) & 1)
+                aba_up_link<true>(M, S, ww, dofoff);
+            else
+                aba_up_link<false>(M, S, ww, dofoff);
         }
         __syncwarp(S.hm);
     }
+}
 
+// One link of the root-to-leaf articulated-body pass: q̈ into S.tau.
+template <bool kSimple>
+__device__ __forceinline__ void aba_down_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff) {
+    const int l = ww_link(ww);
+    const int dof = kSimple ? l + dofoff : link_dof(M, l);
+    if (!kSimple && dof < 0) return;
+    float* u = S.un + kLinkStride * l;
+    const int p = ww_parent(ww);
+    float2* u2 = reinterpret_cast<float2*>(u);
+    const float2 cv = u2[6];
+    float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
+    if (kSimple || p >= 0) {
+        const float* up = S.un + kLinkStride * p;
+        const float2 a01 = reinterpret_cast<const float2*>(up)[0];
+        const float a2 = up[2];
+        const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
+        const float dx = ol.x - op.x, dz = ol.y - op.y;
+        A0 = a01.x;
+        A1 += fmaf(-a01.x, dz, a01.y);
+        A2 += fmaf(a01.x, dx, a2);
+    }
+    // q̈ = (u - U^T A) / D with U0 = D
+    const float2 U = u2[5];
+    const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
+    u2[0] = make_float2(A0 + qdd, A1);
+    u[2] = A2;
+    S.tau[dof] = qdd;
 }
 
 // Floating-root solve (3x3 Cholesky) + articulated-body pass, root -> leaves:
 // q̈ into S.tau.
 __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, int lane) {
+    const int dofoff = M.nrd - M.floating;
     if (M.floating && lane == 0) {
         float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky with reciprocal pivots)
         const float i00 = rsqrt_ftz(u[0]);
@@ -908,30 +958,10 @@ __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, in
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
             if (!(ww >> 31)) break;
-            const int l = ww_link(ww);
-            const int dof = link_dof(M, l);
-            if (dof < 0) continue;
-            float* u = S.un + kLinkStride * l;
-            const int p = ww_parent(ww);
-            float2* u2 = reinterpret_cast<float2*>(u);
-            const float2 cv = u2[6];
-            float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
-            if (p >= 0) {
-                const float* up = S.un + kLinkStride * p;
-                const float2 a01 = reinterpret_cast<const float2*>(up)[0];
-                const float a2 = up[2];
-                const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
-                const float dx = ol.x - op.x, dz = ol.y - op.y;
-                A0 = a01.x;
-                A1 += fmaf(-a01.x, dz, a01.y);
-                A2 += fmaf(a01.x, dx, a2);
-            }
-            // q̈ = (u - U^T A) / D with U0 = D
-            const float2 U = u2[5];
-            const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
-            u2[0] = make_float2(A0 + qdd, A1);
-            u[2] = A2;
-            S.tau[dof] = qdd;
+            if ((ww >> 29) & 1)
+                aba_down_link<true>(M, S, ww, dofoff);
+            else
+                aba_down_link<false>(M, S, ww, dofoff);
         }
         __syncwarp(S.hm);
     }
