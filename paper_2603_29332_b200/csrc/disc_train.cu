@@ -206,9 +206,8 @@ enum Epi : int {
     kEpiHead,      // out0 = H3 = tanh(acc + bias); head row scalars; out1 = d3 = d4 w4 ∘ (1 - H3²)
     kEpiGate,      // out0 = acc ∘ (1 - h²)
     kEpiPlain,     // out0 = acc
-    kEpiGate2,     // out1 = z = acc, out0 = acc ∘ (1 - h²)
     kEpiTHead,     // penalty head: zeta4, V; out0 = S_t, out1 = S_p (layer-3 reverse step); w4 / b column sums
-    kEpiRev        // dual: bu = acc_t, bh = acc_p -> out0 = S_t, out1 = S_p (reverse step); b column sums
+    kEpiRev        // dual: bu = acc_t, bh = acc_p; h, u = G∘ζ -> out0 = S_t, out1 = S_p (reverse step); b column sums
 };
 
 struct RowArgs {
@@ -225,7 +224,7 @@ struct RowArgs {
     const float* bias = nullptr;         // [N]
     const float* w4 = nullptr;           // head weights [N]
     const float* b4 = nullptr;           // head bias
-    Img h, z;                            // gate activations, pre-gate tangent
+    Img h, z;                            // gate activations H_l, gated tangent u_l (kEpiRev)
     Img out[2];
     float *d4 = nullptr, *dd4 = nullptr, *dz4 = nullptr, *vh = nullptr;
     double *lrow = nullptr, *prow = nullptr;
@@ -288,7 +287,7 @@ __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tac
     float* cp1 = g.colpart[1] ? g.colpart[1] + static_cast<size_t>(mb * 4 + q) * g.ldc : nullptr;
     float v[16], x[16];
 
-    if constexpr (EPI == kEpiTanh || EPI == kEpiGate || EPI == kEpiPlain || EPI == kEpiGate2) {
+    if constexpr (EPI == kEpiTanh || EPI == kEpiGate || EPI == kEpiPlain) {
         for (int c = c_lo; c < c_hi; c += 16) {
             tmem_ld16(tl + c, v);
             if (EPI == kEpiTanh) {
@@ -301,11 +300,6 @@ __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tac
                 store16(g.out[0], r, c, v);
             } else {
                 load16(g.h, r, c, x);
-                if (EPI == kEpiGate2) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] = valid ? v[i] : 0.0f;
-                    store16(g.out[1], r, c, v);
-                }
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = valid ? v[i] * (1.0f - x[i] * x[i]) : 0.0f;
                 store16(g.out[0], r, c, v);
@@ -392,19 +386,21 @@ __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tac
             colsum16(sp, cp1 + c, lane);
         }
     } else {  // kEpiRev: accumulator columns [0, 128) tangent rows (b_u), [128, 256) primal rows (b_h)
+        // b_ζ = G∘b_u, b_z = G∘(b_h − 2H∘ζ∘b_u) = G∘b_h − 2H∘u∘b_u with u = G∘ζ, the gated
+        // tangent stored as the next layer's operand (g.z): no pre-gate tangent image
         for (int c = c_lo; c < c_hi; c += 16) {
-            float bh[16], zt[16];
+            float bh[16], ut[16];
             const int oc = obase + c;
             tmem_ld16(tl + c, v);
             tmem_ld16(tl + 128 + c, bh);
             load16(g.h, r, oc, x);
-            load16(g.z, r, oc, zt);
+            load16(g.z, r, oc, ut);
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
                 const float h = x[i], gt = 1.0f - h * h;
-                const float b2 = fmaf(-2.0f * h * zt[i], v[i], bh[i]);
+                const float sp = fmaf(-2.0f * h * ut[i], v[i], gt * bh[i]);
                 v[i] = valid ? gt * v[i] : 0.0f;
-                bh[i] = valid ? gt * b2 : 0.0f;
+                bh[i] = valid ? sp : 0.0f;
             }
             store16(g.out[0], r, oc, v);
             store16(g.out[1], r, oc, bh);
@@ -878,7 +874,7 @@ struct msk_disc_trainer {
     long long* counts = nullptr;  // {Adam step_count, skipped}
     int* bad = nullptr;
     // split images (see iofs)
-    Img X, Xt, H1, H2, H3, D3, T2, T1, At1, At2, Z1, Z2, St, Sp, Ut, Up;
+    Img X, Xt, H1, H2, H3, D3, T2, T1, At1, At2, St, Sp, Ut, Up;
     Img Wf[3], Wb[3];
     float *d4 = nullptr, *dd4 = nullptr, *dz4 = nullptr, *vh = nullptr;
     double *lrow = nullptr, *prow = nullptr, *loss = nullptr, *lpart = nullptr;
@@ -959,7 +955,6 @@ void prepare_kernels() {
     prep_row<kEpiHead>();
     prep_row<kEpiGate>();
     prep_row<kEpiPlain>();
-    prep_row<kEpiGate2>();
     prep_row<kEpiTHead>();
     prep_row<kEpiRev>();
     int dev = 0;
@@ -1087,13 +1082,11 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     a = rargs(t, t->Xt, t->Wf[0], Hp, R);
     a.h = t->H1;
     a.out[0] = t->At1;
-    a.out[1] = t->Z1;
-    row<kEpiGate2>(a, tiles, s);
+    row<kEpiGate>(a, tiles, s);
     a = rargs(t, t->At1, t->Wf[1], Hp, R);
     a.h = t->H2;
     a.out[0] = t->At2;
-    a.out[1] = t->Z2;
-    row<kEpiGate2>(a, tiles, s);
+    row<kEpiGate>(a, tiles, s);
     a = rargs(t, t->At2, t->Wf[2], Hp, R);
     a.h = t->H3;
     a.w4 = w4;
@@ -1116,7 +1109,7 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     a.a_hi[1] = t->Sp.hi;
     a.a_lo[1] = t->Sp.lo;
     a.h = t->H2;
-    a.z = t->Z2;
+    a.z = t->At2;
     a.out[0] = t->Ut;
     a.out[1] = t->Up;
     a.colpart[0] = t->colpart[2];
@@ -1127,7 +1120,7 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
     a.a_hi[1] = t->Up.hi;
     a.a_lo[1] = t->Up.lo;
     a.h = t->H1;
-    a.z = t->Z1;
+    a.z = t->At1;
     a.out[0] = t->St;
     a.out[1] = t->Sp;
     a.colpart[0] = t->colpart[3];
@@ -1232,8 +1225,8 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
         const int Hp = t->Hp, Dp = t->Dp;
         t->X = img_alloc(t, rows_p, Dp);
         t->Xt = img_alloc(t, rows_p, Dp);
-        for (Img* im : {&t->H1, &t->H2, &t->H3, &t->D3, &t->T2, &t->T1, &t->At1, &t->At2, &t->Z1, &t->Z2, &t->St,
-                        &t->Sp, &t->Ut, &t->Up})
+        for (Img* im : {&t->H1, &t->H2, &t->H3, &t->D3, &t->T2, &t->T1, &t->At1, &t->At2, &t->St, &t->Sp, &t->Ut,
+                        &t->Up})
             *im = img_alloc(t, rows_p, Hp);
         for (int l = 0; l < 3; ++l) {
             const int inp = l == 0 ? Dp : Hp;
