@@ -1252,6 +1252,143 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
 }
 
 // ============================================================================
+// step kernel with quad tree passes: one warp per env for the muscle phase,
+// torques and integration (as step_kernel), but the three tree passes of Q env
+// warps run on ONE warp of the group — 32/Q lanes per env (tree levels hold 1-11
+// links), so their instructions serve Q envs while the other Q-1 warps free
+// their issue slots.  Named barriers (one per group) order the phases; every
+// warp runs every substep (inactive / diverged envs do no work but still meet
+// the barriers).  Same per-env arithmetic as step_kernel.
+// ============================================================================
+template <int WPB, int Q, int NSEG, int QSL>
+__global__ void __launch_bounds__(WPB * 32, 1) stepq_kernel(DevModel M, DevState St, int env0, int n_envs,
+                                                             const float* __restrict__ actions, float* obs,
+                                                             float* delta, float* reward_aux, uint8_t* flags,
+                                                             float* power, float* grf, int n_substeps) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    static_assert(QSL >= 1 && QSL <= kMaxQSlots, "DOF slots");
+    static_assert(WPB % Q == 0 && (Q == 2 || Q == 4), "tree groups");
+    constexpr int QS = QSL, GQ = 32 / Q;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int group = warp / Q;
+    load_tree_table(smem, M);
+    const int nq = M.nq, nm = M.nm, nl = M.nl, nrd = M.nrd;
+    const auto group_bar = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + group), "n"(Q * 32) : "memory"); };
+
+    // this warp's env (muscle phase / integration / epilogue)
+    const int slot = warp;
+    const bool has_slot = slot < M.epb;
+    const int le = blockIdx.x * M.epb + slot;
+    const bool exists = has_slot && le < n_envs;
+    const int e = env0 + (exists ? le : 0);
+    bool live = exists;
+    if (live && St.done[e]) {  // contract checks of Env::step (env.cpp:207-210)
+        if (lane == 0 && flags) flags[le] = kFlagNotStepped;
+        live = false;
+    }
+    if (live && St.u_bad[e]) {
+        if (lane == 0 && flags) flags[le] = kFlagBadAction;
+        live = false;
+    }
+    const bool stepped = live;
+    const EnvSmem S = carve(smem, has_slot ? slot : 0, M, 32, 0xffffffffu);
+    const size_t mb = static_cast<size_t>(e) * nm;
+    const float* act_row = St.u + mb;
+    float* pw = nullptr;
+    float* grf_row = nullptr;
+    double qd[QS], dqd[QS];
+    if (stepped) {
+        pw = power ? power + static_cast<size_t>(le) * nm : (M.reward_mode == 2 ? St.power_scratch + mb : nullptr);
+        grf_row = grf ? grf + static_cast<size_t>(le) * 2 * nl : nullptr;
+        load_dofs<QS>(M, S, St.q + static_cast<size_t>(e) * nq, St.dq + static_cast<size_t>(e) * nq, qd, dqd, lane);
+        publish_dofs<QS>(M, S, qd, dqd, lane);
+        if (pw)
+            for (int m = lane; m < nm; m += 32) pw[m] = 0.0f;
+        if (grf_row)
+            for (int i = lane; i < 2 * nl; i += 32) grf_row[i] = 0.0f;
+    }
+    __syncwarp();
+
+    // the group's tree view (used by the group's first warp): env of lane group g
+    const bool leader = (warp % Q) == 0;
+    const int g = lane / GQ, glane = lane % GQ;
+    const int tslot = group * Q + g;
+    const int tle = blockIdx.x * M.epb + tslot;
+    bool t_act = tslot < M.epb && tle < n_envs;  // the tree pass of an existing env slot
+    float* tgrf = nullptr;
+    if (leader && t_act) {
+        const int te = env0 + tle;
+        const bool t_step = !St.done[te] && !St.u_bad[te];
+        tgrf = (grf && t_step) ? grf + static_cast<size_t>(tle) * 2 * nl : nullptr;
+    }
+    const EnvSmem ST = carve(smem, t_act ? tslot : 0, M, GQ, (GQ == 32 ? 0xffffffffu : ((1u << GQ) - 1u) << (GQ * g)));
+
+    int diverged_at = -1;
+    for (int sub = 0; sub < n_substeps; ++sub) {
+        if (live) {
+            if (M.has_general) fk_d(M, S, lane);
+            muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane, sub == n_substeps - 1);
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < QS; ++k) {  // joint torques: fixed-order slot sums, damping, limits
+                const int d = lane + 32 * k;
+                if (d >= nrd && d < nq) {
+                    const int j = d - nrd;
+                    const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
+                    float t = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
+                    int s = s0;
+                    for (; s + 3 < s1; s += 4) {
+                        t += S.un[s];
+                        t1 += S.un[s + 1];
+                        t2 += S.un[s + 2];
+                        t3 += S.un[s + 3];
+                    }
+                    for (; s < s1; ++s) t += S.un[s];
+                    t = (t + t1) + (t2 + t3);
+                    t -= __ldg(M.joint_damping + j) * static_cast<float>(dqd[k]);
+                    const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
+                    if (qd[k] > hi)
+                        t -= static_cast<float>(M.k_lim_d * (qd[k] - hi));
+                    else if (qd[k] < lo)
+                        t -= static_cast<float>(M.k_lim_d * (qd[k] - lo));
+                    S.tau[d] = t;
+                }
+            }
+        }
+        group_bar();  // the group's torques and joint states are in shared memory
+        if (leader && t_act) {
+            if (M.ns) sphere_pen_d(M, ST, glane);
+            tree_sweep<true>(M, ST, glane, tgrf);
+            aba_up(M, ST, glane);
+            aba_down(M, ST, glane);
+        }
+        group_bar();  // q̈ of every env of the group is in shared memory
+        if (live) {
+            bool bad = false;
+#pragma unroll
+            for (int k = 0; k < QS; ++k) {
+                const int d = lane + 32 * k;
+                if (d < nq) {
+                    dqd[k] += static_cast<double>(S.tau[d]) * kSimDt;
+                    qd[k] += dqd[k] * kSimDt;
+                    bad |= !isfinite(qd[k]) || !isfinite(dqd[k]);
+                }
+            }
+            __syncwarp();
+            publish_dofs<QS>(M, S, qd, dqd, lane);
+            __syncwarp();
+            if (__any_sync(0xffffffffu, bad)) {
+                diverged_at = sub;
+                live = false;  // frozen at the diverging substep (msk::step throws there)
+            }
+        }
+    }
+    if (stepped)
+        step_epilogue<QS>(M, St, S, e, le, qd, dqd, diverged_at, n_substeps, obs, delta, reward_aux, flags, power,
+                          grf_row, pw, lane);
+}
+
+// ============================================================================
 // step kernel, NE envs per thread ("env-vectorised"): every lane of a warp
 // advances NE environments at once — muscle constants, tree tables, work words,
 // loop control and address arithmetic are shared by the NE envs, and each
@@ -2147,6 +2284,16 @@ int step_qslots(const DevModel& M) { return M.nq <= 96 ? 3 : kMaxQSlots; }
 // stepn_kernel, opt-in: 15 % fewer instructions at NE = 2 but half the warps per SM,
 // and the 128-register cap of 4 warps per SM partition leaves no room for the ILP
 // that would hide the per-env dependency chains — measured 0.628 / 0.870 ms vs 0.551 ms).
+// Envs per tree warp of the step kernel (MSK_TREEQ: 1 = step_kernel, 2 or 4 = stepq_kernel).
+int step_treeq() {
+    static const int q = [] {
+        const char* v = std::getenv("MSK_TREEQ");
+        const int x = v ? std::atoi(v) : 1;
+        return (x == 1 || x == 2 || x == 4) ? x : 1;
+    }();
+    return kEPW == 1 && kWPB % 4 == 0 ? q : 1;
+}
+
 int step_ne() {
     static const int ne = [] {
         const char* v = std::getenv("MSK_NE");
@@ -2162,6 +2309,10 @@ cudaError_t set_step_smem(int bytes) {
     if ((e = cudaFuncSetAttribute(stepn_kernel<14, 2, NSEG, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
         return e;
     if ((e = cudaFuncSetAttribute(stepn_kernel<7, 4, NSEG, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute(stepq_kernel<kWPB, 2, NSEG, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
+        return e;
+    if ((e = cudaFuncSetAttribute(stepq_kernel<kWPB, 4, NSEG, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes)))
         return e;
     return cudaFuncSetAttribute(step_kernel<kWPB, kMinB, NSEG, kEPW, QSL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 bytes);
@@ -2197,10 +2348,16 @@ void launch_step(const DevModel& M, const DevState& St, int env0, int n, const f
                  int n_substeps) {
     const int blocks = (n + M.epb - 1) / M.epb;
     const size_t smem = block_smem(M);
-    const int ne = step_ne();
+    const int ne = step_ne(), tq = step_treeq();
 #define MSK_STEP(NS, QSL)                                                                                          \
     do {                                                                                                           \
-        if (ne == 2)                                                                                               \
+        if (tq == 2 && ne == 1)                                                                                    \
+            stepq_kernel<kWPB, 2, NS, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta,   \
+                                                                             raux, flags, power, grf, n_substeps); \
+        else if (tq == 4 && ne == 1)                                                                               \
+            stepq_kernel<kWPB, 4, NS, QSL><<<blocks, kWPB * 32, smem, s>>>(M, St, env0, n, actions, obs, delta,   \
+                                                                             raux, flags, power, grf, n_substeps); \
+        else if (ne == 2)                                                                                          \
             stepn_kernel<14, 2, NS, QSL><<<blocks, 14 * 32, smem, s>>>(M, St, env0, n, actions, obs, delta, raux,  \
                                                                          flags, power, grf, n_substeps);           \
         else if (ne == 4)                                                                                          \
