@@ -186,18 +186,24 @@ def cpu_model():
     return {"model": name, "logical_cpus": os.cpu_count()}
 
 
+def ref_build(fast):
+    return ("reference sources (oracle/_ref) g++ -O3 -march=x86-64-v3 -ffp-contract=fast, eager Eigen shim"
+            if fast else "reference sources (oracle/_ref) g++ -O2 -march=x86-64-v3 -ffp-contract=off, eager Eigen shim")
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's CPU path (oracle/_ref) on the host cores."""
     if rank != 0:
         return
-    from oracle.ref import RefBatch, env_config
+    from oracle.ref import REF_FAST_SO, RefBatch, env_config
 
     mp, cp = model_files(args.model)
     C = args.C
     threads = args.cpu_threads or os.cpu_count() or 1
     n_envs = args.ref_envs or 8 * threads  # BASELINE.md §3: E_cpu = 8 x cores
     cfg = env_config(episode_horizon=C["horizon"], rsi=C["rsi"])
-    b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads, reward_mode=C["reward_mode"])
+    fast = os.path.exists(REF_FAST_SO)  # the -O3 / FMA build of the same reference sources
+    b = RefBatch(mp, cp, n_envs, cfg=cfg, threads=threads, reward_mode=C["reward_mode"], fast=fast)
     b.set_eval_mode(C["eval"])
     if C["disc"]:  # Env::step(action, fn) with the reference's own Mlp as fn (same θ as the GPU arm)
         import paper_2603_29332_b200 as pk
@@ -218,21 +224,22 @@ def run_reference(args, rank, world):
                        "parallelism": f"{threads} host threads (ThreadPool::parallel_chunks)"},
             "cpu_baseline": {"value": v, "unit": "env-steps/s", "cores": threads, "kind": "reference",
                              "sample": f"{n_envs} envs x {args.steps} control steps ({secs:.1f} s)",
-                             "cpu": cpu_model()},
+                             "cpu": cpu_model(), "build": ref_build(fast)},
             "e2e": {"value": v, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline_sample(args):
     """Bounded sample (~10-20 s) of the reference CPU path for the cpu_baseline key."""
-    from oracle.ref import RefBatch, env_config
+    from oracle.ref import REF_FAST_SO, RefBatch, env_config
 
     mp, cp = model_files(args.model)
     C = args.C
     threads = args.cpu_threads or os.cpu_count() or 1
     n_envs = 8 * threads  # BASELINE.md §3: E_cpu = 8 x cores
+    fast = os.path.exists(REF_FAST_SO)
     b = RefBatch(mp, cp, n_envs, cfg=env_config(episode_horizon=C["horizon"], rsi=C["rsi"]), threads=threads,
-                 reward_mode=C["reward_mode"])
+                 reward_mode=C["reward_mode"], fast=fast)
     b.set_eval_mode(C["eval"])
     if C["disc"]:
         import paper_2603_29332_b200 as pk
@@ -245,7 +252,8 @@ def cpu_baseline_sample(args):
     k = max(1, min(5000, int(args.cpu_seconds / max(per_step, 1e-3))))
     secs, steps = b.bench(k)
     return {"value": steps / secs, "unit": "env-steps/s", "cores": threads, "kind": "reference",
-            "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)", "cpu": cpu_model()}
+            "sample": f"{n_envs} envs x {k} control steps of {args.model} ({secs:.1f} s)", "cpu": cpu_model(),
+            "build": ref_build(fast)}
 
 
 def self_launch(n):

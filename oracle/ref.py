@@ -19,6 +19,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 REF_SO = os.path.join(HERE, "_ref", "libmsk_ref.so")
+# the same sources built for speed (-O3, FMA contraction): the CPU timing arm only
+REF_FAST_SO = os.path.join(HERE, "_ref", "libmsk_ref_fast.so")
 ORACLE_SO = os.path.join(HERE, "libmsk_oracle.so")
 
 FLAG_DONE, FLAG_FAILED, FLAG_DIVERGED, FLAG_NOT_STEPPED, FLAG_BAD_ACTION = 1, 2, 4, 8, 16
@@ -68,13 +70,15 @@ def _load(path):
     return C.CDLL(path)
 
 
-_REF = None
+_REF = {}
 
 
-def ref_lib():
-    global _REF
-    if _REF is None:
-        lib = _load(REF_SO)
+def ref_lib(fast=False):
+    """The reference build (fast=True: the -O3 / FMA-contracted build used to time
+    the CPU arm; parity checks always use the strict-IEEE build)."""
+    path = REF_FAST_SO if fast else REF_SO
+    if path not in _REF:
+        lib = _load(path)
         lib.ref_create.restype = C.c_void_p
         lib.ref_create.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(EnvConfigC), C.POINTER(RewardConfigC),
                                    C.c_int32, C.c_uint64, C.c_int64, C.c_char_p, C.c_int32]
@@ -131,8 +135,8 @@ def ref_lib():
         lib.ref_mechanical_energy.restype = C.c_double
         lib.ref_mechanical_energy.argtypes = [C.c_void_p, _dp, _dp]
         lib.ref_key_bodies.argtypes = [C.c_void_p, _dp, _dp, _dp]
-        _REF = lib
-    return _REF
+        _REF[path] = lib
+    return _REF[path]
 
 
 def excitations(seed, step, n_envs, nm, global_env_offset=0):
@@ -147,8 +151,8 @@ class RefBatch:
     """E independent reference ``msk::Env`` instances (seed = base_seed + global index)."""
 
     def __init__(self, model_path, clip_path, n_envs, base_seed=0x5EED, cfg=None, reward_mode=0, w_emg=100.0,
-                 w_power=0.05, emg_map=(), global_env_offset=0, threads=1):
-        lib = ref_lib()
+                 w_power=0.05, emg_map=(), global_env_offset=0, threads=1, fast=False):
+        lib = ref_lib(fast)
         self.lib = lib
         cfg = cfg if cfg is not None else env_config()
         self._emg = np.asarray(emg_map, dtype=np.int32)

@@ -308,19 +308,25 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         }
         M.max_seg = c.max_seg;
         M.has_general = c.has_general;
-        {  // chunk runs by padded segment count (muscles are sorted by it): a lane group's
-           // chunk of G consecutive muscles pads to the count of its last muscle
+        {  // fast path over the muscles without a general segment ([0, n_fast), sorted by
+           // segment count) in chunk runs by padded segment count: a lane group's chunk of
+           // G consecutive muscles pads to the count of its last muscle; the generic loop
+           // takes the rest ([gen0, nm))
+            const bool fast = c.n_fast > 0 && c.max_seg_fast <= 4;
+            const int nf = fast ? c.n_fast : 0;
+            M.fast_nseg = fast ? std::max(1, c.max_seg_fast) : 0;
+            M.gen0 = nf;
             const int G = lanes_per_env();
             std::vector<int> chunk_ns;
-            for (int m0 = 0; m0 < c.nm; m0 += G) chunk_ns.push_back(c.pk_meta[std::min(m0 + G, c.nm) - 1] & 0xff);
+            for (int m0 = 0; m0 < nf; m0 += G) chunk_ns.push_back(c.pk_meta[std::min(m0 + G, nf) - 1] & 0xff);
             for (int k = 0; k <= 5; ++k) {
-                int m = c.nm;
+                int m = nf;
                 for (size_t ch = 0; ch < chunk_ns.size(); ++ch)
                     if (chunk_ns[ch] >= k) {
                         m = static_cast<int>(ch) * G;
                         break;
                     }
-                M.seg_run[k] = k == 5 ? c.nm : m;
+                M.seg_run[k] = k == 5 ? nf : m;
             }
             M.seg_run[0] = 0;
         }

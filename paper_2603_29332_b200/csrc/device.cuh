@@ -50,9 +50,11 @@ struct DevModel {
     const float4* m_p0;    // {f_max, -dt/tau_act log2(e), -dt/tau_deact log2(e), l_opt v_max / 10}
     const double2* m_p1a;  // {slack, l_opt}
     const double2* m_p1b;  // {1/l_opt, 1/(dt l_opt v_max)}
-    const int* m_meta;     // nseg | general << 8 | reference index << 9 (muscles sorted by nseg)
+    const int* m_meta;     // nseg | general << 8 | reference index << 9 (general muscles last, then by nseg)
     const int* m_int;      // reference index -> internal index
     int seg_run[6];        // [k, k+1): muscles (whole lane-group chunks) padded to k segments, k = 0..4
+    int fast_nseg;         // NSEG of the fast path (0: the generic loop over all muscles)
+    int gen0;              // first muscle (device order) of the generic loop: general muscles (or 0, or nm)
     // Same-link / adjacent segment k of muscle m at [k * nm + m] (coalesced over m):
     // {K1, K2h, K3h, info bits} with |s|^2 = K1 + 2 (cos K2h + sin K3h) and
     // r x A = cos K3h - sin K2h (cos/sin of the child joint's own angle, f64).

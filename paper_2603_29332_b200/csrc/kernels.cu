@@ -223,7 +223,8 @@ __device__ __forceinline__ double2 via_point_d(const DevModel& M, const double2*
 __device__ __forceinline__ double general_seg_len(const DevModel& M, const EnvSmem& S, int v_end) {
     const double2 pe = via_point_d(M, S.kind, v_end), ps = via_point_d(M, S.kind, v_end - 1);
     const double dx = pe.x - ps.x, dz = pe.y - ps.y;
-    return sqrt(fma(dx, dx, dz * dz));
+    float inv;
+    return sqrt_d(fma(dx, dx, dz * dz), inv);  // f32 rsqrt seed + one f64 Newton step (~46 bits)
 }
 
 // Same-link (kind 0) or adjacent (kind 1) segment from its K constants
@@ -256,21 +257,35 @@ __device__ __forceinline__ double muscle_length(const DevModel& M, const EnvSmem
 // J_m^T F of the general (non-adjacent) segments of muscle m (reference index),
 // world frame (skeleton.cpp:147-170): the segment direction and the lever arm
 // about the joint from the f64 frames (fk_d), the moment rounded to f32 once.
+// A segment's pairs (one per joint on its tree path) are consecutive, so its via
+// points, direction and reciprocal length are computed once per segment.
 __device__ void general_pairs(const DevModel& M, const EnvSmem& S, int m, float F) {
     const int p0 = __ldg(M.m_pair_start + m), p1 = __ldg(M.m_pair_start + m + 1);
+    int ve_cur = -1;
+    double2 pe = make_double2(0.0, 0.0), ps = make_double2(0.0, 0.0);
+    double sx = 0.0, sz = 0.0, inv_len = 0.0;
+    bool ok = false;
     for (int p = p0; p < p1; ++p) {
         const int ve = __ldg(M.pair_via + p), j = __ldg(M.pair_joint + p);
         const float sg = __ldg(M.pair_sign + p);
-        const double2 pe = via_point_d(M, S.kind, ve);
-        const double2 ps = via_point_d(M, S.kind, ve - 1);
-        const double sx = pe.x - ps.x, sz = pe.y - ps.y;
-        const double len = sqrt(fma(sx, sx, sz * sz));
+        if (ve != ve_cur) {
+            ve_cur = ve;
+            pe = via_point_d(M, S.kind, ve);
+            ps = via_point_d(M, S.kind, ve - 1);
+            sx = pe.x - ps.x;
+            sz = pe.y - ps.y;
+            const double l2 = fma(sx, sx, sz * sz);
+            ok = l2 > 1e-24;  // |s| > 1e-12 (skeleton.cpp:160)
+            float inv32;
+            const double len = sqrt_d(l2, inv32);
+            inv_len = 1.0 / len;
+        }
         float val = 0.0f;
-        if (len > 1e-12) {
+        if (ok) {
             const double2 ka = S.kind[2 * (M.floating + j) + 1];  // joint j's child-link origin
             const double2 pt = sg < 0.0f ? pe : ps;
             const double rx = pt.x - ka.x, rz = pt.y - ka.y;
-            val = static_cast<float>(static_cast<double>(sg * F) * (fma(rx, sz, -rz * sx) / len));
+            val = static_cast<float>(static_cast<double>(sg * F) * (fma(rx, sz, -rz * sx) * inv_len));
         }
         S.un[__ldg(M.pair_slot + p)] = val;
     }
@@ -778,45 +793,55 @@ __device__ __forceinline__ void muscle_run(const DevModel& M, const DevState& St
     for (int m = m0 + lane; m < m1; m += S.G) muscle_one<NS>(M, R, S, pw, m, last);
 }
 
+// Muscles [m_begin, nm) through the generic per-segment loop (general segments
+// from the f64 frames of fk_d, adjacent ones in K-form).
+__device__ __forceinline__ void muscle_generic(const DevModel& M, const DevState& St, const EnvSmem& S,
+                                               const float* act_row, size_t mb, float* pw, int lane, bool last,
+                                               int m_begin) {
+    const int nm = M.nm;
+    for (int m = m_begin + lane; m < nm; m += S.G) {
+        const int meta = __ldg(M.m_meta + m);
+        const int nseg = meta & 0xff, ext = meta >> 9;
+        const float4 p0 = __ldg(M.m_p0 + m);
+        const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
+        const MuscleRows R = muscle_rows(St, act_row, mb);
+        const float u = R.u[m];
+        const float a0 = R.act[m];
+        const double lm0 = R.lm[m];
+        double L = 0.0;
+        for (int k = 0; k < nseg; ++k) {
+            const float4 kf = __ldg(M.seg_kf + k * nm + m);
+            const int info = __float_as_int(kf.w);
+            float arm;
+            L += (info & 3) == 2 ? general_seg_len(M, S, info >> 11) : kseg(S, kf, info, arm);
+        }
+        const float F = muscle_update(R, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
+        for (int k = 0; k < nseg; ++k) {
+            const float4 kf = __ldg(M.seg_kf + k * nm + m);
+            const int info = __float_as_int(kf.w);
+            if ((info & 3) != 1) continue;
+            float arm;
+            kseg(S, kf, info, arm);
+            S.un[info >> 11] = -F * arm;
+        }
+        if ((meta >> 8) & 1) general_pairs(M, S, ext, F);
+    }
+}
+
 template <int NSEG>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
                                              const float* act_row, size_t mb, float* pw, int lane, bool last) {
-    const int nm = M.nm;
     if constexpr (NSEG > 0) {
-        // runs of chunks by padded segment count (M.seg_run, muscle units): 0, 1, ..., NSEG
+        // runs of chunks by padded segment count (M.seg_run, muscle units): 0, 1, ..., NSEG,
+        // over the muscles without a general segment; general muscles follow from M.gen0
         muscle_run<0>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[0], M.seg_run[1]);
         if constexpr (NSEG >= 1) muscle_run<1>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[1], M.seg_run[2]);
         if constexpr (NSEG >= 2) muscle_run<2>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[2], M.seg_run[3]);
         if constexpr (NSEG >= 3) muscle_run<3>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[3], M.seg_run[4]);
         if constexpr (NSEG >= 4) muscle_run<4>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[4], M.seg_run[5]);
+        if (M.gen0 < M.nm) muscle_generic(M, St, S, act_row, mb, pw, lane, last, M.gen0);
     } else {
-        for (int m = lane; m < nm; m += S.G) {
-            const int meta = __ldg(M.m_meta + m);
-            const int nseg = meta & 0xff, ext = meta >> 9;
-            const float4 p0 = __ldg(M.m_p0 + m);
-            const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
-            const MuscleRows R = muscle_rows(St, act_row, mb);
-            const float u = R.u[m];
-            const float a0 = R.act[m];
-            const double lm0 = R.lm[m];
-            double L = 0.0;
-            for (int k = 0; k < nseg; ++k) {
-                const float4 kf = __ldg(M.seg_kf + k * nm + m);
-                const int info = __float_as_int(kf.w);
-                float arm;
-                L += (info & 3) == 2 ? general_seg_len(M, S, info >> 11) : kseg(S, kf, info, arm);
-            }
-            const float F = muscle_update(R, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
-            for (int k = 0; k < nseg; ++k) {
-                const float4 kf = __ldg(M.seg_kf + k * nm + m);
-                const int info = __float_as_int(kf.w);
-                if ((info & 3) != 1) continue;
-                float arm;
-                kseg(S, kf, info, arm);
-                S.un[info >> 11] = -F * arm;
-            }
-            if ((meta >> 8) & 1) general_pairs(M, S, ext, F);
-        }
+        muscle_generic(M, St, S, act_row, mb, pw, lane, last, 0);
     }
 }
 
@@ -1471,6 +1496,10 @@ __device__ __forceinline__ void muscle_phase_n(const DevModel& M, const DevState
         if constexpr (NSEG >= 2) muscle_run_n<2, NE>(M, V, S, lane, last, M.seg_run[2], M.seg_run[3]);
         if constexpr (NSEG >= 3) muscle_run_n<3, NE>(M, V, S, lane, last, M.seg_run[3], M.seg_run[4]);
         if constexpr (NSEG >= 4) muscle_run_n<4, NE>(M, V, S, lane, last, M.seg_run[4], M.seg_run[5]);
+        if (M.gen0 < M.nm)  // general muscles: the single-env generic loop per live env
+#pragma unroll
+            for (int e = 0; e < NE; ++e)
+                if (V.live[e]) muscle_generic(M, St, S[e], V.R[e].u, mb[e], V.pw[e], lane, last, M.gen0);
     } else {  // generic segments: the single-env path per live env
 #pragma unroll
         for (int e = 0; e < NE; ++e)
@@ -2276,7 +2305,7 @@ constexpr int kMinB = MSK_MINB;
 constexpr int kEnvsPerBlock = kWPB * kEPW;
 
 // Fast-path segment count for a model (0 = generic path).
-int step_variant(const DevModel& M) { return (!M.has_general && M.max_seg >= 1 && M.max_seg <= 4) ? M.max_seg : 0; }
+int step_variant(const DevModel& M) { return M.fast_nseg; }
 // DOF register slots per lane: 3 covers n_q <= 96 (the whole-body models), else 4.
 int step_qslots(const DevModel& M) { return M.nq <= 96 ? 3 : kMaxQSlots; }
 

@@ -538,11 +538,26 @@ CompiledModel compile_model(const ModelSpec& s) {
     // A warp's 32 muscles then share one padded segment count, so padding
     // costs only at class boundaries.  Per-muscle I/O (actions, obs, power,
     // EMG channels, get/set_state) stays in reference order via m_ext / m_int.
+    // Muscles with a general (non-adjacent) segment go last: the step kernel runs the
+    // compile-time segment-count fast path over [0, n_fast) and the generic loop only
+    // over the tail.
+    std::vector<int> m_general(c.nm, 0);
+    for (int mi = 0; mi < c.nm; ++mi)
+        for (int sg = c.m_seg_start[mi]; sg < c.m_seg_start[mi + 1]; ++sg)
+            if ((c.seg_info[sg] & 3) == 2) m_general[mi] = 1;
     c.m_ext.resize(c.nm);
     for (int i = 0; i < c.nm; ++i) c.m_ext[i] = i;
     std::stable_sort(c.m_ext.begin(), c.m_ext.end(), [&](int a, int b) {
+        if (m_general[a] != m_general[b]) return m_general[a] < m_general[b];
         return c.m_seg_start[a + 1] - c.m_seg_start[a] < c.m_seg_start[b + 1] - c.m_seg_start[b];
     });
+    c.n_fast = 0;
+    c.max_seg_fast = 0;
+    for (int mi = 0; mi < c.nm; ++mi)
+        if (!m_general[mi]) {
+            ++c.n_fast;
+            c.max_seg_fast = std::max(c.max_seg_fast, c.m_seg_start[mi + 1] - c.m_seg_start[mi]);
+        }
     c.m_int.assign(c.nm, 0);
     for (int i = 0; i < c.nm; ++i) c.m_int[c.m_ext[i]] = i;
     if (c.nm >= (1 << 22)) throw ConfigError("model too large for the packed layout");

@@ -119,7 +119,8 @@ struct CompiledModel {
     // 32 consecutive records (coalesced): geo = {ax, az, cx, cz},
     // info = kind | dof << 2 | slot << 11 (kind 2: slot = global via index of the end).
     int max_seg = 0, has_general = 0;
-    // internal muscle order (sorted by segment count): m_ext[i] = reference
+    int n_fast = 0, max_seg_fast = 0;  // muscles without a general segment (device order [0, n_fast)), their max nseg
+    // internal muscle order (general muscles last, then by segment count): m_ext[i] = reference
     // index of internal muscle i, m_int = its inverse; pk_meta carries m_ext << 9
     std::vector<int32_t> m_ext, m_int;
     std::vector<float> pk_p0, pk_geo;

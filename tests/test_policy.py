@@ -234,3 +234,40 @@ def test_rollout_minibatches_are_a_keyed_permutation():
     again = ro.minibatch(11, 1, 0, mb, D, NA)["record_ids"].cpu().numpy()
     assert np.array_equal(again, orders[1][:mb])
     ro.close()
+
+
+_PAIR_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_2603_29332_b200 as pk
+rng = np.random.default_rng(5)
+M, K, N = 512, 320, 512   # 4 row tiles: CTA pairs apply; two N tiles, ragged K
+X = rng.normal(0, 1, (M, K)).astype(np.float32)
+W = rng.normal(0, 1 / np.sqrt(K), (N, K))
+b = rng.normal(0, 0.1, N).astype(np.float32)
+Wc = np.asfortranarray(W).ravel(order="F")
+for epi in (0, 1):
+    Y = np.zeros((M, N), dtype=np.float32)
+    assert pk.lib().msk_gemm_test(X.ctypes.data, M, K, Wc.ctypes.data, b.ctypes.data, N, epi, Y.ctypes.data) == 0
+    np.save(sys.argv[2] + f"_{epi}.npy", Y)
+"""
+
+
+def test_cta_pair_gemm_equals_single_cta(tmp_path):
+    """The opt-in CTA-pair GEMM (MSK_GEMM_2CTA: tcgen05.mma.cta_group::2, both CTAs'
+    TMA tensor copies completing on the leader's barrier) gives the single-CTA
+    kernel's results bit for bit (same K-order per output element)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode, env in (("single", {}), ("pair", {"MSK_GEMM_2CTA": "1"})):
+        base = str(tmp_path / mode)
+        r = subprocess.run([sys.executable, "-c", _PAIR_SCRIPT, root, base], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[mode] = [np.load(base + f"_{epi}.npy") for epi in (0, 1)]
+    for a, b in zip(outs["single"], outs["pair"]):
+        assert np.array_equal(a, b)
