@@ -148,7 +148,7 @@ def _bias_cond_rel(g, ref, theta, din, H, delta, lam):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("math,tol_g,tol_c,tol_l", [(0, 1e-4, 1e-5, 1e-5), (1, 5e-2, 5e-3, 1e-3)])
-@pytest.mark.parametrize("din,H,B", [(9, 16, 37), (102, 256, 1000)])
+@pytest.mark.parametrize("din,H,B", [(9, 16, 37), (102, 256, 1000), (130, 200, 333)])
 def test_device_gradient_matches_oracle(math, tol_g, tol_c, tol_l, din, H, B):
     import torch
 
