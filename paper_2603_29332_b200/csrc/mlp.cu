@@ -24,7 +24,13 @@ namespace msk_b200 {
 
 namespace {
 
-constexpr int kStages = 4;
+#ifndef MSK_GEMM_STAGES
+#define MSK_GEMM_STAGES 4
+#endif
+#ifndef MSK_GEMM_MINB
+#define MSK_GEMM_MINB 1
+#endif
+constexpr int kStages = MSK_GEMM_STAGES;
 constexpr int kABytes = kGemmBM * kGemmBK * 2;  // 16 KB
 constexpr int kWBytes = kGemmBN * kGemmBK * 2;  // 32 KB
 // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: epilogue (two warps per
@@ -300,7 +306,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
 // traffic drops by CL; every MMA commit frees the stage in all CTAs of the
 // cluster (multicast commit), which is what each producer waits for.
 template <int EPI, int CL>
-__global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, MSK_GEMM_MINB) gemm_kernel(GemmArgs g) {
 extern __shared__ __align__(1024) unsigned char smem[];
 unsigned char* sA = smem;                                    // kStages x 16 KB
 unsigned char* sW = smem + kStages * kABytes;                // kStages x 32 KB
@@ -323,7 +329,8 @@ if (threadIdx.x == 0) {
 }
 if constexpr (CL > 1) cluster_sync();  // peers' barriers exist before any multicast
 if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tslot))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tslot)),
+                 "n"(kGemmBN)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
 }
@@ -388,7 +395,7 @@ if (warp == 0 && lane == 0) {  // TMA producer
 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 __syncthreads();
 if constexpr (CL > 1) cluster_sync();  // no CTA leaves while peers may still signal it
-if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kGemmBN) : "memory");
 }
 
 // CTA-pair variant (tcgen05 cta_group::2): a cluster of two CTAs computes a

@@ -17,7 +17,10 @@
 
 namespace msk_b200 {
 
-constexpr int kGemmBM = 128, kGemmBN = 256, kGemmBK = 64;
+#ifndef MSK_GEMM_BN
+#define MSK_GEMM_BN 256
+#endif
+constexpr int kGemmBM = 128, kGemmBN = MSK_GEMM_BN, kGemmBK = 64;
 
 __host__ __device__ inline int pad_to(int x, int m) { return (x + m - 1) / m * m; }
 inline size_t tiled_a_bytes(int M, int K) { return static_cast<size_t>(pad_to(M, kGemmBM)) * pad_to(K, kGemmBK) * 2; }
