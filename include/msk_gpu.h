@@ -325,6 +325,9 @@ int32_t msk_policy_time_features(double t, double* out5);
 /* Test hook: Y = act(X W^T + b) through one tiled tensor-core GEMM (epi 0 tanh, 1 linear). */
 int msk_gemm_test(const float* X, int32_t M, int32_t K, const double* W, const float* b, int32_t N, int32_t epi,
                   float* Y);
+/* Diagnostic: average ms of `reps` back-to-back tanh GEMM layers (M x K by K x N,
+ * zero operands) on the device, programmatic dependent launches. */
+int msk_gemm_bench(int32_t M, int32_t K, int32_t N, int32_t reps, double* ms_per_gemm);
 
 /* ---- on-device rollout buffer + GAE ----------------------
  * h control steps x E envs, step-major: obs, a0, actions, logprob, reward,

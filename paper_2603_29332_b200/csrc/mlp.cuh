@@ -58,6 +58,12 @@ struct GemmArgs {
 };
 
 cudaError_t prepare_gemm();
+// The ψ ODE's 3 n_ode − 1 hidden layers in one persistent launch (see mlp.cu
+// ode_kernel): g2 / g3 / g1 carry W, bias, M, N = K = H and the f32 side buffers
+// (g3: hsum, g1: z, scale = dt); x0 / y0 the two tiled activation images (x0
+// holds tanh(z_0)); qd the per-step ψ1 biases.  H / 256 <= 8 (cluster size).
+cudaError_t launch_ode(const GemmArgs& g2, const GemmArgs& g3, const GemmArgs& g1, void* x0, void* y0,
+                       const float* qd, int n_ode, int H, cudaStream_t s);
 size_t gemm_smem_bytes();
 cudaError_t launch_gemm(const GemmArgs& g, int epi, cudaStream_t s);
 

@@ -20,6 +20,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -248,6 +250,22 @@ void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_
     ckp(launch_gemm(z, kEpiTanhPre, s), "psi1");
     ckp(cudaMemsetAsync(p->hsum, 0, sizeof(float) * static_cast<size_t>(pad_to(n, kGemmBM)) * H, s), "hsum");
     void *x = p->h1, *y = p->h2;  // x: tanh(z_k)
+    // MSK_POLICY_ODE=1: the 3 N_ODE - 1 hidden layers in one persistent launch (mlp.cu ode_kernel;
+    // opt-in, slower at W = 1024); default: one pipelined GEMM launch per layer
+    static const bool persistent = std::getenv("MSK_POLICY_ODE") != nullptr;
+    if (persistent && pad_to(H, kGemmBN) / kGemmBN <= 8) {
+        GemmArgs g2, g3, g1;
+        g2.M = g3.M = g1.M = n;
+        g2.N = g3.N = g1.N = H;
+        g2.K = g3.K = g1.K = H;
+        g2.W = p->qw2; g2.bias = p->qb2;
+        g3.W = p->qw3; g3.bias = p->qb3; g3.out_f = p->hsum; g3.ld_f = H; g3.f4_rows = f4;
+        g1.W = p->qm; g1.addend = p->z1; g1.ld_add = H; g1.out_f = p->z1; g1.ld_f = H; g1.f4_rows = f4;
+        g1.scale = static_cast<float>(p->dt);
+        ckp(launch_ode(g2, g3, g1, x, y, p->qd, p->n_ode, H, s), "ode");
+        x = p->h1;
+        y = p->h2;
+    } else {
     for (int k = 0; k < p->n_ode; ++k) {
         GemmArgs q;
         q.M = n; q.N = H; q.K = H;
@@ -264,6 +282,7 @@ void enqueue_sample(msk_policy* p, const float* obs, int n, int explore, uint64_
             ckp(launch_gemm(u, kEpiTanhPre, s), "psi1");
             std::swap(x, y);
         }
+    }
     }
     // a_N = a_0 + dt (W4 Σ_k h3_k + N b4), in place on the action buffer
     ckp(launch_f32_to_tiled(p->hsum, n, H, H, y, s, f4), "hsum tiles");
@@ -542,6 +561,42 @@ int msk_gemm_test(const float* X, int32_t M, int32_t K, const double* W_host, co
         ckp(cudaDeviceSynchronize(), "sync");
         cudaFree(dW); cudaFree(dX); cudaFree(dO); cudaFree(dY); cudaFree(dXf);
         if (db) cudaFree(db);
+        return MSK_OK;
+    } catch (const std::exception& ex) {
+        return pfail(nullptr, ex.what(), MSK_ERR_CUDA);
+    }
+}
+
+// Diagnostic: average time of `reps` back-to-back tanh GEMM layers [M x K] x [K x N]^T
+// on device buffers (programmatic dependent launches, as in the policy sample).
+int msk_gemm_bench(int32_t M, int32_t K, int32_t N, int32_t reps, double* ms_per_gemm) {
+    try {
+        ckp(prepare_gemm(), "prepare");
+        void *dW, *dX, *dO;
+        ckp(cudaMalloc(&dW, tiled_w_bytes(N, K)), "m");
+        ckp(cudaMemset(dW, 0, tiled_w_bytes(N, K)), "z");
+        ckp(cudaMalloc(&dX, tiled_a_bytes(M, K)), "m");
+        ckp(cudaMemset(dX, 0, tiled_a_bytes(M, K)), "z");
+        ckp(cudaMalloc(&dO, tiled_a_bytes(M, N)), "m");
+        GemmArgs g;
+        g.A = dX; g.W = dW; g.M = M; g.N = N; g.K = K; g.out_a = dO;
+        cudaStream_t s;
+        ckp(cudaStreamCreate(&s), "stream");
+        for (int i = 0; i < 3; ++i) ckp(launch_gemm(g, kEpiTanhTiled, s), "gemm");
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0, s);
+        for (int i = 0; i < reps; ++i) ckp(launch_gemm(g, kEpiTanhTiled, s), "gemm");
+        cudaEventRecord(e1, s);
+        ckp(cudaEventSynchronize(e1), "sync");
+        float ms = 0.0f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        *ms_per_gemm = ms / reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaStreamDestroy(s);
+        cudaFree(dW); cudaFree(dX); cudaFree(dO);
         return MSK_OK;
     } catch (const std::exception& ex) {
         return pfail(nullptr, ex.what(), MSK_ERR_CUDA);

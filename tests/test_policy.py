@@ -271,3 +271,33 @@ def test_cta_pair_gemm_equals_single_cta(tmp_path):
         outs[mode] = [np.load(base + f"_{epi}.npy") for epi in (0, 1)]
     for a, b in zip(outs["single"], outs["pair"]):
         assert np.array_equal(a, b)
+
+
+def test_persistent_ode_kernel_equals_per_layer_launches():
+    """The opt-in persistent ψ-ODE kernel (MSK_POLICY_ODE=1: all hidden layers of the
+    flow ODE in one launch, cluster-wide layer barriers over DSMEM) samples the same
+    actions as the per-layer GEMM launches, bit for bit."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/tests")
+import paper_2603_29332_b200 as pk
+from test_policy import _params, D, NM, H
+pi, ls, psi = _params(3)
+p = pk.Policy(D, NM, H, pi, ls, psi, max_envs=512)
+obs = torch.as_tensor(np.random.default_rng(2).normal(0, 1, (300, D)).astype(np.float32), device="cuda")
+a = p.sample(obs, explore=True, seed=5, step=1)
+np.save(sys.argv[2], a.cpu().numpy())
+"""
+    outs = []
+    for env in ({}, {"MSK_POLICY_ODE": "1"}):
+        path = os.path.join(str(os.environ.get("TMPDIR", "/tmp")), f"ode_{len(outs)}_{os.getpid()}.npy")
+        r = subprocess.run([sys.executable, "-c", script, root, path], env={**os.environ, **env},
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
