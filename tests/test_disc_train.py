@@ -379,3 +379,39 @@ def test_oracle_bias_adjoint_rows_sum_to_the_gradient():
         assert rw.shape == (B + 1, b - a)
         assert np.max(np.abs(rw.sum(0) - g[a:b])) <= 1e-15
         assert np.linalg.norm(np.abs(rw).sum(0)) > 50 * np.linalg.norm(g[a:b])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("din,H,B", [(9, 16, 37), (102, 256, 300)])
+def test_trainer_outputs_stay_inside_caller_buffers(din, H, B):
+    """Out-of-bounds check for the training step's caller buffers (compute-sanitizer
+    is closed on the GPU pool): grad / loss outputs and the Δ input view sit inside
+    larger buffers whose guard bytes must survive gradient() and step()."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2603_29332_b200 as pk
+
+    GUARD = 4096
+    theta = mlp_init(din, H, 7)
+    tr = pk.DiscTrainer(din, H, theta, max_rows=B, math=0)
+    P = len(theta)
+    graw = torch.full((P + 2 * GUARD,), -7.0, device="cuda")
+    lraw = torch.full((3 + 2 * GUARD,), -7.0, dtype=torch.float64, device="cuda")
+    draw = torch.full(((B + 2) * (din + 3),), -7.0, device="cuda")
+    delta = draw[(din + 3):(B + 1) * (din + 3)].view(B, din + 3)[:, :din]  # strided view, guards around
+    delta.copy_(torch.randn(B, din, device="cuda") * 0.3)
+    L = pk.lib()
+    for _ in range(2):
+        assert L.msk_disc_trainer_gradient(tr.h_, C.c_void_p(delta.data_ptr()), B, delta.stride(0),
+                                           C.c_void_p(graw.data_ptr() + 4 * GUARD),
+                                           C.c_void_p(lraw.data_ptr() + 8 * GUARD),
+                                           C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+        tr.step(delta)
+    torch.cuda.synchronize()
+    for raw, n in ((graw, P), (lraw, 3)):
+        assert torch.all(raw[:GUARD] == -7.0) and torch.all(raw[GUARD + n:] == -7.0)
+    assert torch.all(draw[:din + 3] == -7.0) and torch.all(draw[(B + 1) * (din + 3):] == -7.0)
+    assert torch.all(torch.isfinite(graw[GUARD:GUARD + P]))
+    tr.close()
