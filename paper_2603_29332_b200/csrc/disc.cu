@@ -283,7 +283,9 @@ __device__ __forceinline__ void split_bf16(float x, __nv_bfloat16& hi, __nv_bflo
     lo = __float2bfloat16_rn(x - __bfloat162float(hi));
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+constexpr int kThreadsP = 256;  // precise kernel: two warps per TMEM lane quarter (column halves)
+
+__global__ void __launch_bounds__(kThreadsP, 1)
     disc_reward_precise_kernel(DiscDev P, const float* __restrict__ delta, int ld, int n, const float* __restrict__ raux,
                                const uint8_t* __restrict__ flags, float* __restrict__ reward) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
-    for (int i = tid; i < 4 * H; i += kThreads) sb[i] = P.bias[i];
+    for (int i = tid; i < 4 * H; i += kThreadsP) sb[i] = P.bias[i];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -335,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < kRing && c < K1 / 16; ++c) load_chunk(0, c, c);
 
     asm volatile("griddepcontrol.wait;" ::: "memory");  // Δ = the previous kernel's output
-    for (int i = tid; i < kTileM * K1; i += kThreads) {
+    for (int i = tid; i < kTileM * K1; i += kThreadsP) {
         const int r = i / K1, k = i - r * K1, row = row0 + r;
         const float x = (row < n && k < P.din) ? delta[static_cast<size_t>(row) * ld + k] : 0.0f;
         __nv_bfloat16 hi, lo;
@@ -346,8 +348,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     proxy_fence();
     __syncthreads();
 
-    const int r = warp * 32 + lane;
-    const uint32_t trow = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    // epilogue: warp w reads TMEM lane quarter w % 4 (rows), column half w / 4
+    const int q = warp & 3, half = warp >> 2, r = q * 32 + lane;
+    const bool split = H % 32 == 0;  // halves of whole 16-column TMEM loads; else warps 0-3 take all columns
+    const int c_lo = split ? half * (H / 2) : (half ? H : 0), c_hi = split ? c_lo + H / 2 : H;
+    const uint32_t trow = tmem + (static_cast<uint32_t>(q * 32) << 16);
+    float* sdot = reinterpret_cast<float*>(tmem_slot + 4);  // [2][128] head partial dot products
     const uint32_t idesc = instr_desc(H);
     uint32_t done_phase = 0;
     for (int layer = 0; layer < 3; ++layer) {
@@ -382,15 +388,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         done_phase ^= 1;
         tc_fence_after();
         if (layer < 2) {
-            for (int c = 0; c < H; c += 16) {  // tanh(acc + b) -> split bf16 A for the next layer (K = H)
+            for (int c = c_lo; c < c_hi; c += 16) {  // tanh(acc + b) -> split bf16 A for the next layer (K = H)
                 float v[16];
                 tmem_ld16(trow + c, v);
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    __nv_bfloat16 hi, lo;
-                    split_bf16(tanhf(v[i] + sb[layer * H + c + i]), hi, lo);
-                    *reinterpret_cast<__nv_bfloat16*>(sa_hi + img_off(r, c + i, H)) = hi;
-                    *reinterpret_cast<__nv_bfloat16*>(sa_lo + img_off(r, c + i, H)) = lo;
+                for (int j = 0; j < 16; j += 8) {  // 8 columns = one 16-B core-matrix row per plane
+                    uint32_t hw[4], lw[4];
+#pragma unroll
+                    for (int i = 0; i < 8; i += 2) {
+                        __nv_bfloat16 h0, l0, h1, l1;
+                        split_bf16(tanhf(v[j + i] + sb[layer * H + c + j + i]), h0, l0);
+                        split_bf16(tanhf(v[j + i + 1] + sb[layer * H + c + j + i + 1]), h1, l1);
+                        hw[i / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(h0)) |
+                                    (static_cast<uint32_t>(__bfloat16_as_ushort(h1)) << 16);
+                        lw[i / 2] = static_cast<uint32_t>(__bfloat16_as_ushort(l0)) |
+                                    (static_cast<uint32_t>(__bfloat16_as_ushort(l1)) << 16);
+                    }
+                    *reinterpret_cast<uint4*>(sa_hi + img_off(r, c + j, H)) = make_uint4(hw[0], hw[1], hw[2], hw[3]);
+                    *reinterpret_cast<uint4*>(sa_lo + img_off(r, c + j, H)) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
                 }
             }
             proxy_fence();
@@ -400,15 +415,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
     float z = 0.0f;
-    for (int c = 0; c < H; c += 16) {
+    for (int c = c_lo; c < c_hi; c += 16) {
         float v[16];
         tmem_ld16(trow + c, v);
 #pragma unroll
         for (int i = 0; i < 16; ++i) z = fmaf(tanhf(v[i] + sb[2 * H + c + i]), sb[3 * H + c + i], z);
     }
-    z += __ldg(P.bias + 4 * H);
+    sdot[half * kTileM + r] = z;
+    __syncthreads();
+    if (half == 0) z = (sdot[r] + sdot[kTileM + r]) + __ldg(P.bias + 4 * H);
     const int row = row0 + r;
-    if (row < n) {
+    if (half == 0 && row < n) {
         float d = 1.0f / (1.0f + expf(-z));
         d = fminf(fmaxf(d, 1e-4f), 1.0f - 1e-4f);
         const float rw = -log1pf(-d);
@@ -432,7 +449,7 @@ size_t disc_smem_bytes(const DiscDev& P) {
     const int Kmax = std::max(P.k1, P.hidden);
     if (P.precise)  // A hi + lo, the weight ring, biases, barriers
         return 2 * static_cast<size_t>(kTileM) * Kmax * 2 + static_cast<size_t>(kRing) * 2 * P.hidden * 32 +
-               16 * P.hidden + 128;
+               16 * P.hidden + 128 + 2 * kTileM * 4;
     return static_cast<size_t>(kTileM) * Kmax * 2 + static_cast<size_t>(P.hidden) * Kmax * 2 + 16 * P.hidden + 64;
 }
 
@@ -522,7 +539,7 @@ cudaError_t launch_disc(const DiscDev& P, const float* delta, int ld, int n, con
     if (n <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((n + kTileM - 1) / kTileM);
-    cfg.blockDim = dim3(kThreads);
+    cfg.blockDim = dim3(P.precise ? kThreadsP : kThreads);
     cfg.dynamicSmemBytes = disc_smem_bytes(P);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
