@@ -228,7 +228,7 @@ struct RowArgs {
     Img out[2];
     float *d4 = nullptr, *dd4 = nullptr, *dz4 = nullptr, *vh = nullptr;
     double *lrow = nullptr, *prow = nullptr;
-    float* colpart[2] = {nullptr, nullptr};  // [tiles * 4 x ldc] per-warp column sums
+    float* colpart[2] = {nullptr, nullptr};  // [CTAs * 4 x ldc] per-(CTA, warp) column sums
     int ldc = 0;
     int B = 0;
     float lamB = 0.0f;
@@ -255,8 +255,9 @@ __device__ __forceinline__ void load16(const Img& im, int r, int c, float (&v)[1
 }
 // Column sums over the 32 rows (lanes) of a warp for 16 columns: butterfly
 // reduce-scatter over lane bits 3..0, then the two lane halves combined; lanes
-// 0-15 write dst[lane] (fixed order: deterministic).
-__device__ __forceinline__ void colsum16(float (&x)[16], float* dst, int lane) {
+// 0-15 add their column's sum into acc (f64, accumulated over the warp's tiles in
+// a fixed order: deterministic).
+__device__ __forceinline__ void colsum16(float (&x)[16], double& acc, int lane) {
 #pragma unroll
     for (int o = 8; o >= 1; o >>= 1) {
         const bool up = (lane & o) != 0;
@@ -268,7 +269,7 @@ __device__ __forceinline__ void colsum16(float (&x)[16], float* dst, int lane) {
         }
     }
     x[0] += __shfl_xor_sync(0xffffffffu, x[0], 16);
-    if (lane < 16) dst[lane] = x[0];
+    acc += static_cast<double>(x[0]);
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kRowEpiWarps) : "memory"); }
 
@@ -276,15 +277,14 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 // slice j (a quarter of the unit's columns), 16 columns per TMEM load.
 template <int EPI>
 __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tacc, float* sdot, const float* sb,
-                                                  const float* sw, int mb, int nh, int q, int j, int lane) {
+                                                  const float* sw, int mb, int nh, int q, int j, int lane,
+                                                  double (&cacc)[2][4]) {
     constexpr bool kDual = EPI == kEpiRev;
     const int rt = q * 32 + lane, r = mb * 128 + rt;
     const bool valid = r < g.rows;
     const int ncols = kDual ? 128 : g.nb * 128, sl = ncols >> 2, c_lo = j * sl, c_hi = c_lo + sl;
     const int obase = kDual ? nh * 128 : 0;  // output column of accumulator column 0
     const uint32_t tl = tacc + (static_cast<uint32_t>(q * 32) << 16);
-    float* cp0 = g.colpart[0] ? g.colpart[0] + static_cast<size_t>(mb * 4 + q) * g.ldc : nullptr;
-    float* cp1 = g.colpart[1] ? g.colpart[1] + static_cast<size_t>(mb * 4 + q) * g.ldc : nullptr;
     float v[16], x[16];
 
     if constexpr (EPI == kEpiTanh || EPI == kEpiGate || EPI == kEpiPlain) {
@@ -382,8 +382,8 @@ __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tac
             }
             store16(g.out[0], r, c, st);
             store16(g.out[1], r, c, sp);
-            colsum16(x, cp0 + c, lane);
-            colsum16(sp, cp1 + c, lane);
+            colsum16(x, cacc[0][(c - c_lo) >> 4], lane);
+            colsum16(sp, cacc[1][(c - c_lo) >> 4], lane);
         }
     } else {  // kEpiRev: accumulator columns [0, 128) tangent rows (b_u), [128, 256) primal rows (b_h)
         // b_ζ = G∘b_u, b_z = G∘(b_h − 2H∘ζ∘b_u) = G∘b_h − 2H∘u∘b_u with u = G∘ζ, the gated
@@ -404,7 +404,7 @@ __device__ __forceinline__ void row_unit_epilogue(const RowArgs& g, uint32_t tac
             }
             store16(g.out[0], r, oc, v);
             store16(g.out[1], r, oc, bh);
-            colsum16(bh, cp0 + oc, lane);
+            colsum16(bh, cacc[0][(c - c_lo) >> 4], lane);
         }
     }
 }
@@ -519,16 +519,29 @@ __global__ void __launch_bounds__(kRowThreads, 1) row_gemm_kernel(const RowArgs 
         }
         epi_bar();
         const int q = warp & 3, j = (warp - 2) >> 2;
+        double cacc[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};  // column sums of this warp's slice
         int it = 0;
         for (int u = blockIdx.x; u < units; u += gridDim.x, ++it) {
             const int buf = it & 1;
             bar_wait(&acc_full[buf], (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             row_unit_epilogue<EPI>(g, tmem + buf * 256, sdot + buf * 512, sb, sw, kDual ? u / g.nb : u,
-                                   kDual ? u % g.nb : 0, q, j, lane);
+                                   kDual ? u % g.nb : 0, q, j, lane, cacc);
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(&acc_empty[buf])) : "memory");
+        }
+        if (EPI == kEpiTHead || EPI == kEpiRev) {  // one partial row per (CTA, lane quarter); the slice's columns
+            // (a dual CTA always serves the same column half: gridDim.x is even or covers every unit once)
+            const int ncols = kDual ? 128 : g.nb * 128, sl = ncols >> 2, c_lo = j * sl;
+            const int obase = kDual ? (blockIdx.x % g.nb) * 128 : 0;
+            if (lane < 16)
+                for (int ci = 0; ci < (sl >> 4); ++ci)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v)
+                        if (g.colpart[v])
+                            g.colpart[v][static_cast<size_t>(blockIdx.x * 4 + q) * g.ldc + obase + c_lo + 16 * ci +
+                                         lane] = static_cast<float>(cacc[v][ci]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -669,10 +682,12 @@ __global__ void __launch_bounds__(kWgThreads, 1) wgrad_kernel(const __grid_const
 // X image rows [0, rows_p): Δ rows, then the zero row (D(0) term), zeros after;
 // one thread per (row, 8-column group).
 __global__ void pack_input_kernel(const float* __restrict__ delta, int B, int ld, int din, int rows_p, Img X) {
+    // consecutive threads = consecutive rows of one 8-column group: a warp's 16-B
+    // stores fill 512 contiguous bytes of the column-group-major image
     const int groups = X.cols_p >> 3;
     const long long t = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
     if (t >= static_cast<long long>(rows_p) * groups) return;
-    const int r = static_cast<int>(t / groups), c0 = static_cast<int>(t % groups) * 8;
+    const int r = static_cast<int>(t % rows_p), c0 = static_cast<int>(t / rows_p) * 8;
     float v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -720,7 +735,7 @@ __global__ void pack_weights_kernel(WPack P) {
 // All fixed-order gradient reductions in one launch (blockIdx.y = job):
 //   jobs 0-2: grad_W[i * out + o] = Σ_s part[s][i][o] (f64; four interleaved
 //             partial sums combined in a fixed order), one thread per element;
-//   jobs 3-6: out[j] = Σ_rows colpart[row][j], 32 columns per block.
+//   (the column sums of the bias / w4 gradients: colsum_reduce_kernel).
 struct RedJobs {
     const float* part[3];
     int splits[3], a_cols[3], n_in[3];
@@ -744,22 +759,34 @@ __global__ void __launch_bounds__(256) grad_reduce_kernel(const RedJobs J) {
             for (int u = 0; u < 4; ++u) s[u] += p[(k + u) * st];
         for (; k < J.splits[job]; ++k) s[0] += p[k * st];
         J.gW[job][t] = static_cast<float>((s[0] + s[1]) + (s[2] + s[3]));
-    } else {  // 32 columns per block: lanes = columns (coalesced rows), warps = row strides
-        __shared__ double red[8][32];
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, j = blockIdx.x * 32 + lane;
-        if (blockIdx.x * 32 >= J.n_out) return;
-        double s = 0.0;
-        if (j < J.n_out)
-            for (int r = w; r < J.cp_rows; r += 8) s += J.cp[job - 3][static_cast<size_t>(r) * J.ldc + j];
-        red[w][lane] = s;
-        __syncthreads();
-        if (w == 0 && j < J.n_out) {
-            double t = 0.0;
-            for (int k = 0; k < 8; ++k) t += red[k][lane];
-            J.cout[job - 3][j] = static_cast<float>(t);
-        }
     }
 }
+
+// Column sums out[j] = Σ_rows colpart[row][j] (blockIdx.y = vector): 32 columns per
+// 1024-thread block, lanes = columns (coalesced rows), 32 warps = row strides, four
+// interleaved f64 accumulators per thread; fixed-order combination.
+__global__ void __launch_bounds__(1024) colsum_reduce_kernel(const RedJobs J) {
+    __shared__ double red[32][33];
+    const int v = blockIdx.y;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, j = blockIdx.x * 32 + lane;
+    double s[4] = {0.0, 0.0, 0.0, 0.0};
+    if (j < J.n_out) {
+        const float* c = J.cp[v] + j;
+        int r = w;
+        for (; r + 96 < J.cp_rows; r += 128)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s[u] += c[static_cast<size_t>(r + 32 * u) * J.ldc];
+        for (; r < J.cp_rows; r += 32) s[0] += c[static_cast<size_t>(r) * J.ldc];
+    }
+    red[w][lane] = (s[0] + s[1]) + (s[2] + s[3]);
+    __syncthreads();
+    if (w == 0 && j < J.n_out) {
+        double t = 0.0;
+        for (int k = 0; k < 32; ++k) t += red[k][lane];
+        J.cout[v][j] = static_cast<float>(t);
+    }
+}
+
 
 // Row reductions of the loss terms and the head-bias gradient, fixed order:
 // block b sums rows [b R / nb, (b + 1) R / nb) into part[b] = {Σ lrow, Σ prow, Σ b_z4};
@@ -1041,6 +1068,10 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
           *gb2 = g + t->o2 + static_cast<long long>(H) * H, *gw4 = g + t->o3, *gb4 = g + t->o3 + H;
     const int Hp = t->Hp, Dp = t->Dp;
 
+    // per-(CTA, lane quarter) column-sum partials: rows a kernel's grid does not reach stay 0
+    const int cp_rows = std::min(tiles * 2, g_sms) * 4;
+    for (int k = 0; k < 4; ++k)
+        ckc(cudaMemsetAsync(t->colpart[k], 0, static_cast<size_t>(cp_rows) * Hp * sizeof(float), s), "colpart");
     {
         const long long n = static_cast<long long>(rows_p) * (Dp >> 3);
         pack_input_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s>>>(delta, B, ld, din, rows_p, t->X);
@@ -1145,10 +1176,10 @@ void loss_and_grad(msk_disc_trainer* t, const float* delta, int B, int ld, cudaS
         }
         J.s_cols = Hp;
         J.n_out = H;
-        J.cp_rows = tiles * 4;
+        J.cp_rows = cp_rows;  // CTAs of the widest (dual) row GEMM x 4 lane quarters
         J.ldc = Hp;
-        const int bx = std::max((std::max(din, H) * H + 255) / 256, (H + 31) / 32);
-        grad_reduce_kernel<<<dim3(bx, 7), 256, 0, s>>>(J);
+        grad_reduce_kernel<<<dim3((std::max(din, H) * H + 255) / 256, 3), 256, 0, s>>>(J);
+        colsum_reduce_kernel<<<dim3((H + 31) / 32, 4), 1024, 0, s>>>(J);
     }
     const int lb = std::min(kLossBlocks, R);
     loss_part_kernel<<<lb, 256, 0, s>>>(t->lrow, t->prow, t->vh, R, t->lpart);
@@ -1238,7 +1269,7 @@ int msk_disc_trainer_create(int32_t n_in, int32_t hidden, const double* theta, i
         t->prow = talloc<double>(t, rows_p);
         t->loss = talloc<double>(t, 3);
         t->lpart = talloc<double>(t, 3 * kLossBlocks);
-        for (int k = 0; k < 4; ++k) t->colpart[k] = talloc<float>(t, static_cast<size_t>(tiles) * 4 * Hp);
+        for (int k = 0; k < 4; ++k) t->colpart[k] = talloc<float>(t, static_cast<size_t>(std::max(tiles, 148) * 2) * 4 * Hp);
         const int total = 2 * ((max_rows + 1 + kWgRows - 1) / kWgRows);
         for (int l = 0; l < 3; ++l) {
             t->splits[l] = wg_splits(Hp >> 7, total);
