@@ -21,7 +21,8 @@ for f in "$tmp"/*.cu; do
   nvcc $ARCH -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -I$JSON_INC -Iinclude "$@" -c "$f" -o "${f%.cu}.o"
   objs+=("${f%.cu}.o")
 done
-g++ -std=c++17 -O2 -fPIC -I$JSON_INC -c "$tmp/model.cpp" -o "$tmp/model_cpp.o"
+defs=(); for a in "$@"; do case "$a" in -D*) defs+=("$a");; esac; done  # -D flags also reach the host TU
+g++ -std=c++17 -O2 -fPIC -I$JSON_INC "${defs[@]}" -c "$tmp/model.cpp" -o "$tmp/model_cpp.o"
 nvcc $ARCH -shared -o variants/$name.so "${objs[@]}" "$tmp/model_cpp.o" -lcudart -ldl
 rm -rf "$tmp"
 echo "built variants/$name.so"
