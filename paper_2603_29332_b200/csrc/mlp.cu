@@ -35,8 +35,12 @@ constexpr int kABytes = kGemmBM * kGemmBK * 2;  // 16 KB
 constexpr int kWBytes = kGemmBN * kGemmBK * 2;  // 32 KB
 // warp 0: TMA producer, warp 1: MMA issuer, warps 2-9: epilogue (two warps per
 // TMEM lane quarter, each converting one 128-column half of the tile)
-constexpr int kGemmThreads = 320;
-constexpr int kEpiWarps = (kGemmThreads - 64) / 32;
+#ifndef MSK_GEMM_EPIW
+#define MSK_GEMM_EPIW 8  // epilogue warps: 4 x (column slices per TMEM lane quarter)
+#endif
+constexpr int kEpiWarps = MSK_GEMM_EPIW;
+constexpr int kGemmThreads = 64 + 32 * kEpiWarps;
+constexpr int kEpiSlices = kEpiWarps / 4;
 
 __host__ __device__ constexpr uint32_t blk_off(int r, int k) {  // inside a (rows x 64) block
     return static_cast<uint32_t>(((r >> 3) * 8 + (k >> 3)) * 128 + (r & 7) * 16 + (k & 7) * 2);
@@ -277,7 +281,7 @@ __device__ __forceinline__ void gemm_epilogue(const GemmArgs& g, uint32_t tmem, 
     }
     void* oa = out_a ? out_a : g.out_a;
     const int q = warp & 3, r = q * 32 + lane, m = mb * kGemmBM + r;
-    const int c_lo = ((warp - 2) / 4) * (kGemmBN / 2), c_hi = c_lo + kGemmBN / 2;
+    const int c_lo = ((warp - 2) / 4) * (kGemmBN / kEpiSlices), c_hi = c_lo + kGemmBN / kEpiSlices;
     int lds = 0;
     const float* sp = epi_src<EPI>(g, m, lds);
     const int f4 = g.f4_rows;
