@@ -1226,3 +1226,65 @@ def test_env_vectorised_step_kernel_parity(ne):
                        env={**os.environ, "MSK_NE": str(ne)}, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "smoke wb700" in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,q0", [("pendulum1_m2", [1.5707963267948966]), ("arm2_m6", [1.2, -0.7])])
+def test_passive_chain_energy_drift_on_device(assets, tmp_path, name, q0):
+    """SURVEY §4 property test on the GPU kernels: a passive, undamped, contact-free
+    chain (fibres slack, zero excitation) conserves mechanical energy within 2 % of
+    m g d over 10 s of device stepping; the energy is evaluated
+    by the oracle's mechanical_energy on the device's f64 states."""
+    import json
+    import math
+
+    import torch
+
+    import paper_2603_29332_b200 as pk
+    from oracle import oracle as om
+
+    mp, cp = model_paths(name)
+    js = json.load(open(mp))
+    for j in js["joints"]:
+        j["damping"] = 0.0
+        j["limits"] = [-100.0, 100.0]
+    for mu in js["muscles"]:  # no passive stretch: keep fibres slack
+        mu["tendon_slack"] = 10.0
+    p = tmp_path / "passive.json"
+    p.write_text(json.dumps(js))
+    m = om.OracleModel(str(p))
+    n = 2
+    g = pk.EnvBatch(str(p), cp, n, cfg=pk.EnvConfig(episode_horizon=100000, rsi=False))
+    g.set_eval_mode(True)
+    g.reset()
+    s = g.get_state()
+    q = torch.tensor([q0] * n, dtype=torch.float64, device=g.device)
+    s.update(q=q, dq=torch.zeros_like(q), act=torch.zeros_like(s["act"]), l_m=torch.full_like(s["l_m"], 0.01),
+             v_m=torch.zeros_like(s["v_m"]), f_m=torch.zeros_like(s["f_m"]))
+    g.set_state(s)
+    e0 = m.mechanical_energy(np.array(q0), np.zeros(len(q0)))
+    scale = sum(m.d["link_mass"][i] * 9.81 * abs(m.d["link_com"][i]) for i in range(len(q0)))
+    a = torch.zeros(n, g.nm, device=g.device)
+    worst = 0.0
+    for k in range(500):  # 10 s of control steps
+        out = g.step(a)
+        if k % 10 == 9:
+            st = gpu_state(g)
+            assert not np.any(to_np_flags(out) & pk.FLAG_DONE), k
+            for e in range(n):
+                worst = max(worst, abs(m.mechanical_energy(st["q"][e], st["dq"][e]) - e0) / scale)
+    # the reference's semi-implicit integrator itself drifts on the (chaotic) double
+    # pendulum: bound the device by the oracle's own drift over the same 10 s
+    st = dict(q=np.array(q0), dq=np.zeros(len(q0)), act=np.zeros(m.nm), l_m=np.full(m.nm, 0.01),
+              v_m=np.zeros(m.nm), f_m=np.zeros(m.nm))
+    ref_worst = 0.0
+    for _ in range(5000):
+        st, _, bad = m.substep(st["q"], st["dq"], st["act"], st["l_m"], st["v_m"], st["f_m"], np.zeros(m.nm))
+        assert not bad
+        ref_worst = max(ref_worst, abs(m.mechanical_energy(st["q"], st["dq"]) - e0) / scale)
+    assert math.isfinite(worst) and worst < max(0.02, 1.5 * ref_worst), (worst, ref_worst)
+    g.close()
+
+
+def to_np_flags(out):
+    return out["flags"].cpu().numpy()
