@@ -172,6 +172,48 @@ def summarize_clocks(lines, t0=None, t1=None):
 
 
 # ----------------------------------------------------------------------------
+def host_link_bound(dev, h2d_bytes, d2h_bytes, envs, step_ms, e2e_value):
+    """The e2e loop's own ceiling: one step's pinned H2D and D2H copies timed
+    alone (CUDA events, best of 5, directions concurrent on two streams as in
+    the pipelined loop) next to the device step; `frac` = e2e / that bound."""
+    import torch
+
+    hi = torch.empty(h2d_bytes, dtype=torch.uint8, pin_memory=True)
+    hd = torch.empty(h2d_bytes, dtype=torch.uint8, device=dev)
+    ho = torch.empty(d2h_bytes, dtype=torch.uint8, pin_memory=True)
+    do = torch.empty(d2h_bytes, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(s, dst, src):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            dst.copy_(src, non_blocking=True)
+            e1.record(s)
+        return e0, e1
+
+    best = [1e30, 1e30, 1e30]
+    for _ in range(6):
+        torch.cuda.synchronize(dev)
+        a = timed(s1, hd, hi)
+        torch.cuda.synchronize(dev)
+        b = timed(s2, ho, do)
+        torch.cuda.synchronize(dev)
+        c = timed(s1, hd, hi), timed(s2, ho, do)  # both directions at once
+        torch.cuda.synchronize(dev)
+        best[0] = min(best[0], a[0].elapsed_time(a[1]))
+        best[1] = min(best[1], b[0].elapsed_time(b[1]))
+        best[2] = min(best[2], max(c[0][0].elapsed_time(c[0][1]), c[1][0].elapsed_time(c[1][1])))
+    h2d_ms, d2h_ms, both_ms = best
+    bound_ms = max(both_ms, step_ms)
+    bound = envs / (bound_ms * 1e-3)
+    return {"h2d_gbs": h2d_bytes / (h2d_ms * 1e6), "d2h_gbs": d2h_bytes / (d2h_ms * 1e6),
+            "duplex_ms": both_ms, "step_ms": step_ms,
+            "bound": bound, "frac": e2e_value / bound,
+            "note": "e2e ceiling = envs / max(one step's H2D+D2H copies run concurrently, device step); "
+                    "pinned copies timed alone with CUDA events"}
+
+
 def cpu_model():
     """Host CPU model name and logical core count (for the CPU-arm lines)."""
     name = "unknown"
@@ -559,6 +601,7 @@ def main():
                "api": f"msk_gpu_step_host_async/host_wait, {groups} env groups of {eg}"}
         for ge in envs_e:
             ge.close()
+        e2e["link"] = host_link_bound(dev, e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"], E * world, ms / args.steps, e2e["value"])
 
     disc = None
     if C["disc"]:  # the tensor-core kernel alone on this step's Δ (for its own roofline)
