@@ -200,6 +200,76 @@ void grow_outcome_ring(msk_gpu_ctx* ctx, int cap, cudaStream_t s) {
 
 int align16(int x) { return (x + 15) & ~15; }
 
+// Balanced joint-torque sums.  The moment slots of joint j (fixed (muscle,
+// segment) order, CompiledModel::joint_slot_start) are cut into pieces of at most
+// ceil(n_pairs / G) consecutive slots; pieces go to the G lanes longest first
+// (each to the least-loaded lane), and a lane's pieces are laid out as one list:
+// element i of lane l lives in slot i G + l, so every lane sums its list with
+// conflict-free shared loads and stores a piece's partial sum at the piece's last
+// element (flag = piece id).  A joint's torque is then the sum of its pieces in
+// piece order — a fixed summation order, like the joint-major loop it replaces,
+// with max-over-lanes work ~n_pairs / G instead of the largest joints' slot counts.
+struct TorquePlan {
+    std::vector<int> slot_new;      // old slot (0..n_pairs, n_pairs = dummy) -> new slot
+    std::vector<uint8_t> flag;      // len * G: piece id ending at that element, else 0xff
+    std::vector<uint8_t> piece0;    // nj + 1: pieces of joint j = [piece0[j], piece0[j+1])
+    int len = 0, n_pieces = 0;
+};
+
+TorquePlan plan_torques(const CompiledModel& c, int G) {
+    TorquePlan P;
+    const int np = c.n_pairs;
+    // piece size: ~n_pairs / G, grown until the partial sums fit the frame scratch
+    // (one f64 per 8 B: 2 per link; one piece per joint fits since n_joints <= n_links)
+    int cap = std::max(1, (np + G - 1) / G);
+    auto count = [&](int cp) {
+        int n = 0;
+        for (int j = 0; j < c.nj; ++j) n += (c.joint_slot_start[j + 1] - c.joint_slot_start[j] + cp - 1) / cp;
+        return n;
+    };
+    const int lim = std::min(2 * c.nl, 255);
+    while (count(cap) > lim && cap < np) ++cap;
+    if (count(cap) > lim) throw ConfigError("model too large: more than 255 joints with muscle moments");
+    struct Piece { int joint, s0, n; };
+    std::vector<Piece> pieces;
+    P.piece0.assign(c.nj + 1, 0);
+    for (int j = 0; j < c.nj; ++j) {
+        P.piece0[j] = static_cast<uint8_t>(pieces.size());
+        const int a = c.joint_slot_start[j], b = c.joint_slot_start[j + 1], n = b - a;
+        const int k = (n + cap - 1) / cap;
+        for (int q = 0; q < k; ++q) {
+            const int lo = a + static_cast<int>(static_cast<long>(n) * q / k);
+            const int hi = a + static_cast<int>(static_cast<long>(n) * (q + 1) / k);
+            pieces.push_back({j, lo, hi - lo});
+        }
+    }
+    P.piece0[c.nj] = static_cast<uint8_t>(pieces.size());
+    P.n_pieces = static_cast<int>(pieces.size());
+    std::vector<int> order(pieces.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return pieces[x].n > pieces[y].n; });
+    std::vector<std::vector<int>> lane(G);
+    std::vector<int> load(G, 0);
+    for (int id : order) {
+        const int l = static_cast<int>(std::min_element(load.begin(), load.end()) - load.begin());
+        lane[l].push_back(id);
+        load[l] += pieces[id].n;
+    }
+    P.len = std::max(1, *std::max_element(load.begin(), load.end()));
+    P.slot_new.assign(np + 1, 0);
+    P.flag.assign(static_cast<size_t>(P.len) * G, 0xff);
+    for (int l = 0; l < G; ++l) {
+        int i = 0;
+        for (int id : lane[l]) {
+            const Piece& pc = pieces[id];
+            for (int t = 0; t < pc.n; ++t, ++i) P.slot_new[pc.s0 + t] = i * G + l;
+            if (pc.n > 0) P.flag[static_cast<size_t>(i - 1) * G + l] = static_cast<uint8_t>(id);
+        }
+    }
+    P.slot_new[np] = P.len * G;  // dummy slot after the lists
+    return P;
+}
+
 }  // namespace
 
 extern "C" {
@@ -267,6 +337,11 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.c_c = c.c_c;
         M.c_mu = c.c_mu;
         M.inv_c_vs = c.inv_c_vs;
+        const TorquePlan tq = plan_torques(c, lanes_per_env());
+        M.tq_len = tq.len;
+        M.n_pairs = tq.len * lanes_per_env();  // slots incl. the lists' padding; dummy slot = n_pairs
+        std::vector<float4> p0h, kfh;  // host copies for the chunk-major fast-path table
+        std::vector<double2> p1ah, p1bh;
         {
             std::vector<float4> la(c.nl), sp(c.ns);
             for (int l = 0; l < c.nl; ++l) la[l] = make_float4(c.link_ax[l], c.link_az[l], c.link_com[l], c.link_mass[l]);
@@ -297,14 +372,20 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
                     k2 = static_cast<float>(ax * cx + az * cz);
                     k3 = static_cast<float>(az * cx - ax * cz);
                 }
+                // kinds 0/1 carry a moment slot (remapped to the torque lists), kind 2 a via index
+                const int info_new = kind == 2 ? info : (info & 0x7ff) | (tq.slot_new[info >> 11] << 11);
                 float w;
-                std::memcpy(&w, &info, sizeof w);
+                std::memcpy(&w, &info_new, sizeof w);
                 kf[i] = make_float4(k1, k2, k3, w);
             }
             M.m_p0 = ctx->upload(p0);
             M.m_p1a = ctx->upload(p1a);
             M.m_p1b = ctx->upload(p1b);
             M.seg_kf = ctx->upload(kf);
+            p0h = std::move(p0);
+            p1ah = std::move(p1a);
+            p1bh = std::move(p1b);
+            kfh = std::move(kf);
         }
         M.max_seg = c.max_seg;
         M.has_general = c.has_general;
@@ -329,6 +410,26 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
                 M.seg_run[k] = k == 5 ? nf : m;
             }
             M.seg_run[0] = 0;
+            // chunk-major record table of the fast range (device.cuh mtab)
+            std::vector<unsigned char> tab;
+            const size_t fb = static_cast<size_t>(G) * 16;
+            for (int k = 0; k <= 4; ++k) {
+                M.mrun_off[k] = static_cast<int>(tab.size());
+                for (int m0 = M.seg_run[k]; m0 < M.seg_run[k + 1]; m0 += G) {
+                    const size_t r0 = tab.size();
+                    tab.resize(r0 + (3 + k) * fb, 0);
+                    for (int i = 0; i < G && m0 + i < nf; ++i) {
+                        const int m = m0 + i;
+                        unsigned char* e = tab.data() + r0 + 16 * i;
+                        std::memcpy(e, &p0h[m], 16);
+                        std::memcpy(e + fb, &p1ah[m], 16);
+                        std::memcpy(e + 2 * fb, &p1bh[m], 16);
+                        for (int g = 0; g < k; ++g) std::memcpy(e + (3 + g) * fb, &kfh[static_cast<size_t>(g) * c.nm + m], 16);
+                    }
+                }
+            }
+            if (tab.empty()) tab.resize(16, 0);
+            M.mtab = ctx->upload(tab);
         }
         M.link_parent = ctx->upload(c.link_parent);
         M.link_dof = ctx->upload(c.link_dof);
@@ -353,7 +454,11 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.via_z = ctx->upload(c.via_z);
         M.pair_joint = ctx->upload(c.pair_joint);
         M.pair_via = ctx->upload(c.pair_via);
-        M.pair_slot = ctx->upload(c.pair_slot);
+        {
+            std::vector<int32_t> ps(c.pair_slot.size());
+            for (size_t i = 0; i < ps.size(); ++i) ps[i] = tq.slot_new[c.pair_slot[i]];
+            M.pair_slot = ctx->upload(ps);
+        }
         M.pair_sign = ctx->upload(c.pair_sign);
         M.key_bodies = ctx->upload(c.key_bodies);
         M.clip_q = ctx->upload(clip.q);
@@ -386,7 +491,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         M.off_root = off;
         off = align16(off + 16);
         M.off_union = off;
-        off = align16(off + 4 * std::max({c.n_pairs + 1, kLinkStride * c.nl, 2 * c.nq}));  // +1: dummy slot
+        off = align16(off + 4 * std::max({M.n_pairs + 1, kLinkStride * c.nl, 2 * c.nq}));  // +1: dummy slot
         M.off_kind = off;  // f64 link frames, only for models with general muscle segments
         if (c.has_general) off = align16(off + 32 * c.nl);
         M.off_pen = off;  // contact-sphere penetrations
@@ -411,6 +516,10 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             t = align16(t);
             M.tab_off_work = t;  // per (level, slot < 32) work words of the tree passes
             t += 4 * 32 * c.n_levels;
+            M.tab_off_tq = t;  // joint-torque lists: piece flags, then pieces per joint
+            t += static_cast<int>(tq.flag.size());
+            M.tab_off_tqp = t;
+            t += c.nj + 1;
             M.tab_bytes = align16(t);
             std::vector<unsigned char> blob(M.tab_bytes, 0);
             auto put = [&](int at, const void* src, size_t n) { std::memcpy(blob.data() + at, src, n); };
@@ -451,6 +560,8 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
                     put(M.tab_off_work + 4 * (32 * d + i), &w, 4);
                 }
             }
+            put(M.tab_off_tq, tq.flag.data(), tq.flag.size());
+            put(M.tab_off_tqp, tq.piece0.data(), tq.piece0.size());
             M.tab_blob = reinterpret_cast<const int4*>(ctx->upload(blob));
         }
         // as many env slots per block as shared memory allows (28 for the whole-body models)

@@ -55,6 +55,12 @@ struct DevModel {
     int seg_run[6];        // [k, k+1): muscles (whole lane-group chunks) padded to k segments, k = 0..4
     int fast_nseg;         // NSEG of the fast path (0: the generic loop over all muscles)
     int gen0;              // first muscle (device order) of the generic loop: general muscles (or 0, or nm)
+    // Fast-path muscle constants, chunk-major: one record per lane-group chunk of the
+    // fast range with (3 + k) fields of G x 16 B each — p0 | p1a | p1b | K of segment
+    // 0..k-1 — for a chunk of run k; lane i's entry of field f at f G 16 + 16 i, so
+    // one chunk pointer serves every load of a muscle (immediate offsets).
+    const unsigned char* mtab;
+    int mrun_off[5];       // byte offset of run k's first chunk record
     // Same-link / adjacent segment k of muscle m at [k * nm + m] (coalesced over m):
     // {K1, K2h, K3h, info bits} with |s|^2 = K1 + 2 (cos K2h + sin K3h) and
     // r x A = cos K3h - sin K2h (cos/sin of the child joint's own angle, f64).
@@ -87,6 +93,8 @@ struct DevModel {
     // block-shared tree table at the head of dynamic smem (bytes)
     const int4* tab_blob;
     int tab_bytes, tab_off_a, tab_off_in, tab_off_meta, tab_off_child, tab_off_lvl, tab_off_lvs, tab_off_work;
+    int tab_off_tq, tab_off_tqp;  // joint-torque lists (capi.cu plan_torques): u8 flags [tq_len][G], u8 pieces [nj+1]
+    int tq_len;                   // elements per lane of the joint-torque lists
 };
 
 // Per-env mutable state (device pointers, env-major rows).

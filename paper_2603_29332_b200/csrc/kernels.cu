@@ -73,6 +73,8 @@ struct EnvSmem {
     const uint8_t* tlvl;   // links grouped by depth
     const uint8_t* tlvs;   // level starts
     const uint32_t* twork; // [level][32] work words (see capi.cu): link, parent, children, sphere flag
+    const uint8_t* tqf;    // [tq_len][G] joint-torque list flags: piece id ending at the element, else 0xff
+    const uint8_t* tqp;    // nj + 1: pieces of joint j = [tqp[j], tqp[j+1])
     int G;                 // lanes per env (32 or 16)
     unsigned hm;           // mask of this env's lanes
 };
@@ -121,6 +123,8 @@ __device__ __forceinline__ EnvSmem carve(unsigned char* smem, int slot, const De
     s.tlvl = smem + M.tab_off_lvl;
     s.tlvs = smem + M.tab_off_lvs;
     s.twork = reinterpret_cast<const uint32_t*>(smem + M.tab_off_work);
+    s.tqf = smem + M.tab_off_tq;
+    s.tqp = smem + M.tab_off_tqp;
     return s;
 }
 
@@ -731,20 +735,29 @@ __device__ __forceinline__ MuscleRows muscle_rows(const DevState& St, const floa
     return MuscleRows{act_row, St.act + mb, St.lm + mb, St.vm + mb, St.fm + mb};
 }
 
+// activation_step (muscle.cpp:42-56), fibre kinematics and the Hill force: the
+// new activation a1, fibre length lm1 and velocity vm; returns F.
+__device__ __forceinline__ float muscle_force(float4 p0, double2 pa, double2 pb, float u, float a0, double lm0,
+                                              double L, float& a1, double& lm1, float& vm) {
+    const float gain = fmaf(1.5f, a0, 0.5f);
+    const float ex = ex2_ftz(u > a0 ? p0.y * rcp_ftz(gain) : p0.z * gain);  // p0.y/z carry log2(e)
+    a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
+    const double prev_len = fma(lm0, pa.y, pa.x);
+    vm = static_cast<float>((L - prev_len) * pb.y);
+    lm1 = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
+#ifdef MSK_F64_HILL
+    return mtu_force_d(a1, lm1, (L - prev_len) * pb.y, p0.x);
+#else
+    return mtu_force(a1, static_cast<float>(lm1), vm, p0.x);
+#endif
+}
+
 __device__ __forceinline__ float muscle_update(const MuscleRows& R, int m, int ext, float4 p0, double2 pa,
                                                double2 pb, float u, float a0, double lm0, double L, float* pw,
                                                bool last) {
-    const float gain = fmaf(1.5f, a0, 0.5f);
-    const float ex = ex2_ftz(u > a0 ? p0.y * rcp_ftz(gain) : p0.z * gain);  // p0.y/z carry log2(e)
-    const float a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
-    const double prev_len = fma(lm0, pa.y, pa.x);
-    const float vm = static_cast<float>((L - prev_len) * pb.y);
-    const double lm1 = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
-#ifdef MSK_F64_HILL
-    const float F = mtu_force_d(a1, lm1, (L - prev_len) * pb.y, p0.x);
-#else
-    const float F = mtu_force(a1, static_cast<float>(lm1), vm, p0.x);
-#endif
+    float a1, vm;
+    double lm1;
+    const float F = muscle_force(p0, pa, pb, u, a0, lm0, L, a1, lm1, vm);
     R.act[m] = a1;
     R.lm[m] = lm1;
     if (last) {
@@ -755,42 +768,52 @@ __device__ __forceinline__ float muscle_update(const MuscleRows& R, int m, int e
     return F;
 }
 
-// Inputs of one muscle for the fast path (all loads issued before any math).
-// One muscle of a chunk whose muscles all have (at most) NS segments — NS is
-// a compile-time constant: the segment loop unrolls without predicates (padding
-// segments have K = 0 and write the dummy slot) and the per-segment smem
-// address arithmetic is shared.
-template <int NS>
-__device__ __forceinline__ void muscle_one(const DevModel& M, const MuscleRows& R, const EnvSmem& S, float* pw, int m,
-                                           bool last) {
-    const int nm = M.nm;
-    float4 kc[NS > 0 ? NS : 1];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) kc[k] = ldc4(M.seg_kf + k * nm + m);
-    const float4 p0 = ldc4(M.m_p0 + m);  // f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10
-    const double2 pa = ldc2d(M.m_p1a + m), pb = ldc2d(M.m_p1b + m);
-    const float u = R.u[m];  // clamped, device order (prep_actions_kernel)
-    const float a0 = R.act[m];
-    const double lm0 = R.lm[m];
-    const int ext = pw ? (__ldg(M.m_meta + m) >> 9) : 0;  // reference index: power output only
-    double L = 0.0;
-    float tq[NS > 0 ? NS : 1];
-#pragma unroll
-    for (int k = 0; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
-    const float F = muscle_update(R, m, ext, p0, pa, pb, u, a0, lm0, L, pw, last);
-#pragma unroll
-    for (int k = 0; k < NS; ++k) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
-}
-
-// Muscles [m0, m1) (whole chunks of the lane group, muscles sorted by segment
-// count) with NS segments each.
-template <int NS>
+// Fast path: the muscles [m0, m1) of run NS (whole chunks of the lane group,
+// muscles sorted by segment count), NS segments each — a compile-time count, so
+// the segment loop unrolls without predicates (padding segments have K = 0 and
+// write the dummy slot).  Every constant of a muscle comes from its chunk record
+// (M.mtab: one pointer, immediate field offsets) and the env's muscle rows
+// advance by pointer increments; the power accumulation is compiled in only when
+// requested (kPow), not predicated per muscle.
+template <int NS, bool kPow, int G>
 __device__ __forceinline__ void muscle_run(const DevModel& M, const DevState& St, const EnvSmem& S,
                                            const float* act_row, size_t mb, float* pw, int lane, bool last, int m0,
                                            int m1) {
-    if (m0 + lane >= m1) return;
-    const MuscleRows R = muscle_rows(St, act_row, mb);
-    for (int m = m0 + lane; m < m1; m += S.G) muscle_one<NS>(M, R, S, pw, m, last);
+    int m = m0 + lane;
+    if (m >= m1) return;
+    constexpr int kField = G * 16, kRec = (3 + NS) * kField;
+    const unsigned char* rec = M.mtab + M.mrun_off[NS] + 16 * lane;
+    const float* up = act_row + m;
+    float* ap = St.act + mb + m;
+    double* lp = St.lm + mb + m;
+    for (; m < m1; m += G, rec += kRec, up += G, ap += G, lp += G) {
+        float4 kc[NS > 0 ? NS : 1];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) kc[k] = ldc4(reinterpret_cast<const float4*>(rec + (3 + k) * kField));
+        // {f_max, -dt/tau_act log2e, -dt/tau_deact log2e, l_opt v_max/10}, {slack, l_opt}, {1/l_opt, 1/(dt l_opt v_max)}
+        const float4 p0 = ldc4(reinterpret_cast<const float4*>(rec));
+        const double2 pa = ldc2d(reinterpret_cast<const double2*>(rec + kField));
+        const double2 pb = ldc2d(reinterpret_cast<const double2*>(rec + 2 * kField));
+        const float u = *up;  // clamped, device order (prep_actions_kernel)
+        const float a0 = *ap;
+        const double lm0 = *lp;
+        double L = 0.0;
+        float tq[NS > 0 ? NS : 1];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
+        float a1, vm;
+        double lm1;
+        const float F = muscle_force(p0, pa, pb, u, a0, lm0, L, a1, lm1, vm);
+        *ap = a1;
+        *lp = lm1;
+        if (last) {
+            St.vm[mb + m] = vm;
+            St.fm[mb + m] = F;
+        }
+        if constexpr (kPow) pw[__ldg(M.m_meta + m) >> 9] += fabsf(F * vm * p0.w);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) S.un[__float_as_int(kc[k].w) >> 11] = -F * tq[k];
+    }
 }
 
 // Muscles [m_begin, nm) through the generic per-segment loop (general segments
@@ -828,21 +851,72 @@ __device__ __forceinline__ void muscle_generic(const DevModel& M, const DevState
     }
 }
 
-template <int NSEG>
+template <int NSEG, bool kPow, int G>
+__device__ __forceinline__ void muscle_runs(const DevModel& M, const DevState& St, const EnvSmem& S,
+                                            const float* act_row, size_t mb, float* pw, int lane, bool last) {
+    // runs of chunks by padded segment count (M.seg_run, muscle units): 0, 1, ..., NSEG,
+    // over the muscles without a general segment
+    muscle_run<0, kPow, G>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[0], M.seg_run[1]);
+    if constexpr (NSEG >= 1) muscle_run<1, kPow, G>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[1], M.seg_run[2]);
+    if constexpr (NSEG >= 2) muscle_run<2, kPow, G>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[2], M.seg_run[3]);
+    if constexpr (NSEG >= 3) muscle_run<3, kPow, G>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[3], M.seg_run[4]);
+    if constexpr (NSEG >= 4) muscle_run<4, kPow, G>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[4], M.seg_run[5]);
+}
+
+template <int NSEG, int G = 32>
 __device__ __forceinline__ void muscle_phase(const DevModel& M, const DevState& St, const EnvSmem& S,
                                              const float* act_row, size_t mb, float* pw, int lane, bool last) {
     if constexpr (NSEG > 0) {
-        // runs of chunks by padded segment count (M.seg_run, muscle units): 0, 1, ..., NSEG,
-        // over the muscles without a general segment; general muscles follow from M.gen0
-        muscle_run<0>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[0], M.seg_run[1]);
-        if constexpr (NSEG >= 1) muscle_run<1>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[1], M.seg_run[2]);
-        if constexpr (NSEG >= 2) muscle_run<2>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[2], M.seg_run[3]);
-        if constexpr (NSEG >= 3) muscle_run<3>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[3], M.seg_run[4]);
-        if constexpr (NSEG >= 4) muscle_run<4>(M, St, S, act_row, mb, pw, lane, last, M.seg_run[4], M.seg_run[5]);
+        if (pw)
+            muscle_runs<NSEG, true, G>(M, St, S, act_row, mb, pw, lane, last);
+        else
+            muscle_runs<NSEG, false, G>(M, St, S, act_row, mb, pw, lane, last);
+        // general muscles follow from M.gen0
         if (M.gen0 < M.nm) muscle_generic(M, St, S, act_row, mb, pw, lane, last, M.gen0);
     } else {
         muscle_generic(M, St, S, act_row, mb, pw, lane, last, 0);
     }
+}
+
+// Joint torques J_m^T F from the moment slots in a fixed summation order, in two
+// parts (capi.cu plan_torques).  piece_sums: each lane runs down its list of
+// slots (element i at slot i G + lane: conflict-free) and stores every piece's
+// partial sum into the link-frame scratch (frames are dead between the
+// integration and the next tree sweep); joint_torque: a joint's pieces in piece
+// order, then damping and the joint-limit spring (skeleton.cpp:271-290).
+// The sums run in f64 (exact for up to ~2^29 f32 terms of similar magnitude):
+// agonist / antagonist moments cancel, so an f32 chain of ~n_pairs / G terms
+// would round visibly; the joint torque is rounded to f32 once.
+__device__ __forceinline__ void piece_sums(const DevModel& M, const EnvSmem& S, int lane) {
+    double* part = reinterpret_cast<double*>(S.kin);
+    const uint8_t* fl = S.tqf + lane;
+    const float* un = S.un + lane;
+    const int G = S.G, n = M.tq_len;
+    double acc = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < n; ++i) {
+        acc += static_cast<double>(un[i * G]);
+        const int f = fl[i * G];
+        if (f != 0xff) {
+            part[f] = acc;
+            acc = 0.0;
+        }
+    }
+}
+
+__device__ __forceinline__ float joint_torque(const DevModel& M, const EnvSmem& S, int j, double q, double dq) {
+    const double* part = reinterpret_cast<const double*>(S.kin);
+    const int p1 = S.tqp[j + 1];
+    double ts = 0.0;
+    for (int p = S.tqp[j]; p < p1; ++p) ts += part[p];
+    float t = static_cast<float>(ts);
+    t -= __ldg(M.joint_damping + j) * static_cast<float>(dq);
+    const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
+    if (q > hi)
+        t -= static_cast<float>(M.k_lim_d * (q - hi));
+    else if (q < lo)
+        t -= static_cast<float>(M.k_lim_d * (q - lo));
+    return t;
 }
 
 // Articulated-body pass, leaves -> root (per link U = IA e0, D, Schur
@@ -1200,38 +1274,17 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         if (M.has_general) fk_d(M, S, lane);  // f64 world frames of the general segments
 
         // ---- 1. muscles + J_m^T F contributions ----
-        muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane, sub == n_substeps - 1);
+        muscle_phase<NSEG, G>(M, St, S, act_row, mb, pw, lane, sub == n_substeps - 1);
         __syncwarp(S.hm);
 
         PHASE_MARK(0);
         // ---- 2. joint torques: fixed-order slot sums, damping, limits ----
+        piece_sums(M, S, lane);
+        __syncwarp(S.hm);
 #pragma unroll
         for (int k = 0; k < QS; ++k) {
             const int d = lane + S.G * k;
-            if (d >= nrd && d < nq) {
-                const int j = d - nrd;
-                const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
-                float t = 0.0f;
-                {  // fixed-order sum with 4 independent accumulators (latency / 4)
-                    float t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
-                    int s = s0;
-                    for (; s + 3 < s1; s += 4) {
-                        t += S.un[s];
-                        t1 += S.un[s + 1];
-                        t2 += S.un[s + 2];
-                        t3 += S.un[s + 3];
-                    }
-                    for (; s < s1; ++s) t += S.un[s];
-                    t = (t + t1) + (t2 + t3);
-                }
-                t -= __ldg(M.joint_damping + j) * static_cast<float>(dqd[k]);
-                const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
-                if (qd[k] > hi)
-                    t -= static_cast<float>(M.k_lim_d * (qd[k] - hi));
-                else if (qd[k] < lo)
-                    t -= static_cast<float>(M.k_lim_d * (qd[k] - lo));
-                S.tau[d] = t;
-            }
+            if (d >= nrd && d < nq) S.tau[d] = joint_torque(M, S, d - nrd, qd[k], dqd[k]);
         }
         __syncwarp(S.hm);
 
@@ -1354,30 +1407,12 @@ __global__ void __launch_bounds__(WPB * 32, 1) stepq_kernel(DevModel M, DevState
             if (M.has_general) fk_d(M, S, lane);
             muscle_phase<NSEG>(M, St, S, act_row, mb, pw, lane, sub == n_substeps - 1);
             __syncwarp();
+            piece_sums(M, S, lane);  // joint torques: fixed-order slot sums, damping, limits
+            __syncwarp();
 #pragma unroll
-            for (int k = 0; k < QS; ++k) {  // joint torques: fixed-order slot sums, damping, limits
+            for (int k = 0; k < QS; ++k) {
                 const int d = lane + 32 * k;
-                if (d >= nrd && d < nq) {
-                    const int j = d - nrd;
-                    const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
-                    float t = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
-                    int s = s0;
-                    for (; s + 3 < s1; s += 4) {
-                        t += S.un[s];
-                        t1 += S.un[s + 1];
-                        t2 += S.un[s + 2];
-                        t3 += S.un[s + 3];
-                    }
-                    for (; s < s1; ++s) t += S.un[s];
-                    t = (t + t1) + (t2 + t3);
-                    t -= __ldg(M.joint_damping + j) * static_cast<float>(dqd[k]);
-                    const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
-                    if (qd[k] > hi)
-                        t -= static_cast<float>(M.k_lim_d * (qd[k] - hi));
-                    else if (qd[k] < lo)
-                        t -= static_cast<float>(M.k_lim_d * (qd[k] - lo));
-                    S.tau[d] = t;
-                }
+                if (d >= nrd && d < nq) S.tau[d] = joint_torque(M, S, d - nrd, qd[k], dqd[k]);
             }
         }
         group_bar();  // the group's torques and joint states are in shared memory
@@ -1822,33 +1857,14 @@ __global__ void __launch_bounds__(WPB * 32, 1) stepn_kernel(DevModel M, DevState
 
         // ---- 2. joint torques: fixed-order slot sums, damping, limits ----
 #pragma unroll
+        for (int k = 0; k < NE; ++k) piece_sums(M, S[k], lane);
+        __syncwarp();
+#pragma unroll
         for (int kq = 0; kq < QS; ++kq) {
             const int d = lane + 32 * kq;
             if (d >= nrd && d < nq) {
-                const int j = d - nrd;
-                const int s0 = __ldg(M.joint_slot_start + j), s1 = __ldg(M.joint_slot_start + j + 1);
-                const float damp = __ldg(M.joint_damping + j);
-                const double hi = __ldg(M.joint_hi + j), lo = __ldg(M.joint_lo + j);
 #pragma unroll
-                for (int k = 0; k < NE; ++k) {
-                    const float* un = S[k].un;
-                    float t = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
-                    int s = s0;
-                    for (; s + 3 < s1; s += 4) {
-                        t += un[s];
-                        t1 += un[s + 1];
-                        t2 += un[s + 2];
-                        t3 += un[s + 3];
-                    }
-                    for (; s < s1; ++s) t += un[s];
-                    t = (t + t1) + (t2 + t3);
-                    t -= damp * static_cast<float>(dqd[k][kq]);
-                    if (qd[k][kq] > hi)
-                        t -= static_cast<float>(M.k_lim_d * (qd[k][kq] - hi));
-                    else if (qd[k][kq] < lo)
-                        t -= static_cast<float>(M.k_lim_d * (qd[k][kq] - lo));
-                    S[k].tau[d] = t;
-                }
+                for (int k = 0; k < NE; ++k) S[k].tau[d] = joint_torque(M, S[k], d - nrd, qd[k][kq], dqd[k][kq]);
             }
         }
         __syncwarp();
