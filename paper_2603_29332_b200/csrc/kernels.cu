@@ -103,7 +103,13 @@ __device__ __forceinline__ void load_tree_table(unsigned char* smem, const DevMo
         : "memory");
 }
 
-__device__ __forceinline__ EnvSmem carve(unsigned char* smem, int slot, const DevModel& M, int G, unsigned hm) {
+__device__ __forceinline__ EnvSmem carve(unsigned char* smem0, int slot, const DevModel& M, int G, unsigned hm) {
+    // The CTA's shared-window address of the dynamic smem, pinned in a register
+    // (opaque to the optimiser): otherwise, at the 72-register cap, every pass
+    // rematerialises it from SR_CgaCtaId (4 instructions per tree level), +1 %.
+    uint32_t sb = static_cast<uint32_t>(__cvta_generic_to_shared(smem0));
+    asm volatile("" : "+r"(sb));
+    unsigned char* smem = static_cast<unsigned char*>(__cvta_shared_to_generic(sb));
     EnvSmem s;
     s.G = G;
     s.hm = hm;
