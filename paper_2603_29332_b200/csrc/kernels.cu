@@ -141,6 +141,11 @@ __device__ __forceinline__ int ww_child0(uint32_t w) { return static_cast<int>((
 __device__ __forceinline__ int ww_nchild(uint32_t w) { return static_cast<int>((w >> 24) & 0xf); }
 
 // Origin (x, z) half of a link's frame record {cos, sin, x, z}: an 8-B load.
+// During the substeps (tree_sweep<true>) the record holds the origin RELATIVE
+// to the parent's origin instead (R_p anchor): the passes only use differences.
+__device__ __forceinline__ float2 frame_rel(const EnvSmem& S, int l) {
+    return reinterpret_cast<const float2*>(S.kin + l)[1];
+}
 __device__ __forceinline__ float2 frame_origin(const EnvSmem& S, int l) {
     return reinterpret_cast<const float2*>(S.kin + l)[1];
 }
@@ -390,16 +395,17 @@ __device__ __forceinline__ void sweep_link(const DevModel& M, const EnvSmem& S, 
         const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
         if (kSimple || p >= 0) {
             const float4 kp = S.kin[p];
-            ox = fmaf(kp.x, la.x, fmaf(-kp.y, la.y, kp.z));
-            oz = fmaf(kp.y, la.x, fmaf(kp.x, la.y, kp.w));
+            // kFull: origin relative to the parent's (frame_rel); else absolute (root-relative)
+            ox = fmaf(kp.x, la.x, kFull ? -kp.y * la.y : fmaf(-kp.y, la.y, kp.z));
+            oz = fmaf(kp.y, la.x, kFull ? kp.x * la.y : fmaf(kp.x, la.y, kp.w));
             c = fmaf(kp.x, cr, -kp.y * sr);
             s = fmaf(kp.y, cr, kp.x * sr);
             if (kFull) {
                 const float* up = S.un + kLinkStride * p;
                 const float2 wv = reinterpret_cast<const float2*>(up)[5];  // parent (omega, v_x)
                 w = wv.x + S.dqf[dof];
-                vx = fmaf(-wv.x, oz - kp.w, wv.y);
-                vz = fmaf(wv.x, ox - kp.z, up[9]);
+                vx = fmaf(-wv.x, oz, wv.y);
+                vz = fmaf(wv.x, ox, up[9]);
             }
         } else {
             ox = la.x;
@@ -977,8 +983,8 @@ __device__ __forceinline__ void aba_up_link(const DevModel& M, const EnvSmem& S,
     u2[5] = make_float2(U1, U2);
     const int p = ww_parent(ww);
     if (kSimple || p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
-        const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
-        const float dx = ol.x - op.x, dz = ol.y - op.y;
+        const float2 d = frame_rel(S, l);  // origin relative to the parent's
+        const float dx = d.x, dz = d.y;
         const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
         u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
         u2[1] = make_float2(be, a);
@@ -1018,8 +1024,8 @@ __device__ __forceinline__ void aba_down_link(const DevModel& M, const EnvSmem& 
         const float* up = S.un + kLinkStride * p;
         const float2 a01 = reinterpret_cast<const float2*>(up)[0];
         const float a2 = up[2];
-        const float2 ol = frame_origin(S, l), op = frame_origin(S, p);  // positions only
-        const float dx = ol.x - op.x, dz = ol.y - op.y;
+        const float2 d = frame_rel(S, l);  // origin relative to the parent's
+        const float dx = d.x, dz = d.y;
         A0 = a01.x;
         A1 += fmaf(-a01.x, dz, a01.y);
         A2 += fmaf(a01.x, dx, a2);
