@@ -172,6 +172,12 @@ __device__ __forceinline__ float rsqrt_ftz(float x) {
 }
 constexpr float kLog2e = 1.4426950408889634f;
 
+// l_m = std::max((L - slack) / l_opt, kMinFiberLength) (skeleton.cpp:279, 305):
+// std::max's compare-select, NaN in the first argument propagates as there.
+__device__ __forceinline__ double fiber_clamp(double x) {
+    return x < static_cast<double>(kMinFiber) ? static_cast<double>(kMinFiber) : x;
+}
+
 // Read-only model-constant loads (non-coherent path; the tables never change
 // during a launch).
 __device__ __forceinline__ float4 ldc4(const float4* p) { return __ldg(p); }
@@ -659,7 +665,7 @@ __device__ void init_muscles(const DevModel& M, const DevState& St, const EnvSme
     for (int m = lane; m < M.nm; m += S.G) {
         const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
         const double L = muscle_length(M, S, m);
-        const double lm = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
+        const double lm = fiber_clamp((L - pa.x) * pb.x);
         St.act[mb + m] = a0;
         St.lm[mb + m] = lm;
         St.vm[mb + m] = 0.0f;
@@ -756,7 +762,7 @@ __device__ __forceinline__ float muscle_force(float4 p0, double2 pa, double2 pb,
     a1 = fminf(fmaxf(fmaf(a0 - u, ex, u), 0.0f), 1.0f);
     const double prev_len = fma(lm0, pa.y, pa.x);
     vm = static_cast<float>((L - prev_len) * pb.y);
-    lm1 = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
+    lm1 = fiber_clamp((L - pa.x) * pb.x);
 #ifdef MSK_F64_HILL
     return mtu_force_d(a1, lm1, (L - prev_len) * pb.y, p0.x);
 #else
@@ -809,10 +815,13 @@ __device__ __forceinline__ void muscle_run(const DevModel& M, const DevState& St
         const float u = *up;  // clamped, device order (prep_actions_kernel)
         const float a0 = *ap;
         const double lm0 = *lp;
-        double L = 0.0;
         float tq[NS > 0 ? NS : 1];
+        double L = 0.0;
+        if constexpr (NS > 0) {  // (not 0.0 + len: the add cannot be folded under IEEE signed zeros)
+            L = kseg(S, kc[0], __float_as_int(kc[0].w), tq[0]);
 #pragma unroll
-        for (int k = 0; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
+            for (int k = 1; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), tq[k]);
+        }
         float a1, vm;
         double lm1;
         const float F = muscle_force(p0, pa, pb, u, a0, lm0, L, a1, lm1, vm);
@@ -1511,7 +1520,7 @@ __device__ __forceinline__ void muscle_one_n(const DevModel& M, const EnvRowsN<N
         const float a1 = fminf(fmaxf(fmaf(a0[e] - u[e], ex, u[e]), 0.0f), 1.0f);
         const double prev_len = fma(lm0[e], pa.y, pa.x);
         const float vm = static_cast<float>((L - prev_len) * pb.y);
-        const double lm1 = fmax((L - pa.x) * pb.x, static_cast<double>(kMinFiber));
+        const double lm1 = fiber_clamp((L - pa.x) * pb.x);
         const float F = mtu_force(a1, static_cast<float>(lm1), vm, p0.x);
         if (V.live[e]) {
             V.R[e].act[m] = a1;
