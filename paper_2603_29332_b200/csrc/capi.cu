@@ -520,6 +520,10 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             t += static_cast<int>(tq.flag.size());
             M.tab_off_tqp = t;
             t += c.nj + 1;
+            M.tab_off_chain = t;  // per level: chain flag | super-level end (see the work-word slots below)
+            t += c.n_levels;
+            M.tab_off_slstart = t;  // per level: first level of its super-level
+            t += c.n_levels;
             M.tab_bytes = align16(t);
             std::vector<unsigned char> blob(M.tab_bytes, 0);
             auto put = [&](int at, const void* src, size_t n) { std::memcpy(blob.data() + at, src, n); };
@@ -537,10 +541,37 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             }
             for (int d = 0; d <= c.n_levels; ++d) blob[M.tab_off_lvs + d] = static_cast<unsigned char>(c.level_start[d]);
             // work word of slot i of level d: link | (parent + 1) << 8 | child_off << 16 |
-            // nchild << 24 | has_sphere << 28 | simple level << 29 | valid << 31 (one shared load per level)
+            // nchild << 24 | has_sphere << 28 | simple level << 29 | valid << 31 (one shared load per level).
+            // Chain levels: every link of level d is its parent's only child (and no link of
+            // level d - 1 has more than one child).  Their links take their parent's slot, so
+            // the step kernel's passes run each lane down (or up) a chain of such levels in
+            // registers, with no warp barrier in between (tree_sweep_chain & co.); slots of a
+            // chain level can have gaps (a leaf parent), every pass skips invalid slots.
+            std::vector<int> slot_of(c.nl, -1);
             for (int d = 0; d < c.n_levels; ++d) {
                 const int b = c.level_start[d], n = c.level_start[d + 1] - b;
                 if (n > 32) throw ConfigError("model too wide: a tree level has more than 32 links");
+                bool chain = d > 0;
+                for (int i = 0; i < n && chain; ++i) {
+                    const int l = c.level_links[b + i], pl = c.link_parent[l];
+                    chain = pl >= 0 && c.child_start[pl + 1] - c.child_start[pl] == 1 && l >= c.floating;
+                }
+                blob[M.tab_off_chain + d] = chain ? 0x80 : 0;
+                for (int i = 0; i < n; ++i) {
+                    const int l = c.level_links[b + i];
+                    slot_of[l] = chain ? slot_of[c.link_parent[l]] : i;
+                }
+            }
+            for (int d0 = 0; d0 < c.n_levels;) {  // super-levels [d0, d1): first -> end, last -> first
+                int d1 = d0 + 1;
+                while (d1 < c.n_levels && (blob[M.tab_off_chain + d1] & 0x80)) ++d1;
+                if (d1 > 127) throw ConfigError("model too deep: more than 127 tree levels");
+                blob[M.tab_off_chain + d0] |= static_cast<unsigned char>(d1);
+                for (int d = d0; d < d1; ++d) blob[M.tab_off_slstart + d] = static_cast<unsigned char>(d0);
+                d0 = d1;
+            }
+            for (int d = 0; d < c.n_levels; ++d) {
+                const int b = c.level_start[d], n = c.level_start[d + 1] - b;
                 // bit 29: the level is "simple" — every link has a parent link and a joint DOF
                 // (no root, no child of the fixed base), so the passes skip those branches
                 bool simple = true;
@@ -557,7 +588,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
                                        (static_cast<uint32_t>(c.child_start[l]) << 16) |
                                        (static_cast<uint32_t>(nchild) << 24) | (static_cast<uint32_t>(has_sph) << 28) |
                                        (static_cast<uint32_t>(simple) << 29) | (1u << 31);
-                    put(M.tab_off_work + 4 * (32 * d + i), &w, 4);
+                    put(M.tab_off_work + 4 * (32 * d + slot_of[l]), &w, 4);
                 }
             }
             put(M.tab_off_tq, tq.flag.data(), tq.flag.size());

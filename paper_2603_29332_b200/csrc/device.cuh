@@ -93,7 +93,7 @@ struct DevModel {
     // block-shared tree table at the head of dynamic smem (bytes)
     const int4* tab_blob;
     int tab_bytes, tab_off_a, tab_off_in, tab_off_meta, tab_off_child, tab_off_lvl, tab_off_lvs, tab_off_work;
-    int tab_off_tq, tab_off_tqp;  // joint-torque lists (capi.cu plan_torques): u8 flags [tq_len][G], u8 pieces [nj+1]
+    int tab_off_tq, tab_off_tqp, tab_off_chain, tab_off_slstart;  // joint-torque lists (capi.cu plan_torques): u8 flags [tq_len][G], u8 pieces [nj+1]
     int tq_len;                   // elements per lane of the joint-torque lists
 };
 

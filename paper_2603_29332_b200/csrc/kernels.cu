@@ -75,6 +75,8 @@ struct EnvSmem {
     const uint32_t* twork; // [level][32] work words (see capi.cu): link, parent, children, sphere flag
     const uint8_t* tqf;    // [tq_len][G] joint-torque list flags: piece id ending at the element, else 0xff
     const uint8_t* tqp;    // nj + 1: pieces of joint j = [tqp[j], tqp[j+1])
+    const uint8_t* tchain; // n_levels: 0x80 = chain level (its links sit in their parent's slot) | super-level end
+    const uint8_t* tslstart;  // n_levels: first level of the level's super-level
     int G;                 // lanes per env (32 or 16)
     unsigned hm;           // mask of this env's lanes
 };
@@ -131,6 +133,8 @@ __device__ __forceinline__ EnvSmem carve(unsigned char* smem0, int slot, const D
     s.twork = reinterpret_cast<const uint32_t*>(smem + M.tab_off_work);
     s.tqf = smem + M.tab_off_tq;
     s.tqp = smem + M.tab_off_tqp;
+    s.tchain = smem + M.tab_off_chain;
+    s.tslstart = smem + M.tab_off_slstart;
     return s;
 }
 
@@ -379,8 +383,15 @@ __device__ __forceinline__ void sphere_pen_d(const DevModel& M, const EnvSmem& S
 // One link of the root-to-leaf sweep (tree_sweep).  kSimple: the level has no
 // root and no child of the fixed base (work-word bit 29), so the link has a
 // parent and a joint DOF = l + nrd - floating.
-template <bool kFull, bool kSimple>
-__device__ __forceinline__ void sweep_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff, float* grf) {
+// Parent state forwarded in registers along a chain of levels (tree_sweep_chain).
+struct SweepPar {
+    float c, s, w, vx, vz;
+};
+
+template <bool kFull, bool kSimple, bool kFwd = false>
+__device__ __forceinline__ SweepPar sweep_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff,
+                                               float* grf, const SweepPar& par = SweepPar{}) {
+    static_assert(!kFwd || (kFull && kSimple), "forwarding: substep sweep of a chain level");
     const int l = ww_link(ww);
     const int dof = kSimple ? l + dofoff : link_dof(M, l);
     const float4 la = S.ta[l];
@@ -400,18 +411,30 @@ __device__ __forceinline__ void sweep_link(const DevModel& M, const EnvSmem& S, 
         const double2 rd = S.relcs[dof];
         const float cr = static_cast<float>(rd.x), sr = static_cast<float>(rd.y);
         if (kSimple || p >= 0) {
-            const float4 kp = S.kin[p];
+            float4 kp;
+            float2 wv;   // parent (omega, v_x)
+            float pvz;   // parent v_z
+            if constexpr (kFwd) {
+                kp = make_float4(par.c, par.s, 0.0f, 0.0f);
+                wv = make_float2(par.w, par.vx);
+                pvz = par.vz;
+            } else {
+                kp = S.kin[p];
+                if (kFull) {
+                    const float* up = S.un + kLinkStride * p;
+                    wv = reinterpret_cast<const float2*>(up)[5];
+                    pvz = up[9];
+                }
+            }
             // kFull: origin relative to the parent's (frame_rel); else absolute (root-relative)
             ox = fmaf(kp.x, la.x, kFull ? -kp.y * la.y : fmaf(-kp.y, la.y, kp.z));
             oz = fmaf(kp.y, la.x, kFull ? kp.x * la.y : fmaf(kp.x, la.y, kp.w));
             c = fmaf(kp.x, cr, -kp.y * sr);
             s = fmaf(kp.y, cr, kp.x * sr);
             if (kFull) {
-                const float* up = S.un + kLinkStride * p;
-                const float2 wv = reinterpret_cast<const float2*>(up)[5];  // parent (omega, v_x)
                 w = wv.x + S.dqf[dof];
                 vx = fmaf(-wv.x, oz, wv.y);
-                vz = fmaf(wv.x, ox, up[9]);
+                vz = fmaf(wv.x, ox, pvz);
             }
         } else {
             ox = la.x;
@@ -422,7 +445,7 @@ __device__ __forceinline__ void sweep_link(const DevModel& M, const EnvSmem& S, 
         }
     }
     S.kin[l] = make_float4(c, s, ox, oz);
-    if (!kFull) return;
+    if (!kFull) return SweepPar{};
     float* u = S.un + kLinkStride * l;
     // link record (14 floats): [0..5] articulated inertia, [6..8] bias force,
     // [9] u/D, [10..11] U1/D, U2/D, [12..13] c; velocity (omega, v_x | v_z)
@@ -474,6 +497,7 @@ __device__ __forceinline__ void sweep_link(const DevModel& M, const EnvSmem& S, 
     u2[3] = make_float2(p0, p1);
     u[8] = p2;
     u2[6] = make_float2(c1, c2);
+    return SweepPar{c, s, w, vx, vz};
 }
 
 // Root-to-leaf sweep.  FK by rotation composition R_l = R_p R_joint
@@ -488,13 +512,42 @@ __device__ __forceinline__ void tree_sweep(const DevModel& M, const EnvSmem& S, 
     for (int lev = 0; lev < M.n_levels; ++lev) {
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
-            if (!(ww >> 31)) break;
+            if (!(ww >> 31)) continue;
             if ((ww >> 29) & 1)
                 sweep_link<kFull, true>(M, S, ww, dofoff, grf);
             else
                 sweep_link<kFull, false>(M, S, ww, dofoff, grf);
         }
         __syncwarp(S.hm);
+    }
+}
+
+// Super-levels: a non-chain level followed by its chain levels (capi.cu): one
+// lane runs its slot's links down the chain with the parent state in registers
+// and no warp barrier between the levels (wb700: 15 levels -> 6 super-levels).
+// tchain[lev] (capi.cu): bit 7 = chain level; bits 0-6 = one past the
+// super-level's last level (for lev = its first level).
+__device__ __forceinline__ int superlevel_end(const DevModel& M, const EnvSmem& S, int lev) {
+    return S.tchain[lev] & 0x7f;
+}
+
+// tree_sweep<true> over super-levels (one slot per lane: G = 32).
+__device__ __forceinline__ void tree_sweep_chain(const DevModel& M, const EnvSmem& S, int lane, float* grf) {
+    const int dofoff = M.nrd - M.floating;
+    for (int lev = 0; lev < M.n_levels;) {
+        const int end = superlevel_end(M, S, lev);
+        uint32_t ww = S.twork[32 * lev + lane];
+        if (ww >> 31) {
+            SweepPar par = ((ww >> 29) & 1) ? sweep_link<true, true>(M, S, ww, dofoff, grf)
+                                            : sweep_link<true, false>(M, S, ww, dofoff, grf);
+            for (int d = lev + 1; d < end; ++d) {
+                ww = S.twork[32 * d + lane];
+                if (!(ww >> 31)) break;
+                par = sweep_link<true, true, true>(M, S, ww, dofoff, grf, par);
+            }
+        }
+        __syncwarp(S.hm);
+        lev = end;
     }
 }
 
@@ -506,7 +559,7 @@ __device__ __forceinline__ void fk_d(const DevModel& M, const EnvSmem& S, int la
     for (int lev = 0; lev < M.n_levels; ++lev) {
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
-            if (!(ww >> 31)) break;
+            if (!(ww >> 31)) continue;
             const int l = ww_link(ww);
             const int dof = link_dof(M, l);
             double2 cs, o;
@@ -942,28 +995,51 @@ __device__ __forceinline__ float joint_torque(const DevModel& M, const EnvSmem& 
 
 // Articulated-body pass, leaves -> root (per link U = IA e0, D, Schur
 // complement, shift to the parent origin; children summed in fixed order).
-template <bool kSimple>
-__device__ __forceinline__ void aba_up_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff) {
+// A link's articulated inertia and bias shifted to its parent's origin (the
+// parent's children sum): forwarded in registers along a chain (aba_up_chain).
+struct UpRec {
+    float2 r0, r1, r2, r3;
+    float p2;
+};
+
+// kFwdIn: the link's only child's shifted record comes in registers (chain);
+// kStoreOut: the shifted record goes to shared memory for a parent in another
+// lane / super-level (else it is only returned).
+template <bool kSimple, bool kFwdIn = false, bool kStoreOut = true>
+__device__ __forceinline__ UpRec aba_up_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff,
+                                             const UpRec& child = UpRec{}) {
     const int l = ww_link(ww);
     float* u = S.un + kLinkStride * l;
     float2* u2 = reinterpret_cast<float2*>(u);
     float2 r0 = u2[0], r1 = u2[1], r2 = u2[2], r3 = u2[3];
     float P2 = u[8];
-    const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
+    if constexpr (kFwdIn) {
+        r0.x += child.r0.x;
+        r0.y += child.r0.y;
+        r1.x += child.r1.x;
+        r1.y += child.r1.y;
+        r2.x += child.r2.x;
+        r2.y += child.r2.y;
+        r3.x += child.r3.x;
+        r3.y += child.r3.y;
+        P2 += child.p2;
+    } else {
+        const int c0 = ww_child0(ww), c1 = c0 + ww_nchild(ww);
 #pragma unroll 1  // mostly one child: an unrolled 4/2/1 cascade costs more branches than it saves (A/B +1.8 %)
-    for (int c = c0; c < c1; ++c) {
-        const float* uc = S.un + kLinkStride * S.tchild[c];
-        const float2* uc2 = reinterpret_cast<const float2*>(uc);
-        const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
-        r0.x += a0.x;
-        r0.y += a0.y;
-        r1.x += a1.x;
-        r1.y += a1.y;
-        r2.x += a2.x;
-        r2.y += a2.y;
-        r3.x += a3.x;
-        r3.y += a3.y;
-        P2 += uc[8];
+        for (int c = c0; c < c1; ++c) {
+            const float* uc = S.un + kLinkStride * S.tchild[c];
+            const float2* uc2 = reinterpret_cast<const float2*>(uc);
+            const float2 a0 = uc2[0], a1 = uc2[1], a2 = uc2[2], a3 = uc2[3];
+            r0.x += a0.x;
+            r0.y += a0.y;
+            r1.x += a1.x;
+            r1.y += a1.y;
+            r2.x += a2.x;
+            r2.y += a2.y;
+            r3.x += a3.x;
+            r3.y += a3.y;
+            P2 += uc[8];
+        }
     }
     const float I00 = r0.x, I01 = r0.y, I02 = r1.x, I11 = r1.y, I12 = r2.x, I22 = r2.y;
     const float P0 = r3.x, P1 = r3.y;
@@ -974,7 +1050,7 @@ __device__ __forceinline__ void aba_up_link(const DevModel& M, const EnvSmem& S,
         u2[2] = r2;
         u2[3] = r3;
         u[8] = P2;
-        return;
+        return UpRec{};
     }
     // hinge with S = (1,0,0) at the link origin: U = IA[:,0], D = U0
     const float invD = rcp_ftz(I00);  // (IEEE 1/x costs a range check + slow-path call)
@@ -991,15 +1067,63 @@ __device__ __forceinline__ void aba_up_link(const DevModel& M, const EnvSmem& S,
     u[9] = uu;
     u2[5] = make_float2(U1, U2);
     const int p = ww_parent(ww);
+    UpRec out{};
     if (kSimple || p >= 0) {  // shift to the parent's origin: X^T Ia X, X^T pa
         const float2 d = frame_rel(S, l);  // origin relative to the parent's
         const float dx = d.x, dz = d.y;
         const float al = fmaf(-a, dz, bb * dx), be = fmaf(-bb, dz, cq * dx);
-        u2[0] = make_float2(fmaf(-dz, al, be * dx), al);
-        u2[1] = make_float2(be, a);
-        u2[2] = make_float2(bb, cq);
-        u2[3] = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
-        u[8] = q2;
+        out.r0 = make_float2(fmaf(-dz, al, be * dx), al);
+        out.r1 = make_float2(be, a);
+        out.r2 = make_float2(bb, cq);
+        out.r3 = make_float2(fmaf(-dz, q1, fmaf(dx, q2, t)), q1);
+        out.p2 = q2;
+        if (kStoreOut) {
+            u2[0] = out.r0;
+            u2[1] = out.r1;
+            u2[2] = out.r2;
+            u2[3] = out.r3;
+            u[8] = out.p2;
+        }
+    }
+    return out;
+}
+
+// aba_up over super-levels, bottom up (one slot per lane: G = 32): each lane
+// takes its slot's chain from the deepest link (children, in the next
+// super-level, summed from shared memory) up to the super-level's first link,
+// each link's only child's shifted record forwarded in registers; only the
+// first link's record (its parent sits in another super-level) is stored.
+__device__ __forceinline__ void aba_up_chain(const DevModel& M, const EnvSmem& S, int lane) {
+    const int dofoff = M.nrd - M.floating;
+    for (int end = M.n_levels; end > 0;) {
+        const int lev = S.tslstart[end - 1];  // the super-level's first level
+        const uint32_t wl = S.twork[32 * (end - 1) + lane];
+        if (lev == end - 1) {  // a single level: children from shared memory, record stored
+            if (wl >> 31) {
+                if ((wl >> 29) & 1)
+                    aba_up_link<true>(M, S, wl, dofoff);
+                else
+                    aba_up_link<false>(M, S, wl, dofoff);
+            }
+        } else {
+            // deepest level (children in the next super-level); a chain that ends higher up
+            // ends in a leaf, whose forwarded child record is zero
+            UpRec rc{};
+            if (wl >> 31) rc = aba_up_link<true, false, false>(M, S, wl, dofoff);  // chain levels are simple
+            for (int d = end - 2; d > lev; --d) {
+                const uint32_t ww = S.twork[32 * d + lane];
+                if (ww >> 31) rc = aba_up_link<true, true, false>(M, S, ww, dofoff, rc);
+            }
+            const uint32_t wt = S.twork[32 * lev + lane];
+            if (wt >> 31) {
+                if ((wt >> 29) & 1)
+                    aba_up_link<true, true, true>(M, S, wt, dofoff, rc);
+                else
+                    aba_up_link<false, true, true>(M, S, wt, dofoff, rc);
+            }
+        }
+        __syncwarp(S.hm);
+        end = lev;
     }
 }
 
@@ -1008,7 +1132,7 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
     for (int lev = M.n_levels - 1; lev >= 0; --lev) {
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
-            if (!(ww >> 31)) break;
+            if (!(ww >> 31)) continue;
             if ((ww >> 29) & 1)
                 aba_up_link<true>(M, S, ww, dofoff);
             else
@@ -1018,21 +1142,36 @@ __device__ __forceinline__ void aba_up(const DevModel& M, const EnvSmem& S, int 
     }
 }
 
-// One link of the root-to-leaf articulated-body pass: q̈ into S.tau.
-template <bool kSimple>
-__device__ __forceinline__ void aba_down_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff) {
+// A link's spatial acceleration terms {A0 + q̈, A1, A2} as its children read them.
+struct DownPar {
+    float a0, a1, a2;
+};
+
+// One link of the root-to-leaf articulated-body pass: q̈ into S.tau.  kFwd:
+// the parent's terms come in registers (chain); store: its children read them
+// from shared memory (another lane / super-level).
+template <bool kSimple, bool kFwd = false>
+__device__ __forceinline__ DownPar aba_down_link(const DevModel& M, const EnvSmem& S, uint32_t ww, int dofoff,
+                                                 const DownPar& par = DownPar{}, bool store = true) {
     const int l = ww_link(ww);
     const int dof = kSimple ? l + dofoff : link_dof(M, l);
-    if (!kSimple && dof < 0) return;
     float* u = S.un + kLinkStride * l;
+    if (!kSimple && dof < 0) return DownPar{u[0], u[1], u[2]};  // floating root: the root solve's terms
     const int p = ww_parent(ww);
     float2* u2 = reinterpret_cast<float2*>(u);
     const float2 cv = u2[6];
     float A0 = 0.0f, A1 = cv.x, A2 = cv.y;
     if (kSimple || p >= 0) {
-        const float* up = S.un + kLinkStride * p;
-        const float2 a01 = reinterpret_cast<const float2*>(up)[0];
-        const float a2 = up[2];
+        float2 a01;
+        float a2;
+        if constexpr (kFwd) {
+            a01 = make_float2(par.a0, par.a1);
+            a2 = par.a2;
+        } else {
+            const float* up = S.un + kLinkStride * p;
+            a01 = reinterpret_cast<const float2*>(up)[0];
+            a2 = up[2];
+        }
         const float2 d = frame_rel(S, l);  // origin relative to the parent's
         const float dx = d.x, dz = d.y;
         A0 = a01.x;
@@ -1042,17 +1181,19 @@ __device__ __forceinline__ void aba_down_link(const DevModel& M, const EnvSmem& 
     // q̈ = (u - U^T A) / D with U0 = D
     const float2 U = u2[5];
     const float qdd = u[9] - A0 - fmaf(U.x, A1, U.y * A2);
-    u2[0] = make_float2(A0 + qdd, A1);
-    u[2] = A2;
+    if (store) {
+        u2[0] = make_float2(A0 + qdd, A1);
+        u[2] = A2;
+    }
     S.tau[dof] = qdd;
+    return DownPar{A0 + qdd, A1, A2};
 }
 
-// Floating-root solve (3x3 Cholesky) + articulated-body pass, root -> leaves:
-// q̈ into S.tau.
-__device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, int lane) {
-    const int dofoff = M.nrd - M.floating;
-    if (M.floating && lane == 0) {
-        float* u = S.un;  // link 0: solve IA A = -pA (3x3 SPD, Cholesky with reciprocal pivots)
+// Floating root (link 0): solve IA A = -pA (3x3 SPD, Cholesky with reciprocal
+// pivots) and the root's coordinate accelerations.
+__device__ __forceinline__ void root_solve(const EnvSmem& S) {
+    {
+        float* u = S.un;
         const float i00 = rsqrt_ftz(u[0]);
         const float l10 = u[1] * i00, l20 = u[2] * i00;
         const float i11 = rsqrt_ftz(u[3] - l10 * l10);
@@ -1073,11 +1214,18 @@ __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, in
         S.tau[1] = fmaf(wd, S.dqf[0], x2);
         S.tau[2] = x0;
     }
+}
+
+// Floating-root solve (3x3 Cholesky) + articulated-body pass, root -> leaves:
+// q̈ into S.tau.
+__device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, int lane) {
+    const int dofoff = M.nrd - M.floating;
+    if (M.floating && lane == 0) root_solve(S);
     __syncwarp(S.hm);
     for (int lev = 0; lev < M.n_levels; ++lev) {
         for (int i = lane; i < 32; i += S.G) {
             const uint32_t ww = S.twork[32 * lev + i];
-            if (!(ww >> 31)) break;
+            if (!(ww >> 31)) continue;
             if ((ww >> 29) & 1)
                 aba_down_link<true>(M, S, ww, dofoff);
             else
@@ -1085,7 +1233,28 @@ __device__ __forceinline__ void aba_down(const DevModel& M, const EnvSmem& S, in
         }
         __syncwarp(S.hm);
     }
+}
 
+// aba_down over super-levels (one slot per lane: G = 32); the root solve first.
+__device__ __forceinline__ void aba_down_chain(const DevModel& M, const EnvSmem& S, int lane) {
+    const int dofoff = M.nrd - M.floating;
+    if (M.floating && lane == 0) root_solve(S);
+    __syncwarp(S.hm);
+    for (int lev = 0; lev < M.n_levels;) {
+        const int end = superlevel_end(M, S, lev);
+        uint32_t ww = S.twork[32 * lev + lane];
+        if (ww >> 31) {
+            DownPar par = ((ww >> 29) & 1) ? aba_down_link<true>(M, S, ww, dofoff, DownPar{}, lev == end - 1)
+                                           : aba_down_link<false>(M, S, ww, dofoff, DownPar{}, lev == end - 1);
+            for (int d = lev + 1; d < end; ++d) {
+                ww = S.twork[32 * d + lane];
+                if (!(ww >> 31)) break;
+                par = aba_down_link<true, true>(M, S, ww, dofoff, par, d == end - 1);
+            }
+        }
+        __syncwarp(S.hm);
+        lev = end;
+    }
 }
 
 // Loads an env's q, dq (f64) into the DOF-owning lanes.
@@ -1313,15 +1482,24 @@ __global__ void __launch_bounds__(WPB * 32, MINB) step_kernel(DevModel M, DevSta
         {
             // ---- 3. FK + velocities + per-link articulated-body terms ----
             if (M.ns) sphere_pen_d(M, S, lane);
-            tree_sweep<true>(M, S, lane, grf_row);
+            if constexpr (G == 32)  // one slot per lane: chains of levels in registers
+                tree_sweep_chain(M, S, lane, grf_row);
+            else
+                tree_sweep<true>(M, S, lane, grf_row);
 
             PHASE_MARK(2);
             // ---- 4a. articulated-body pass, leaves -> root ----
-            aba_up(M, S, lane);
+            if constexpr (G == 32)
+                aba_up_chain(M, S, lane);
+            else
+                aba_up(M, S, lane);
 
             PHASE_MARK(3);
             // ---- 4b. root solve + articulated-body pass, root -> leaves ----
-            aba_down(M, S, lane);
+            if constexpr (G == 32)
+                aba_down_chain(M, S, lane);
+            else
+                aba_down(M, S, lane);
         }
 
         PHASE_MARK(4);
