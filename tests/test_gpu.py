@@ -1288,3 +1288,76 @@ def test_passive_chain_energy_drift_on_device(assets, tmp_path, name, q0):
 
 def to_np_flags(out):
     return out["flags"].cpu().numpy()
+
+
+def _hopper(path_model, path_clip):
+    """A floating root with ONE chain below it (torso -> thigh -> shank -> foot):
+    every level below the root is a chain level, so the step kernel's
+    super-level passes forward the floating root's terms down the chain."""
+    import math
+
+    from tools import gen_assets as ga
+
+    m = ga.Model("hopper4_m8", "floating")
+    m.joint_limit_stiffness = 200.0
+    m.contact = {"stiffness": 2.0e4, "damping": 300.0, "friction": 0.9, "smoothing_vel": 0.05}
+    m.links = [
+        ga.Link("torso", 0.60, 30.0, 30.0 * 0.6**2 / 12, 0.30),
+        ga.Link("thigh", 0.45, 7.0, 7.0 * 0.45**2 / 12, 0.20),
+        ga.Link("shank", 0.45, 3.5, 3.5 * 0.45**2 / 12, 0.20),
+        ga.Link("foot", 0.20, 1.0, 1.0 * 0.2**2 / 12, 0.08),
+    ]
+    m.joints = [
+        ga.Joint("hip", 1, 0, (0.0, 0.0), math.pi, (-2.2, 1.2), 0.5),
+        ga.Joint("knee", 2, 1, (0.45, 0.0), 0.0, (-2.4, 0.05), 0.3),
+        ga.Joint("ankle", 3, 2, (0.45, 0.0), -math.pi / 2, (-0.8, 0.8), 0.2),
+    ]
+    q0 = np.array([0.0, 1.05, math.pi / 2, 0.1, -0.2, 0.05])
+    m.muscles = [
+        ga.make_muscle(m, "hip_flexor", [(0, (0.12, -0.06)), (1, (0.12, -0.04))], q0, 2500.0),
+        ga.make_muscle(m, "hip_extensor", [(0, (0.10, 0.07)), (1, (0.12, 0.04))], q0, 2500.0),
+        ga.make_muscle(m, "knee_flexor", [(1, (0.30, 0.04)), (2, (0.06, 0.03))], q0, 2000.0),
+        ga.make_muscle(m, "knee_extensor", [(1, (0.30, -0.05)), (2, (0.06, -0.035))], q0, 2000.0),
+        ga.make_muscle(m, "hamstring", [(0, (0.05, 0.06)), (1, (0.25, 0.05)), (2, (0.07, 0.03))], q0, 1500.0),
+        ga.make_muscle(m, "gastroc", [(1, (0.40, 0.04)), (2, (0.25, 0.04)), (3, (0.05, 0.02))], q0, 800.0),
+        ga.make_muscle(m, "tibialis", [(2, (0.20, -0.035)), (3, (0.06, -0.02))], q0, 800.0),
+        ga.make_muscle(m, "soleus", [(2, (0.25, 0.04)), (3, (0.04, 0.02))], q0, 900.0),
+    ]
+    m.spheres = [{"link": 3, "offset": [0.0, 0.0], "radius": 0.04}, {"link": 3, "offset": [0.18, 0.0], "radius": 0.03}]
+    m.key_bodies = [0, 2, 3]
+    ga.write_model(path_model, m)
+    ga.write_clip(path_clip, m, ga.ground_offset(m, ga.sinusoid_clip(m, 301, 5)))
+
+
+@pytest.mark.gpu
+def test_floating_root_single_chain_parity(assets, tmp_path):
+    """Super-level tree passes on a floating root whose only child starts a chain
+    (the root's solve terms and articulated inertia forwarded in registers):
+    one control step from perturbed clip states matches the oracle within the
+    single-step bounds, flags bit-exact."""
+    import torch
+
+    mp, cp = str(tmp_path / "hopper.json"), str(tmp_path / "hopper_clip.csv")
+    _hopper(mp, cp)
+    n = 8
+    g, o = make_pair(mp, cp, n, cfg_kw=dict(episode_horizon=1000, rsi=False))
+    g.set_eval_mode(True)
+    o.set_eval_mode(True)
+    fmax = o.model.d["m_fmax"]
+    for trial in range(2):
+        fr = (np.arange(n) * 31 + 7 * trial) % (o.frames - 2)
+        g.reset_to_frame(fr)
+        o.reset_to_frame(fr)
+        s = o.get_state()
+        rng = np.random.default_rng(trial)
+        s["dq"] = s["dq"] + rng.normal(0, 0.3, s["dq"].shape)
+        s["act"] = rng.uniform(0, 1, s["act"].shape)
+        s = f32_state(s)
+        o.set_state(s)
+        g.set_state(s)
+        a = excitations(77 + trial, 0, n, g.nm).astype(np.float32)
+        og, oo = step_both(g, o, a)
+        _check_step("hopper", gpu_state(g), o.get_state(), fmax)
+        assert np.array_equal(og["flags"], oo["flags"])
+    g.close()
+    torch.cuda.synchronize()
