@@ -470,7 +470,9 @@ def main():
         if rollout is not None:  # the observation the action is taken from
             rollout.record(s % rollout.h, obs=obs)
         if C["exchange"]:  # the normaliser sees every observation the policy acts on
-            mom_acc = pkd.fold_moments(mom_acc, env.obs_moments(obs), env.obs_dim)
+            if mom_acc is None:  # count 0: the first fold takes the batch moments exactly
+                mom_acc = torch.zeros(1 + 2 * env.obs_dim, dtype=torch.float64, device=dev)
+            env.obs_moments_fold(obs, mom_acc)
         if policy is not None:
             policy.sample(obs, explore=True, seed=seed, step=s, global_env_offset=rank * E, actions=actions,
                           a0=ro_a0 if rollout is not None else None, logprob=ro_lp if rollout is not None else None,

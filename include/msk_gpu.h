@@ -272,6 +272,11 @@ int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, c
 /* Batch moments of obs [n x obs_dim] (RunningNorm::update's batch mean and
  * population variance, nn.cpp:246-256) in f64: out = [n, mean[D], var[D]]. */
 int msk_gpu_obs_moments(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream);
+/* The same batch moments folded into a running acc [1 + 2 obs_dim] = {count,
+ * mean, var} (f64, in/out) as RunningNorm::update (nn.cpp:257-270): count 0
+ * takes the batch exactly, n = 0 leaves acc unchanged.  Accumulates an
+ * iteration's h x E observations without a host round trip (three launches). */
+int msk_gpu_obs_moments_fold(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* acc, void* stream);
 int msk_gpu_merge_outcomes(msk_gpu_ctx* ctx, const int32_t* bins, const uint8_t* failed, const int32_t* counts,
                            int64_t n_envs_total, int32_t cap, void* stream);
 

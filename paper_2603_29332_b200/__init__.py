@@ -367,6 +367,7 @@ def lib():
         L.msk_rollout_field.restype = C.c_void_p
         L.msk_rollout_field.argtypes = [_vp, C.c_int32]
         L.msk_gpu_obs_moments.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
+        L.msk_gpu_obs_moments_fold.argtypes = [_vp, _vp, C.c_int32, _vp, _vp]
         L.msk_gpu_iteration_exchange.argtypes = [_vp, _vp, C.c_int32, _vp, _vp, _vp, _vp, _vp]
         L.msk_gpu_set_discriminator.argtypes = [_vp, _vp, C.c_int64, C.c_int32]
         L.msk_gpu_set_discriminator_mode.argtypes = [_vp, C.c_int32]
@@ -660,6 +661,13 @@ class EnvBatch:
                                                            device=self.device)
         self._ck(lib().msk_gpu_obs_moments(self.h, _p(obs.contiguous()), int(n), _p(out), self._s(stream)))
         return out
+
+    def obs_moments_fold(self, obs, acc, stream=None):
+        """msk_gpu_obs_moments_fold: folds the batch moments of obs [n x obs_dim]
+        into acc (f64 [1 + 2 obs_dim] {count, mean, var}, device, in place)."""
+        self._ck(lib().msk_gpu_obs_moments_fold(self.h, _p(obs.contiguous()), int(obs.shape[0]), _p(acc),
+                                                self._s(stream)))
+        return acc
 
     def iteration_exchange(self, cap, obs, stats, norm, stats_out=None, nccl_comm=None, stream=None):
         """msk_gpu_iteration_exchange: drain + stats + obs moments, all-gather over

@@ -50,7 +50,7 @@ void launch_permute_muscles(const DevModel&, int n, const double* src, double* d
 void launch_rollout_stats(const DevState&, int n, const float* reward, const uint8_t* flags, double* stats,
                           cudaStream_t);
 int obs_moments_chunks(int n);
-void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t);
+void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t, bool fold = false);
 void launch_excitations(int n, int nm, long long env_offset, uint64_t seed, uint32_t step, float* out,
                         cudaStream_t);
 void launch_merge_block(const DevModel& M, const int* bins, const uint8_t* failed, const int* counts, long long n,
@@ -637,7 +637,7 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
         ctx->obs_dim = 3 * c.nq + 6 * c.nk + 4 * c.nm;
         // obs-moment partials for a whole batch, allocated up front (no allocation,
         // hence no implicit sync, at the first iteration boundary)
-        ctx->mom_cap = static_cast<size_t>(obs_moments_chunks(n_envs)) * ctx->obs_dim * 2;
+        ctx->mom_cap = static_cast<size_t>(obs_moments_chunks(n_envs)) * ctx->obs_dim * 2 + 1;
         ctx->mom_part = ctx->dalloc<double>(ctx->mom_cap);
         ctx->delta_dim = 3 + c.nj + 2 * c.nk;
 
@@ -1124,19 +1124,28 @@ int msk_gpu_rollout_stats(msk_gpu_ctx* ctx, const float* reward, const uint8_t* 
     });
 }
 
+namespace {
+void obs_moments_impl(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream, bool fold) {
+    if ((!obs && n > 0) || !out || n < 0) throw ConfigError("obs_moments: bad arguments");
+    const size_t need = static_cast<size_t>(obs_moments_chunks(n)) * ctx->obs_dim * 2 + 1;
+    if (need > ctx->mom_cap) {
+        ctx->mom_part = ctx->dalloc<double>(need);
+        ctx->mom_cap = need;
+    }
+    launch_obs_moments(obs, n, ctx->obs_dim, ctx->mom_part, out, as_stream(stream), fold);
+    ctx->count(n > 0 ? 2 : (fold ? 0 : 1));
+    ctx->check_launch();
+}
+}  // namespace
+
 int msk_gpu_obs_moments(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* out, void* stream) {
     const msk_b200::NvtxRange nvtx_("msk_gpu_obs_moments");
-    return guarded(ctx, [&] {
-        if (!obs || !out || n < 0) throw ConfigError("obs_moments: bad arguments");
-        const size_t need = static_cast<size_t>(obs_moments_chunks(n)) * ctx->obs_dim * 2;
-        if (need > ctx->mom_cap) {
-            ctx->mom_part = ctx->dalloc<double>(need);
-            ctx->mom_cap = need;
-        }
-        launch_obs_moments(obs, n, ctx->obs_dim, ctx->mom_part, out, as_stream(stream));
-        ctx->count(2);
-        ctx->check_launch();
-    });
+    return guarded(ctx, [&] { obs_moments_impl(ctx, obs, n, out, stream, false); });
+}
+
+int msk_gpu_obs_moments_fold(msk_gpu_ctx* ctx, const float* obs, int32_t n, double* acc, void* stream) {
+    const msk_b200::NvtxRange nvtx_("msk_gpu_obs_moments_fold");
+    return guarded(ctx, [&] { obs_moments_impl(ctx, obs, n, acc, stream, true); });
 }
 
 int msk_gpu_record_own_outcomes(msk_gpu_ctx* ctx, void* stream) {
@@ -1250,7 +1259,7 @@ int msk_gpu_iteration_exchange(msk_gpu_ctx* ctx, void* nccl_comm, int32_t cap, c
         launch_drain(ctx->St, ctx->n_envs, cap, reinterpret_cast<int*>(b), b + off_failed,
                      reinterpret_cast<int*>(b + off_counts), s);
         ck(cudaMemcpyAsync(b + off_stats, stats_in, 8 * 7, cudaMemcpyDeviceToDevice, s), "stats");
-        const size_t need = static_cast<size_t>(obs_moments_chunks(ctx->n_envs)) * D * 2;
+        const size_t need = static_cast<size_t>(obs_moments_chunks(ctx->n_envs)) * D * 2 + 1;
         if (need > ctx->mom_cap) {
             ctx->mom_part = ctx->dalloc<double>(need);
             ctx->mom_cap = need;

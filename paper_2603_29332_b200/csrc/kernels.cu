@@ -2781,42 +2781,95 @@ __global__ void __launch_bounds__(1024) rollout_stats_kernel(DevState St, int n,
 }
 
 // Column moments of an [n x D] f32 batch in f64 (RunningNorm::update's batch
-// terms, nn.cpp:246-256): pass 1 gives per row-chunk (mean, M2) per column
-// (two passes over the chunk, L2-resident); pass 2 merges the chunks in order
-// (Chan et al.), writing out = [n, mean[D], var[D]] (population variance).
-constexpr int kMomRows = 256;
+// terms, nn.cpp:246-256): pass 1 gives per row-chunk (mean, M2) per column in
+// ONE read of the chunk (sums shifted by the chunk's first row: exact enough in
+// f64 for f32 data, ~1e-15 relative), pass 2 merges the chunks (the Chan et al.
+// merge in closed form), writing out = [n, mean[D], var[D]] (population variance) — or, with
+// `fold`, folding those batch moments into the running {count, mean, var} at
+// out exactly as dist.running_norm_fold_t / RunningNorm::update (nn.cpp:257-270).
+constexpr int kMomRows = 64;
 
-__global__ void obs_moments_part_kernel(const float* x, int n, int D, double* part) {
+__global__ void obs_moments_part_kernel(const float* x, int n, int D, double* part, const double* acc,
+                                        double* acc_count) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+    if (acc && c == 0 && k == 0) *acc_count = acc[0];  // the fold's running count, read before it advances
     if (c >= D) return;
     const int r0 = k * kMomRows, r1 = min(n, r0 + kMomRows);
-    double s = 0.0;
-    for (int r = r0; r < r1; ++r) s += static_cast<double>(x[static_cast<size_t>(r) * D + c]);
-    const double mean = s / static_cast<double>(r1 - r0);
-    double m2 = 0.0;
-    for (int r = r0; r < r1; ++r) {
-        const double d = static_cast<double>(x[static_cast<size_t>(r) * D + c]) - mean;
-        m2 += d * d;
+    const float* col = x + static_cast<size_t>(r0) * D + c;
+    const double sh = static_cast<double>(col[0]);
+    double s1 = 0.0, s2 = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < r1 - r0; ++r) {
+        const double d = static_cast<double>(col[static_cast<size_t>(r) * D]) - sh;
+        s1 += d;
+        s2 = fma(d, d, s2);
     }
-    part[(static_cast<size_t>(k) * D + c) * 2] = mean;
-    part[(static_cast<size_t>(k) * D + c) * 2 + 1] = m2;
+    const double nk = static_cast<double>(r1 - r0);
+    part[(static_cast<size_t>(k) * D + c) * 2] = sh + s1 / nk;
+    part[(static_cast<size_t>(k) * D + c) * 2 + 1] = fmax(s2 - s1 * (s1 / nk), 0.0);
 }
 
-__global__ void obs_moments_merge_kernel(const double* part, int n, int D, int chunks, double* out) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c == 0) out[0] = static_cast<double>(n);
-    if (c >= D) return;
-    double cnt = 0.0, mean = 0.0, m2 = 0.0;
-    for (int k = 0; k < chunks; ++k) {
-        const double nk = static_cast<double>(min(n - k * kMomRows, kMomRows));
-        const double mk = part[(static_cast<size_t>(k) * D + c) * 2], qk = part[(static_cast<size_t>(k) * D + c) * 2 + 1];
-        const double tot = cnt + nk, d = mk - mean;
-        mean += d * (nk / tot);
-        m2 += qk + d * d * (cnt * nk / tot);
-        cnt = tot;
+// Chunk merge: 32 columns x kMomGroups chunk groups per block; the groups' sums
+// are added in group order (fixed), in closed form: mean = sum n_k m_k / n,
+// M2 = sum (M2_k + n_k (m_k - mean)^2) — the Chan merge's result.
+constexpr int kMomGroups = 8;
+
+__global__ void __launch_bounds__(32 * kMomGroups) obs_moments_merge_kernel(const double* part, int n, int D,
+                                                                            int chunks, double* out,
+                                                                            const double* acc_count) {
+    __shared__ double red[kMomGroups][32];
+    const int tx = threadIdx.x, ty = threadIdx.y, c = blockIdx.x * 32 + tx;
+    const int per = (chunks + kMomGroups - 1) / kMomGroups, k0 = ty * per, k1 = min(chunks, k0 + per);
+    double s = 0.0;
+    if (c < D)
+        for (int k = k0; k < k1; ++k)
+            s = fma(static_cast<double>(min(n - k * kMomRows, kMomRows)), part[(static_cast<size_t>(k) * D + c) * 2], s);
+    red[ty][tx] = s;
+    __syncthreads();
+    double tot = 0.0;
+    for (int g = 0; g < kMomGroups; ++g) tot += red[g][tx];
+    const double mean = n > 0 ? tot / static_cast<double>(n) : 0.0;
+    __syncthreads();
+    double q = 0.0;
+    if (c < D)
+        for (int k = k0; k < k1; ++k) {
+            const double nk = static_cast<double>(min(n - k * kMomRows, kMomRows));
+            const double d = part[(static_cast<size_t>(k) * D + c) * 2] - mean;
+            q += fma(nk * d, d, part[(static_cast<size_t>(k) * D + c) * 2 + 1]);
+        }
+    red[ty][tx] = q;
+    __syncthreads();
+    if (ty != 0) return;
+    double m2 = 0.0;
+    for (int g = 0; g < kMomGroups; ++g) m2 += red[g][tx];
+    const double bn = static_cast<double>(n), bvar = n > 0 ? m2 / bn : 0.0;
+    if (!acc_count) {
+        if (c == 0) out[0] = bn;
+        if (c < D) {
+            out[1 + c] = mean;
+            out[1 + D + c] = bvar;
+        }
+        return;
     }
-    out[1 + c] = mean;
-    out[1 + D + c] = n > 0 ? m2 / static_cast<double>(n) : 0.0;
+    // running_norm_fold_t: tot = count + n; delta = bmean - mean;
+    // var = (var count + bvar n + delta^2 (count n / tot)) / tot; mean += delta (n / tot)
+    const double count = *acc_count;
+    if (n == 0) return;
+    if (c == 0) out[0] = __dadd_rn(count, bn);
+    if (c >= D) return;
+    if (count == 0.0) {
+        out[1 + c] = mean;
+        out[1 + D + c] = bvar;
+    } else {
+        const double tn = __dadd_rn(count, bn);
+        const double rm = out[1 + c], rv = out[1 + D + c];
+        const double delta = __dadd_rn(mean, -rm);
+        const double w = __ddiv_rn(__dmul_rn(count, bn), tn);
+        const double num = __dadd_rn(__dadd_rn(__dmul_rn(rv, count), __dmul_rn(bvar, bn)),
+                                     __dmul_rn(__dmul_rn(delta, delta), w));
+        out[1 + D + c] = __ddiv_rn(num, tn);
+        out[1 + c] = __dadd_rn(rm, __dmul_rn(delta, __ddiv_rn(bn, tn)));
+    }
 }
 
 void launch_rollout_stats(const DevState& St, int n, const float* reward, const uint8_t* flags, double* stats,
@@ -2826,10 +2879,16 @@ void launch_rollout_stats(const DevState& St, int n, const float* reward, const 
 
 int obs_moments_chunks(int n) { return (n + kMomRows - 1) / kMomRows; }
 
-void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t s) {
+// part: chunks x D x 2 partials + 1 (the fold's running count, snapshot by the part kernel)
+void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t s, bool fold) {
     const int chunks = obs_moments_chunks(n);
-    if (chunks > 0) obs_moments_part_kernel<<<dim3((D + 127) / 128, chunks), 128, 0, s>>>(x, n, D, part);
-    obs_moments_merge_kernel<<<(D + 127) / 128, 128, 0, s>>>(part, n, D, chunks, out);
+    double* cnt = part + static_cast<size_t>(chunks) * D * 2;
+    if (chunks > 0)
+        obs_moments_part_kernel<<<dim3((D + 127) / 128, chunks), 128, 0, s>>>(x, n, D, part, fold ? out : nullptr, cnt);
+    else if (fold)
+        return;  // an empty batch leaves the running moments unchanged
+    obs_moments_merge_kernel<<<(D + 31) / 32, dim3(32, kMomGroups), 0, s>>>(part, n, D, chunks, out,
+                                                                          fold ? cnt : nullptr);
 }
 
 void launch_drain(const DevState& St, int n, int cap, int* bins, uint8_t* failed, int* counts, cudaStream_t s) {

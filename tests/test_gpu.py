@@ -636,6 +636,19 @@ def test_iteration_reductions_match_torch(assets):
     assert float(m[0]) == n
     assert torch.allclose(m[1:1 + g.obs_dim], x.mean(0), rtol=1e-12, atol=1e-12)
     assert torch.allclose(m[1 + g.obs_dim:], x.var(0, unbiased=False), rtol=1e-9, atol=1e-12)
+    # msk_gpu_obs_moments_fold == RunningNorm::update's fold (dist.fold_moments) of the
+    # batch moments, step by step; count 0 takes the first batch exactly
+    from paper_2603_29332_b200 import dist as pkd
+
+    acc = torch.zeros(1 + 2 * g.obs_dim, dtype=torch.float64, device=g.device)
+    ref = None
+    for k in range(3):
+        ob = obs[k * 200:(k + 1) * 200 + 37 * k]
+        g.obs_moments_fold(ob, acc)
+        ref = pkd.fold_moments(ref, g.obs_moments(ob), g.obs_dim)
+    g.obs_moments_fold(obs[:0], acc)  # an empty batch leaves it unchanged
+    torch.cuda.synchronize()
+    assert torch.equal(acc, ref), float((acc - ref).abs().max())
     g.close()
 
 
