@@ -2809,6 +2809,35 @@ __global__ void obs_moments_part_kernel(const float* x, int n, int D, double* pa
     part[(static_cast<size_t>(k) * D + c) * 2 + 1] = fmax(s2 - s1 * (s1 / nk), 0.0);
 }
 
+// Two columns per thread (8-B loads; even D, 8-B aligned rows), same arithmetic.
+__global__ void obs_moments_part2_kernel(const float* x, int n, int D, double* part, const double* acc,
+                                         double* acc_count) {
+    const int c = 2 * (blockIdx.x * blockDim.x + threadIdx.x), k = blockIdx.y;
+    if (acc && c == 0 && k == 0) *acc_count = acc[0];
+    if (c >= D) return;
+    const int r0 = k * kMomRows, r1 = min(n, r0 + kMomRows);
+    const float2* col = reinterpret_cast<const float2*>(x + static_cast<size_t>(r0) * D + c);
+    const int D2 = D / 2;
+    const float2 v0 = col[0];
+    const double sa = v0.x, sb = v0.y;
+    double a1 = 0.0, a2 = 0.0, b1 = 0.0, b2 = 0.0;
+#pragma unroll 8
+    for (int r = 0; r < r1 - r0; ++r) {
+        const float2 v = col[static_cast<size_t>(r) * D2];
+        const double da = static_cast<double>(v.x) - sa, db = static_cast<double>(v.y) - sb;
+        a1 += da;
+        a2 = fma(da, da, a2);
+        b1 += db;
+        b2 = fma(db, db, b2);
+    }
+    const double nk = static_cast<double>(r1 - r0);
+    double* o = part + (static_cast<size_t>(k) * D + c) * 2;
+    o[0] = sa + a1 / nk;
+    o[1] = fmax(a2 - a1 * (a1 / nk), 0.0);
+    o[2] = sb + b1 / nk;
+    o[3] = fmax(b2 - b1 * (b1 / nk), 0.0);
+}
+
 // Chunk merge: 32 columns x kMomGroups chunk groups per block; the groups' sums
 // are added in group order (fixed), in closed form: mean = sum n_k m_k / n,
 // M2 = sum (M2_k + n_k (m_k - mean)^2) — the Chan merge's result.
@@ -2883,7 +2912,10 @@ int obs_moments_chunks(int n) { return (n + kMomRows - 1) / kMomRows; }
 void launch_obs_moments(const float* x, int n, int D, double* part, double* out, cudaStream_t s, bool fold) {
     const int chunks = obs_moments_chunks(n);
     double* cnt = part + static_cast<size_t>(chunks) * D * 2;
-    if (chunks > 0)
+    if (chunks > 0 && D % 2 == 0 && (reinterpret_cast<uintptr_t>(x) & 7) == 0)
+        obs_moments_part2_kernel<<<dim3((D / 2 + 127) / 128, chunks), 128, 0, s>>>(x, n, D, part,
+                                                                                  fold ? out : nullptr, cnt);
+    else if (chunks > 0)
         obs_moments_part_kernel<<<dim3((D + 127) / 128, chunks), 128, 0, s>>>(x, n, D, part, fold ? out : nullptr, cnt);
     else if (fold)
         return;  // an empty batch leaves the running moments unchanged
