@@ -712,10 +712,56 @@ __device__ bool write_delta(const DevModel& M, const EnvSmem& S, const double* q
 }
 
 // make_initial_state (skeleton.cpp:264-284) for the env's muscles (relcs/FK in smem).
+// make_initial_state's muscle part for the fast-path run of NS segments
+// [m0, m1): the chunk records (M.mtab) give every load of a muscle up front
+// (no per-muscle segment-count lookup ahead of the segment loads).
+template <int NS>
+__device__ __forceinline__ void init_run(const DevModel& M, const DevState& St, const EnvSmem& S, size_t mb, int lane,
+                                         int m0, int m1, float a0) {
+    const int G = S.G, field = 16 * G, rec_bytes = (3 + NS) * field;
+    for (int m = m0 + lane; m < m1; m += G) {
+        const unsigned char* rec = M.mtab + M.mrun_off[NS] + ((m - m0) / G) * rec_bytes + 16 * ((m - m0) % G);
+        float4 kc[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) kc[k] = ldc4(reinterpret_cast<const float4*>(rec + (3 + k) * field));
+        const float fmax_ = ldc4(reinterpret_cast<const float4*>(rec)).x;
+        const double2 pa = ldc2d(reinterpret_cast<const double2*>(rec + field));
+        const double2 pb = ldc2d(reinterpret_cast<const double2*>(rec + 2 * field));
+        float arm;
+        double L = kseg(S, kc[0], __float_as_int(kc[0].w), arm);
+#pragma unroll
+        for (int k = 1; k < NS; ++k) L += kseg(S, kc[k], __float_as_int(kc[k].w), arm);
+        const double lm = fiber_clamp((L - pa.x) * pb.x);
+        St.act[mb + m] = a0;
+        St.lm[mb + m] = lm;
+        St.vm[mb + m] = 0.0f;
+        St.fm[mb + m] = mtu_force(a0, static_cast<float>(lm), 0.0f, fmax_);
+    }
+}
+
 __device__ void init_muscles(const DevModel& M, const DevState& St, const EnvSmem& S, int e, int lane) {
     const size_t mb = static_cast<size_t>(e) * M.nm;
     const float a0 = static_cast<float>(M.init_act);
-    for (int m = lane; m < M.nm; m += S.G) {
+    int m_begin = 0;
+    if (M.fast_nseg > 0) {  // same-link / adjacent segments only: chunk runs by segment count
+        const int* r = M.seg_run;
+        if (r[0] < r[1]) {  // zero segments: L = 0
+            for (int m = r[0] + lane; m < r[1]; m += S.G) {
+                const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
+                const double lm = fiber_clamp((0.0 - pa.x) * pb.x);
+                St.act[mb + m] = a0;
+                St.lm[mb + m] = lm;
+                St.vm[mb + m] = 0.0f;
+                St.fm[mb + m] = mtu_force(a0, static_cast<float>(lm), 0.0f, __ldg(M.m_p0 + m).x);
+            }
+        }
+        init_run<1>(M, St, S, mb, lane, r[1], r[2], a0);
+        init_run<2>(M, St, S, mb, lane, r[2], r[3], a0);
+        init_run<3>(M, St, S, mb, lane, r[3], r[4], a0);
+        init_run<4>(M, St, S, mb, lane, r[4], r[5], a0);
+        m_begin = M.gen0;
+    }
+    for (int m = m_begin + lane; m < M.nm; m += S.G) {
         const double2 pa = __ldg(M.m_p1a + m), pb = __ldg(M.m_p1b + m);
         const double L = muscle_length(M, S, m);
         const double lm = fiber_clamp((L - pa.x) * pb.x);
