@@ -530,7 +530,11 @@ int msk_gpu_create(const char* model_json_path, const char* clip_csv_path, const
             for (int l = 0; l < c.nl; ++l) {
                 const float a[4] = {c.link_ax[l], c.link_az[l], c.link_com[l], c.link_mass[l]};
                 put(M.tab_off_a + 16 * l, a, 16);
-                put(M.tab_off_in + 4 * l, &c.link_inertia[l], 4);
+                // rotational inertia about the link origin, I + m com^2 (the frame-independent
+                // (0,0) entry of the spatial inertia; the sweep no longer forms it per substep)
+                const float i0 = static_cast<float>(static_cast<double>(c.link_inertia[l]) +
+                                                    static_cast<double>(c.link_mass[l]) * c.link_com[l] * c.link_com[l]);
+                put(M.tab_off_in + 4 * l, &i0, 4);
                 const int nchild = c.child_start[l + 1] - c.child_start[l];
                 const int has_sph = c.sphere_start[l + 1] > c.sphere_start[l] ? 1 : 0;
                 const int meta = (c.link_parent[l] + 1) | (nchild << 8) | (c.child_start[l] << 16) | (has_sph << 24);

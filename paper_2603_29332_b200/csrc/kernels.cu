@@ -452,9 +452,9 @@ __device__ __forceinline__ SweepPar sweep_link(const DevModel& M, const EnvSmem&
     // lives in [10..11 | 9] during this sweep only
     reinterpret_cast<float2*>(u)[5] = make_float2(w, vx);
     u[9] = vz;
-    const float m = la.w, I = S.tin[l];
+    const float m = la.w;
     const float cx = la.z * c, cz = la.z * s;
-    const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
+    const float i00 = S.tin[l], i01 = -m * cz, i02 = m * cx;  // tin: I + m com^2 (about the origin)
     const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
     const float mg = m * M.gravity;
     float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
@@ -485,7 +485,7 @@ __device__ __forceinline__ SweepPar sweep_link(const DevModel& M, const EnvSmem&
         }
     }
     float c1 = 0.0f, c2 = 0.0f;
-    if (dof >= 0) {  // c = V x S qdot at the joint: (0, qdot v_z, -qdot v_x)
+    if (kSimple || dof >= 0) {  // c = V x S qdot at the joint: (0, qdot v_z, -qdot v_x)
         const float qdot = S.dqf[dof];
         c1 = qdot * vz;
         c2 = -qdot * vx;
@@ -1838,7 +1838,7 @@ __device__ __forceinline__ void tree_sweep_n(const DevModel& M, const EnvSmem (&
                 reinterpret_cast<float2*>(u)[5] = make_float2(w, vx);
                 u[9] = vz;
                 const float cx = la.z * c, cz = la.z * s;
-                const float i00 = fmaf(m, fmaf(cx, cx, cz * cz), I), i01 = -m * cz, i02 = m * cx;
+                const float i00 = I, i01 = -m * cz, i02 = m * cx;
                 const float h1 = fmaf(i01, w, m * vx), h2 = fmaf(i02, w, m * vz);
                 float p0 = fmaf(vx, h2, -vz * h1) - cx * mg, p1 = -w * h2, p2 = fmaf(w, h1, -mg);
                 if ((ww >> 28) & 1) {  // link carries contact spheres
