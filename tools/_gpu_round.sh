@@ -6,6 +6,7 @@ CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
 # the step-kernel capture first: bench.py's roofline.issue reads profiles/step_kernel_traffic.json
 timeout 300 $CMD > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -f -o gpurun_out/prof_step $CMD > gpurun_out/ncu_full.log 2>&1; echo ncu2 rc=$?
 python tools/ncu_summary.py gpurun_out/prof_step.ncu-rep gpurun_out/prof_summary > gpurun_out/ncu_summary.log 2>&1
+python tools/ncu_source_breakdown.py gpurun_out/prof_step.ncu-rep > gpurun_out/step_kernel_source_breakdown.txt 2>&1
 MSK_PARITY_REPORT=gpurun_out/parity_report.json timeout 1500 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/pytest_gpu.log 2>&1; echo pytest rc=$?
 timeout 600 python bench.py > gpurun_out/bench.log 2>&1; echo bench rc=$?
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo ref rc=$?
