@@ -650,6 +650,17 @@ def test_iteration_reductions_match_torch(assets):
     torch.cuda.synchronize()
     assert torch.equal(acc, ref), float((acc - ref).abs().max())
     g.close()
+    # the two-columns-per-thread chunk pass (even obs_dim, 8-B aligned rows): whole-body model
+    mp, cp = model_paths("wb700_fixed")
+    g = pk.EnvBatch(mp, cp, 8)
+    assert g.obs_dim % 2 == 0
+    x32 = torch.randn(1000, g.obs_dim, device=g.device) * 3.0 + 7.0
+    m = g.obs_moments(x32)
+    x = x32.double()
+    assert float(m[0]) == 1000
+    assert torch.allclose(m[1:1 + g.obs_dim], x.mean(0), rtol=1e-12, atol=1e-12)
+    assert torch.allclose(m[1 + g.obs_dim:], x.var(0, unbiased=False), rtol=1e-9, atol=1e-12)
+    g.close()
 
 
 def _gpu_rows(g, rows):
